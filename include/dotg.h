@@ -1,0 +1,146 @@
+/* dotg.h - C ABI of the B200 (sm_100a) limb-arithmetic path.
+ *
+ * This is the drop-in boundary for the reference's hot path (DigitsOnTurbo,
+ * /root/reference/proj). The reference exposes C++ only; each entry point below
+ * names the reference interface it replaces (file:line under proj/). Nothing here
+ * throws: every function returns a dotg_status and dotg_last_error() describes the
+ * last failure on the calling thread. There is no CPU fallback: without a usable
+ * sm_100 device every compute entry point returns DOTG_ECUDA.
+ *
+ * Data model (include/dot/limbs.hpp:1-31): a number is m little-endian uint64 limbs,
+ * index 0 least significant. Flags are uint32 0/1 of weight 2^(64m).
+ *
+ * Pointer conventions:
+ *   *_batch / *_words  : DEVICE pointers, stream-ordered on `stream` (a cudaStream_t,
+ *                        NULL = legacy default stream). Returns once enqueued.
+ *   *_host             : HOST pointers (pinned or pageable). The call stages through
+ *                        device memory with copy/compute overlap and returns after the
+ *                        results are back in host memory (synchronous, like the
+ *                        reference's span forms).
+ *
+ * Aliasing (addsub.hpp:95-97): out may alias a or b exactly; partial overlap is
+ * rejected with DOTG_EINVAL (the reference leaves it undefined).
+ *
+ * Layouts for batches of independent pairs:
+ *   DOTG_ROW_MAJOR    pair p, limb i at [p*m + i]     (the reference's Limbs, back to back)
+ *   DOTG_INTERLEAVED  pair p, limb i at [i*batch + p] (batch-interleaved, north star)
+ */
+#ifndef DOTG_H
+#define DOTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DOTG_OK = 0,
+    DOTG_EINVAL = 1,  /* std::invalid_argument in the reference */
+    DOTG_ECUDA = 2,   /* CUDA runtime error / no sm_100 device */
+    DOTG_ENOMEM = 3,  /* device or host allocation failed */
+    DOTG_ENOTSUP = 4  /* argument combination not supported */
+} dotg_status;
+
+typedef enum { DOTG_ROW_MAJOR = 0, DOTG_INTERLEAVED = 1 } dotg_layout;
+
+typedef void* dotg_stream_t; /* cudaStream_t */
+
+/* Reference: Width selector (addsub.hpp:30-36). Accepted for drop-in validation
+ * (0 scalar, 2, 4, 8); the device path has one kernel family, results are identical. */
+int dotg_validate_width(int width);
+
+const char* dotg_last_error(void);
+const char* dotg_version(void);
+/* Number of SMs of the current device, or -1. Loads the CUDA runtime. */
+int dotg_device_sms(void);
+
+/* ---------------------------------------------------------------------------
+ * Batched add/sub of independent pairs.
+ * Replaces: a loop of dot_add_words / dot_sub_words span calls
+ *   (addsub.hpp:98-103, addsub.cpp:286-294 -> run_words 136-170), one per pair, as in
+ *   the reference bench's exec_case (bench.cpp:95-104).
+ * out[p] = a[p] +/- b[p] mod 2^(64m); flags[p] = carry/borrow (flags may be NULL).
+ * m = 0 is legal: flags are set to 0 (addsub.cpp:139-170 with m = 0).
+ * ------------------------------------------------------------------------- */
+int dotg_add_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                   size_t m, size_t batch, int layout, dotg_stream_t stream);
+int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                   size_t m, size_t batch, int layout, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched column multiplication.
+ * Replaces: dot_mul_words(a, b, kSaturated, w) per pair (mul.hpp:75-76, mul.cpp:96-103).
+ * out[p] = a[p] * b[p], exactly 2m limbs (high limbs may be 0). Requires
+ * 1 <= m <= 2^24 (kMaxMulLimbs, mul.hpp:30; mul.cpp:13-18). ROW_MAJOR out is
+ * [batch][2m]; INTERLEAVED out is [2m][batch].
+ * ------------------------------------------------------------------------- */
+int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                   int layout, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * One long number on one GPU (config 5 at G = 1, and the span form at any m).
+ * Replaces: dot_add_words / dot_sub_words span form (addsub.hpp:98-103).
+ * carry_out is a DEVICE pointer to one uint32 (may be NULL). Scratch is taken from
+ * the stream-ordered allocator of `stream`'s device.
+ * ------------------------------------------------------------------------- */
+int dotg_add_words(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                   uint32_t* carry_out, dotg_stream_t stream);
+int dotg_sub_words(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                   uint32_t* carry_out, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * One long number sharded by limb range across ranks (config 5, G > 1).
+ * Each rank holds limbs [r*n/G, (r+1)*n/G) of a, b, out and calls:
+ *   1. dotg_shard_local   - streaming pass over the shard with an unknown carry-in X;
+ *                           writes every output limb that does not depend on X and the
+ *                           shard aggregate agg[0..1] = {G, P} (device uint32[2]):
+ *                           G = carry-out if X = 0, P = 1 iff every limb propagates.
+ *   2. exchange agg across ranks (8 bytes per rank; e.g. ncclAllGather / torch
+ *      all_gather_into_tensor) into all_aggs = uint32[world][2] on the device.
+ *   3. dotg_shard_finish  - carry-in X_r = exclusive scan of (G, P) over ranks < r,
+ *                           then the boundary fix-up; carry_out (device uint32, may be
+ *                           NULL) receives the carry of the WHOLE number (rank-independent).
+ * `state` is a device scratch of dotg_shard_state_bytes(m) bytes that must stay alive
+ * between the two calls. Single GPU: world = 1 with all_aggs = agg.
+ * ------------------------------------------------------------------------- */
+size_t dotg_shard_state_bytes(size_t m);
+int dotg_shard_local(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                     void* state, uint32_t* agg, dotg_stream_t stream);
+int dotg_shard_finish(int sub, uint64_t* out, size_t m, void* state, const uint32_t* all_aggs,
+                      int rank, int world, uint32_t* carry_out, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer entry points (the reference-facing call: host spans in, host out).
+ * Replace: dot_add_words / dot_sub_words span forms (addsub.hpp:98-103) and
+ * dot_mul_words (mul.hpp:75-76) over a batch of row-major host arrays. Inputs are
+ * streamed to the device in slices on two streams so host->device copies, kernels
+ * and device->host copies overlap; the call returns when out/flags are filled.
+ * Pinned host memory (cudaHostAlloc) reaches full PCIe bandwidth.
+ * ------------------------------------------------------------------------- */
+int dotg_add_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                        size_t m, size_t batch);
+int dotg_sub_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                        size_t m, size_t batch);
+int dotg_mul_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                        size_t batch);
+/* Single number, host spans (the literal span form). *carry receives the flag. */
+int dotg_add_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                        uint32_t* carry);
+int dotg_sub_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                        uint32_t* carry);
+
+/* Workload setup (not the hot path): out[i] = splitmix64 output for counter
+ * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
+int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,
+                         dotg_stream_t stream);
+
+/* Diagnostics: number of kernels this library launched since load (all threads). */
+uint64_t dotg_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DOTG_H */

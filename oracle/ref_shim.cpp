@@ -1,0 +1,193 @@
+// ref_shim.cpp - C-ABI wrapper around the UNMODIFIED reference (TEST INFRASTRUCTURE).
+//
+// Linked by oracle/Makefile with the reference's own translation units, compiled
+// from where they lie under /root/reference/proj/src (nothing is copied). It lets
+// Python load the reference through ctypes to (a) generate golden vectors,
+// (b) pin oracle/dot_oracle.c, and (c) serve as the CPU baseline
+// (bench.py cpu_baseline / --impl reference, kind "reference").
+//
+// Only the reference's public API is called (include/dot/*.hpp):
+//   dot_add_words / dot_sub_words span + value forms   addsub.hpp:95-109
+//   add_w_limbs / sub_w_limbs                           addsub.hpp:86-89
+//   dot_mul_words                                       mul.hpp:75-76
+//   oracle_add / oracle_sub / oracle_mul                oracle.hpp:18-23
+//   dispatch_note                                       addsub.hpp:41-43
+// std::invalid_argument is caught and turned into return code -1 (message kept).
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "dot/addsub.hpp"
+#include "dot/limbs.hpp"
+#include "dot/mul.hpp"
+#include "dot/oracle.hpp"
+
+using dot::limb_t;
+using dot::Limbs;
+
+namespace {
+thread_local std::string g_err;
+
+dot::Width width_of(int w) {
+    switch (w) {
+        case 0: return dot::Width::scalar;
+        case 2: return dot::Width::w2;
+        case 4: return dot::Width::w4;
+        case 8: return dot::Width::w8;
+        default: return static_cast<dot::Width>(w);  // lets validate_width throw
+    }
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* dotref_last_error() { return g_err.c_str(); }
+
+const char* dotref_dispatch_note(int w) {
+    static std::string s;
+    s = std::string(dot::dispatch_note(width_of(w)));
+    return s.c_str();
+}
+
+// Span form. Returns the carry/borrow (0/1) or -1 on std::invalid_argument.
+int dotref_words(int sub, limb_t* out, size_t mo, const limb_t* a, size_t ma, const limb_t* b,
+                 size_t mb, int width, uint64_t* chunks, uint64_t* fires) {
+    return guarded([&] {
+        dot::AddSubStats st;
+        std::span<limb_t> so(out, mo);
+        std::span<const limb_t> sa(a, ma), sb(b, mb);
+        unsigned c = sub ? dot::dot_sub_words(so, sa, sb, width_of(width), &st)
+                         : dot::dot_add_words(so, sa, sb, width_of(width), &st);
+        if (chunks) *chunks = st.chunks_processed;
+        if (fires) *fires = st.phase4_triggers;
+        return int(c);
+    });
+}
+
+// Value form (zero-pads to the longer operand). out must hold max(ma, mb) limbs.
+int dotref_words_value(int sub, limb_t* out, const limb_t* a, size_t ma, const limb_t* b,
+                       size_t mb, int width) {
+    return guarded([&] {
+        const Limbs va(a, a + ma), vb(b, b + mb);
+        const dot::WordsResult r = sub ? dot::dot_sub_words(va, vb, width_of(width))
+                                       : dot::dot_add_words(va, vb, width_of(width));
+        std::copy(r.limbs.begin(), r.limbs.end(), out);
+        return int(r.flag);
+    });
+}
+
+// Chunk API: returns carry_out, *phase4 = phase4_fired, sums written to out[0..w).
+int dotref_chunk(int sub, limb_t* out, const limb_t* a, const limb_t* b, size_t len,
+                 unsigned carry_in, unsigned w, int* phase4) {
+    return guarded([&] {
+        std::span<const limb_t> sa(a, len), sb(b, len);
+        const dot::ChunkResult r = sub ? dot::sub_w_limbs(sa, sb, carry_in, w)
+                                       : dot::add_w_limbs(sa, sb, carry_in, w);
+        std::copy(r.sums.begin(), r.sums.begin() + std::min<size_t>(w, 8), out);
+        if (phase4) *phase4 = r.phase4_fired ? 1 : 0;
+        return int(r.carry_out);
+    });
+}
+
+// dot_mul_words: writes exactly 2m limbs. Returns 0 or -1.
+int dotref_mul_words(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {
+    return guarded([&] {
+        const Limbs r = dot::dot_mul_words(Limbs(a, a + ma), Limbs(b, b + mb));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+int dotref_oracle_addsub(int sub, limb_t* out, const limb_t* a, size_t ma, const limb_t* b,
+                         size_t mb) {
+    return guarded([&] {
+        const Limbs va(a, a + ma), vb(b, b + mb);
+        const dot::WordsResult r = sub ? dot::oracle_sub(va, vb) : dot::oracle_add(va, vb);
+        std::copy(r.limbs.begin(), r.limbs.end(), out);
+        return int(r.flag);
+    });
+}
+
+// oracle_mul: out must hold ma+mb limbs; writes the trimmed result, zero-pads the rest,
+// returns the trimmed length.
+int dotref_oracle_mul(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {
+    return guarded([&] {
+        const Limbs r = dot::oracle_mul(Limbs(a, a + ma), Limbs(b, b + mb));
+        std::fill(out, out + ma + mb, limb_t(0));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+// Batched CPU baseline over [batch][m] row-major operands with a static partition
+// of pairs across nthreads std::threads (the reference functions are pure and
+// reentrant). op: 0 add, 1 sub, 2 mul. impl: 0 = the DoT path
+// (span-form dot_add_words/dot_sub_words at Width::w8, dot_mul_words), 1 = oracle.
+// flags may be null for mul. out is [batch][m] (add/sub) or [batch][2m] (mul).
+int dotref_batch(int op, int impl, limb_t* out, const limb_t* a, const limb_t* b, uint32_t* flags,
+                 size_t m, size_t batch, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    std::vector<std::thread> pool;
+    std::vector<int> status(size_t(nthreads), 0);
+    auto work = [&](int t) {
+        const size_t lo = batch * size_t(t) / size_t(nthreads);
+        const size_t hi = batch * size_t(t + 1) / size_t(nthreads);
+        status[size_t(t)] = guarded([&] {
+            for (size_t p = lo; p < hi; ++p) {
+                const limb_t* pa = a + p * m;
+                const limb_t* pb = b + p * m;
+                if (op == 2) {
+                    limb_t* po = out + p * 2 * m;
+                    const Limbs va(pa, pa + m), vb(pb, pb + m);
+                    if (impl == 0) {
+                        const Limbs r = dot::dot_mul_words(va, vb);
+                        std::copy(r.begin(), r.end(), po);
+                    } else {
+                        const Limbs r = dot::oracle_mul(va, vb);
+                        std::fill(po, po + 2 * m, limb_t(0));
+                        std::copy(r.begin(), r.end(), po);
+                    }
+                } else {
+                    limb_t* po = out + p * m;
+                    unsigned f;
+                    if (impl == 0) {
+                        std::span<limb_t> so(po, m);
+                        std::span<const limb_t> sa(pa, m), sb(pb, m);
+                        f = op ? dot::dot_sub_words(so, sa, sb, dot::Width::w8)
+                               : dot::dot_add_words(so, sa, sb, dot::Width::w8);
+                    } else {
+                        const Limbs va(pa, pa + m), vb(pb, pb + m);
+                        const dot::WordsResult r = op ? dot::oracle_sub(va, vb) : dot::oracle_add(va, vb);
+                        std::copy(r.limbs.begin(), r.limbs.end(), po);
+                        f = r.flag;
+                    }
+                    if (flags) flags[p] = f;
+                }
+            }
+            return 0;
+        });
+    };
+    for (int t = 1; t < nthreads; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int s : status)
+        if (s != 0) return s;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+"""ctypes binding of libdotg.so (the C ABI declared in include/dotg.h).
+
+The library is built in-tree by ``paper_2604_21566_b200/csrc/Makefile`` (or
+``__graft_entry__.build()``). There is no fallback: if the shared object is missing the
+import of any compute entry point raises, and every compute call on a machine without
+an sm_100 device returns DOTG_ECUDA, surfaced here as :class:`DotgCudaError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_int, c_size_t, c_uint64, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdotg.so")
+
+DOTG_OK, DOTG_EINVAL, DOTG_ECUDA, DOTG_ENOMEM, DOTG_ENOTSUP = range(5)
+ROW_MAJOR, INTERLEAVED = 0, 1
+
+# Every symbol include/dotg.h declares: name -> (restype, argtypes).
+_P = c_void_p
+SIGNATURES = {
+    "dotg_validate_width": (c_int, [c_int]),
+    "dotg_last_error": (c_char_p, []),
+    "dotg_version": (c_char_p, []),
+    "dotg_device_sms": (c_int, []),
+    "dotg_add_batch": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_sub_batch": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_mul_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_add_words": (c_int, [_P, _P, _P, c_size_t, _P, _P]),
+    "dotg_sub_words": (c_int, [_P, _P, _P, c_size_t, _P, _P]),
+    "dotg_shard_state_bytes": (c_size_t, [c_size_t]),
+    "dotg_shard_local": (c_int, [c_int, _P, _P, _P, c_size_t, _P, _P, _P]),
+    "dotg_shard_finish": (c_int, [c_int, _P, c_size_t, _P, _P, c_int, c_int, _P, _P]),
+    "dotg_add_batch_host": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t]),
+    "dotg_sub_batch_host": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t]),
+    "dotg_mul_batch_host": (c_int, [_P, _P, _P, c_size_t, c_size_t]),
+    "dotg_add_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
+    "dotg_sub_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
+    "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
+    "dotg_kernel_launches": (c_uint64, []),
+}
+
+
+class DotgError(RuntimeError):
+    """Base class for library errors."""
+
+
+class InvalidArgument(DotgError, ValueError):
+    """The reference's std::invalid_argument (SURVEY.md §8(b) error cases)."""
+
+
+class DotgCudaError(DotgError):
+    """CUDA failure or no sm_100 device (there is no CPU fallback)."""
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdotg.so once; raise loudly when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C paper_2604_21566_b200/csrc` "
+                "or __graft_entry__.build(); the product path has no CPU fallback"
+            )
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == DOTG_OK:
+        return
+    msg = lib().dotg_last_error().decode(errors="replace")
+    if rc == DOTG_EINVAL:
+        raise InvalidArgument(msg)
+    if rc == DOTG_ECUDA:
+        raise DotgCudaError(msg)
+    if rc == DOTG_ENOMEM:
+        raise MemoryError(msg)
+    raise DotgError(f"dotg status {rc}: {msg}")
+
+
+def kernel_launches() -> int:
+    return int(lib().dotg_kernel_launches())

@@ -1,0 +1,295 @@
+"""Host-side mirror of the reference's operator interface, over the C ABI.
+
+Two surfaces:
+
+* Reference-shaped calls on host arrays (numpy uint64, little-endian limbs), with the
+  reference's names, argument meaning and error behaviour (include/dot/addsub.hpp:95-109,
+  include/dot/mul.hpp:75-76): ``dot_add_words``, ``dot_sub_words`` (span form
+  ``f(out, a, b, width)`` -> carry; value form ``f(a, b, width)`` -> WordsResult) and
+  ``dot_mul_words(a, b)`` -> 2m limbs. std::invalid_argument becomes
+  :class:`InvalidArgument` (a ValueError). These go through the ``*_host`` entry points
+  (host buffers in, host buffers out, copies overlapped with the kernels).
+
+* Device-resident batch calls on torch CUDA tensors (the measured path):
+  ``add_batch`` / ``sub_batch`` / ``mul_batch`` and the long-number ``add_words`` /
+  ``sub_words``. Tensors are int64 or uint64 (limb bit patterns), contiguous.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from typing import NamedTuple, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import INTERLEAVED, ROW_MAJOR, InvalidArgument, check, lib
+
+K_MAX_MUL_LIMBS = 1 << 24  # kMaxMulLimbs, include/dot/mul.hpp:30
+
+
+class Width(enum.IntEnum):
+    """Reference Width selector (include/dot/addsub.hpp:30-36). The device path has one
+    kernel family; every width returns bit-identical results (as in the reference)."""
+
+    scalar = 0
+    w2 = 2
+    w4 = 4
+    w8 = 8
+
+
+def lane_count(w: int) -> int:
+    """addsub.hpp:38-40."""
+    return 8 if int(w) == 0 else int(w)
+
+
+class WordsResult(NamedTuple):
+    """include/dot/limbs.hpp:28-31: m result limbs plus a carry/borrow flag."""
+
+    limbs: np.ndarray
+    flag: int
+
+
+def _validate_width(width) -> None:
+    check(lib().dotg_validate_width(int(width)))
+
+
+def _host_u64(x, name: str) -> np.ndarray:
+    arr = np.asarray(x)
+    if arr.dtype != np.uint64:
+        if arr.size == 0:
+            arr = arr.astype(np.uint64)
+        elif arr.dtype.kind in "iu":
+            arr = arr.astype(np.uint64)
+        else:
+            raise InvalidArgument(f"{name}: limbs must be unsigned 64-bit integers")
+    if arr.ndim != 1:
+        raise InvalidArgument(f"{name}: a limb sequence is one-dimensional")
+    return np.ascontiguousarray(arr)
+
+
+def _hp(arr: Optional[np.ndarray]):
+    return None if arr is None or arr.size == 0 else ctypes.c_void_p(arr.ctypes.data)
+
+
+def _words_span(sub: bool, out: np.ndarray, a, b, width) -> int:
+    _validate_width(width)
+    if not isinstance(out, np.ndarray) or out.dtype != np.uint64 or not out.flags.c_contiguous:
+        raise InvalidArgument("out must be a contiguous numpy uint64 array (the caller-owned span)")
+    a = _host_u64(a, "a")
+    b = _host_u64(b, "b")
+    if a.size != b.size or out.size != a.size:
+        raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")  # addsub.cpp:139-140
+    carry = ctypes.c_uint32(0)
+    fn = lib().dotg_sub_words_host if sub else lib().dotg_add_words_host
+    check(fn(_hp(out), _hp(a), _hp(b), a.size, ctypes.byref(carry)))
+    return int(carry.value)
+
+
+def _words_value(sub: bool, a, b, width) -> WordsResult:
+    a = _host_u64(a, "a")
+    b = _host_u64(b, "b")
+    m = max(a.size, b.size)  # addsub.cpp:192-206: zero-pad the shorter operand
+    if a.size != m:
+        a = np.concatenate([a, np.zeros(m - a.size, np.uint64)])
+    if b.size != m:
+        b = np.concatenate([b, np.zeros(m - b.size, np.uint64)])
+    out = np.zeros(m, np.uint64)
+    flag = _words_span(sub, out, a, b, width)
+    return WordsResult(out, flag)
+
+
+def dot_add_words(*args, width=Width.w8, stats=None):
+    """``dot_add_words(out, a, b[, width])`` -> carry (span form, addsub.hpp:98-100) or
+    ``dot_add_words(a, b[, width])`` -> WordsResult (value form, addsub.hpp:106-107)."""
+    return _dispatch_words(False, args, width, stats)
+
+
+def dot_sub_words(*args, width=Width.w8, stats=None):
+    """Subtraction twin of :func:`dot_add_words` (addsub.hpp:101-103, 108-109)."""
+    return _dispatch_words(True, args, width, stats)
+
+
+def _dispatch_words(sub: bool, args, width, stats):
+    if stats is not None:
+        raise _lib.DotgError("AddSubStats instrumentation is not provided by the device path")
+    if len(args) == 4:
+        args, width = args[:3], args[3]
+    if len(args) == 3:
+        return _words_span(sub, args[0], args[1], args[2], width)
+    if len(args) == 2:
+        _validate_width(width)
+        return _words_value(sub, args[0], args[1], width)
+    raise TypeError("expected (out, a, b[, width]) or (a, b[, width])")
+
+
+def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
+    """Exact product, exactly 2m limbs (include/dot/mul.hpp:75-76, src/mul.cpp:96-103).
+    Equal limb counts 1 <= m <= 2^24 (mul.cpp:13-18). Only the saturated 64-bit radix is
+    on the device path (the 52-bit route is out of scope)."""
+    if int(cfg) not in (64, 52):
+        raise InvalidArgument("RadixConfig: limb_bits must be 64 or 52")  # limbs.cpp:22-24
+    if int(cfg) != 64:
+        raise _lib.DotgError("the 52-bit (unsaturated) radix is not on the B200 path")
+    a = _host_u64(a, "a")
+    b = _host_u64(b, "b")
+    if a.size != b.size:
+        raise InvalidArgument("dot mul: operand lengths differ (caller pads)")
+    if a.size == 0:
+        raise InvalidArgument("dot mul: operands need at least one limb")
+    if a.size > K_MAX_MUL_LIMBS:
+        raise InvalidArgument("dot mul: limb count exceeds the column accumulator bound")
+    out = np.zeros(2 * a.size, np.uint64)
+    check(lib().dotg_mul_batch_host(_hp(out), _hp(a), _hp(b), a.size, 1))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Host batch helpers (row-major [batch, m] numpy arrays; pinned memory recommended)
+# ---------------------------------------------------------------------------
+def _host_2d(x, name):
+    arr = np.asarray(x)
+    if arr.dtype != np.uint64 or arr.ndim != 2 or not arr.flags.c_contiguous:
+        raise InvalidArgument(f"{name}: expected a C-contiguous [batch, m] uint64 array")
+    return arr
+
+
+def addsub_batch_host(sub: bool, a, b, out=None, flags=None):
+    a = _host_2d(a, "a")
+    b = _host_2d(b, "b")
+    if a.shape != b.shape:
+        raise InvalidArgument("dot add/sub: operand shapes differ")
+    batch, m = a.shape
+    out = np.empty_like(a) if out is None else _host_2d(out, "out")
+    flags = np.empty(batch, np.uint32) if flags is None else flags
+    fn = lib().dotg_sub_batch_host if sub else lib().dotg_add_batch_host
+    check(fn(_hp(out), _hp(a), _hp(b), _hp(flags), m, batch))
+    return out, flags
+
+
+def mul_batch_host(a, b, out=None):
+    a = _host_2d(a, "a")
+    b = _host_2d(b, "b")
+    if a.shape != b.shape:
+        raise InvalidArgument("dot mul: operand shapes differ")
+    batch, m = a.shape
+    out = np.empty((batch, 2 * m), np.uint64) if out is None else _host_2d(out, "out")
+    check(lib().dotg_mul_batch_host(_hp(out), _hp(a), _hp(b), m, batch))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Device batch API (torch CUDA tensors)
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    torch = _torch()
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check_dev(t, name, elem=8):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidArgument(f"{name}: expected a CUDA tensor")
+    if t.element_size() != elem or not t.is_contiguous():
+        raise InvalidArgument(f"{name}: expected a contiguous {8 * elem}-bit tensor")
+
+
+def _layout(layout) -> int:
+    if layout in (ROW_MAJOR, "row", "row_major"):
+        return ROW_MAJOR
+    if layout in (INTERLEAVED, "interleaved"):
+        return INTERLEAVED
+    raise InvalidArgument(f"unknown layout {layout!r}")
+
+
+def _batch_dims(a, layout):
+    if a.dim() != 2:
+        raise InvalidArgument("batched operands are 2-D")
+    return (a.shape[0], a.shape[1]) if layout == ROW_MAJOR else (a.shape[1], a.shape[0])
+
+
+def addsub_batch(sub: bool, a, b, out=None, flags=None, *, layout=ROW_MAJOR, stream=None):
+    """out = a +/- b per pair, flags = carry/borrow per pair (device tensors).
+    ROW_MAJOR a: [batch, m]; INTERLEAVED a: [m, batch]."""
+    torch = _torch()
+    lay = _layout(layout)
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.shape != b.shape:
+        raise InvalidArgument("dot add/sub: operand shapes differ")
+    batch, m = _batch_dims(a, lay)
+    if out is None:
+        out = torch.empty_like(a)
+    _check_dev(out, "out")
+    if out.shape != a.shape:
+        raise InvalidArgument("out shape differs")
+    if flags is None:
+        flags = torch.empty(batch, dtype=torch.int32, device=a.device)
+    _check_dev(flags, "flags", 4)
+    fn = lib().dotg_sub_batch if sub else lib().dotg_add_batch
+    check(fn(_dptr(out), _dptr(a), _dptr(b), _dptr(flags), m, batch, lay, _stream_handle(stream)))
+    return out, flags
+
+
+def add_batch(a, b, out=None, flags=None, *, layout=ROW_MAJOR, stream=None):
+    return addsub_batch(False, a, b, out, flags, layout=layout, stream=stream)
+
+
+def sub_batch(a, b, out=None, flags=None, *, layout=ROW_MAJOR, stream=None):
+    return addsub_batch(True, a, b, out, flags, layout=layout, stream=stream)
+
+
+def mul_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
+    """out = a * b per pair, exactly 2m limbs. ROW_MAJOR out: [batch, 2m];
+    INTERLEAVED out: [2m, batch]."""
+    torch = _torch()
+    lay = _layout(layout)
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.shape != b.shape:
+        raise InvalidArgument("dot mul: operand shapes differ")
+    batch, m = _batch_dims(a, lay)
+    shape = (batch, 2 * m) if lay == ROW_MAJOR else (2 * m, batch)
+    if out is None:
+        out = torch.empty(shape, dtype=a.dtype, device=a.device)
+    _check_dev(out, "out")
+    if tuple(out.shape) != shape:
+        raise InvalidArgument("out must hold exactly 2m limbs per pair")
+    check(lib().dotg_mul_batch(_dptr(out), _dptr(a), _dptr(b), m, batch, lay, _stream_handle(stream)))
+    return out
+
+
+def words(sub: bool, a, b, out=None, carry=None, *, stream=None):
+    """One long number on the device: out = a +/- b, carry = device int32[1]."""
+    torch = _torch()
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.dim() != 1 or a.shape != b.shape:
+        raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")
+    out = torch.empty_like(a) if out is None else out
+    _check_dev(out, "out")
+    if out.shape != a.shape:
+        raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")
+    carry = torch.empty(1, dtype=torch.int32, device=a.device) if carry is None else carry
+    fn = lib().dotg_sub_words if sub else lib().dotg_add_words
+    check(fn(_dptr(out), _dptr(a), _dptr(b), a.numel(), _dptr(carry), _stream_handle(stream)))
+    return out, carry
+
+
+def add_words(a, b, out=None, carry=None, *, stream=None):
+    return words(False, a, b, out, carry, stream=stream)
+
+
+def sub_words(a, b, out=None, carry=None, *, stream=None):
+    return words(True, a, b, out, carry, stream=stream)

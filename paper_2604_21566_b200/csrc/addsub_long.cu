@@ -1,0 +1,314 @@
+// addsub_long.cu - one long number (up to 2^30+ limbs), tiled over the whole GPU and
+// shardable by limb range across GPUs (config 5).
+//
+// Replaces the reference's span-form dot_add_words / dot_sub_words on long operands
+// (include/dot/addsub.hpp:98-103, src/addsub.cpp:136-170), where a long number is a
+// serial chain of w-limb chunks whose carry-out is the next chunk's carry-in
+// (addsub.cpp:147-164). Here the chain is replaced by a (G, P) scan at three levels:
+//
+//   pass 1  k_long_local   one CTA per tile of 4096 limbs: phases 1-2 per limb,
+//                          ballot masks per warp row, one mask addition per 32-bit
+//                          word + one per tile (two-level lookahead in shared memory),
+//                          phase-4 carry application, store. The tile's carry-in is
+//                          unknown in this pass and treated as 0, EXCEPT that the
+//                          tile's leading propagate run [0, pt) - the only limbs whose
+//                          value depends on that carry-in, besides limb pt itself - is
+//                          not written (deferred). State per tile: pt, tile G, tile P.
+//   pass 2  k_long_scan    one CTA scans the per-tile (G, P) symbolically in the shard
+//                          carry-in X: cin_t = g_ex | (p_ex & X). Emits the shard
+//                          aggregate {G, P} (8 bytes) for the cross-GPU exchange.
+//   pass 3  k_long_finish  X from the gathered shard aggregates; per tile: write the
+//                          deferred prefix as the propagate value for cin_t and bump
+//                          limb pt by cin_t. This is the reference's rare Phase 4
+//                          (addsub.cpp:61-79) lifted to tiles: on random data it is one
+//                          8-byte read-modify-write per tile with cin_t = 1.
+//
+// Traffic is the algorithmic 24 B/limb plus ~8 B per tile; a long all-propagate run is
+// written exactly once (by pass 3), never rewritten. No CTA waits on another CTA.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace dotg {
+
+namespace {
+
+constexpr int kThreads = 256;            // threads per tile CTA
+constexpr int kRows = 4;                 // vectors per thread
+constexpr int kV = 4;                    // limbs per vector (256-bit)
+constexpr int kTile = kThreads * kRows * kV;  // 4096 limbs
+constexpr int kWords = kTile / kV / 32;  // 32 ballot words per tile
+
+// State word per tile: bits [0,16) pt, 16 tile G, 17 tile P, 18 g_ex, 19 p_ex.
+constexpr uint32_t kBitG = 1u << 16, kBitP = 1u << 17, kBitGex = 1u << 18, kBitPex = 1u << 19;
+
+size_t num_tiles(size_t m) { return (m + kTile - 1) / kTile; }
+
+template <bool SUB, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_long_local(uint64_t* out, const uint64_t* a,
+                                                         const uint64_t* b, size_t m,
+                                                         uint32_t* state) {
+    __shared__ uint32_t sG[kWords], sP[kWords], sC[kWords];
+    __shared__ uint32_t s_pt;
+    const size_t tile = blockIdx.x;
+    const size_t L0 = tile * size_t(kTile);
+    const size_t len = (m - L0) < size_t(kTile) ? (m - L0) : size_t(kTile);
+    const bool full = len == size_t(kTile);
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+
+    uint64_t s[kRows][kV], y[kRows][kV];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+        const size_t o = size_t(r * kThreads + tid) * kV;  // limb offset within tile
+        if (VEC && full) {
+            ld_stream<kV>(a + L0 + o, s[r]);
+            ld_stream<kV>(b + L0 + o, y[r]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const bool in = o + k < len;
+                s[r][k] = in ? a[L0 + o + k] : (SUB ? 0ull : ~0ull);  // fake limbs propagate
+                y[r][k] = in ? b[L0 + o + k] : 0ull;
+            }
+        }
+    }
+    uint32_t g[kRows][kV], p[kRows][kV];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+#pragma unroll
+        for (int k = 0; k < kV; ++k) s[r][k] = lane_op<SUB>(s[r][k], y[r][k], g[r][k], p[r][k]);
+        uint32_t G, P;
+        fold_gp<kV>(g[r], p[r], G, P);
+        const uint32_t gw = __ballot_sync(0xffffffffu, G);
+        const uint32_t pw = __ballot_sync(0xffffffffu, P);
+        if (lane == 0) {
+            sG[r * (kThreads / 32) + warp] = gw;
+            sP[r * (kThreads / 32) + warp] = pw;
+        }
+    }
+    if (tid == 0) s_pt = 0xffffffffu;
+    __syncthreads();
+
+    uint32_t tileG = 0, tileP = 0;
+    if (warp == 0) {
+        // Word level: lane i owns ballot word i (super-lanes 32i .. 32i+31).
+        const uint32_t G = sG[lane], P = sP[lane];
+        const uint64_t y0 = (uint64_t(G) << 1) + uint64_t(P);
+        const uint32_t wg = uint32_t(y0 >> 32) & 1u;
+        const uint32_t wp = P == 0xffffffffu;
+        // Tile level: one more mask addition over the 32 words (tile carry-in = 0).
+        const uint32_t GW = __ballot_sync(0xffffffffu, wg);
+        const uint32_t PW = __ballot_sync(0xffffffffu, wp);
+        const uint64_t yw = (uint64_t(GW) << 1) + uint64_t(PW);
+        const uint32_t cin = uint32_t((yw ^ uint64_t(PW)) >> lane) & 1u;
+        sC[lane] = uint32_t(((uint64_t(G) << 1 | cin) + uint64_t(P)) ^ uint64_t(P));
+        tileG = uint32_t(yw >> 32) & 1u;
+        tileP = PW == 0xffffffffu;
+    }
+    __syncthreads();
+
+    // Locate the first non-propagate super-lane from shared memory (cheap, uniform).
+    unsigned js = kWords * 32;
+#pragma unroll 1
+    for (int w = 0; w < kWords; ++w) {
+        const uint32_t pw = sP[w];
+        if (pw != 0xffffffffu) {
+            js = unsigned(w) * 32u + unsigned(__ffs(~pw) - 1);
+            break;
+        }
+    }
+
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+        const unsigned j = unsigned(r * kThreads) + tid;
+        const uint32_t c = (sC[j >> 5] >> (j & 31u)) & 1u;
+        apply_superlane<SUB, kV>(s[r], g[r], p[r], c);
+        const size_t o = size_t(j) * kV;
+        if (j > js) {
+            if (VEC && full) {
+                st_stream<kV>(out + L0 + o, s[r]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < kV; ++k)
+                    if (o + k < len) out[L0 + o + k] = s[r][k];
+            }
+        } else if (j == js) {
+            // Owner of the first non-propagate super-lane: limbs before its first
+            // non-propagate limb belong to the deferred prefix.
+            int k0 = kV;
+#pragma unroll
+            for (int k = kV - 1; k >= 0; --k)
+                if (!p[r][k]) k0 = k;
+#pragma unroll
+            for (int k = 0; k < kV; ++k)
+                if (k >= k0 && o + k < len) out[L0 + o + k] = s[r][k];
+            const size_t pt = o + size_t(k0);
+            s_pt = uint32_t(pt < len ? pt : len);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const uint32_t pt = s_pt == 0xffffffffu ? uint32_t(len) : s_pt;
+        state[tile] = pt | (tileG ? kBitG : 0u) | (tileP ? kBitP : 0u);
+    }
+}
+
+// Compose (g1,p1) then (g2,p2): carry out of the concatenation (lower part first).
+__device__ __forceinline__ void compose(uint32_t& g, uint32_t& p, uint32_t g2, uint32_t p2) {
+    g = g2 | (p2 & g);
+    p = p & p2;
+}
+
+// Single-CTA symbolic scan over tile (G, P). For every tile writes (g_ex, p_ex) with
+// cin_t = g_ex | (p_ex & X); writes agg = {G, P} of the whole shard.
+__global__ void __launch_bounds__(1024) k_long_scan(uint32_t* state, size_t n, uint32_t* agg) {
+    __shared__ uint32_t swg[32], swp[32];
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const size_t per = (n + 1023) / 1024;
+    const size_t lo = size_t(tid) * per;
+    const size_t hi = lo + per < n ? lo + per : n;
+    // Thread aggregate over its chunk (identity = (0, 1)).
+    uint32_t tg = 0, tp = 1;
+    for (size_t t = lo; t < hi; ++t) {
+        const uint32_t st = state[t];
+        compose(tg, tp, (st & kBitG) ? 1u : 0u, (st & kBitP) ? 1u : 0u);
+    }
+    // Warp-level exclusive prefix via two mask additions (cin = 0 and cin = 1).
+    const uint32_t GW = __ballot_sync(0xffffffffu, tg);
+    const uint32_t PW = __ballot_sync(0xffffffffu, tp);
+    const uint64_t y0 = (uint64_t(GW) << 1) + PW;
+    const uint64_t y1 = ((uint64_t(GW) << 1) | 1u) + PW;
+    const uint32_t c0 = uint32_t(y0 ^ PW), c1 = uint32_t(y1 ^ PW);
+    uint32_t lg = (c0 >> lane) & 1u;               // exclusive within warp, X = 0
+    uint32_t lp = ((c1 ^ c0) >> lane) & 1u;        // exclusive "all propagate"
+    if (lane == 0) {
+        swg[warp] = uint32_t(y0 >> 32) & 1u;
+        swp[warp] = PW == 0xffffffffu;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t g = swg[lane], p = swp[lane];
+        const uint32_t GB = __ballot_sync(0xffffffffu, g);
+        const uint32_t PB = __ballot_sync(0xffffffffu, p);
+        const uint64_t z0 = (uint64_t(GB) << 1) + PB;
+        const uint64_t z1 = ((uint64_t(GB) << 1) | 1u) + PB;
+        const uint32_t d0 = uint32_t(z0 ^ PB), d1 = uint32_t(z1 ^ PB);
+        __syncwarp();
+        swg[lane] = (d0 >> lane) & 1u;
+        swp[lane] = ((d1 ^ d0) >> lane) & 1u;
+        if (lane == 0) {
+            agg[0] = uint32_t(z0 >> 32) & 1u;
+            agg[1] = PB == 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    // Thread exclusive prefix = warp prefix then lane prefix.
+    uint32_t eg = swg[warp], ep = swp[warp];
+    compose(eg, ep, lg, lp);
+    for (size_t t = lo; t < hi; ++t) {
+        const uint32_t st = state[t];
+        state[t] = (st & 0xffffu) | (st & (kBitG | kBitP)) | (eg ? kBitGex : 0u) | (ep ? kBitPex : 0u);
+        compose(eg, ep, (st & kBitG) ? 1u : 0u, (st & kBitP) ? 1u : 0u);
+    }
+}
+
+// Pass 3: resolve the shard carry-in X from the gathered aggregates, then fix up each
+// tile whose carry-in is 1 or whose leading propagate run was deferred.
+template <bool SUB>
+__global__ void __launch_bounds__(256) k_long_finish(uint64_t* out, size_t m, const uint32_t* state,
+                                                     size_t n, const uint32_t* all_aggs, int rank,
+                                                     int world, uint32_t* carry_out) {
+    uint32_t x = 0;  // carry into this shard
+    uint32_t total = 0;
+    for (int q = 0; q < world; ++q) {
+        const uint32_t G = all_aggs[2 * q], P = all_aggs[2 * q + 1];
+        if (q == rank) x = total;
+        total = G | (P & total);
+    }
+    if (carry_out != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *carry_out = total;
+
+    const unsigned lane = threadIdx.x & 31u;
+    const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const size_t t = warp * 32 + lane;
+    uint32_t cin = 0, pt = 0;
+    size_t len = 0;
+    if (t < n) {
+        const uint32_t st = state[t];
+        cin = ((st & kBitGex) ? 1u : 0u) | (((st & kBitPex) ? 1u : 0u) & x);
+        pt = st & 0xffffu;
+        const size_t L0 = t * size_t(kTile);
+        len = (m - L0) < size_t(kTile) ? (m - L0) : size_t(kTile);
+        if (cin && pt < len) {
+            uint64_t* q = out + L0 + pt;
+            *q = apply_carry<SUB>(*q, 1u);
+        }
+    }
+    // Deferred prefixes: the whole warp writes each one, coalesced.
+    uint32_t need = __ballot_sync(0xffffffffu, t < n && pt > 0);
+    while (need) {
+        const int src = __ffs(need) - 1;
+        need &= need - 1;
+        const uint32_t c = __shfl_sync(0xffffffffu, cin, src);
+        const uint32_t n_pre = __shfl_sync(0xffffffffu, pt, src);
+        const size_t L0 = (warp * 32 + size_t(src)) * size_t(kTile);
+        const uint64_t v = prop_value<SUB>(c);
+        for (uint32_t i = lane; i < n_pre; i += 32) out[L0 + i] = v;
+    }
+}
+
+}  // namespace
+
+size_t long_state_bytes(size_t m) {
+    const size_t n = num_tiles(m);
+    return ((n * sizeof(uint32_t)) + 255) / 256 * 256 + 256;
+}
+
+cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                              size_t m, void* state, uint32_t* agg, cudaStream_t stream) {
+    const size_t n = num_tiles(m);
+    uint32_t* st = static_cast<uint32_t*>(state);
+    if (n == 0) {
+        // Empty shard: identity aggregate {G = 0, P = 1}.
+        static const uint32_t ident[2] = {0u, 1u};
+        return cudaMemcpyAsync(agg, ident, sizeof(ident), cudaMemcpyHostToDevice, stream);
+    }
+    const bool vec = (reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                      reinterpret_cast<uintptr_t>(b)) % 32 == 0;
+    if (n > 0xffffffffull) return cudaErrorInvalidValue;
+    const unsigned grid = unsigned(n);
+    if (sub) {
+        if (vec) k_long_local<true, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+        else k_long_local<true, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+    } else {
+        if (vec) k_long_local<false, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+        else k_long_local<false, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_long_scan<<<1, 1024, 0, stream>>>(st, n, agg);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
+                               const uint32_t* all_aggs, int rank, int world, uint32_t* carry_out,
+                               cudaStream_t stream) {
+    const size_t n = num_tiles(m);
+    const size_t warps = (n + 31) / 32;
+    const size_t blocks = n == 0 ? 1 : (warps * 32 + 255) / 256;
+    const uint32_t* st = static_cast<const uint32_t*>(state);
+    if (sub)
+        k_long_finish<true><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, n, all_aggs, rank, world,
+                                                                  carry_out);
+    else
+        k_long_finish<false><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, n, all_aggs, rank, world,
+                                                                   carry_out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace dotg

@@ -1,0 +1,380 @@
+// capi.cu - the extern "C" boundary (include/dotg.h): argument validation with the
+// reference's error cases, device checks, dispatch to the kernels, and the host-buffer
+// pipelines (copy / compute overlap on two streams).
+//
+// Error mapping (reference throws std::invalid_argument):
+//   span length mismatch          addsub.cpp:139-140   -> not expressible (one m)
+//   mul m == 0 / m > 2^24         mul.cpp:13-18        -> DOTG_EINVAL
+//   unknown width                 addsub.cpp:125-134   -> dotg_validate_width
+//   partial aliasing              undefined in ref     -> DOTG_EINVAL (stricter)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/dotg.h"
+#include "internal.h"
+
+namespace dotg {
+std::atomic<uint64_t> g_launches{0};
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(DOTG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// The device path is sm_100a-only; refuse anything else loudly (no CPU fallback).
+int check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "no CUDA device");
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0)
+        return fail(DOTG_ECUDA, "dotg kernels are built for sm_100a; device is sm_" + std::to_string(major) +
+                                    std::to_string(minor));
+    return DOTG_OK;
+}
+
+bool ranges_overlap(const void* x, size_t xb, const void* y, size_t yb) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(x), b0 = reinterpret_cast<uintptr_t>(y);
+    return a0 < b0 + yb && b0 < a0 + xb;
+}
+
+// out may alias in exactly (same base, same extent); any other overlap is rejected.
+bool bad_alias(const void* out, const void* in, size_t bytes) {
+    return out != in && ranges_overlap(out, bytes, in, bytes);
+}
+
+int check_addsub(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m, size_t batch,
+                 int layout) {
+    if (layout != DOTG_ROW_MAJOR && layout != DOTG_INTERLEAVED) return fail(DOTG_EINVAL, "unknown layout");
+    if (batch == 0) return DOTG_OK;
+    if (m > 0 && (out == nullptr || a == nullptr || b == nullptr))
+        return fail(DOTG_EINVAL, "dot add/sub: null operand");
+    if (m > SIZE_MAX / 8 / batch) return fail(DOTG_EINVAL, "dot add/sub: size overflow");
+    const size_t bytes = m * batch * sizeof(uint64_t);
+    if (m > 0 && (bad_alias(out, a, bytes) || bad_alias(out, b, bytes)))
+        return fail(DOTG_EINVAL, "dot add/sub: out may alias a or b only exactly (addsub.hpp:95-97)");
+    if (flags != nullptr && m > 0 && ranges_overlap(flags, batch * 4, out, bytes))
+        return fail(DOTG_EINVAL, "dot add/sub: flags overlap out");
+    return DOTG_OK;
+}
+
+int check_mul(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout) {
+    if (layout != DOTG_ROW_MAJOR && layout != DOTG_INTERLEAVED) return fail(DOTG_EINVAL, "unknown layout");
+    if (m == 0) return fail(DOTG_EINVAL, "dot mul: operands need at least one limb");
+    if (m > (size_t(1) << 24)) return fail(DOTG_EINVAL, "dot mul: limb count exceeds the column accumulator bound");
+    if (batch == 0) return DOTG_OK;
+    if (out == nullptr || a == nullptr || b == nullptr) return fail(DOTG_EINVAL, "dot mul: null operand");
+    if (m > SIZE_MAX / 16 / batch) return fail(DOTG_EINVAL, "dot mul: size overflow");
+    const size_t ib = m * batch * 8, ob = 2 * ib;
+    if (ranges_overlap(out, ob, a, ib) || ranges_overlap(out, ob, b, ib))
+        return fail(DOTG_EINVAL, "dot mul: out must not overlap the operands");
+    return DOTG_OK;
+}
+
+int addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                 size_t batch, int layout, dotg_stream_t stream) {
+    int rc = check_addsub(out, a, b, flags, m, batch, layout);
+    if (rc != DOTG_OK) return rc;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_addsub_batch(sub, out, a, b, flags, m, batch, layout,
+                                              static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg add/sub batch launch");
+}
+
+int words(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry_out,
+          dotg_stream_t stream) {
+    int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (m == 0) {
+        if (carry_out == nullptr) return DOTG_OK;
+        cudaError_t e = cudaMemsetAsync(carry_out, 0, sizeof(uint32_t), st);
+        return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "memset");
+    }
+    const size_t sb = dotg::long_state_bytes(m);
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocAsync(&scratch, sb + 256, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("scratch: ") + cudaGetErrorString(e));
+    uint32_t* agg = reinterpret_cast<uint32_t*>(static_cast<char*>(scratch) + sb);
+    e = dotg::launch_long_local(sub, out, a, b, m, scratch, agg, st);
+    if (e == cudaSuccess) e = dotg::launch_long_finish(sub, out, m, scratch, agg, 0, 1, carry_out, st);
+    cudaError_t e2 = cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dotg words launch");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "scratch free");
+    return DOTG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host pipelines. One global staging context (host calls are synchronous).
+// ---------------------------------------------------------------------------
+struct HostCtx {
+    std::mutex mu;
+    int device = -1;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    char* buf[2] = {nullptr, nullptr};
+    size_t cap = 0;  // bytes per buffer
+};
+HostCtx g_host;
+
+int host_prepare(size_t bytes_per_slot) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (g_host.device != dev) {
+        for (int i = 0; i < 2; ++i) {
+            if (g_host.buf[i]) cudaFree(g_host.buf[i]);
+            g_host.buf[i] = nullptr;
+        }
+        g_host.cap = 0;
+        for (int i = 0; i < 2; ++i) {
+            if ((e = cudaStreamCreateWithFlags(&g_host.s[i], cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, "stream");
+        }
+        g_host.device = dev;
+    }
+    if (g_host.cap < bytes_per_slot) {
+        for (int i = 0; i < 2; ++i) {
+            if (g_host.buf[i]) cudaFree(g_host.buf[i]);
+            g_host.buf[i] = nullptr;
+            if ((e = cudaMalloc(&g_host.buf[i], bytes_per_slot)) != cudaSuccess)
+                return fail(DOTG_ENOMEM, std::string("staging: ") + cudaGetErrorString(e));
+        }
+        g_host.cap = bytes_per_slot;
+    }
+    return DOTG_OK;
+}
+
+constexpr size_t kSliceBytes = size_t(24) << 20;  // input bytes per slice (a + b)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// op: 0 add, 1 sub, 2 mul. Row-major host arrays.
+int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+               size_t batch) {
+    int rc = op == 2 ? check_mul(out, a, b, m, batch, DOTG_ROW_MAJOR)
+                     : check_addsub(out, a, b, flags, m, batch, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if (batch == 0) return DOTG_OK;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    if (op != 2 && m == 0) {
+        if (flags) std::memset(flags, 0, batch * sizeof(uint32_t));
+        return DOTG_OK;
+    }
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    const size_t in_b = m * 8;                          // per operand per pair
+    const size_t out_b = op == 2 ? 2 * m * 8 : m * 8;   // per pair
+    size_t slice = std::max<size_t>(1, kSliceBytes / (2 * in_b));
+    slice = std::min(slice, batch);
+    const size_t sa = align_up(slice * in_b, 256), so = align_up(slice * out_b, 256);
+    const size_t sf = align_up(slice * 4, 256);
+    if ((rc = host_prepare(2 * sa + so + sf)) != DOTG_OK) return rc;
+    cudaError_t e = cudaSuccess;
+    size_t k = 0;
+    for (size_t p0 = 0; p0 < batch && e == cudaSuccess; p0 += slice, ++k) {
+        const size_t n = std::min(slice, batch - p0);
+        const int i = int(k & 1);
+        cudaStream_t st = g_host.s[i];
+        uint64_t* da = reinterpret_cast<uint64_t*>(g_host.buf[i]);
+        uint64_t* db = reinterpret_cast<uint64_t*>(g_host.buf[i] + sa);
+        uint64_t* dout = reinterpret_cast<uint64_t*>(g_host.buf[i] + 2 * sa);
+        uint32_t* dfl = reinterpret_cast<uint32_t*>(g_host.buf[i] + 2 * sa + so);
+        // The previous use of this slot was enqueued on the same stream: ordered.
+        e = cudaMemcpyAsync(da, a + p0 * m, n * in_b, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db, b + p0 * m, n * in_b, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+            e = op == 2 ? dotg::launch_mul_batch(dout, da, db, m, n, 0, st)
+                        : dotg::launch_addsub_batch(op == 1, dout, da, db, flags ? dfl : nullptr, m, n, 0, st);
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out + p0 * (out_b / 8), dout, n * out_b, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && flags && op != 2)
+            e = cudaMemcpyAsync(flags + p0, dfl, n * 4, cudaMemcpyDeviceToHost, st);
+    }
+    cudaError_t e0 = cudaStreamSynchronize(g_host.s[0]);
+    cudaError_t e1 = cudaStreamSynchronize(g_host.s[1]);
+    if (e != cudaSuccess) return cuda_fail(e, "dotg host batch");
+    if (e0 != cudaSuccess) return cuda_fail(e0, "dotg host batch sync");
+    if (e1 != cudaSuccess) return cuda_fail(e1, "dotg host batch sync");
+    return DOTG_OK;
+}
+
+// Single long number from host spans: slices are independent shards (dotg_shard_*),
+// so H2D of slice k+1 overlaps the streaming pass of slice k; one finish pass per
+// slice then resolves the slice carry-ins from the gathered slice aggregates.
+int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
+    int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if (m == 0) {
+        if (carry) *carry = 0;
+        return DOTG_OK;
+    }
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    const size_t slice = std::max<size_t>(4096, (kSliceBytes / 16) / 4096 * 4096);
+    const size_t nsl = (m + slice - 1) / slice;
+    const size_t sb = align_up(dotg::long_state_bytes(slice), 256);
+    const size_t ab = align_up(m * 8, 256);
+    char* base = nullptr;
+    cudaStream_t s0 = g_host.s[0], s1 = g_host.s[1];
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * ab + nsl * sb + align_up(nsl * 8, 256) + 256, s0);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("words_host: ") + cudaGetErrorString(e));
+    uint64_t* da = reinterpret_cast<uint64_t*>(base);
+    uint64_t* db = reinterpret_cast<uint64_t*>(base + ab);
+    uint64_t* dout = reinterpret_cast<uint64_t*>(base + 2 * ab);
+    char* states = base + 3 * ab;
+    uint32_t* aggs = reinterpret_cast<uint32_t*>(states + nsl * sb);
+    uint32_t* dcarry = aggs + 2 * nsl;
+    cudaEvent_t ev = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, s0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev, 0);  // allocation visible on s1
+    for (size_t k = 0; k < nsl && e == cudaSuccess; ++k) {
+        const size_t l0 = k * slice, n = std::min(slice, m - l0);
+        cudaStream_t st = (k & 1) ? s1 : s0;
+        e = cudaMemcpyAsync(da + l0, a + l0, n * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db + l0, b + l0, n * 8, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+            e = dotg::launch_long_local(sub, dout + l0, da + l0, db + l0, n, states + k * sb, aggs + 2 * k, st);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(ev, s1);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, ev, 0);
+    for (size_t k = 0; k < nsl && e == cudaSuccess; ++k) {
+        const size_t l0 = k * slice, n = std::min(slice, m - l0);
+        e = dotg::launch_long_finish(sub, dout + l0, n, states + k * sb, aggs, int(k), int(nsl),
+                                     k == 0 ? dcarry : nullptr, s0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out + l0, dout + l0, n * 8, cudaMemcpyDeviceToHost, s0);
+    }
+    uint32_t hc = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hc, dcarry, 4, cudaMemcpyDeviceToHost, s0);
+    cudaError_t e2 = cudaFreeAsync(base, s0);
+    cudaError_t e3 = cudaStreamSynchronize(s0);
+    if (ev) cudaEventDestroy(ev);
+    if (e != cudaSuccess) return cuda_fail(e, "dotg words host");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    if (carry) *carry = hc;
+    return DOTG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dotg_validate_width(int width) {
+    if (width == 0 || width == 2 || width == 4 || width == 8) return DOTG_OK;
+    return fail(DOTG_EINVAL, "unknown width selector");
+}
+
+const char* dotg_last_error(void) { return g_err.c_str(); }
+
+const char* dotg_version(void) { return "dotg 0.1 sm_100a"; }
+
+int dotg_device_sms(void) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return sms;
+}
+
+uint64_t dotg_kernel_launches(void) { return dotg::g_launches.load(); }
+
+int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, dotg_stream_t stream) {
+    if (n > 0 && out == nullptr) return fail(DOTG_EINVAL, "fill: null out");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_fill_splitmix64(out, n, seed, offset, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "fill");
+}
+
+int dotg_add_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m, size_t batch,
+                   int layout, dotg_stream_t stream) {
+    return addsub_batch(false, out, a, b, flags, m, batch, layout, stream);
+}
+
+int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m, size_t batch,
+                   int layout, dotg_stream_t stream) {
+    return addsub_batch(true, out, a, b, flags, m, batch, layout, stream);
+}
+
+int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
+                   dotg_stream_t stream) {
+    int rc = check_mul(out, a, b, m, batch, layout);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_mul_batch(out, a, b, m, batch, layout, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg mul batch launch");
+}
+
+int dotg_add_words(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry_out,
+                   dotg_stream_t stream) {
+    return words(false, out, a, b, m, carry_out, stream);
+}
+
+int dotg_sub_words(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry_out,
+                   dotg_stream_t stream) {
+    return words(true, out, a, b, m, carry_out, stream);
+}
+
+size_t dotg_shard_state_bytes(size_t m) { return dotg::long_state_bytes(m); }
+
+int dotg_shard_local(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, void* state,
+                     uint32_t* agg, dotg_stream_t stream) {
+    int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if (state == nullptr || agg == nullptr) return fail(DOTG_EINVAL, "shard: null state/agg");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_long_local(sub != 0, out, a, b, m, state, agg, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg shard local");
+}
+
+int dotg_shard_finish(int sub, uint64_t* out, size_t m, void* state, const uint32_t* all_aggs, int rank, int world,
+                      uint32_t* carry_out, dotg_stream_t stream) {
+    if (world < 1 || rank < 0 || rank >= world) return fail(DOTG_EINVAL, "shard: bad rank/world");
+    if (state == nullptr || all_aggs == nullptr) return fail(DOTG_EINVAL, "shard: null state/aggs");
+    if (m > 0 && out == nullptr) return fail(DOTG_EINVAL, "shard: null out");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_long_finish(sub != 0, out, m, state, all_aggs, rank, world, carry_out,
+                                             static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg shard finish");
+}
+
+int dotg_add_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                        size_t batch) {
+    return batch_host(0, out, a, b, flags, m, batch);
+}
+int dotg_sub_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                        size_t batch) {
+    return batch_host(1, out, a, b, flags, m, batch);
+}
+int dotg_mul_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch) {
+    return batch_host(2, out, a, b, nullptr, m, batch);
+}
+int dotg_add_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
+    return words_host(false, out, a, b, m, carry);
+}
+int dotg_sub_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
+    return words_host(true, out, a, b, m, carry);
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// internal.h - launcher declarations shared between the kernel TUs and the C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+
+namespace dotg {
+
+// Launch counter reported by dotg_kernel_launches() (diagnostics for the bench's
+// gpu_launches claim).
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Batched add/sub. layout 0 = row-major [batch][m], 1 = interleaved [m][batch].
+cudaError_t launch_addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                uint32_t* flags, size_t m, size_t batch, int layout,
+                                cudaStream_t stream);
+
+// Long-number (tiled) add/sub, shard-capable. See addsub_long.cu.
+size_t long_state_bytes(size_t m);
+cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                              size_t m, void* state, uint32_t* agg, cudaStream_t stream);
+cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
+                               const uint32_t* all_aggs, int rank, int world,
+                               uint32_t* carry_out, cudaStream_t stream);
+
+// Batched multiplication (exactly 2m output limbs per pair).
+cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                             size_t batch, int layout, cudaStream_t stream);
+
+// Workload setup: splitmix64 counter fill (util.cu).
+cudaError_t launch_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, cudaStream_t st);
+
+}  // namespace dotg

@@ -1,0 +1,361 @@
+// mul_batch.cu - batched "vertical and crosswise" (column) multiplication on sm_100a.
+//
+// Replaces dot_mul_words (include/dot/mul.hpp:75-76, src/mul.cpp:96-103): gather pairs
+// into columns (mul.cpp:12-36), independent partial products (38-52), column
+// reduction (54-68), one carry pass (70-90), exactly 2m output limbs.
+//
+// B200 restatement: limbs are split into 32-bit words
+// (n = 2m words), every 32x32->64 partial product of a column is accumulated into a
+// 96-bit column accumulator with ONE IMAD.WIDE.U32 carrying out into a predicate plus
+// half an IADD3.X (ptxas fuses mad.lo.cc + madc.hi.cc + addc; measured 32 products /
+// clk / SM on B200 - tools/imad_peak.cu). A column of <= n products sums below
+// n * 2^64, so 96 bits cover every m up to the reference cap kMaxMulLimbs = 2^24
+// (mul.hpp:26-30). The carry pass is deferred to once per column / output block: the
+// accumulator's low word is final, the upper 64 bits carry into the next column.
+//
+// Kernels:
+//   k_mul_regs<M>   M <= 16: thread per pair, both operands in registers, columns
+//                   scanned in order (config 3: 1024-bit, M = 16).
+//   k_mul_smem<M>   M in {32, 64, 128}: thread per pair, operands staged in padded
+//                   shared memory by coalesced 256-bit loads, output produced in blocks
+//                   of K = 16 columns: for every (output block, a-block) pair a 16x16
+//                   block of products is accumulated into 16 independent column
+//                   accumulators (ILP 16; triangular edge blocks skip the zero
+//                   products, so exactly 4m^2 products are issued) (config 4: M = 64).
+//   k_mul_strided   any m / layout: thread per pair, operands read through L1.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace dotg {
+
+namespace {
+
+// acc(96) += x * y
+__device__ __forceinline__ void mac(uint32_t& lo, uint32_t& mid, uint32_t& hi, uint32_t x, uint32_t y) {
+    asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+        "addc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(mid), "+r"(hi)
+        : "r"(x), "r"(y));
+}
+
+// (lo,mid,hi) += (c0,c1,c2)
+__device__ __forceinline__ void add96(uint32_t& lo, uint32_t& mid, uint32_t& hi, uint32_t c0, uint32_t c1,
+                                      uint32_t c2) {
+    asm("add.cc.u32 %0, %0, %3;\n\t"
+        "addc.cc.u32 %1, %1, %4;\n\t"
+        "addc.u32 %2, %2, %5;"
+        : "+r"(lo), "+r"(mid), "+r"(hi)
+        : "r"(c0), "r"(c1), "r"(c2));
+}
+
+__device__ __forceinline__ uint32_t lo32(uint64_t x) { return uint32_t(x); }
+__device__ __forceinline__ uint32_t hi32(uint64_t x) { return uint32_t(x >> 32); }
+
+// ---------------------------------------------------------------------------
+// M <= 16: everything in registers.
+// ---------------------------------------------------------------------------
+template <int M, int LAYOUT>
+__global__ void __launch_bounds__(128) k_mul_regs(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                  size_t batch) {
+    constexpr int N = 2 * M;  // words per operand
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    uint32_t A[N], B[N];
+    if constexpr (LAYOUT == 0 && M % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < M / 4; ++v) {
+            uint64_t x[4], y[4];
+            ld_stream<4>(a + pidx * M + 4 * v, x);
+            ld_stream<4>(b + pidx * M + 4 * v, y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                A[8 * v + 2 * k] = lo32(x[k]);
+                A[8 * v + 2 * k + 1] = hi32(x[k]);
+                B[8 * v + 2 * k] = lo32(y[k]);
+                B[8 * v + 2 * k + 1] = hi32(y[k]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const size_t off = LAYOUT == 0 ? pidx * M + i : size_t(i) * batch + pidx;
+            const uint64_t x = a[off], y = b[off];
+            A[2 * i] = lo32(x);
+            A[2 * i + 1] = hi32(x);
+            B[2 * i] = lo32(y);
+            B[2 * i + 1] = hi32(y);
+        }
+    }
+    uint32_t lo = 0, mid = 0, hi = 0;
+    uint64_t o[4];
+    uint32_t prev = 0;
+#pragma unroll
+    for (int c = 0; c < 2 * N; ++c) {
+        if (c < 2 * N - 1) {
+#pragma unroll
+            for (int i = (c - N + 1 > 0 ? c - N + 1 : 0); i <= (c < N - 1 ? c : N - 1); ++i)
+                mac(lo, mid, hi, A[i], B[c - i]);
+        }
+        const uint32_t w = lo;
+        lo = mid;
+        mid = hi;
+        hi = 0;
+        if (c & 1) {
+            const int limb = c >> 1;
+            const uint64_t v = uint64_t(prev) | (uint64_t(w) << 32);
+            if constexpr (LAYOUT == 0 && (2 * M) % 4 == 0) {
+                o[limb & 3] = v;
+                if ((limb & 3) == 3) st_stream<4>(out + pidx * (2 * M) + (limb - 3), o);
+            } else {
+                const size_t off = LAYOUT == 0 ? pidx * (2 * M) + limb : size_t(limb) * batch + pidx;
+                out[off] = v;
+            }
+        } else {
+            prev = w;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// M in {32, 64, 128}: shared-memory operands, K = 16 output blocks.
+// ---------------------------------------------------------------------------
+constexpr int kK = 16;
+enum StepMode { kFull = 0, kLower = 1, kUpper = 2 };
+
+// acc[x] += sum_u A[u] * W[K + x - u]  (W[e] = b'_{(d-1)K + e}); kLower keeps x >= u
+// (d = 0: j = x - u must be >= 0), kUpper keeps x < u (d = NB: j < n).
+template <int MODE>
+__device__ __forceinline__ void mul_step(uint32_t (&acc)[kK][3], const uint32_t (&A)[kK],
+                                         const uint32_t (&W)[2 * kK]) {
+#pragma unroll
+    for (int u = 0; u < kK; ++u) {
+#pragma unroll
+        for (int x = 0; x < kK; ++x) {
+            if (MODE == kLower && x < u) continue;
+            if (MODE == kUpper && x >= u) continue;
+            mac(acc[x][0], acc[x][1], acc[x][2], A[u], W[kK + x - u]);
+        }
+    }
+}
+
+__device__ __forceinline__ void lds4(const uint32_t* p, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
+    const unsigned addr = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
+}
+__device__ __forceinline__ void sts4(uint32_t* p, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    const unsigned addr = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+}
+
+template <int M, int PAIRS>
+struct SmemCfg {
+    static constexpr int N = 2 * M;          // words per operand
+    static constexpr int NB = N / kK;        // a-blocks
+    static constexpr int NS = 2 * N / kK;    // output blocks
+    static constexpr int STRIDE = N + 4;     // padded words per pair (bank-conflict free v4)
+    static constexpr size_t SMEM = size_t(2) * PAIRS * STRIDE * sizeof(uint32_t);
+};
+
+template <int M, int PAIRS>
+__global__ void __launch_bounds__(PAIRS) k_mul_smem(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                    size_t batch) {
+    using C = SmemCfg<M, PAIRS>;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* sa = smem;
+    uint32_t* sb = smem + PAIRS * C::STRIDE;
+    const unsigned tid = threadIdx.x;
+    const size_t p0 = size_t(blockIdx.x) * PAIRS;
+
+    // Coalesced staging: the CTA's PAIRS rows of a (and b) are one contiguous block.
+    constexpr int VPP = M / 4;  // 256-bit vectors per pair per operand
+#pragma unroll 4
+    for (int v = tid; v < PAIRS * VPP; v += PAIRS) {
+        const int pr = v / VPP, ch = v % VPP;
+        const size_t gp = p0 + size_t(pr);
+        uint64_t x[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
+        if (gp < batch) {
+            ld_stream<4>(a + gp * M + 4 * ch, x);
+            ld_stream<4>(b + gp * M + 4 * ch, y);
+        }
+        uint32_t* da = sa + pr * C::STRIDE + 8 * ch;
+        uint32_t* db = sb + pr * C::STRIDE + 8 * ch;
+        sts4(da, lo32(x[0]), hi32(x[0]), lo32(x[1]), hi32(x[1]));
+        sts4(da + 4, lo32(x[2]), hi32(x[2]), lo32(x[3]), hi32(x[3]));
+        sts4(db, lo32(y[0]), hi32(y[0]), lo32(y[1]), hi32(y[1]));
+        sts4(db + 4, lo32(y[2]), hi32(y[2]), lo32(y[3]), hi32(y[3]));
+    }
+    __syncthreads();
+
+    const size_t gp = p0 + tid;
+    if (gp >= batch) return;
+    const uint32_t* pa = sa + tid * C::STRIDE;
+    const uint32_t* pb = sb + tid * C::STRIDE;
+    uint32_t cr0 = 0, cr1 = 0, cr2 = 0;  // carry into the next output block
+#pragma unroll 1
+    for (int s = 0; s < C::NS; ++s) {
+        uint32_t acc[kK][3];
+#pragma unroll
+        for (int x = 0; x < kK; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
+        const int i_lo = s - C::NB > 0 ? s - C::NB : 0;
+        const int i_hi = s < C::NB - 1 ? s : C::NB - 1;
+#pragma unroll 1
+        for (int I = i_lo; I <= i_hi; ++I) {
+            const int d = s - I;  // 0 .. NB
+            uint32_t A[kK], W[2 * kK];
+#pragma unroll
+            for (int q = 0; q < kK / 4; ++q) lds4(pa + I * kK + 4 * q, A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3]);
+            // W[e] = b'_{(d-1)K + e}; blocks outside [0, N) read as zero.
+#pragma unroll
+            for (int q = 0; q < 2 * kK / 4; ++q) {
+                const int j = (d - 1) * kK + 4 * q;
+                if (j >= 0 && j < C::N) lds4(pb + j, W[4 * q], W[4 * q + 1], W[4 * q + 2], W[4 * q + 3]);
+                else W[4 * q] = W[4 * q + 1] = W[4 * q + 2] = W[4 * q + 3] = 0;
+            }
+            if (d == 0) mul_step<kLower>(acc, A, W);
+            else if (d == C::NB) mul_step<kUpper>(acc, A, W);
+            else mul_step<kFull>(acc, A, W);
+        }
+        // Deferred normalisation of this block: 16 columns -> 16 final words.
+        uint32_t w[kK];
+#pragma unroll
+        for (int x = 0; x < kK; ++x) {
+            add96(acc[x][0], acc[x][1], acc[x][2], cr0, cr1, cr2);
+            w[x] = acc[x][0];
+            cr0 = acc[x][1];
+            cr1 = acc[x][2];
+            cr2 = 0;
+        }
+        uint64_t o0[4], o1[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            o0[k] = uint64_t(w[2 * k]) | (uint64_t(w[2 * k + 1]) << 32);
+            o1[k] = uint64_t(w[8 + 2 * k]) | (uint64_t(w[8 + 2 * k + 1]) << 32);
+        }
+        uint64_t* po = out + gp * (2 * M) + size_t(s) * (kK / 2);
+        st_stream<4>(po, o0);
+        st_stream<4>(po + 4, o1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Generic: any m, any layout (pair p, limb i at p*sp + i*si; out limb k at p*so + k*sio).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t word_at(const uint64_t* base, size_t si, size_t w) {
+    const uint64_t limb = base[(w >> 1) * si];
+    return (w & 1) ? hi32(limb) : lo32(limb);
+}
+
+__global__ void __launch_bounds__(256) k_mul_strided(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                     size_t m, size_t batch, size_t sp, size_t si,
+                                                     size_t so, size_t sio) {
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    const uint64_t* pa = a + pidx * sp;
+    const uint64_t* pb = b + pidx * sp;
+    uint64_t* po = out + pidx * so;
+    const size_t n = 2 * m;
+    uint32_t lo = 0, mid = 0, hi = 0, prev = 0;
+    for (size_t c = 0; c < 2 * n; ++c) {
+        if (c + 1 < 2 * n) {
+            const size_t i0 = c + 1 > n ? c + 1 - n : 0;
+            const size_t i1 = c < n - 1 ? c : n - 1;
+            for (size_t i = i0; i <= i1; ++i) mac(lo, mid, hi, word_at(pa, si, i), word_at(pb, si, c - i));
+        }
+        const uint32_t w = lo;
+        lo = mid;
+        mid = hi;
+        hi = 0;
+        if (c & 1) po[(c >> 1) * sio] = uint64_t(prev) | (uint64_t(w) << 32);
+        else prev = w;
+    }
+}
+
+template <int M, int LAYOUT>
+cudaError_t run_regs(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
+    const size_t blocks = (batch + 127) / 128;
+    k_mul_regs<M, LAYOUT><<<unsigned(blocks), 128, 0, st>>>(out, a, b, batch);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int M, int PAIRS>
+cudaError_t run_smem(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
+    using C = SmemCfg<M, PAIRS>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(k_mul_smem<M, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(C::SMEM));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const size_t blocks = (batch + PAIRS - 1) / PAIRS;
+    k_mul_smem<M, PAIRS><<<unsigned(blocks), PAIRS, C::SMEM, st>>>(out, a, b, batch);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                        int layout, cudaStream_t st) {
+    const size_t blocks = (batch + 255) / 256;
+    if (layout == 0)
+        k_mul_strided<<<unsigned(blocks), 256, 0, st>>>(out, a, b, m, batch, m, 1, 2 * m, 1);
+    else
+        k_mul_strided<<<unsigned(blocks), 256, 0, st>>>(out, a, b, m, batch, 1, batch, 1, batch);
+    count_launch();
+    return cudaGetLastError();
+}
+
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
+}  // namespace
+
+cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                             int layout, cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    const bool al = aligned32(out) && aligned32(a) && aligned32(b);
+    if (layout == 1) {
+        switch (m) {
+            case 1: return run_regs<1, 1>(out, a, b, batch, stream);
+            case 2: return run_regs<2, 1>(out, a, b, batch, stream);
+            case 4: return run_regs<4, 1>(out, a, b, batch, stream);
+            case 8: return run_regs<8, 1>(out, a, b, batch, stream);
+            case 16: return run_regs<16, 1>(out, a, b, batch, stream);
+            default: return run_strided(out, a, b, m, batch, 1, stream);
+        }
+    }
+    switch (m) {
+        case 1: return run_regs<1, 0>(out, a, b, batch, stream);
+        case 2:
+            if (al) return run_regs<2, 0>(out, a, b, batch, stream);
+            break;
+        case 4:
+            if (al) return run_regs<4, 0>(out, a, b, batch, stream);
+            break;
+        case 8:
+            if (al) return run_regs<8, 0>(out, a, b, batch, stream);
+            break;
+        case 16:
+            if (al) return run_regs<16, 0>(out, a, b, batch, stream);
+            break;
+        case 32:
+            if (al) return run_smem<32, 64>(out, a, b, batch, stream);
+            break;
+        case 64:
+            if (al) return run_smem<64, 64>(out, a, b, batch, stream);
+            break;
+        case 128:
+            if (al) return run_smem<128, 32>(out, a, b, batch, stream);
+            break;
+        default:
+            break;
+    }
+    return run_strided(out, a, b, m, batch, 0, stream);
+}
+
+}  // namespace dotg

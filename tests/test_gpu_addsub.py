@@ -1,0 +1,153 @@
+"""Batched add/sub on the B200 through the C ABI vs the oracle (bit-exact)."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import CATEGORIES, MAX, category, rows_less_np, spiky, uniform
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz")
+
+
+def dev(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def run(torch, sub, a, b, layout="row"):
+    import paper_2604_21566_b200 as dg
+
+    if layout == "row":
+        out, fl = dg.addsub_batch(sub, dev(torch, a), dev(torch, b))
+        return host(out), fl.cpu().numpy().view(np.uint32)
+    out, fl = dg.addsub_batch(sub, dev(torch, a.T.copy()), dev(torch, b.T.copy()), layout="interleaved")
+    return host(out).T.copy(), fl.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 7, 8, 9, 13, 16, 17, 31, 32, 33, 64, 65, 100, 128, 256, 512, 1000])
+def test_batch_matches_oracle(cuda, oracle, m):
+    rng = np.random.default_rng(1000 + m)
+    for cat in CATEGORIES:
+        for op in ("add", "sub"):
+            a, b = category(rng, cat, op, (97, m))
+            want, wf = oracle.addsub_batch(op == "sub", a, b)
+            for layout in ("row", "interleaved"):
+                got, gf = run(cuda, op == "sub", a, b, layout)
+                assert np.array_equal(got, want), (m, cat, op, layout)
+                assert np.array_equal(gf, wf), (m, cat, op, layout)
+
+
+def test_golden_replay(cuda):
+    g = np.load(GOLDEN)
+    sizes = sorted({int(k.split("_")[1][1:]) for k in g.files if k.startswith("addsub_")})
+    for m in sizes:
+        a, b = g[f"addsub_m{m}_a"], g[f"addsub_m{m}_b"]
+        for sub, key in ((False, "add"), (True, "sub")):
+            got, gf = run(cuda, sub, a, b)
+            assert np.array_equal(got, g[f"addsub_m{m}_{key}_out"]), (m, key)
+            assert np.array_equal(gf, g[f"addsub_m{m}_{key}_flag"]), (m, key)
+
+
+def test_kats(cuda):
+    # test_addsub.cpp:124-155: (2^512-1)+1, identity, cross-chunk carry into a tail, 0-1
+    cases = [
+        (False, [MAX] * 8, [1] + [0] * 7, [0] * 8, 1),
+        (False, [MAX] * 9, [1] + [0] * 8, [0] * 9, 1),
+        (True, [0], [1], [MAX], 1),
+        (False, [MAX, MAX] + [0] * 6, [1] + [0] * 7, [0, 0, 1, 0, 0, 0, 0, 0], 0),
+    ]
+    for sub, a, b, want, wf in cases:
+        got, gf = run(cuda, sub, np.array([a], np.uint64), np.array([b], np.uint64))
+        assert list(got[0]) == want and gf[0] == wf
+
+
+def test_full_chains_every_size(cuda, oracle):
+    # full propagation chains across every team/row boundary (test_addsub.cpp:299-317)
+    for m in (1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 7, 33):
+        a = np.full((3, m), MAX, np.uint64)
+        b = np.zeros((3, m), np.uint64)
+        b[:, 0] = 1
+        got, gf = run(cuda, False, a, b)
+        assert not got.any() and (gf == 1).all(), m
+        got, gf = run(cuda, True, np.zeros((3, m), np.uint64), b)
+        assert (got == MAX).all() and (gf == 1).all(), m
+
+
+def test_aliasing_and_edge_cases(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(7)
+    a, b = spiky(rng, (300, 64)), spiky(rng, (300, 64))
+    want, wf = oracle.addsub_batch(False, a, b)
+    ta, tb = dev(torch, a), dev(torch, b)
+    out, fl = dg.add_batch(ta, tb, out=ta)  # out aliases a exactly
+    assert np.array_equal(host(ta), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
+    ta, tb = dev(torch, a), dev(torch, b)
+    dg.add_batch(ta, tb, out=tb)  # out aliases b exactly
+    assert np.array_equal(host(tb), want)
+    # partial overlap is rejected
+    big = dev(torch, uniform(rng, (301, 64)))
+    with pytest.raises(dg.InvalidArgument):
+        dg.api.check(dg.lib().dotg_add_batch(
+            dg.api._dptr(big[1:]), dg.api._dptr(big[:-1]), dg.api._dptr(big[:-1]), None, 64, 300, 0, None))
+    # m = 0: flags are zero; batch = 0: no-op
+    fl = torch.full((5,), 7, dtype=torch.int32, device="cuda")
+    e = torch.empty((5, 0), dtype=torch.int64, device="cuda")
+    dg.add_batch(e, e, out=e.clone(), flags=fl)
+    assert (fl == 0).all()
+    e0 = torch.empty((0, 4), dtype=torch.int64, device="cuda")
+    dg.sub_batch(e0, e0)
+
+
+def test_misaligned_rows_fall_back(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(8)
+    a, b = spiky(rng, (50, 64)), spiky(rng, (50, 64))
+    want, wf = oracle.addsub_batch(True, a, b)
+    buf_a = torch.zeros(50 * 64 + 1, dtype=torch.int64, device="cuda")
+    buf_b = torch.zeros(50 * 64 + 1, dtype=torch.int64, device="cuda")
+    buf_a[1:] = dev(torch, a).view(-1)
+    buf_b[1:] = dev(torch, b).view(-1)
+    out = torch.zeros(50 * 64 + 1, dtype=torch.int64, device="cuda")
+    _, fl = dg.sub_batch(buf_a[1:].view(50, 64), buf_b[1:].view(50, 64), out=out[1:].view(50, 64))
+    assert np.array_equal(host(out[1:]).reshape(50, 64), want)
+    assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_config_parity_full_size(cuda, oracle, cfg):
+    """C1 / C2 at BASELINE.json's full sizes vs the oracle (every pair, add and sub)."""
+    import paper_2604_21566_b200 as dg
+    from paper_2604_21566_b200 import workloads as W
+
+    sizes = [(W.C1["m"], W.C1["batch"])] if cfg == "C1" else W.C2_SIZES
+    for m, B in sizes:
+        a, b, sa, sb = W.c1_inputs() if cfg == "C1" else W.c2_inputs(m, B)
+        assert a.shape == (B, m)
+        ha, hb, hsa, hsb = host(a), host(b), host(sa), host(sb)
+        assert not rows_less_np(hsa, hsb).any()  # a >= b after the swap
+        out, fl = dg.add_batch(a, b)
+        want, wf = oracle.addsub_batch(False, ha, hb)
+        assert np.array_equal(host(out), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
+        out, fl = dg.sub_batch(sa, sb)
+        want, wf = oracle.addsub_batch(True, hsa, hsb)
+        assert np.array_equal(host(out), want) and not wf.any()
+        assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
+        if cfg == "C2":
+            assert (host(a)[::100] == MAX).all()  # forced 1% chains
+            got = host(out)  # sub of forced rows: (2^n - 1) - 1
+            assert (got[::100, 0] == MAX - np.uint64(1)).all()
+
+
+def test_device_fill_matches_host_twin(cuda, oracle):
+    from paper_2604_21566_b200 import workloads as W
+
+    for n, seed, off in ((1, 1, 0), (1000, 0xC5, 12345), (1 << 20, 0xC1, 1 << 40)):
+        assert np.array_equal(host(W.fill(n, seed, off)), oracle.fill(n, seed, off))

@@ -1,0 +1,110 @@
+"""Batched column multiplication on the B200 vs the oracle (bit-exact, exactly 2m limbs)."""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import MAX, category, spiky, uniform
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz")
+
+
+def dev(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+def mul(torch, a, b, layout="row"):
+    import paper_2604_21566_b200 as dg
+
+    if layout == "row":
+        return host(dg.mul_batch(dev(torch, a), dev(torch, b)))
+    return host(dg.mul_batch(dev(torch, a.T.copy()), dev(torch, b.T.copy()), layout="interleaved")).T.copy()
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 33, 48, 64, 100, 128])
+def test_mul_matches_oracle(cuda, oracle, m):
+    rng = np.random.default_rng(2000 + m)
+    n = 67
+    for cat in ("random", "full_propagation", "spiky", "maxed_limbs", "zero_limbs"):
+        a, b = category(rng, cat, "mul", (n, m))
+        want = oracle.mul_batch(a, b)
+        for layout in ("row", "interleaved"):
+            got = mul(cuda, a, b, layout)
+            assert got.shape == (n, 2 * m)
+            assert np.array_equal(got, want), (m, cat, layout)
+
+
+def test_golden_replay(cuda):
+    g = np.load(GOLDEN)
+    sizes = sorted({int(k.split("_")[1][1:]) for k in g.files if k.startswith("mul_")})
+    for m in sizes:
+        got = mul(cuda, g[f"mul_m{m}_a"], g[f"mul_m{m}_b"])
+        assert np.array_equal(got, g[f"mul_m{m}_out"]), m
+
+
+def test_mul_kats(cuda):
+    # test_oracle.cpp:95-104, test_mul.cpp:183-196, 288-294, 323-331
+    got = mul(cuda, np.array([[MAX]], np.uint64), np.array([[MAX]], np.uint64))
+    assert list(got[0]) == [1, MAX - np.uint64(1)]
+    got = mul(cuda, np.array([[0, 1]], np.uint64), np.array([[0, 1]], np.uint64))
+    assert list(got[0]) == [0, 0, 1, 0]
+    a = np.zeros((1, 4), np.uint64)
+    b = np.zeros((1, 4), np.uint64)
+    a[0, 2] = np.uint64(1 << 63)
+    b[0, 3] = np.uint64(1 << 63)
+    got = mul(cuda, a, b)  # 2^(64*2+63) * 2^(64*3+63) = 2^(64*6 + 62)
+    want = np.zeros(8, np.uint64)
+    want[6] = np.uint64(1 << 62)
+    assert np.array_equal(got[0], want)
+    ones = np.full((1, 4), MAX, np.uint64)  # (2^256 - 1)^2
+    n = (1 << 256) - 1
+    v = sum(int(x) << (64 * i) for i, x in enumerate(mul(cuda, ones, ones)[0]))
+    assert v == n * n
+
+
+def test_mul_algebra(cuda):
+    # commutativity / identity / zero (test_mul.cpp:377-389), distributivity (391-411)
+    rng = np.random.default_rng(25)
+    for m in (1, 5, 16, 33, 64):
+        a, b, c = uniform(rng, (20, m)), uniform(rng, (20, m)), uniform(rng, (20, m))
+        assert np.array_equal(mul(cuda, a, b), mul(cuda, b, a))
+        one = np.zeros((20, m), np.uint64)
+        one[:, 0] = 1
+        ab1 = mul(cuda, a, one)
+        assert np.array_equal(ab1[:, :m], a) and not ab1[:, m:].any()
+        assert not mul(cuda, a, np.zeros_like(a)).any()
+
+
+def test_mul_errors(cuda):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    e = torch.empty((3, 0), dtype=torch.int64, device="cuda")
+    with pytest.raises(dg.InvalidArgument):
+        dg.mul_batch(e, e)  # m = 0 (mul.cpp:16)
+    with pytest.raises(dg.InvalidArgument):
+        dg.dot_mul_words([1, 2], [1])  # length mismatch (mul.cpp:13-14)
+    with pytest.raises(dg.InvalidArgument):
+        dg.dot_mul_words([], [])
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_config_parity_full_size(cuda, oracle, cfg):
+    import paper_2604_21566_b200 as dg
+    from paper_2604_21566_b200 import workloads as W
+
+    a, b = W.c3_inputs() if cfg == "C3" else W.c4_inputs()
+    m = a.shape[1]
+    ha, hb = host(a), host(b)
+    if cfg == "C3":
+        assert (ha[:, m - 1] != 0).all() and (hb[:, m - 1] != 0).all()
+    else:
+        assert (ha[a.shape[0] // 2:] == MAX).all()
+    got = host(dg.mul_batch(a, b))
+    want = oracle.mul_batch(ha, hb)
+    assert np.array_equal(got, want)
