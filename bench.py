@@ -1,0 +1,573 @@
+#!/usr/bin/env python
+"""bench.py - B200 limb arithmetic (DigitsOnTurbo hot path) benchmark.
+
+Headline workload (BASELINE.json configs[1], "C2"): the carry-stress add/sub sweep -
+(m, B) in (4, 2^20), (16, 2^18), (64, 2^16), (256, 2^14); each limb all-ones with p=1/2
+else uniform, 1% of pairs forced to a full-length carry chain; sub swaps pairs so a >= b.
+One step = batched add at all four sizes, then batched sub at all four sizes, through the
+device C ABI (dotg_add_batch / dotg_sub_batch). Metric: algorithmic GB/s
+(24m + 4 bytes per pair-op), roofline = measured HBM copy bandwidth.
+
+The same JSON line also reports C1 (4096-bit add/sub), C3/C4 (1024/4096-bit mul,
+products/s vs the measured IMAD.WIDE roofline) and C5 (one 2^30-limb add/sub) under
+"configs".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--only C2] [--no-secondary]
+
+N > 1: launched by torch.distributed.run, one rank per GPU; every rank runs the full
+batch sweep on its own GPU (weak scaling, no collective on the data path); value = the
+bytes of all ranks / max-over-ranks time. --impl reference times the reference's own
+CPU implementation (oracle/_ref/libdotref.so: span-form dot_add_words / dot_sub_words
+at Width::w8 and dot_mul_words) on all host cores; under torchrun only rank 0 works.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+IMAD_WIDE_PER_CLK_SM = 32.0  # measured: profiles/r01_imad_peak.json (cc_chain_products)
+C2_SIZES = [(4, 1 << 20), (16, 1 << 18), (64, 1 << 16), (256, 1 << 14)]
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", HBM_FALLBACK_GBS)), "measured", float(j.get("sm_max_mhz", 1965.0))
+    return HBM_FALLBACK_GBS, "fallback", 1965.0
+
+
+def traffic_table():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0, period_ms=50):
+        self.index, self.period_ms = index, period_ms
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 f"-lms={self.period_ms}"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        load = [s for s in sm if s > 400] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm (oracle/_ref/libdotref.so, or the oracle port without it)
+# ---------------------------------------------------------------------------
+class CpuRef:
+    def __init__(self):
+        ref_so = os.path.join(ROOT, "oracle", "_ref", "libdotref.so")
+        orc_so = os.path.join(ROOT, "oracle", "liboracle.so")
+        self.threads = os.cpu_count() or 1
+        if os.path.exists(ref_so):
+            self.kind = "reference"
+            L = ctypes.CDLL(ref_so)
+            L.dotref_batch.restype = ctypes.c_int
+            L.dotref_batch.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 4 + [ctypes.c_size_t] * 2 + [
+                ctypes.c_int]
+            L.dotref_dispatch_note.restype = ctypes.c_char_p
+            L.dotref_dispatch_note.argtypes = [ctypes.c_int]
+            self.note = L.dotref_dispatch_note(8).decode()
+        elif os.path.exists(orc_so):
+            self.kind = "port"
+            L = ctypes.CDLL(orc_so)
+            self.threads = 1
+            self.note = "oracle port (scalar)"
+        else:
+            raise SystemExit("neither oracle/_ref/libdotref.so nor oracle/liboracle.so is built")
+        self.L = L
+
+    def run(self, op, a, b, out, flags):
+        """op 0 add, 1 sub, 2 mul on [B, m] numpy uint64 arrays (reference DoT path)."""
+        B, m = a.shape
+        P = lambda x: None if x is None else ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+        if self.kind == "reference":
+            rc = self.L.dotref_batch(op, 0, P(out), P(a), P(b), P(flags), m, B, self.threads)
+            if rc != 0:
+                raise RuntimeError("reference batch failed")
+        else:
+            if op == 2:
+                self.L.dotor_mul_batch(P(out), P(a), P(b), ctypes.c_size_t(m), ctypes.c_size_t(B))
+            else:
+                self.L.dotor_addsub_batch(op, P(out), P(a), P(b), P(flags), ctypes.c_size_t(m), ctypes.c_size_t(B))
+
+
+def host_c2_inputs():
+    """C2 inputs on the host via the oracle's splitmix64 twin (same values as the device
+    generator in paper_2604_21566_b200/workloads.py)."""
+    import numpy as np
+
+    L = ctypes.CDLL(os.path.join(ROOT, "oracle", "liboracle.so"))
+    L.dotor_fill_splitmix64.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_uint64]
+
+    def fill(n, seed, off):
+        x = np.empty(n, np.uint64)
+        L.dotor_fill_splitmix64(ctypes.c_void_p(x.ctypes.data), n, seed, off)
+        return x
+
+    MAX = np.uint64(0xFFFFFFFFFFFFFFFF)
+    sets = []
+    for m, B in C2_SIZES:
+        s, n = 0xC2 + m, B * m
+
+        def operand(off):
+            v = fill(n, s, off)
+            sel = fill(n, s, off + n)
+            v[(sel & np.uint64(1)) == 1] = MAX
+            return v.reshape(B, m)
+
+        a, b = operand(0), operand(2 * n)
+        a[::100] = MAX
+        b[::100] = 0
+        b[::100, 0] = 1
+        ne = a != b
+        idx = (m - 1) - np.argmax(ne[:, ::-1], axis=1)
+        r = np.arange(B)
+        lt = (ne.any(axis=1) & (a[r, idx] < b[r, idx]))[:, None]
+        sa, sb = np.where(lt, b, a), np.where(lt, a, b)
+        sets.append((m, B, a, b, np.ascontiguousarray(sa), np.ascontiguousarray(sb)))
+    return sets
+
+
+def c2_bytes():
+    return sum(2 * (B * (24 * m + 4)) for m, B in C2_SIZES)
+
+
+def cpu_c2_measure(cpu, sets, min_seconds=3.0, max_reps=200):
+    """Time the reference on the full C2 step (add + sub at all sizes), repeated until
+    min_seconds of CPU work; returns (GB/s, reps, seconds)."""
+    import numpy as np
+
+    outs = [(np.empty_like(a), np.empty(B, np.uint32)) for (m, B, a, b, sa, sb) in sets]
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        for (m, B, a, b, sa, sb), (o, f) in zip(sets, outs):
+            cpu.run(0, a, b, o, f)
+        for (m, B, a, b, sa, sb), (o, f) in zip(sets, outs):
+            cpu.run(1, sa, sb, o, f)
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds or reps >= max_reps:
+            break
+    return c2_bytes() * reps / dt / 1e9, reps, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cpu = CpuRef()
+    sets = host_c2_inputs()
+    import numpy as np
+
+    outs = [(np.empty_like(a), np.empty(B, np.uint32)) for (m, B, a, b, sa, sb) in sets]
+
+    def step():
+        for (m, B, a, b, sa, sb), (o, f) in zip(sets, outs):
+            cpu.run(0, a, b, o, f)
+        for (m, B, a, b, sa, sb), (o, f) in zip(sets, outs):
+            cpu.run(1, sa, sb, o, f)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    gbs = c2_bytes() * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": "add/sub GB/s (C2 carry-stress sweep, 4/16/64/256 limbs)", "value": gbs,
+        "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (seeded splitmix64, BASELINE.json configs[1] distribution)",
+        "config": {"workload": "C2 carry-stress add+sub sweep", "sizes": C2_SIZES, "layout": "row-major"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
+                         "sample": f"full C2 step (add+sub, 4 sizes) x {args.steps} steps; route {cpu.note}"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+class Launcher:
+    """Pre-bound ctypes calls of the device C ABI (keeps Python off the critical path)."""
+
+    def __init__(self, torch, lib, stream):
+        self.torch, self.lib = torch, lib
+        self.stream = ctypes.c_void_p(stream.cuda_stream)
+
+    def addsub(self, sub, out, a, b, flags, m, B):
+        fn = self.lib.dotg_sub_batch if sub else self.lib.dotg_add_batch
+        args = (ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                ctypes.c_void_p(flags.data_ptr()), m, B, 0, self.stream)
+        return lambda: fn(*args)
+
+    def mul(self, out, a, b, m, B):
+        fn = self.lib.dotg_mul_batch
+        args = (ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), m, B,
+                0, self.stream)
+        return lambda: fn(*args)
+
+
+def timed_steps(torch, dist, world, stream, calls, steps, warmup):
+    """Run `calls` (zero-arg callables, one device launch sequence each) per step:
+    W warm-up steps, then K timed steps bracketed by barrier + synchronize and timed
+    with CUDA events on the launching stream (max over ranks). A second pass of K steps
+    records an event pair around every call to get per-kernel durations (the roofline's
+    launch duration) without slowing the lean timed loop. Returns
+    (ms_per_step, [mean ms per call])."""
+    for _ in range(warmup):
+        for c in calls:
+            rc = c()
+            if rc != 0:
+                raise RuntimeError(f"dotg call failed rc={rc}")
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        for c in calls:
+            c()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    total_ms = t0.elapsed_time(t1)
+    if dist is not None and world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
+           for _ in range(steps)]
+    for s in range(steps):
+        for i, c in enumerate(calls):
+            evs[s][i][0].record(stream)
+            c()
+            evs[s][i][1].record(stream)
+    torch.cuda.synchronize()
+    per_call = [sum(evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(steps)) / steps for i in range(len(calls))]
+    return total_ms / steps, per_call
+
+
+def run_ours(args, rank, world, dist):
+    import numpy as np
+    import torch
+
+    import paper_2604_21566_b200 as dg
+    from paper_2604_21566_b200 import workloads as W
+
+    lib = dg.lib()  # raises if libdotg.so is missing: no fallback
+    torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+    stream = torch.cuda.current_stream()
+    L = Launcher(torch, lib, stream)
+    hbm_peak, peak_kind, sm_max = peaks()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+
+    # ---- headline: C2 sweep, device-resident ----
+    bufs = []
+    for m, B in C2_SIZES:
+        a, b, sa, sb = W.c2_inputs(m, B)
+        bufs.append(dict(m=m, B=B, a=a, b=b, sa=sa, sb=sb, oa=torch.empty_like(a), os=torch.empty_like(a),
+                         fa=torch.empty(B, dtype=torch.int32, device="cuda"),
+                         fs=torch.empty(B, dtype=torch.int32, device="cuda")))
+    calls = [L.addsub(False, x["oa"], x["a"], x["b"], x["fa"], x["m"], x["B"]) for x in bufs]
+    calls += [L.addsub(True, x["os"], x["sa"], x["sb"], x["fs"], x["m"], x["B"]) for x in bufs]
+    calls_meta = list(range(len(calls)))
+    call_bytes = [x["B"] * (24 * x["m"] + 4) for x in bufs] * 2
+    step_bytes = sum(call_bytes)
+    assert step_bytes == c2_bytes()
+    working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per step (a, b, sa, sb)
+
+    sampler = ClockSampler(env_int("LOCAL_RANK", 0))
+    sampler.start()
+    time.sleep(0.2)
+    launches0 = dg.kernel_launches()
+    ms_step, per_call = timed_steps(torch, dist if world > 1 else None, world, stream, calls, args.steps,
+                                    args.warmup)
+    # launches inside the lean timed region (the event pass repeats it once more)
+    launches = (dg.kernel_launches() - launches0 - args.warmup * len(calls)) // 2
+    clocks = sampler.stop()
+    value = step_bytes * world / (ms_step * 1e-3) / 1e9
+    # average launch duration of the batched add/sub kernel = lean-loop step time / launches
+    # (inter-launch gaps included: conservative); per_size uses event-bracketed launches.
+    achieved = step_bytes / (ms_step * 1e-3) / 1e9
+    per_size = {f"m{x['m']}": {"add_gbs": call_bytes[i] / (per_call[i] * 1e-3) / 1e9,
+                               "sub_gbs": call_bytes[i] / (per_call[i + 4] * 1e-3) / 1e9}
+                for i, x in enumerate(bufs)}
+    traffic = traffic_table().get("C2_per_launch_bytes")
+
+    # ---- e2e: the same step through the host-buffer C ABI (pinned host arrays) ----
+    e2e = None
+    if not args.no_e2e:
+        hsets = []
+        for x in bufs:
+            hs = {}
+            for k in ("a", "b", "sa", "sb"):
+                h = torch.empty(x[k].shape, dtype=torch.int64, pin_memory=True)
+                h.copy_(x[k])
+                hs[k] = h
+            hs["o"] = torch.empty(x["a"].shape, dtype=torch.int64, pin_memory=True)
+            hs["f"] = torch.empty(x["B"], dtype=torch.int32, pin_memory=True)
+            hsets.append((x["m"], x["B"], hs))
+        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+
+        def e2e_step():
+            for m, B, hs in hsets:
+                rc = lib.dotg_add_batch_host(P(hs["o"]), P(hs["a"]), P(hs["b"]), P(hs["f"]), m, B)
+                assert rc == 0, lib.dotg_last_error()
+            for m, B, hs in hsets:
+                rc = lib.dotg_sub_batch_host(P(hs["o"]), P(hs["sa"]), P(hs["sb"]), P(hs["f"]), m, B)
+                assert rc == 0, lib.dotg_last_error()
+
+        e2e_step()
+        # correctness spot check of the e2e path against the device result (last call = sub m=256)
+        m, B, hs = hsets[-1]
+        assert torch.equal(hs["o"], bufs[-1]["os"].cpu()), "e2e result mismatch"
+        e_steps = max(3, min(args.steps, 20))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = sum(2 * 2 * B * m * 8 for m, B in C2_SIZES)
+        d2h = sum(2 * (B * m * 8 + 4 * B) for m, B in C2_SIZES)
+        e2e = {"value": step_bytes * world * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": e_steps,
+               "api": "dotg_add_batch_host / dotg_sub_batch_host (pinned host buffers, 2-stream copy/compute overlap)"}
+        del hsets
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = CpuRef()
+            sets = host_c2_inputs()
+            gbs, reps, dt = cpu_c2_measure(cpu, sets, min_seconds=args.cpu_seconds)
+            cpu_baseline = {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
+                            "sample": f"full C2 step (add+sub at 4 sizes, {c2_bytes() / 1e6:.0f} MB) x {reps} reps "
+                                      f"({dt:.1f} s), span-form dot_add_words/dot_sub_words route {cpu.note}"}
+            del sets
+        except Exception as e:  # noqa: BLE001
+            cpu_baseline = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
+
+    # free the headline buffers before the secondary configs
+    del bufs, calls
+    torch.cuda.empty_cache()
+
+    secondary = {}
+    if not args.no_secondary:
+        secondary = run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms)
+
+    line = {
+        "metric": "add/sub GB/s vs HBM peak (C2 carry-stress sweep, 4/16/64/256 limbs)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: limb all-ones p=0.5 else "
+                "uniform, 1% forced full carry chains, sub swapped to a>=b)",
+        "config": {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
+                   "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
+                   "step": "8 launches: add at 4 sizes then sub at 4 sizes",
+                   "l2": f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct "
+                         "inputs (126 MB L2), every buffer touched once per step",
+                   "per_rank": "full sweep on every rank (weak scaling, no collective)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "k_addsub_team (batched add/sub, warp-ballot lookahead)",
+                     "algorithmic_bytes_per_launch": step_bytes / len(calls_meta),
+                     "launch_us_avg": ms_step * 1e3 / len(calls_meta), "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                     "per_size": per_size},
+        "cpu_baseline": cpu_baseline,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "configs": secondary,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms):
+    out = {}
+    steps = max(3, min(args.steps, 50))
+    warm = max(3, args.warmup)
+    dd = dist if world > 1 else None
+
+    # C1: 4096-bit add + sub (rotate 3 input sets -> 300 MB between reuses > L2)
+    sets = []
+    for r in range(3):
+        a = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 0).view(-1, 64)
+        b = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 1 << 40).view(-1, 64)
+        sa, sb = W.swap_for_sub(a, b)
+        sets.append((a, b, sa, sb, torch.empty_like(a), torch.empty(a.shape[0], dtype=torch.int32, device="cuda")))
+    B = W.C1["batch"]
+    calls = []
+    for a, b, sa, sb, o, f in sets:
+        calls.append(L.addsub(False, o, a, b, f, 64, B))
+        calls.append(L.addsub(True, o, sa, sb, f, 64, B))
+    ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
+    byts = B * (24 * 64 + 4)
+    out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * len(calls) * world / (ms * 1e-3) / 1e9,
+                 "unit": "GB/s", "kernel_gbs": byts * len(calls) / (sum(per) * 1e-3) / 1e9,
+                 "frac_hbm": byts * len(calls) / (sum(per) * 1e-3) / 1e9 / hbm_peak,
+                 "add_us": statistics.mean(per[0::2]) * 1e3, "sub_us": statistics.mean(per[1::2]) * 1e3}
+    del sets, calls
+    torch.cuda.empty_cache()
+
+    imad_peak_pps = sms * IMAD_WIDE_PER_CLK_SM * sm_max * 1e6  # u32 products / s at max clock
+    for name, gen, m in (("C3", W.c3_inputs, 16), ("C4", W.c4_inputs, 64)):
+        a, b = gen()
+        Bn = a.shape[0]
+        o = torch.empty((Bn, 2 * m), dtype=torch.int64, device="cuda")
+        calls = [L.mul(o, a, b, m, Bn)]
+        ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
+        pairs_s = Bn / (per[0] * 1e-3)
+        prods = 4 * m * m
+        out[name] = {"metric": f"{64 * m}-bit mul products/s (pairs/s)", "value": Bn * world / (ms * 1e-3),
+                     "unit": "pairs/s", "kernel_pairs_s": pairs_s, "kernel_us": per[0] * 1e3,
+                     "u32_products_per_s": pairs_s * prods,
+                     "imad_roofline_u32_products_per_s": imad_peak_pps,
+                     "frac_imad": pairs_s * prods / imad_peak_pps,
+                     "hbm_gbs": Bn * 32 * m / (per[0] * 1e-3) / 1e9,
+                     "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
+        del a, b, o, calls
+        torch.cuda.empty_cache()
+
+    if not args.no_c5:
+        m = W.C5_M if world == 1 else W.C5_M // world
+        if world == 1:
+            free = torch.cuda.mem_get_info()[0]
+            if free < 3 * m * 8 + (1 << 30):
+                out["C5"] = {"skipped": f"needs {3 * m * 8 / 2**30:.0f} GiB free"}
+                return out
+        res = {}
+        for sub in (False, True):
+            if world == 1:
+                a, b = W.c5_inputs(sub)
+                o = torch.empty_like(a)
+                c = torch.empty(1, dtype=torch.int32, device="cuda")
+                fn = dg.lib().dotg_sub_words if sub else dg.lib().dotg_add_words
+                args_ = (ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                         m, ctypes.c_void_p(c.data_ptr()), L.stream)
+                ms, per = timed_steps(torch, None, 1, stream, [lambda: fn(*args_)], 3, 2)
+                res["sub" if sub else "add"] = {"ms": ms, "gbs": 24 * m / (ms * 1e-3) / 1e9,
+                                                "frac_hbm": 24 * m / (ms * 1e-3) / 1e9 / hbm_peak,
+                                                "carry": int(c.item())}
+                del a, b, o
+            torch.cuda.empty_cache()
+        out["C5"] = {"metric": "one 2^30-limb add/sub GB/s", "unit": "GB/s", "n_limbs": W.C5_M,
+                     "run": list(W.C5_RUN), **res}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        if args.impl == "ours":
+            torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    try:
+        if args.impl == "reference":
+            return run_reference(args, rank, world)
+        return run_ours(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,149 @@
+// dot_b200.hpp - header-only C++ drop-in for the reference's hot-path API, over the C ABI.
+//
+// Mirrors namespace dot of the reference (include/dot/limbs.hpp, addsub.hpp, mul.hpp):
+// same type names, same signatures, same argument meaning, same std::invalid_argument
+// cases. A caller switches by replacing `#include "dot/addsub.hpp"` / `"dot/mul.hpp"`
+// with this header and `dot::` with `dot_b200::` (or a namespace alias), and linking
+// libdotg.so. The arithmetic runs on the B200 (sm_100a); host spans are staged through
+// device memory by the *_host entry points of dotg.h. There is no CPU fallback: without
+// a usable device every call throws std::runtime_error.
+//
+// Differences, by design:
+//   * AddSubStats instrumentation (addsub.hpp:53-72) is not produced by the device path;
+//     passing a non-null stats pointer throws std::logic_error.
+//   * Only the saturated 64-bit radix is on the device path (RadixConfig{52} throws
+//     std::logic_error; the 52-bit 4x4/5x5 route is out of scope).
+//   * Partial aliasing of out with a/b (undefined in the reference) throws.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dotg.h"
+
+namespace dot_b200 {
+
+using limb_t = std::uint64_t;       // limbs.hpp:17
+using Limbs = std::vector<limb_t>;  // limbs.hpp:18
+
+struct WordsResult {  // limbs.hpp:28-31
+    Limbs limbs;
+    unsigned flag = 0;
+};
+
+struct RadixConfig {  // limbs.hpp:39-49
+    unsigned limb_bits = 64;
+};
+inline constexpr RadixConfig kSaturated{64};
+inline constexpr RadixConfig kUnsaturated{52};
+
+enum class Width : std::uint8_t { scalar = 0, w2 = 2, w4 = 4, w8 = 8 };  // addsub.hpp:30
+constexpr unsigned lane_count(Width w) { return w == Width::scalar ? 8u : static_cast<unsigned>(w); }
+
+inline constexpr std::size_t kMaxMulLimbs = std::size_t(1) << 24;  // mul.hpp:30
+
+struct AddSubStats;  // accepted for signature compatibility only (see header note)
+
+namespace detail {
+inline void check(int rc) {
+    if (rc == DOTG_OK) return;
+    const std::string msg = dotg_last_error();
+    if (rc == DOTG_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("dotg: " + msg);
+}
+inline void no_stats(const AddSubStats* st) {
+    if (st != nullptr) throw std::logic_error("AddSubStats is not produced by the B200 path");
+}
+inline void validate(Width w) { check(dotg_validate_width(static_cast<int>(w))); }
+
+inline unsigned run_words(bool sub, std::span<limb_t> out, std::span<const limb_t> a,
+                          std::span<const limb_t> b, Width w) {
+    validate(w);
+    if (a.size() != b.size() || out.size() != a.size())  // addsub.cpp:139-140
+        throw std::invalid_argument("dot add/sub: operand lengths differ (caller pads)");
+    std::uint32_t carry = 0;
+    check(sub ? dotg_sub_words_host(out.data(), a.data(), b.data(), a.size(), &carry)
+              : dotg_add_words_host(out.data(), a.data(), b.data(), a.size(), &carry));
+    return carry;
+}
+
+inline WordsResult run_limbs(bool sub, const Limbs& a, const Limbs& b, Width w) {  // addsub.cpp:192-211
+    const std::size_t m = a.size() > b.size() ? a.size() : b.size();
+    Limbs pa = a, pb = b;
+    pa.resize(m, 0);
+    pb.resize(m, 0);
+    WordsResult r;
+    r.limbs.resize(m);
+    r.flag = run_words(sub, r.limbs, pa, pb, w);
+    return r;
+}
+}  // namespace detail
+
+// out = a + b (mod 2^(64m)); returns the carry (addsub.hpp:98-100).
+inline unsigned dot_add_words(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
+                              Width w = Width::w8, AddSubStats* stats = nullptr) {
+    detail::no_stats(stats);
+    return detail::run_words(false, out, a, b, w);
+}
+// out = a - b (mod 2^(64m)); returns the borrow (addsub.hpp:101-103).
+inline unsigned dot_sub_words(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
+                              Width w = Width::w8, AddSubStats* stats = nullptr) {
+    detail::no_stats(stats);
+    return detail::run_words(true, out, a, b, w);
+}
+// Value forms: unequal lengths are zero-padded to the longer one (addsub.hpp:106-109).
+inline WordsResult dot_add_words(const Limbs& a, const Limbs& b, Width w = Width::w8,
+                                 AddSubStats* stats = nullptr) {
+    detail::no_stats(stats);
+    return detail::run_limbs(false, a, b, w);
+}
+inline WordsResult dot_sub_words(const Limbs& a, const Limbs& b, Width w = Width::w8,
+                                 AddSubStats* stats = nullptr) {
+    detail::no_stats(stats);
+    return detail::run_limbs(true, a, b, w);
+}
+
+// Exact product, exactly 2m limbs; equal lengths 1 <= m <= 2^24 (mul.hpp:75-76).
+inline Limbs dot_mul_words(const Limbs& a, const Limbs& b, RadixConfig cfg = kSaturated,
+                           Width w = Width::w8) {
+    if (cfg.limb_bits != 64 && cfg.limb_bits != 52)
+        throw std::invalid_argument("RadixConfig: limb_bits must be 64 or 52");
+    if (cfg.limb_bits != 64) throw std::logic_error("the 52-bit radix is not on the B200 path");
+    detail::validate(w);
+    if (a.size() != b.size()) throw std::invalid_argument("dot mul: operand lengths differ (caller pads)");
+    if (a.empty()) throw std::invalid_argument("dot mul: operands need at least one limb");
+    if (a.size() > kMaxMulLimbs)
+        throw std::invalid_argument("dot mul: limb count exceeds the column accumulator bound");
+    Limbs out(2 * a.size());
+    detail::check(dotg_mul_batch_host(out.data(), a.data(), b.data(), a.size(), 1));
+    return out;
+}
+
+// Batched extensions (no reference equivalent; one call instead of a loop over pairs):
+// row-major host arrays [batch][m]; flags[batch] may be empty.
+inline void dot_add_batch(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
+                          std::span<std::uint32_t> flags, std::size_t m) {
+    if (m == 0 || a.size() % m || a.size() != b.size() || out.size() != a.size())
+        throw std::invalid_argument("dot add batch: shapes differ");
+    detail::check(dotg_add_batch_host(out.data(), a.data(), b.data(), flags.empty() ? nullptr : flags.data(), m,
+                                      a.size() / m));
+}
+inline void dot_sub_batch(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
+                          std::span<std::uint32_t> flags, std::size_t m) {
+    if (m == 0 || a.size() % m || a.size() != b.size() || out.size() != a.size())
+        throw std::invalid_argument("dot sub batch: shapes differ");
+    detail::check(dotg_sub_batch_host(out.data(), a.data(), b.data(), flags.empty() ? nullptr : flags.data(), m,
+                                      a.size() / m));
+}
+inline void dot_mul_batch(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
+                          std::size_t m) {
+    if (m == 0 || a.size() % m || a.size() != b.size() || out.size() != 2 * a.size())
+        throw std::invalid_argument("dot mul batch: shapes differ");
+    detail::check(dotg_mul_batch_host(out.data(), a.data(), b.data(), m, a.size() / m));
+}
+
+}  // namespace dot_b200

@@ -1,0 +1,267 @@
+// test_shim.cpp - C++ drop-in parity test: the reference's own test cases
+// (proj/tests/test_addsub.cpp, test_mul.cpp, test_oracle.cpp), restated against
+// dot_b200:: (include/dot_b200.hpp -> libdotg.so on the B200) with the same seeded
+// std::mt19937_64 draws, checked against the oracle restatement (oracle/dot_oracle.c).
+// Dependency-free: a minimal CHECK runner instead of doctest (absent in this image).
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dot_b200.hpp"
+
+extern "C" {
+#include "../../oracle/dot_oracle.h"
+}
+
+using namespace dot_b200;
+
+namespace {
+int g_checks = 0, g_fail = 0;
+const char* g_case = "";
+#define CHECK(c)                                                                      \
+    do {                                                                              \
+        ++g_checks;                                                                   \
+        if (!(c)) {                                                                   \
+            ++g_fail;                                                                 \
+            std::fprintf(stderr, "FAIL [%s] %s:%d: %s\n", g_case, __FILE__, __LINE__, #c); \
+        }                                                                             \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)          \
+    do {                                  \
+        bool thrown_ = false;             \
+        try {                             \
+            (void)(expr);                 \
+        } catch (const T&) {              \
+            thrown_ = true;               \
+        } catch (...) {                   \
+        }                                 \
+        CHECK(thrown_ && #expr);          \
+    } while (0)
+
+constexpr limb_t kMax = ~limb_t(0);
+
+Limbs uniform_limbs(std::mt19937_64& rng, std::size_t m) {
+    Limbs a(m);
+    for (auto& x : a) x = rng();
+    return a;
+}
+Limbs spiky_limbs(std::mt19937_64& rng, std::size_t m) {  // test_addsub.cpp:28-40
+    Limbs a(m);
+    for (auto& x : a) {
+        switch (rng() & 3u) {
+            case 0: x = kMax; break;
+            case 1: x = 0; break;
+            default: x = rng(); break;
+        }
+    }
+    return a;
+}
+WordsResult oracle_add(const Limbs& a, const Limbs& b) {
+    WordsResult r;
+    r.limbs.resize(a.size());
+    r.flag = dotor_add(r.limbs.data(), a.data(), b.data(), a.size());
+    return r;
+}
+WordsResult oracle_sub(const Limbs& a, const Limbs& b) {
+    WordsResult r;
+    r.limbs.resize(a.size());
+    r.flag = dotor_sub(r.limbs.data(), a.data(), b.data(), a.size());
+    return r;
+}
+Limbs oracle_mul_padded(const Limbs& a, const Limbs& b) {
+    Limbs r(a.size() + b.size(), 0);
+    dotor_mul(r.data(), a.data(), a.size(), b.data(), b.size());
+    return r;
+}
+bool eq(const Limbs& a, const Limbs& b) {
+    return dotor_compare(a.data(), a.size(), b.data(), b.size()) == 0;
+}
+
+void run(const char* name, const std::function<void()>& f) {
+    g_case = name;
+    try {
+        f();
+    } catch (const std::exception& e) {
+        ++g_fail;
+        std::fprintf(stderr, "FAIL [%s] unexpected exception: %s\n", name, e.what());
+    }
+}
+}  // namespace
+
+int main() {
+    run("2^512 - 1 plus 1 rolls over into the flag", [] {  // test_addsub.cpp:124-130
+        const WordsResult r = dot_add_words(Limbs(8, kMax), Limbs{1});
+        CHECK(r.limbs == Limbs(8, 0));
+        CHECK(r.flag == 1);
+    });
+    run("adding zero is the identity", [] {
+        std::mt19937_64 rng(7);
+        const Limbs a = uniform_limbs(rng, 12);
+        const WordsResult r = dot_add_words(a, Limbs{});
+        CHECK(r.limbs == a);
+        CHECK(r.flag == 0);
+    });
+    run("carry crosses the chunk boundary into a masked tail", [] {
+        Limbs a(9, kMax), b(9, 0);
+        b[0] = 1;
+        const WordsResult r = dot_add_words(a, b, Width::w8);
+        CHECK(r.limbs == Limbs(9, 0));
+        CHECK(r.flag == 1);
+    });
+    run("subtracting below zero wraps and reports the borrow", [] {
+        const WordsResult r = dot_sub_words(Limbs{0}, Limbs{1});
+        CHECK(r.limbs == Limbs{kMax});
+        CHECK(r.flag == 1);
+    });
+    run("words match the oracle across sizes and widths", [] {  // test_addsub.cpp:161-180
+        std::mt19937_64 rng(0x51edbeefu);
+        const std::size_t sizes[] = {1, 2, 3, 5, 7, 8, 9, 13, 16, 17, 31, 32, 33, 64};
+        for (const std::size_t m : sizes) {
+            for (int iter = 0; iter < 25; ++iter) {
+                const Limbs a = spiky_limbs(rng, m), b = spiky_limbs(rng, m);
+                const WordsResult aw = oracle_add(a, b), sw = oracle_sub(a, b);
+                for (const Width w : {Width::scalar, Width::w2, Width::w4, Width::w8}) {
+                    const WordsResult ag = dot_add_words(a, b, w);
+                    CHECK(ag.limbs == aw.limbs && ag.flag == aw.flag);
+                    const WordsResult sg = dot_sub_words(a, b, w);
+                    CHECK(sg.limbs == sw.limbs && sg.flag == sw.flag);
+                }
+            }
+        }
+    });
+    run("add then sub round-trips, flag acting as the extra limb", [] {  // 182-199
+        std::mt19937_64 rng(0xabad1deau);
+        for (int iter = 0; iter < 60; ++iter) {
+            const std::size_t m = 1 + rng() % 40;
+            const Limbs a = spiky_limbs(rng, m), b = spiky_limbs(rng, m);
+            WordsResult sum = dot_add_words(a, b);
+            Limbs wide = sum.limbs;
+            wide.push_back(sum.flag);
+            Limbs wide_b = b;
+            wide_b.resize(wide.size(), 0);
+            const WordsResult back = dot_sub_words(wide, wide_b);
+            CHECK(back.flag == 0);
+            CHECK(eq(back.limbs, a));
+        }
+    });
+    run("unequal lengths are padded like the oracle with an equal pad", [] {  // 201-217
+        std::mt19937_64 rng(0x00c0ffeeu);
+        for (int iter = 0; iter < 60; ++iter) {
+            const std::size_t ma = 1 + rng() % 20, mb = 1 + rng() % 20;
+            const Limbs a = spiky_limbs(rng, ma), b = spiky_limbs(rng, mb);
+            Limbs pa = a, pb = b;
+            const std::size_t m = ma > mb ? ma : mb;
+            pa.resize(m, 0);
+            pb.resize(m, 0);
+            const WordsResult want = oracle_add(pa, pb);
+            const WordsResult got = dot_add_words(a, b);
+            CHECK(got.limbs == want.limbs && got.flag == want.flag);
+        }
+    });
+    run("span form length mismatch throws", [] {  // 219-223
+        Limbs a(4, 1), b(5, 1), out(5, 0);
+        CHECK_THROWS_AS(dot_add_words(std::span<limb_t>(out), a, b), std::invalid_argument);
+        CHECK_THROWS_AS(dot_sub_words(std::span<limb_t>(out), a, b), std::invalid_argument);
+    });
+    run("output may alias either input exactly", [] {  // 250-276
+        std::mt19937_64 rng(0x0dd5eedu);
+        for (int iter = 0; iter < 40; ++iter) {
+            const std::size_t m = 1 + rng() % 24;
+            const Limbs a = spiky_limbs(rng, m), b = spiky_limbs(rng, m);
+            const WordsResult want = oracle_add(a, b);
+            Limbs acc = a;
+            const unsigned c1 = dot_add_words(std::span<limb_t>(acc), acc, b);
+            CHECK(acc == want.limbs && c1 == want.flag);
+            Limbs acc2 = b;
+            const unsigned c2 = dot_add_words(std::span<limb_t>(acc2), a, acc2);
+            CHECK(acc2 == want.limbs && c2 == want.flag);
+            const WordsResult dwant = oracle_sub(a, b);
+            Limbs acc3 = a;
+            const unsigned c3 = dot_sub_words(std::span<limb_t>(acc3), acc3, b);
+            CHECK(acc3 == dwant.limbs && c3 == dwant.flag);
+        }
+    });
+    run("full propagation chains", [] {  // 299-317
+        const std::size_t m = 64;
+        Limbs a(m, kMax), b(m, 0);
+        b[0] = 1;
+        const WordsResult r = dot_add_words(a, b);
+        CHECK(r.limbs == Limbs(m, 0) && r.flag == 1);
+        const WordsResult d = dot_sub_words(Limbs(m, 0), Limbs{1});
+        CHECK(d.limbs == Limbs(m, kMax) && d.flag == 1);
+    });
+    run("one-limb product is exactly the two-limb scalar product", [] {  // test_mul.cpp:323-331
+        std::mt19937_64 rng(21);
+        for (int iter = 0; iter < 50; ++iter) {
+            const limb_t x = rng(), y = rng();
+            const unsigned __int128 p = (unsigned __int128)x * y;
+            CHECK(dot_mul_words(Limbs{x}, Limbs{y}) == (Limbs{limb_t(p), limb_t(p >> 64)}));
+        }
+    });
+    run("generic product matches the oracle across sizes", [] {  // test_mul.cpp:345-359
+        std::mt19937_64 rng(23);
+        const std::size_t sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 33, 48, 64};
+        for (const std::size_t m : sizes) {
+            for (int iter = 0; iter < 12; ++iter) {
+                const Limbs a = uniform_limbs(rng, m), b = uniform_limbs(rng, m);
+                const Limbs got = dot_mul_words(a, b);
+                CHECK(got.size() == 2 * m);
+                CHECK(got == oracle_mul_padded(a, b));
+            }
+        }
+    });
+    run("generic product commutes and respects identity and zero", [] {  // 377-389
+        std::mt19937_64 rng(25);
+        for (int iter = 0; iter < 30; ++iter) {
+            const std::size_t m = 1 + rng() % 16;
+            const Limbs a = uniform_limbs(rng, m), b = uniform_limbs(rng, m);
+            CHECK(dot_mul_words(a, b) == dot_mul_words(b, a));
+            Limbs one(m, 0);
+            one[0] = 1;
+            CHECK(eq(dot_mul_words(a, one), a));
+            const Limbs z = dot_mul_words(a, Limbs(m, 0));
+            CHECK(eq(z, Limbs{}));
+        }
+    });
+    run("product distributes over addition", [] {  // 391-411
+        std::mt19937_64 rng(26);
+        for (int iter = 0; iter < 30; ++iter) {
+            const std::size_t m = 1 + rng() % 12;
+            const Limbs a = uniform_limbs(rng, m), b = uniform_limbs(rng, m), c = uniform_limbs(rng, m);
+            WordsResult s = dot_add_words(b, c);
+            Limbs sum = s.limbs;
+            sum.push_back(s.flag);
+            Limbs a_pad = a;
+            a_pad.resize(sum.size(), 0);
+            const Limbs lhs = dot_mul_words(a_pad, sum);
+            WordsResult r = dot_add_words(dot_mul_words(a, b), dot_mul_words(a, c));
+            Limbs rhs = r.limbs;
+            rhs.push_back(r.flag);
+            CHECK(eq(lhs, rhs));
+        }
+    });
+    run("mul argument validation", [] {  // test_mul.cpp:97-101
+        CHECK_THROWS_AS(dot_mul_words(Limbs{1, 2}, Limbs{1}), std::invalid_argument);
+        CHECK_THROWS_AS(dot_mul_words(Limbs{}, Limbs{}), std::invalid_argument);
+        CHECK_THROWS_AS(dot_mul_words(Limbs{1}, Limbs{1}, RadixConfig{40}), std::invalid_argument);
+    });
+    run("batched extension matches the span form", [] {
+        std::mt19937_64 rng(99);
+        const std::size_t m = 64, B = 3000;
+        Limbs a(m * B), b(m * B), out(m * B);
+        for (auto& x : a) x = rng();
+        for (auto& x : b) x = rng();
+        std::vector<std::uint32_t> fl(B);
+        dot_sub_batch(out, a, b, fl, m);
+        for (std::size_t p = 0; p < B; p += 97) {
+            Limbs pa(a.begin() + p * m, a.begin() + (p + 1) * m), pb(b.begin() + p * m, b.begin() + (p + 1) * m);
+            const WordsResult w = oracle_sub(pa, pb);
+            CHECK(Limbs(out.begin() + p * m, out.begin() + (p + 1) * m) == w.limbs && fl[p] == w.flag);
+        }
+    });
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
