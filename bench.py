@@ -271,6 +271,17 @@ class Launcher:
                 ctypes.c_void_p(flags.data_ptr()), m, B, 0, self.stream)
         return lambda: fn(*args)
 
+    def grouped(self, problems):
+        """problems: list of (sub, out, a, b, flags, m, B) -> one dotg_addsub_grouped call."""
+        from paper_2604_21566_b200._lib import AddSubProblem
+
+        arr = (AddSubProblem * len(problems))()
+        for i, (sub, out, a, b, flags, m, B) in enumerate(problems):
+            arr[i] = AddSubProblem(int(sub), 0, out.data_ptr(), a.data_ptr(), b.data_ptr(), flags.data_ptr(), m, B)
+        fn, n, st = self.lib.dotg_addsub_grouped, len(problems), self.stream
+        self._keep = arr
+        return lambda: fn(arr, n, st)
+
     def mul(self, out, a, b, m, B):
         fn = self.lib.dotg_mul_batch
         args = (ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()), m, B,
@@ -342,11 +353,17 @@ def run_ours(args, rank, world, dist):
         bufs.append(dict(m=m, B=B, a=a, b=b, sa=sa, sb=sb, oa=torch.empty_like(a), os=torch.empty_like(a),
                          fa=torch.empty(B, dtype=torch.int32, device="cuda"),
                          fs=torch.empty(B, dtype=torch.int32, device="cuda")))
-    calls = [L.addsub(False, x["oa"], x["a"], x["b"], x["fa"], x["m"], x["B"]) for x in bufs]
-    calls += [L.addsub(True, x["os"], x["sa"], x["sb"], x["fs"], x["m"], x["B"]) for x in bufs]
-    calls_meta = list(range(len(calls)))
+    probs = [(False, x["oa"], x["a"], x["b"], x["fa"], x["m"], x["B"]) for x in bufs]
+    probs += [(True, x["os"], x["sa"], x["sb"], x["fs"], x["m"], x["B"]) for x in bufs]
     call_bytes = [x["B"] * (24 * x["m"] + 4) for x in bufs] * 2
     step_bytes = sum(call_bytes)
+    # per-problem launches (event-bracketed breakdown, and --ungrouped timing)
+    single_calls = [L.addsub(*q) for q in probs]
+    if args.ungrouped:
+        calls = single_calls
+    else:
+        calls = [L.grouped(probs)]  # the whole sweep = one persistent launch
+    calls_meta = list(range(len(calls)))
     assert step_bytes == c2_bytes()
     working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per step (a, b, sa, sb)
 
@@ -363,8 +380,9 @@ def run_ours(args, rank, world, dist):
     # average launch duration of the batched add/sub kernel = lean-loop step time / launches
     # (inter-launch gaps included: conservative); per_size uses event-bracketed launches.
     achieved = step_bytes / (ms_step * 1e-3) / 1e9
-    per_size = {f"m{x['m']}": {"add_gbs": call_bytes[i] / (per_call[i] * 1e-3) / 1e9,
-                               "sub_gbs": call_bytes[i] / (per_call[i + 4] * 1e-3) / 1e9}
+    _, per_single = timed_steps(torch, None, 1, stream, single_calls, max(3, args.steps // 4), 2)
+    per_size = {f"m{x['m']}": {"add_gbs": call_bytes[i] / (per_single[i] * 1e-3) / 1e9,
+                               "sub_gbs": call_bytes[i] / (per_single[i + 4] * 1e-3) / 1e9}
                 for i, x in enumerate(bufs)}
     traffic = traffic_table().get("C2_per_launch_bytes")
 
@@ -428,7 +446,7 @@ def run_ours(args, rank, world, dist):
             cpu_baseline = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
 
     # free the headline buffers before the secondary configs
-    del bufs, calls
+    del bufs, calls, single_calls
     torch.cuda.empty_cache()
 
     secondary = {}
@@ -443,13 +461,14 @@ def run_ours(args, rank, world, dist):
                 "uniform, 1% forced full carry chains, sub swapped to a>=b)",
         "config": {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
                    "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
-                   "step": "8 launches: add at 4 sizes then sub at 4 sizes",
+                   "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if args.ungrouped else
+                            "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"),
                    "l2": f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct "
                          "inputs (126 MB L2), every buffer touched once per step",
                    "per_rank": "full sweep on every rank (weak scaling, no collective)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_addsub_team (batched add/sub, warp-ballot lookahead)",
+                     "kernel": "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
                      "algorithmic_bytes_per_launch": step_bytes / len(calls_meta),
                      "launch_us_avg": ms_step * 1e3 / len(calls_meta), "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                      "per_size": per_size},
@@ -547,6 +566,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

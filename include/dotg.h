@@ -70,6 +70,25 @@ int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t
                    size_t m, size_t batch, int layout, dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * Grouped batched add/sub: up to any number of INDEPENDENT problems (sizes may differ)
+ * in as few launches as possible - one persistent launch for every row-major,
+ * power-of-two m <= 256 problem (up to 32 per launch). No problem's out may overlap
+ * another problem's operands or output. Replaces a loop of span calls over pairs of
+ * several sizes (e.g. the reference corpus sweep, testgen.cpp:61-66 sizes).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int op;          /* 0 add, 1 sub */
+    int layout;      /* dotg_layout */
+    uint64_t* out;
+    const uint64_t* a;
+    const uint64_t* b;
+    uint32_t* flags; /* may be NULL */
+    size_t m;
+    size_t batch;
+} dotg_addsub_problem;
+int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Batched column multiplication.
  * Replaces: dot_mul_words(a, b, kSaturated, w) per pair (mul.hpp:75-76, mul.cpp:96-103).
  * out[p] = a[p] * b[p], exactly 2m limbs (high limbs may be 0). Requires

@@ -23,6 +23,7 @@ from .api import (  # noqa: F401
     add_words,
     addsub_batch,
     addsub_batch_host,
+    addsub_grouped,
     dot_add_words,
     dot_mul_words,
     dot_sub_words,
@@ -48,6 +49,7 @@ __all__ = [
     "add_words",
     "addsub_batch",
     "addsub_batch_host",
+    "addsub_grouped",
     "dot_add_words",
     "dot_mul_words",
     "dot_sub_words",

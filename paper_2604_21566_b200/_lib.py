@@ -26,6 +26,7 @@ SIGNATURES = {
     "dotg_device_sms": (c_int, []),
     "dotg_add_batch": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, c_int, _P]),
     "dotg_sub_batch": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_addsub_grouped": (c_int, [_P, c_int, _P]),
     "dotg_mul_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
     "dotg_add_words": (c_int, [_P, _P, _P, c_size_t, _P, _P]),
     "dotg_sub_words": (c_int, [_P, _P, _P, c_size_t, _P, _P]),
@@ -40,6 +41,13 @@ SIGNATURES = {
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_kernel_launches": (c_uint64, []),
 }
+
+
+class AddSubProblem(ctypes.Structure):
+    """dotg_addsub_problem (include/dotg.h)."""
+
+    _fields_ = [("op", c_int), ("layout", c_int), ("out", c_void_p), ("a", c_void_p), ("b", c_void_p),
+                ("flags", c_void_p), ("m", c_size_t), ("batch", c_size_t)]
 
 
 class DotgError(RuntimeError):

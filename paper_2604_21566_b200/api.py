@@ -250,6 +250,32 @@ def sub_batch(a, b, out=None, flags=None, *, layout=ROW_MAJOR, stream=None):
     return addsub_batch(True, a, b, out, flags, layout=layout, stream=stream)
 
 
+def addsub_grouped(problems, *, stream=None):
+    """Several independent batched add/sub problems in one call (one persistent launch
+    for the row-major power-of-two sizes). problems: iterable of dicts with keys
+    op ('add'|'sub'), a, b, out, flags (optional), layout (optional)."""
+    plist = list(problems)
+    arr = (_lib.AddSubProblem * max(1, len(plist)))()
+    keep = []
+    for i, q in enumerate(plist):
+        lay = _layout(q.get("layout", ROW_MAJOR))
+        a, b, out = q["a"], q["b"], q["out"]
+        for t, nm in ((a, "a"), (b, "b"), (out, "out")):
+            _check_dev(t, nm)
+        if a.shape != b.shape or out.shape != a.shape:
+            raise InvalidArgument("dot add/sub: operand shapes differ")
+        batch, m = _batch_dims(a, lay)
+        fl = q.get("flags")
+        if fl is not None:
+            _check_dev(fl, "flags", 4)
+        op = {"add": 0, "sub": 1, 0: 0, 1: 1}[q["op"]]
+        arr[i] = _lib.AddSubProblem(op, lay, out.data_ptr(), a.data_ptr(), b.data_ptr(),
+                                    None if fl is None else fl.data_ptr(), m, batch)
+        keep.append(q)
+    check(lib().dotg_addsub_grouped(arr, len(plist), _stream_handle(stream)))
+    return plist
+
+
 def mul_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
     """out = a * b per pair, exactly 2m limbs. ROW_MAJOR out: [batch, 2m];
     INTERLEAVED out: [2m, batch]."""

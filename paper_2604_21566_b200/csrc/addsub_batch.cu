@@ -16,9 +16,17 @@
 //
 // Row-major layout [batch][m] (the reference's Limbs back to back): a team of T lanes
 // owns one number; lane t of the team holds R vectors of V limbs at limb offsets
-// r*V*T + t*V, so each vector load of a warp covers 32/T whole numbers contiguously
-// (coalesced 256-bit LDG/STG). Interleaved layout [m][batch] and non-power-of-two m use
-// a thread-per-pair strided kernel with the same carry semantics.
+// r*V*T + t*V, so each 256-bit vector load of a warp covers 32/T whole numbers
+// contiguously. Every warp task is 256 limbs per operand whatever m is, so tasks of
+// different sizes cost the same.
+//
+// Launch shape: ONE persistent kernel per call, grid = SMs x resident CTAs, warps
+// striding over the concatenated task lists of up to kMaxGroup independent problems
+// (dotg_addsub_grouped). A whole multi-size sweep is one launch: no inter-kernel gaps,
+// no wave-quantisation tail per size.
+//
+// Interleaved layout [m][batch] and non-power-of-two m use a thread-per-pair strided
+// kernel with the same carry semantics.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,27 +46,35 @@ struct TeamCfg {
     static_assert(M % V == 0 && SL % T == 0, "M must be a power of two multiple of V");
 };
 
+// (V, U) per power-of-two m: 256 limbs per operand per warp task for every m >= 4.
+__host__ __device__ constexpr int team_v(uint32_t m) { return m >= 4 ? 4 : int(m); }
+__host__ __device__ constexpr int team_u(uint32_t m) { return m >= 256 ? 1 : 2; }
+__host__ __device__ constexpr uint64_t numbers_per_task(uint32_t m) {
+    // NPW * U with T = min(m / V, 32)
+    return uint64_t(32 / ((m / team_v(m)) < 32 ? (m / team_v(m)) : 32)) * uint64_t(team_u(m));
+}
+
 template <bool SUB, int M, int V, int U>
-__global__ void __launch_bounds__(256) k_addsub_team(uint64_t* out, const uint64_t* a,
-                                                     const uint64_t* b, uint32_t* flags,
-                                                     size_t batch) {
+__device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task) {
     using C = TeamCfg<M, V>;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned team = lane / C::T;
     const unsigned t = lane % C::T;
-    const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const size_t base_num = warp * size_t(C::NPW * U);
+    const uint64_t base_num = task * uint64_t(C::NPW * U);
+    const uint64_t batch = P.batch;
+    const uint64_t* __restrict__ a = P.a;
+    const uint64_t* __restrict__ b = P.b;
 
     uint64_t s[U][C::R][V];
     uint64_t bv[U][C::R][V];
-    // Issue every load of the warp's U row-groups before any arithmetic (MLP).
+    // Issue every load of the task before any arithmetic (MLP).
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const size_t num = base_num + size_t(u * C::NPW) + team;
+        const uint64_t num = base_num + uint64_t(u * C::NPW) + team;
         const bool ok = num < batch;
 #pragma unroll
         for (int r = 0; r < C::R; ++r) {
-            const size_t off = num * M + size_t(r * V * C::T + t * V);
+            const uint64_t off = num * M + uint64_t(r * V * C::T + t * V);
             if (ok) {
                 ld_stream<V>(a + off, s[u][r]);
                 ld_stream<V>(b + off, bv[u][r]);
@@ -71,7 +87,7 @@ __global__ void __launch_bounds__(256) k_addsub_team(uint64_t* out, const uint64
 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const size_t num = base_num + size_t(u * C::NPW) + team;
+        const uint64_t num = base_num + uint64_t(u * C::NPW) + team;
         const bool ok = num < batch;
         uint32_t g[C::R][V], p[C::R][V];
         uint64_t Gm[C::W], Pm[C::W];
@@ -82,10 +98,10 @@ __global__ void __launch_bounds__(256) k_addsub_team(uint64_t* out, const uint64
             // Phase 1 + 2.
 #pragma unroll
             for (int k = 0; k < V; ++k) s[u][r][k] = lane_op<SUB>(s[u][r][k], bv[u][r][k], g[r][k], p[r][k]);
-            uint32_t G, P;
-            fold_gp<V>(g[r], p[r], G, P);
+            uint32_t G, P2;
+            fold_gp<V>(g[r], p[r], G, P2);
             const uint32_t gw = __ballot_sync(0xffffffffu, G);
-            const uint32_t pw = __ballot_sync(0xffffffffu, P);
+            const uint32_t pw = __ballot_sync(0xffffffffu, P2);
             if constexpr (C::T == 32) {
                 Gm[r / 2] |= uint64_t(gw) << (32 * (r % 2));
                 Pm[r / 2] |= uint64_t(pw) << (32 * (r % 2));
@@ -113,9 +129,46 @@ __global__ void __launch_bounds__(256) k_addsub_team(uint64_t* out, const uint64
             const unsigned j = unsigned(r * C::T) + t;
             const uint32_t c = uint32_t(Cm[j / 64] >> (j % 64)) & 1u;
             apply_superlane<SUB, V>(s[u][r], g[r], p[r], c);
-            if (ok) st_stream<V>(out + num * M + size_t(r * V * C::T + t * V), s[u][r]);
+            if (ok) st_stream<V>(P.out + num * M + uint64_t(r * V * C::T + t * V), s[u][r]);
         }
-        if (flags != nullptr && ok && t == 0) flags[num] = flag;
+        if (P.flags != nullptr && ok && t == 0) P.flags[num] = flag;
+    }
+}
+
+template <bool SUB>
+__device__ __forceinline__ void dispatch_small(const AddSubProblem& P, uint64_t task) {
+    switch (P.m) {
+        case 1: team_task<SUB, 1, 1, 2>(P, task); break;
+        case 2: team_task<SUB, 2, 2, 2>(P, task); break;
+        case 4: team_task<SUB, 4, 4, 2>(P, task); break;
+        case 8: team_task<SUB, 8, 4, 2>(P, task); break;
+        case 16: team_task<SUB, 16, 4, 2>(P, task); break;
+        case 32: team_task<SUB, 32, 4, 2>(P, task); break;
+        case 64: team_task<SUB, 64, 4, 2>(P, task); break;
+        case 128: team_task<SUB, 128, 4, 2>(P, task); break;
+        case 256: team_task<SUB, 256, 4, 1>(P, task); break;
+        default: break;
+    }
+}
+
+// BIG = false: m in {1, ..., 256}; BIG = true: m == 512 (kept apart so its register
+// footprint does not cap the occupancy of the common sizes).
+template <bool BIG>
+__global__ void __launch_bounds__(256) k_addsub_grouped(const __grid_constant__ AddSubGroup grp) {
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    int pi = 0;
+    for (uint64_t t = warp; t < grp.total_tasks; t += nw) {
+        while (pi + 1 < grp.n && grp.p[pi + 1].task_begin <= t) ++pi;
+        const AddSubProblem& P = grp.p[pi];
+        const uint64_t task = t - P.task_begin;
+        if constexpr (BIG) {
+            if (P.sub) team_task<true, 512, 4, 1>(P, task);
+            else team_task<false, 512, 4, 1>(P, task);
+        } else {
+            if (P.sub) dispatch_small<true>(P, task);
+            else dispatch_small<false>(P, task);
+        }
     }
 }
 
@@ -164,18 +217,6 @@ __global__ void __launch_bounds__(256) k_addsub_strided(uint64_t* out, const uin
 
 namespace {
 
-template <bool SUB, int M, int V, int U>
-cudaError_t run_team(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
-                     size_t batch, cudaStream_t st) {
-    using C = TeamCfg<M, V>;
-    const size_t per_warp = size_t(C::NPW) * U;
-    const size_t warps = (batch + per_warp - 1) / per_warp;
-    const size_t blocks = (warps * 32 + 255) / 256;
-    k_addsub_team<SUB, M, V, U><<<unsigned(blocks), 256, 0, st>>>(out, a, b, flags, batch);
-    count_launch();
-    return cudaGetLastError();
-}
-
 template <bool SUB>
 cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
                         size_t m, size_t batch, size_t sp, size_t si, cudaStream_t st) {
@@ -186,60 +227,103 @@ cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
 }
 
 bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+bool pow2(size_t m) { return m != 0 && (m & (m - 1)) == 0; }
 
-template <bool SUB>
-cudaError_t dispatch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
-                     size_t batch, int layout, cudaStream_t st) {
-    if (layout == 1) return run_strided<SUB>(out, a, b, flags, m, batch, 1, batch, st);
-    const bool a32 = aligned(out, 32) && aligned(a, 32) && aligned(b, 32);
-    const bool a16 = aligned(out, 16) && aligned(a, 16) && aligned(b, 16);
-    switch (m) {
-        case 1: return run_team<SUB, 1, 1, 2>(out, a, b, flags, batch, st);
-        case 2:
-            if (a16) return run_team<SUB, 2, 2, 2>(out, a, b, flags, batch, st);
-            break;
-        case 4:
-            if (a32) return run_team<SUB, 4, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 8:
-            if (a32) return run_team<SUB, 8, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 16:
-            if (a32) return run_team<SUB, 16, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 32:
-            if (a32) return run_team<SUB, 32, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 64:
-            if (a32) return run_team<SUB, 64, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 128:
-            if (a32) return run_team<SUB, 128, 4, 2>(out, a, b, flags, batch, st);
-            break;
-        case 256:
-            if (a32) return run_team<SUB, 256, 4, 1>(out, a, b, flags, batch, st);
-            break;
-        case 512:
-            if (a32) return run_team<SUB, 512, 4, 1>(out, a, b, flags, batch, st);
-            break;
-        default:
-            break;
+// 0: team-small kernel, 1: team-big (m = 512), 2: strided kernel
+int route(const AddSubProblem& P, int layout) {
+    if (layout == 1 || !pow2(P.m) || P.m > 512) return 2;
+    const size_t need = P.m >= 4 ? 32 : P.m * 8;
+    if (!aligned(P.out, need) || !aligned(P.a, need) || !aligned(P.b, need)) return 2;
+    return P.m == 512 ? 1 : 0;
+}
+
+struct DevInfo {
+    int dev = -1, sms = 148, blocks_small = 8, blocks_big = 4;
+};
+
+const DevInfo& dev_info() {
+    static thread_local DevInfo info;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (info.dev != dev) {
+        info.dev = dev;
+        cudaDeviceGetAttribute(&info.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.blocks_small, k_addsub_grouped<false>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&info.blocks_big, k_addsub_grouped<true>, 256, 0);
+        if (info.blocks_small < 1) info.blocks_small = 1;
+        if (info.blocks_big < 1) info.blocks_big = 1;
     }
-    return run_strided<SUB>(out, a, b, flags, m, batch, m, 1, st);
+    return info;
+}
+
+cudaError_t launch_group(bool big, AddSubGroup& g, cudaStream_t st) {
+    if (g.n == 0 || g.total_tasks == 0) return cudaSuccess;
+    const DevInfo& di = dev_info();
+    const uint64_t need_blocks = (g.total_tasks + 7) / 8;  // 8 warps per CTA
+    const uint64_t cap = uint64_t(di.sms) * uint64_t(big ? di.blocks_big : di.blocks_small);
+    const unsigned blocks = unsigned(need_blocks < cap ? need_blocks : cap);
+    if (big) k_addsub_grouped<true><<<blocks, 256, 0, st>>>(g);
+    else k_addsub_grouped<false><<<blocks, 256, 0, st>>>(g);
+    count_launch();
+    return cudaGetLastError();
 }
 
 }  // namespace
 
+cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, int n, cudaStream_t stream) {
+    AddSubGroup small{}, big{};
+    for (int i = 0; i < n; ++i) {
+        AddSubProblem P = probs[i];
+        if (P.batch == 0) continue;
+        if (P.m == 0) {
+            if (P.flags != nullptr) {
+                cudaError_t e = cudaMemsetAsync(P.flags, 0, P.batch * sizeof(uint32_t), stream);
+                if (e != cudaSuccess) return e;
+            }
+            continue;
+        }
+        const int r = route(P, layouts[i]);
+        if (r == 2) {
+            const bool inter = layouts[i] == 1;
+            cudaError_t e = P.sub ? run_strided<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, inter ? 1 : P.m,
+                                                      inter ? P.batch : 1, stream)
+                                  : run_strided<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, inter ? 1 : P.m,
+                                                       inter ? P.batch : 1, stream);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        AddSubGroup& g = r == 1 ? big : small;
+        if (g.n == kMaxGroup) {
+            cudaError_t e = launch_group(r == 1, g, stream);
+            if (e != cudaSuccess) return e;
+            g = AddSubGroup{};
+        }
+        P.task_begin = g.total_tasks;
+        g.total_tasks += (P.batch + numbers_per_task(P.m) - 1) / numbers_per_task(P.m);
+        g.p[g.n++] = P;
+    }
+    cudaError_t e = launch_group(false, small, stream);
+    if (e != cudaSuccess) return e;
+    return launch_group(true, big, stream);
+}
+
 cudaError_t launch_addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
                                 uint32_t* flags, size_t m, size_t batch, int layout,
                                 cudaStream_t stream) {
-    if (batch == 0) return cudaSuccess;
-    if (m == 0) {
-        if (flags == nullptr) return cudaSuccess;
-        return cudaMemsetAsync(flags, 0, batch * sizeof(uint32_t), stream);
+    AddSubProblem P{};
+    P.out = out;
+    P.a = a;
+    P.b = b;
+    P.flags = flags;
+    P.batch = batch;
+    P.m = uint32_t(m);
+    P.sub = sub ? 1u : 0u;
+    if (m > 0xffffffffull) {
+        // absurdly long rows: only the strided kernel takes a 64-bit m
+        return sub ? run_strided<true>(out, a, b, flags, m, batch, layout == 1 ? 1 : m, layout == 1 ? batch : 1, stream)
+                   : run_strided<false>(out, a, b, flags, m, batch, layout == 1 ? 1 : m, layout == 1 ? batch : 1, stream);
     }
-    return sub ? dispatch<true>(out, a, b, flags, m, batch, layout, stream)
-               : dispatch<false>(out, a, b, flags, m, batch, layout, stream);
+    return launch_addsub_group(&P, &layout, 1, stream);
 }
 
 }  // namespace dotg

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/dotg.h"
 #include "internal.h"
@@ -39,15 +40,18 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 // The device path is sm_100a-only; refuse anything else loudly (no CPU fallback).
 int check_device() {
+    static thread_local int ok_dev = -1;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "no CUDA device");
+    if (dev == ok_dev) return DOTG_OK;
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
     if (major != 10 || minor != 0)
         return fail(DOTG_ECUDA, "dotg kernels are built for sm_100a; device is sm_" + std::to_string(major) +
                                     std::to_string(minor));
+    ok_dev = dev;
     return DOTG_OK;
 }
 
@@ -314,6 +318,45 @@ int dotg_add_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t
 int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m, size_t batch,
                    int layout, dotg_stream_t stream) {
     return addsub_batch(true, out, a, b, flags, m, batch, layout, stream);
+}
+
+int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_t stream) {
+    if (n < 0 || (n > 0 && problems == nullptr)) return fail(DOTG_EINVAL, "grouped: bad problem list");
+    if (n == 0) return DOTG_OK;
+    std::vector<dotg::AddSubProblem> ps;
+    std::vector<int> layouts;
+    ps.reserve(size_t(n));
+    for (int i = 0; i < n; ++i) {
+        const dotg_addsub_problem& q = problems[i];
+        if (q.op != 0 && q.op != 1) return fail(DOTG_EINVAL, "grouped: op must be 0 (add) or 1 (sub)");
+        int rc = check_addsub(q.out, q.a, q.b, q.flags, q.m, q.batch, q.layout);
+        if (rc != DOTG_OK) return rc;
+        if (q.m > 0xffffffffull) return fail(DOTG_EINVAL, "grouped: m must fit 32 bits (use dotg_add_batch)");
+        const size_t bytes = q.m * q.batch * 8;
+        for (int j = 0; j < i && bytes; ++j) {
+            const dotg_addsub_problem& o = problems[j];
+            const size_t ob = o.m * o.batch * 8;
+            if (!ob) continue;
+            if (ranges_overlap(q.out, bytes, o.out, ob) || ranges_overlap(q.out, bytes, o.a, ob) ||
+                ranges_overlap(q.out, bytes, o.b, ob) || ranges_overlap(o.out, ob, q.a, bytes) ||
+                ranges_overlap(o.out, ob, q.b, bytes))
+                return fail(DOTG_EINVAL, "grouped: problems must be independent (an output overlaps another problem)");
+        }
+        dotg::AddSubProblem P{};
+        P.out = q.out;
+        P.a = q.a;
+        P.b = q.b;
+        P.flags = q.flags;
+        P.batch = q.batch;
+        P.m = uint32_t(q.m);
+        P.sub = uint32_t(q.op);
+        ps.push_back(P);
+        layouts.push_back(q.layout);
+    }
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_addsub_group(ps.data(), layouts.data(), n, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg grouped launch");
 }
 
 int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,

@@ -14,6 +14,27 @@ namespace dotg {
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// One independent batched add/sub problem as the grouped kernel sees it.
+struct AddSubProblem {
+    uint64_t* out;
+    const uint64_t* a;
+    const uint64_t* b;
+    uint32_t* flags;
+    uint64_t batch;
+    uint64_t task_begin;  // first warp task of this problem in the group's task space
+    uint32_t m;
+    uint32_t sub;
+};
+constexpr int kMaxGroup = 32;
+struct AddSubGroup {  // passed by value as a __grid_constant__ kernel parameter
+    uint64_t total_tasks;
+    int n;
+    AddSubProblem p[kMaxGroup];
+};
+
+// Grouped batched add/sub: every problem independent; layouts[i] per problem.
+cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, int n, cudaStream_t stream);
+
 // Batched add/sub. layout 0 = row-major [batch][m], 1 = interleaved [m][batch].
 cudaError_t launch_addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
                                 uint32_t* flags, size_t m, size_t batch, int layout,

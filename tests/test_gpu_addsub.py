@@ -151,3 +151,33 @@ def test_device_fill_matches_host_twin(cuda, oracle):
 
     for n, seed, off in ((1, 1, 0), (1000, 0xC5, 12345), (1 << 20, 0xC1, 1 << 40)):
         assert np.array_equal(host(W.fill(n, seed, off)), oracle.fill(n, seed, off))
+
+
+def test_grouped_matches_oracle(cuda, oracle):
+    """Several sizes, both ops, mixed layouts and one non-power-of-two problem in one call."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(31)
+    specs = [("add", 4, 3000), ("sub", 16, 1001), ("add", 64, 257), ("sub", 256, 33), ("add", 512, 9),
+             ("sub", 7, 100), ("add", 1, 5000), ("sub", 2, 77), ("add", 128, 64), ("sub", 32, 999)]
+    probs, wants = [], []
+    for i, (op, m, B) in enumerate(specs):
+        a, b = category(rng, CATEGORIES[i % len(CATEGORIES)], op, (B, m))
+        wants.append(oracle.addsub_batch(op == "sub", a, b))
+        lay = "interleaved" if i == 5 else "row"
+        ta, tb = (dev(torch, a.T.copy()), dev(torch, b.T.copy())) if lay == "interleaved" else (dev(torch, a), dev(torch, b))
+        probs.append(dict(op=op, a=ta, b=tb, out=torch.empty_like(ta), layout=lay,
+                          flags=torch.empty(B, dtype=torch.int32, device="cuda")))
+    dg.addsub_grouped(probs)
+    for q, (want, wf), (op, m, B) in zip(probs, wants, specs):
+        got = host(q["out"])
+        if q["layout"] == "interleaved":
+            got = got.T
+        assert np.array_equal(got, want), (op, m)
+        assert np.array_equal(q["flags"].cpu().numpy().view(np.uint32), wf), (op, m)
+    # dependent problems are rejected
+    a = dev(torch, uniform(rng, (10, 4)))
+    with pytest.raises(dg.InvalidArgument):
+        dg.addsub_grouped([dict(op="add", a=a, b=a, out=torch.empty_like(a)),
+                           dict(op="add", a=a, b=a, out=a)])
