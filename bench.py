@@ -341,6 +341,15 @@ def run_ours(args, rank, world, dist):
 
     lib = dg.lib()  # raises if libdotg.so is missing: no fallback
     torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+    if args.only:
+        stream = torch.cuda.current_stream()
+        hbm_peak, _, sm_max = peaks()
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        res = run_secondary(args, torch, dg, W, Launcher(torch, lib, stream), stream, world, dist, hbm_peak,
+                            sm_max, sms)
+        if rank == 0:
+            print(json.dumps({"only": args.only, "configs": res}), flush=True)
+        return 0
     stream = torch.cuda.current_stream()
     L = Launcher(torch, lib, stream)
     hbm_peak, peak_kind, sm_max = peaks()
@@ -489,21 +498,28 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
     warm = max(3, args.warmup)
     dd = dist if world > 1 else None
 
+    def want(k):
+        return not args.only or k in args.only.split(",")
+
     # C1: 4096-bit add + sub (rotate 3 input sets -> 300 MB between reuses > L2)
     sets = []
-    for r in range(3):
+    for r in range(3 if want("C1") else 0):
         a = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 0).view(-1, 64)
         b = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 1 << 40).view(-1, 64)
         sa, sb = W.swap_for_sub(a, b)
         sets.append((a, b, sa, sb, torch.empty_like(a), torch.empty(a.shape[0], dtype=torch.int32, device="cuda")))
     B = W.C1["batch"]
     calls = []
+    if not want("C1"):
+        sets = []
     for a, b, sa, sb, o, f in sets:
         calls.append(L.addsub(False, o, a, b, f, 64, B))
         calls.append(L.addsub(True, o, sa, sb, f, 64, B))
-    ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
+    if sets:
+        ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
     byts = B * (24 * 64 + 4)
-    out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * len(calls) * world / (ms * 1e-3) / 1e9,
+    if sets:
+        out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * len(calls) * world / (ms * 1e-3) / 1e9,
                  "unit": "GB/s", "kernel_gbs": byts * len(calls) / (sum(per) * 1e-3) / 1e9,
                  "frac_hbm": byts * len(calls) / (sum(per) * 1e-3) / 1e9 / hbm_peak,
                  "add_us": statistics.mean(per[0::2]) * 1e3, "sub_us": statistics.mean(per[1::2]) * 1e3}
@@ -512,6 +528,8 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
 
     imad_peak_pps = sms * IMAD_WIDE_PER_CLK_SM * sm_max * 1e6  # u32 products / s at max clock
     for name, gen, m in (("C3", W.c3_inputs, 16), ("C4", W.c4_inputs, 64)):
+        if not want(name):
+            continue
         a, b = gen()
         Bn = a.shape[0]
         o = torch.empty((Bn, 2 * m), dtype=torch.int64, device="cuda")
@@ -529,7 +547,7 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         del a, b, o, calls
         torch.cuda.empty_cache()
 
-    if not args.no_c5:
+    if not args.no_c5 and want("C5"):
         m = W.C5_M if world == 1 else W.C5_M // world
         if world == 1:
             free = torch.cuda.mem_get_info()[0]
@@ -566,6 +584,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of C1,C3,C4,C5: run only those secondary configs")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     args = ap.parse_args()

@@ -14,10 +14,12 @@
 // accumulator's low word is final, the upper 64 bits carry into the next column.
 //
 // Kernels:
-//   k_mul_regs<M>   M <= 16: thread per pair, both operands in registers, columns
-//                   scanned in order (config 3: 1024-bit, M = 16).
-//   k_mul_smem<M>   M in {32, 64, 128}: thread per pair, operands staged in padded
-//                   shared memory by coalesced 256-bit loads, output produced in blocks
+//   k_mul_regs<M>   M <= 4 and the interleaved layout: thread per pair, operands in
+//                   registers, columns scanned in order.
+//   k_mul_regblk<M> M in {8, 16}: registers, output blocks of 16 columns (config 3).
+//   k_mul_smem<M>   M in {32, 64, 128}: persistent, thread per pair, operands staged in
+//                   XOR-swizzled shared memory (2 CTAs per SM fill it) by coalesced
+//                   256-bit loads, output produced in blocks
 //                   of K = 16 columns: for every (output block, a-block) pair a 16x16
 //                   block of products is accumulated into 16 independent column
 //                   accumulators (ILP 16; triangular edge blocks skip the zero
@@ -143,85 +145,178 @@ __device__ __forceinline__ void mul_step(uint32_t (&acc)[kK][3], const uint32_t 
     }
 }
 
-__device__ __forceinline__ void lds4(const uint32_t* p, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
-    const unsigned addr = unsigned(__cvta_generic_to_shared(p));
+// Shared-window byte addresses (computed once per kernel from __cvta_generic_to_shared;
+// converting a generic pointer per access costs an S2UR + ULEA chain on sm_100).
+__device__ __forceinline__ void lds4(uint32_t addr, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
 }
-__device__ __forceinline__ void sts4(uint32_t* p, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
-    const unsigned addr = unsigned(__cvta_generic_to_shared(p));
+__device__ __forceinline__ void sts4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w)
                  : "memory");
 }
 
-template <int M, int PAIRS>
+template <int M>
 struct SmemCfg {
     static constexpr int N = 2 * M;          // words per operand
     static constexpr int NB = N / kK;        // a-blocks
     static constexpr int NS = 2 * N / kK;    // output blocks
-    static constexpr int STRIDE = N + 4;     // padded words per pair (bank-conflict free v4)
-    static constexpr size_t SMEM = size_t(2) * PAIRS * STRIDE * sizeof(uint32_t);
+    static constexpr int CH = N / 4;         // 16-byte chunks per operand per pair
+    static constexpr size_t PAIR_BYTES = size_t(2) * N * sizeof(uint32_t);
 };
 
-template <int M, int PAIRS>
-__global__ void __launch_bounds__(PAIRS) k_mul_smem(uint64_t* out, const uint64_t* a, const uint64_t* b,
-                                                    size_t batch) {
-    using C = SmemCfg<M, PAIRS>;
+// Physical word offset of logical word w of pair p: 16-byte chunks XOR-swizzled by
+// (p & 7) so that 8 consecutive threads reading the same logical chunk hit 8 distinct
+// bank groups (conflict-free ld.shared.v4) without padding.
+// Byte offset of logical word w (w % 4 == 0) of pair p.
+template <int N>
+__device__ __forceinline__ uint32_t swz(int p, int w) {
+    return uint32_t(p * N * 4) + (uint32_t((w >> 2) ^ (p & 7)) << 4);
+}
+
+// Persistent: each CTA (blockDim.x = pairs per group) loops over groups of pairs:
+// stage the group's operands (coalesced 256-bit loads -> swizzled smem), then every
+// thread multiplies its pair. Groups per CTA are balanced so the last round is full.
+template <int M>
+__global__ void __launch_bounds__(128) k_mul_smem(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                  size_t batch) {
+    using C = SmemCfg<M>;
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* sa = smem;
-    uint32_t* sb = smem + PAIRS * C::STRIDE;
-    const unsigned tid = threadIdx.x;
-    const size_t p0 = size_t(blockIdx.x) * PAIRS;
-
-    // Coalesced staging: the CTA's PAIRS rows of a (and b) are one contiguous block.
+    const int P = int(blockDim.x);
+    const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
+    const uint32_t sb = sa + uint32_t(P * C::N * 4);
+    const int tid = int(threadIdx.x);
+    const size_t ngroups = (batch + size_t(P) - 1) / size_t(P);
     constexpr int VPP = M / 4;  // 256-bit vectors per pair per operand
-#pragma unroll 4
-    for (int v = tid; v < PAIRS * VPP; v += PAIRS) {
-        const int pr = v / VPP, ch = v % VPP;
-        const size_t gp = p0 + size_t(pr);
-        uint64_t x[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
-        if (gp < batch) {
-            ld_stream<4>(a + gp * M + 4 * ch, x);
-            ld_stream<4>(b + gp * M + 4 * ch, y);
-        }
-        uint32_t* da = sa + pr * C::STRIDE + 8 * ch;
-        uint32_t* db = sb + pr * C::STRIDE + 8 * ch;
-        sts4(da, lo32(x[0]), hi32(x[0]), lo32(x[1]), hi32(x[1]));
-        sts4(da + 4, lo32(x[2]), hi32(x[2]), lo32(x[3]), hi32(x[3]));
-        sts4(db, lo32(y[0]), hi32(y[0]), lo32(y[1]), hi32(y[1]));
-        sts4(db + 4, lo32(y[2]), hi32(y[2]), lo32(y[3]), hi32(y[3]));
-    }
-    __syncthreads();
 
-    const size_t gp = p0 + tid;
-    if (gp >= batch) return;
-    const uint32_t* pa = sa + tid * C::STRIDE;
-    const uint32_t* pb = sb + tid * C::STRIDE;
-    uint32_t cr0 = 0, cr1 = 0, cr2 = 0;  // carry into the next output block
+    for (size_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const size_t p0 = g * size_t(P);
+        __syncthreads();  // previous group's smem reads are done
+#pragma unroll 4
+        for (int v = tid; v < P * VPP; v += P) {
+            const int pr = v / VPP, ch = v % VPP;
+            const size_t gp = p0 + size_t(pr);
+            uint64_t x[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
+            if (gp < batch) {
+                ld_stream<4>(a + gp * M + 4 * ch, x);
+                ld_stream<4>(b + gp * M + 4 * ch, y);
+            }
+            sts4(sa + swz<C::N>(pr, 8 * ch), lo32(x[0]), hi32(x[0]), lo32(x[1]), hi32(x[1]));
+            sts4(sa + swz<C::N>(pr, 8 * ch + 4), lo32(x[2]), hi32(x[2]), lo32(x[3]), hi32(x[3]));
+            sts4(sb + swz<C::N>(pr, 8 * ch), lo32(y[0]), hi32(y[0]), lo32(y[1]), hi32(y[1]));
+            sts4(sb + swz<C::N>(pr, 8 * ch + 4), lo32(y[2]), hi32(y[2]), lo32(y[3]), hi32(y[3]));
+        }
+        __syncthreads();
+
+        const size_t gp = p0 + size_t(tid);
+        if (gp >= batch) continue;
+        uint32_t cr0 = 0, cr1 = 0, cr2 = 0;  // carry into the next output block
 #pragma unroll 1
-    for (int s = 0; s < C::NS; ++s) {
+        for (int s = 0; s < C::NS; ++s) {
+            uint32_t acc[kK][3];
+#pragma unroll
+            for (int x = 0; x < kK; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
+            const int i_lo = s - C::NB > 0 ? s - C::NB : 0;
+            const int i_hi = s < C::NB - 1 ? s : C::NB - 1;
+#pragma unroll 1
+            for (int I = i_lo; I <= i_hi; ++I) {
+                const int d = s - I;  // 0 .. NB
+                uint32_t A[kK], W[2 * kK];
+#pragma unroll
+                for (int q = 0; q < kK / 4; ++q)
+                    lds4(sa + swz<C::N>(tid, I * kK + 4 * q), A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3]);
+                // W[e] = b'_{(d-1)K + e}; blocks outside [0, N) read as zero.
+#pragma unroll
+                for (int q = 0; q < 2 * kK / 4; ++q) {
+                    const int j = (d - 1) * kK + 4 * q;
+                    if (j >= 0 && j < C::N)
+                        lds4(sb + swz<C::N>(tid, j), W[4 * q], W[4 * q + 1], W[4 * q + 2], W[4 * q + 3]);
+                    else
+                        W[4 * q] = W[4 * q + 1] = W[4 * q + 2] = W[4 * q + 3] = 0;
+                }
+                if (d == 0) mul_step<kLower>(acc, A, W);
+                else if (d == C::NB) mul_step<kUpper>(acc, A, W);
+                else mul_step<kFull>(acc, A, W);
+            }
+            // Deferred normalisation of this block: 16 columns -> 16 final words.
+            uint32_t w[kK];
+#pragma unroll
+            for (int x = 0; x < kK; ++x) {
+                add96(acc[x][0], acc[x][1], acc[x][2], cr0, cr1, cr2);
+                w[x] = acc[x][0];
+                cr0 = acc[x][1];
+                cr1 = acc[x][2];
+                cr2 = 0;
+            }
+            uint64_t o0[4], o1[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o0[k] = uint64_t(w[2 * k]) | (uint64_t(w[2 * k + 1]) << 32);
+                o1[k] = uint64_t(w[8 + 2 * k]) | (uint64_t(w[8 + 2 * k + 1]) << 32);
+            }
+            uint64_t* po = out + gp * (2 * M) + size_t(s) * (kK / 2);
+            st_stream<4>(po, o0);
+            st_stream<4>(po + 4, o1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// M in {8, 16} (config 3): operands in registers, output in blocks of K = 16 columns
+// with 16 independent column accumulators (ILP 16; one accumulator per column would
+// leave the IMAD.WIDE carry chain latency-bound - tools/mac_sweep.cu: 1 accumulator
+// tops out at ~22 products/clk/SM, 16 accumulators at ~29 of the 32 peak).
+// ---------------------------------------------------------------------------
+// Flat grid, one pair per thread. (Measured on B200, r01: a persistent thread-stride
+// loop, and prefetching the next pair into L2 or into shared memory with cp.async, were
+// all slower than this - 48-54 us vs 43.6 us for config 3 - and a compute-only variant
+// with no loads ran at the same 43.5 us, i.e. the kernel is IMAD-issue bound, not
+// memory bound: ~25.5 products/clk/SM while SMs are active.)
+template <int M>
+__global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                    size_t batch) {
+    constexpr int N = 2 * M;         // words per operand
+    constexpr int NB = N / kK;       // a-blocks
+    constexpr int NS = 2 * N / kK;   // output blocks
+    static_assert(N % kK == 0, "M must be a multiple of 8");
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    {
+        uint32_t A[N], B[N];
+#pragma unroll
+        for (int v = 0; v < M / 4; ++v) {
+            uint64_t x[4], y[4];
+            ld_stream<4>(a + pidx * M + 4 * v, x);
+            ld_stream<4>(b + pidx * M + 4 * v, y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                A[8 * v + 2 * k] = lo32(x[k]);
+                A[8 * v + 2 * k + 1] = hi32(x[k]);
+                B[8 * v + 2 * k] = lo32(y[k]);
+                B[8 * v + 2 * k + 1] = hi32(y[k]);
+            }
+        }
+        uint32_t cr0 = 0, cr1 = 0, cr2 = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
         uint32_t acc[kK][3];
 #pragma unroll
         for (int x = 0; x < kK; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
-        const int i_lo = s - C::NB > 0 ? s - C::NB : 0;
-        const int i_hi = s < C::NB - 1 ? s : C::NB - 1;
-#pragma unroll 1
-        for (int I = i_lo; I <= i_hi; ++I) {
-            const int d = s - I;  // 0 .. NB
-            uint32_t A[kK], W[2 * kK];
 #pragma unroll
-            for (int q = 0; q < kK / 4; ++q) lds4(pa + I * kK + 4 * q, A[4 * q], A[4 * q + 1], A[4 * q + 2], A[4 * q + 3]);
-            // W[e] = b'_{(d-1)K + e}; blocks outside [0, N) read as zero.
+        for (int I = 0; I < NB; ++I) {
+            const int d = s - I;
+            if (d < 0 || d > NB) continue;
+            uint32_t Ab[kK], W[2 * kK];
 #pragma unroll
-            for (int q = 0; q < 2 * kK / 4; ++q) {
-                const int j = (d - 1) * kK + 4 * q;
-                if (j >= 0 && j < C::N) lds4(pb + j, W[4 * q], W[4 * q + 1], W[4 * q + 2], W[4 * q + 3]);
-                else W[4 * q] = W[4 * q + 1] = W[4 * q + 2] = W[4 * q + 3] = 0;
+            for (int u = 0; u < kK; ++u) Ab[u] = A[I * kK + u];
+#pragma unroll
+            for (int e = 0; e < 2 * kK; ++e) {
+                const int j = (d - 1) * kK + e;
+                W[e] = (j >= 0 && j < N) ? B[j < 0 ? 0 : (j >= N ? N - 1 : j)] : 0u;
             }
-            if (d == 0) mul_step<kLower>(acc, A, W);
-            else if (d == C::NB) mul_step<kUpper>(acc, A, W);
-            else mul_step<kFull>(acc, A, W);
+            if (d == 0) mul_step<kLower>(acc, Ab, W);
+            else if (d == NB) mul_step<kUpper>(acc, Ab, W);
+            else mul_step<kFull>(acc, Ab, W);
         }
-        // Deferred normalisation of this block: 16 columns -> 16 final words.
         uint32_t w[kK];
 #pragma unroll
         for (int x = 0; x < kK; ++x) {
@@ -237,9 +332,10 @@ __global__ void __launch_bounds__(PAIRS) k_mul_smem(uint64_t* out, const uint64_
             o0[k] = uint64_t(w[2 * k]) | (uint64_t(w[2 * k + 1]) << 32);
             o1[k] = uint64_t(w[8 + 2 * k]) | (uint64_t(w[8 + 2 * k + 1]) << 32);
         }
-        uint64_t* po = out + gp * (2 * M) + size_t(s) * (kK / 2);
+        uint64_t* po = out + pidx * (2 * M) + size_t(s) * (kK / 2);
         st_stream<4>(po, o0);
         st_stream<4>(po + 4, o1);
+    }
     }
 }
 
@@ -284,18 +380,43 @@ cudaError_t run_regs(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
     return cudaGetLastError();
 }
 
-template <int M, int PAIRS>
+template <int M>
+cudaError_t run_regblk(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
+    const size_t blocks = (batch + 127) / 128;
+    k_mul_regblk<M><<<unsigned(blocks), 128, 0, st>>>(out, a, b, batch);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Pairs per group (= threads per CTA) chosen so that two CTAs fill the SM's shared
+// memory and the batch splits into whole rounds of groups across all SMs.
+template <int M>
 cudaError_t run_smem(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
-    using C = SmemCfg<M, PAIRS>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(k_mul_smem<M, PAIRS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(C::SMEM));
-        if (e != cudaSuccess) return e;
-        configured = true;
+    using C = SmemCfg<M>;
+    static int sms = 0, max_smem = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     }
-    const size_t blocks = (batch + PAIRS - 1) / PAIRS;
-    k_mul_smem<M, PAIRS><<<unsigned(blocks), PAIRS, C::SMEM, st>>>(out, a, b, batch);
+    // two CTAs per SM, 1 KB reserved per CTA
+    int P = int((size_t(max_smem) / 2 - 1024) / C::PAIR_BYTES);
+    if (P > 128) P = 128;
+    if (P < 1) P = 1;
+    const size_t smem = size_t(P) * C::PAIR_BYTES;
+    static size_t configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute(k_mul_smem<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    const size_t groups = (batch + size_t(P) - 1) / size_t(P);
+    const size_t slots = size_t(sms) * 2;
+    // balanced rounds: every CTA gets ceil(groups / slots) or one fewer groups
+    const size_t rounds = (groups + slots - 1) / slots;
+    const size_t grid = (groups + rounds - 1) / rounds;
+    k_mul_smem<M><<<unsigned(grid), unsigned(P), smem, st>>>(out, a, b, batch);
     count_launch();
     return cudaGetLastError();
 }
@@ -338,19 +459,19 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
             if (al) return run_regs<4, 0>(out, a, b, batch, stream);
             break;
         case 8:
-            if (al) return run_regs<8, 0>(out, a, b, batch, stream);
+            if (al) return run_regblk<8>(out, a, b, batch, stream);
             break;
         case 16:
-            if (al) return run_regs<16, 0>(out, a, b, batch, stream);
+            if (al) return run_regblk<16>(out, a, b, batch, stream);
             break;
         case 32:
-            if (al) return run_smem<32, 64>(out, a, b, batch, stream);
+            if (al) return run_smem<32>(out, a, b, batch, stream);
             break;
         case 64:
-            if (al) return run_smem<64, 64>(out, a, b, batch, stream);
+            if (al) return run_smem<64>(out, a, b, batch, stream);
             break;
         case 128:
-            if (al) return run_smem<128, 32>(out, a, b, batch, stream);
+            if (al) return run_smem<128>(out, a, b, batch, stream);
             break;
         default:
             break;
