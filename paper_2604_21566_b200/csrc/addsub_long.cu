@@ -14,10 +14,13 @@
 //                          tile's leading propagate run [0, pt) - the only limbs whose
 //                          value depends on that carry-in, besides limb pt itself - is
 //                          not written (deferred). State per tile: pt, tile G, tile P.
-//   pass 2  k_long_scan    one CTA scans the per-tile (G, P) symbolically in the shard
-//                          carry-in X: cin_t = g_ex | (p_ex & X). Emits the shard
+//   pass 2  k_long_scan_chunks + k_long_shard_agg: one CTA per 1024 tiles scans the tile
+//                          (G, P) symbolically in the unknown carry-in X with warp
+//                          ballots (cin_t = g_ex | (p_ex & X) relative to the chunk),
+//                          one warp composes the chunk aggregates into the shard
 //                          aggregate {G, P} (8 bytes) for the cross-GPU exchange.
-//   pass 3  k_long_finish  X from the gathered shard aggregates; per tile: write the
+//   pass 3  k_long_finish  X from the gathered shard aggregates, the chunk carry-in from
+//                          a ballot scan of the chunk aggregates; per tile: write the
 //                          deferred prefix as the propagate value for cin_t and bump
 //                          limb pt by cin_t. This is the reference's rare Phase 4
 //                          (addsub.cpp:61-79) lifted to tiles: on random data it is one
@@ -162,56 +165,72 @@ __device__ __forceinline__ void compose(uint32_t& g, uint32_t& p, uint32_t g2, u
     p = p & p2;
 }
 
-// Single-CTA symbolic scan over tile (G, P). For every tile writes (g_ex, p_ex) with
-// cin_t = g_ex | (p_ex & X); writes agg = {G, P} of the whole shard.
-__global__ void __launch_bounds__(1024) k_long_scan(uint32_t* state, size_t n, uint32_t* agg) {
+// Compose 32 lanes' (g, p) (lane 0 lowest) with two mask additions: returns each lane's
+// exclusive prefix (eg, ep) and the aggregate of all 32 (ag, ap). cin = eg | (ep & X).
+__device__ __forceinline__ void warp_scan_gp(uint32_t g, uint32_t p, unsigned lane, uint32_t& eg, uint32_t& ep,
+                                             uint32_t& ag, uint32_t& ap) {
+    const uint32_t GW = __ballot_sync(0xffffffffu, g);
+    const uint32_t PW = __ballot_sync(0xffffffffu, p);
+    const uint64_t y0 = (uint64_t(GW) << 1) + PW;          // carry-in X = 0
+    const uint64_t y1 = ((uint64_t(GW) << 1) | 1u) + PW;   // carry-in X = 1
+    const uint32_t c0 = uint32_t(y0 ^ PW), c1 = uint32_t(y1 ^ PW);
+    eg = (c0 >> lane) & 1u;
+    ep = ((c1 ^ c0) >> lane) & 1u;
+    ag = uint32_t(y0 >> 32) & 1u;
+    ap = PW == 0xffffffffu;
+}
+
+constexpr int kChunk = 1024;  // tiles per scan chunk (one CTA of pass 2)
+
+// Pass 2a: one CTA per chunk of 1024 tiles. Each tile gets its exclusive (g, p) relative
+// to the chunk start; each chunk its aggregate (bit 0 G, bit 1 P).
+__global__ void __launch_bounds__(kChunk) k_long_scan_chunks(uint32_t* state, size_t n, uint32_t* chunk_agg) {
     __shared__ uint32_t swg[32], swp[32];
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const size_t per = (n + 1023) / 1024;
-    const size_t lo = size_t(tid) * per;
-    const size_t hi = lo + per < n ? lo + per : n;
-    // Thread aggregate over its chunk (identity = (0, 1)).
-    uint32_t tg = 0, tp = 1;
-    for (size_t t = lo; t < hi; ++t) {
-        const uint32_t st = state[t];
-        compose(tg, tp, (st & kBitG) ? 1u : 0u, (st & kBitP) ? 1u : 0u);
-    }
-    // Warp-level exclusive prefix via two mask additions (cin = 0 and cin = 1).
-    const uint32_t GW = __ballot_sync(0xffffffffu, tg);
-    const uint32_t PW = __ballot_sync(0xffffffffu, tp);
-    const uint64_t y0 = (uint64_t(GW) << 1) + PW;
-    const uint64_t y1 = ((uint64_t(GW) << 1) | 1u) + PW;
-    const uint32_t c0 = uint32_t(y0 ^ PW), c1 = uint32_t(y1 ^ PW);
-    uint32_t lg = (c0 >> lane) & 1u;               // exclusive within warp, X = 0
-    uint32_t lp = ((c1 ^ c0) >> lane) & 1u;        // exclusive "all propagate"
+    const size_t t = size_t(blockIdx.x) * kChunk + tid;
+    const uint32_t st = t < n ? state[t] : kBitP;  // identity (G = 0, P = 1) past the end
+    uint32_t lg, lp, wg, wp;
+    warp_scan_gp((st & kBitG) ? 1u : 0u, (st & kBitP) ? 1u : 0u, lane, lg, lp, wg, wp);
     if (lane == 0) {
-        swg[warp] = uint32_t(y0 >> 32) & 1u;
-        swp[warp] = PW == 0xffffffffu;
+        swg[warp] = wg;
+        swp[warp] = wp;
     }
     __syncthreads();
     if (warp == 0) {
-        const uint32_t g = swg[lane], p = swp[lane];
-        const uint32_t GB = __ballot_sync(0xffffffffu, g);
-        const uint32_t PB = __ballot_sync(0xffffffffu, p);
-        const uint64_t z0 = (uint64_t(GB) << 1) + PB;
-        const uint64_t z1 = ((uint64_t(GB) << 1) | 1u) + PB;
-        const uint32_t d0 = uint32_t(z0 ^ PB), d1 = uint32_t(z1 ^ PB);
+        uint32_t eg, ep, cg, cp;
+        warp_scan_gp(swg[lane], swp[lane], lane, eg, ep, cg, cp);
         __syncwarp();
-        swg[lane] = (d0 >> lane) & 1u;
-        swp[lane] = ((d1 ^ d0) >> lane) & 1u;
-        if (lane == 0) {
-            agg[0] = uint32_t(z0 >> 32) & 1u;
-            agg[1] = PB == 0xffffffffu;
-        }
+        swg[lane] = eg;
+        swp[lane] = ep;
+        if (lane == 0) chunk_agg[blockIdx.x] = cg | (cp << 1);
     }
     __syncthreads();
-    // Thread exclusive prefix = warp prefix then lane prefix.
     uint32_t eg = swg[warp], ep = swp[warp];
     compose(eg, ep, lg, lp);
-    for (size_t t = lo; t < hi; ++t) {
-        const uint32_t st = state[t];
-        state[t] = (st & 0xffffu) | (st & (kBitG | kBitP)) | (eg ? kBitGex : 0u) | (ep ? kBitPex : 0u);
-        compose(eg, ep, (st & kBitG) ? 1u : 0u, (st & kBitP) ? 1u : 0u);
+    if (t < n) state[t] = (st & (0xffffu | kBitG | kBitP)) | (eg ? kBitGex : 0u) | (ep ? kBitPex : 0u);
+}
+
+// Exclusive (g, p) over chunk aggregates [0, c) (whole warp, result in every lane).
+__device__ __forceinline__ void chunk_prefix(const uint32_t* chunk_agg, size_t c, unsigned lane, uint32_t& g,
+                                             uint32_t& p) {
+    g = 0;
+    p = 1;
+    for (size_t base = 0; base < c; base += 32) {
+        const size_t k = base + lane;
+        const uint32_t v = k < c ? chunk_agg[k] : 2u;  // identity past c
+        uint32_t eg, ep, ag, ap;
+        warp_scan_gp(v & 1u, (v >> 1) & 1u, lane, eg, ep, ag, ap);
+        compose(g, p, ag, ap);
+    }
+}
+
+// Pass 2b: shard aggregate {G, P} = composition of all chunk aggregates.
+__global__ void __launch_bounds__(32) k_long_shard_agg(const uint32_t* chunk_agg, size_t nchunks, uint32_t* agg) {
+    uint32_t g, p;
+    chunk_prefix(chunk_agg, nchunks, threadIdx.x, g, p);
+    if (threadIdx.x == 0) {
+        agg[0] = g;
+        agg[1] = p;
     }
 }
 
@@ -219,8 +238,9 @@ __global__ void __launch_bounds__(1024) k_long_scan(uint32_t* state, size_t n, u
 // tile whose carry-in is 1 or whose leading propagate run was deferred.
 template <bool SUB>
 __global__ void __launch_bounds__(256) k_long_finish(uint64_t* out, size_t m, const uint32_t* state,
-                                                     size_t n, const uint32_t* all_aggs, int rank,
-                                                     int world, uint32_t* carry_out) {
+                                                     const uint32_t* chunk_agg, size_t n,
+                                                     const uint32_t* all_aggs, int rank, int world,
+                                                     uint32_t* carry_out) {
     uint32_t x = 0;  // carry into this shard
     uint32_t total = 0;
     for (int q = 0; q < world; ++q) {
@@ -233,11 +253,15 @@ __global__ void __launch_bounds__(256) k_long_finish(uint64_t* out, size_t m, co
     const unsigned lane = threadIdx.x & 31u;
     const size_t warp = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const size_t t = warp * 32 + lane;
+    // carry into this warp's chunk (all 32 tiles of a warp share one chunk)
+    uint32_t cg, cp;
+    chunk_prefix(chunk_agg, (warp * 32) / kChunk, lane, cg, cp);
+    const uint32_t xc = cg | (cp & x);
     uint32_t cin = 0, pt = 0;
     size_t len = 0;
     if (t < n) {
         const uint32_t st = state[t];
-        cin = ((st & kBitGex) ? 1u : 0u) | (((st & kBitPex) ? 1u : 0u) & x);
+        cin = ((st & kBitGex) ? 1u : 0u) | (((st & kBitPex) ? 1u : 0u) & xc);
         pt = st & 0xffffu;
         const size_t L0 = t * size_t(kTile);
         len = (m - L0) < size_t(kTile) ? (m - L0) : size_t(kTile);
@@ -255,15 +279,27 @@ __global__ void __launch_bounds__(256) k_long_finish(uint64_t* out, size_t m, co
         const uint32_t n_pre = __shfl_sync(0xffffffffu, pt, src);
         const size_t L0 = (warp * 32 + size_t(src)) * size_t(kTile);
         const uint64_t v = prop_value<SUB>(c);
-        for (uint32_t i = lane; i < n_pre; i += 32) out[L0 + i] = v;
+        uint64_t* o = out + L0;
+        uint32_t i0 = 0;
+        if ((reinterpret_cast<uintptr_t>(o) & 31u) == 0) {  // 256-bit stores for the bulk
+            const uint64_t vv[4] = {v, v, v, v};
+            const uint32_t n4 = n_pre & ~3u;
+            for (uint32_t i = 4 * lane; i < n4; i += 128) st_stream<4>(o + i, vv);
+            i0 = n4;
+        }
+        for (uint32_t i = i0 + lane; i < n_pre; i += 32) o[i] = v;
     }
 }
 
 }  // namespace
 
+// State scratch: one word per tile, then one word per chunk of kChunk tiles.
+size_t state_words(size_t n) { return (n + 63) / 64 * 64; }
+size_t num_chunks(size_t n) { return (n + kChunk - 1) / kChunk; }
+
 size_t long_state_bytes(size_t m) {
     const size_t n = num_tiles(m);
-    return ((n * sizeof(uint32_t)) + 255) / 256 * 256 + 256;
+    return (state_words(n) + num_chunks(n) + 64) * sizeof(uint32_t);
 }
 
 cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
@@ -289,7 +325,11 @@ cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const 
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_long_scan<<<1, 1024, 0, stream>>>(st, n, agg);
+    uint32_t* chunk_agg = st + state_words(n);
+    const size_t nch = num_chunks(n);
+    k_long_scan_chunks<<<unsigned(nch), kChunk, 0, stream>>>(st, n, chunk_agg);
+    count_launch();
+    k_long_shard_agg<<<1, 32, 0, stream>>>(chunk_agg, nch, agg);
     count_launch();
     return cudaGetLastError();
 }
@@ -301,12 +341,13 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
     const size_t warps = (n + 31) / 32;
     const size_t blocks = n == 0 ? 1 : (warps * 32 + 255) / 256;
     const uint32_t* st = static_cast<const uint32_t*>(state);
+    const uint32_t* chunk_agg = st + state_words(n);
     if (sub)
-        k_long_finish<true><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, n, all_aggs, rank, world,
-                                                                  carry_out);
+        k_long_finish<true><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, chunk_agg, n, all_aggs, rank,
+                                                                  world, carry_out);
     else
-        k_long_finish<false><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, n, all_aggs, rank, world,
-                                                                   carry_out);
+        k_long_finish<false><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, chunk_agg, n, all_aggs, rank,
+                                                                   world, carry_out);
     count_launch();
     return cudaGetLastError();
 }
