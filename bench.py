@@ -406,22 +406,28 @@ def run_ours(args, rank, world, dist):
                 h.copy_(x[k])
                 hs[k] = h
             hs["o"] = torch.empty(x["a"].shape, dtype=torch.int64, pin_memory=True)
+            hs["os"] = torch.empty(x["a"].shape, dtype=torch.int64, pin_memory=True)
             hs["f"] = torch.empty(x["B"], dtype=torch.int32, pin_memory=True)
+            hs["fs"] = torch.empty(x["B"], dtype=torch.int32, pin_memory=True)
             hsets.append((x["m"], x["B"], hs))
-        P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        from paper_2604_21566_b200._lib import AddSubProblem
+
+        hprobs = (AddSubProblem * 8)()
+        for i, (m, B, hs) in enumerate(hsets):
+            hprobs[i] = AddSubProblem(0, 0, hs["o"].data_ptr(), hs["a"].data_ptr(), hs["b"].data_ptr(),
+                                      hs["f"].data_ptr(), m, B)
+            hprobs[4 + i] = AddSubProblem(1, 0, hs["os"].data_ptr(), hs["sa"].data_ptr(), hs["sb"].data_ptr(),
+                                          hs["fs"].data_ptr(), m, B)
 
         def e2e_step():
-            for m, B, hs in hsets:
-                rc = lib.dotg_add_batch_host(P(hs["o"]), P(hs["a"]), P(hs["b"]), P(hs["f"]), m, B)
-                assert rc == 0, lib.dotg_last_error()
-            for m, B, hs in hsets:
-                rc = lib.dotg_sub_batch_host(P(hs["o"]), P(hs["sa"]), P(hs["sb"]), P(hs["f"]), m, B)
-                assert rc == 0, lib.dotg_last_error()
+            rc = lib.dotg_addsub_grouped_host(hprobs, 8)
+            assert rc == 0, lib.dotg_last_error()
 
         e2e_step()
         # correctness spot check of the e2e path against the device result (last call = sub m=256)
         m, B, hs = hsets[-1]
-        assert torch.equal(hs["o"], bufs[-1]["os"].cpu()), "e2e result mismatch"
+        assert torch.equal(hs["os"], bufs[-1]["os"].cpu()), "e2e result mismatch"
+        assert torch.equal(hsets[0][2]["o"], bufs[0]["oa"].cpu()), "e2e result mismatch"
         e_steps = max(3, min(args.steps, 20))
         if world > 1:
             dist.barrier()
@@ -437,7 +443,7 @@ def run_ours(args, rank, world, dist):
         d2h = sum(2 * (B * m * 8 + 4 * B) for m, B in C2_SIZES)
         e2e = {"value": step_bytes * world * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e_steps,
-               "api": "dotg_add_batch_host / dotg_sub_batch_host (pinned host buffers, 2-stream copy/compute overlap)"}
+               "api": "dotg_addsub_grouped_host: the 8 host problems through one 3-stream H2D/kernel/D2H pipeline (pinned host buffers)"}
         del hsets
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
@@ -492,7 +498,7 @@ def run_ours(args, rank, world, dist):
     return 0
 
 
-def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms):
+def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms, rank0=True):
     out = {}
     steps = max(3, min(args.steps, 50))
     warm = max(3, args.warmup)
@@ -544,6 +550,44 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
                      "frac_imad": pairs_s * prods / imad_peak_pps,
                      "hbm_gbs": Bn * 32 * m / (per[0] * 1e-3) / 1e9,
                      "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
+        if not args.no_e2e:
+            # e2e: pinned host arrays through dotg_mul_batch_host (copies inside the timed region)
+            ha = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
+            hb = torch.empty(b.shape, dtype=torch.int64, pin_memory=True)
+            ho = torch.empty(o.shape, dtype=torch.int64, pin_memory=True)
+            ha.copy_(a)
+            hb.copy_(b)
+            lib = dg.lib()
+            P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+            assert lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, Bn) == 0
+            assert torch.equal(ho, o.cpu()), "mul e2e mismatch"
+            reps = 5
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, Bn)
+            dt = (time.perf_counter() - t0) / reps
+            out[name]["e2e"] = {"value": Bn * world / dt, "unit": "pairs/s", "h2d_bytes_per_step": 2 * Bn * m * 8,
+                                "d2h_bytes_per_step": Bn * 2 * m * 8, "api": "dotg_mul_batch_host"}
+            if rank0 and world == 1 and not args.no_cpu:
+                try:
+                    cpu = CpuRef()
+                    import numpy as np
+
+                    nsamp = Bn // 16
+                    sa_ = ha[:nsamp].numpy().view(np.uint64)
+                    sb_ = hb[:nsamp].numpy().view(np.uint64)
+                    so_ = np.empty((nsamp, 2 * m), np.uint64)
+                    cpu.run(2, sa_, sb_, so_, None)  # warm
+                    t0 = time.perf_counter()
+                    cpu.run(2, sa_, sb_, so_, None)
+                    cdt = time.perf_counter() - t0
+                    assert np.array_equal(so_, ho[:nsamp].numpy().view(np.uint64)), "cpu/gpu mismatch"
+                    out[name]["cpu_baseline"] = {"value": nsamp / cdt, "unit": "pairs/s", "cores": cpu.threads,
+                                                 "kind": cpu.kind,
+                                                 "sample": f"{nsamp} pairs of the same batch, dot_mul_words"}
+                except Exception as e:  # noqa: BLE001
+                    out[name]["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)}
+            del ha, hb, ho
         del a, b, o, calls
         torch.cuda.empty_cache()
 

@@ -144,6 +144,9 @@ int dotg_sub_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
                         size_t m, size_t batch);
 int dotg_mul_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                         size_t batch);
+/* Several independent row-major problems through ONE copy/compute pipeline (no drain
+ * between problems); host pointers; layout must be DOTG_ROW_MAJOR. */
+int dotg_addsub_grouped_host(const dotg_addsub_problem* problems, int n);
 /* Single number, host spans (the literal span form). *carry receives the flag. */
 int dotg_add_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                         uint32_t* carry);

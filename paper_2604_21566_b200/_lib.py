@@ -36,6 +36,7 @@ SIGNATURES = {
     "dotg_add_batch_host": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t]),
     "dotg_sub_batch_host": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t]),
     "dotg_mul_batch_host": (c_int, [_P, _P, _P, c_size_t, c_size_t]),
+    "dotg_addsub_grouped_host": (c_int, [_P, c_int]),
     "dotg_add_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
     "dotg_sub_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),

@@ -139,14 +139,20 @@ int words(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t 
 }
 
 // ---------------------------------------------------------------------------
-// Host pipelines. One global staging context (host calls are synchronous).
+// Host pipelines. One global staging context (host calls are synchronous). A call's
+// work is cut into slices of ~24 MB of input; slice k runs on stream k % kNS with its
+// own device staging slot: H2D(a, b) -> kernel -> D2H(out, flags). Consecutive slices
+// sit on different streams, so the H2D copy engine, the SMs and the D2H copy engine
+// work on three slices at once; several jobs (e.g. a whole multi-size sweep) share one
+// pipeline with no drain between jobs.
 // ---------------------------------------------------------------------------
+constexpr int kNS = 3;
 struct HostCtx {
     std::mutex mu;
     int device = -1;
-    cudaStream_t s[2] = {nullptr, nullptr};
-    char* buf[2] = {nullptr, nullptr};
-    size_t cap = 0;  // bytes per buffer
+    cudaStream_t s[kNS] = {};
+    char* buf[kNS] = {};
+    size_t cap = 0;  // bytes per slot
 };
 HostCtx g_host;
 
@@ -155,19 +161,19 @@ int host_prepare(size_t bytes_per_slot) {
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     if (g_host.device != dev) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNS; ++i) {
             if (g_host.buf[i]) cudaFree(g_host.buf[i]);
             g_host.buf[i] = nullptr;
         }
         g_host.cap = 0;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNS; ++i) {
             if ((e = cudaStreamCreateWithFlags(&g_host.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "stream");
         }
         g_host.device = dev;
     }
     if (g_host.cap < bytes_per_slot) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNS; ++i) {
             if (g_host.buf[i]) cudaFree(g_host.buf[i]);
             g_host.buf[i] = nullptr;
             if ((e = cudaMalloc(&g_host.buf[i], bytes_per_slot)) != cudaSuccess)
@@ -182,7 +188,77 @@ constexpr size_t kSliceBytes = size_t(24) << 20;  // input bytes per slice (a + 
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// op: 0 add, 1 sub, 2 mul. Row-major host arrays.
+struct HostJob {  // op: 0 add, 1 sub, 2 mul; row-major host arrays
+    int op;
+    uint64_t* out;
+    const uint64_t* a;
+    const uint64_t* b;
+    uint32_t* flags;
+    size_t m, batch;
+};
+
+struct SliceGeom {
+    size_t in_b, out_b, slice, sa, so, sf;
+};
+
+SliceGeom geom(const HostJob& j) {
+    SliceGeom g{};
+    g.in_b = j.m * 8;
+    g.out_b = j.op == 2 ? 2 * j.m * 8 : j.m * 8;
+    g.slice = std::min(std::max<size_t>(1, kSliceBytes / (2 * g.in_b)), j.batch);
+    g.sa = align_up(g.slice * g.in_b, 256);
+    g.so = align_up(g.slice * g.out_b, 256);
+    g.sf = align_up(g.slice * 4, 256);
+    return g;
+}
+
+// Jobs must be validated; m > 0 and batch > 0 for every job.
+int run_host_jobs(const HostJob* jobs, int n) {
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    size_t slot = 256;
+    for (int q = 0; q < n; ++q) {
+        const SliceGeom g = geom(jobs[q]);
+        slot = std::max(slot, 2 * g.sa + g.so + g.sf);
+    }
+    int rc = host_prepare(slot);
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = cudaSuccess;
+    size_t k = 0;
+    for (int q = 0; q < n && e == cudaSuccess; ++q) {
+        const HostJob& j = jobs[q];
+        const SliceGeom g = geom(j);
+        for (size_t p0 = 0; p0 < j.batch && e == cudaSuccess; p0 += g.slice, ++k) {
+            const size_t cnt = std::min(g.slice, j.batch - p0);
+            const int i = int(k % kNS);
+            cudaStream_t st = g_host.s[i];
+            uint64_t* da = reinterpret_cast<uint64_t*>(g_host.buf[i]);
+            uint64_t* db = reinterpret_cast<uint64_t*>(g_host.buf[i] + g.sa);
+            uint64_t* dout = reinterpret_cast<uint64_t*>(g_host.buf[i] + 2 * g.sa);
+            uint32_t* dfl = reinterpret_cast<uint32_t*>(g_host.buf[i] + 2 * g.sa + g.so);
+            // The previous use of this slot was enqueued on the same stream: ordered.
+            e = cudaMemcpyAsync(da, j.a + p0 * j.m, cnt * g.in_b, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(db, j.b + p0 * j.m, cnt * g.in_b, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) {
+                e = j.op == 2 ? dotg::launch_mul_batch(dout, da, db, j.m, cnt, 0, st)
+                              : dotg::launch_addsub_batch(j.op == 1, dout, da, db, j.flags ? dfl : nullptr, j.m, cnt,
+                                                          0, st);
+            }
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(j.out + p0 * (g.out_b / 8), dout, cnt * g.out_b, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess && j.flags && j.op != 2)
+                e = cudaMemcpyAsync(j.flags + p0, dfl, cnt * 4, cudaMemcpyDeviceToHost, st);
+        }
+    }
+    cudaError_t es = cudaSuccess;
+    for (int i = 0; i < kNS; ++i) {
+        cudaError_t x = cudaStreamSynchronize(g_host.s[i]);
+        if (es == cudaSuccess) es = x;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "dotg host pipeline");
+    if (es != cudaSuccess) return cuda_fail(es, "dotg host pipeline sync");
+    return DOTG_OK;
+}
+
 int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                size_t batch) {
     int rc = op == 2 ? check_mul(out, a, b, m, batch, DOTG_ROW_MAJOR)
@@ -194,42 +270,8 @@ int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint
         if (flags) std::memset(flags, 0, batch * sizeof(uint32_t));
         return DOTG_OK;
     }
-    std::lock_guard<std::mutex> lk(g_host.mu);
-    const size_t in_b = m * 8;                          // per operand per pair
-    const size_t out_b = op == 2 ? 2 * m * 8 : m * 8;   // per pair
-    size_t slice = std::max<size_t>(1, kSliceBytes / (2 * in_b));
-    slice = std::min(slice, batch);
-    const size_t sa = align_up(slice * in_b, 256), so = align_up(slice * out_b, 256);
-    const size_t sf = align_up(slice * 4, 256);
-    if ((rc = host_prepare(2 * sa + so + sf)) != DOTG_OK) return rc;
-    cudaError_t e = cudaSuccess;
-    size_t k = 0;
-    for (size_t p0 = 0; p0 < batch && e == cudaSuccess; p0 += slice, ++k) {
-        const size_t n = std::min(slice, batch - p0);
-        const int i = int(k & 1);
-        cudaStream_t st = g_host.s[i];
-        uint64_t* da = reinterpret_cast<uint64_t*>(g_host.buf[i]);
-        uint64_t* db = reinterpret_cast<uint64_t*>(g_host.buf[i] + sa);
-        uint64_t* dout = reinterpret_cast<uint64_t*>(g_host.buf[i] + 2 * sa);
-        uint32_t* dfl = reinterpret_cast<uint32_t*>(g_host.buf[i] + 2 * sa + so);
-        // The previous use of this slot was enqueued on the same stream: ordered.
-        e = cudaMemcpyAsync(da, a + p0 * m, n * in_b, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(db, b + p0 * m, n * in_b, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) {
-            e = op == 2 ? dotg::launch_mul_batch(dout, da, db, m, n, 0, st)
-                        : dotg::launch_addsub_batch(op == 1, dout, da, db, flags ? dfl : nullptr, m, n, 0, st);
-        }
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out + p0 * (out_b / 8), dout, n * out_b, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess && flags && op != 2)
-            e = cudaMemcpyAsync(flags + p0, dfl, n * 4, cudaMemcpyDeviceToHost, st);
-    }
-    cudaError_t e0 = cudaStreamSynchronize(g_host.s[0]);
-    cudaError_t e1 = cudaStreamSynchronize(g_host.s[1]);
-    if (e != cudaSuccess) return cuda_fail(e, "dotg host batch");
-    if (e0 != cudaSuccess) return cuda_fail(e0, "dotg host batch sync");
-    if (e1 != cudaSuccess) return cuda_fail(e1, "dotg host batch sync");
-    return DOTG_OK;
+    const HostJob j{op, out, a, b, flags, m, batch};
+    return run_host_jobs(&j, 1);
 }
 
 // Single long number from host spans: slices are independent shards (dotg_shard_*),
@@ -411,6 +453,28 @@ int dotg_shard_finish(int sub, uint64_t* out, size_t m, void* state, const uint3
     cudaError_t e = dotg::launch_long_finish(sub != 0, out, m, state, all_aggs, rank, world, carry_out,
                                              static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg shard finish");
+}
+
+int dotg_addsub_grouped_host(const dotg_addsub_problem* problems, int n) {
+    if (n < 0 || (n > 0 && problems == nullptr)) return fail(DOTG_EINVAL, "grouped: bad problem list");
+    std::vector<HostJob> jobs;
+    for (int i = 0; i < n; ++i) {
+        const dotg_addsub_problem& q = problems[i];
+        if (q.op != 0 && q.op != 1) return fail(DOTG_EINVAL, "grouped: op must be 0 (add) or 1 (sub)");
+        if (q.layout != DOTG_ROW_MAJOR) return fail(DOTG_EINVAL, "grouped host: row-major only");
+        int rc = check_addsub(q.out, q.a, q.b, q.flags, q.m, q.batch, q.layout);
+        if (rc != DOTG_OK) return rc;
+        if (q.batch == 0) continue;
+        if (q.m == 0) {
+            if (q.flags) std::memset(q.flags, 0, q.batch * sizeof(uint32_t));
+            continue;
+        }
+        jobs.push_back(HostJob{q.op, q.out, q.a, q.b, q.flags, q.m, q.batch});
+    }
+    if (jobs.empty()) return DOTG_OK;
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    return run_host_jobs(jobs.data(), int(jobs.size()));
 }
 
 int dotg_add_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,

@@ -107,3 +107,25 @@ def test_batch_host_pipeline(cuda, oracle):
     assert np.array_equal(out, want) and np.array_equal(fl, wf)
     a, b = uniform(rng, (30000, 16)), uniform(rng, (30000, 16))
     assert np.array_equal(dg.mul_batch_host(a, b), oracle.mul_batch(a, b))
+
+
+def test_grouped_host_pipeline(cuda, oracle):
+    import ctypes
+
+    import paper_2604_21566_b200 as dg
+    from paper_2604_21566_b200._lib import AddSubProblem
+
+    rng = np.random.default_rng(13)
+    specs = [(0, 4, 300_000), (1, 16, 70_000), (0, 64, 20_000), (1, 256, 5_000), (0, 3, 1000), (1, 0, 10)]
+    arr = (AddSubProblem * len(specs))()
+    keep = []
+    for i, (op, m, B) in enumerate(specs):
+        a, b = spiky(rng, (B, m)), spiky(rng, (B, m))
+        out, fl = np.zeros((B, m), np.uint64), np.full(B, 9, np.uint32)
+        keep.append((op, a, b, out, fl))
+        arr[i] = AddSubProblem(op, 0, out.ctypes.data if out.size else None, a.ctypes.data if a.size else None,
+                               b.ctypes.data if b.size else None, fl.ctypes.data, m, B)
+    dg.api.check(dg.lib().dotg_addsub_grouped_host(arr, len(specs)))
+    for op, a, b, out, fl in keep:
+        want, wf = oracle.addsub_batch(op, a, b)
+        assert np.array_equal(out, want) and np.array_equal(fl, wf)
