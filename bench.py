@@ -393,7 +393,7 @@ def run_ours(args, rank, world, dist):
     per_size = {f"m{x['m']}": {"add_gbs": call_bytes[i] / (per_single[i] * 1e-3) / 1e9,
                                "sub_gbs": call_bytes[i] / (per_single[i + 4] * 1e-3) / 1e9}
                 for i, x in enumerate(bufs)}
-    traffic = traffic_table().get("C2_per_launch_bytes")
+    traffic = traffic_table().get("C2_per_launch_bytes_grouped" if not args.ungrouped else "C2_per_launch_bytes")
 
     # ---- e2e: the same step through the host-buffer C ABI (pinned host arrays) ----
     e2e = None
