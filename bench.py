@@ -39,6 +39,21 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 IMAD_WIDE_PER_CLK_SM = 32.0  # measured: profiles/r01_imad_peak.json (cc_chain_products)
 C2_SIZES = [(4, 1 << 20), (16, 1 << 18), (64, 1 << 16), (256, 1 << 14)]
+METRIC = "add/sub GB/s vs HBM peak (C2 carry-stress sweep, 4/16/64/256 limbs)"
+DATA = ("synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: limb all-ones p=0.5 else uniform, "
+        "1% forced full carry chains, sub swapped to a>=b)")
+
+
+def c2_config(ungrouped=False, working_set=None):
+    cfg = {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
+           "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
+           "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if ungrouped else
+                    "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"),
+           "per_rank": "full sweep on every rank (weak scaling, no collective)"}
+    if working_set is not None:
+        cfg["l2"] = (f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct inputs "
+                     "(126 MB L2), every buffer touched once per step")
+    return cfg
 
 
 # ---------------------------------------------------------------------------
@@ -242,11 +257,11 @@ def run_reference(args, rank, world):
     dt = time.perf_counter() - t0
     gbs = c2_bytes() * args.steps / dt / 1e9
     line = {
-        "impl": "reference", "metric": "add/sub GB/s (C2 carry-stress sweep, 4/16/64/256 limbs)", "value": gbs,
+        "impl": "reference", "metric": METRIC, "value": gbs,
         "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u64", "data": "synthetic (seeded splitmix64, BASELINE.json configs[1] distribution)",
-        "config": {"workload": "C2 carry-stress add+sub sweep", "sizes": C2_SIZES, "layout": "row-major"},
+        "dtype": "u64", "data": DATA,
+        "config": c2_config(),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
                          "sample": f"full C2 step (add+sub, 4 sizes) x {args.steps} steps; route {cpu.note}"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -466,21 +481,14 @@ def run_ours(args, rank, world, dist):
 
     secondary = {}
     if not args.no_secondary:
-        secondary = run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms)
+        secondary = run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms, rank == 0)
 
     line = {
-        "metric": "add/sub GB/s vs HBM peak (C2 carry-stress sweep, 4/16/64/256 limbs)",
+        "metric": METRIC,
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: limb all-ones p=0.5 else "
-                "uniform, 1% forced full carry chains, sub swapped to a>=b)",
-        "config": {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
-                   "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
-                   "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if args.ungrouped else
-                            "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"),
-                   "l2": f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct "
-                         "inputs (126 MB L2), every buffer touched once per step",
-                   "per_rank": "full sweep on every rank (weak scaling, no collective)"},
+        "data": DATA,
+        "config": c2_config(args.ungrouped, working_set),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
@@ -592,29 +600,46 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         torch.cuda.empty_cache()
 
     if not args.no_c5 and want("C5"):
-        m = W.C5_M if world == 1 else W.C5_M // world
-        if world == 1:
-            free = torch.cuda.mem_get_info()[0]
-            if free < 3 * m * 8 + (1 << 30):
-                out["C5"] = {"skipped": f"needs {3 * m * 8 / 2**30:.0f} GiB free"}
-                return out
+        from paper_2604_21566_b200.sharded import ShardedWords, shard_bounds
+
+        M5 = W.C5_M
+        rank = dist.get_rank() if world > 1 else 0
+        lo, hi = shard_bounds(M5, rank, world)
+        n_local = hi - lo
+        free = torch.cuda.mem_get_info()[0]
+        if free < 3 * n_local * 8 + (1 << 30):
+            out["C5"] = {"skipped": f"needs {3 * n_local * 8 / 2**30:.0f} GiB free per GPU"}
+            return out
         res = {}
         for sub in (False, True):
+            a, b = W.c5_shard_inputs(sub, lo, hi) if world > 1 else W.c5_inputs(sub)
+            o = torch.empty_like(a)
+            c = torch.empty(1, dtype=torch.int32, device="cuda")
             if world == 1:
-                a, b = W.c5_inputs(sub)
-                o = torch.empty_like(a)
-                c = torch.empty(1, dtype=torch.int32, device="cuda")
                 fn = dg.lib().dotg_sub_words if sub else dg.lib().dotg_add_words
                 args_ = (ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
-                         m, ctypes.c_void_p(c.data_ptr()), L.stream)
-                ms, per = timed_steps(torch, None, 1, stream, [lambda: fn(*args_)], 3, 2)
-                res["sub" if sub else "add"] = {"ms": ms, "gbs": 24 * m / (ms * 1e-3) / 1e9,
-                                                "frac_hbm": 24 * m / (ms * 1e-3) / 1e9 / hbm_peak,
-                                                "carry": int(c.item())}
-                del a, b, o
+                         n_local, ctypes.c_void_p(c.data_ptr()), L.stream)
+                call = lambda: fn(*args_)  # noqa: E731
+            else:
+                # limb-range shards: local pass, 8-byte NCCL all-gather, boundary fix-up
+                sw = ShardedWords()
+                state = sw.state_for(n_local, a.device)
+
+                def call():
+                    sw.run(sub, o, a, b, state=state)
+                    return 0
+            ms, per = timed_steps(torch, dd, world, stream, [call], 3, 2)
+            carry = int(c.item()) if world == 1 else None
+            res["sub" if sub else "add"] = {"ms": ms, "gbs": 24 * M5 / (ms * 1e-3) / 1e9,
+                                            "frac_hbm_per_gpu": 24 * M5 / world / (ms * 1e-3) / 1e9 / hbm_peak,
+                                            "carry": carry}
+            del a, b, o
             torch.cuda.empty_cache()
-        out["C5"] = {"metric": "one 2^30-limb add/sub GB/s", "unit": "GB/s", "n_limbs": W.C5_M,
-                     "run": list(W.C5_RUN), **res}
+        out["C5"] = {"metric": "one 2^30-limb add/sub GB/s (whole number, all GPUs)", "unit": "GB/s",
+                     "n_limbs": M5, "shard_limbs": n_local, "run": list(W.C5_RUN),
+                     "mode": "single GPU tiled path" if world == 1 else
+                             f"{world} limb-range shards, NCCL all_gather of 8-byte (G,P) per rank",
+                     **res}
     return out
 
 

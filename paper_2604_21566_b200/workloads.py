@@ -137,3 +137,28 @@ def c5_inputs(sub: bool, m: int = C5_M, run=C5_RUN, device="cuda", seed: int = 0
         a[m - 1] = ALL_ONES
         b[m - 1] = 0
     return a, b
+
+
+def c5_shard_inputs(sub: bool, lo: int, hi: int, m: int = C5_M, run=C5_RUN, device="cuda", seed: int = 0xC5):
+    """Limbs [lo, hi) of c5_inputs(sub, m, run): what rank r holds when the number is
+    sharded by limb range. Identical values to slicing the single-GPU operands."""
+    n = hi - lo
+    a = fill(n, seed, lo, device)
+    b = fill(n, seed, m + lo, device)
+    rlo, rhi = run
+    s0, s1 = max(rlo, lo), min(rhi, hi)
+    if s1 > s0:
+        a[s0 - lo:s1 - lo] = ALL_ONES
+        b[s0 - lo:s1 - lo] = ALL_ONES if sub else 0
+    if rhi > rlo and rlo > 0 and lo <= rlo - 1 < hi:
+        i = rlo - 1 - lo
+        if sub:
+            a[i] = 0
+            b[i] = 1
+        else:
+            a[i] = ALL_ONES
+            b[i] = 1
+    if sub and lo <= m - 1 < hi:
+        a[m - 1 - lo] = ALL_ONES
+        b[m - 1 - lo] = 0
+    return a, b

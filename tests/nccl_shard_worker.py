@@ -1,0 +1,44 @@
+"""Worker for test_gpu_nccl.py: the config-5 shard protocol over a real NCCL process
+group (launched by torch.distributed.run, one rank per visible GPU)."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+
+def main():
+    from helpers import Oracle
+
+    from paper_2604_21566_b200 import workloads as W
+    from paper_2604_21566_b200.sharded import ShardedWords, shard_bounds
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dist.init_process_group("nccl")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    m = 3 << 20
+    run = (3 * m // 8, 5 * m // 8)
+    orc = Oracle()
+    for sub in (False, True):
+        lo, hi = shard_bounds(m, rank, world)
+        a, b = W.c5_shard_inputs(sub, lo, hi, m=m, run=run)
+        ga, gb = W.c5_inputs(sub, m=m, run=run)
+        assert torch.equal(ga[lo:hi], a) and torch.equal(gb[lo:hi], b)
+        out = torch.empty_like(a)
+        sw = ShardedWords()
+        out, carry = sw.run(sub, out, a, b)
+        ha, hb = ga.cpu().numpy().view(np.uint64), gb.cpu().numpy().view(np.uint64)
+        want, wf = orc.sub(ha, hb) if sub else orc.add(ha, hb)
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want[lo:hi]), (rank, sub)
+        assert int(carry.item()) == wf
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"rank {rank}/{world} ok")
+
+
+if __name__ == "__main__":
+    main()
