@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -146,7 +147,27 @@ int words(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t 
 // work on three slices at once; several jobs (e.g. a whole multi-size sweep) share one
 // pipeline with no drain between jobs.
 // ---------------------------------------------------------------------------
-constexpr int kNS = 3;
+constexpr int kNS = 4;  // max pipeline depth; the used depth is host_streams()
+
+// Tunables (environment, read once): DOTG_HOST_STREAMS (1..4, default 3) and
+// DOTG_HOST_SLICE_MB (input MB per slice, default 24).
+int host_streams() {
+    static const int v = [] {
+        const char* e = std::getenv("DOTG_HOST_STREAMS");
+        const int x = e ? std::atoi(e) : 3;
+        return x < 1 ? 1 : (x > kNS ? kNS : x);
+    }();
+    return v;
+}
+size_t slice_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("DOTG_HOST_SLICE_MB");
+        const long x = e ? std::atol(e) : 24;
+        return size_t(x < 1 ? 1 : x) << 20;
+    }();
+    return v;
+}
+
 struct HostCtx {
     std::mutex mu;
     int device = -1;
@@ -184,7 +205,6 @@ int host_prepare(size_t bytes_per_slot) {
     return DOTG_OK;
 }
 
-constexpr size_t kSliceBytes = size_t(24) << 20;  // input bytes per slice (a + b)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -205,7 +225,7 @@ SliceGeom geom(const HostJob& j) {
     SliceGeom g{};
     g.in_b = j.m * 8;
     g.out_b = j.op == 2 ? 2 * j.m * 8 : j.m * 8;
-    g.slice = std::min(std::max<size_t>(1, kSliceBytes / (2 * g.in_b)), j.batch);
+    g.slice = std::min(std::max<size_t>(1, slice_bytes() / (2 * g.in_b)), j.batch);
     g.sa = align_up(g.slice * g.in_b, 256);
     g.so = align_up(g.slice * g.out_b, 256);
     g.sf = align_up(g.slice * 4, 256);
@@ -229,7 +249,7 @@ int run_host_jobs(const HostJob* jobs, int n) {
         const SliceGeom g = geom(j);
         for (size_t p0 = 0; p0 < j.batch && e == cudaSuccess; p0 += g.slice, ++k) {
             const size_t cnt = std::min(g.slice, j.batch - p0);
-            const int i = int(k % kNS);
+            const int i = int(k % size_t(host_streams()));
             cudaStream_t st = g_host.s[i];
             uint64_t* da = reinterpret_cast<uint64_t*>(g_host.buf[i]);
             uint64_t* db = reinterpret_cast<uint64_t*>(g_host.buf[i] + g.sa);
@@ -287,7 +307,7 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
     if ((rc = check_device()) != DOTG_OK) return rc;
     std::lock_guard<std::mutex> lk(g_host.mu);
     if ((rc = host_prepare(256)) != DOTG_OK) return rc;
-    const size_t slice = std::max<size_t>(4096, (kSliceBytes / 16) / 4096 * 4096);
+    const size_t slice = std::max<size_t>(4096, (slice_bytes() / 16) / 4096 * 4096);
     const size_t nsl = (m + slice - 1) / slice;
     const size_t sb = align_up(dotg::long_state_bytes(slice), 256);
     const size_t ab = align_up(m * 8, 256);
