@@ -9,8 +9,8 @@
 // a usable device every call throws std::runtime_error.
 //
 // Differences, by design:
-//   * AddSubStats instrumentation (addsub.hpp:53-72) is not produced by the device path;
-//     passing a non-null stats pointer throws std::logic_error.
+//   * AddSubStats (addsub.hpp:53-72): chunks_processed / phase4_triggers are produced
+//     (derived on the device); the rdtsc phase ticks are not (collect_ticks throws).
 //   * Only the saturated 64-bit radix is on the device path (RadixConfig{52} throws
 //     std::logic_error; the 52-bit 4x4/5x5 route is out of scope).
 //   * Partial aliasing of out with a/b (undefined in the reference) throws.
@@ -46,7 +46,21 @@ constexpr unsigned lane_count(Width w) { return w == Width::scalar ? 8u : static
 
 inline constexpr std::size_t kMaxMulLimbs = std::size_t(1) << 24;  // mul.hpp:30
 
-struct AddSubStats;  // accepted for signature compatibility only (see header note)
+// The counters of the reference's AddSubStats (addsub.hpp:53-72) that the device path
+// reproduces (derived on the device from a, b and the result, csrc/stats.cu). The rdtsc
+// phase ticks have no device equivalent: collect_ticks = true throws std::logic_error.
+struct AddSubStats {
+    std::uint64_t chunks_processed = 0;
+    std::uint64_t phase4_triggers = 0;
+    bool collect_ticks = false;
+    double phase4_rate() const {
+        return chunks_processed ? double(phase4_triggers) / double(chunks_processed) : 0.0;
+    }
+    void merge(const AddSubStats& o) {
+        chunks_processed += o.chunks_processed;
+        phase4_triggers += o.phase4_triggers;
+    }
+};
 
 namespace detail {
 inline void check(int rc) {
@@ -55,30 +69,41 @@ inline void check(int rc) {
     if (rc == DOTG_EINVAL) throw std::invalid_argument(msg);
     throw std::runtime_error("dotg: " + msg);
 }
-inline void no_stats(const AddSubStats* st) {
-    if (st != nullptr) throw std::logic_error("AddSubStats is not produced by the B200 path");
+inline void no_ticks(const AddSubStats* st) {
+    if (st != nullptr && st->collect_ticks)
+        throw std::logic_error("AddSubStats::collect_ticks (rdtsc phase ticks) has no device equivalent");
 }
 inline void validate(Width w) { check(dotg_validate_width(static_cast<int>(w))); }
 
 inline unsigned run_words(bool sub, std::span<limb_t> out, std::span<const limb_t> a,
-                          std::span<const limb_t> b, Width w) {
+                          std::span<const limb_t> b, Width w, AddSubStats* st) {
     validate(w);
+    no_ticks(st);
     if (a.size() != b.size() || out.size() != a.size())  // addsub.cpp:139-140
         throw std::invalid_argument("dot add/sub: operand lengths differ (caller pads)");
     std::uint32_t carry = 0;
+    if (st != nullptr) {
+        std::uint64_t ch = 0, fi = 0;
+        check(dotg_words_host_stats(sub ? 1 : 0, out.data(), a.data(), b.data(), a.size(), static_cast<int>(w),
+                                    &carry, &ch, &fi));
+        st->chunks_processed += ch;
+        st->phase4_triggers += fi;
+        return carry;
+    }
     check(sub ? dotg_sub_words_host(out.data(), a.data(), b.data(), a.size(), &carry)
               : dotg_add_words_host(out.data(), a.data(), b.data(), a.size(), &carry));
     return carry;
 }
 
-inline WordsResult run_limbs(bool sub, const Limbs& a, const Limbs& b, Width w) {  // addsub.cpp:192-211
+inline WordsResult run_limbs(bool sub, const Limbs& a, const Limbs& b, Width w,
+                             AddSubStats* st) {  // addsub.cpp:192-211
     const std::size_t m = a.size() > b.size() ? a.size() : b.size();
     Limbs pa = a, pb = b;
     pa.resize(m, 0);
     pb.resize(m, 0);
     WordsResult r;
     r.limbs.resize(m);
-    r.flag = run_words(sub, r.limbs, pa, pb, w);
+    r.flag = run_words(sub, r.limbs, pa, pb, w, st);
     return r;
 }
 }  // namespace detail
@@ -86,25 +111,21 @@ inline WordsResult run_limbs(bool sub, const Limbs& a, const Limbs& b, Width w) 
 // out = a + b (mod 2^(64m)); returns the carry (addsub.hpp:98-100).
 inline unsigned dot_add_words(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
                               Width w = Width::w8, AddSubStats* stats = nullptr) {
-    detail::no_stats(stats);
-    return detail::run_words(false, out, a, b, w);
+    return detail::run_words(false, out, a, b, w, stats);
 }
 // out = a - b (mod 2^(64m)); returns the borrow (addsub.hpp:101-103).
 inline unsigned dot_sub_words(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,
                               Width w = Width::w8, AddSubStats* stats = nullptr) {
-    detail::no_stats(stats);
-    return detail::run_words(true, out, a, b, w);
+    return detail::run_words(true, out, a, b, w, stats);
 }
 // Value forms: unequal lengths are zero-padded to the longer one (addsub.hpp:106-109).
 inline WordsResult dot_add_words(const Limbs& a, const Limbs& b, Width w = Width::w8,
                                  AddSubStats* stats = nullptr) {
-    detail::no_stats(stats);
-    return detail::run_limbs(false, a, b, w);
+    return detail::run_limbs(false, a, b, w, stats);
 }
 inline WordsResult dot_sub_words(const Limbs& a, const Limbs& b, Width w = Width::w8,
                                  AddSubStats* stats = nullptr) {
-    detail::no_stats(stats);
-    return detail::run_limbs(true, a, b, w);
+    return detail::run_limbs(true, a, b, w, stats);
 }
 
 // Exact product, exactly 2m limbs; equal lengths 1 <= m <= 2^24 (mul.hpp:75-76).

@@ -153,6 +153,20 @@ int dotg_add_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, siz
 int dotg_sub_words_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                         uint32_t* carry);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation parity with AddSubStats (addsub.hpp:53-72): after out = a +/- b has
+ * been computed, counts the reference's w-limb chunks (w = lane_count(width): 8 for
+ * scalar/w8, 2, 4) and how many of them would have taken the rare Phase 4
+ * (addsub.cpp:48-79). Derived on the device from a, b and out; off the hot path.
+ * counters: DEVICE uint64[2] {chunks_processed, phase4_triggers}, ACCUMULATED into.
+ * ------------------------------------------------------------------------- */
+int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                      size_t batch, int layout, int width, uint64_t* counters, dotg_stream_t stream);
+/* Span form with stats on host spans: out = a +/- b (m limbs), *carry = flag and the two
+ * counters ADDED to *chunks / *fires (AddSubStats semantics). */
+int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                          int width, uint32_t* carry, uint64_t* chunks, uint64_t* fires);
+
 /* Workload setup (not the hot path): out[i] = splitmix64 output for counter
  * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,

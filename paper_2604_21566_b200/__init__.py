@@ -17,6 +17,7 @@ from ._lib import (  # noqa: F401
 )
 from .api import (  # noqa: F401
     K_MAX_MUL_LIMBS,
+    AddSubStats,
     Width,
     WordsResult,
     add_batch,
@@ -37,6 +38,7 @@ from .api import (  # noqa: F401
 from . import api, sharded, workloads  # noqa: F401,E402
 
 __all__ = [
+    "AddSubStats",
     "INTERLEAVED",
     "ROW_MAJOR",
     "DotgCudaError",

@@ -39,6 +39,8 @@ SIGNATURES = {
     "dotg_addsub_grouped_host": (c_int, [_P, c_int]),
     "dotg_add_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
     "dotg_sub_words_host": (c_int, [_P, _P, _P, c_size_t, _P]),
+    "dotg_addsub_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_size_t, c_int, c_int, _P, _P]),
+    "dotg_words_host_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_int, _P, _P, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_kernel_launches": (c_uint64, []),
 }

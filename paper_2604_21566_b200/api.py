@@ -43,6 +43,25 @@ def lane_count(w: int) -> int:
     return 8 if int(w) == 0 else int(w)
 
 
+class AddSubStats:
+    """Counters of the reference's AddSubStats (include/dot/addsub.hpp:53-72) that the
+    device path reproduces: chunks_processed and phase4_triggers (derived on the device,
+    see csrc/stats.cu). Accumulated across calls like the reference. The rdtsc phase
+    ticks (collect_ticks) have no device equivalent and are rejected."""
+
+    def __init__(self):
+        self.chunks_processed = 0
+        self.phase4_triggers = 0
+        self.collect_ticks = False
+
+    def phase4_rate(self) -> float:
+        return self.phase4_triggers / self.chunks_processed if self.chunks_processed else 0.0
+
+    def merge(self, other: "AddSubStats") -> None:
+        self.chunks_processed += other.chunks_processed
+        self.phase4_triggers += other.phase4_triggers
+
+
 class WordsResult(NamedTuple):
     """include/dot/limbs.hpp:28-31: m result limbs plus a carry/borrow flag."""
 
@@ -72,7 +91,7 @@ def _hp(arr: Optional[np.ndarray]):
     return None if arr is None or arr.size == 0 else ctypes.c_void_p(arr.ctypes.data)
 
 
-def _words_span(sub: bool, out: np.ndarray, a, b, width) -> int:
+def _words_span(sub: bool, out: np.ndarray, a, b, width, stats=None) -> int:
     _validate_width(width)
     if not isinstance(out, np.ndarray) or out.dtype != np.uint64 or not out.flags.c_contiguous:
         raise InvalidArgument("out must be a contiguous numpy uint64 array (the caller-owned span)")
@@ -81,12 +100,21 @@ def _words_span(sub: bool, out: np.ndarray, a, b, width) -> int:
     if a.size != b.size or out.size != a.size:
         raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")  # addsub.cpp:139-140
     carry = ctypes.c_uint32(0)
+    if stats is not None:
+        if stats.collect_ticks:
+            raise _lib.DotgError("AddSubStats.collect_ticks (rdtsc phase ticks) has no device equivalent")
+        ch, fi = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(lib().dotg_words_host_stats(int(sub), _hp(out), _hp(a), _hp(b), a.size, int(width),
+                                          ctypes.byref(carry), ctypes.byref(ch), ctypes.byref(fi)))
+        stats.chunks_processed += int(ch.value)
+        stats.phase4_triggers += int(fi.value)
+        return int(carry.value)
     fn = lib().dotg_sub_words_host if sub else lib().dotg_add_words_host
     check(fn(_hp(out), _hp(a), _hp(b), a.size, ctypes.byref(carry)))
     return int(carry.value)
 
 
-def _words_value(sub: bool, a, b, width) -> WordsResult:
+def _words_value(sub: bool, a, b, width, stats=None) -> WordsResult:
     a = _host_u64(a, "a")
     b = _host_u64(b, "b")
     m = max(a.size, b.size)  # addsub.cpp:192-206: zero-pad the shorter operand
@@ -95,7 +123,7 @@ def _words_value(sub: bool, a, b, width) -> WordsResult:
     if b.size != m:
         b = np.concatenate([b, np.zeros(m - b.size, np.uint64)])
     out = np.zeros(m, np.uint64)
-    flag = _words_span(sub, out, a, b, width)
+    flag = _words_span(sub, out, a, b, width, stats)
     return WordsResult(out, flag)
 
 
@@ -110,17 +138,25 @@ def dot_sub_words(*args, width=Width.w8, stats=None):
     return _dispatch_words(True, args, width, stats)
 
 
+def _is_limbs(x) -> bool:
+    return isinstance(x, (np.ndarray, list, tuple))
+
+
 def _dispatch_words(sub: bool, args, width, stats):
-    if stats is not None:
-        raise _lib.DotgError("AddSubStats instrumentation is not provided by the device path")
-    if len(args) == 4:
-        args, width = args[:3], args[3]
-    if len(args) == 3:
-        return _words_span(sub, args[0], args[1], args[2], width)
-    if len(args) == 2:
-        _validate_width(width)
-        return _words_value(sub, args[0], args[1], width)
-    raise TypeError("expected (out, a, b[, width]) or (a, b[, width])")
+    """Positional forms of the reference: (out, a, b[, width[, stats]]) is the span form
+    (the third argument is a limb array), (a, b[, width[, stats]]) the value form."""
+    span = len(args) >= 3 and _is_limbs(args[2])
+    nfix = 3 if span else 2
+    if len(args) < nfix or len(args) > nfix + 2:
+        raise TypeError("expected (out, a, b[, width[, stats]]) or (a, b[, width[, stats]])")
+    if len(args) > nfix:
+        width = args[nfix]
+    if len(args) > nfix + 1:
+        stats = args[nfix + 1]
+    if span:
+        return _words_span(sub, args[0], args[1], args[2], width, stats)
+    _validate_width(width)
+    return _words_value(sub, args[0], args[1], width, stats)
 
 
 def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:

@@ -497,6 +497,69 @@ int dotg_addsub_grouped_host(const dotg_addsub_problem* problems, int n) {
     return run_host_jobs(jobs.data(), int(jobs.size()));
 }
 
+int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                      int layout, int width, uint64_t* counters, dotg_stream_t stream) {
+    int rc = dotg_validate_width(width);
+    if (rc != DOTG_OK) return rc;
+    if (layout != DOTG_ROW_MAJOR && layout != DOTG_INTERLEAVED) return fail(DOTG_EINVAL, "unknown layout");
+    if (counters == nullptr) return fail(DOTG_EINVAL, "stats: null counters");
+    if (m > 0 && batch > 0 && (out == nullptr || a == nullptr || b == nullptr))
+        return fail(DOTG_EINVAL, "stats: null operand");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    const unsigned lanes = width == 0 ? 8u : unsigned(width);
+    cudaError_t e = dotg::launch_addsub_stats(sub != 0, out, a, b, m, batch, layout, lanes, counters,
+                                              static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "stats");
+}
+
+int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, int width,
+                          uint32_t* carry, uint64_t* chunks, uint64_t* fires) {
+    int rc = dotg_validate_width(width);
+    if (rc != DOTG_OK) return rc;
+    if ((rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR)) != DOTG_OK) return rc;
+    if (m == 0) {
+        if (carry) *carry = 0;
+        return DOTG_OK;
+    }
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    cudaStream_t st = g_host.s[0];
+    const size_t ab = align_up(m * 8, 256);
+    const size_t sb = align_up(dotg::long_state_bytes(m), 256);
+    char* base = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * ab + sb + 256, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("stats: ") + cudaGetErrorString(e));
+    uint64_t* da = reinterpret_cast<uint64_t*>(base);
+    uint64_t* db = reinterpret_cast<uint64_t*>(base + ab);
+    uint64_t* dout = reinterpret_cast<uint64_t*>(base + 2 * ab);
+    char* state = base + 3 * ab;
+    uint32_t* agg = reinterpret_cast<uint32_t*>(state + sb);  // agg[0..1], carry agg[2]
+    uint64_t* cnt = reinterpret_cast<uint64_t*>(state + sb + 64);
+    uint64_t hc[2] = {0, 0};
+    uint32_t hcarry = 0;
+    e = cudaMemcpyAsync(da, a, m * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db, b, m * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cnt, 0, 16, st);
+    if (e == cudaSuccess) e = dotg::launch_long_local(sub != 0, dout, da, db, m, state, agg, st);
+    if (e == cudaSuccess) e = dotg::launch_long_finish(sub != 0, dout, m, state, agg, 0, 1, agg + 2, st);
+    if (e == cudaSuccess)
+        e = dotg::launch_addsub_stats(sub != 0, dout, da, db, m, 1, DOTG_ROW_MAJOR, width == 0 ? 8u : unsigned(width),
+                                      cnt, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, m * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hcarry, agg + 2, 4, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaFreeAsync(base, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "stats words");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    if (carry) *carry = hcarry;
+    if (chunks) *chunks += hc[0];
+    if (fires) *fires += hc[1];
+    return DOTG_OK;
+}
+
 int dotg_add_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                         size_t batch) {
     return batch_host(0, out, a, b, flags, m, batch);

@@ -52,6 +52,10 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                              size_t batch, int layout, cudaStream_t stream);
 
+// AddSubStats parity counters (stats.cu): counters = device uint64[2] {chunks, fires}.
+cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                                size_t batch, int layout, unsigned lanes, uint64_t* counters, cudaStream_t st);
+
 // Workload setup: splitmix64 counter fill (util.cu).
 cudaError_t launch_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, cudaStream_t st);
 

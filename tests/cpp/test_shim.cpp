@@ -193,6 +193,40 @@ int main() {
         const WordsResult d = dot_sub_words(Limbs(m, 0), Limbs{1});
         CHECK(d.limbs == Limbs(m, kMax) && d.flag == 1);
     });
+    run("phase 4 never fires on uniform random operands", [] {  // test_addsub.cpp:282-297
+        std::mt19937_64 rng(0x5eedf00du);
+        for (const Width w : {Width::scalar, Width::w2, Width::w4, Width::w8}) {
+            AddSubStats st;
+            for (int iter = 0; iter < 20; ++iter) {
+                const Limbs a = uniform_limbs(rng, 8), b = uniform_limbs(rng, 8);
+                (void)dot_add_words(a, b, w, &st);
+                (void)dot_sub_words(a, b, w, &st);
+            }
+            CHECK(st.phase4_triggers == 0);
+            CHECK(st.chunks_processed == 20u * 2u * (8 / lane_count(w)));
+        }
+    });
+    run("phase 4 fires on every chunk of a full propagation chain", [] {  // 299-317
+        const std::size_t m = 64;
+        Limbs a(m, kMax), b(m, 0);
+        b[0] = 1;
+        for (const Width w : {Width::scalar, Width::w2, Width::w4, Width::w8}) {
+            AddSubStats st;
+            const WordsResult r = dot_add_words(a, b, w, &st);
+            CHECK(r.limbs == Limbs(m, 0) && r.flag == 1);
+            CHECK(st.chunks_processed == m / lane_count(w));
+            CHECK(st.phase4_rate() == 1.0);
+            AddSubStats sb;
+            const WordsResult d = dot_sub_words(Limbs(m, 0), Limbs{1}, w, &sb);
+            CHECK(d.limbs == Limbs(m, kMax) && d.flag == 1);
+            CHECK(sb.phase4_rate() == 1.0);
+        }
+    });
+    run("tick collection is rejected, counters without ticks work", [] {
+        AddSubStats st;
+        st.collect_ticks = true;
+        CHECK_THROWS_AS(dot_add_words(Limbs(4, 1), Limbs(4, 1), Width::w8, &st), std::logic_error);
+    });
     run("one-limb product is exactly the two-limb scalar product", [] {  // test_mul.cpp:323-331
         std::mt19937_64 rng(21);
         for (int iter = 0; iter < 50; ++iter) {

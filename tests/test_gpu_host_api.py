@@ -129,3 +129,58 @@ def test_grouped_host_pipeline(cuda, oracle):
     for op, a, b, out, fl in keep:
         want, wf = oracle.addsub_batch(op, a, b)
         assert np.array_equal(out, want) and np.array_equal(fl, wf)
+
+
+def test_addsub_stats_parity(cuda, oracle):
+    """AddSubStats chunks/phase-4 counters vs the reference's own counts (golden vectors,
+    w8) and the oracle's 4-phase restatement for every width."""
+    import os
+
+    import paper_2604_21566_b200 as dg
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz"))
+    for m in (9, 64, 256):
+        a, b = g[f"addsub_m{m}_a"], g[f"addsub_m{m}_b"]
+        for sub, key in ((False, "add"), (True, "sub")):
+            for i in range(a.shape[0]):
+                st = dg.AddSubStats()
+                out = np.zeros(m, np.uint64)
+                fn = dg.dot_sub_words if sub else dg.dot_add_words
+                c = fn(out, a[i], b[i], dg.Width.w8, st)
+                assert c == g[f"addsub_m{m}_{key}_flag"][i]
+                assert st.chunks_processed == (m + 7) // 8
+                assert st.phase4_triggers == g[f"addsub_m{m}_{key}_p4"][i]
+    rng = np.random.default_rng(4)
+    for w in (0, 2, 4, 8):
+        for m in (1, 7, 33):
+            a, b = spiky(rng, m), spiky(rng, m)
+            for sub in (False, True):
+                st = dg.AddSubStats()
+                r = (dg.dot_sub_words if sub else dg.dot_add_words)(a, b, w, st)
+                o, c, ch, fi = oracle.words(sub, a, b, dg.lane_count(w))
+                assert np.array_equal(r.limbs, o) and r.flag == c
+                assert (st.chunks_processed, st.phase4_triggers) == (ch, fi)
+    # 0 triggers on uniform data, every chunk on a full chain (test_addsub.cpp:282-317)
+    st = dg.AddSubStats()
+    dg.dot_add_words(np.full(64, MAX, np.uint64), np.eye(1, 64, dtype=np.uint64)[0], dg.Width.w8, st)
+    assert st.chunks_processed == 8 and st.phase4_rate() == 1.0
+
+
+def test_batch_stats_device(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(5)
+    a, b = spiky(rng, (500, 24)), spiky(rng, (500, 24))
+    ta = torch.from_numpy(a.view(np.int64)).cuda()
+    tb = torch.from_numpy(b.view(np.int64)).cuda()
+    out, _ = dg.add_batch(ta, tb)
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    dg.api.check(dg.lib().dotg_addsub_stats(0, dg.api._dptr(out), dg.api._dptr(ta), dg.api._dptr(tb), 24, 500, 0, 4,
+                                            dg.api._dptr(cnt), dg.api._stream_handle(None)))
+    want_ch = want_fi = 0
+    for i in range(500):
+        _, _, ch, fi = oracle.words(False, a[i], b[i], 4)
+        want_ch += ch
+        want_fi += fi
+    assert cnt.tolist() == [want_ch, want_fi]
