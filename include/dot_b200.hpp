@@ -144,6 +144,31 @@ inline Limbs dot_mul_words(const Limbs& a, const Limbs& b, RadixConfig cfg = kSa
     return out;
 }
 
+struct KaratsubaConfig {  // mul.hpp:91-93
+    std::size_t theta = 4;
+};
+
+// mul.hpp:95-102: inputs trimmed, unequal lengths padded at entry, result trimmed.
+// Breadth-first on the device (dotg_karatsuba_batch_host).
+inline Limbs karatsuba_mul(const Limbs& a, const Limbs& b, KaratsubaConfig cfg = {}) {
+    if (cfg.theta < 1) throw std::invalid_argument("karatsuba: threshold must be at least 1");
+    auto sig = [](const Limbs& x) {
+        std::size_t n = x.size();
+        while (n > 0 && x[n - 1] == 0) --n;
+        return n;
+    };
+    const std::size_t na = sig(a), nb = sig(b);
+    if (na == 0 || nb == 0) return {};
+    const std::size_t m = na > nb ? na : nb;
+    Limbs pa(a.begin(), a.begin() + na), pb(b.begin(), b.begin() + nb);
+    pa.resize(m, 0);
+    pb.resize(m, 0);
+    Limbs out(2 * m);
+    detail::check(dotg_karatsuba_batch_host(out.data(), pa.data(), pb.data(), m, 1, cfg.theta));
+    out.resize(sig(out));
+    return out;
+}
+
 // Batched extensions (no reference equivalent; one call instead of a loop over pairs):
 // row-major host arrays [batch][m]; flags[batch] may be empty.
 inline void dot_add_batch(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,

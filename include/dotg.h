@@ -99,6 +99,18 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
                    int layout, dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * Batched Karatsuba (reference karatsuba_mul / kara_rec, mul.hpp:87-102,
+ * mul.cpp:161-233): equal-length row-major pairs, exactly 2m output limbs, recursion
+ * until m <= theta (theta >= 1), odd levels zero-padded, base case = the column multiply
+ * (bit-identical to dot_mul_4x4 / dot_mul_words). Breadth-first on the device: one
+ * batched launch per recursion level. Scratch from the stream-ordered allocator.
+ * ------------------------------------------------------------------------- */
+int dotg_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                         size_t theta, dotg_stream_t stream);
+int dotg_karatsuba_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                              size_t theta);
+
+/* ---------------------------------------------------------------------------
  * One long number on one GPU (config 5 at G = 1, and the span form at any m).
  * Replaces: dot_add_words / dot_sub_words span form (addsub.hpp:98-103).
  * carry_out is a DEVICE pointer to one uint32 (may be NULL). Scratch is taken from

@@ -18,6 +18,7 @@ from ._lib import (  # noqa: F401
 from .api import (  # noqa: F401
     K_MAX_MUL_LIMBS,
     AddSubStats,
+    KaratsubaConfig,
     Width,
     WordsResult,
     add_batch,
@@ -28,6 +29,8 @@ from .api import (  # noqa: F401
     dot_add_words,
     dot_mul_words,
     dot_sub_words,
+    karatsuba_batch,
+    karatsuba_mul,
     lane_count,
     mul_batch,
     mul_batch_host,
@@ -39,6 +42,7 @@ from . import api, sharded, workloads  # noqa: F401,E402
 
 __all__ = [
     "AddSubStats",
+    "KaratsubaConfig",
     "INTERLEAVED",
     "ROW_MAJOR",
     "DotgCudaError",
@@ -55,6 +59,8 @@ __all__ = [
     "dot_add_words",
     "dot_mul_words",
     "dot_sub_words",
+    "karatsuba_batch",
+    "karatsuba_mul",
     "kernel_launches",
     "lane_count",
     "lib",

@@ -355,3 +355,54 @@ def add_words(a, b, out=None, carry=None, *, stream=None):
 
 def sub_words(a, b, out=None, carry=None, *, stream=None):
     return words(True, a, b, out, carry, stream=stream)
+
+
+# ---------------------------------------------------------------------------
+# Karatsuba (reference karatsuba_mul, include/dot/mul.hpp:87-102, src/mul.cpp:161-233)
+# ---------------------------------------------------------------------------
+class KaratsubaConfig(NamedTuple):
+    """mul.hpp:91-93: limb count at or below which the base case runs."""
+
+    theta: int = 4
+
+
+def karatsuba_mul(a, b, cfg: KaratsubaConfig = KaratsubaConfig()) -> np.ndarray:
+    """Reference semantics: inputs trimmed, unequal lengths zero-padded to the longer,
+    empty/zero operand -> empty result, result trimmed (mul.cpp:222-233). The product
+    runs on the device (dotg_karatsuba_batch_host)."""
+    theta = int(cfg.theta if isinstance(cfg, KaratsubaConfig) else cfg)
+    if theta < 1:
+        raise InvalidArgument("karatsuba: threshold must be at least 1")
+    a = _trim(_host_u64(a, "a"))
+    b = _trim(_host_u64(b, "b"))
+    if a.size == 0 or b.size == 0:
+        return np.zeros(0, np.uint64)
+    m = max(a.size, b.size)
+    pa = np.zeros(m, np.uint64)
+    pb = np.zeros(m, np.uint64)
+    pa[:a.size] = a
+    pb[:b.size] = b
+    out = np.zeros(2 * m, np.uint64)
+    check(lib().dotg_karatsuba_batch_host(_hp(out), _hp(pa), _hp(pb), m, 1, theta))
+    return _trim(out)
+
+
+def karatsuba_batch(a, b, out=None, *, theta: int = 4, stream=None):
+    """Device batch form: row-major [batch, m] tensors -> [batch, 2m] (untrimmed)."""
+    torch = _torch()
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.shape != b.shape or a.dim() != 2:
+        raise InvalidArgument("dot mul: operand shapes differ")
+    batch, m = a.shape
+    if out is None:
+        out = torch.empty((batch, 2 * m), dtype=a.dtype, device=a.device)
+    _check_dev(out, "out")
+    check(lib().dotg_karatsuba_batch(_dptr(out), _dptr(a), _dptr(b), m, batch, int(theta), _stream_handle(stream)))
+    return out
+
+
+def _trim(x: np.ndarray) -> np.ndarray:
+    """normalized() (src/limbs.cpp:40-44): drop high zero limbs."""
+    nz = np.flatnonzero(x)
+    return x[: nz[-1] + 1].copy() if nz.size else np.zeros(0, np.uint64)

@@ -52,6 +52,10 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                              size_t batch, int layout, cudaStream_t stream);
 
+// Breadth-first batched Karatsuba over the column multiply (karatsuba.cu).
+cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                   size_t theta, cudaStream_t st);
+
 // AddSubStats parity counters (stats.cu): counters = device uint64[2] {chunks, fires}.
 cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                                 size_t batch, int layout, unsigned lanes, uint64_t* counters, cudaStream_t st);

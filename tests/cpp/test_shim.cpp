@@ -282,6 +282,20 @@ int main() {
         CHECK_THROWS_AS(dot_mul_words(Limbs{}, Limbs{}), std::invalid_argument);
         CHECK_THROWS_AS(dot_mul_words(Limbs{1}, Limbs{1}, RadixConfig{40}), std::invalid_argument);
     });
+    run("karatsuba matches the oracle across thresholds and sizes", [] {  // test_mul.cpp:429-442
+        std::mt19937_64 rng(28);
+        const std::size_t sizes[] = {1, 2, 3, 4, 5, 7, 9, 16, 23, 33, 64, 100};
+        for (const std::size_t theta : {1u, 2u, 4u, 8u}) {
+            for (const std::size_t m : sizes) {
+                const Limbs a = uniform_limbs(rng, m), b = uniform_limbs(rng, m);
+                Limbs want = oracle_mul_padded(a, b);
+                while (!want.empty() && want.back() == 0) want.pop_back();
+                CHECK(karatsuba_mul(a, b, {.theta = theta}) == want);
+            }
+        }
+        CHECK(karatsuba_mul(Limbs{1, 2}, Limbs{}).empty());
+        CHECK_THROWS_AS(karatsuba_mul(Limbs{1}, Limbs{1}, {.theta = 0}), std::invalid_argument);
+    });
     run("batched extension matches the span form", [] {
         std::mt19937_64 rng(99);
         const std::size_t m = 64, B = 3000;

@@ -1,0 +1,71 @@
+"""Batched Karatsuba on the B200 vs the oracle - the reference's own Karatsuba tests
+(test_mul.cpp:417-474) restated: degeneration at theta, thresholds {1,2,4,8} x sizes up
+to 128 limbs, unequal lengths, the default threshold on 512-bit operands, spiky operands."""
+import numpy as np
+import pytest
+
+from helpers import MAX, spiky, uniform
+
+pytestmark = pytest.mark.gpu
+
+
+def test_zero_and_degeneration(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    rng = np.random.default_rng(27)
+    a = uniform(rng, 12)
+    assert dg.karatsuba_mul(a, np.zeros(0, np.uint64)).size == 0
+    assert dg.karatsuba_mul(np.zeros(0, np.uint64), a).size == 0
+    assert dg.karatsuba_mul(a, np.zeros(12, np.uint64)).size == 0
+    want = oracle.mul(a, a)
+    assert np.array_equal(dg.karatsuba_mul(a, a, dg.KaratsubaConfig(theta=12)), want)
+    assert np.array_equal(dg.karatsuba_mul(a, a, dg.KaratsubaConfig(theta=64)), want)
+    with pytest.raises(dg.InvalidArgument):
+        dg.karatsuba_mul(a, a, dg.KaratsubaConfig(theta=0))
+
+
+@pytest.mark.parametrize("theta", [1, 2, 4, 8])
+def test_matches_oracle_across_thresholds(cuda, oracle, theta):
+    import paper_2604_21566_b200 as dg
+
+    rng = np.random.default_rng(28 + theta)
+    for m in (1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 16, 23, 31, 32, 33, 64, 100, 128):
+        for _ in range(3 if m <= 16 else 2):
+            a, b = uniform(rng, m), uniform(rng, m)
+            assert np.array_equal(dg.karatsuba_mul(a, b, dg.KaratsubaConfig(theta)), oracle.mul(a, b)), (theta, m)
+
+
+def test_unequal_lengths_and_default(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    rng = np.random.default_rng(29)
+    for _ in range(40):
+        a, b = uniform(rng, 1 + int(rng.integers(24))), uniform(rng, 1 + int(rng.integers(24)))
+        assert np.array_equal(dg.karatsuba_mul(a, b), oracle.mul(a, b))
+    for _ in range(40):
+        a, b = uniform(rng, 8), uniform(rng, 8)
+        assert np.array_equal(dg.karatsuba_mul(a, b), oracle.mul(a, b))
+
+
+def test_spiky_and_all_ones(cuda, oracle):
+    import paper_2604_21566_b200 as dg
+
+    rng = np.random.default_rng(31)
+    for it in range(60):
+        m = 1 + int(rng.integers(40))
+        a, b = spiky(rng, m), spiky(rng, m)
+        theta = 1 + it % 8
+        assert np.array_equal(dg.karatsuba_mul(a, b, dg.KaratsubaConfig(theta)), oracle.mul(a, b))
+    ones = np.full(64, MAX, np.uint64)
+    assert np.array_equal(dg.karatsuba_mul(ones, ones, dg.KaratsubaConfig(2)), oracle.mul(ones, ones))
+
+
+def test_device_batch_equals_column_multiply(cuda):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(32)
+    for m, theta in ((64, 16), (64, 32), (100, 8), (256, 32)):
+        a = torch.from_numpy(spiky(rng, (300, m)).view(np.int64)).cuda()
+        b = torch.from_numpy(spiky(rng, (300, m)).view(np.int64)).cuda()
+        assert torch.equal(dg.karatsuba_batch(a, b, theta=theta), dg.mul_batch(a, b)), (m, theta)
