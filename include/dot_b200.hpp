@@ -11,8 +11,8 @@
 // Differences, by design:
 //   * AddSubStats (addsub.hpp:53-72): chunks_processed / phase4_triggers are produced
 //     (derived on the device); the rdtsc phase ticks are not (collect_ticks throws).
-//   * Only the saturated 64-bit radix is on the device path (RadixConfig{52} throws
-//     std::logic_error; the 52-bit 4x4/5x5 route is out of scope).
+//   * dot_mul_4x4 computes the 64-bit product directly (the reference routes it through
+//     52-bit repacking and dot_mul_5x5; the 8 result limbs are identical).
 //   * Partial aliasing of out with a/b (undefined in the reference) throws.
 #pragma once
 
@@ -133,14 +133,54 @@ inline Limbs dot_mul_words(const Limbs& a, const Limbs& b, RadixConfig cfg = kSa
                            Width w = Width::w8) {
     if (cfg.limb_bits != 64 && cfg.limb_bits != 52)
         throw std::invalid_argument("RadixConfig: limb_bits must be 64 or 52");
-    if (cfg.limb_bits != 64) throw std::logic_error("the 52-bit radix is not on the B200 path");
     detail::validate(w);
     if (a.size() != b.size()) throw std::invalid_argument("dot mul: operand lengths differ (caller pads)");
     if (a.empty()) throw std::invalid_argument("dot mul: operands need at least one limb");
     if (a.size() > kMaxMulLimbs)
         throw std::invalid_argument("dot mul: limb count exceeds the column accumulator bound");
     Limbs out(2 * a.size());
-    detail::check(dotg_mul_batch_host(out.data(), a.data(), b.data(), a.size(), 1));
+    if (cfg.limb_bits == 52)  // unsaturated radix: limbs < 2^52 (checked), 2m limbs < 2^52
+        detail::check(dotg_mul52_batch_host(out.data(), a.data(), b.data(), a.size(), 1));
+    else
+        detail::check(dotg_mul_batch_host(out.data(), a.data(), b.data(), a.size(), 1));
+    return out;
+}
+
+// Fixed 5-limb product over 52-bit limbs, exactly 10 limbs (mul.hpp:78-80).
+inline Limbs dot_mul_5x5(const Limbs& a, const Limbs& b) {
+    if (a.size() != 5 || b.size() != 5) throw std::invalid_argument("dot mul 5x5: operands must be exactly 5 limbs");
+    return dot_mul_words(a, b, kUnsaturated);
+}
+
+// Fixed 4-limb product, exactly 8 limbs (mul.hpp:82-85).
+inline Limbs dot_mul_4x4(const Limbs& a, const Limbs& b) {
+    if (a.size() != 4 || b.size() != 4) throw std::invalid_argument("dot mul 4x4: operands must be exactly 4 limbs");
+    return dot_mul_words(a, b);
+}
+
+// 64 <-> 52-bit re-slicing (limbs.hpp:111-117); host representation helpers.
+inline Limbs pack_64_to_52(const Limbs& a) {
+    const std::size_t n = (a.size() * 64 + 51) / 52;
+    Limbs out(n);
+    for (std::size_t j = 0; j < n; ++j) {
+        const std::size_t bit = j * 52, word = bit / 64;
+        const unsigned off = unsigned(bit % 64);
+        limb_t v = a[word] >> off;
+        if (off > 12 && word + 1 < a.size()) v |= a[word + 1] << (64 - off);
+        out[j] = v & ((limb_t(1) << 52) - 1);
+    }
+    return out;
+}
+inline Limbs unpack_52_to_64(const Limbs& a) {
+    Limbs out((a.size() * 52 + 63) / 64, 0);
+    for (std::size_t j = 0; j < a.size(); ++j) {
+        if (a[j] >> 52) throw std::invalid_argument("limb " + std::to_string(j) + " exceeds the configured limb width");
+        const std::size_t bit = j * 52, word = bit / 64;
+        const unsigned off = unsigned(bit % 64);
+        out[word] |= a[j] << off;
+        if (off > 12) out[word + 1] |= a[j] >> (64 - off);
+    }
+    while (!out.empty() && out.back() == 0) out.pop_back();
     return out;
 }
 

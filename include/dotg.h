@@ -98,6 +98,12 @@ int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_
 int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                    int layout, dotg_stream_t stream);
 
+/* Unsaturated 52-bit radix (RadixConfig kUnsaturated): dot_mul_words(a, b, kUnsaturated)
+ * and dot_mul_5x5 (mul.hpp:73-85, mul.cpp:38-90, 127-150). Host row-major arrays; every
+ * limb must be < 2^52 (check_limbs, limbs.cpp:26-33 -> DOTG_EINVAL); exactly 2m output
+ * limbs, each < 2^52. */
+int dotg_mul52_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch);
+
 /* ---------------------------------------------------------------------------
  * Batched Karatsuba (reference karatsuba_mul / kara_rec, mul.hpp:87-102,
  * mul.cpp:161-233): equal-length row-major pairs, exactly 2m output limbs, recursion

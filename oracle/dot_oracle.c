@@ -195,3 +195,25 @@ static uint64_t splitmix64_at(uint64_t seed, uint64_t k) {
 void dotor_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset) {
     for (size_t i = 0; i < n; ++i) out[i] = splitmix64_at(seed, offset + i + 1);
 }
+
+/* dot_mul_words at k = 52 (RadixConfig kUnsaturated; mul.cpp:38-90): low halves of every
+ * 52x52-bit product into column c, high halves (>> 52) into c + 1, carry pass in radix
+ * 2^52. Writes exactly 2m limbs, each < 2^52. Inputs must be < 2^52 (caller checks). */
+void dotor_mul_columns52(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m) {
+    const uint64_t mask = ((uint64_t)1 << 52) - 1;
+    const size_t ncol = 2 * m;
+    u128* col = (u128*)calloc(ncol, sizeof(u128));
+    for (size_t i = 0; i < m; ++i)
+        for (size_t j = 0; j < m; ++j) {
+            const u128 p = (u128)a[i] * b[j];
+            col[i + j] += (uint64_t)p & mask;
+            col[i + j + 1] += (uint64_t)(p >> 52);
+        }
+    u128 carry = 0;
+    for (size_t c = 0; c < ncol; ++c) {
+        const u128 v = col[c] + carry;
+        out[c] = (uint64_t)v & mask;
+        carry = v >> 52;
+    }
+    free(col);
+}

@@ -46,6 +46,9 @@ unsigned dotor_words(int sub, uint64_t* out, const uint64_t* a, const uint64_t* 
  * k=64 (38-52), align_and_reduce (54-68), carry_pass (70-90). Writes exactly 2m limbs. */
 void dotor_mul_columns(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m);
 
+/* dot_mul_words(a, b, kUnsaturated) (mul.cpp:38-90 at k = 52): exactly 2m limbs < 2^52. */
+void dotor_mul_columns52(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m);
+
 /* compare (src/limbs.cpp:46-53): -1 / 0 / +1 ignoring high zero limbs. */
 int dotor_compare(const uint64_t* a, size_t ma, const uint64_t* b, size_t mb);
 

@@ -113,6 +113,48 @@ int dotref_mul_words(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, s
     });
 }
 
+// 52-bit radix routes (mul.hpp:73-85): dot_mul_words(kUnsaturated), dot_mul_5x5,
+// dot_mul_4x4, and the repacking helpers (limbs.hpp:111-117). Return the output length.
+int dotref_mul_words52(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {
+    return guarded([&] {
+        const Limbs r = dot::dot_mul_words(Limbs(a, a + ma), Limbs(b, b + mb), dot::kUnsaturated);
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+int dotref_mul_5x5(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {
+    return guarded([&] {
+        const Limbs r = dot::dot_mul_5x5(Limbs(a, a + ma), Limbs(b, b + mb));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+int dotref_mul_4x4(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {
+    return guarded([&] {
+        const Limbs r = dot::dot_mul_4x4(Limbs(a, a + ma), Limbs(b, b + mb));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+int dotref_pack_64_to_52(limb_t* out, const limb_t* a, size_t m) {
+    return guarded([&] {
+        const Limbs r = dot::pack_64_to_52(Limbs(a, a + m));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
+int dotref_unpack_52_to_64(limb_t* out, const limb_t* a, size_t m) {
+    return guarded([&] {
+        const Limbs r = dot::unpack_52_to_64(Limbs(a, a + m));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
 int dotref_oracle_addsub(int sub, limb_t* out, const limb_t* a, size_t ma, const limb_t* b,
                          size_t mb) {
     return guarded([&] {

@@ -165,8 +165,7 @@ def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
     on the device path (the 52-bit route is out of scope)."""
     if int(cfg) not in (64, 52):
         raise InvalidArgument("RadixConfig: limb_bits must be 64 or 52")  # limbs.cpp:22-24
-    if int(cfg) != 64:
-        raise _lib.DotgError("the 52-bit (unsaturated) radix is not on the B200 path")
+    _validate_width(width)
     a = _host_u64(a, "a")
     b = _host_u64(b, "b")
     if a.size != b.size:
@@ -176,8 +175,53 @@ def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
     if a.size > K_MAX_MUL_LIMBS:
         raise InvalidArgument("dot mul: limb count exceeds the column accumulator bound")
     out = np.zeros(2 * a.size, np.uint64)
-    check(lib().dotg_mul_batch_host(_hp(out), _hp(a), _hp(b), a.size, 1))
+    if int(cfg) == 52:
+        check(lib().dotg_mul52_batch_host(_hp(out), _hp(a), _hp(b), a.size, 1))
+    else:
+        check(lib().dotg_mul_batch_host(_hp(out), _hp(a), _hp(b), a.size, 1))
     return out
+
+
+def dot_mul_5x5(a, b) -> np.ndarray:
+    """Fixed 5-limb product over unsaturated 52-bit limbs, exactly 10 limbs
+    (mul.hpp:78-80, mul.cpp:127-150)."""
+    a, b = _host_u64(a, "a"), _host_u64(b, "b")
+    if a.size != 5 or b.size != 5:
+        raise InvalidArgument("dot mul 5x5: operands must be exactly 5 limbs")
+    return dot_mul_words(a, b, 52)
+
+
+def dot_mul_4x4(a, b) -> np.ndarray:
+    """Fixed 4-limb product over saturated limbs, exactly 8 limbs (mul.hpp:82-85,
+    mul.cpp:152-159; the reference routes it through 52-bit repacking and the 5x5
+    kernel, the device computes it directly - identical result)."""
+    a, b = _host_u64(a, "a"), _host_u64(b, "b")
+    if a.size != 4 or b.size != 4:
+        raise InvalidArgument("dot mul 4x4: operands must be exactly 4 limbs")
+    return dot_mul_words(a, b)
+
+
+def pack_64_to_52(a) -> np.ndarray:
+    """limbs.hpp:111-113: re-slice 64m bits into ceil(64m/52) 52-bit groups (host-side
+    representation helper, not arithmetic)."""
+    a = _host_u64(a, "a")
+    n = (64 * a.size + 51) // 52
+    v = int.from_bytes(a.astype("<u8").tobytes(), "little")
+    return np.array([(v >> (52 * i)) & ((1 << 52) - 1) for i in range(n)], dtype=np.uint64)
+
+
+def unpack_52_to_64(a) -> np.ndarray:
+    """limbs.hpp:115-117: inverse re-slicing, trims high zero words so a pack round trip
+    returns the original limb count; any word >= 2^52 is std::invalid_argument."""
+    a = _host_u64(a, "a")
+    if a.size and int(a.max()) >= (1 << 52):
+        raise InvalidArgument("unpack_52_to_64: word exceeds 52 bits")
+    v = 0
+    for i in range(a.size - 1, -1, -1):
+        v = (v << 52) | int(a[i])
+    n = (52 * a.size + 63) // 64
+    out = np.array([(v >> (64 * i)) & ((1 << 64) - 1) for i in range(n)], dtype=np.uint64)
+    return _trim(out)
 
 
 # ---------------------------------------------------------------------------

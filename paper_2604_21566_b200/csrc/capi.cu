@@ -441,6 +441,36 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg mul batch launch");
 }
 
+int dotg_mul52_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch) {
+    int rc = check_mul(out, a, b, m, batch, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    const uint64_t kHead = ~((uint64_t(1) << 52) - 1);
+    for (size_t i = 0; i < m * batch; ++i)  // check_limbs (limbs.cpp:26-33)
+        if ((a[i] | b[i]) & kHead)
+            return fail(DOTG_EINVAL, "limb " + std::to_string(i % m) + " exceeds the configured limb width");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    cudaStream_t st = g_host.s[0];
+    const size_t ib = align_up(m * batch * 8, 256);
+    char* base = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 4 * ib, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("mul52: ") + cudaGetErrorString(e));
+    uint64_t* da = reinterpret_cast<uint64_t*>(base);
+    uint64_t* db = reinterpret_cast<uint64_t*>(base + ib);
+    uint64_t* dout = reinterpret_cast<uint64_t*>(base + 2 * ib);
+    e = cudaMemcpyAsync(da, a, m * batch * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db, b, m * batch * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = dotg::launch_mul52_batch(dout, da, db, m, batch, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, 2 * m * batch * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaFreeAsync(base, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "dotg mul52");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    return DOTG_OK;
+}
+
 int dotg_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, size_t theta,
                          dotg_stream_t stream) {
     if (theta < 1) return fail(DOTG_EINVAL, "karatsuba: threshold must be at least 1");  // mul.cpp:223-224

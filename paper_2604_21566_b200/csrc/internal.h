@@ -52,6 +52,10 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                              size_t batch, int layout, cudaStream_t stream);
 
+// Unsaturated 52-bit radix product (row-major, limbs < 2^52, exactly 2m limbs out).
+cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st);
+
 // Breadth-first batched Karatsuba over the column multiply (karatsuba.cu).
 cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                    size_t theta, cudaStream_t st);

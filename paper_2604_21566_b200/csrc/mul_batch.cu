@@ -434,7 +434,47 @@ cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, siz
 
 bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
+// ---------------------------------------------------------------------------
+// Unsaturated 52-bit radix (RadixConfig kUnsaturated, limbs.hpp:39-49): the generic
+// pipeline at k = 52 (mul.cpp:38-90) and the fixed 5x5 route (mul.cpp:127-150): every
+// 52x52-bit product splits at bit 52, low half into column c, high half into c + 1,
+// then one carry pass in radix 2^52. Thread per pair, 128-bit column accumulators
+// (a column of m pairs sums below 2m * 2^52). Exactly 2m output limbs, each < 2^52.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_mul52(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
+                                               size_t batch) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= batch) return;
+    const uint64_t* pa = a + p * m;
+    const uint64_t* pb = b + p * m;
+    uint64_t* po = out + p * 2 * m;
+    constexpr uint64_t kMask = (uint64_t(1) << 52) - 1;
+    typedef unsigned __int128 u128;
+    u128 carry = 0;
+    for (size_t c = 0; c < 2 * m; ++c) {
+        u128 col = carry;
+        // low halves of column c, high halves of column c - 1
+        const size_t i0 = c + 1 > m ? c + 1 - m : 0, i1 = c < m - 1 ? c : m - 1;
+        for (size_t i = i0; i <= i1 && c + 1 < 2 * m; ++i) col += uint64_t(u128(pa[i]) * pb[c - i]) & kMask;
+        if (c >= 1) {
+            const size_t d = c - 1;
+            const size_t j0 = d + 1 > m ? d + 1 - m : 0, j1 = d < m - 1 ? d : m - 1;
+            for (size_t i = j0; i <= j1; ++i) col += uint64_t((u128(pa[i]) * pb[d - i]) >> 52);
+        }
+        po[c] = uint64_t(col) & kMask;
+        carry = col >> 52;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    k_mul52<<<unsigned((batch + 127) / 128), 128, 0, st>>>(out, a, b, m, batch);
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                              int layout, cudaStream_t stream) {

@@ -296,6 +296,39 @@ int main() {
         CHECK(karatsuba_mul(Limbs{1, 2}, Limbs{}).empty());
         CHECK_THROWS_AS(karatsuba_mul(Limbs{1}, Limbs{1}, {.theta = 0}), std::invalid_argument);
     });
+    run("5x5 / 4x4 / 52-bit radix routes", [] {  // test_mul.cpp:258-317
+        std::mt19937_64 rng(18);
+        const limb_t mask52 = (limb_t(1) << 52) - 1;
+        for (int iter = 0; iter < 200; ++iter) {
+            Limbs a(5), b(5);
+            for (auto& x : a) x = rng() & mask52;
+            for (auto& x : b) x = rng() & mask52;
+            const Limbs got = dot_mul_5x5(a, b);
+            CHECK(got.size() == 10);
+            Limbs want = oracle_mul_padded(unpack_52_to_64(a), unpack_52_to_64(b));
+            while (!want.empty() && want.back() == 0) want.pop_back();
+            CHECK(unpack_52_to_64(got) == want);
+        }
+        const Limbs ones(4, kMax);
+        const Limbs sq = dot_mul_4x4(ones, ones);
+        CHECK(sq.size() == 8 && sq[0] == 1 && sq[4] == kMax - 1 && sq[7] == kMax);
+        std::mt19937_64 r2(19);
+        Limbs x(4);
+        for (auto& v : x) v = r2();
+        const Limbs one_prod = dot_mul_4x4(x, Limbs{1, 0, 0, 0});
+        CHECK(Limbs(one_prod.begin(), one_prod.begin() + 4) == x);
+        Limbs bad(5, 1);
+        bad[2] = limb_t(1) << 52;
+        CHECK_THROWS_AS(dot_mul_5x5(bad, Limbs(5, 1)), std::invalid_argument);
+        CHECK_THROWS_AS(dot_mul_5x5(Limbs(4, 1), Limbs(5, 1)), std::invalid_argument);
+        CHECK_THROWS_AS(dot_mul_words(Limbs{kMax}, Limbs{1}, kUnsaturated), std::invalid_argument);
+        for (std::size_t m : {1u, 3u, 4u, 9u}) {
+            Limbs y(m);
+            for (auto& v : y) v = r2();
+            y.back() |= 1;
+            CHECK(unpack_52_to_64(pack_64_to_52(y)) == y);
+        }
+    });
     run("batched extension matches the span form", [] {
         std::mt19937_64 rng(99);
         const std::size_t m = 64, B = 3000;

@@ -18,7 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 
-from helpers import CATEGORIES, Reference, category, spiky  # noqa: E402
+from helpers import CATEGORIES, Reference, category, spiky, uniform  # noqa: E402
 
 ADDSUB_SIZES = [1, 2, 3, 4, 5, 7, 8, 9, 13, 16, 17, 31, 32, 33, 64, 65, 128, 256]
 MUL_SIZES = [1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 33, 48, 64]
@@ -90,6 +90,32 @@ def main():
         out[f"chunk_w{w}_a"] = a
         out[f"chunk_w{w}_b"] = b
         out[f"chunk_w{w}_cin"] = cin
+    # 52-bit radix routes (mul.hpp:73-85) and the 64<->52 repacking (limbs.hpp:111-117)
+    mask52 = np.uint64((1 << 52) - 1)
+    for m in (1, 2, 3, 5, 8, 20):
+        a = uniform(rng, (12, m)) & mask52
+        b = uniform(rng, (12, m)) & mask52
+        a[0] = mask52
+        b[0] = mask52
+        out["mul52_m%d_a" % m] = a
+        out["mul52_m%d_b" % m] = b
+        out["mul52_m%d_out" % m] = np.array([ref.mul2("dotref_mul_words52", a[i], b[i], 2 * m) for i in range(12)],
+                                            dtype=np.uint64)
+    a5 = uniform(rng, (20, 5)) & mask52
+    b5 = uniform(rng, (20, 5)) & mask52
+    out["mul5x5_a"], out["mul5x5_b"] = a5, b5
+    out["mul5x5_out"] = np.array([ref.mul2("dotref_mul_5x5", a5[i], b5[i], 10) for i in range(20)], dtype=np.uint64)
+    a4, b4 = uniform(rng, (20, 4)), uniform(rng, (20, 4))
+    a4[0] = ~np.uint64(0)
+    b4[0] = ~np.uint64(0)
+    out["mul4x4_a"], out["mul4x4_b"] = a4, b4
+    out["mul4x4_out"] = np.array([ref.mul2("dotref_mul_4x4", a4[i], b4[i], 8) for i in range(20)], dtype=np.uint64)
+    for m in (1, 3, 4, 7, 13):
+        x = uniform(rng, m)
+        p = ref.repack("dotref_pack_64_to_52", x)
+        out["pack_m%d_in" % m] = x
+        out["pack_m%d_out" % m] = p
+        out["pack_m%d_back" % m] = ref.repack("dotref_unpack_52_to_64", p)
     meta = {"dispatch_note_w8": ref.dispatch_note(8)}
     out["meta_dispatch_note_w8"] = np.frombuffer(meta["dispatch_note_w8"].encode(), dtype=np.uint8)
     path = os.path.join(HERE, "reference_vectors.npz")

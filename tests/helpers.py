@@ -54,6 +54,8 @@ class Oracle:
         L.dotor_addsub_batch.argtypes = [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t]
         L.dotor_mul_batch.restype = None
         L.dotor_mul_batch.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t, c_size_t]
+        L.dotor_mul_columns52.restype = None
+        L.dotor_mul_columns52.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t]
         L.dotor_fill_splitmix64.restype = None
         L.dotor_fill_splitmix64.argtypes = [c_void_p, c_size_t, c_uint64, c_uint64]
         self.L = L
@@ -86,6 +88,12 @@ class Oracle:
         a, b = u64(a), u64(b)
         out = np.zeros(2 * a.size, U64)
         self.L.dotor_mul_columns(_p(out), _p(a), _p(b), a.size)
+        return out
+
+    def mul_columns52(self, a, b):
+        a, b = u64(a), u64(b)
+        out = np.zeros(2 * a.size, U64)
+        self.L.dotor_mul_columns52(_p(out), _p(a), _p(b), a.size)
         return out
 
     def chunk(self, sub, a, b, cin, t):
@@ -156,6 +164,12 @@ class Reference:
         L.dotref_oracle_mul.argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t]
         L.dotref_batch.restype = c_int
         L.dotref_batch.argtypes = [c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_int]
+        for fn in ("dotref_mul_words52", "dotref_mul_5x5", "dotref_mul_4x4"):
+            getattr(L, fn).restype = c_int
+            getattr(L, fn).argtypes = [c_void_p, c_void_p, c_size_t, c_void_p, c_size_t]
+        for fn in ("dotref_pack_64_to_52", "dotref_unpack_52_to_64"):
+            getattr(L, fn).restype = c_int
+            getattr(L, fn).argtypes = [c_void_p, c_void_p, c_size_t]
         L.dotref_dispatch_note.restype = ctypes.c_char_p
         L.dotref_dispatch_note.argtypes = [c_int]
         L.dotref_last_error.restype = ctypes.c_char_p
@@ -188,6 +202,22 @@ class Reference:
         a, b = u64(a), u64(b)
         out = np.zeros(2 * max(a.size, 1), U64)
         n = self.L.dotref_mul_words(_p(out), _p(a), a.size, _p(b), b.size)
+        if n < 0:
+            raise ValueError(self.L.dotref_last_error().decode())
+        return out[:n].copy()
+
+    def mul2(self, fn, a, b, cap):
+        a, b = u64(a), u64(b)
+        out = np.zeros(cap, U64)
+        n = getattr(self.L, fn)(_p(out), _p(a), a.size, _p(b), b.size)
+        if n < 0:
+            raise ValueError(self.L.dotref_last_error().decode())
+        return out[:n].copy()
+
+    def repack(self, fn, a):
+        a = u64(a)
+        out = np.zeros(2 * a.size + 2, U64)
+        n = getattr(self.L, fn)(_p(out), _p(a), a.size)
         if n < 0:
             raise ValueError(self.L.dotref_last_error().decode())
         return out[:n].copy()
