@@ -1,0 +1,50 @@
+"""dotg-verify on a reference-format JSONL corpus (tests/golden/corpus_small.jsonl, made
+by tests/golden/make_corpus.py with the reference's oracle): all cases match; a corrupted
+corpus reports the mismatching case ids with exit code 1; malformed input exits 2
+(the reference's dotarith verify behaviour, test_cli.cpp:142-165)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOOL = os.path.join(ROOT, "tools", "build", "dotg-verify")
+CORPUS = os.path.join(ROOT, "tests", "golden", "corpus_small.jsonl")
+
+
+def run(*args):
+    if not os.path.exists(TOOL):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "tools")], check=True)
+    return subprocess.run([TOOL, *args], capture_output=True, text=True, timeout=300)
+
+
+def test_corpus_verifies(cuda):
+    r = run("verify", CORPUS)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "216 cases, 0 mismatches" in r.stdout
+
+
+def test_corrupted_corpus_reports_ids(cuda, tmp_path):
+    lines = open(CORPUS).read().splitlines()
+    for i in (3, 100, 200):  # flip the last hex digit of the expected value
+        head, exp_tail = lines[i].split('"expected":"')
+        val, rest = exp_tail.split('"', 1)
+        val = val[:-1] + ("0" if val[-1] != "0" else "1")
+        lines[i] = head + '"expected":"' + val + '"' + rest
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text("\n".join(lines) + "\n")
+    r = run("verify", str(bad))
+    assert r.returncode == 1
+    assert "3 mismatches" in r.stdout
+    for i in (3, 100, 200):
+        assert f"mismatch at case {i}" in r.stdout
+
+
+def test_malformed_input(cuda, tmp_path):
+    p = tmp_path / "broken.jsonl"
+    p.write_text('{"op":"add","bits":100,"category":"random","a":"1","b":"2","expected":"3","flag":0}\n')
+    r = run("verify", str(p))
+    assert r.returncode == 2 and "parse error at line 1" in r.stderr
+    assert run("verify", str(tmp_path / "missing.jsonl")).returncode == 2
+    assert run("verify", CORPUS, "--width", "16").returncode == 2
