@@ -1,4 +1,4 @@
-for v in 0 3 4; do echo "V=$v"; DOTG_MUL64=$v python bench.py --only C4 --steps 10 --warmup 3 --no-e2e 2>&1 | python -c "
+for v in 1 2; do echo "V=$v"; DOTG_MUL64=$v python bench.py --only C4 --steps 10 --warmup 3 --no-e2e 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
