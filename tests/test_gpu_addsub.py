@@ -41,6 +41,20 @@ def test_batch_matches_oracle(cuda, oracle, m):
                 assert np.array_equal(gf, wf), (m, cat, op, layout)
 
 
+@pytest.mark.parametrize("m,batch", [(128, 128), (200, 130), (256, 64), (256, 190), (129, 66)])
+def test_interleaved_segmented(cuda, oracle, m, batch):
+    # even batches take the 128-bit vector loads of k_addsub_interleaved, ragged m the
+    # partial last segment, batch % 64 != 0 the partial last CTA
+    rng = np.random.default_rng(7000 + m + batch)
+    for cat in CATEGORIES:
+        for op in ("add", "sub"):
+            a, b = category(rng, cat, op, (batch, m))
+            want, wf = oracle.addsub_batch(op == "sub", a, b)
+            got, gf = run(cuda, op == "sub", a, b, "interleaved")
+            assert np.array_equal(got, want), (m, batch, cat, op)
+            assert np.array_equal(gf, wf), (m, batch, cat, op)
+
+
 def test_golden_replay(cuda):
     g = np.load(GOLDEN)
     sizes = sorted({int(k.split("_")[1][1:]) for k in g.files if k.startswith("addsub_")})
