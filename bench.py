@@ -38,6 +38,8 @@ sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 IMAD_WIDE_PER_CLK_SM = 32.0  # measured: profiles/r01_imad_peak.json (cc_chain_products)
+IMMA_U8_MACS_PER_CLK_SM = 2048.0  # measured: profiles/r01_imma_peak.json (mma.sync m16n8k32 u8)
+IMMA_ROUTE_M = (32, 64, 128)  # m the library multiplies on the tensor pipe (mul_batch.cu)
 C2_SIZES = [(4, 1 << 20), (16, 1 << 18), (64, 1 << 16), (256, 1 << 14)]
 METRIC = "add/sub GB/s vs HBM peak (C2 carry-stress sweep, 4/16/64/256 limbs)"
 DATA = ("synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: limb all-ones p=0.5 else uniform, "
@@ -558,6 +560,18 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
                      "frac_imad": pairs_s * prods / imad_peak_pps,
                      "hbm_gbs": Bn * 32 * m / (per[0] * 1e-3) / 1e9,
                      "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
+        if m in IMMA_ROUTE_M:
+            # tensor-pipe kernel (k_mul_imma): radix-2^8 products, (8m)^2 byte-MACs per pair
+            imma_peak = sms * IMMA_U8_MACS_PER_CLK_SM * sm_max * 1e6
+            out[name].update({"pipe": "imma (mma.sync m16n8k32 u8, k_mul_imma)",
+                              "u8_macs_per_s": pairs_s * (8 * m) ** 2,
+                              "imma_roofline_u8_macs_per_s": imma_peak,
+                              "frac_imma": pairs_s * (8 * m) ** 2 / imma_peak,
+                              "note": "frac_imad: u32-product equivalents vs the IMAD.WIDE roofline (148 x 32/clk x "
+                                      "max clock); frac_imma: byte MACs vs the measured u8 IMMA rate (148 x 2048/clk "
+                                      "x max clock, tools/imma_peak.cu)"})
+        else:
+            out[name]["pipe"] = "imad (IMAD.WIDE.U32 96-bit column MAC)"
         if not args.no_e2e:
             # e2e: pinned host arrays through dotg_mul_batch_host (copies inside the timed region)
             ha = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)

@@ -98,6 +98,19 @@ int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_
 int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                    int layout, dotg_stream_t stream);
 
+/* Which pipe dotg_mul_batch (and everything built on it) takes the partial products on.
+ * AUTO: the integer tensor pipe (radix-2^8 IMMA column sums) for row-major m in
+ * {32, 64, 128} with 32-byte aligned pointers, the IMAD column kernels otherwise.
+ * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
+ * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it
+ * does not cover). Both are bit-exact; the knob exists for A/B measurement and for
+ * parity tests of both kernels. Process-wide. Returns the previous route, or
+ * DOTG_EINVAL for an unknown value. */
+#define DOTG_MUL_AUTO 0
+#define DOTG_MUL_IMAD 1
+#define DOTG_MUL_IMMA 2
+int dotg_set_mul_route(int route);
+
 /* Unsaturated 52-bit radix (RadixConfig kUnsaturated): dot_mul_words(a, b, kUnsaturated)
  * and dot_mul_5x5 (mul.hpp:73-85, mul.cpp:38-90, 127-150). Host row-major arrays; every
  * limb must be < 2^52 (check_limbs, limbs.cpp:26-33 -> DOTG_EINVAL); exactly 2m output

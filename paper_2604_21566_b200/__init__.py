@@ -14,6 +14,7 @@ from ._lib import (  # noqa: F401
     InvalidArgument,
     kernel_launches,
     lib,
+    set_mul_route,
 )
 from .api import (  # noqa: F401
     K_MAX_MUL_LIMBS,
@@ -66,6 +67,7 @@ __all__ = [
     "lib",
     "mul_batch",
     "mul_batch_host",
+    "set_mul_route",
     "sub_batch",
     "sub_words",
     "words",

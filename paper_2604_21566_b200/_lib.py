@@ -46,6 +46,7 @@ SIGNATURES = {
     "dotg_words_host_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_int, _P, _P, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_kernel_launches": (c_uint64, []),
+    "dotg_set_mul_route": (c_int, [c_int]),
 }
 
 
@@ -104,3 +105,15 @@ def check(rc: int) -> None:
 
 def kernel_launches() -> int:
     return int(lib().dotg_kernel_launches())
+
+
+MUL_AUTO, MUL_IMAD, MUL_IMMA = 0, 1, 2
+_ROUTES = {"auto": MUL_AUTO, "imad": MUL_IMAD, "imma": MUL_IMMA}
+
+
+def set_mul_route(route: str) -> str:
+    """Select the multiply pipe ("auto", "imad", "imma"); returns the previous one."""
+    if route not in _ROUTES:
+        raise InvalidArgument(f"mul route must be one of {sorted(_ROUTES)}")
+    prev = int(lib().dotg_set_mul_route(_ROUTES[route]))
+    return {v: k for k, v in _ROUTES.items()}[prev]

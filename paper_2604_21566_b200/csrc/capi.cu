@@ -375,6 +375,12 @@ int dotg_device_sms(void) {
 
 uint64_t dotg_kernel_launches(void) { return dotg::g_launches.load(); }
 
+int dotg_set_mul_route(int route) {
+    if (route != DOTG_MUL_AUTO && route != DOTG_MUL_IMAD && route != DOTG_MUL_IMMA)
+        return fail(DOTG_EINVAL, "set_mul_route: route must be DOTG_MUL_AUTO, DOTG_MUL_IMAD or DOTG_MUL_IMMA");
+    return dotg::g_mul_route.exchange(route);
+}
+
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, dotg_stream_t stream) {
     if (n > 0 && out == nullptr) return fail(DOTG_EINVAL, "fill: null out");
     int rc = check_device();

@@ -52,6 +52,13 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                              size_t batch, int layout, cudaStream_t stream);
 
+// Integer tensor-pipe column multiply (mul_imma.cu), row-major, m in {8,16,32,64}.
+bool mul_imma_supported(size_t m);
+cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                            cudaStream_t st);
+// Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
+extern std::atomic<int> g_mul_route;
+
 // Unsaturated 52-bit radix product (row-major, limbs < 2^52, exactly 2m limbs out).
 cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st);

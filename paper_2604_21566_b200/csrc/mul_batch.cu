@@ -476,10 +476,18 @@ cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t*
     return cudaGetLastError();
 }
 
+std::atomic<int> g_mul_route{0};
+
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                              int layout, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     const bool al = aligned32(out) && aligned32(a) && aligned32(b);
+    // Tensor pipe where it beats the IMAD kernels (tools/mul_timing.py on B200: m = 32
+    // 1.27x, 64 2.26x, 128 3.8x; at m = 8 / 16 the per-pair warp overhead loses to the
+    // thread-per-pair IMAD kernels, so only a forced IMMA route takes them there).
+    const int route = g_mul_route.load(std::memory_order_relaxed);
+    if (layout == 0 && al && mul_imma_supported(m) && route != 1 && (route == 2 || m >= 32))
+        return launch_mul_imma(out, a, b, m, batch, stream);
     if (layout == 1) {
         switch (m) {
             case 1: return run_regs<1, 1>(out, a, b, batch, stream);

@@ -26,8 +26,19 @@ def mul(torch, a, b, layout="row"):
     return host(dg.mul_batch(dev(torch, a.T.copy()), dev(torch, b.T.copy()), layout="interleaved")).T.copy()
 
 
+@pytest.fixture(params=["auto", "imad"])
+def route(request, cuda):
+    """Run a test on the default route (IMMA tensor-pipe kernels where they apply) and
+    again with the IMAD column kernels forced, so both stay bit-exact."""
+    import paper_2604_21566_b200 as dg
+
+    prev = dg.set_mul_route(request.param)
+    yield request.param
+    dg.set_mul_route(prev)
+
+
 @pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 33, 48, 64, 100, 128])
-def test_mul_matches_oracle(cuda, oracle, m):
+def test_mul_matches_oracle(cuda, oracle, route, m):
     rng = np.random.default_rng(2000 + m)
     n = 67
     for cat in ("random", "full_propagation", "spiky", "maxed_limbs", "zero_limbs"):
@@ -37,6 +48,47 @@ def test_mul_matches_oracle(cuda, oracle, m):
             got = mul(cuda, a, b, layout)
             assert got.shape == (n, 2 * m)
             assert np.array_equal(got, want), (m, cat, layout)
+
+
+@pytest.mark.parametrize("m", [8, 16, 32, 64, 128])
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 130])
+def test_imma_shapes(cuda, oracle, m, n):
+    """The IMMA kernel (one warp per pair, 4 pairs per CTA): partial last CTA, all-ones
+    operands (largest column sums, 2^27 per byte column at m = 128), single-byte spikes at
+    block edges, and a misaligned view that must take the IMAD route instead."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(31 * m + n)
+    prev = dg.set_mul_route("imma")
+    try:
+        for cat in ("random", "maxed_limbs", "spiky", "full_propagation"):
+            a, b = category(rng, cat, "mul", (n, m))
+            assert np.array_equal(mul(torch, a, b), oracle.mul_batch(a, b)), (m, n, cat)
+        a = np.full((n, m), MAX, np.uint64)
+        assert np.array_equal(mul(torch, a, a), oracle.mul_batch(a, a))
+        a = np.zeros((n, m), np.uint64)
+        b = np.zeros((n, m), np.uint64)
+        a[:, ::4] = np.uint64(0xFF << 56)  # top byte of every 32-byte block
+        b[:, 3::4] = np.uint64(0xFF)  # low byte of every block's last limb
+        assert np.array_equal(mul(torch, a, b), oracle.mul_batch(a, b))
+        # 8-byte (not 32-byte) aligned operands: IMAD fallback, still exact
+        a, b = uniform(rng, (n, m)), uniform(rng, (n, m))
+        da = dev(torch, np.concatenate([np.zeros(1, np.uint64), a.ravel()]))[1:].view(n, m)
+        db = dev(torch, np.concatenate([np.zeros(1, np.uint64), b.ravel()]))[1:].view(n, m)
+        assert np.array_equal(host(dg.mul_batch(da, db)), oracle.mul_batch(a, b))
+    finally:
+        dg.set_mul_route(prev)
+
+
+def test_mul_route_knob(cuda):
+    import paper_2604_21566_b200 as dg
+
+    prev = dg.set_mul_route("imad")
+    assert dg.set_mul_route("imma") == "imad"
+    assert dg.set_mul_route(prev) == "imma"
+    with pytest.raises(dg.InvalidArgument):
+        dg.set_mul_route("fp64")
 
 
 def test_golden_replay(cuda):
@@ -94,7 +146,7 @@ def test_mul_errors(cuda):
 
 
 @pytest.mark.parametrize("cfg", ["C3", "C4"])
-def test_config_parity_full_size(cuda, oracle, cfg):
+def test_config_parity_full_size(cuda, oracle, route, cfg):
     import paper_2604_21566_b200 as dg
     from paper_2604_21566_b200 import workloads as W
 
