@@ -528,17 +528,24 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
     calls = []
     if not want("C1"):
         sets = []
+    outs2 = []
     for a, b, sa, sb, o, f in sets:
-        calls.append(L.addsub(False, o, a, b, f, 64, B))
-        calls.append(L.addsub(True, o, sa, sb, f, 64, B))
+        # add and sub of one set: one grouped launch (two problems, separate outputs)
+        o2, f2 = torch.empty_like(o), torch.empty_like(f)
+        outs2.append((o2, f2))
+        calls.append(L.grouped([(False, o, a, b, f, 64, B), (True, o2, sa, sb, f2, 64, B)]))
     if sets:
         ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
     byts = B * (24 * 64 + 4)
     if sets:
-        out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * len(calls) * world / (ms * 1e-3) / 1e9,
-                 "unit": "GB/s", "kernel_gbs": byts * len(calls) / (sum(per) * 1e-3) / 1e9,
-                 "frac_hbm": byts * len(calls) / (sum(per) * 1e-3) / 1e9 / hbm_peak,
-                 "add_us": statistics.mean(per[0::2]) * 1e3, "sub_us": statistics.mean(per[1::2]) * 1e3}
+        nops = 2 * len(calls)
+        out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * nops * world / (ms * 1e-3) / 1e9,
+                     "unit": "GB/s", "kernel_gbs": byts * nops / (sum(per) * 1e-3) / 1e9,
+                     "frac_hbm": byts * nops / (sum(per) * 1e-3) / 1e9 / hbm_peak,
+                     "launch_us": statistics.mean(per) * 1e3,
+                     "step": "3 rotating input sets (300 MB apart > L2); per set add + sub in one dotg_addsub_grouped "
+                             "launch"}
+    del outs2
     del sets, calls
     torch.cuda.empty_cache()
 
@@ -657,6 +664,113 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
     return out
 
 
+def cpu_ref_table():
+    """BASELINE.md §4 CPU columns (part of the CPU-baseline leg): the reference's own
+    DoT path (oracle/_ref/libdotref.so) on this host, 1 thread and all threads, per
+    config, on bounded samples of the configs' inputs (device generators, copied to the
+    host). add/sub in algorithmic GB/s (24m + 4 B per pair-op), mul in pairs/s, C5 in
+    GB/s (24 B per limb, single thread: the reference's carry chain is serial)."""
+    import numpy as np
+    import torch
+
+    from paper_2604_21566_b200 import workloads as W
+
+    L = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libdotref.so"))
+    L.dotref_batch.restype = ctypes.c_int
+    L.dotref_batch.argtypes = [ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 4 + [ctypes.c_size_t] * 2 + [ctypes.c_int]
+    L.dotref_words.restype = ctypes.c_int
+    L.dotref_words.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    L.dotref_dispatch_note.restype = ctypes.c_char_p
+    L.dotref_dispatch_note.argtypes = [ctypes.c_int]
+    NT = os.cpu_count() or 1
+    P = lambda x: None if x is None else ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+
+    def host(t):
+        return t.cpu().numpy().view(np.uint64).copy()
+
+    def best_of(fn, reps=3):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    def batch_rate(op, a, b, threads):
+        B, m = a.shape
+        out = np.empty((B, 2 * m if op == 2 else m), np.uint64)
+        fl = None if op == 2 else np.empty(B, np.uint32)
+        dt = best_of(lambda: L.dotref_batch(op, 0, P(out), P(a), P(b), P(fl), m, B, threads))
+        return dt
+
+    res = {"cpu": open("/proc/cpuinfo").read().split("model name")[1].split("\n")[0].strip(": \t"),
+           "threads_all": NT, "route": L.dotref_dispatch_note(8).decode(), "rows": []}
+
+    def row(cfg, unit, sample, v1, vn):
+        res["rows"].append({"config": cfg, "unit": unit, "sample": sample, "one_thread": v1, "all_threads": vn})
+
+    # C1: 4096-bit add + sub, sample 16384 of 65536 pairs
+    a, b, sa, sb = W.c1_inputs()
+    n = 16384
+    ha, hb, hsa, hsb = host(a[:n]), host(b[:n]), host(sa[:n]), host(sb[:n])
+    byts = 2 * n * (24 * 64 + 4)
+    for th in (1, NT):
+        dt = batch_rate(0, ha, hb, th) + batch_rate(1, hsa, hsb, th)
+        if th == 1:
+            v1 = byts / dt / 1e9
+        else:
+            vn = byts / dt / 1e9
+    row("C1 add+sub m=64", "GB/s", f"{n} pairs add + sub", v1, vn)
+    del a, b, sa, sb
+
+    # C2: the four carry-stress sizes, 1/4 of each batch
+    tot_b, tot_t = 0, {1: 0.0, NT: 0.0}
+    for m, B in W.C2_SIZES:
+        a, b, sa, sb = W.c2_inputs(m, B)
+        n = B // 4
+        ha, hb, hsa, hsb = host(a[:n]), host(b[:n]), host(sa[:n]), host(sb[:n])
+        byts = 2 * n * (24 * m + 4)
+        vals = {}
+        for th in (1, NT):
+            dt = batch_rate(0, ha, hb, th) + batch_rate(1, hsa, hsb, th)
+            vals[th] = byts / dt / 1e9
+            tot_t[th] += dt
+        tot_b += byts
+        row(f"C2 add+sub m={m}", "GB/s", f"{n} of {B} pairs add + sub", vals[1], vals[NT])
+        del a, b, sa, sb
+    row("C2 sweep (all sizes)", "GB/s", "1/4 of every batch", tot_b / tot_t[1] / 1e9, tot_b / tot_t[NT] / 1e9)
+
+    # C3 / C4 multiplication (dot_mul_words)
+    for name, gen, n in (("C3 mul m=16", W.c3_inputs, 16384), ("C4 mul m=64", W.c4_inputs, 2048)):
+        a, b = gen()
+        half = a.shape[0] // 2
+        if name.startswith("C4"):  # half random, half all-ones pairs, as in the config
+            idx = torch.cat([torch.arange(0, n // 2), torch.arange(half, half + n // 2)]).cuda()
+            ha, hb = host(a[idx]), host(b[idx])
+        else:
+            ha, hb = host(a[:n]), host(b[:n])
+        vals = {th: n / batch_rate(2, ha, hb, th) for th in (1, NT)}
+        row(name, "pairs/s", f"{n} pairs", vals[1], vals[NT])
+        del a, b
+
+    # C5: one long add / sub, single thread (the reference's carry chain is serial)
+    m5 = 1 << 28
+    run = (3 << 25, 5 << 25)
+    for sub in (False, True):
+        a_d, b_d = W.c5_inputs(sub, m=m5, run=run)
+        ha, hb = host(a_d), host(b_d)
+        del a_d, b_d
+        out = np.empty(m5, np.uint64)
+        dt = best_of(lambda: L.dotref_words(int(sub), P(out), m5, P(ha), m5, P(hb), m5, 8, None, None), reps=2)
+        row(f"C5 {'sub' if sub else 'add'} (2^28-limb sample)", "GB/s", f"{m5} limbs, run of 2^26 limbs",
+            24 * m5 / dt / 1e9, None)
+        del ha, hb, out
+
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -670,7 +784,12 @@ def main():
     ap.add_argument("--only", default="", help="comma list of C1,C3,C4,C5: run only those secondary configs")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    ap.add_argument("--cpu-table", action="store_true",
+                    help="print the CPU reference table (1 thread / all threads per config) and exit")
     args = ap.parse_args()
+    if args.cpu_table:
+        print(json.dumps(cpu_ref_table(), indent=1))
+        return 0
     args.warmup = max(3, args.warmup)
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
