@@ -76,12 +76,13 @@ def lib() -> ctypes.CDLL:
     """Load libdotg.so once; raise loudly when it has not been built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("DOTG_LIB_PATH", LIB_PATH)  # experiments: an alternative build
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB_PATH} is missing: build it with `make -C paper_2604_21566_b200/csrc` "
+                f"{path} is missing: build it with `make -C paper_2604_21566_b200/csrc` "
                 "or __graft_entry__.build(); the product path has no CPU fallback"
             )
-        handle = ctypes.CDLL(LIB_PATH)
+        handle = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(handle, name)
             fn.restype = res

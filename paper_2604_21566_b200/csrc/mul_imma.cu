@@ -63,7 +63,10 @@ struct ImmaCfg {
     static constexpr int A_WORDS = 12 * (NB + 14);
     static constexpr int NCOL = 64 * NB;          // product bytes = column sums
     static constexpr int S_WORDS = NCOL + 4 * (NCOL / 32);  // padded index x + 4 (x >> 5)
-    static constexpr int ST = M >= 64 ? 4 : 8;    // bulk-copy ring stages per warp
+#ifndef DOTG_IMMA_ST_BIG
+#define DOTG_IMMA_ST_BIG 4
+#endif
+    static constexpr int ST = M >= 64 ? DOTG_IMMA_ST_BIG : 8;  // bulk-copy ring stages per warp
     static constexpr int RAW_WORDS = ST * 2 * NW; // ring of raw (a, b) pairs
     static constexpr int WARP_WORDS = RAW_WORDS + COPY_WORDS + A_WORDS + S_WORDS;
     static constexpr int NC0 = (2 * NB + 7) / 8;  // accumulator tiles per R0
@@ -144,7 +147,10 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 // Persistent: every warp walks pairs gw, gw + nwarps, ... and prefetches the next
 // pair's operands into registers while the current one is on the tensor pipe.
 template <int NB>
-__global__ void __launch_bounds__(kImmaWarps * 32) k_mul_imma(uint64_t* __restrict__ out,
+#ifndef DOTG_IMMA_MINB16
+#define DOTG_IMMA_MINB16 1
+#endif
+__global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b, size_t batch) {
     using C = ImmaCfg<NB>;

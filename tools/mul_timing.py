@@ -27,6 +27,9 @@ def t(fn, reps=20):
 
 ROOF = 148 * 32 * 1.965e9
 shapes = [(8, 1 << 19), (16, 1 << 18), (32, 1 << 17), (64, 1 << 16), (128, 1 << 14)]
+if len(sys.argv) > 1:
+    keep = {int(x) for x in sys.argv[1].split(",")}
+    shapes = [(m, B) for m, B in shapes if m in keep]
 for m, B in shapes:
     if (m, B) == (16, 1 << 18):
         a, b = W.c3_inputs()
