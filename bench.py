@@ -411,6 +411,22 @@ def run_ours(args, rank, world, dist):
                                "sub_gbs": call_bytes[i] / (per_single[i + 4] * 1e-3) / 1e9}
                 for i, x in enumerate(bufs)}
     traffic = traffic_table().get("C2_per_launch_bytes_grouped" if not args.ungrouped else "C2_per_launch_bytes")
+    # stress level of the sweep: AddSubStats counters of the reference's
+    # w8 chunking, derived on the device from the step's own inputs and outputs
+    stress = {}
+    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for x in bufs:
+        row = {}
+        for sub, o, a_, b_ in ((0, x["oa"], x["a"], x["b"]), (1, x["os"], x["sa"], x["sb"])):
+            ctr.zero_()
+            rc = lib.dotg_addsub_stats(sub, ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a_.data_ptr()),
+                                       ctypes.c_void_p(b_.data_ptr()), x["m"], x["B"], 0, 8,
+                                       ctypes.c_void_p(ctr.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+            if rc == 0:
+                c = ctr.cpu().tolist()
+                row["sub" if sub else "add"] = {"chunks": c[0], "phase4_triggers": c[1],
+                                                "phase4_fraction": c[1] / max(1, c[0])}
+        stress[f"m{x['m']}"] = row
 
     # ---- e2e: the same step through the host-buffer C ABI (pinned host arrays) ----
     e2e = None
@@ -501,6 +517,7 @@ def run_ours(args, rank, world, dist):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clocks,
+        "carry_stress": stress,
         "configs": secondary,
     }
     if rank == 0:
