@@ -99,8 +99,10 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
                    int layout, dotg_stream_t stream);
 
 /* Which pipe dotg_mul_batch (and everything built on it) takes the partial products on.
- * AUTO: the integer tensor pipe (radix-2^8 IMMA column sums) for row-major m in
- * {32, 64, 128} with 32-byte aligned pointers, the IMAD column kernels otherwise.
+ * AUTO (row-major, 32-byte aligned pointers): m <= 16 on the IMAD column kernels; m in
+ * {32, 64, 128} on the integer tensor pipe (radix-2^8 IMMA column sums); other
+ * 16 < m < 128 zero-padded to the next of those; m > 128 as padded Karatsuba down to
+ * m = 128 tensor-pipe leaves. Interleaved or misaligned operands: IMAD kernels.
  * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
  * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it
  * does not cover). Both are bit-exact; the knob exists for A/B measurement and for

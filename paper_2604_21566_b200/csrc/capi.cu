@@ -116,17 +116,7 @@ int words(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t 
         return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "memset");
     }
     const size_t sb = dotg::long_state_bytes(m);
-    static thread_local int pool_dev = -1;  // keep freed scratch in the stream-ordered pool
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (pool_dev != dev) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = ~uint64_t(0);
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_dev = dev;
-    }
+    dotg::retain_stream_pool();
     void* scratch = nullptr;
     cudaError_t e = cudaMallocAsync(&scratch, sb + 256, st);
     if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("scratch: ") + cudaGetErrorString(e));

@@ -66,6 +66,11 @@ cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t*
 // Breadth-first batched Karatsuba over the column multiply (karatsuba.cu).
 cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                    size_t theta, cudaStream_t st);
+// m padded to base * 2^L (base a tensor-pipe size); L = 0 pads the rows and multiplies.
+cudaError_t launch_karatsuba_padded(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                    size_t base, cudaStream_t st);
+// Keep freed stream-ordered scratch cached in the device pool (per host thread, device).
+void retain_stream_pool();
 
 // AddSubStats parity counters (stats.cu): counters = device uint64[2] {chunks, fires}.
 cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,

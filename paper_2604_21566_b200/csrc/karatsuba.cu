@@ -11,7 +11,13 @@
 // so a level is ONE batched launch: the 3 children of each of the `count` pairs are
 // stacked as [lo; hi; |hi - lo|] into a [3*count][h] batch, down to a single batched
 // base-case multiply of 3^L * batch pairs, then one combine launch per level on the way
-// back up. Launch count is O(levels), not O(3^levels).
+// back up. Launch count is O(levels), not O(3^levels). Split and combine run one warp per
+// pair with lane-strided (coalesced) limbs and ballot-lookahead carries.
+//
+// Two descents share the machinery: the reference's (h = ceil(m / 2) until m <= theta,
+// dotg_karatsuba_batch) and the padded one dotg_mul_batch uses for m > 128 and for
+// in-between sizes: m padded to base * 2^L with base a tensor-pipe size (mul_imma.cu),
+// so every leaf is one exact IMMA multiply.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,90 +29,125 @@ namespace dotg {
 
 namespace {
 
-typedef unsigned __int128 u128;
-typedef __int128 s128;
+// ---------------------------------------------------------------------------
+// Warp-per-pair split / combine. Limbs are lane-strided (limb i on lane i % 32, so every
+// access is coalesced) and processed in 32-limb chunks; each multi-limb add/sub resolves
+// its carries with the add kernel's ballot lookahead (device.cuh algebra):
+//   C = (((G << 1) | cin) + P) ^ P per chunk, carry out = bit 32, chained over chunks.
+// ---------------------------------------------------------------------------
+constexpr int kKaraWarps = 8;
 
-// Children of pair p (rows of m limbs, read as 2h limbs with a zero pad when m is odd):
-//   lo[p] = A[p][0:h], hi[p] = A[p][h:2h], df[p] = |hi - lo|, sign[p] = (hi < lo).
-__global__ void k_kara_split(const uint64_t* A, size_t m, size_t h, size_t count, uint64_t* lo, uint64_t* hi,
-                             uint64_t* df, uint32_t* sign) {
-    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// carry-in of this lane and the chunk carry-out for generate/propagate bits (g, p)
+__device__ __forceinline__ uint32_t chunk_carry(uint32_t g, uint32_t p, uint32_t& cin, int lane) {
+    const uint32_t G = __ballot_sync(0xffffffffu, g), P = __ballot_sync(0xffffffffu, p);
+    const uint64_t y = ((uint64_t(G) << 1) | cin) + uint64_t(P);
+    cin = uint32_t(y >> 32);
+    return ((uint32_t(y) ^ P) >> lane) & 1u;
+}
+
+// Children of pair p, parent read as 2h limbs with zero padding above its m limbs:
+//   lo = A[0:h], hi = A[h:2h], df = |hi - lo|, sign = (hi < lo).
+__global__ void __launch_bounds__(kKaraWarps * 32) k_kara_split_w(const uint64_t* __restrict__ A, size_t m,
+                                                                  size_t h, size_t count, uint64_t* lo,
+                                                                  uint64_t* hi, uint64_t* df, uint32_t* sign) {
+    const int lane = threadIdx.x & 31;
+    const size_t p = size_t(blockIdx.x) * kKaraWarps + (threadIdx.x >> 5);
     if (p >= count) return;
     const uint64_t* a = A + p * m;
-    auto limb = [&](size_t i) -> uint64_t { return i < m ? a[i] : 0ull; };
-    // compare hi vs lo from the top (limbs.cpp:46-53 restricted to equal lengths)
-    int cmp = 0;
-    for (size_t i = h; i-- > 0;) {
-        const uint64_t x = limb(h + i), y = limb(i);
-        if (x != y) {
-            cmp = x < y ? -1 : 1;
-            break;
-        }
+    auto limb = [&](size_t i) -> uint64_t { return i < m ? __ldg(a + i) : 0ull; };
+    // highest limb where hi and lo differ decides the sign (compare, limbs.cpp:46-53)
+    unsigned top = 0;  // 1 + index of the highest differing limb seen by this lane
+    for (size_t i = lane; i < h; i += 32)
+        if (limb(h + i) != limb(i)) top = unsigned(i) + 1;
+    const unsigned hi_diff = __reduce_max_sync(0xffffffffu, top);
+    bool neg = false;
+    if (hi_diff != 0) {
+        const size_t i = hi_diff - 1;
+        neg = limb(h + i) < limb(i);  // every lane reads the same limb (broadcast)
     }
-    const bool neg = cmp < 0;
     uint64_t* plo = lo + p * h;
     uint64_t* phi = hi + p * h;
     uint64_t* pdf = df + p * h;
-    uint32_t bw = 0;
-    for (size_t i = 0; i < h; ++i) {
-        const uint64_t x = limb(h + i), y = limb(i);
-        plo[i] = y;
-        phi[i] = x;
+    uint32_t cin = 0;
+    for (size_t base = 0; base < h; base += 32) {
+        const size_t i = base + lane;
+        const bool ok = i < h;
+        const uint64_t x = ok ? limb(h + i) : 0ull, y = ok ? limb(i) : 0ull;
         const uint64_t u = neg ? y : x, v = neg ? x : y;  // larger minus smaller
         const uint64_t d = u - v;
-        const uint32_t b1 = u < v;
-        const uint64_t r = d - bw;
-        bw = b1 | (d < uint64_t(bw));
-        pdf[i] = r;
+        const uint32_t bin = chunk_carry(ok && u < v, ok && d == 0, cin, lane);
+        if (ok) {
+            plo[i] = y;
+            phi[i] = x;
+            pdf[i] = d - bin;
+        }
     }
-    sign[p] = neg ? 1u : 0u;
+    if (lane == 0) sign[p] = neg ? 1u : 0u;
 }
 
 // Parent product of pair p from its children's products P = [P0; P1; PD] (each
 // [count][2h]): out[p] (2m limbs) = P0 + X (P0 + P1 -+ PD) + X^2 P1, truncated to 2m.
-__global__ void k_kara_combine(const uint64_t* P, size_t h, size_t count, const uint32_t* sa, const uint32_t* sb,
-                               uint64_t* out, size_t m) {
-    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+// Three chained multi-limb passes per chunk: T = P0 + P1, M = T -+ PD (>= 0, 2h + 1
+// limbs), R[h + j] = base + M[j] with base = P0 below 2h, P1 above.
+__global__ void __launch_bounds__(kKaraWarps * 32) k_kara_combine_w(const uint64_t* __restrict__ P, size_t h,
+                                                                    size_t count, const uint32_t* sa,
+                                                                    const uint32_t* sb, uint64_t* out, size_t m) {
+    const int lane = threadIdx.x & 31;
+    const size_t p = size_t(blockIdx.x) * kKaraWarps + (threadIdx.x >> 5);
     if (p >= count) return;
-    const size_t n2 = 2 * h;
+    const size_t n2 = 2 * h, n_out = 2 * m;
     const uint64_t* p0 = P + p * n2;
     const uint64_t* p1 = P + (count + p) * n2;
     const uint64_t* pd = P + (2 * count + p) * n2;
     const bool minus = sa[p] == sb[p];  // same-sign differences: mid = P0 + P1 - PD
-    uint64_t* o = out + p * (2 * m);
-    s128 vc = 0;   // signed carry of V = P0 + P1 -+ PD (V >= 0, 2h + 1 limbs)
-    u128 oc = 0;   // carry of the final sum
-    for (size_t k = 0; k < 4 * h; ++k) {
-        u128 t = oc + (k < n2 ? p0[k] : p1[k - n2]);
-        if (k >= h && k <= 3 * h) {
-            const size_t j = k - h;
-            uint64_t vj;
-            if (j < n2) {
-                const s128 s = vc + s128(p0[j]) + s128(p1[j]) + (minus ? -s128(pd[j]) : s128(pd[j]));
-                vj = uint64_t(s);
-                vc = s >> 64;
-            } else {
-                vj = uint64_t(vc);  // V's top limb (non-negative)
-            }
-            t += vj;
+    uint64_t* o = out + p * n_out;
+    for (size_t k = lane; k < h && k < n_out; k += 32) o[k] = __ldg(p0 + k);
+    uint32_t cT = 0, cM = 0, cR = 0;
+    for (size_t base = 0; base < 3 * h; base += 32) {
+        const size_t j = base + lane, k = h + j;
+        const bool ok = j < 3 * h;
+        const bool low = j < n2;
+        const uint64_t x0 = ok && low ? __ldg(p0 + j) : 0ull, x1 = ok && low ? __ldg(p1 + j) : 0ull;
+        const uint64_t dd = ok && low ? __ldg(pd + j) : 0ull;
+        // T = P0 + P1
+        const uint64_t ts = x0 + x1;
+        const uint64_t t = ts + chunk_carry(ok && ts < x0, ok && ts == ~0ull, cT, lane);
+        // M = T -+ PD
+        uint64_t mj;
+        if (minus) {
+            const uint64_t ms = t - dd;
+            mj = ms - chunk_carry(ok && t < dd, ok && ms == 0, cM, lane);
+        } else {
+            const uint64_t ms = t + dd;
+            mj = ms + chunk_carry(ok && ms < t, ok && ms == ~0ull, cM, lane);
         }
-        if (k < 2 * m) o[k] = uint64_t(t);
-        oc = t >> 64;
+        // R[h + j] = base + M[j]
+        const uint64_t bk = !ok ? 0ull : (k < n2 ? __ldg(p0 + k) : __ldg(p1 + (k - n2)));
+        const uint64_t rs = bk + mj;
+        const uint64_t r = rs + chunk_carry(ok && rs < bk, ok && rs == ~0ull, cR, lane);
+        if (ok && k < n_out) o[k] = r;
     }
 }
 
-unsigned blocks_for(size_t n) { return unsigned((n + 127) / 128); }
+// dst[r][0:nd) = src[r][0:ns) zero-extended or truncated (warp per row, coalesced).
+__global__ void __launch_bounds__(kKaraWarps * 32) k_copy_rows(const uint64_t* __restrict__ src, size_t ns,
+                                                               uint64_t* __restrict__ dst, size_t nd, size_t rows) {
+    const int lane = threadIdx.x & 31;
+    const size_t r = size_t(blockIdx.x) * kKaraWarps + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    for (size_t i = lane; i < nd; i += 32) dst[r * nd + i] = i < ns ? __ldg(src + r * ns + i) : 0ull;
+}
 
-}  // namespace
+// The level sizes of a descent: parent m_i (the limbs actually read), half h_i.
+struct KaraPlan {
+    std::vector<size_t> pm, h;
+};
 
-cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
-                                   size_t theta, cudaStream_t st) {
-    if (batch == 0) return cudaSuccess;
-    if (m <= theta) return launch_mul_batch(out, a, b, m, batch, 0, st);
+cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, const KaraPlan& plan,
+                          cudaStream_t st) {
     struct Level {
         size_t m, h, count;
-        uint64_t *A, *B;   // inputs of this level: [count][m]
-        uint32_t *sa, *sb; // signs of this level's differences: [count]
+        uint32_t *sa, *sb;  // signs of this level's differences: [count]
     };
     std::vector<Level> lv;
     std::vector<void*> allocs;
@@ -116,17 +157,16 @@ cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint6
         allocs.push_back(p);
         return p;
     };
-    cudaError_t e = cudaSuccess;
     auto cleanup = [&]() {
         for (void* p : allocs) cudaFreeAsync(p, st);
     };
-    size_t cm = m, count = batch;
+    size_t count = batch, cm = plan.pm.empty() ? 0 : plan.pm[0];
     const uint64_t* A = a;
     const uint64_t* B = b;
     // Descend: split every level until the base case.
-    while (cm > theta) {
-        const size_t h = (cm + 1) / 2;
-        Level L{cm, h, count, nullptr, nullptr, nullptr, nullptr};
+    for (size_t d = 0; d < plan.h.size(); ++d) {
+        const size_t h = plan.h[d];
+        Level L{plan.pm[d], h, count, nullptr, nullptr};
         uint64_t* nA = static_cast<uint64_t*>(alloc(3 * count * h * 8));
         uint64_t* nB = static_cast<uint64_t*>(alloc(3 * count * h * 8));
         L.sa = static_cast<uint32_t*>(alloc(count * 4));
@@ -135,9 +175,10 @@ cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint6
             cleanup();
             return cudaErrorMemoryAllocation;
         }
-        k_kara_split<<<blocks_for(count), 128, 0, st>>>(A, cm, h, count, nA, nA + count * h, nA + 2 * count * h,
+        const unsigned grid = unsigned((count + kKaraWarps - 1) / kKaraWarps);
+        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(A, L.m, h, count, nA, nA + count * h, nA + 2 * count * h,
                                                          L.sa);
-        k_kara_split<<<blocks_for(count), 128, 0, st>>>(B, cm, h, count, nB, nB + count * h, nB + 2 * count * h,
+        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(B, L.m, h, count, nB, nB + count * h, nB + 2 * count * h,
                                                          L.sb);
         count_launch(2);
         lv.push_back(L);
@@ -152,7 +193,7 @@ cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint6
         cleanup();
         return cudaErrorMemoryAllocation;
     }
-    e = launch_mul_batch(P, A, B, cm, count, 0, st);
+    cudaError_t e = launch_mul_batch(P, A, B, cm, count, 0, st);
     // Ascend: combine level by level.
     for (size_t i = lv.size(); e == cudaSuccess && i-- > 0;) {
         const Level& L = lv[i];
@@ -161,13 +202,92 @@ cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint6
             e = cudaErrorMemoryAllocation;
             break;
         }
-        k_kara_combine<<<blocks_for(L.count), 128, 0, st>>>(P, L.h, L.count, L.sa, L.sb, dst, L.m);
+        k_kara_combine_w<<<unsigned((L.count + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(
+            P, L.h, L.count, L.sa, L.sb, dst, L.m);
         count_launch();
         e = cudaGetLastError();
         P = dst;
     }
     cleanup();
     return e;
+}
+
+}  // namespace
+
+void retain_stream_pool() {
+    // keep freed scratch (Karatsuba levels, long-number state) cached in the device's
+    // stream-ordered pool, up to 8 GiB, instead of returning it to the driver at every sync
+    static thread_local int pool_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (pool_dev == dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = uint64_t(8) << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_dev = dev;
+}
+
+// Reference recursion (kara_rec, mul.cpp:176-233): split h = ceil(m / 2) until m <= theta.
+cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                   size_t theta, cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    if (m <= theta) return launch_mul_batch(out, a, b, m, batch, 0, st);
+    retain_stream_pool();
+    KaraPlan plan;
+    for (size_t cm = m; cm > theta; cm = (cm + 1) / 2) {
+        plan.pm.push_back(cm);
+        plan.h.push_back((cm + 1) / 2);
+    }
+    return run_karatsuba(out, a, b, batch, plan, st);
+}
+
+// Large products for dotg_mul_batch: pad m up to base * 2^L (base a tensor-pipe size),
+// so every leaf is an exact tensor-pipe multiply; the top split zero-pads, the top
+// combine truncates to 2m limbs.
+cudaError_t launch_karatsuba_padded(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                    size_t base, cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    retain_stream_pool();
+    size_t mp = base;
+    int levels = 0;
+    while (mp < m) {
+        mp *= 2;
+        ++levels;
+    }
+    if (levels == 0) {
+        if (m == mp) return launch_mul_batch(out, a, b, m, batch, 0, st);
+        // zero-pad the rows to the tensor-pipe size, multiply, keep the low 2m limbs
+        uint64_t *pa = nullptr, *pb = nullptr, *po = nullptr;
+        cudaError_t e = cudaMallocAsync(&pa, batch * mp * 8, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&pb, batch * mp * 8, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&po, batch * 2 * mp * 8, st);
+        const unsigned grid = unsigned((batch + kKaraWarps - 1) / kKaraWarps);
+        if (e == cudaSuccess) {
+            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(a, m, pa, mp, batch);
+            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(b, m, pb, mp, batch);
+            count_launch(2);
+            e = launch_mul_batch(po, pa, pb, mp, batch, 0, st);
+        }
+        if (e == cudaSuccess) {
+            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(po, 2 * mp, out, 2 * m, batch);
+            count_launch();
+            e = cudaGetLastError();
+        }
+        for (void* q : {static_cast<void*>(pa), static_cast<void*>(pb), static_cast<void*>(po)})
+            if (q != nullptr) cudaFreeAsync(q, st);
+        return e;
+    }
+    KaraPlan plan;
+    size_t cm = m, full = mp;
+    for (int d = 0; d < levels; ++d) {
+        plan.pm.push_back(cm);
+        plan.h.push_back(full / 2);
+        full /= 2;
+        cm = full;
+    }
+    return run_karatsuba(out, a, b, batch, plan, st);
 }
 
 }  // namespace dotg

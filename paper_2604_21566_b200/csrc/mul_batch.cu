@@ -395,24 +395,26 @@ cudaError_t run_regblk(uint64_t* out, const uint64_t* a, const uint64_t* b, size
 template <int M>
 cudaError_t run_smem(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
     using C = SmemCfg<M>;
-    static int sms = 0, max_smem = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    }
+    // per (host thread, device): the smem opt-in is a per-device function attribute
+    static thread_local struct { int dev = -1, sms = 0, max_smem = 0; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
     // two CTAs per SM, 1 KB reserved per CTA
-    int P = int((size_t(max_smem) / 2 - 1024) / C::PAIR_BYTES);
-    if (P > 128) P = 128;
-    if (P < 1) P = 1;
-    const size_t smem = size_t(P) * C::PAIR_BYTES;
-    static size_t configured = 0;
-    if (configured < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_mul_smem<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    auto pairs_per_cta = [](int max_smem) {
+        int P = int((size_t(max_smem) / 2 - 1024) / C::PAIR_BYTES);
+        return P > 128 ? 128 : (P < 1 ? 1 : P);
+    };
+    if (di.dev != dev) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&di.max_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaError_t e = cudaFuncSetAttribute(k_mul_smem<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(size_t(pairs_per_cta(di.max_smem)) * C::PAIR_BYTES));
         if (e != cudaSuccess) return e;
-        configured = smem;
+        di.dev = dev;
     }
+    const int P = pairs_per_cta(di.max_smem);
+    const size_t smem = size_t(P) * C::PAIR_BYTES;
+    const int sms = di.sms;
     const size_t groups = (batch + size_t(P) - 1) / size_t(P);
     const size_t slots = size_t(sms) * 2;
     // balanced rounds: every CTA gets ceil(groups / slots) or one fewer groups
@@ -490,6 +492,11 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     const int route = g_mul_route.load(std::memory_order_relaxed);
     if (layout == 0 && al && mul_imma_supported(m) && route != 1 && (route == 2 || m >= 32))
         return launch_mul_imma(out, a, b, m, batch, stream);
+    // Sizes without a dedicated kernel: 16 < m < 128 zero-pads to the next tensor-pipe
+    // size; m > 128 runs padded Karatsuba down to m = 128 tensor-pipe leaves (the generic
+    // thread-per-pair kernel would be 100x slower there: tools/kara_timing.py).
+    if (layout == 0 && al && route != 1 && m > 16 && !mul_imma_supported(m))
+        return launch_karatsuba_padded(out, a, b, m, batch, m <= 32 ? 32 : (m <= 64 ? 64 : 128), stream);
     if (layout == 1) {
         switch (m) {
             case 1: return run_regs<1, 1>(out, a, b, batch, stream);

@@ -333,10 +333,12 @@ template <int NB>
 cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
     using C = ImmaCfg<NB>;
     const size_t smem = size_t(kImmaWarps) * C::WARP_WORDS * sizeof(uint32_t);
-    static int grid_cap = 0;
-    if (grid_cap == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+    // per (host thread, device): the smem opt-in is a per-device function attribute
+    static thread_local struct { int dev = -1, grid_cap = 0; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k_mul_imma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -344,10 +346,11 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
         }
         cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mul_imma<NB>, kImmaWarps * 32, smem);
         if (e != cudaSuccess) return e;
-        grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+        di.grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+        di.dev = dev;
     }
     const size_t need = (batch + kImmaWarps - 1) / kImmaWarps;
-    const size_t grid = need < size_t(grid_cap) ? need : size_t(grid_cap);
+    const size_t grid = need < size_t(di.grid_cap) ? need : size_t(di.grid_cap);
     k_mul_imma<NB><<<unsigned(grid), kImmaWarps * 32, smem, st>>>(out, a, b, batch);
     count_launch();
     return cudaGetLastError();

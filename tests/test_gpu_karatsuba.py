@@ -69,3 +69,40 @@ def test_device_batch_equals_column_multiply(cuda):
         a = torch.from_numpy(spiky(rng, (300, m)).view(np.int64)).cuda()
         b = torch.from_numpy(spiky(rng, (300, m)).view(np.int64)).cuda()
         assert torch.equal(dg.karatsuba_batch(a, b, theta=theta), dg.mul_batch(a, b)), (m, theta)
+
+
+@pytest.mark.parametrize("m", [129, 200, 256, 300, 512, 1024])
+def test_large_mul_batch_route(cuda, oracle, m):
+    """dotg_mul_batch for m > 128 runs padded Karatsuba down to tensor-pipe leaves
+    (m -> 128 * 2^L, split zero-pads, combine truncates); exact vs the oracle, with
+    all-ones rows (largest middle terms) and equal halves (|hi - lo| = 0) included."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(900 + m)
+    n = 9
+    a, b = spiky(rng, (n, m)), uniform(rng, (n, m))
+    a[0] = MAX
+    b[0] = MAX
+    h = m // 2
+    a[1, h:2 * h] = a[1, :h]  # hi == lo
+    b[2, :] = 0
+    b[3, m - 1] = 0
+    got = dg.mul_batch(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), oracle.mul_batch(a, b)), m
+
+
+@pytest.mark.parametrize("m", [17, 20, 31, 33, 40, 63, 65, 96, 127])
+def test_padded_mul_batch_route(cuda, oracle, m):
+    """16 < m < 128 without a dedicated kernel: rows zero-padded to 32 / 64 / 128 limbs,
+    one tensor-pipe multiply, low 2m limbs kept."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(950 + m)
+    for cat in (uniform, spiky):
+        a, b = cat(rng, (37, m)), cat(rng, (37, m))
+        a[0] = MAX
+        b[0] = MAX
+        got = dg.mul_batch(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
+        assert np.array_equal(got.cpu().numpy().view(np.uint64), oracle.mul_batch(a, b)), m

@@ -27,3 +27,15 @@ for name, gen in (("C4", W.c4_inputs), ("C3", W.c3_inputs)):
         o = dg.karatsuba_batch(a, b, theta=theta)
         assert torch.equal(o, ref)
         print(name, "karatsuba theta", theta, "us", round(t(lambda: dg.karatsuba_batch(a, b, theta=theta)), 1))
+
+# large operands: plain mul_batch (generic column kernel for m > 128) vs Karatsuba down to
+# the tensor-pipe base case (m = 128 / 64 / 32)
+for m, B in ((256, 1 << 12), (512, 1 << 10), (1024, 1 << 8)):
+    a = W.fill(B * m, 0x5A + m, 0).view(B, m)
+    b = W.fill(B * m, 0x5B + m, 0).view(B, m)
+    ref = dg.mul_batch(a, b)
+    print(f"m={m} B={B} schoolbook us", round(t(lambda: dg.mul_batch(a, b), reps=3), 1))
+    for theta in (128, 64, 32):
+        o = dg.karatsuba_batch(a, b, theta=theta)
+        assert torch.equal(o, ref)
+        print(f"m={m} karatsuba theta {theta} us", round(t(lambda: dg.karatsuba_batch(a, b, theta=theta), reps=5), 1))
