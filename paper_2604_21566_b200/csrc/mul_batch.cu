@@ -266,9 +266,10 @@ __global__ void __launch_bounds__(128) k_mul_smem(uint64_t* out, const uint64_t*
 // leave the IMAD.WIDE carry chain latency-bound - tools/mac_sweep.cu: 1 accumulator
 // tops out at ~22 products/clk/SM, 16 accumulators at ~29 of the 32 peak).
 // ---------------------------------------------------------------------------
-// Flat grid, one pair per thread. (Measured on B200, r01: a persistent loop with an
-// exactly balanced pair range per CTA (48.2 us: the 2.77 pairs/thread quantisation moves
-// into the warps as partial last iterations), a persistent thread-stride
+// Flat grid, one pair per thread. (Measured on B200, r01: one-warp CTAs with the resident
+// warps per SM capped so the batch ends just below a whole wave (43.9 us), a persistent
+// loop with an exactly balanced pair range per CTA (48.2 us: the 2.77 pairs/thread
+// quantisation moves into the warps as partial last iterations), a persistent thread-stride
 // loop, and prefetching the next pair into L2 or into shared memory with cp.async, were
 // all slower than this - 48-54 us vs 43.6 us for config 3 - and a compute-only variant
 // with no loads ran at the same 43.5 us, i.e. the kernel is IMAD-issue bound, not
