@@ -144,12 +144,15 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
     }
 }
 
-// Persistent: every warp walks pairs gw, gw + nwarps, ... and prefetches the next
-// pair's operands into registers while the current one is on the tensor pipe.
-template <int NB>
+// Persistent: every warp walks pairs gw, gw + nwarps, ... with the next ST pairs'
+// operands in flight through the bulk-copy ring. (Measured r01: software-pipelining the
+// warp - pair k-1's epilogue and pair k+1's staging placed inside pair k's unrolled beta
+// loop, two staging buffers, column sums aliasing the dead buffer - is bit-exact but
+// slower at every size: C4 99.1 us vs 83.1 us, 128 registers.)
 #ifndef DOTG_IMMA_MINB16
 #define DOTG_IMMA_MINB16 1
 #endif
+template <int NB>
 __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b, size_t batch) {
