@@ -215,55 +215,67 @@ __global__ void __launch_bounds__(256) k_addsub_strided(uint64_t* out, const uin
     if (flags != nullptr) flags[pidx] = c;
 }
 
-// Interleaved layout [m][batch], limb-segmented: a CTA owns 64 consecutive pairs; warp w
-// of the CTA owns limbs [w*L, w*L + L) of those pairs, lane l the pairs 2l, 2l+1 (one
-// 128-bit load per limb row covers both: the warp reads 512 contiguous bytes per row).
+// Interleaved layout [m][batch], limb-segmented: a CTA owns 32 * PPL consecutive pairs;
+// warp w of the CTA owns limbs [w*L, w*L + L) of those pairs, lane l the pairs
+// PPL*l .. PPL*l + PPL - 1 (for PPL = 2 one 128-bit load per limb row covers both).
 // Each thread resolves its segment with carry-in 0 keeping the sums and g/p bits in
 // registers, publishes the segment's (G, P) per pair in shared memory, folds the (G, P)
 // of the lower segments of its pair into its carry-in, and only then stores - every
-// output written once. A batch of few long numbers gets S = ceil(m / L) warps per 64
-// pairs instead of one serial thread per pair.
-constexpr int kIL = 16;     // limbs per thread-segment
-constexpr int kIMaxS = 16;  // segments per CTA (m <= 256)
-
-template <bool SUB>
+// output written once. A batch of few long numbers gets S = ceil(m / L) warps per strip
+// of pairs instead of one serial thread per pair.
+constexpr int kPPL = 1;  // pairs per lane (2 with 128-bit row loads measured slower)
+template <int kIL, int kIMaxS, bool SUB>  // limbs per thread-segment, segments per CTA
 __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* out, const uint64_t* a,
                                                                      const uint64_t* b, uint32_t* flags,
                                                                      size_t m, size_t batch, bool vec_ok) {
-    __shared__ uint32_t sgp[kIMaxS][64];  // bit 0 G, bit 1 P per (segment, pair)
+    __shared__ uint32_t sgp[kIMaxS][32 * kPPL];  // bit 0 G, bit 1 P per (segment, pair)
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
     const int S = int(blockDim.x >> 5);
-    const size_t p = size_t(blockIdx.x) * 64 + size_t(2 * lane);  // first of the lane's two pairs
+    const size_t p = size_t(blockIdx.x) * (32 * kPPL) + size_t(kPPL * lane);  // lane's first pair
     const size_t i0 = size_t(w) * kIL;
     const int L = int(m - i0 < size_t(kIL) ? m - i0 : size_t(kIL));
-    const bool ok0 = p < batch, ok1 = p + 1 < batch;
-    const bool vec = ok1 && vec_ok;  // batch even and 16-byte aligned bases
-    uint64_t s[2][kIL];
-    uint32_t gm[2] = {0, 0}, pm[2] = {0, 0};  // per-limb generate / propagate bits
-    uint32_t G[2] = {0, 0}, P[2] = {1, 1};
+    bool ok[kPPL];
+#pragma unroll
+    for (int q = 0; q < kPPL; ++q) ok[q] = p + q < batch;
+    const bool vec = kPPL == 2 && ok[kPPL - 1] && vec_ok;  // batch even, 16-byte aligned bases
+    uint64_t s[kPPL][kIL];
+    uint32_t gm[kPPL], pm[kPPL];  // per-limb generate / propagate bits
+#pragma unroll
+    for (int q = 0; q < kPPL; ++q) gm[q] = pm[q] = 0;
 #pragma unroll
     for (int k = 0; k < kIL; ++k) {
         if (k < L) {
             const size_t off = (i0 + size_t(k)) * batch + p;
-            uint64_t x0 = 0, x1 = 0, y0 = 0, y1 = 0;
-            if (vec) {
-                asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(x0), "=l"(x1) : "l"(a + off));
-                asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(y0), "=l"(y1) : "l"(b + off));
-            } else {
-                if (ok0) { x0 = a[off]; y0 = b[off]; }
-                if (ok1) { x1 = a[off + 1]; y1 = b[off + 1]; }
+            uint64_t x[kPPL], y[kPPL];
+#pragma unroll
+            for (int q = 0; q < kPPL; ++q) x[q] = y[q] = 0;
+            if constexpr (kPPL == 2) {
+                if (vec) {
+                    asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                                 : "=l"(x[0]), "=l"(x[kPPL - 1]) : "l"(a + off));
+                    asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
+                                 : "=l"(y[0]), "=l"(y[kPPL - 1]) : "l"(b + off));
+                }
             }
-            uint32_t g0, p0, g1, p1;
-            s[0][k] = lane_op<SUB>(x0, y0, g0, p0);
-            s[1][k] = lane_op<SUB>(x1, y1, g1, p1);
-            gm[0] |= g0 << k;
-            pm[0] |= p0 << k;
-            gm[1] |= g1 << k;
-            pm[1] |= p1 << k;
+            if (!vec) {
+#pragma unroll
+                for (int q = 0; q < kPPL; ++q)
+                    if (ok[q]) {
+                        x[q] = a[off + q];
+                        y[q] = b[off + q];
+                    }
+            }
+#pragma unroll
+            for (int q = 0; q < kPPL; ++q) {
+                uint32_t gq, pq;
+                s[q][k] = lane_op<SUB>(x[q], y[q], gq, pq);
+                gm[q] |= gq << k;
+                pm[q] |= pq << k;
+            }
         }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kPPL; ++q) {
         uint32_t c = 0, all = 1;
 #pragma unroll
         for (int k = 0; k < kIL; ++k)
@@ -271,16 +283,14 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* ou
                 c = ((gm[q] >> k) & 1u) | (((pm[q] >> k) & 1u) & c);
                 all &= (pm[q] >> k) & 1u;
             }
-        G[q] = c;
-        P[q] = all;
-        sgp[w][2 * lane + q] = G[q] | (P[q] << 1);
+        sgp[w][kPPL * lane + q] = c | (all << 1);
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < kPPL; ++q) {
         uint32_t cin = 0;  // carry into this segment: fold lower segments of the pair
         for (int j = 0; j < w; ++j) {
-            const uint32_t v = sgp[j][2 * lane + q];
+            const uint32_t v = sgp[j][kPPL * lane + q];
             cin = (v & 1u) | (((v >> 1) & 1u) & cin);
         }
         uint32_t c = cin;
@@ -290,37 +300,52 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* ou
                 s[q][k] = apply_carry<SUB>(s[q][k], c);
                 c = ((gm[q] >> k) & 1u) | (((pm[q] >> k) & 1u) & c);
             }
-        if (w == S - 1 && flags != nullptr && (q ? ok1 : ok0)) flags[p + q] = c;
+        if (w == S - 1 && flags != nullptr && ok[q]) flags[p + q] = c;
     }
 #pragma unroll
     for (int k = 0; k < kIL; ++k) {
         if (k < L) {
             const size_t off = (i0 + size_t(k)) * batch + p;
-            if (vec) {
-                asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out + off), "l"(s[0][k]),
-                             "l"(s[1][k])
-                             : "memory");
-            } else {
-                if (ok0) out[off] = s[0][k];
-                if (ok1) out[off + 1] = s[1][k];
+            if constexpr (kPPL == 2) {
+                if (vec) {
+                    asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out + off), "l"(s[0][k]),
+                                 "l"(s[kPPL - 1][k])
+                                 : "memory");
+                    continue;
+                }
             }
+#pragma unroll
+            for (int q = 0; q < kPPL; ++q)
+                if (ok[q]) out[off + q] = s[q][k];
         }
     }
 }
 
 namespace {
 
-template <bool SUB>
+template <int kIL, int kIMaxS, bool SUB>
 cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                             size_t batch, cudaStream_t st) {
     const size_t S = (m + kIL - 1) / kIL;
-    const size_t blocks = (batch + 63) / 64;
+    const size_t blocks = (batch + 32 * kPPL - 1) / (32 * kPPL);
     const bool vec_ok = batch % 2 == 0 &&
                         ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
                           reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
-    k_addsub_interleaved<SUB><<<unsigned(blocks), unsigned(S * 32), 0, st>>>(out, a, b, flags, m, batch, vec_ok);
+    k_addsub_interleaved<kIL, kIMaxS, SUB><<<unsigned(blocks), unsigned(S * 32), 0, st>>>(out, a, b, flags, m,
+                                                                                        batch, vec_ok);
     count_launch();
     return cudaGetLastError();
+}
+
+// Interleaved problems by length (tools/layout_timing.py, B200, B x m = 2^22 limbs):
+// m < 128 thread-per-pair strided (5.2-6.6 TB/s); 128 <= m <= 256 8-limb segments, up to
+// 32 per CTA (4.0-4.3 TB/s vs 3.0 for 16-limb segments of two pairs per lane); 256 < m <=
+// 512 32-limb segments (2.0 TB/s vs 1.1 strided); longer numbers strided.
+template <bool SUB>
+cudaError_t run_interleaved_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                                size_t batch, cudaStream_t st) {
+    if (m <= 256) return run_interleaved<8, 32, SUB>(out, a, b, flags, m, batch, st);
+    return run_interleaved<32, 16, SUB>(out, a, b, flags, m, batch, st);
 }
 
 template <bool SUB>
@@ -389,9 +414,9 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             continue;
         }
         const int r = route(P, layouts[i]);
-        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= size_t(kIL) * kIMaxS) {
-            cudaError_t e = P.sub ? run_interleaved<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
-                                  : run_interleaved<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 512) {
+            cudaError_t e = P.sub ? run_interleaved_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                                  : run_interleaved_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
             if (e != cudaSuccess) return e;
             continue;
         }
