@@ -483,10 +483,61 @@ cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t*
 
 std::atomic<int> g_mul_route{0};
 
+// dst[c][r] = src[r][c] for a rows x cols u64 matrix: 32 x 32 tiles through shared
+// memory (coalesced on both sides; the 33-word row pitch keeps the column reads
+// conflict-free).
+static __global__ void __launch_bounds__(256) k_transpose_u64(const uint64_t* __restrict__ src, size_t rows, size_t cols,
+                                                       uint64_t* __restrict__ dst) {
+    __shared__ uint64_t tile[32][33];
+    const size_t r0 = size_t(blockIdx.y) * 32, c0 = size_t(blockIdx.x) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const size_t r = r0 + ty + k, c = c0 + tx;
+        if (r < rows && c < cols) tile[ty + k][tx] = __ldg(src + r * cols + c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const size_t c = c0 + ty + k, r = r0 + tx;
+        if (r < rows && c < cols) dst[c * rows + r] = tile[tx][ty + k];
+    }
+}
+
+static cudaError_t transpose_u64(const uint64_t* src, size_t rows, size_t cols, uint64_t* dst, cudaStream_t st) {
+    const dim3 grid(unsigned((cols + 31) / 32), unsigned((rows + 31) / 32));
+    if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+    k_transpose_u64<<<grid, 256, 0, st>>>(src, rows, cols, dst);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Interleaved [m][batch] products for m > 16 go through the row-major kernels: the
+// thread-per-pair kernel reading the interleaved layout directly is compute-serial per
+// pair (8-18x slower at m = 32 / 64, tools/mul_layout_timing.py), while three transposes
+// cost one extra pass over the operands and the product.
+static cudaError_t mul_interleaved_via_rows(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                     cudaStream_t st) {
+    retain_stream_pool();
+    uint64_t *ta = nullptr, *tb = nullptr, *to = nullptr;
+    cudaError_t e = cudaMallocAsync(&ta, batch * m * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&tb, batch * m * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&to, batch * 2 * m * 8, st);
+    if (e == cudaSuccess) e = transpose_u64(a, m, batch, ta, st);
+    if (e == cudaSuccess) e = transpose_u64(b, m, batch, tb, st);
+    if (e == cudaSuccess) e = launch_mul_batch(to, ta, tb, m, batch, 0, st);
+    if (e == cudaSuccess) e = transpose_u64(to, batch, 2 * m, out, st);
+    for (void* q : {static_cast<void*>(ta), static_cast<void*>(tb), static_cast<void*>(to)})
+        if (q != nullptr) cudaFreeAsync(q, st);
+    return e;
+}
+
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                              int layout, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     const bool al = aligned32(out) && aligned32(a) && aligned32(b);
+    if (layout == 1 && m > 16 && g_mul_route.load(std::memory_order_relaxed) != 1 && batch <= (size_t(65535) * 32))
+        return mul_interleaved_via_rows(out, a, b, m, batch, stream);
     // Tensor pipe where it beats the IMAD kernels (tools/mul_timing.py on B200: m = 32
     // 1.27x, 64 2.26x, 128 3.8x; at m = 8 / 16 the per-pair warp overhead loses to the
     // thread-per-pair IMAD kernels, so only a forced IMMA route takes them there).
