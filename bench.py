@@ -411,6 +411,21 @@ def run_ours(args, rank, world, dist):
                                "sub_gbs": call_bytes[i] / (per_single[i + 4] * 1e-3) / 1e9}
                 for i, x in enumerate(bufs)}
     traffic = traffic_table().get("C2_per_launch_bytes_grouped" if not args.ungrouped else "C2_per_launch_bytes")
+    # the same byte mix without carries: a plain 2-read / 1-write streaming add measured
+    # live (tools/stream_peak.cu) - the practical ceiling for this kernel's traffic
+    mix_peak = None
+    sp = os.path.join(ROOT, "tools", "build", "stream_peak")
+    if os.path.exists(sp) and rank == 0:
+        try:
+            import subprocess
+
+            r = subprocess.run([sp], capture_output=True, text=True, timeout=120)
+            probe = json.loads(r.stdout)
+            mix_peak = {"GBps": probe["add_2r1w"]["GBps"], "frac": achieved / probe["add_2r1w"]["GBps"],
+                        "copy_1r1w_GBps": probe["copy_1r1w"]["GBps"], "read_GBps": probe["read_2r"]["GBps"],
+                        "source": "tools/stream_peak.cu: out = a + b, 256-bit ld/st, 805 MB, best of 20"}
+        except Exception as e:  # noqa: BLE001
+            mix_peak = {"error": str(e)[:200]}
     # stress level of the sweep: AddSubStats counters of the reference's
     # w8 chunking, derived on the device from the step's own inputs and outputs
     stress = {}
@@ -512,7 +527,7 @@ def run_ours(args, rank, world, dist):
                      "kernel": "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
                      "algorithmic_bytes_per_launch": step_bytes / len(calls_meta),
                      "launch_us_avg": ms_step * 1e3 / len(calls_meta), "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "per_size": per_size},
+                     "per_size": per_size, "mix_peak": mix_peak},
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
         "gpu_launches": int(launches),
