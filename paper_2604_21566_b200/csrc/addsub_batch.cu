@@ -321,6 +321,95 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* ou
     }
 }
 
+// Row-major, any m (no power-of-two team shape): the batch is one flat limb array, so a
+// warp walks a task of whole pairs as 128-limb chunks (lane = 4 consecutive limbs, one
+// 256-bit load per operand when aligned) and resolves carries with the ballot mask
+// addition of the team kernels made *segmented*: a limb that starts a pair resets the
+// carry, so in the lane fold it clears both G and P (nothing crosses a pair boundary),
+// and the flag of a pair is the carry out of its last limb. Pair positions advance by
+// the precomputed 128 / m and 128 % m per chunk - no division in the loop.
+template <bool SUB>
+__global__ void __launch_bounds__(256) k_addsub_rows_any(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                         const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
+                                                         size_t batch, size_t ppt, size_t ntasks, bool vec) {
+    const int lane = threadIdx.x & 31;
+    const size_t nwarps = size_t(gridDim.x) * (blockDim.x >> 5);
+    const uint32_t mm = uint32_t(m);  // m < 2^32 (checked by the launcher)
+    const uint32_t q128 = 128u / mm, r128 = 128u % mm;
+    const uint32_t l4 = 4u * uint32_t(lane);
+    const uint32_t q_l = l4 / mm, r_l = l4 % mm;
+    for (size_t task = size_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); task < ntasks; task += nwarps) {
+        const size_t p0 = task * ppt;
+        const size_t p1 = p0 + ppt < batch ? p0 + ppt : batch;
+        const size_t end = p1 * m;
+        size_t pidx = p0 + q_l;  // pair of this lane's first limb in the current chunk
+        uint32_t pos = r_l;      // its position inside that pair
+        uint32_t cin = 0;        // carry into the chunk
+        for (size_t cb = p0 * m; cb < end; cb += 128) {
+            const size_t f = cb + l4;
+            uint64_t x[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
+            if (vec && f + 3 < end) {
+                ld_stream<4>(a + f, x);
+                ld_stream<4>(b + f, y);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (f + k < end) {
+                        x[k] = a[f + k];
+                        y[k] = b[f + k];
+                    }
+            }
+            uint64_t sv[4];
+            uint32_t g[4], pr[4], start = 0, last = 0;
+            uint32_t G = 0, P = 1;
+            {
+                uint32_t ps = pos;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool ok = f + k < end;
+                    sv[k] = lane_op<SUB>(x[k], y[k], g[k], pr[k]);
+                    if (!ok) g[k] = pr[k] = 0;
+                    if (ok && ps == 0) start |= 1u << k;
+                    if (ok && ps + 1 == mm) last |= 1u << k;
+                    if ((start >> k) & 1u) G = P = 0;  // a pair starts: nothing enters from below
+                    G = g[k] | (pr[k] & G);
+                    P &= pr[k];
+                    ps = ps + 1 == mm ? 0 : ps + 1;
+                }
+            }
+            const uint32_t Gm = __ballot_sync(0xffffffffu, G), Pm = __ballot_sync(0xffffffffu, P);
+            const uint64_t yv = ((uint64_t(Gm) << 1) | cin) + uint64_t(Pm);
+            uint32_t c = ((uint32_t(yv) ^ Pm) >> lane) & 1u;
+            cin = uint32_t(yv >> 32);
+            size_t pq = pidx;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if ((start >> k) & 1u) c = 0;
+                const uint64_t o = apply_carry<SUB>(sv[k], c);
+                c = g[k] | (pr[k] & c);
+                sv[k] = o;
+                if ((last >> k) & 1u) {
+                    if (flags != nullptr) flags[pq] = c;
+                    ++pq;
+                }
+            }
+            if (vec && f + 3 < end) {
+                st_stream<4>(out + f, sv);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (f + k < end) out[f + k] = sv[k];
+            }
+            pidx += q128;
+            pos += r128;
+            if (pos >= mm) {
+                pos -= mm;
+                ++pidx;
+            }
+        }
+    }
+}
+
 namespace {
 
 template <int kIL, int kIMaxS, bool SUB>
@@ -358,6 +447,33 @@ cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
 }
 
 bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+template <bool SUB>
+cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                         size_t batch, cudaStream_t st) {
+    // tasks of whole pairs, ~512 limbs each, with a limb count that keeps every task start
+    // 4-limb (32-byte) aligned so the 256-bit path applies throughout
+    size_t ppt = m >= 512 ? 1 : 512 / m;
+    const size_t g4 = (m % 4 == 0) ? 1 : (m % 2 == 0 ? 2 : 4);  // pairs per 4-limb alignment
+    ppt = (ppt + g4 - 1) / g4 * g4;
+    const bool vec = (ppt * m) % 4 == 0 && aligned(out, 32) && aligned(a, 32) && aligned(b, 32);
+    const size_t ntasks = (batch + ppt - 1) / ppt;
+    static thread_local struct { int dev = -1, cap = 0; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_addsub_rows_any<SUB>, 256, 0);
+        di.cap = sms * (per > 0 ? per : 1);
+        di.dev = dev;
+    }
+    const size_t need = (ntasks + 7) / 8;
+    const unsigned grid = unsigned(need < size_t(di.cap) ? need : size_t(di.cap));
+    k_addsub_rows_any<SUB><<<grid, 256, 0, st>>>(out, a, b, flags, m, batch, ppt, ntasks, vec);
+    count_launch();
+    return cudaGetLastError();
+}
 bool pow2(size_t m) { return m != 0 && (m & (m - 1)) == 0; }
 
 // 0: team-small kernel, 1: team-big (m = 512), 2: strided kernel
@@ -417,6 +533,13 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
         if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 512) {
             cudaError_t e = P.sub ? run_interleaved_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                                   : run_interleaved_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        if (r == 2 && layouts[i] == 0 && P.m >= 3 && P.m < (size_t(1) << 31) &&
+            aligned(P.out, 8) && aligned(P.a, 8) && aligned(P.b, 8)) {
+            cudaError_t e = P.sub ? run_rows_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                                  : run_rows_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
             if (e != cudaSuccess) return e;
             continue;
         }
