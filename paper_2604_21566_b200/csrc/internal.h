@@ -56,6 +56,9 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
 bool mul_imma_supported(size_t m);
 cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st);
+// Even 16 < m < 128, 16-byte aligned rows: zero-extended to the next tensor-pipe size.
+cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st);
 // Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
 extern std::atomic<int> g_mul_route;
 
@@ -69,6 +72,10 @@ cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint6
 // m padded to base * 2^L (base a tensor-pipe size); L = 0 pads the rows and multiplies.
 cudaError_t launch_karatsuba_padded(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                     size_t base, cudaStream_t st);
+// Rows copied into aligned temporaries zero-extended to mp >= m limbs, multiplied there,
+// low 2m limbs of each product kept (any alignment of out / a / b).
+cudaError_t mul_padded_rows(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, size_t mp,
+                            cudaStream_t st);
 // Keep freed stream-ordered scratch cached in the device pool (per host thread, device).
 void retain_stream_pool();
 

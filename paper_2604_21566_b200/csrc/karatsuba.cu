@@ -129,13 +129,30 @@ __global__ void __launch_bounds__(kKaraWarps * 32) k_kara_combine_w(const uint64
     }
 }
 
-// dst[r][0:nd) = src[r][0:ns) zero-extended or truncated (warp per row, coalesced).
-__global__ void __launch_bounds__(kKaraWarps * 32) k_copy_rows(const uint64_t* __restrict__ src, size_t ns,
-                                                               uint64_t* __restrict__ dst, size_t nd, size_t rows) {
-    const int lane = threadIdx.x & 31;
-    const size_t r = size_t(blockIdx.x) * kKaraWarps + (threadIdx.x >> 5);
-    if (r >= rows) return;
-    for (size_t i = lane; i < nd; i += 32) dst[r * nd + i] = i < ns ? __ldg(src + r * ns + i) : 0ull;
+// dst[r][0:nd) = src[r][0:ns) zero-extended or truncated: one thread per destination
+// limb over the flat [rows][nd] array (coalesced stores; the row index comes from a 32-bit
+// division when the array is small enough, which covers every batch that fits in HBM
+// for the row widths this serves).
+__global__ void __launch_bounds__(256) k_copy_rows(const uint64_t* __restrict__ src, size_t ns,
+                                                   uint64_t* __restrict__ dst, size_t nd, size_t rows) {
+    const size_t total = rows * nd;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        size_t r, c;
+        if (total < (size_t(1) << 32)) {
+            r = uint32_t(i) / uint32_t(nd);
+            c = uint32_t(i) - uint32_t(r) * uint32_t(nd);
+        } else {
+            r = i / nd;
+            c = i - r * nd;
+        }
+        dst[i] = c < ns ? __ldg(src + r * ns + c) : 0ull;
+    }
+}
+
+unsigned copy_grid(size_t rows, size_t nd) {
+    const size_t need = (rows * nd + 255) / 256;
+    return unsigned(need < size_t(148 * 16) ? need : size_t(148 * 16));
 }
 
 // The level sizes of a descent: parent m_i (the limbs actually read), half h_i.
@@ -229,6 +246,33 @@ void retain_stream_pool() {
     pool_dev = dev;
 }
 
+// Copy the rows into aligned temporaries zero-extended to mp >= m limbs, multiply there
+// (row-major fast kernels need 32-byte aligned rows of their own sizes), keep the low 2m
+// limbs of each product. Any alignment of out / a / b.
+cudaError_t mul_padded_rows(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, size_t mp,
+                            cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    retain_stream_pool();
+    uint64_t *pa = nullptr, *pb = nullptr, *po = nullptr;
+    cudaError_t e = cudaMallocAsync(&pa, batch * mp * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pb, batch * mp * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&po, batch * 2 * mp * 8, st);
+    if (e == cudaSuccess) {
+        k_copy_rows<<<copy_grid(batch, mp), 256, 0, st>>>(a, m, pa, mp, batch);
+        k_copy_rows<<<copy_grid(batch, mp), 256, 0, st>>>(b, m, pb, mp, batch);
+        count_launch(2);
+        e = launch_mul_batch(po, pa, pb, mp, batch, 0, st);
+    }
+    if (e == cudaSuccess) {
+        k_copy_rows<<<copy_grid(batch, 2 * m), 256, 0, st>>>(po, 2 * mp, out, 2 * m, batch);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    for (void* q : {static_cast<void*>(pa), static_cast<void*>(pb), static_cast<void*>(po)})
+        if (q != nullptr) cudaFreeAsync(q, st);
+    return e;
+}
+
 // Reference recursion (kara_rec, mul.cpp:176-233): split h = ceil(m / 2) until m <= theta.
 cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                    size_t theta, cudaStream_t st) {
@@ -258,26 +302,7 @@ cudaError_t launch_karatsuba_padded(uint64_t* out, const uint64_t* a, const uint
     }
     if (levels == 0) {
         if (m == mp) return launch_mul_batch(out, a, b, m, batch, 0, st);
-        // zero-pad the rows to the tensor-pipe size, multiply, keep the low 2m limbs
-        uint64_t *pa = nullptr, *pb = nullptr, *po = nullptr;
-        cudaError_t e = cudaMallocAsync(&pa, batch * mp * 8, st);
-        if (e == cudaSuccess) e = cudaMallocAsync(&pb, batch * mp * 8, st);
-        if (e == cudaSuccess) e = cudaMallocAsync(&po, batch * 2 * mp * 8, st);
-        const unsigned grid = unsigned((batch + kKaraWarps - 1) / kKaraWarps);
-        if (e == cudaSuccess) {
-            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(a, m, pa, mp, batch);
-            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(b, m, pb, mp, batch);
-            count_launch(2);
-            e = launch_mul_batch(po, pa, pb, mp, batch, 0, st);
-        }
-        if (e == cudaSuccess) {
-            k_copy_rows<<<grid, kKaraWarps * 32, 0, st>>>(po, 2 * mp, out, 2 * m, batch);
-            count_launch();
-            e = cudaGetLastError();
-        }
-        for (void* q : {static_cast<void*>(pa), static_cast<void*>(pb), static_cast<void*>(po)})
-            if (q != nullptr) cudaFreeAsync(q, st);
-        return e;
+        return mul_padded_rows(out, a, b, m, batch, mp, st);
     }
     KaraPlan plan;
     size_t cm = m, full = mp;

@@ -274,9 +274,11 @@ __global__ void __launch_bounds__(128) k_mul_smem(uint64_t* out, const uint64_t*
 // all slower than this - 48-54 us vs 43.6 us for config 3 - and a compute-only variant
 // with no loads ran at the same 43.5 us, i.e. the kernel is IMAD-issue bound, not
 // memory bound: ~25.5 products/clk/SM while SMs are active.)
-template <int M>
+// RT: the pairs are mr < M limbs (rows of mr limbs, any 8-byte alignment), computed as
+// M-limb products of zero-extended operands; only the 2 mr product limbs are stored.
+template <int M, bool RT = false>
 __global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_t* a, const uint64_t* b,
-                                                    size_t batch) {
+                                                    size_t batch, int mr = M) {
     constexpr int N = 2 * M;         // words per operand
     constexpr int NB = N / kK;       // a-blocks
     constexpr int NS = 2 * N / kK;   // output blocks
@@ -285,17 +287,29 @@ __global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_
     if (pidx >= batch) return;
     {
         uint32_t A[N], B[N];
+        if constexpr (RT) {
 #pragma unroll
-        for (int v = 0; v < M / 4; ++v) {
-            uint64_t x[4], y[4];
-            ld_stream<4>(a + pidx * M + 4 * v, x);
-            ld_stream<4>(b + pidx * M + 4 * v, y);
+            for (int i = 0; i < M; ++i) {
+                const uint64_t x = i < mr ? __ldg(a + pidx * mr + i) : 0ull;
+                const uint64_t y = i < mr ? __ldg(b + pidx * mr + i) : 0ull;
+                A[2 * i] = lo32(x);
+                A[2 * i + 1] = hi32(x);
+                B[2 * i] = lo32(y);
+                B[2 * i + 1] = hi32(y);
+            }
+        } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                A[8 * v + 2 * k] = lo32(x[k]);
-                A[8 * v + 2 * k + 1] = hi32(x[k]);
-                B[8 * v + 2 * k] = lo32(y[k]);
-                B[8 * v + 2 * k + 1] = hi32(y[k]);
+            for (int v = 0; v < M / 4; ++v) {
+                uint64_t x[4], y[4];
+                ld_stream<4>(a + pidx * M + 4 * v, x);
+                ld_stream<4>(b + pidx * M + 4 * v, y);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    A[8 * v + 2 * k] = lo32(x[k]);
+                    A[8 * v + 2 * k + 1] = hi32(x[k]);
+                    B[8 * v + 2 * k] = lo32(y[k]);
+                    B[8 * v + 2 * k + 1] = hi32(y[k]);
+                }
             }
         }
         uint32_t cr0 = 0, cr1 = 0, cr2 = 0;
@@ -335,9 +349,18 @@ __global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_
             o0[k] = uint64_t(w[2 * k]) | (uint64_t(w[2 * k + 1]) << 32);
             o1[k] = uint64_t(w[8 + 2 * k]) | (uint64_t(w[8 + 2 * k + 1]) << 32);
         }
-        uint64_t* po = out + pidx * (2 * M) + size_t(s) * (kK / 2);
-        st_stream<4>(po, o0);
-        st_stream<4>(po + 4, o1);
+        if constexpr (RT) {
+            uint64_t* po = out + pidx * (2 * size_t(mr));
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int limb = s * (kK / 2) + k;
+                if (limb < 2 * mr) po[limb] = k < 4 ? o0[k] : o1[k - 4];
+            }
+        } else {
+            uint64_t* po = out + pidx * (2 * M) + size_t(s) * (kK / 2);
+            st_stream<4>(po, o0);
+            st_stream<4>(po + 4, o1);
+        }
     }
     }
 }
@@ -391,6 +414,15 @@ cudaError_t run_regblk(uint64_t* out, const uint64_t* a, const uint64_t* b, size
     return cudaGetLastError();
 }
 
+template <int M>
+cudaError_t run_regblk_rt(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                          cudaStream_t st) {
+    const size_t blocks = (batch + 127) / 128;
+    k_mul_regblk<M, true><<<unsigned(blocks), 128, 0, st>>>(out, a, b, batch, int(m));
+    count_launch();
+    return cudaGetLastError();
+}
+
 // Pairs per group (= threads per CTA) chosen so that two CTAs fill the SM's shared
 // memory and the batch splits into whole rounds of groups across all SMs.
 template <int M>
@@ -438,6 +470,7 @@ cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, siz
 }
 
 bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ---------------------------------------------------------------------------
 // Unsaturated 52-bit radix (RadixConfig kUnsaturated, limbs.hpp:39-49): the generic
@@ -542,13 +575,22 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     // 1.27x, 64 2.26x, 128 3.8x; at m = 8 / 16 the per-pair warp overhead loses to the
     // thread-per-pair IMAD kernels, so only a forced IMMA route takes them there).
     const int route = g_mul_route.load(std::memory_order_relaxed);
-    if (layout == 0 && al && mul_imma_supported(m) && route != 1 && (route == 2 || m >= 32))
-        return launch_mul_imma(out, a, b, m, batch, stream);
+    if (layout == 0 && mul_imma_supported(m) && route != 1 && (route == 2 || m >= 32))
+        return al ? launch_mul_imma(out, a, b, m, batch, stream) : mul_padded_rows(out, a, b, m, batch, m, stream);
     // Sizes without a dedicated kernel: 16 < m < 128 zero-pads to the next tensor-pipe
     // size; m > 128 runs padded Karatsuba down to m = 128 tensor-pipe leaves (the generic
-    // thread-per-pair kernel would be 100x slower there: tools/kara_timing.py).
-    if (layout == 0 && al && route != 1 && m > 16 && !mul_imma_supported(m))
+    // thread-per-pair kernel would be 100x slower there: tools/kara_timing.py). Both copy
+    // the rows, so any alignment works.
+    if (layout == 0 && route != 1 && m > 16 && m < 128 && m % 2 == 0 && aligned16(out) && aligned16(a) &&
+        aligned16(b))
+        return launch_mul_imma_rt(out, a, b, m, batch, stream);
+    if (layout == 0 && route != 1 && m > 16 && !mul_imma_supported(m))
         return launch_karatsuba_padded(out, a, b, m, batch, m <= 32 ? 32 : (m <= 64 ? 64 : 128), stream);
+    // 4 < m < 16 off the power-of-two kernels, or misaligned rows of 5..16: the register
+    // kernels of the next size with zero-extended operands, any alignment
+    // (tools/odd_m_mul_timing.py: m = 12 92 us vs 492 us thread-per-pair generic).
+    if (layout == 0 && route != 1 && m > 4 && m <= 16 && (!al || (m & (m - 1)) != 0))
+        return m <= 8 ? run_regblk_rt<8>(out, a, b, m, batch, stream) : run_regblk_rt<16>(out, a, b, m, batch, stream);
     if (layout == 1) {
         switch (m) {
             case 1: return run_regs<1, 1>(out, a, b, batch, stream);

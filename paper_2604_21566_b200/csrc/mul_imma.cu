@@ -155,7 +155,11 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 template <int NB>
 __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
-                                                              const uint64_t* __restrict__ b, size_t batch) {
+                                                              const uint64_t* __restrict__ b, size_t batch,
+                                                              int mr) {
+    // mr < M: rows of mr limbs (mr even, 16-byte aligned rows), zero-extended in the raw
+    // ring to M limbs - only the first 8 mr bytes of a slot are ever loaded, the rest stays
+    // zero - and only 2 mr product limbs are stored.
     using C = ImmaCfg<NB>;
     extern __shared__ __align__(16) uint32_t smem_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,15 +171,18 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
     __shared__ uint64_t bars[kImmaWarps][C::ST];
     uint64_t* bar = bars[warp];
     for (int i = lane; i < C::COPY_WORDS + C::A_WORDS; i += 32) cp[i] = 0;  // padding stays zero
+    if (mr < C::M)
+        for (int i = lane; i < C::RAW_WORDS; i += 32) raw[i] = 0;
+    __syncwarp();
 
     const size_t nwarps = size_t(gridDim.x) * kImmaWarps;
     const size_t first = size_t(blockIdx.x) * kImmaWarps + warp;
-    constexpr uint32_t kOpBytes = C::NW * 4u;  // bytes per operand
+    const uint32_t kOpBytes = uint32_t(mr) * 8u;  // bytes per operand row
     auto issue = [&](int stage, size_t p) {  // lane 0 only
         uint32_t* dst = raw + stage * 2 * C::NW;
         mbar_expect_tx(&bar[stage], 2 * kOpBytes);
-        bulk_load(dst, a + p * C::M, kOpBytes, &bar[stage]);
-        bulk_load(dst + C::NW, b + p * C::M, kOpBytes, &bar[stage]);
+        bulk_load(dst, a + p * size_t(mr), kOpBytes, &bar[stage]);
+        bulk_load(dst + C::NW, b + p * size_t(mr), kOpBytes, &bar[stage]);
     };
     if (lane == 0) {
         for (int st = 0; st < C::ST; ++st) mbar_init(&bar[st]);
@@ -325,15 +332,16 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
             lo[k] = sv;
         }
         if (active) {
-            uint64_t* po = out + pair * C::OUT_LIMBS + lane;
+            uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
 #pragma unroll
-            for (int k = 0; k < C::LPL; ++k) po[32 * k] = lo[k];
+            for (int k = 0; k < C::LPL; ++k)
+                if (lane + 32 * k < 2 * mr) po[32 * k] = lo[k];
         }
     }
 }
 
 template <int NB>
-cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, cudaStream_t st) {
+cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, int mr, cudaStream_t st) {
     using C = ImmaCfg<NB>;
     const size_t smem = size_t(kImmaWarps) * C::WARP_WORDS * sizeof(uint32_t);
     // per (host thread, device): the smem opt-in is a per-device function attribute
@@ -354,7 +362,7 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
     }
     const size_t need = (batch + kImmaWarps - 1) / kImmaWarps;
     const size_t grid = need < size_t(di.grid_cap) ? need : size_t(di.grid_cap);
-    k_mul_imma<NB><<<unsigned(grid), kImmaWarps * 32, smem, st>>>(out, a, b, batch);
+    k_mul_imma<NB><<<unsigned(grid), kImmaWarps * 32, smem, st>>>(out, a, b, batch, mr);
     count_launch();
     return cudaGetLastError();
 }
@@ -366,14 +374,27 @@ bool mul_imma_supported(size_t m) { return m == 8 || m == 16 || m == 32 || m == 
 cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
+    const int mr = int(m);
     switch (m) {
-        case 8: return run_imma<2>(out, a, b, batch, st);
-        case 16: return run_imma<4>(out, a, b, batch, st);
-        case 32: return run_imma<8>(out, a, b, batch, st);
-        case 64: return run_imma<16>(out, a, b, batch, st);
-        case 128: return run_imma<32>(out, a, b, batch, st);
+        case 8: return run_imma<2>(out, a, b, batch, mr, st);
+        case 16: return run_imma<4>(out, a, b, batch, mr, st);
+        case 32: return run_imma<8>(out, a, b, batch, mr, st);
+        case 64: return run_imma<16>(out, a, b, batch, mr, st);
+        case 128: return run_imma<32>(out, a, b, batch, mr, st);
         default: return cudaErrorNotSupported;
     }
+}
+
+// Even 16 < m < 128 with 16-byte aligned rows: the next tensor-pipe size's kernel with the
+// operand rows zero-extended in shared memory (no padded copies in HBM).
+cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    if (m % 2 != 0 || m <= 16 || m >= 128) return cudaErrorNotSupported;
+    const int mr = int(m);
+    if (m <= 32) return run_imma<8>(out, a, b, batch, mr, st);
+    if (m <= 64) return run_imma<16>(out, a, b, batch, mr, st);
+    return run_imma<32>(out, a, b, batch, mr, st);
 }
 
 }  // namespace dotg
