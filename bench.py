@@ -46,18 +46,12 @@ DATA = ("synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: li
         "1% forced full carry chains, sub swapped to a>=b)")
 
 
-def c2_config(ungrouped=False, working_set=None, reference=False):
-    if reference:
-        step = "the reference's span-form dot_add_words/dot_sub_words (Width::w8) over every pair, all host threads"
-    elif ungrouped:
-        step = "8 launches: add at 4 sizes then sub at 4 sizes"
-    else:
-        step = "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"
+def c2_config(ungrouped=False, working_set=None):
     cfg = {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
            "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
-           "step": step,
-           "per_rank": ("rank 0 only (host CPU)" if reference else
-                        "full sweep on every rank (weak scaling, no collective)")}
+           "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if ungrouped else
+                    "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"),
+           "per_rank": "full sweep on every rank (weak scaling, no collective)"}
     if working_set is not None:
         cfg["l2"] = (f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct inputs "
                      "(126 MB L2), every buffer touched once per step")
@@ -308,7 +302,7 @@ def run_reference(args, rank, world):
         "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": DATA,
-        "config": c2_config(reference=True),
+        "config": c2_config(),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
                          "sample": f"full C2 step (add+sub, 4 sizes) x {args.steps} steps; route {cpu.note}"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
