@@ -536,6 +536,14 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             if (e != cudaSuccess) return e;
             continue;
         }
+        // long numbers: two tiles (8192 limbs) or more each -> the tiled long-number passes
+        // for the whole batch (a warp walking a pair's chunks serially would leave the GPU
+        // idle for batches of a few numbers: tools/long_batch_timing.py)
+        if (layouts[i] == 0 && P.m >= 8192 && P.batch <= 65535) {
+            cudaError_t e = launch_long_batch(P.sub != 0, P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
         if (r == 2 && layouts[i] == 0 && P.m >= 3 && P.m < (size_t(1) << 31) &&
             aligned(P.out, 8) && aligned(P.a, 8) && aligned(P.b, 8)) {
             cudaError_t e = P.sub ? run_rows_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)

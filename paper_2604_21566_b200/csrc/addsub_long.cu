@@ -53,9 +53,15 @@ size_t num_tiles(size_t m) { return (m + kTile - 1) / kTile; }
 template <bool SUB, bool VEC>
 __global__ void __launch_bounds__(kThreads) k_long_local(uint64_t* out, const uint64_t* a,
                                                          const uint64_t* b, size_t m,
-                                                         uint32_t* state) {
+                                                         uint32_t* state, size_t sw) {
     __shared__ uint32_t sG[kWords], sP[kWords], sC[kWords];
     __shared__ uint32_t s_pt;
+    // grid.y = independent numbers of m limbs each (batch of long numbers), state regions
+    // of sw words apiece; grid.y = 1 for the single number / shard
+    out += size_t(blockIdx.y) * m;
+    a += size_t(blockIdx.y) * m;
+    b += size_t(blockIdx.y) * m;
+    state += size_t(blockIdx.y) * sw;
     const size_t tile = blockIdx.x;
     const size_t L0 = tile * size_t(kTile);
     const size_t len = (m - L0) < size_t(kTile) ? (m - L0) : size_t(kTile);
@@ -184,8 +190,11 @@ constexpr int kChunk = 1024;  // tiles per scan chunk (one CTA of pass 2)
 
 // Pass 2a: one CTA per chunk of 1024 tiles. Each tile gets its exclusive (g, p) relative
 // to the chunk start; each chunk its aggregate (bit 0 G, bit 1 P).
-__global__ void __launch_bounds__(kChunk) k_long_scan_chunks(uint32_t* state, size_t n, uint32_t* chunk_agg) {
+__global__ void __launch_bounds__(kChunk) k_long_scan_chunks(uint32_t* state, size_t n, uint32_t* chunk_agg,
+                                                              size_t sw) {
     __shared__ uint32_t swg[32], swp[32];
+    state += size_t(blockIdx.y) * sw;
+    chunk_agg += size_t(blockIdx.y) * sw;
     const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const size_t t = size_t(blockIdx.x) * kChunk + tid;
     const uint32_t st = t < n ? state[t] : kBitP;  // identity (G = 0, P = 1) past the end
@@ -225,7 +234,10 @@ __device__ __forceinline__ void chunk_prefix(const uint32_t* chunk_agg, size_t c
 }
 
 // Pass 2b: shard aggregate {G, P} = composition of all chunk aggregates.
-__global__ void __launch_bounds__(32) k_long_shard_agg(const uint32_t* chunk_agg, size_t nchunks, uint32_t* agg) {
+__global__ void __launch_bounds__(32) k_long_shard_agg(const uint32_t* chunk_agg, size_t nchunks, uint32_t* agg,
+                                                       size_t sw) {
+    chunk_agg += size_t(blockIdx.y) * sw;
+    agg += 2 * size_t(blockIdx.y);
     uint32_t g, p;
     chunk_prefix(chunk_agg, nchunks, threadIdx.x, g, p);
     if (threadIdx.x == 0) {
@@ -240,7 +252,13 @@ template <bool SUB>
 __global__ void __launch_bounds__(256) k_long_finish(uint64_t* out, size_t m, const uint32_t* state,
                                                      const uint32_t* chunk_agg, size_t n,
                                                      const uint32_t* all_aggs, int rank, int world,
-                                                     uint32_t* carry_out) {
+                                                     uint32_t* carry_out, size_t sw) {
+    // grid.y > 1: a batch of independent numbers (world = 1, own aggregate, own carry)
+    out += size_t(blockIdx.y) * m;
+    state += size_t(blockIdx.y) * sw;
+    chunk_agg += size_t(blockIdx.y) * sw;
+    all_aggs += 2 * size_t(blockIdx.y);
+    if (carry_out != nullptr) carry_out += blockIdx.y;
     uint32_t x = 0;  // carry into this shard
     uint32_t total = 0;
     for (int q = 0; q < world; ++q) {
@@ -316,20 +334,20 @@ cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const 
     if (n > 0xffffffffull) return cudaErrorInvalidValue;
     const unsigned grid = unsigned(n);
     if (sub) {
-        if (vec) k_long_local<true, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
-        else k_long_local<true, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+        if (vec) k_long_local<true, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st, 0);
+        else k_long_local<true, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st, 0);
     } else {
-        if (vec) k_long_local<false, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
-        else k_long_local<false, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st);
+        if (vec) k_long_local<false, true><<<grid, kThreads, 0, stream>>>(out, a, b, m, st, 0);
+        else k_long_local<false, false><<<grid, kThreads, 0, stream>>>(out, a, b, m, st, 0);
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     uint32_t* chunk_agg = st + state_words(n);
     const size_t nch = num_chunks(n);
-    k_long_scan_chunks<<<unsigned(nch), kChunk, 0, stream>>>(st, n, chunk_agg);
+    k_long_scan_chunks<<<unsigned(nch), kChunk, 0, stream>>>(st, n, chunk_agg, 0);
     count_launch();
-    k_long_shard_agg<<<1, 32, 0, stream>>>(chunk_agg, nch, agg);
+    k_long_shard_agg<<<1, 32, 0, stream>>>(chunk_agg, nch, agg, 0);
     count_launch();
     return cudaGetLastError();
 }
@@ -344,12 +362,51 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
     const uint32_t* chunk_agg = st + state_words(n);
     if (sub)
         k_long_finish<true><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, chunk_agg, n, all_aggs, rank,
-                                                                  world, carry_out);
+                                                                  world, carry_out, 0);
     else
         k_long_finish<false><<<unsigned(blocks), 256, 0, stream>>>(out, m, st, chunk_agg, n, all_aggs, rank,
-                                                                   world, carry_out);
+                                                                   world, carry_out, 0);
     count_launch();
     return cudaGetLastError();
+}
+
+// A batch of long numbers (row-major [batch][m]): the three passes once for all of them,
+// grid.y = number; each number is its own single "shard" (world 1), its carry its flag.
+cudaError_t launch_long_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                              size_t m, size_t batch, cudaStream_t stream) {
+    if (batch == 0 || m == 0) return cudaErrorInvalidValue;
+    if (batch > 65535) return cudaErrorInvalidConfiguration;
+    const size_t n = num_tiles(m);
+    const size_t sw = long_state_bytes(m) / sizeof(uint32_t);  // words per number (64-aligned pad inside)
+    retain_stream_pool();
+    uint32_t* st = nullptr;
+    cudaError_t e = cudaMallocAsync(&st, (batch * sw + 2 * batch) * sizeof(uint32_t), stream);
+    if (e != cudaSuccess) return e;
+    uint32_t* aggs = st + batch * sw;
+    const bool vec = (m % 4 == 0) && (reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                                      reinterpret_cast<uintptr_t>(b)) % 32 == 0;
+    const dim3 g1{unsigned(n), unsigned(batch), 1u};
+    if (sub) {
+        if (vec) k_long_local<true, true><<<g1, kThreads, 0, stream>>>(out, a, b, m, st, sw);
+        else k_long_local<true, false><<<g1, kThreads, 0, stream>>>(out, a, b, m, st, sw);
+    } else {
+        if (vec) k_long_local<false, true><<<g1, kThreads, 0, stream>>>(out, a, b, m, st, sw);
+        else k_long_local<false, false><<<g1, kThreads, 0, stream>>>(out, a, b, m, st, sw);
+    }
+    const size_t nch = num_chunks(n);
+    uint32_t* chunk_agg = st + state_words(n);
+    k_long_scan_chunks<<<dim3(unsigned(nch), unsigned(batch)), kChunk, 0, stream>>>(st, n, chunk_agg, sw);
+    k_long_shard_agg<<<dim3(1, unsigned(batch)), 32, 0, stream>>>(chunk_agg, nch, aggs, sw);
+    const size_t warps = (n + 31) / 32;
+    const dim3 g3{unsigned((warps * 32 + 255) / 256), unsigned(batch), 1u};
+    if (sub)
+        k_long_finish<true><<<g3, 256, 0, stream>>>(out, m, st, chunk_agg, n, aggs, 0, 1, flags, sw);
+    else
+        k_long_finish<false><<<g3, 256, 0, stream>>>(out, m, st, chunk_agg, n, aggs, 0, 1, flags, sw);
+    count_launch(4);
+    e = cudaGetLastError();
+    cudaFreeAsync(st, stream);
+    return e;
 }
 
 }  // namespace dotg

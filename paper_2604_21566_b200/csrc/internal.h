@@ -48,6 +48,10 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
                                const uint32_t* all_aggs, int rank, int world,
                                uint32_t* carry_out, cudaStream_t stream);
 
+// A batch of long numbers (row-major, m >= 1 tile): the tiled passes with grid.y = number.
+cudaError_t launch_long_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                              size_t m, size_t batch, cudaStream_t stream);
+
 // Batched multiplication (exactly 2m output limbs per pair).
 cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                              size_t batch, int layout, cudaStream_t stream);

@@ -150,3 +150,30 @@ def test_config5_full_size(cuda, oracle):
         assert total == wf and np.array_equal(host(out), want)
         del out, a, b
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("m,batch", [(8192, 3), (8193, 5), (12345, 2), (40000, 4), (65536, 1)])
+def test_long_batch_route(cuda, oracle, m, batch):
+    """Batches of long numbers (m >= 8192) take the tiled long-number passes with one grid
+    row per number: carries across tile boundaries inside each number, none across numbers,
+    each number's carry its flag; sub included, with propagate runs over tile edges."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(77 + m + batch)
+    a = rng.integers(0, 2**64, size=(batch, m), dtype=np.uint64)
+    b = rng.integers(0, 2**64, size=(batch, m), dtype=np.uint64)
+    MAXV = np.uint64(0xFFFFFFFFFFFFFFFF)
+    a[0, 100:m - 3] = MAXV  # long propagate run across every tile of number 0
+    b[0, 100:m - 3] = 0
+    b[0, 99] = MAXV
+    a[0, 99] = 1
+    if batch > 1:
+        a[1, :] = MAXV  # full chain with carry out
+        b[1, :] = 0
+        b[1, 0] = 1
+    for sub in (False, True):
+        want, wf = oracle.addsub_batch(sub, a, b)
+        out, fl = dg.addsub_batch(sub, torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (m, batch, sub)
+        assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf), (m, batch, sub)
