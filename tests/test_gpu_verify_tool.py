@@ -5,6 +5,7 @@ corpus reports the mismatching case ids with exit code 1; malformed input exits 
 import os
 import subprocess
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -48,3 +49,29 @@ def test_malformed_input(cuda, tmp_path):
     assert r.returncode == 2 and "parse error at line 1" in r.stderr
     assert run("verify", str(tmp_path / "missing.jsonl")).returncode == 2
     assert run("verify", CORPUS, "--width", "16").returncode == 2
+
+
+def _hex_limbs(text, m):
+    v = int(text, 16)
+    return np.array([(v >> (64 * i)) & ((1 << 64) - 1) for i in range(m)], dtype=np.uint64)
+
+
+@pytest.mark.parametrize("width", ["8", "4", "2", "scalar"])
+def test_stats_line_matches_reference(cuda, ref, width):
+    """The AddSubStats line (dotarith verify prints it for the vector add/sub kernels,
+    bench.cpp:160-161) equals the reference's own counters summed over the corpus."""
+    import json
+
+    w = 0 if width == "scalar" else int(width)
+    chunks = fires = 0
+    for line in open(CORPUS):
+        c = json.loads(line)
+        if c["op"] == "mul":
+            continue
+        m = c["bits"] // 64
+        _, _, ch, fi = ref.words(c["op"] == "sub", _hex_limbs(c["a"], m), _hex_limbs(c["b"], m), w)
+        chunks += ch
+        fires += fi
+    r = run("verify", CORPUS, "--width", width)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"chunks {chunks}, phase4 triggers {fires} (rate {fires / chunks:.6f})" in r.stdout, r.stdout

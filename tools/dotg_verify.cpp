@@ -6,8 +6,9 @@
 // each group is ONE batched call (dotg_add_batch_host / dotg_sub_batch_host /
 // dotg_mul_batch_host), instead of the reference's per-case loop (bench.cpp:147-170).
 // Output and exit codes follow `dotarith verify` (tools/dotarith_cli.cpp:57-82):
-//   "kernel b200 (w=8, sm_100a): N cases, K mismatches", up to 10 "mismatch at case i"
-//   lines, exit 0 = all match, 1 = mismatch, 2 = usage / input error.
+//   "kernel b200 (w=8, sm_100a): N cases, K mismatches", the AddSubStats line
+//   "chunks C, phase4 triggers T (rate R)" when the corpus has add/sub cases, up to 10
+//   "mismatch at case i" lines, exit 0 = all match, 1 = mismatch, 2 = usage / input error.
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
@@ -206,9 +207,26 @@ int main(int argc, char** argv) {
             if (!ok) bad.push_back(ids[k]);
         }
     }
+    // AddSubStats of the add/sub cases (bench.cpp:160-161 collects them for the vector
+    // add/sub kernels): chunks of lane_count(width) limbs and how many would have taken
+    // the rare Phase 4, derived on the device per case (dotg_words_host_stats).
+    uint64_t chunks = 0, fires = 0;
+    for (const Case& c : corpus) {
+        if (c.op == "mul") continue;
+        Limbs o(c.a.size());
+        uint32_t carry = 0;
+        if (dotg_words_host_stats(c.op == "sub", o.data(), c.a.data(), c.b.data(), c.a.size(), width, &carry,
+                                  &chunks, &fires) != DOTG_OK) {
+            std::fprintf(stderr, "error: stats call failed: %s\n", dotg_last_error());
+            return 2;
+        }
+    }
     std::sort(bad.begin(), bad.end());
     std::printf("kernel b200 (w=%s, sm_100a): %zu cases, %zu mismatches\n",
                 width == 0 ? "scalar" : std::to_string(width).c_str(), corpus.size(), bad.size());
+    if (chunks > 0)
+        std::printf("chunks %llu, phase4 triggers %llu (rate %.6f)\n", static_cast<unsigned long long>(chunks),
+                    static_cast<unsigned long long>(fires), double(fires) / double(chunks));
     for (size_t s = 0; s < bad.size(); ++s) {
         if (s == 10) {
             std::printf("  ... %zu more\n", bad.size() - 10);
