@@ -266,7 +266,10 @@ __global__ void __launch_bounds__(128) k_mul_smem(uint64_t* out, const uint64_t*
 // leave the IMAD.WIDE carry chain latency-bound - tools/mac_sweep.cu: 1 accumulator
 // tops out at ~22 products/clk/SM, 16 accumulators at ~29 of the 32 peak).
 // ---------------------------------------------------------------------------
-// Flat grid, one pair per thread. (Measured on B200, r01: one-warp CTAs with the resident
+// Flat grid, one pair per thread. (Measured on B200, r01: 8-column output blocks (42.9 us,
+// same), 6 / 7 CTAs per SM forced through launch bounds (80 / 72 registers with spills:
+// 45.9 / 55.9 us - ncu: the FMA-heavy pipe at ~80%, stalls split between math-pipe
+// throttle and fixed-latency waits), one-warp CTAs with the resident
 // warps per SM capped so the batch ends just below a whole wave (43.9 us), a persistent
 // loop with an exactly balanced pair range per CTA (48.2 us: the 2.77 pairs/thread
 // quantisation moves into the warps as partial last iterations), a persistent thread-stride
