@@ -530,7 +530,37 @@ def run_ours(args, rank, world, dist):
         d2h = sum(2 * (B * m * 8 + 4 * B) for m, B in C2_SIZES)
         e2e = {"value": step_bytes * world * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e_steps,
-               "api": "dotg_addsub_grouped_host: the 8 host problems through one 3-stream H2D/kernel/D2H pipeline (pinned host buffers)"}
+               "api": "dotg_addsub_grouped_host: the 8 host problems through one H2D / kernel / D2H stream "
+                      "pipeline (pinned host buffers)"}
+        # the PCIe ceiling of this step: the same bytes moved with no kernels at all
+        # (uploads on one stream, downloads concurrently on another, 24 MB chunks)
+        try:
+            xa = torch.empty(h2d // 8, dtype=torch.int64, pin_memory=True)
+            xb = torch.empty(d2h // 8, dtype=torch.int64, pin_memory=True)
+            ya, yb = torch.empty_like(xa, device="cuda"), torch.empty_like(xb, device="cuda")
+            s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+            ch = 3 << 20
+
+            def xfer():
+                with torch.cuda.stream(s1):
+                    for i in range(0, xa.numel(), ch):
+                        ya[i:i + ch].copy_(xa[i:i + ch], non_blocking=True)
+                with torch.cuda.stream(s2):
+                    for i in range(0, xb.numel(), ch):
+                        xb[i:i + ch].copy_(yb[i:i + ch], non_blocking=True)
+                torch.cuda.synchronize()
+
+            xfer()
+            t0 = time.perf_counter()
+            for _ in range(5):
+                xfer()
+            tx = (time.perf_counter() - t0) / 5
+            e2e["transfer_only_GBps"] = step_bytes / tx / 1e9
+            e2e["frac_of_transfer_only"] = e2e["value"] / world / e2e["transfer_only_GBps"]
+            del xa, xb, ya, yb
+        except Exception as ex:  # noqa: BLE001
+            e2e["transfer_only_GBps"] = None
+            e2e["transfer_note"] = str(ex)[:200]
         del hsets
 
     # ---- CPU baseline (rank 0, N = 1 only) ----

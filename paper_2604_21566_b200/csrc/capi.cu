@@ -164,6 +164,9 @@ struct HostCtx {
     cudaStream_t s[kNS] = {};
     char* buf[kNS] = {};
     size_t cap = 0;  // bytes per slot
+    char* flat = nullptr;  // whole-call device image (flat pipeline)
+    size_t flat_cap = 0;
+    std::vector<cudaEvent_t> ev;
 };
 HostCtx g_host;
 
@@ -177,6 +180,10 @@ int host_prepare(size_t bytes_per_slot) {
             g_host.buf[i] = nullptr;
         }
         g_host.cap = 0;
+        if (g_host.flat) cudaFree(g_host.flat);
+        g_host.flat = nullptr;
+        g_host.flat_cap = 0;
+        g_host.ev.clear();  // events of the previous device are not reused
         for (int i = 0; i < kNS; ++i) {
             if ((e = cudaStreamCreateWithFlags(&g_host.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "stream");
@@ -222,9 +229,115 @@ SliceGeom geom(const HostJob& j) {
     return g;
 }
 
+// Flat pipeline: the whole call's inputs and outputs get their own device image (no slot
+// reuse), so the uploads run back to back on one stream, the kernels on a second and the
+// downloads on a third, each slice linked only by its own two events: nothing ever waits
+// for a download to free a staging slot. Used while the image fits in kFlatMax bytes.
+constexpr size_t kFlatMax = size_t(16) << 30;
+
+struct FlatGeom {
+    size_t da, db, dout, dfl;  // offsets of the job's arrays in the image
+};
+
+size_t flat_layout(const HostJob* jobs, int n, std::vector<FlatGeom>& fg, size_t& slices) {
+    size_t off = 0;
+    slices = 0;
+    fg.resize(size_t(n));
+    for (int q = 0; q < n; ++q) {
+        const HostJob& j = jobs[q];
+        const SliceGeom g = geom(j);
+        const size_t in = j.batch * g.in_b, outb = j.batch * g.out_b;
+        fg[q].da = off;
+        off += align_up(in, 256);
+        fg[q].db = off;
+        off += align_up(in, 256);
+        fg[q].dout = off;
+        off += align_up(outb, 256);
+        fg[q].dfl = off;
+        off += align_up(j.batch * 4, 256);
+        slices += (j.batch + g.slice - 1) / g.slice;
+    }
+    return off;
+}
+
+int run_host_jobs_flat(const HostJob* jobs, int n, const std::vector<FlatGeom>& fg, size_t bytes, size_t slices) {
+    cudaError_t e = cudaSuccess;
+    if (g_host.flat_cap < bytes) {
+        if (g_host.flat) cudaFree(g_host.flat);
+        g_host.flat = nullptr;
+        g_host.flat_cap = 0;
+        if ((e = cudaMalloc(&g_host.flat, bytes)) != cudaSuccess)
+            return fail(DOTG_ENOMEM, std::string("host pipeline image: ") + cudaGetErrorString(e));
+        g_host.flat_cap = bytes;
+    }
+    while (g_host.ev.size() < 2 * slices) {
+        cudaEvent_t ev;
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+        g_host.ev.push_back(ev);
+    }
+    cudaStream_t sh = g_host.s[0], sc = g_host.s[1], sd = g_host.s[2];
+    size_t k = 0;
+    for (int q = 0; q < n && e == cudaSuccess; ++q) {
+        const HostJob& j = jobs[q];
+        const SliceGeom g = geom(j);
+        uint64_t* da = reinterpret_cast<uint64_t*>(g_host.flat + fg[q].da);
+        uint64_t* db = reinterpret_cast<uint64_t*>(g_host.flat + fg[q].db);
+        uint64_t* dout = reinterpret_cast<uint64_t*>(g_host.flat + fg[q].dout);
+        uint32_t* dfl = reinterpret_cast<uint32_t*>(g_host.flat + fg[q].dfl);
+        for (size_t p0 = 0; p0 < j.batch && e == cudaSuccess; p0 += g.slice, ++k) {
+            const size_t cnt = std::min(g.slice, j.batch - p0);
+            cudaEvent_t ev_in = g_host.ev[2 * k], ev_k = g_host.ev[2 * k + 1];
+            e = cudaMemcpyAsync(da + p0 * j.m, j.a + p0 * j.m, cnt * g.in_b, cudaMemcpyHostToDevice, sh);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(db + p0 * j.m, j.b + p0 * j.m, cnt * g.in_b, cudaMemcpyHostToDevice, sh);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_in, sh);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(sc, ev_in, 0);
+            if (e == cudaSuccess) {
+                uint64_t* o = dout + p0 * (g.out_b / 8);
+                e = j.op == 2 ? dotg::launch_mul_batch(o, da + p0 * j.m, db + p0 * j.m, j.m, cnt, 0, sc)
+                              : dotg::launch_addsub_batch(j.op == 1, o, da + p0 * j.m, db + p0 * j.m,
+                                                          j.flags ? dfl + p0 : nullptr, j.m, cnt, 0, sc);
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(ev_k, sc);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev_k, 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(j.out + p0 * (g.out_b / 8), dout + p0 * (g.out_b / 8), cnt * g.out_b,
+                                    cudaMemcpyDeviceToHost, sd);
+            if (e == cudaSuccess && j.flags && j.op != 2)
+                e = cudaMemcpyAsync(j.flags + p0, dfl + p0, cnt * 4, cudaMemcpyDeviceToHost, sd);
+        }
+    }
+    cudaError_t es = cudaSuccess;
+    for (cudaStream_t st : {sh, sc, sd}) {
+        cudaError_t x = cudaStreamSynchronize(st);
+        if (es == cudaSuccess) es = x;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "dotg host pipeline");
+    if (es != cudaSuccess) return cuda_fail(es, "dotg host pipeline sync");
+    return DOTG_OK;
+}
+
+bool host_flat_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("DOTG_HOST_FLAT");
+        return e == nullptr || std::atoi(e) != 0;
+    }();
+    return v;
+}
+
 // Jobs must be validated; m > 0 and batch > 0 for every job.
 int run_host_jobs(const HostJob* jobs, int n) {
     std::lock_guard<std::mutex> lk(g_host.mu);
+    if (host_flat_enabled()) {
+        std::vector<FlatGeom> fg;
+        size_t slices = 0;
+        const size_t bytes = flat_layout(jobs, n, fg, slices);
+        if (bytes <= kFlatMax) {
+            int rc = host_prepare(256);
+            if (rc != DOTG_OK) return rc;
+            return run_host_jobs_flat(jobs, n, fg, bytes, slices);
+        }
+    }
     size_t slot = 256;
     for (int q = 0; q < n; ++q) {
         const SliceGeom g = geom(jobs[q]);
