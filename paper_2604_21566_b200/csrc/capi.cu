@@ -183,7 +183,8 @@ int host_prepare(size_t bytes_per_slot) {
         if (g_host.flat) cudaFree(g_host.flat);
         g_host.flat = nullptr;
         g_host.flat_cap = 0;
-        g_host.ev.clear();  // events of the previous device are not reused
+        for (cudaEvent_t ev : g_host.ev) cudaEventDestroy(ev);
+        g_host.ev.clear();  // events belong to the previous device
         for (int i = 0; i < kNS; ++i) {
             if ((e = cudaStreamCreateWithFlags(&g_host.s[i], cudaStreamNonBlocking)) != cudaSuccess)
                 return cuda_fail(e, "stream");
@@ -311,6 +312,11 @@ int run_host_jobs_flat(const HostJob* jobs, int n, const std::vector<FlatGeom>& 
     for (cudaStream_t st : {sh, sc, sd}) {
         cudaError_t x = cudaStreamSynchronize(st);
         if (es == cudaSuccess) es = x;
+    }
+    if (g_host.flat_cap > (size_t(4) << 30)) {  // do not keep a huge image resident between calls
+        cudaFree(g_host.flat);
+        g_host.flat = nullptr;
+        g_host.flat_cap = 0;
     }
     if (e != cudaSuccess) return cuda_fail(e, "dotg host pipeline");
     if (es != cudaSuccess) return cuda_fail(es, "dotg host pipeline sync");
