@@ -817,6 +817,22 @@ def cpu_ref_table():
     n = 16384
     ha, hb, hsa, hsb = host(a[:n]), host(b[:n]), host(sa[:n]), host(sb[:n])
     byts = 2 * n * (24 * 64 + 4)
+    # the reference bench's methodology on one core: ns per op, mean +- Student-t CI95
+    # over 7 repetitions, span form and value form (bench.cpp:95-104, 216-225)
+    t_975_6 = 2.447
+    for impl, form in ((0, "span"), (2, "value")):
+        out_ = np.empty_like(ha)
+        fl_ = np.empty(n, np.uint32)
+        L.dotref_batch(0, impl, P(out_), P(ha), P(hb), P(fl_), 64, n, 1)
+        ts = []
+        for _ in range(7):
+            t0 = time.perf_counter()
+            L.dotref_batch(0, impl, P(out_), P(ha), P(hb), P(fl_), 64, n, 1)
+            ts.append((time.perf_counter() - t0) / n * 1e9)
+        mean = statistics.mean(ts)
+        ci = t_975_6 * statistics.stdev(ts) / len(ts) ** 0.5
+        res["rows"].append({"config": f"C1 add m=64, {form} form, 1 thread", "unit": "ns/op", "sample": f"{n} ops x 7",
+                            "one_thread": mean, "ci95": ci, "all_threads": None})
     for th in (1, NT):
         dt = batch_rate(0, ha, hb, th) + batch_rate(1, hsa, hsb, th)
         if th == 1:

@@ -178,7 +178,8 @@ int dotref_oracle_mul(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, 
 
 // Batched CPU baseline over [batch][m] row-major operands with a static partition
 // of pairs across nthreads std::threads (the reference functions are pure and
-// reentrant). op: 0 add, 1 sub, 2 mul. impl: 0 = the DoT path
+// reentrant). op: 0 add, 1 sub, 2 mul. impl: 0 = the DoT path, 2 = its
+// value form for add/sub
 // (span-form dot_add_words/dot_sub_words at Width::w8, dot_mul_words), 1 = oracle.
 // flags may be null for mul. out is [batch][m] (add/sub) or [batch][2m] (mul).
 int dotref_batch(int op, int impl, limb_t* out, const limb_t* a, const limb_t* b, uint32_t* flags,
@@ -212,6 +213,12 @@ int dotref_batch(int op, int impl, limb_t* out, const limb_t* a, const limb_t* b
                         std::span<const limb_t> sa(pa, m), sb(pb, m);
                         f = op ? dot::dot_sub_words(so, sa, sb, dot::Width::w8)
                                : dot::dot_add_words(so, sa, sb, dot::Width::w8);
+                    } else if (impl == 2) {  // value form (allocates the result, bench.cpp:95-104)
+                        const Limbs va(pa, pa + m), vb(pb, pb + m);
+                        const dot::WordsResult r = op ? dot::dot_sub_words(va, vb, dot::Width::w8)
+                                                      : dot::dot_add_words(va, vb, dot::Width::w8);
+                        std::copy(r.limbs.begin(), r.limbs.end(), po);
+                        f = r.flag;
                     } else {
                         const Limbs va(pa, pa + m), vb(pb, pb + m);
                         const dot::WordsResult r = op ? dot::oracle_sub(va, vb) : dot::oracle_add(va, vb);
