@@ -196,3 +196,21 @@ def test_grouped_matches_oracle(cuda, oracle):
     with pytest.raises(dg.InvalidArgument):
         dg.addsub_grouped([dict(op="add", a=a, b=a, out=torch.empty_like(a)),
                            dict(op="add", a=a, b=a, out=a)])
+
+
+@pytest.mark.parametrize("m,batch", [(5, 300), (100, 77), (1000, 9), (9000, 3)])
+def test_aliasing_every_route(cuda, oracle, m, batch):
+    """out == a and out == b (exactly) on the any-m row kernel and the long-batch passes."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(900 + m)
+    a, b = spiky(rng, (batch, m)), spiky(rng, (batch, m))
+    for sub in (False, True):
+        want, wf = oracle.addsub_batch(sub, a, b)
+        ta, tb = dev(torch, a), dev(torch, b)
+        _, fl = dg.addsub_batch(sub, ta, tb, out=ta)
+        assert np.array_equal(host(ta), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf), (m, sub)
+        ta, tb = dev(torch, a), dev(torch, b)
+        _, fl = dg.addsub_batch(sub, ta, tb, out=tb)
+        assert np.array_equal(host(tb), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf), (m, sub)
