@@ -131,11 +131,13 @@ int words(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t 
 
 // ---------------------------------------------------------------------------
 // Host pipelines. One global staging context (host calls are synchronous). A call's
-// work is cut into slices of ~24 MB of input; slice k runs on stream k % kNS with its
-// own device staging slot: H2D(a, b) -> kernel -> D2H(out, flags). Consecutive slices
-// sit on different streams, so the H2D copy engine, the SMs and the D2H copy engine
-// work on three slices at once; several jobs (e.g. a whole multi-size sweep) share one
-// pipeline with no drain between jobs.
+// work is cut into slices of ~24 MB of input, each H2D(a, b) -> kernel -> D2H(out,
+// flags). Calls whose data fits kFlatMax get a device image of their own and run the
+// flat pipeline (run_host_jobs_flat: uploads, kernels and downloads on three streams
+// linked per slice by events); larger calls reuse kNS staging slots, slice k on stream
+// k % kNS, so the H2D copy engine, the SMs and the D2H copy engine still work on three
+// slices at once. Several jobs (e.g. a whole multi-size sweep) share one pipeline with no
+// drain between jobs.
 // ---------------------------------------------------------------------------
 constexpr int kNS = 4;  // max pipeline depth; the used depth is host_streams()
 

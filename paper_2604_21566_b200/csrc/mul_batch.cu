@@ -13,11 +13,16 @@
 // (mul.hpp:26-30). The carry pass is deferred to once per column / output block: the
 // accumulator's low word is final, the upper 64 bits carry into the next column.
 //
-// Kernels:
+// Kernels (the route per size / layout / alignment is launch_mul_batch at the bottom):
 //   k_mul_regs<M>   M <= 4 and the interleaved layout: thread per pair, operands in
 //                   registers, columns scanned in order.
-//   k_mul_regblk<M> M in {8, 16}: registers, output blocks of 16 columns (config 3).
-//   k_mul_smem<M>   M in {32, 64, 128}: persistent, thread per pair, operands staged in
+//   k_mul_regblk<M> M in {8, 16}: registers, output blocks of 16 columns (config 3);
+//                   with RT also 4 < m < 16 on zero-extended operands, any alignment.
+//   k_mul_imma<NB>  (mul_imma.cu) m in {32, 64, 128} and even sizes between: the integer
+//                   tensor pipe - the default for those sizes (config 4).
+//   padded Karatsuba (karatsuba.cu) m > 128, and copy-padded odd 16 < m < 128.
+//   k_transpose_u64 interleaved m > 16: to row-major and back around the row route.
+//   k_mul_smem<M>   M in {32, 64, 128} when the IMAD route is forced: persistent, thread per pair, operands staged in
 //                   XOR-swizzled shared memory (2 CTAs per SM fill it) by coalesced
 //                   256-bit loads, output produced in blocks
 //                   of K = 16 columns: for every (output block, a-block) pair a 16x16
