@@ -16,8 +16,10 @@
 // Kernels (the route per size / layout / alignment is launch_mul_batch at the bottom):
 //   k_mul_regs<M>   M <= 4 and the interleaved layout: thread per pair, operands in
 //                   registers, columns scanned in order.
-//   k_mul_regblk<M> M in {8, 16}: registers, output blocks of 16 columns (config 3);
-//                   with RT also 4 < m < 16 on zero-extended operands, any alignment.
+//   k_mul_kara16    M = 16 (config 3): one in-register Karatsuba level over three
+//                   16 x 16-word column products (768 instead of 1024 IMAD.WIDE).
+//   k_mul_regblk<M> M = 8: registers, output blocks of 16 columns; with RT also
+//                   4 < m < 16 on zero-extended operands, any alignment.
 //   k_mul_imma<NB>  (mul_imma.cu) m in {32, 64, 128} and even sizes between: the integer
 //                   tensor pipe - the default for those sizes (config 4).
 //   padded Karatsuba (karatsuba.cu) m > 128, and copy-padded odd 16 < m < 128.
@@ -374,6 +376,133 @@ __global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_
 }
 
 // ---------------------------------------------------------------------------
+// M = 16 (config 3) with one in-register Karatsuba level: three 16 x 16-word column
+// products (768 instead of 1024 IMAD.WIDE) - z0 = lo*lo, z2 = hi*hi, z1 = |a_hi - a_lo| *
+// |b_hi - b_lo| - and mid = z0 + z2 -+ z1 (reference kara_rec, mul.cpp:176-233, the
+// subtractive form), recombined with 32-bit carry chains on the ALU pipe.
+// ---------------------------------------------------------------------------
+// Z = A * B for 16-word operands: one 16-column block below (kLower) and one above (kUpper).
+__device__ __forceinline__ void mul16_words(const uint32_t (&A)[kK], const uint32_t (&B)[kK], uint32_t (&Z)[2 * kK]) {
+    uint32_t cr0 = 0, cr1 = 0, cr2 = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        uint32_t acc[kK][3];
+#pragma unroll
+        for (int x = 0; x < kK; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
+        uint32_t W[2 * kK];
+#pragma unroll
+        for (int e = 0; e < 2 * kK; ++e) {
+            const int j = (s - 1) * kK + e;
+            W[e] = (j >= 0 && j < kK) ? B[j < 0 ? 0 : (j >= kK ? kK - 1 : j)] : 0u;
+        }
+        if (s == 0) mul_step<kLower>(acc, A, W);
+        else mul_step<kUpper>(acc, A, W);
+#pragma unroll
+        for (int x = 0; x < kK; ++x) {
+            add96(acc[x][0], acc[x][1], acc[x][2], cr0, cr1, cr2);
+            Z[s * kK + x] = acc[x][0];
+            cr0 = acc[x][1];
+            cr1 = acc[x][2];
+            cr2 = 0;
+        }
+    }
+}
+
+// D = |X - Y| (16 words), returns X < Y.
+__device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uint32_t (&Y)[kK], uint32_t (&D)[kK]) {
+    uint32_t bw = 0;
+#pragma unroll
+    for (int i = 0; i < kK; ++i) {
+        const uint64_t t = uint64_t(X[i]) - uint64_t(Y[i]) - bw;
+        D[i] = uint32_t(t);
+        bw = uint32_t(t >> 63);
+    }
+    // negative: D = -D (two's complement over 16 words)
+    const uint32_t mask = 0u - bw;
+    uint32_t c = bw;
+#pragma unroll
+    for (int i = 0; i < kK; ++i) {
+        const uint64_t t = uint64_t(D[i] ^ mask) + c;
+        D[i] = uint32_t(t);
+        c = uint32_t(t >> 32);
+    }
+    return bw;
+}
+
+// 126 registers (4 CTAs/SM); forcing 5 CTAs/SM spills and runs slower (42.7 vs 40.0 us).
+__global__ void __launch_bounds__(128) k_mul_kara16(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                    size_t batch) {
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    uint32_t Al[kK], Ah[kK], Bl[kK], Bh[kK];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        uint64_t x[4], y[4];
+        ld_stream<4>(a + pidx * 16 + 4 * v, x);
+        ld_stream<4>(b + pidx * 16 + 4 * v, y);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int w = 8 * v + 2 * k;  // word index 0..31
+            uint32_t* pa = w < kK ? &Al[w] : &Ah[w - kK];
+            uint32_t* pb = w < kK ? &Bl[w] : &Bh[w - kK];
+            pa[0] = lo32(x[k]);
+            pa[1] = hi32(x[k]);
+            pb[0] = lo32(y[k]);
+            pb[1] = hi32(y[k]);
+        }
+    }
+    uint32_t Da[kK], Db[kK];
+    const uint32_t sa = absdiff16(Ah, Al, Da), sb = absdiff16(Bh, Bl, Db);
+    uint32_t Z1[2 * kK], Z0[2 * kK], Z2[2 * kK];
+    mul16_words(Da, Db, Z1);
+    mul16_words(Al, Bl, Z0);
+    mul16_words(Ah, Bh, Z2);
+    uint64_t* po = out + pidx * 32;
+    {  // R[0, 16) = z0[0, 16)
+        uint64_t o0[4], o1[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            o0[k] = uint64_t(Z0[2 * k]) | (uint64_t(Z0[2 * k + 1]) << 32);
+            o1[k] = uint64_t(Z0[8 + 2 * k]) | (uint64_t(Z0[8 + 2 * k + 1]) << 32);
+        }
+        st_stream<4>(po, o0);
+        st_stream<4>(po + 4, o1);
+    }
+    // mid = z0 + z2 - z1 (same signs) or + z1 (33 words; the true value is < 2^1025)
+    const uint32_t neg = sa == sb ? 1u : 0u, mask = 0u - neg;
+    uint32_t mid[2 * kK + 1];
+    {
+        uint32_t c = neg;
+#pragma unroll
+        for (int i = 0; i < 2 * kK; ++i) {
+            const uint64_t t = uint64_t(Z0[i]) + Z2[i] + (Z1[i] ^ mask) + c;
+            mid[i] = uint32_t(t);
+            c = uint32_t(t >> 32);
+        }
+        mid[2 * kK] = c + mask;
+    }
+    // R[16, 64) = (z0[16, 32) | z2 << 512) + mid
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {  // 6 x 8 words = 48 words = 24 limbs
+        uint32_t r[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int i = 8 * q + e;
+            const uint32_t base = i < kK ? Z0[kK + i] : Z2[i - kK];
+            const uint32_t add = i <= 2 * kK ? mid[i <= 2 * kK ? i : 0] : 0u;
+            const uint64_t t = uint64_t(base) + add + c;
+            r[e] = uint32_t(t);
+            c = uint32_t(t >> 32);
+        }
+        uint64_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = uint64_t(r[2 * k]) | (uint64_t(r[2 * k + 1]) << 32);
+        st_stream<4>(po + 8 + 4 * q, o);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Generic: any m, any layout (pair p, limb i at p*sp + i*si; out limb k at p*so + k*sio).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t word_at(const uint64_t* base, size_t si, size_t w) {
@@ -621,7 +750,11 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
             if (al) return run_regblk<8>(out, a, b, batch, stream);
             break;
         case 16:
-            if (al) return run_regblk<16>(out, a, b, batch, stream);
+            if (al) {  // C3: 40.0 us vs 42.1 us for the plain 16-column kernel (tools/mul_timing.py)
+                k_mul_kara16<<<unsigned((batch + 127) / 128), 128, 0, stream>>>(out, a, b, batch);
+                count_launch();
+                return cudaGetLastError();
+            }
             break;
         case 32:
             if (al) return run_smem<32>(out, a, b, batch, stream);
