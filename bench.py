@@ -643,6 +643,7 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * nops * world / (ms * 1e-3) / 1e9,
                      "unit": "GB/s", "kernel_gbs": byts * nops / (sum(per) * 1e-3) / 1e9,
                      "frac_hbm": byts * nops / (sum(per) * 1e-3) / 1e9 / hbm_peak,
+                     "frac_hbm_back_to_back": byts * nops / (ms * 1e-3) / 1e9 / hbm_peak,
                      "launch_us": statistics.mean(per) * 1e3,
                      "step": "3 rotating input sets (300 MB apart > L2); per set add + sub in one dotg_addsub_grouped "
                              "launch"}
