@@ -706,7 +706,10 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
                              int layout, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     const bool al = aligned32(out) && aligned32(a) && aligned32(b);
-    if (layout == 1 && m > 16 && g_mul_route.load(std::memory_order_relaxed) != 1 && batch <= (size_t(65535) * 32))
+    // interleaved m > 16, and 4 < m < 16 off the powers of two (no interleaved register
+    // kernel for those): transpose around the row-major route
+    if (layout == 1 && (m > 16 || (m > 4 && (m & (m - 1)) != 0)) && g_mul_route.load(std::memory_order_relaxed) != 1 &&
+        batch <= (size_t(65535) * 32))
         return mul_interleaved_via_rows(out, a, b, m, batch, stream);
     // Tensor pipe where it beats the IMAD kernels (tools/mul_timing.py on B200: m = 32
     // 1.27x, 64 2.26x, 128 3.8x; at m = 8 / 16 the per-pair warp overhead loses to the
