@@ -15,7 +15,6 @@ src/addsub.cpp:147-164); the same (G, P) operator that chains its chunks chains 
 """
 from __future__ import annotations
 
-import ctypes
 from typing import Callable, List, Optional, Sequence, Tuple
 
 from ._lib import InvalidArgument, check, lib

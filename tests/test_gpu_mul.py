@@ -4,7 +4,7 @@ import os
 import numpy as np
 import pytest
 
-from helpers import MAX, category, spiky, uniform
+from helpers import MAX, category, uniform
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz")
