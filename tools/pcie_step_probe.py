@@ -7,8 +7,13 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-h2d = 536870912
-d2h = 279576576
+import argparse
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--h2d", type=int, default=536870912)
+ap.add_argument("--d2h", type=int, default=279576576)
+args = ap.parse_args()
+h2d, d2h = args.h2d, args.d2h
 ha = torch.empty(h2d // 8, dtype=torch.int64, pin_memory=True)
 hb = torch.empty(d2h // 8, dtype=torch.int64, pin_memory=True)
 da = torch.empty_like(ha, device="cuda")
