@@ -159,6 +159,20 @@ size_t slice_bytes() {
     }();
     return v;
 }
+// Multiply slices download as many bytes as they upload, so each slice's download is on
+// the critical path once the uploads end: smaller slices shorten that drain, down to the
+// size where per-copy and per-launch overhead takes over (tools/pcie_step_probe.py, 64 +
+// 64 MB, download of chunk k after its upload: 2 MB 1.97 ms, 8 MB 1.57 ms, 24 MB 1.79 ms;
+// the C3 / C4 host calls: 4 MB 1.22e8 / 2.99e7, 12 MB 1.44e8 / 3.59e7, 24 MB 1.39e8 /
+// 3.48e7 pairs/s).
+size_t mul_slice_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("DOTG_HOST_MUL_SLICE_MB");
+        const long x = e ? std::atol(e) : 12;
+        return size_t(x < 1 ? 1 : x) << 20;
+    }();
+    return v;
+}
 
 struct HostCtx {
     std::mutex mu;
@@ -225,7 +239,8 @@ SliceGeom geom(const HostJob& j) {
     SliceGeom g{};
     g.in_b = j.m * 8;
     g.out_b = j.op == 2 ? 2 * j.m * 8 : j.m * 8;
-    g.slice = std::min(std::max<size_t>(1, slice_bytes() / (2 * g.in_b)), j.batch);
+    const size_t sb = j.op == 2 ? mul_slice_bytes() : slice_bytes();
+    g.slice = std::min(std::max<size_t>(1, sb / (2 * g.in_b)), j.batch);
     g.sa = align_up(g.slice * g.in_b, 256);
     g.so = align_up(g.slice * g.out_b, 256);
     g.sf = align_up(g.slice * 4, 256);
