@@ -138,16 +138,16 @@ enum StepMode { kFull = 0, kLower = 1, kUpper = 2 };
 
 // acc[x] += sum_u A[u] * W[K + x - u]  (W[e] = b'_{(d-1)K + e}); kLower keeps x >= u
 // (d = 0: j = x - u must be >= 0), kUpper keeps x < u (d = NB: j < n).
-template <int MODE>
-__device__ __forceinline__ void mul_step(uint32_t (&acc)[kK][3], const uint32_t (&A)[kK],
-                                         const uint32_t (&W)[2 * kK]) {
+template <int MODE, int K = kK>
+__device__ __forceinline__ void mul_step(uint32_t (&acc)[K][3], const uint32_t (&A)[K],
+                                         const uint32_t (&W)[2 * K]) {
 #pragma unroll
-    for (int u = 0; u < kK; ++u) {
+    for (int u = 0; u < K; ++u) {
 #pragma unroll
-        for (int x = 0; x < kK; ++x) {
+        for (int x = 0; x < K; ++x) {
             if (MODE == kLower && x < u) continue;
             if (MODE == kUpper && x >= u) continue;
-            mac(acc[x][0], acc[x][1], acc[x][2], A[u], W[kK + x - u]);
+            mac(acc[x][0], acc[x][1], acc[x][2], A[u], W[K + x - u]);
         }
     }
 }
@@ -382,25 +382,26 @@ __global__ void __launch_bounds__(128) k_mul_regblk(uint64_t* out, const uint64_
 // subtractive form), recombined with 32-bit carry chains on the ALU pipe.
 // ---------------------------------------------------------------------------
 // Z = A * B for 16-word operands: one 16-column block below (kLower) and one above (kUpper).
-__device__ __forceinline__ void mul16_words(const uint32_t (&A)[kK], const uint32_t (&B)[kK], uint32_t (&Z)[2 * kK]) {
+template <int K>
+__device__ __forceinline__ void mulK_words(const uint32_t (&A)[K], const uint32_t (&B)[K], uint32_t (&Z)[2 * K]) {
     uint32_t cr0 = 0, cr1 = 0, cr2 = 0;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-        uint32_t acc[kK][3];
+        uint32_t acc[K][3];
 #pragma unroll
-        for (int x = 0; x < kK; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
-        uint32_t W[2 * kK];
+        for (int x = 0; x < K; ++x) acc[x][0] = acc[x][1] = acc[x][2] = 0;
+        uint32_t W[2 * K];
 #pragma unroll
-        for (int e = 0; e < 2 * kK; ++e) {
-            const int j = (s - 1) * kK + e;
-            W[e] = (j >= 0 && j < kK) ? B[j < 0 ? 0 : (j >= kK ? kK - 1 : j)] : 0u;
+        for (int e = 0; e < 2 * K; ++e) {
+            const int j = (s - 1) * K + e;
+            W[e] = (j >= 0 && j < K) ? B[j < 0 ? 0 : (j >= K ? K - 1 : j)] : 0u;
         }
-        if (s == 0) mul_step<kLower>(acc, A, W);
-        else mul_step<kUpper>(acc, A, W);
+        if (s == 0) mul_step<kLower, K>(acc, A, W);
+        else mul_step<kUpper, K>(acc, A, W);
 #pragma unroll
-        for (int x = 0; x < kK; ++x) {
+        for (int x = 0; x < K; ++x) {
             add96(acc[x][0], acc[x][1], acc[x][2], cr0, cr1, cr2);
-            Z[s * kK + x] = acc[x][0];
+            Z[s * K + x] = acc[x][0];
             cr0 = acc[x][1];
             cr1 = acc[x][2];
             cr2 = 0;
@@ -408,25 +409,35 @@ __device__ __forceinline__ void mul16_words(const uint32_t (&A)[kK], const uint3
     }
 }
 
-// D = |X - Y| (16 words), returns X < Y.
-__device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uint32_t (&Y)[kK], uint32_t (&D)[kK]) {
+// D = |X - Y| (K words), returns X < Y.
+template <int K>
+__device__ __forceinline__ uint32_t absdiff(const uint32_t (&X)[K], const uint32_t (&Y)[K], uint32_t (&D)[K]) {
     uint32_t bw = 0;
 #pragma unroll
-    for (int i = 0; i < kK; ++i) {
+    for (int i = 0; i < K; ++i) {
         const uint64_t t = uint64_t(X[i]) - uint64_t(Y[i]) - bw;
         D[i] = uint32_t(t);
         bw = uint32_t(t >> 63);
     }
-    // negative: D = -D (two's complement over 16 words)
+    // negative: D = -D (two's complement over K words)
     const uint32_t mask = 0u - bw;
     uint32_t c = bw;
 #pragma unroll
-    for (int i = 0; i < kK; ++i) {
+    for (int i = 0; i < K; ++i) {
         const uint64_t t = uint64_t(D[i] ^ mask) + c;
         D[i] = uint32_t(t);
         c = uint32_t(t >> 32);
     }
     return bw;
+}
+
+// (A second Karatsuba level - nine 8 x 8-word products, 576 IMAD.WIDE - needs 168
+// registers and ran 44.2 us; one level stays.)
+__device__ __forceinline__ void mul16_words(const uint32_t (&A)[kK], const uint32_t (&B)[kK], uint32_t (&Z)[2 * kK]) {
+    mulK_words<kK>(A, B, Z);
+}
+__device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uint32_t (&Y)[kK], uint32_t (&D)[kK]) {
+    return absdiff<kK>(X, Y, D);
 }
 
 // 126 registers (4 CTAs/SM); forcing 5 CTAs/SM spills and runs slower (42.7 vs 40.0 us).
