@@ -428,6 +428,28 @@ def run_ours(args, rank, world, dist):
         calls = single_calls
     else:
         calls = [L.grouped(probs)]  # the whole sweep = one persistent launch
+    # The step as a CUDA graph (one replay per step): same kernel, same bytes, without the
+    # host launch path between consecutive steps. --no-graph keeps direct launches.
+    graph_launches = None
+    if not args.ungrouped and not args.no_graph:
+        try:
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            Lc = Launcher(torch, lib, cap)
+            cap_call = Lc.grouped(probs)
+            with torch.cuda.stream(cap):
+                assert cap_call() == 0
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            n0 = dg.kernel_launches()
+            with torch.cuda.graph(graph, stream=cap):
+                cap_call()
+            graph_launches = dg.kernel_launches() - n0
+            torch.cuda.synchronize()
+            calls = [lambda: (graph.replay(), 0)[1]]
+        except Exception as e:  # noqa: BLE001
+            graph_launches = None
+            print(f"graph capture unavailable ({e}); direct launches", file=sys.stderr)
     calls_meta = list(range(len(calls)))
     assert step_bytes == c2_bytes()
     working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per step (a, b, sa, sb)
@@ -438,8 +460,11 @@ def run_ours(args, rank, world, dist):
     launches0 = dg.kernel_launches()
     ms_step, per_call = timed_steps(torch, dist if world > 1 else None, world, stream, calls, args.steps,
                                     args.warmup)
-    # launches inside the lean timed region (the event pass repeats it once more)
+    # launches inside the lean timed region (the event pass repeats it once more); graph
+    # replays do not pass the library's launch counter: launches per captured step x steps
     launches = (dg.kernel_launches() - launches0 - args.warmup * len(calls)) // 2
+    if graph_launches is not None:
+        launches = graph_launches * args.steps
     clocks = sampler.stop()
     value = step_bytes * world / (ms_step * 1e-3) / 1e9
     # average launch duration of the batched add/sub kernel = lean-loop step time / launches
@@ -600,6 +625,8 @@ def run_ours(args, rank, world, dist):
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
         "gpu_launches": int(launches),
+        "launch_mode": ("one CUDA-graph replay per step (the captured dotg_addsub_grouped launch)"
+                        if graph_launches is not None else "direct C-ABI launches"),
         "clocks": clocks,
         "carry_stress": stress,
         "configs": secondary,
@@ -901,6 +928,7 @@ def main():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--only", default="", help="comma list of C1,C3,C4,C5: run only those secondary configs")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
+    ap.add_argument("--no-graph", action="store_true", help="direct launches instead of one CUDA-graph replay per step")
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
     ap.add_argument("--cpu-table", action="store_true",
                     help="print the CPU reference table (1 thread / all threads per config) and exit")
