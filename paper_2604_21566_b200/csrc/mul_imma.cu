@@ -29,7 +29,11 @@
 // Epilogue: D tiles -> per-warp shared column array (conflict-free padded index), each
 // lane folds 8 columns per output limb into a 128-bit value, and one warp-ballot carry
 // lookahead (device.cuh) resolves the inter-limb carries - the same generate/propagate
-// algebra as the add kernel, used as the deferred carry-normalisation pass.
+// algebra as the add kernel, used as the deferred carry-normalisation pass. (Measured
+// r01: the epilogue is ~17 of C4's 85 us. A shared-memory-free version - Hankel rows
+// permuted so a lane holds adjacent byte columns, limbs assembled by two shuffle
+// butterflies and a lane permutation - was bit-exact but no faster at m = 64 (84.7 us),
+// 5% faster at m = 32 and spilled at m = 128 (92.8 vs 63 us).)
 #include <cuda_runtime.h>
 
 #include <cstdint>
