@@ -757,6 +757,10 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         lo, hi = shard_bounds(M5, rank, world)
         n_local = hi - lo
         free = torch.cuda.mem_get_info()[0]
+        if world > 1:  # the skip decision must be the same on every rank (collectives follow)
+            t = torch.tensor([free], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            free = int(t.item())
         if free < 3 * n_local * 8 + (1 << 30):
             out["C5"] = {"skipped": f"needs {3 * n_local * 8 / 2**30:.0f} GiB free per GPU"}
             return out
