@@ -345,6 +345,21 @@ class Launcher:
         return lambda: fn(*args)
 
 
+def device_index():
+    """This rank's GPU: LOCAL_RANK, or 0 for every rank in the shared-GPU rehearsal."""
+    return 0 if os.environ.get("DOTG_BENCH_SHARED_GPU") == "1" else env_int("LOCAL_RANK", 0)
+
+
+def reduce_scalar(dist, x, op):
+    """max / min of a host scalar over ranks (a CUDA tensor for NCCL, a CPU one for gloo)."""
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def timed_steps(torch, dist, world, stream, calls, steps, warmup):
     """Run `calls` (zero-arg callables, one device launch sequence each) per step:
     W warm-up steps, then K timed steps bracketed by barrier + synchronize and timed
@@ -373,9 +388,7 @@ def timed_steps(torch, dist, world, stream, calls, steps, warmup):
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
     if dist is not None and world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = reduce_scalar(dist, total_ms, "max")
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in calls]
            for _ in range(steps)]
     for s in range(steps):
@@ -396,7 +409,7 @@ def run_ours(args, rank, world, dist):
     from paper_2604_21566_b200 import workloads as W
 
     lib = dg.lib()  # raises if libdotg.so is missing: no fallback
-    torch.cuda.set_device(env_int("LOCAL_RANK", 0))
+    torch.cuda.set_device(device_index())
     if args.only:
         stream = torch.cuda.current_stream()
         hbm_peak, _, sm_max = peaks()
@@ -454,7 +467,7 @@ def run_ours(args, rank, world, dist):
     assert step_bytes == c2_bytes()
     working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per step (a, b, sa, sb)
 
-    sampler = ClockSampler(env_int("LOCAL_RANK", 0))
+    sampler = ClockSampler(device_index())
     sampler.start()
     time.sleep(0.2)
     launches0 = dg.kernel_launches()
@@ -548,9 +561,7 @@ def run_ours(args, rank, world, dist):
             e2e_step()
         dt = time.perf_counter() - t0
         if world > 1:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+            dt = reduce_scalar(dist, dt, "max")
         h2d = sum(2 * 2 * B * m * 8 for m, B in C2_SIZES)
         d2h = sum(2 * (B * m * 8 + 4 * B) for m, B in C2_SIZES)
         e2e = {"value": step_bytes * world * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
@@ -758,9 +769,7 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         n_local = hi - lo
         free = torch.cuda.mem_get_info()[0]
         if world > 1:  # the skip decision must be the same on every rank (collectives follow)
-            t = torch.tensor([free], dtype=torch.int64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)
-            free = int(t.item())
+            free = int(reduce_scalar(dist, float(free), "min"))
         if free < 3 * n_local * 8 + (1 << 30):
             out["C5"] = {"skipped": f"needs {3 * n_local * 8 / 2**30:.0f} GiB free per GPU"}
             return out
@@ -948,9 +957,13 @@ def main():
         import torch
         import torch.distributed as dist
 
+        # DOTG_BENCH_SHARED_GPU=1: every rank on GPU 0 with gloo - a control-flow rehearsal
+        # of the multi-rank bench on a one-GPU box (numbers meaningless, no kernel waits on
+        # another rank's kernel: the exchanges are host-orchestrated collectives)
+        shared = os.environ.get("DOTG_BENCH_SHARED_GPU") == "1"
         if args.impl == "ours":
-            torch.cuda.set_device(env_int("LOCAL_RANK", 0))
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+            torch.cuda.set_device(device_index())
+        dist.init_process_group("nccl" if args.impl == "ours" and not shared else "gloo")
     try:
         if args.impl == "reference":
             return run_reference(args, rank, world)

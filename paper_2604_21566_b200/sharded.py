@@ -86,7 +86,13 @@ class ShardedWords:
         agg = torch.zeros(2, dtype=torch.int32, device=dev)
         self.local_fn(sub, out, a, b, state, agg, stream)
         all_aggs = torch.empty(2 * self.world, dtype=torch.int32, device=dev)
-        self.dist.all_gather_into_tensor(all_aggs, agg, group=self.group)
+        if dev.type == "cuda" and self.dist.get_backend(self.group) != "nccl":
+            # gloo (CPU collectives): stage the 8 bytes through host memory
+            host = torch.empty(2 * self.world, dtype=torch.int32)
+            self.dist.all_gather_into_tensor(host, agg.cpu(), group=self.group)
+            all_aggs.copy_(host)
+        else:
+            self.dist.all_gather_into_tensor(all_aggs, agg, group=self.group)
         carry = torch.zeros(1, dtype=torch.int32, device=dev)
         self.finish_fn(sub, out, state, all_aggs, self.rank, self.world, carry, stream)
         return out, carry
