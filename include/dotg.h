@@ -200,6 +200,14 @@ int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uin
 int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                           int width, uint32_t* carry, uint64_t* chunks, uint64_t* fires);
 
+/* ---------------------------------------------------------------------------
+ * Batched comparison. Replaces: compare(a, b) per pair (limbs.hpp:84, limbs.cpp:46-53),
+ * the a >= b check of the sub configs. out[p] = -1 / 0 / +1 for a[p] < = > b[p] (equal
+ * lengths: the first difference from the top). Device pointers, stream-ordered.
+ * ------------------------------------------------------------------------- */
+int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
+                       dotg_stream_t stream);
+
 /* Workload setup (not the hot path): out[i] = splitmix64 output for counter
  * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,

@@ -27,6 +27,7 @@ from .api import (  # noqa: F401
     addsub_batch,
     addsub_batch_host,
     addsub_grouped,
+    compare_batch,
     dot_add_words,
     dot_mul_words,
     dot_sub_words,
@@ -57,6 +58,7 @@ __all__ = [
     "addsub_batch",
     "addsub_batch_host",
     "addsub_grouped",
+    "compare_batch",
     "dot_add_words",
     "dot_mul_words",
     "dot_sub_words",

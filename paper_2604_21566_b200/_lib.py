@@ -45,6 +45,7 @@ SIGNATURES = {
     "dotg_addsub_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_size_t, c_int, c_int, _P, _P]),
     "dotg_words_host_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_int, _P, _P, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
+    "dotg_compare_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
     "dotg_kernel_launches": (c_uint64, []),
     "dotg_set_mul_route": (c_int, [c_int]),
 }

@@ -376,6 +376,23 @@ def mul_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
     return out
 
 
+def compare_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
+    """compare(a[p], b[p]) per pair (limbs.hpp:84): int32 tensor of -1 / 0 / +1."""
+    torch = _torch()
+    lay = _layout(layout)
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.shape != b.shape:
+        raise InvalidArgument("compare: operand shapes differ")
+    batch, m = _batch_dims(a, lay)
+    if out is None:
+        out = torch.empty(batch, dtype=torch.int32, device=a.device)
+    if out.dtype != torch.int32 or out.numel() != batch or not out.is_contiguous():
+        raise InvalidArgument("compare: out must be a contiguous int32 tensor of batch entries")
+    check(lib().dotg_compare_batch(_dptr(out), _dptr(a), _dptr(b), m, batch, lay, _stream_handle(stream)))
+    return out
+
+
 def words(sub: bool, a, b, out=None, carry=None, *, stream=None):
     """One long number on the device: out = a +/- b, carry = device int32[1]."""
     torch = _torch()

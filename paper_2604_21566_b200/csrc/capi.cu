@@ -714,6 +714,21 @@ int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uin
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "stats");
 }
 
+int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
+                       dotg_stream_t stream) {
+    if (layout != DOTG_ROW_MAJOR && layout != DOTG_INTERLEAVED) return fail(DOTG_EINVAL, "unknown layout");
+    if (batch == 0) return DOTG_OK;
+    if (out == nullptr || (m > 0 && (a == nullptr || b == nullptr))) return fail(DOTG_EINVAL, "compare: null operand");
+    if (m > SIZE_MAX / 8 / batch) return fail(DOTG_EINVAL, "compare: size overflow");
+    const size_t bytes = m * batch * 8;
+    if (m > 0 && (ranges_overlap(out, batch * 4, a, bytes) || ranges_overlap(out, batch * 4, b, bytes)))
+        return fail(DOTG_EINVAL, "compare: out overlaps an operand");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_compare_batch(out, a, b, m, batch, layout, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "compare");
+}
+
 int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, int width,
                           uint32_t* carry, uint64_t* chunks, uint64_t* fires) {
     int rc = dotg_validate_width(width);

@@ -83,6 +83,10 @@ cudaError_t mul_padded_rows(uint64_t* out, const uint64_t* a, const uint64_t* b,
 // Keep freed stream-ordered scratch cached in the device pool (per host thread, device).
 void retain_stream_pool();
 
+// Batched compare (compare.cu): out[p] in {-1, 0, 1}.
+cudaError_t launch_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                                 int layout, cudaStream_t st);
+
 // AddSubStats parity counters (stats.cu): counters = device uint64[2] {chunks, fires}.
 cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                                 size_t batch, int layout, unsigned lanes, uint64_t* counters, cudaStream_t st);

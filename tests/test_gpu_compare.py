@@ -1,0 +1,60 @@
+"""Batched compare (limbs.hpp:84, limbs.cpp:46-53) on the B200 vs the oracle's compare:
+equal rows, rows differing only in the lowest / highest limb, all-ones rows, both
+layouts, team widths of every row kernel."""
+import numpy as np
+import pytest
+
+from helpers import MAX
+
+pytestmark = pytest.mark.gpu
+
+
+def cases(rng, m, batch):
+    a = rng.integers(0, 2**64, size=(batch, m), dtype=np.uint64)
+    b = a.copy()
+    kind = np.arange(batch) % 6
+    r = np.arange(batch)
+    # 0: equal; 1: differ in limb 0; 2: differ in the top limb; 3: differ at a random limb;
+    # 4: independent random; 5: all-ones vs all-ones minus a low bit
+    b[kind == 1, 0] ^= np.uint64(1)
+    b[kind == 2, m - 1] ^= np.uint64(1 << 63)
+    pos = rng.integers(0, m, size=batch)
+    sel = kind == 3
+    b[r[sel], pos[sel]] += np.uint64(1)
+    b[kind == 4] = rng.integers(0, 2**64, size=(int((kind == 4).sum()), m), dtype=np.uint64)
+    a[kind == 5] = MAX
+    b[kind == 5] = MAX
+    b[kind == 5, 0] = MAX - np.uint64(1)
+    swap = rng.random(batch) < 0.5
+    a[swap], b[swap] = b[swap].copy(), a[swap].copy()
+    return a, b
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 8, 16, 33, 64, 100, 300])
+def test_compare_batch(cuda, oracle, m, layout):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(1000 * m + layout)
+    batch = 777
+    a, b = cases(rng, m, batch)
+    want = np.array([oracle.compare(a[p], b[p]) for p in range(batch)], dtype=np.int32)
+
+    def put(x):
+        x = x.T if layout == 1 else x
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
+
+    got = dg.compare_batch(put(a), put(b), layout=layout).cpu().numpy()
+    assert np.array_equal(got, want), (m, layout, np.nonzero(got != want)[0][:5])
+
+
+def test_compare_empty_and_errors(cuda):
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    z = torch.zeros((0, 4), dtype=torch.int64, device="cuda")
+    assert dg.compare_batch(z, z).numel() == 0
+    a = torch.zeros((3, 4), dtype=torch.int64, device="cuda")
+    with pytest.raises(dg.InvalidArgument):
+        dg.compare_batch(a, torch.zeros((3, 5), dtype=torch.int64, device="cuda"))
