@@ -16,6 +16,7 @@
 //   * Partial aliasing of out with a/b (undefined in the reference) throws.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
 #include <span>
@@ -107,6 +108,37 @@ inline WordsResult run_limbs(bool sub, const Limbs& a, const Limbs& b, Width w,
     return r;
 }
 }  // namespace detail
+
+// Chunk-level operations (addsub.hpp:78-89): one chunk of w lanes, 1 <= w <= 8.
+struct ChunkResult {
+    std::array<limb_t, 8> sums{};  // first w entries valid
+    unsigned carry_out = 0;        // borrow_out for subtraction
+    bool phase4_fired = false;
+};
+
+namespace detail {
+inline ChunkResult run_chunk(bool sub, std::span<const limb_t> a, std::span<const limb_t> b, unsigned carry_in,
+                             unsigned w) {  // addsub.cpp:172-190
+    if (w < 1 || w > 8) throw std::invalid_argument("chunk width must be in 1..8");
+    if (a.size() != w || b.size() != w) throw std::invalid_argument("chunk operands must have exactly w limbs");
+    if (carry_in > 1) throw std::invalid_argument("carry_in must be 0 or 1");
+    ChunkResult r;
+    std::uint32_t co = 0, fired = 0;
+    check(dotg_chunk_host(sub ? 1 : 0, r.sums.data(), &co, &fired, a.data(), b.data(), carry_in, w));
+    r.carry_out = co;
+    r.phase4_fired = fired != 0;
+    return r;
+}
+}  // namespace detail
+
+inline ChunkResult add_w_limbs(std::span<const limb_t> a, std::span<const limb_t> b, unsigned carry_in,
+                               unsigned w) {
+    return detail::run_chunk(false, a, b, carry_in, w);
+}
+inline ChunkResult sub_w_limbs(std::span<const limb_t> a, std::span<const limb_t> b, unsigned borrow_in,
+                               unsigned w) {
+    return detail::run_chunk(true, a, b, borrow_in, w);
+}
 
 // out = a + b (mod 2^(64m)); returns the carry (addsub.hpp:98-100).
 inline unsigned dot_add_words(std::span<limb_t> out, std::span<const limb_t> a, std::span<const limb_t> b,

@@ -208,6 +208,20 @@ int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint6
 int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
                        dotg_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Chunk-level operations. Replaces: add_w_limbs / sub_w_limbs (addsub.hpp:78-89,
+ * addsub.cpp:172-190). One chunk = w limbs, 1 <= w <= 8 (the reference's masked-tail form
+ * for w < 8). Batched device form: chunk p at a/b/sums + p*w, carry_in[p] (NULL = all 0),
+ * carry_out[p], phase4_fired[p] (NULL = not wanted; 1 iff the reference's Phase 4 fires
+ * for that chunk). A carry_in entry > 1 (the reference throws) sets carry_out[p] to
+ * 0xFFFFFFFF and leaves that chunk's sums unwritten. sums may alias a or b exactly.
+ * Host form: one chunk from host memory, carry_in > 1 is DOTG_EINVAL.
+ * ------------------------------------------------------------------------- */
+int dotg_chunk_batch(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phase4_fired, const uint64_t* a,
+                     const uint64_t* b, const uint32_t* carry_in, unsigned w, size_t batch, dotg_stream_t stream);
+int dotg_chunk_host(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phase4_fired, const uint64_t* a,
+                    const uint64_t* b, uint32_t carry_in, unsigned w);
+
 /* Workload setup (not the hot path): out[i] = splitmix64 output for counter
  * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,

@@ -19,14 +19,17 @@ from ._lib import (  # noqa: F401
 from .api import (  # noqa: F401
     K_MAX_MUL_LIMBS,
     AddSubStats,
+    ChunkResult,
     KaratsubaConfig,
     Width,
     WordsResult,
     add_batch,
+    add_w_limbs,
     add_words,
     addsub_batch,
     addsub_batch_host,
     addsub_grouped,
+    chunk_batch,
     compare_batch,
     dot_add_words,
     dot_mul_words,
@@ -37,6 +40,7 @@ from .api import (  # noqa: F401
     mul_batch,
     mul_batch_host,
     sub_batch,
+    sub_w_limbs,
     sub_words,
     words,
 )
@@ -44,6 +48,7 @@ from . import api, sharded, workloads  # noqa: F401,E402
 
 __all__ = [
     "AddSubStats",
+    "ChunkResult",
     "KaratsubaConfig",
     "INTERLEAVED",
     "ROW_MAJOR",
@@ -54,10 +59,12 @@ __all__ = [
     "Width",
     "WordsResult",
     "add_batch",
+    "add_w_limbs",
     "add_words",
     "addsub_batch",
     "addsub_batch_host",
     "addsub_grouped",
+    "chunk_batch",
     "compare_batch",
     "dot_add_words",
     "dot_mul_words",
@@ -71,6 +78,7 @@ __all__ = [
     "mul_batch_host",
     "set_mul_route",
     "sub_batch",
+    "sub_w_limbs",
     "sub_words",
     "words",
 ]

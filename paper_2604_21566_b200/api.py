@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import operator
 from typing import NamedTuple, Optional
 
 import numpy as np
@@ -74,6 +75,11 @@ def _validate_width(width) -> None:
 
 
 def _host_u64(x, name: str) -> np.ndarray:
+    if isinstance(x, (list, tuple)):  # Python ints (any mix with numpy scalars) up to 2^64 - 1
+        try:
+            x = np.array([operator.index(v) for v in x], dtype=np.uint64)
+        except (OverflowError, TypeError, ValueError):
+            raise InvalidArgument(f"{name}: limbs must be unsigned 64-bit integers") from None
     arr = np.asarray(x)
     if arr.dtype != np.uint64:
         if arr.size == 0:
@@ -157,6 +163,40 @@ def _dispatch_words(sub: bool, args, width, stats):
         return _words_span(sub, args[0], args[1], args[2], width, stats)
     _validate_width(width)
     return _words_value(sub, args[0], args[1], width, stats)
+
+
+class ChunkResult(NamedTuple):
+    """include/dot/addsub.hpp:78-82: sums (first w entries valid), carry_out, phase4_fired."""
+
+    sums: np.ndarray
+    carry_out: int
+    phase4_fired: bool
+
+
+def _chunk(sub: bool, a, b, carry_in: int, w: int) -> ChunkResult:
+    w = int(w)
+    if w < 1 or w > 8:
+        raise InvalidArgument("chunk width must be in 1..8")  # addsub.cpp:174
+    a, b = _host_u64(a, "a"), _host_u64(b, "b")
+    if a.size != w or b.size != w:
+        raise InvalidArgument("chunk operands must have exactly w limbs")  # addsub.cpp:175-176
+    if int(carry_in) not in (0, 1):
+        raise InvalidArgument("carry_in must be 0 or 1")  # addsub.cpp:177
+    sums = np.zeros(8, np.uint64)
+    co, fi = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    check(lib().dotg_chunk_host(int(sub), _hp(sums), ctypes.byref(co), ctypes.byref(fi), _hp(a), _hp(b),
+                                int(carry_in), w))
+    return ChunkResult(sums, int(co.value), bool(fi.value))
+
+
+def add_w_limbs(a, b, carry_in: int, w: int) -> ChunkResult:
+    """One chunk of w lanes (addsub.hpp:86-87)."""
+    return _chunk(False, a, b, carry_in, w)
+
+
+def sub_w_limbs(a, b, borrow_in: int, w: int) -> ChunkResult:
+    """One chunk of w lanes, subtraction (addsub.hpp:88-89)."""
+    return _chunk(True, a, b, borrow_in, w)
 
 
 def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
@@ -391,6 +431,28 @@ def compare_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
         raise InvalidArgument("compare: out must be a contiguous int32 tensor of batch entries")
     check(lib().dotg_compare_batch(_dptr(out), _dptr(a), _dptr(b), m, batch, lay, _stream_handle(stream)))
     return out
+
+
+def chunk_batch(sub: bool, a, b, carry_in=None, *, stream=None):
+    """Batched add_w_limbs / sub_w_limbs: a, b are [batch, w] device tensors (1 <= w <= 8),
+    carry_in an int32 [batch] tensor or None. Returns (sums, carry_out, phase4_fired)."""
+    torch = _torch()
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.dim() != 2 or a.shape != b.shape:
+        raise InvalidArgument("chunk: operands are [batch, w] tensors of one shape")
+    batch, w = a.shape
+    sums = torch.empty_like(a)
+    co = torch.empty(batch, dtype=torch.int32, device=a.device)
+    fi = torch.empty(batch, dtype=torch.int32, device=a.device)
+    cin = 0
+    if carry_in is not None:
+        if carry_in.dtype != torch.int32 or carry_in.numel() != batch or not carry_in.is_contiguous():
+            raise InvalidArgument("chunk: carry_in must be a contiguous int32 tensor of batch entries")
+        cin = _dptr(carry_in)
+    check(lib().dotg_chunk_batch(int(sub), _dptr(sums), _dptr(co), _dptr(fi), _dptr(a), _dptr(b), cin, w, batch,
+                                 _stream_handle(stream)))
+    return sums, co, fi
 
 
 def words(sub: bool, a, b, out=None, carry=None, *, stream=None):

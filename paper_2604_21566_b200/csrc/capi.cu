@@ -729,6 +729,56 @@ int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "compare");
 }
 
+int dotg_chunk_batch(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phase4_fired, const uint64_t* a,
+                     const uint64_t* b, const uint32_t* carry_in, unsigned w, size_t batch, dotg_stream_t stream) {
+    if (w < 1 || w > 8) return fail(DOTG_EINVAL, "chunk width must be in 1..8");  // addsub.cpp:174
+    if (batch == 0) return DOTG_OK;
+    if (sums == nullptr || carry_out == nullptr || a == nullptr || b == nullptr)
+        return fail(DOTG_EINVAL, "chunk: null operand");
+    if (batch > SIZE_MAX / 64) return fail(DOTG_EINVAL, "chunk: size overflow");
+    const size_t bytes = batch * w * 8;
+    if (bad_alias(sums, a, bytes) || bad_alias(sums, b, bytes))
+        return fail(DOTG_EINVAL, "chunk: sums partially overlaps an operand");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_chunk_batch(sub != 0, sums, carry_out, phase4_fired, a, b, carry_in, w, batch,
+                                             static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "chunk");
+}
+
+int dotg_chunk_host(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phase4_fired, const uint64_t* a,
+                    const uint64_t* b, uint32_t carry_in, unsigned w) {
+    if (w < 1 || w > 8) return fail(DOTG_EINVAL, "chunk width must be in 1..8");  // addsub.cpp:174
+    if (carry_in > 1) return fail(DOTG_EINVAL, "carry_in must be 0 or 1");         // addsub.cpp:177
+    if (sums == nullptr || carry_out == nullptr || a == nullptr || b == nullptr)
+        return fail(DOTG_EINVAL, "chunk: null operand");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    cudaStream_t st = g_host.s[0];
+    // one staging block: a[8] b[8] sums[8] | carry_in carry_out fired
+    uint64_t* d = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), 26 * 8, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("chunk: ") + cudaGetErrorString(e));
+    uint32_t* flags = reinterpret_cast<uint32_t*>(d + 24);
+    uint32_t res[2] = {0, 0};
+    e = cudaMemcpyAsync(d, a, w * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + 8, b, w * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(flags, &carry_in, 4, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = dotg::launch_chunk_batch(sub != 0, d + 16, flags + 1, flags + 2, d, d + 8, flags, w, 1, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(sums, d + 16, w * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(res, flags + 1, 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaFreeAsync(d, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "chunk host");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    *carry_out = res[0];
+    if (phase4_fired != nullptr) *phase4_fired = res[1];
+    return DOTG_OK;
+}
+
 int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, int width,
                           uint32_t* carry, uint64_t* chunks, uint64_t* fires) {
     int rc = dotg_validate_width(width);

@@ -91,6 +91,11 @@ cudaError_t launch_compare_batch(int32_t* out, const uint64_t* a, const uint64_t
 cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                                 size_t batch, int layout, unsigned lanes, uint64_t* counters, cudaStream_t st);
 
+// Chunk-level add_w_limbs / sub_w_limbs, batched (chunk.cu).
+cudaError_t launch_chunk_batch(bool sub, uint64_t* sums, uint32_t* carry_out, uint32_t* fired, const uint64_t* a,
+                               const uint64_t* b, const uint32_t* carry_in, unsigned w, size_t batch,
+                               cudaStream_t st);
+
 // Workload setup: splitmix64 counter fill (util.cu).
 cudaError_t launch_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, cudaStream_t st);
 

@@ -92,6 +92,51 @@ void run(const char* name, const std::function<void()>& f) {
 }  // namespace
 
 int main() {
+    run("add chunk: all-ones plus carry-in clears every lane", [] {  // test_addsub.cpp:50-57
+        const ChunkResult r = add_w_limbs(Limbs(8, kMax), Limbs(8, 0), 1, 8);
+        for (unsigned i = 0; i < 8; ++i) CHECK(r.sums[i] == 0);
+        CHECK(r.carry_out == 1);
+        CHECK(r.phase4_fired);
+    });
+    run("sub chunk: borrow-in cascades through zero lanes", [] {  // 59-66
+        const ChunkResult r = sub_w_limbs(Limbs(8, 0), Limbs(8, 0), 1, 8);
+        for (unsigned i = 0; i < 8; ++i) CHECK(r.sums[i] == kMax);
+        CHECK(r.carry_out == 1);
+        CHECK(r.phase4_fired);
+    });
+    run("add chunk: generated carry ripples into a later lane", [] {  // 68-79
+        const ChunkResult r = add_w_limbs(Limbs{kMax, kMax, 0, 0, 0, 0, 0, 0}, Limbs{1, 0, 0, 0, 0, 0, 0, 0}, 0, 8);
+        CHECK(r.sums[0] == 0 && r.sums[1] == 0 && r.sums[2] == 1);
+        for (unsigned i = 3; i < 8; ++i) CHECK(r.sums[i] == 0);
+        CHECK(r.carry_out == 0);
+        CHECK(r.phase4_fired);
+    });
+    run("chunk argument validation", [] {  // 81-90
+        const Limbs a(8, 1), b(8, 1), short_b(7, 1);
+        CHECK_THROWS_AS(add_w_limbs(a, b, 0, 0), std::invalid_argument);
+        CHECK_THROWS_AS(add_w_limbs(a, b, 0, 9), std::invalid_argument);
+        CHECK_THROWS_AS(add_w_limbs(a, b, 2, 8), std::invalid_argument);
+        CHECK_THROWS_AS(add_w_limbs(a, short_b, 0, 8), std::invalid_argument);
+        CHECK_THROWS_AS(sub_w_limbs(a, b, 0, 9), std::invalid_argument);
+    });
+    run("random chunks match the oracle chunk for every w", [] {  // 92-118
+        std::mt19937_64 rng(0x9d5c0ff1u);
+        for (unsigned w = 1; w <= 8; ++w) {
+            for (int iter = 0; iter < 300; ++iter) {
+                const Limbs a = spiky_limbs(rng, w), b = spiky_limbs(rng, w);
+                const unsigned cin = unsigned(rng() & 1u);
+                for (int sub = 0; sub < 2; ++sub) {
+                    Limbs want(8, 0);
+                    int p4 = 0;
+                    const unsigned wc = dotor_chunk(sub, want.data(), a.data(), b.data(), cin, w, &p4);
+                    const ChunkResult r = sub ? sub_w_limbs(a, b, cin, w) : add_w_limbs(a, b, cin, w);
+                    CHECK(Limbs(r.sums.begin(), r.sums.begin() + w) == Limbs(want.begin(), want.begin() + w));
+                    CHECK(r.carry_out == wc);
+                    CHECK(r.phase4_fired == (p4 != 0));
+                }
+            }
+        }
+    });
     run("2^512 - 1 plus 1 rolls over into the flag", [] {  // test_addsub.cpp:124-130
         const WordsResult r = dot_add_words(Limbs(8, kMax), Limbs{1});
         CHECK(r.limbs == Limbs(8, 0));
