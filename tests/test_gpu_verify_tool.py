@@ -75,3 +75,34 @@ def test_stats_line_matches_reference(cuda, ref, width):
     r = run("verify", CORPUS, "--width", width)
     assert r.returncode == 0, r.stdout + r.stderr
     assert f"chunks {chunks}, phase4 triggers {fires} (rate {fires / chunks:.6f})" in r.stdout, r.stdout
+
+
+def test_bench_rows_and_gate(cuda, tmp_path):
+    """dotg-verify bench (dotarith bench over a corpus): one row per (op, bits) group with
+    device and host-buffer ns/op and the Phase-4 rate; a group that fails verification
+    gets no row and the exit code is 1 (bench.cpp:201-204, dotarith_cli.cpp:120-131)."""
+    import json
+
+    groups = {(c["op"], c["bits"]) for c in map(json.loads, open(CORPUS))}
+    csv = tmp_path / "rows.csv"
+    r = run("bench", CORPUS, "--reps", "3", "--csv", str(csv))
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = [ln.split() for ln in r.stdout.splitlines()[1:] if ln.split() and ln.split()[0] in ("add", "sub", "mul")]
+    assert {(x[0], int(x[1])) for x in rows} == groups
+    for x in rows:
+        assert float(x[5]) > 0 and float(x[7]) > 0 and x[-1] == "cuda-events"
+    lines = csv.read_text().splitlines()
+    assert lines[0].startswith("op,bits,w,kernel") and len(lines) == len(groups) + 1
+    # corrupt one add case: its group loses its row, the others still print
+    src = open(CORPUS).read().splitlines()
+    i = next(k for k, ln in enumerate(src) if json.loads(ln)["op"] == "add")
+    c = json.loads(src[i])
+    head, tail = src[i].split('"expected":"')
+    val, rest = tail.split('"', 1)
+    src[i] = head + '"expected":"' + val[:-1] + ("0" if val[-1] != "0" else "1") + '"' + rest
+    bad = tmp_path / "bad.jsonl"
+    bad.write_text("\n".join(src) + "\n")
+    r = run("bench", str(bad), "--reps", "2")
+    assert r.returncode == 1 and "failed verification" in r.stderr
+    rows = [ln.split() for ln in r.stdout.splitlines()[1:] if ln.split() and ln.split()[0] in ("add", "sub", "mul")]
+    assert ("add", c["bits"]) not in {(x[0], int(x[1])) for x in rows} and len(rows) == len(groups) - 1

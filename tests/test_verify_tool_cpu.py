@@ -17,7 +17,14 @@ def run(*args):
 
 def test_usage_and_width():
     assert run().returncode == 2
-    assert run("bench", CORPUS).returncode == 2
+    assert run("gen", CORPUS).returncode == 2
+    r = run("bench", CORPUS, "--reps", "0")
+    assert r.returncode == 2 and "at least one repetition" in r.stderr
+    r = run("bench", CORPUS, "--warmup", "3")
+    assert r.returncode == 2 and "unknown option" in r.stderr
+    r = run("verify", CORPUS, "--reps", "3")  # bench-only option
+    assert r.returncode == 2 and "unknown option" in r.stderr
+    assert run("bench", CORPUS, "--width").returncode == 2
     r = run("verify", CORPUS, "--width", "16")
     assert r.returncode == 2 and "unknown width" in r.stderr
 

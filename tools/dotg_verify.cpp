@@ -9,7 +9,18 @@
 //   "kernel b200 (w=8, sm_100a): N cases, K mismatches", the AddSubStats line
 //   "chunks C, phase4 triggers T (rate R)" when the corpus has add/sub cases, up to 10
 //   "mismatch at case i" lines, exit 0 = all match, 1 = mismatch, 2 = usage / input error.
+//
+// `dotg-verify bench <corpus.jsonl> [--width w] [--reps R] [--csv path]` is the device
+// counterpart of `dotarith bench` (dotarith_cli.cpp:103-139, bench.cpp:176-245) over a
+// corpus file: per (op, bits) group the verification gate first (no row for a group that
+// mismatches, exit 1), then R timed repetitions of the group's batched call with the
+// operands resident in device memory (CUDA events; ns per case, mean and Student-t 95%
+// half-width like bench.cpp:216-225), the same call through the host-buffer entry point
+// (PCIe copies included), and the group's Phase-4 rate.
+#include <cuda_runtime.h>
+
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -147,18 +158,229 @@ std::vector<Case> read_corpus(const std::string& path) {  // read_vectors, testg
     return out;
 }
 
+using Groups = std::map<std::pair<std::string, unsigned>, std::vector<size_t>>;
+
+Groups group_cases(const std::vector<Case>& corpus) {  // one batched device call per (op, bits)
+    Groups groups;
+    for (size_t i = 0; i < corpus.size(); ++i) groups[{corpus[i].op, corpus[i].bits}].push_back(i);
+    return groups;
+}
+
+// Row-major operands of one group.
+void gather(const std::vector<Case>& corpus, const std::vector<size_t>& ids, size_t m, Limbs& A, Limbs& B) {
+    const size_t n = ids.size();
+    A.assign(n * m, 0);
+    B.assign(n * m, 0);
+    for (size_t k = 0; k < n; ++k)
+        for (size_t j = 0; j < m; ++j) {
+            A[k * m + j] = corpus[ids[k]].a[j];
+            B[k * m + j] = corpus[ids[k]].b[j];
+        }
+}
+
+int host_call(const std::string& op, Limbs& out, const Limbs& A, const Limbs& B, std::vector<uint32_t>& fl,
+              size_t m, size_t n) {
+    return op == "mul"   ? dotg_mul_batch_host(out.data(), A.data(), B.data(), m, n)
+           : op == "add" ? dotg_add_batch_host(out.data(), A.data(), B.data(), fl.data(), m, n)
+                         : dotg_sub_batch_host(out.data(), A.data(), B.data(), fl.data(), m, n);
+}
+
+// Verification gate of one group: ids of the mismatching cases.
+std::vector<size_t> check_group(const std::vector<Case>& corpus, const std::string& op, size_t m,
+                                const std::vector<size_t>& ids) {
+    const size_t n = ids.size();
+    const bool mul = op == "mul";
+    Limbs A, B;
+    gather(corpus, ids, m, A, B);
+    Limbs out(n * m * (mul ? 2 : 1));
+    std::vector<uint32_t> fl(n);
+    if (host_call(op, out, A, B, fl, m, n) != DOTG_OK)
+        throw std::runtime_error(std::string("device call failed: ") + dotg_last_error());
+    std::vector<size_t> bad;
+    for (size_t k = 0; k < n; ++k) {
+        const Case& c = corpus[ids[k]];
+        bool ok;
+        if (mul) {
+            size_t len = 2 * m;
+            while (len > 0 && out[k * 2 * m + len - 1] == 0) --len;  // products compare trimmed
+            ok = c.expected == Limbs(out.begin() + k * 2 * m, out.begin() + k * 2 * m + len);
+        } else {
+            ok = c.expected == Limbs(out.begin() + k * m, out.begin() + (k + 1) * m) && c.flag == fl[k];
+        }
+        if (!ok) bad.push_back(ids[k]);
+    }
+    return bad;
+}
+
+// AddSubStats of the add/sub cases of `ids` (bench.cpp:160-161 collects them for the vector
+// add/sub kernels): chunks of lane_count(width) limbs and how many would have taken the
+// rare Phase 4, derived on the device per case (dotg_words_host_stats).
+void group_stats(const std::vector<Case>& corpus, const std::vector<size_t>& ids, int width, uint64_t& chunks,
+                 uint64_t& fires) {
+    for (const size_t i : ids) {
+        const Case& c = corpus[i];
+        if (c.op == "mul") continue;
+        Limbs o(c.a.size());
+        uint32_t carry = 0;
+        if (dotg_words_host_stats(c.op == "sub", o.data(), c.a.data(), c.b.data(), c.a.size(), width, &carry,
+                                  &chunks, &fires) != DOTG_OK)
+            throw std::runtime_error(std::string("stats call failed: ") + dotg_last_error());
+    }
+}
+
+double t95(size_t dof) {  // two-sided Student t, 95% (bench.cpp:216-225 uses the same table idea)
+    static const double tab[] = {0, 12.706, 4.303, 3.182, 2.776, 2.571, 2.447, 2.365, 2.306, 2.262, 2.228,
+                                 2.201, 2.179, 2.160, 2.145, 2.131, 2.120, 2.110, 2.101, 2.093, 2.086,
+                                 2.080, 2.074, 2.069, 2.064, 2.060, 2.056, 2.052, 2.048, 2.045, 2.042};
+    return dof < sizeof(tab) / sizeof(tab[0]) ? tab[dof] : 1.960;
+}
+
+void mean_ci(const std::vector<double>& v, double& mean, double& ci) {
+    mean = 0;
+    for (double x : v) mean += x;
+    mean /= double(v.size());
+    ci = 0;
+    if (v.size() > 1) {
+        double var = 0;
+        for (double x : v) var += (x - mean) * (x - mean);
+        var /= double(v.size() - 1);
+        ci = t95(v.size() - 1) * std::sqrt(var / double(v.size()));
+    }
+}
+
+#define CUDA_OR_THROW(x)                                                                            \
+    do {                                                                                            \
+        const cudaError_t e_ = (x);                                                                 \
+        if (e_ != cudaSuccess) throw std::runtime_error(std::string(#x ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+int cmd_bench(const std::vector<Case>& corpus, int width, unsigned reps, const std::string& csv_path) {
+    const Groups groups = group_cases(corpus);
+    bool mismatched = false;
+    std::string csv = "op,bits,w,kernel,cases,ns_per_op_device,ci95_device,ns_per_op_host,ci95_host,phase4,timer\n";
+    const std::string wname = width == 0 ? "scalar" : "w" + std::to_string(width);
+    std::printf("%-4s %6s %7s %-12s %7s %14s %10s %14s %10s %8s %s\n", "op", "bits", "w", "kernel", "cases",
+                "ns/op(dev)", "ci95", "ns/op(host)", "ci95", "phase4", "timer");
+    for (const auto& [key, ids] : groups) {
+        const std::string& op = key.first;
+        const size_t m = key.second / 64, n = ids.size();
+        const std::vector<size_t> bad = check_group(corpus, op, m, ids);
+        if (!bad.empty()) {  // no row for a group that fails verification (bench.cpp:201-204)
+            std::fprintf(stderr, "bench: b200 failed verification at %u bits (%s): %zu mismatches\n", key.second,
+                         op.c_str(), bad.size());
+            mismatched = true;
+            continue;
+        }
+        const bool mul = op == "mul";
+        Limbs A, B;
+        gather(corpus, ids, m, A, B);
+        const size_t in_bytes = n * m * 8, out_bytes = in_bytes * (mul ? 2 : 1);
+        uint64_t *da = nullptr, *db = nullptr, *dout = nullptr;
+        uint32_t* dfl = nullptr;
+        cudaStream_t st = nullptr;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        CUDA_OR_THROW(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CUDA_OR_THROW(cudaEventCreate(&e0));
+        CUDA_OR_THROW(cudaEventCreate(&e1));
+        CUDA_OR_THROW(cudaMalloc(&da, in_bytes));
+        CUDA_OR_THROW(cudaMalloc(&db, in_bytes));
+        CUDA_OR_THROW(cudaMalloc(&dout, out_bytes));
+        CUDA_OR_THROW(cudaMalloc(&dfl, n * 4));
+        CUDA_OR_THROW(cudaMemcpy(da, A.data(), in_bytes, cudaMemcpyHostToDevice));
+        CUDA_OR_THROW(cudaMemcpy(db, B.data(), in_bytes, cudaMemcpyHostToDevice));
+        auto dev_call = [&] {
+            const int rc = mul ? dotg_mul_batch(dout, da, db, m, n, DOTG_ROW_MAJOR, st)
+                           : op == "add" ? dotg_add_batch(dout, da, db, dfl, m, n, DOTG_ROW_MAJOR, st)
+                                         : dotg_sub_batch(dout, da, db, dfl, m, n, DOTG_ROW_MAJOR, st);
+            if (rc != DOTG_OK) throw std::runtime_error(std::string("device call failed: ") + dotg_last_error());
+        };
+        // device-resident: each sample is a CUDA-event-timed launch sequence of `inner` calls
+        const unsigned inner = 10;
+        std::vector<double> dev(reps), host(reps);
+        for (int w = 0; w < 3; ++w) dev_call();
+        for (unsigned r = 0; r < reps; ++r) {
+            CUDA_OR_THROW(cudaEventRecord(e0, st));
+            for (unsigned k = 0; k < inner; ++k) dev_call();
+            CUDA_OR_THROW(cudaEventRecord(e1, st));
+            CUDA_OR_THROW(cudaEventSynchronize(e1));
+            float ms = 0;
+            CUDA_OR_THROW(cudaEventElapsedTime(&ms, e0, e1));
+            dev[r] = double(ms) * 1e6 / double(inner) / double(n);
+        }
+        // host buffers: the same call through the host entry point, copies included
+        Limbs out(out_bytes / 8);
+        std::vector<uint32_t> fl(n);
+        for (unsigned r = 0; r < reps; ++r) {
+            CUDA_OR_THROW(cudaEventRecord(e0, nullptr));
+            if (host_call(op, out, A, B, fl, m, n) != DOTG_OK)
+                throw std::runtime_error(std::string("device call failed: ") + dotg_last_error());
+            CUDA_OR_THROW(cudaEventRecord(e1, nullptr));
+            CUDA_OR_THROW(cudaEventSynchronize(e1));
+            float ms = 0;
+            CUDA_OR_THROW(cudaEventElapsedTime(&ms, e0, e1));
+            host[r] = double(ms) * 1e6 / double(n);
+        }
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dout);
+        cudaFree(dfl);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        uint64_t chunks = 0, fires = 0;
+        group_stats(corpus, ids, width, chunks, fires);
+        const double p4 = chunks ? double(fires) / double(chunks) : 0.0;
+        double dm, dc, hm, hc;
+        mean_ci(dev, dm, dc);
+        mean_ci(host, hm, hc);
+        std::printf("%-4s %6u %7s %-12s %7zu %14.3f %10.3f %14.3f %10.3f %8.4f %s\n", op.c_str(), key.second,
+                    wname.c_str(), "b200", n, dm, dc, hm, hc, p4, "cuda-events");
+        char line[512];
+        std::snprintf(line, sizeof line, "%s,%u,%s,b200,%zu,%.4f,%.4f,%.4f,%.4f,%.6f,cuda-events\n", op.c_str(),
+                      key.second, wname.c_str(), n, dm, dc, hm, hc, p4);
+        csv += line;
+    }
+    std::printf("timer: cuda-events (device clock; ns per case, batched per (op, bits) group)\n");
+    if (!csv_path.empty()) {
+        std::ofstream f(csv_path, std::ios::binary | std::ios::trunc);
+        if (!f || !(f << csv)) throw std::runtime_error("cannot write " + csv_path);
+    }
+    return mismatched ? 1 : 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
-    if (argc < 3 || std::string(argv[1]) != "verify") {
-        std::fprintf(stderr, "usage: dotg-verify verify <corpus.jsonl> [--width scalar|2|4|8]\n");
+    const std::string cmd = argc >= 2 ? argv[1] : "";
+    if (argc < 3 || (cmd != "verify" && cmd != "bench")) {
+        std::fprintf(stderr,
+                     "usage: dotg-verify verify <corpus.jsonl> [--width scalar|2|4|8]\n"
+                     "       dotg-verify bench <corpus.jsonl> [--width scalar|2|4|8] [--reps R] [--csv path]\n");
         return 2;
     }
     int width = 8;
-    for (int i = 3; i + 1 < argc; i += 2) {
-        if (std::string(argv[i]) == "--width") {
-            const std::string w = argv[i + 1];
-            width = w == "scalar" ? 0 : std::atoi(w.c_str());
+    unsigned reps = 10;
+    std::string csv_path;
+    for (int i = 3; i < argc; i += 2) {
+        const std::string opt = argv[i];
+        if (i + 1 >= argc) {
+            std::fprintf(stderr, "option %s needs a value\n", opt.c_str());
+            return 2;
+        }
+        const std::string val = argv[i + 1];
+        if (opt == "--width") {
+            width = val == "scalar" ? 0 : std::atoi(val.c_str());
+        } else if (opt == "--reps" && cmd == "bench") {
+            reps = unsigned(std::strtoul(val.c_str(), nullptr, 10));
+            if (reps == 0) {
+                std::fprintf(stderr, "bench needs at least one repetition\n");
+                return 2;
+            }
+        } else if (opt == "--csv" && cmd == "bench") {
+            csv_path = val;
+        } else {
+            std::fprintf(stderr, "unknown option: %s\n", opt.c_str());
+            return 2;
         }
     }
     if (dotg_validate_width(width) != DOTG_OK) {
@@ -172,54 +394,27 @@ int main(int argc, char** argv) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 2;
     }
-    // group case ids by (op, bits): one batched device call per group
-    std::map<std::pair<std::string, unsigned>, std::vector<size_t>> groups;
-    for (size_t i = 0; i < corpus.size(); ++i) groups[{corpus[i].op, corpus[i].bits}].push_back(i);
-    std::vector<size_t> bad;
-    for (const auto& [key, ids] : groups) {
-        const size_t m = key.second / 64, n = ids.size();
-        Limbs A(n * m), B(n * m);
-        for (size_t k = 0; k < n; ++k)
-            for (size_t j = 0; j < m; ++j) {
-                A[k * m + j] = corpus[ids[k]].a[j];
-                B[k * m + j] = corpus[ids[k]].b[j];
-            }
-        const bool mul = key.first == "mul";
-        Limbs out(n * m * (mul ? 2 : 1));
-        std::vector<uint32_t> fl(n);
-        int rc = mul ? dotg_mul_batch_host(out.data(), A.data(), B.data(), m, n)
-                     : key.first == "add" ? dotg_add_batch_host(out.data(), A.data(), B.data(), fl.data(), m, n)
-                                          : dotg_sub_batch_host(out.data(), A.data(), B.data(), fl.data(), m, n);
-        if (rc != DOTG_OK) {
-            std::fprintf(stderr, "error: device call failed: %s\n", dotg_last_error());
+    if (cmd == "bench") {
+        try {
+            return cmd_bench(corpus, width, reps, csv_path);
+        } catch (const std::exception& e) {
+            std::fprintf(stderr, "error: %s\n", e.what());
             return 2;
-        }
-        for (size_t k = 0; k < n; ++k) {
-            const Case& c = corpus[ids[k]];
-            bool ok;
-            if (mul) {
-                size_t len = 2 * m;
-                while (len > 0 && out[k * 2 * m + len - 1] == 0) --len;  // products compare trimmed
-                ok = c.expected == Limbs(out.begin() + k * 2 * m, out.begin() + k * 2 * m + len);
-            } else {
-                ok = c.expected == Limbs(out.begin() + k * m, out.begin() + (k + 1) * m) && c.flag == fl[k];
-            }
-            if (!ok) bad.push_back(ids[k]);
         }
     }
-    // AddSubStats of the add/sub cases (bench.cpp:160-161 collects them for the vector
-    // add/sub kernels): chunks of lane_count(width) limbs and how many would have taken
-    // the rare Phase 4, derived on the device per case (dotg_words_host_stats).
+    std::vector<size_t> bad;
     uint64_t chunks = 0, fires = 0;
-    for (const Case& c : corpus) {
-        if (c.op == "mul") continue;
-        Limbs o(c.a.size());
-        uint32_t carry = 0;
-        if (dotg_words_host_stats(c.op == "sub", o.data(), c.a.data(), c.b.data(), c.a.size(), width, &carry,
-                                  &chunks, &fires) != DOTG_OK) {
-            std::fprintf(stderr, "error: stats call failed: %s\n", dotg_last_error());
-            return 2;
+    try {
+        for (const auto& [key, ids] : group_cases(corpus)) {
+            const std::vector<size_t> b = check_group(corpus, key.first, key.second / 64, ids);
+            bad.insert(bad.end(), b.begin(), b.end());
         }
+        std::vector<size_t> all(corpus.size());
+        for (size_t i = 0; i < all.size(); ++i) all[i] = i;
+        group_stats(corpus, all, width, chunks, fires);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 2;
     }
     std::sort(bad.begin(), bad.end());
     std::printf("kernel b200 (w=%s, sm_100a): %zu cases, %zu mismatches\n",
