@@ -416,6 +416,24 @@ def mul_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
     return out
 
 
+def addsub_stats(sub: bool, out, a, b, *, width=Width.w8, layout=ROW_MAJOR, stream=None):
+    """AddSubStats counters (addsub.hpp:53-72) of a finished batched add/sub, derived on the
+    device from a, b and out (csrc/stats.cu): (chunks_processed, phase4_triggers) for chunks
+    of lane_count(width) limbs. Synchronises the stream to return host integers."""
+    torch = _torch()
+    lay = _layout(layout)
+    for t, name in ((out, "out"), (a, "a"), (b, "b")):
+        _check_dev(t, name)
+    if not (a.shape == b.shape == out.shape):
+        raise InvalidArgument("stats: operand shapes differ")
+    batch, m = _batch_dims(a, lay)
+    cnt = torch.zeros(2, dtype=torch.int64, device=a.device)
+    check(lib().dotg_addsub_stats(int(sub), _dptr(out), _dptr(a), _dptr(b), m, batch, lay, int(width), _dptr(cnt),
+                                  _stream_handle(stream)))
+    ch, fi = cnt.tolist()
+    return int(ch), int(fi)
+
+
 def compare_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
     """compare(a[p], b[p]) per pair (limbs.hpp:84): int32 tensor of -1 / 0 / +1."""
     torch = _torch()

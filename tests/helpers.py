@@ -296,6 +296,11 @@ def category(rng, cat, op, shape):
         b |= top
     elif cat == "spiky":
         a, b = spiky(rng, shape), spiky(rng, shape)
+    elif cat == "mixed":  # testgen.cpp:129-137: per case one of the six non-mixed shapes
+        pick = rng.integers(0, 6, size=shape[:-1])
+        for k, sub_cat in enumerate(CATEGORIES[:6]):
+            sa, sb = category(rng, sub_cat, op, shape)
+            a[pick == k], b[pick == k] = sa[pick == k], sb[pick == k]
     else:
         raise ValueError(cat)
     return a, b
