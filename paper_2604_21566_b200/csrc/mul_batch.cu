@@ -440,9 +440,18 @@ __device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uin
     return absdiff<kK>(X, Y, D);
 }
 
-// 126 registers (4 CTAs/SM); forcing 5 CTAs/SM spills and runs slower (42.7 vs 40.0 us).
-__global__ void __launch_bounds__(128) k_mul_kara16(uint64_t* out, const uint64_t* a, const uint64_t* b,
-                                                    size_t batch) {
+// 128 registers, 16 warps/SM. One warp per CTA (16 CTAs/SM) trims the partial last wave:
+// C3 38.5 us vs 39.7 us with 128-thread CTAs (tools/k16var.sh). Capping registers for 20
+// warps/SM (96 registers) spills 236 B and runs 44-46 us; uncapped, ptxas takes 186
+// registers (8 warps/SM) and runs 54-56 us.
+#ifndef DOTG_K16_TPB
+#define DOTG_K16_TPB 32
+#endif
+#ifndef DOTG_K16_MINB
+#define DOTG_K16_MINB 16
+#endif
+__global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint64_t* out, const uint64_t* a,
+                                                                           const uint64_t* b, size_t batch) {
     const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (pidx >= batch) return;
     uint32_t Al[kK], Ah[kK], Bl[kK], Bh[kK];
@@ -765,7 +774,8 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
             break;
         case 16:
             if (al) {  // C3: 40.0 us vs 42.1 us for the plain 16-column kernel (tools/mul_timing.py)
-                k_mul_kara16<<<unsigned((batch + 127) / 128), 128, 0, stream>>>(out, a, b, batch);
+                k_mul_kara16<<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0, stream>>>(
+                    out, a, b, batch);
                 count_launch();
                 return cudaGetLastError();
             }
