@@ -49,7 +49,7 @@ __global__ void k_imad(uint32_t* out, long long* cyc, uint32_t seed, int iters) 
 
 __global__ void k_imad_wide(uint32_t* out, long long* cyc, uint32_t seed, int iters) {
     uint64_t x[kChains];
-    const uint32_t y = seed ^ threadIdx.x, z = seed * 3u + 1u;
+    const uint32_t y = seed ^ threadIdx.x;
     for (int j = 0; j < kChains; ++j) x[j] = seed + threadIdx.x * 7u + j;
     __syncthreads();
     long long t0 = clock64();
