@@ -41,6 +41,10 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 // The device path is sm_100a-only; refuse anything else loudly (no CPU fallback).
 int check_device() {
+    // Start every call with a clean runtime error state: a non-sticky error left by an
+    // earlier failed call (e.g. an allocation that ran out of memory) must not be reported
+    // by this call's first cudaGetLastError. Sticky device faults persist regardless.
+    (void)cudaGetLastError();
     static thread_local int ok_dev = -1;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);

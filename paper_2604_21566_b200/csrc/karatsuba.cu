@@ -20,7 +20,9 @@
 // so every leaf is one exact IMMA multiply.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -160,35 +162,69 @@ struct KaraPlan {
     std::vector<size_t> pm, h;
 };
 
-cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, const KaraPlan& plan,
-                          cudaStream_t st) {
+// Peak scratch bytes of a breadth-first run over levels d0.. of `plan`: each level's
+// buffers are released (stream-ordered) as soon as the next level has consumed them, so
+// the peak is the largest adjacent pair of levels (in practice the leaves: their operands
+// plus their products) plus the per-level sign arrays.
+size_t kara_bf_bytes(const KaraPlan& plan, size_t d0, size_t batch) {
+    auto r256 = [](size_t x) { return (x < 256 ? 256 : x + 255) / 256 * 256; };
+    const size_t L = plan.h.size();
+    std::vector<size_t> cnt(L + 1);
+    cnt[d0] = batch;
+    for (size_t d = d0; d < L; ++d) cnt[d + 1] = 3 * cnt[d];
+    size_t signs = 0, peak = 0;
+    for (size_t d = d0; d < L; ++d) {
+        signs += 2 * r256(cnt[d] * 4);
+        const size_t in = d > d0 ? 2 * r256(cnt[d] * plan.pm[d] * 8) : 0;
+        peak = std::max(peak, in + 2 * r256(3 * cnt[d] * plan.h[d] * 8));
+    }
+    const size_t cm = plan.h[L - 1];
+    peak = std::max(peak, 2 * r256(cnt[L] * cm * 8) + r256(cnt[L] * 2 * cm * 8));
+    for (size_t d = d0 + 1; d < L; ++d)  // combine at level d: children's products -> level-d products
+        peak = std::max(peak, r256(cnt[d + 1] * 2 * plan.h[d] * 8) + r256(cnt[d] * 2 * plan.pm[d] * 8));
+    return peak + signs;
+}
+
+cudaError_t run_karatsuba_bf(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch,
+                             const KaraPlan& plan, size_t d0, cudaStream_t st) {
     struct Level {
         size_t m, h, count;
         uint32_t *sa, *sb;  // signs of this level's differences: [count]
     };
     std::vector<Level> lv;
-    std::vector<void*> allocs;
+    std::vector<void*> signs;  // released at the end
     auto alloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
         if (cudaMallocAsync(&p, bytes < 256 ? 256 : bytes, st) != cudaSuccess) return nullptr;
-        allocs.push_back(p);
         return p;
     };
-    auto cleanup = [&]() {
-        for (void* p : allocs) cudaFreeAsync(p, st);
+    auto release = [&](const void* p) {
+        if (p != nullptr) cudaFreeAsync(const_cast<void*>(p), st);
     };
-    size_t count = batch, cm = plan.pm.empty() ? 0 : plan.pm[0];
+    auto cleanup = [&]() {
+        for (void* p : signs) cudaFreeAsync(p, st);
+    };
+    size_t count = batch, cm = plan.pm.empty() ? 0 : plan.pm[d0];
     const uint64_t* A = a;
     const uint64_t* B = b;
-    // Descend: split every level until the base case.
-    for (size_t d = 0; d < plan.h.size(); ++d) {
+    // Descend: split every level until the base case; a level's operands are released once
+    // the next level's split has been issued.
+    for (size_t d = d0; d < plan.h.size(); ++d) {
         const size_t h = plan.h[d];
         Level L{plan.pm[d], h, count, nullptr, nullptr};
         uint64_t* nA = static_cast<uint64_t*>(alloc(3 * count * h * 8));
         uint64_t* nB = static_cast<uint64_t*>(alloc(3 * count * h * 8));
         L.sa = static_cast<uint32_t*>(alloc(count * 4));
         L.sb = static_cast<uint32_t*>(alloc(count * 4));
+        if (L.sa) signs.push_back(L.sa);
+        if (L.sb) signs.push_back(L.sb);
         if (!nA || !nB || !L.sa || !L.sb) {
+            release(nA);
+            release(nB);
+            if (d > d0) {
+                release(A);
+                release(B);
+            }
             cleanup();
             return cudaErrorMemoryAllocation;
         }
@@ -198,6 +234,10 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
         k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(B, L.m, h, count, nB, nB + count * h, nB + 2 * count * h,
                                                          L.sb);
         count_launch(2);
+        if (d > d0) {
+            release(A);
+            release(B);
+        }
         lv.push_back(L);
         A = nA;
         B = nB;
@@ -207,11 +247,15 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
     // Base case: one batched column multiply of all 3^L * batch leaves.
     uint64_t* P = static_cast<uint64_t*>(alloc(count * 2 * cm * 8));
     if (!P) {
+        release(A);
+        release(B);
         cleanup();
         return cudaErrorMemoryAllocation;
     }
     cudaError_t e = launch_mul_batch(P, A, B, cm, count, 0, st);
-    // Ascend: combine level by level.
+    release(A);
+    release(B);
+    // Ascend: combine level by level, releasing each level's products once combined.
     for (size_t i = lv.size(); e == cudaSuccess && i-- > 0;) {
         const Level& L = lv[i];
         uint64_t* dst = i == 0 ? out : static_cast<uint64_t*>(alloc(L.count * 2 * L.m * 8));
@@ -223,24 +267,79 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
             P, L.h, L.count, L.sa, L.sb, dst, L.m);
         count_launch();
         e = cudaGetLastError();
+        release(P);
         P = dst;
     }
+    if (e != cudaSuccess && P != out) release(P);
     cleanup();
     return e;
+}
+
+// Depth-first above the level where the breadth-first scratch fits: the three children
+// of the top level run one after another (each as its own, smaller, breadth-first run),
+// so the largest products (up to the reference cap of 2^24 limbs, mul.hpp:26-30) stay
+// within device memory. Budget: 70% of the memory free at the call.
+cudaError_t run_karatsuba_at(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch,
+                             const KaraPlan& plan, size_t d0, size_t budget, cudaStream_t st) {
+    if (kara_bf_bytes(plan, d0, batch) <= budget || d0 + 1 == plan.h.size())
+        return run_karatsuba_bf(out, a, b, batch, plan, d0, st);
+    const size_t m = plan.pm[d0], h = plan.h[d0];
+    uint64_t *nA = nullptr, *nB = nullptr, *P = nullptr;
+    uint32_t *sa = nullptr, *sb = nullptr;
+    cudaError_t e = cudaMallocAsync(&nA, 3 * batch * h * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&nB, 3 * batch * h * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&sa, batch * 4 < 256 ? 256 : batch * 4, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&sb, batch * 4 < 256 ? 256 : batch * 4, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&P, 3 * batch * 2 * h * 8, st);
+    if (e == cudaSuccess) {
+        const unsigned grid = unsigned((batch + kKaraWarps - 1) / kKaraWarps);
+        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(a, m, h, batch, nA, nA + batch * h, nA + 2 * batch * h, sa);
+        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(b, m, h, batch, nB, nB + batch * h, nB + 2 * batch * h, sb);
+        count_launch(2);
+        e = cudaGetLastError();
+        // the next level's plan entry describes a child of h limbs (pm[d0 + 1] == h)
+        for (int k = 0; k < 3 && e == cudaSuccess; ++k)
+            e = run_karatsuba_at(P + size_t(k) * batch * 2 * h, nA + size_t(k) * batch * h,
+                                 nB + size_t(k) * batch * h, batch, plan, d0 + 1, budget, st);
+    }
+    if (e == cudaSuccess) {
+        k_kara_combine_w<<<unsigned((batch + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(P, h, batch, sa,
+                                                                                                   sb, out, m);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    for (void* q : {static_cast<void*>(nA), static_cast<void*>(nB), static_cast<void*>(sa), static_cast<void*>(sb),
+                    static_cast<void*>(P)})
+        if (q != nullptr) cudaFreeAsync(q, st);
+    return e;
+}
+
+cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, const KaraPlan& plan,
+                          cudaStream_t st) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(16) << 30;
+    size_t budget = free_b / 10 * 7;
+    if (const char* e = std::getenv("DOTG_KARA_BUDGET_MB")) budget = size_t(std::strtoull(e, nullptr, 10)) << 20;
+    return run_karatsuba_at(out, a, b, batch, plan, 0, budget, st);
 }
 
 }  // namespace
 
 void retain_stream_pool() {
     // keep freed scratch (Karatsuba levels, long-number state) cached in the device's
-    // stream-ordered pool, up to 8 GiB, instead of returning it to the driver at every sync
+    // stream-ordered pool instead of returning it to the driver at every sync
     static thread_local int pool_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (pool_dev == dev) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = uint64_t(8) << 30;
+        // a quarter of the device (45 GB on a B200): repeated large products reuse their
+        // scratch instead of re-mapping it after every synchronisation (measured: a 2^20-limb
+        // product 500-870 ms with an 8 GiB threshold, 101 ms when its 6-10 GB stay cached)
+        size_t free_b = 0, total_b = 0;
+        uint64_t thr = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? uint64_t(total_b) / 4 : uint64_t(8) << 30;
+        if (const char* e = std::getenv("DOTG_POOL_KEEP_GB")) thr = uint64_t(std::strtoull(e, nullptr, 10)) << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     pool_dev = dev;
