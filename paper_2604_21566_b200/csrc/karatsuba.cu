@@ -278,7 +278,7 @@ cudaError_t run_karatsuba_bf(uint64_t* out, const uint64_t* a, const uint64_t* b
 // Depth-first above the level where the breadth-first scratch fits: the three children
 // of the top level run one after another (each as its own, smaller, breadth-first run),
 // so the largest products (up to the reference cap of 2^24 limbs, mul.hpp:26-30) stay
-// within device memory. Budget: 70% of the memory free at the call.
+// within device memory. Budget: see run_karatsuba.
 cudaError_t run_karatsuba_at(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch,
                              const KaraPlan& plan, size_t d0, size_t budget, cudaStream_t st) {
     if (kara_bf_bytes(plan, d0, batch) <= budget || d0 + 1 == plan.h.size())
@@ -318,6 +318,9 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
                           cudaStream_t st) {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(16) << 30;
+    // breadth-first whenever it fits 70% of free memory: every depth-first level serialises
+    // three children that breadth-first runs concurrently (a 16 GiB cap made 2^22 limbs
+    // 1.48 s and 2^24 limbs 16.3 s, against 1.0-2.5 s and 8.8 s)
     size_t budget = free_b / 10 * 7;
     if (const char* e = std::getenv("DOTG_KARA_BUDGET_MB")) budget = size_t(std::strtoull(e, nullptr, 10)) << 20;
     return run_karatsuba_at(out, a, b, batch, plan, 0, budget, st);
@@ -334,11 +337,10 @@ void retain_stream_pool() {
     if (pool_dev == dev) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        // a quarter of the device (45 GB on a B200): repeated large products reuse their
-        // scratch instead of re-mapping it after every synchronisation (measured: a 2^20-limb
-        // product 500-870 ms with an 8 GiB threshold, 101 ms when its 6-10 GB stay cached)
-        size_t free_b = 0, total_b = 0;
-        uint64_t thr = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess ? uint64_t(total_b) / 4 : uint64_t(8) << 30;
+        // up to 8 GiB stays reserved (memory held here is invisible to cudaMalloc users such
+        // as torch's allocator, so the cache is bounded; DOTG_POOL_KEEP_GB overrides). Scratch
+        // beyond it is re-mapped per call: a 2^21-limb product's 20 GB leaves, for example.
+        uint64_t thr = uint64_t(8) << 30;
         if (const char* e = std::getenv("DOTG_POOL_KEEP_GB")) thr = uint64_t(std::strtoull(e, nullptr, 10)) << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
