@@ -157,6 +157,141 @@ unsigned copy_grid(size_t rows, size_t nd) {
     return unsigned(need < size_t(148 * 16) ? need : size_t(148 * 16));
 }
 
+// ---------------------------------------------------------------------------
+// Wide split / combine for the top levels of very large products (few pairs of many
+// limbs): a warp per pair would walk a whole 2^23-limb half serially, so these levels are
+// composed from the batched long-number add/sub (addsub_long.cu: multi-CTA per number,
+// three passes) plus coalesced copy / select kernels. Same results as the warp kernels.
+// ---------------------------------------------------------------------------
+// dst[r * ds + doff + c] = src ? src[r * ss + soff + c] : 0, for c < n
+__global__ void __launch_bounds__(256) k_copy_2d(uint64_t* __restrict__ dst, size_t ds, size_t doff,
+                                                 const uint64_t* __restrict__ src, size_t ss, size_t soff, size_t n,
+                                                 size_t rows) {
+    const size_t total = rows * n, stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const size_t r = i / n, c = i - r * n;
+        dst[r * ds + doff + c] = src != nullptr ? __ldg(src + r * ss + soff + c) : 0ull;
+    }
+}
+
+// Rows of dst (n limbs) replaced by the rows of alt where flag[r] != 0.
+__global__ void __launch_bounds__(256) k_select_rows(uint64_t* __restrict__ dst, const uint64_t* __restrict__ alt,
+                                                     const uint32_t* __restrict__ flag, size_t n, size_t rows) {
+    const size_t total = rows * n, stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const size_t r = i / n;
+        if (__ldg(flag + r) != 0u) dst[i] = __ldg(alt + i);
+    }
+}
+
+// Mz[r] (3h limbs) = M (2h limbs) ++ top ++ 0...: M = T - PD if the two differences have
+// the same sign, else T + PD; top = cT - borrow or cT + carry (the true mid is >= 0 and
+// below 2^(64 (2h + 1)), so top is 0 or 1).
+__global__ void __launch_bounds__(256) k_make_mid(uint64_t* __restrict__ mz, const uint64_t* __restrict__ mplus,
+                                                  const uint64_t* __restrict__ mminus, const uint32_t* cT,
+                                                  const uint32_t* cP, const uint32_t* bM, const uint32_t* sa,
+                                                  const uint32_t* sb, size_t h, size_t rows) {
+    const size_t n2 = 2 * h, n3 = 3 * h, total = rows * n3, stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const size_t r = i / n3, c = i - r * n3;
+        const bool minus = __ldg(sa + r) == __ldg(sb + r);
+        uint64_t v = 0;
+        if (c < n2) v = __ldg((minus ? mminus : mplus) + r * n2 + c);
+        else if (c == n2) v = uint64_t(__ldg(cT + r)) + (minus ? uint64_t(0) - __ldg(bM + r) : uint64_t(__ldg(cP + r)));
+        mz[i] = v;
+    }
+}
+
+unsigned flat_grid(size_t total) {
+    const size_t need = (total + 255) / 256;
+    return unsigned(need < size_t(148 * 16) ? need : size_t(148 * 16));
+}
+
+// Wide when each warp would walk >= 4096 limbs and there are too few pairs to fill the
+// GPU with warps; the long-number kernels take at most 65535 numbers per launch.
+bool kara_wide(size_t h, size_t count) { return h >= 4096 && count <= 2048; }
+
+cudaError_t split_wide(const uint64_t* A, size_t m, size_t h, size_t count, uint64_t* lo, uint64_t* hi,
+                       uint64_t* df, uint32_t* sign, cudaStream_t st) {
+    uint64_t* alt = nullptr;
+    cudaError_t e = cudaMallocAsync(&alt, count * h * 8, st);
+    if (e != cudaSuccess) return e;
+    k_copy_2d<<<flat_grid(count * h), 256, 0, st>>>(lo, h, 0, A, m, 0, h, count);
+    k_copy_2d<<<flat_grid(count * (m - h)), 256, 0, st>>>(hi, h, 0, A, m, h, m - h, count);
+    if (m - h < h) k_copy_2d<<<flat_grid(count * (2 * h - m)), 256, 0, st>>>(hi, h, m - h, nullptr, 0, 0, 2 * h - m, count);
+    count_launch(m - h < h ? 3 : 2);
+    e = cudaGetLastError();
+    // df = hi - lo, borrow = (hi < lo) = the sign; where negative, df = lo - hi instead
+    if (e == cudaSuccess) e = launch_long_batch(true, df, hi, lo, sign, h, count, st);
+    if (e == cudaSuccess) e = launch_long_batch(true, alt, lo, hi, nullptr, h, count, st);
+    if (e == cudaSuccess) {
+        k_select_rows<<<flat_grid(count * h), 256, 0, st>>>(df, alt, sign, h, count);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(alt, st);
+    return e;
+}
+
+cudaError_t combine_wide(const uint64_t* P, size_t h, size_t count, const uint32_t* sa, const uint32_t* sb,
+                         uint64_t* out, size_t m, cudaStream_t st) {
+    const size_t n2 = 2 * h, n3 = 3 * h;
+    const uint64_t* p0 = P;
+    const uint64_t* p1 = P + count * n2;
+    const uint64_t* pd = P + 2 * count * n2;
+    char* base = nullptr;
+    const size_t w2 = count * n2 * 8, w3 = count * n3 * 8, fl = (count * 4 + 255) / 256 * 256;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * w2 + 2 * w3 + 3 * fl, st);
+    if (e != cudaSuccess) return e;
+    uint64_t* T = reinterpret_cast<uint64_t*>(base);
+    uint64_t* Mp = reinterpret_cast<uint64_t*>(base + w2);
+    uint64_t* Mm = reinterpret_cast<uint64_t*>(base + 2 * w2);
+    uint64_t* Mz = reinterpret_cast<uint64_t*>(base + 3 * w2);
+    uint64_t* Rh = reinterpret_cast<uint64_t*>(base + 3 * w2 + w3);
+    uint32_t* cT = reinterpret_cast<uint32_t*>(base + 3 * w2 + 2 * w3);
+    uint32_t* cP = reinterpret_cast<uint32_t*>(base + 3 * w2 + 2 * w3 + fl);
+    uint32_t* bM = reinterpret_cast<uint32_t*>(base + 3 * w2 + 2 * w3 + 2 * fl);
+    e = launch_long_batch(false, T, p0, p1, cT, n2, count, st);                 // T = P0 + P1
+    if (e == cudaSuccess) e = launch_long_batch(false, Mp, T, pd, cP, n2, count, st);  // T + PD
+    if (e == cudaSuccess) e = launch_long_batch(true, Mm, T, pd, bM, n2, count, st);   // T - PD
+    if (e == cudaSuccess) {
+        k_make_mid<<<flat_grid(count * n3), 256, 0, st>>>(Mz, Mp, Mm, cT, cP, bM, sa, sb, h, count);
+        // Rh = P0[h:2h) ++ P1: the parent product's limbs from h up before adding the mid
+        k_copy_2d<<<flat_grid(count * h), 256, 0, st>>>(Rh, n3, 0, p0, n2, h, h, count);
+        k_copy_2d<<<flat_grid(count * n2), 256, 0, st>>>(Rh, n3, h, p1, n2, 0, n2, count);
+        count_launch(3);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = launch_long_batch(false, Rh, Rh, Mz, nullptr, n3, count, st);  // += mid * X
+    if (e == cudaSuccess) {
+        const size_t no = 2 * m;  // out rows: P0[0:h) ++ Rh, truncated to 2m limbs
+        k_copy_2d<<<flat_grid(count * h), 256, 0, st>>>(out, no, 0, p0, n2, 0, h, count);
+        k_copy_2d<<<flat_grid(count * (no - h)), 256, 0, st>>>(out, no, h, Rh, n3, 0, no - h, count);
+        count_launch(2);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(base, st);
+    return e;
+}
+
+cudaError_t kara_split(const uint64_t* A, size_t m, size_t h, size_t count, uint64_t* lo, uint64_t* hi,
+                       uint64_t* df, uint32_t* sign, cudaStream_t st) {
+    if (kara_wide(h, count)) return split_wide(A, m, h, count, lo, hi, df, sign, st);
+    const unsigned grid = unsigned((count + kKaraWarps - 1) / kKaraWarps);
+    k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(A, m, h, count, lo, hi, df, sign);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t kara_combine(const uint64_t* P, size_t h, size_t count, const uint32_t* sa, const uint32_t* sb,
+                         uint64_t* out, size_t m, cudaStream_t st) {
+    if (kara_wide(h, count)) return combine_wide(P, h, count, sa, sb, out, m, st);
+    k_kara_combine_w<<<unsigned((count + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(P, h, count, sa,
+                                                                                                   sb, out, m);
+    count_launch();
+    return cudaGetLastError();
+}
+
 // The level sizes of a descent: parent m_i (the limbs actually read), half h_i.
 struct KaraPlan {
     std::vector<size_t> pm, h;
@@ -228,15 +363,17 @@ cudaError_t run_karatsuba_bf(uint64_t* out, const uint64_t* a, const uint64_t* b
             cleanup();
             return cudaErrorMemoryAllocation;
         }
-        const unsigned grid = unsigned((count + kKaraWarps - 1) / kKaraWarps);
-        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(A, L.m, h, count, nA, nA + count * h, nA + 2 * count * h,
-                                                         L.sa);
-        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(B, L.m, h, count, nB, nB + count * h, nB + 2 * count * h,
-                                                         L.sb);
-        count_launch(2);
+        cudaError_t es = kara_split(A, L.m, h, count, nA, nA + count * h, nA + 2 * count * h, L.sa, st);
+        if (es == cudaSuccess) es = kara_split(B, L.m, h, count, nB, nB + count * h, nB + 2 * count * h, L.sb, st);
         if (d > d0) {
             release(A);
             release(B);
+        }
+        if (es != cudaSuccess) {
+            release(nA);
+            release(nB);
+            cleanup();
+            return es;
         }
         lv.push_back(L);
         A = nA;
@@ -263,10 +400,7 @@ cudaError_t run_karatsuba_bf(uint64_t* out, const uint64_t* a, const uint64_t* b
             e = cudaErrorMemoryAllocation;
             break;
         }
-        k_kara_combine_w<<<unsigned((L.count + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(
-            P, L.h, L.count, L.sa, L.sb, dst, L.m);
-        count_launch();
-        e = cudaGetLastError();
+        e = kara_combine(P, L.h, L.count, L.sa, L.sb, dst, L.m, st);
         release(P);
         P = dst;
     }
@@ -292,22 +426,14 @@ cudaError_t run_karatsuba_at(uint64_t* out, const uint64_t* a, const uint64_t* b
     if (e == cudaSuccess) e = cudaMallocAsync(&sb, batch * 4 < 256 ? 256 : batch * 4, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&P, 3 * batch * 2 * h * 8, st);
     if (e == cudaSuccess) {
-        const unsigned grid = unsigned((batch + kKaraWarps - 1) / kKaraWarps);
-        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(a, m, h, batch, nA, nA + batch * h, nA + 2 * batch * h, sa);
-        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(b, m, h, batch, nB, nB + batch * h, nB + 2 * batch * h, sb);
-        count_launch(2);
-        e = cudaGetLastError();
+        e = kara_split(a, m, h, batch, nA, nA + batch * h, nA + 2 * batch * h, sa, st);
+        if (e == cudaSuccess) e = kara_split(b, m, h, batch, nB, nB + batch * h, nB + 2 * batch * h, sb, st);
         // the next level's plan entry describes a child of h limbs (pm[d0 + 1] == h)
         for (int k = 0; k < 3 && e == cudaSuccess; ++k)
             e = run_karatsuba_at(P + size_t(k) * batch * 2 * h, nA + size_t(k) * batch * h,
                                  nB + size_t(k) * batch * h, batch, plan, d0 + 1, budget, st);
     }
-    if (e == cudaSuccess) {
-        k_kara_combine_w<<<unsigned((batch + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(P, h, batch, sa,
-                                                                                                   sb, out, m);
-        count_launch();
-        e = cudaGetLastError();
-    }
+    if (e == cudaSuccess) e = kara_combine(P, h, batch, sa, sb, out, m, st);
     for (void* q : {static_cast<void*>(nA), static_cast<void*>(nB), static_cast<void*>(sa), static_cast<void*>(sb),
                     static_cast<void*>(P)})
         if (q != nullptr) cudaFreeAsync(q, st);
@@ -318,10 +444,12 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
                           cudaStream_t st) {
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(16) << 30;
-    // breadth-first whenever it fits 70% of free memory: every depth-first level serialises
-    // three children that breadth-first runs concurrently (a 16 GiB cap made 2^22 limbs
-    // 1.48 s and 2^24 limbs 16.3 s, against 1.0-2.5 s and 8.8 s)
-    size_t budget = free_b / 10 * 7;
+    // breadth-first while its scratch stays inside the pool's 8 GiB reserve (7 GiB, or 70%
+    // of free memory if less): larger scratch is re-mapped by the driver on every call, which
+    // cost more than going depth-first now that the top levels split and combine with the
+    // multi-CTA long-number passes (tools/mul_max_timing.py: 2^22 limbs 140 ms vs 0.7-0.8 s,
+    // 2^24 limbs 1.21 s vs 1.7-1.9 s with a 70%-of-free budget)
+    size_t budget = std::min(free_b / 10 * 7, size_t(7) << 30);
     if (const char* e = std::getenv("DOTG_KARA_BUDGET_MB")) budget = size_t(std::strtoull(e, nullptr, 10)) << 20;
     return run_karatsuba_at(out, a, b, batch, plan, 0, budget, st);
 }

@@ -57,6 +57,26 @@ def test_depth_first_schedule_exact(cuda, oracle, small_budget):
         assert np.array_equal(got, oracle.mul_batch(a, b)), m
 
 
+def test_wide_split_combine_exact(cuda, oracle):
+    """The top levels of large products (halves of >= 4096 limbs, few pairs) run the wide
+    split / combine (batched long add/sub + copies): exact against the oracle."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(77)
+    for m, batch in ((8192, 2), (10000, 1), (16384, 1), (9001, 3)):
+        a, b = uniform(rng, (batch, m)), uniform(rng, (batch, m))
+        a[0, : m // 2] = MAX  # equal halves / long propagate runs in the splits
+        b[-1] = MAX
+        got = host(dg.mul_batch(dev(torch, a), dev(torch, b)))
+        assert np.array_equal(got, oracle.mul_batch(a, b)), m
+    for m in (9000, 8193):
+        a, b = uniform(rng, (2, m)), uniform(rng, (2, m))
+        a[1, m // 2:] = a[1, : m - m // 2]  # hi == lo: zero difference, sign 0
+        got = host(dg.karatsuba_batch(dev(torch, a), dev(torch, b), theta=4))
+        assert np.array_equal(got, oracle.mul_batch(a, b)), m
+
+
 @pytest.mark.parametrize("m", [1 << 24, (1 << 22) + 3])
 def test_maximum_size_products(cuda, oracle, m):
     import paper_2604_21566_b200 as dg
