@@ -69,3 +69,24 @@ def test_python_validation_raises_invalid_argument():
     with pytest.raises(dg.InvalidArgument):
         dg.dot_add_words(np.ones(2, np.uint64), np.ones(2, np.uint64), width=3)
     assert issubclass(dg.InvalidArgument, ValueError)
+
+
+def test_headers_compile_standalone(tmp_path):
+    """include/dotg.h is plain C (C99) and include/dot_b200.hpp builds as C++20 against it:
+    what a reference-side caller compiles."""
+    import shutil
+    import subprocess
+
+    inc = os.path.join(ROOT, "include")
+    if shutil.which("gcc") is None or shutil.which("g++") is None:
+        pytest.skip("no host compiler")
+    c = tmp_path / "use.c"
+    c.write_text('#include "dotg.h"\nint main(void) { return dotg_validate_width(8); }\n')
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-fsyntax-only", f"-I{inc}", str(c)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    cc = tmp_path / "use.cpp"
+    cc.write_text('#include "dot_b200.hpp"\nint main() { dot_b200::Limbs a{1}; (void)a; return 0; }\n')
+    r = subprocess.run(["g++", "-std=c++20", "-Wall", "-Wextra", "-Werror", "-fsyntax-only", f"-I{inc}", str(cc)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
