@@ -68,6 +68,13 @@ int dotg_add_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t
                    size_t m, size_t batch, int layout, dotg_stream_t stream);
 int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
                    size_t m, size_t batch, int layout, dotg_stream_t stream);
+/* Row-pitched form (the stride_limbs of SURVEY.md §8(b)): pair p's limb i at
+ * a[p * lda + i], b[p * ldb + i], out[p * ldo + i] (pitches in limbs, >= m when
+ * batch > 1), so callers can pass views of wider arrays without a copy. Pitches equal to m
+ * take the dense kernels; other pitches run a thread per pair. out may alias a or b
+ * exactly (same pointer and pitch). */
+int dotg_addsub_batch_strided(int sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b,
+                              size_t ldb, uint32_t* flags, size_t m, size_t batch, dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Grouped batched add/sub: up to any number of INDEPENDENT problems (sizes may differ)

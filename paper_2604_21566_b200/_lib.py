@@ -46,6 +46,8 @@ SIGNATURES = {
     "dotg_words_host_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_int, _P, _P, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_compare_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_addsub_batch_strided": (c_int, [c_int, _P, c_size_t, _P, c_size_t, _P, c_size_t, _P, c_size_t, c_size_t,
+                                          _P]),
     "dotg_chunk_batch": (c_int, [c_int, _P, _P, _P, _P, _P, _P, c_uint, c_size_t, _P]),
     "dotg_chunk_host": (c_int, [c_int, _P, _P, _P, _P, _P, c_uint32, c_uint]),
     "dotg_kernel_launches": (c_uint64, []),

@@ -339,11 +339,34 @@ def _batch_dims(a, layout):
     return (a.shape[0], a.shape[1]) if layout == ROW_MAJOR else (a.shape[1], a.shape[0])
 
 
+def _row_pitched(t) -> bool:
+    """A 2-D CUDA int64 view whose rows are contiguous (stride(1) == 1) at a pitch >= m."""
+    torch = _torch()
+    return (isinstance(t, torch.Tensor) and t.is_cuda and t.element_size() == 8 and t.dim() == 2
+            and (t.shape[1] <= 1 or t.stride(1) == 1) and (t.shape[0] <= 1 or t.stride(0) >= t.shape[1]))
+
+
 def addsub_batch(sub: bool, a, b, out=None, flags=None, *, layout=ROW_MAJOR, stream=None):
     """out = a +/- b per pair, flags = carry/borrow per pair (device tensors).
-    ROW_MAJOR a: [batch, m]; INTERLEAVED a: [m, batch]."""
+    ROW_MAJOR a: [batch, m]; INTERLEAVED a: [m, batch]. Row-major operands may be views
+    with a row pitch (e.g. x[:, :m] of a wider tensor): dotg_addsub_batch_strided."""
     torch = _torch()
     lay = _layout(layout)
+    views = [t for t in (a, b, out) if t is not None]
+    if lay == ROW_MAJOR and not all(t.is_contiguous() for t in views if isinstance(t, torch.Tensor)) and all(
+            _row_pitched(t) for t in views):
+        if a.shape != b.shape or (out is not None and out.shape != a.shape):
+            raise InvalidArgument("dot add/sub: operand shapes differ")
+        batch, m = a.shape
+        if out is None:
+            out = torch.empty_like(a, memory_format=torch.contiguous_format)
+        if flags is None:
+            flags = torch.empty(batch, dtype=torch.int32, device=a.device)
+        _check_dev(flags, "flags", 4)
+        pitch = [t.stride(0) if t.shape[0] > 1 else m for t in (out, a, b)]
+        check(lib().dotg_addsub_batch_strided(int(sub), _dptr(out), pitch[0], _dptr(a), pitch[1], _dptr(b), pitch[2],
+                                              _dptr(flags), m, batch, _stream_handle(stream)))
+        return out, flags
     _check_dev(a, "a")
     _check_dev(b, "b")
     if a.shape != b.shape:

@@ -215,6 +215,26 @@ __global__ void __launch_bounds__(256) k_addsub_strided(uint64_t* out, const uin
     if (flags != nullptr) flags[pidx] = c;
 }
 
+// Row-pitched thread per pair: operand rows at their own pitches (views of wider arrays).
+template <bool SUB>
+__global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,
+                                                        const uint64_t* b, size_t ldb, uint32_t* flags, size_t m,
+                                                        size_t batch) {
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    const uint64_t* pa = a + pidx * lda;
+    const uint64_t* pb = b + pidx * ldb;
+    uint64_t* po = out + pidx * ldo;
+    uint32_t c = 0;
+    for (size_t i = 0; i < m; ++i) {
+        uint32_t g, p;
+        const uint64_t sv = lane_op<SUB>(pa[i], pb[i], g, p);
+        po[i] = apply_carry<SUB>(sv, c);
+        c = g | (p & c);
+    }
+    if (flags != nullptr) flags[pidx] = c;
+}
+
 // Interleaved layout [m][batch], limb-segmented: a CTA owns 32 * PPL consecutive pairs;
 // warp w of the CTA owns limbs [w*L, w*L + L) of those pairs, lane l the pairs
 // PPL*l .. PPL*l + PPL - 1 (for PPL = 2 one 128-bit load per limb row covers both).
@@ -573,6 +593,18 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
     cudaError_t e = launch_group(false, small, stream);
     if (e != cudaSuccess) return e;
     return launch_group(true, big, stream);
+}
+
+cudaError_t launch_addsub_pitched(bool sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,
+                                  const uint64_t* b, size_t ldb, uint32_t* flags, size_t m, size_t batch,
+                                  cudaStream_t stream) {
+    if (batch == 0) return cudaSuccess;
+    if (ldo == m && lda == m && ldb == m) return launch_addsub_batch(sub, out, a, b, flags, m, batch, 0, stream);
+    const unsigned blocks = unsigned((batch + 255) / 256);
+    if (sub) k_addsub_pitched<true><<<blocks, 256, 0, stream>>>(out, ldo, a, lda, b, ldb, flags, m, batch);
+    else k_addsub_pitched<false><<<blocks, 256, 0, stream>>>(out, ldo, a, lda, b, ldb, flags, m, batch);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,

@@ -529,6 +529,37 @@ int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t
     return addsub_batch(true, out, a, b, flags, m, batch, layout, stream);
 }
 
+int dotg_addsub_batch_strided(int sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b,
+                              size_t ldb, uint32_t* flags, size_t m, size_t batch, dotg_stream_t stream) {
+    if (batch == 0) return DOTG_OK;
+    if (m > 0 && (out == nullptr || a == nullptr || b == nullptr))
+        return fail(DOTG_EINVAL, "dot add/sub: null operand");
+    if (batch > 1 && (ldo < m || lda < m || ldb < m))
+        return fail(DOTG_EINVAL, "dot add/sub: row pitch below the limb count");
+    const size_t mx = std::max(ldo, std::max(lda, ldb));
+    if (m > 0 && (mx > SIZE_MAX / 8 / batch || m > SIZE_MAX / 8))
+        return fail(DOTG_EINVAL, "dot add/sub: size overflow");
+    // spanned bytes of each operand: (batch - 1) rows of pitch plus one row of m limbs
+    auto span = [&](size_t ld) { return ((batch - 1) * ld + m) * sizeof(uint64_t); };
+    if (m > 0) {
+        const bool ea = out == a && ldo == lda, eb = out == b && ldo == ldb;
+        if ((!ea && ranges_overlap(out, span(ldo), a, span(lda))) || (!eb && ranges_overlap(out, span(ldo), b, span(ldb))))
+            return fail(DOTG_EINVAL, "dot add/sub: out may alias a or b only exactly (same pointer and pitch)");
+        if (flags != nullptr && ranges_overlap(flags, batch * 4, out, span(ldo)))
+            return fail(DOTG_EINVAL, "dot add/sub: flags overlap out");
+    }
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    if (m == 0) {
+        if (flags == nullptr) return DOTG_OK;
+        cudaError_t e = cudaMemsetAsync(flags, 0, batch * sizeof(uint32_t), static_cast<cudaStream_t>(stream));
+        return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "memset");
+    }
+    cudaError_t e = dotg::launch_addsub_pitched(sub != 0, out, ldo, a, lda, b, ldb, flags, m, batch,
+                                                static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg add/sub strided launch");
+}
+
 int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_t stream) {
     if (n < 0 || (n > 0 && problems == nullptr)) return fail(DOTG_EINVAL, "grouped: bad problem list");
     if (n == 0) return DOTG_OK;

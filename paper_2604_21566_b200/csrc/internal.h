@@ -49,6 +49,9 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
                                uint32_t* carry_out, cudaStream_t stream);
 
 // A batch of long numbers (row-major, m >= 1 tile): the tiled passes with grid.y = number.
+cudaError_t launch_addsub_pitched(bool sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,
+                                  const uint64_t* b, size_t ldb, uint32_t* flags, size_t m, size_t batch,
+                                  cudaStream_t stream);
 cudaError_t launch_long_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
                               size_t m, size_t batch, cudaStream_t stream);
 

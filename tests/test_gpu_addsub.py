@@ -214,3 +214,33 @@ def test_aliasing_every_route(cuda, oracle, m, batch):
         ta, tb = dev(torch, a), dev(torch, b)
         _, fl = dg.addsub_batch(sub, ta, tb, out=tb)
         assert np.array_equal(host(tb), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf), (m, sub)
+
+
+def test_row_pitched_views(cuda, oracle):
+    """dotg_addsub_batch_strided (row pitches, SURVEY.md §8(b) stride_limbs): views of wider
+    tensors, mixed pitches, exact in-place aliasing, pitch == m taking the dense route."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(404)
+    for m, batch, wa, wb in ((5, 300, 8, 7), (64, 1000, 80, 64), (1, 50, 3, 2), (17, 1, 17, 40)):
+        A = spiky(rng, (batch, wa))
+        B = spiky(rng, (batch, wb))
+        a, b = A[:, :m], B[:, :m]
+        ta = torch.from_numpy(A.view(np.int64)).cuda()[:, :m]
+        tb = torch.from_numpy(B.view(np.int64)).cuda()[:, :m]
+        for sub in (False, True):
+            want, wf = oracle.addsub_batch(sub, np.ascontiguousarray(a), np.ascontiguousarray(b))
+            out, fl = dg.addsub_batch(sub, ta, tb)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (m, sub)
+            assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
+            # in place into a pitched view
+            tc = torch.from_numpy(A.view(np.int64).copy()).cuda()
+            tcv = tc[:, :m]
+            dg.addsub_batch(sub, tcv, tb, out=tcv)
+            got = tc.cpu().numpy().view(np.uint64)
+            assert np.array_equal(got[:, :m], want) and np.array_equal(got[:, m:], A[:, m:])
+    # partial overlap is rejected
+    T = torch.zeros((10, 16), dtype=torch.int64, device="cuda")
+    with pytest.raises(dg.InvalidArgument):
+        dg.addsub_batch(False, T[:, 0:8], T[:, 8:16], out=T[:, 4:12])
