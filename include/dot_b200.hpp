@@ -160,6 +160,69 @@ inline WordsResult dot_sub_words(const Limbs& a, const Limbs& b, Width w = Width
     return detail::run_limbs(true, a, b, w, stats);
 }
 
+// ---- The column pipeline as separate stages (mul.hpp:32-67, mul.cpp:12-90), each run on
+// the device (dotg_*_host stages of dotg.h); dot_mul_words below does not go through them
+// (its kernels fuse the four stages in registers).
+using u128 = unsigned __int128;  // limbs.hpp:20-24
+
+constexpr std::size_t num_pairs(std::size_t c, std::size_t m) {  // mul.hpp:36-38
+    const std::size_t x = c + 1, y = 2 * m - 1 - c;
+    return x < m ? (x < y ? x : y) : (m < y ? m : y);
+}
+
+struct ColumnBuffers {  // mul.hpp:42-49
+    std::size_t m = 0;
+    std::vector<limb_t> m_a;
+    std::vector<limb_t> m_b;
+    std::vector<limb_t> p_lo;
+    std::vector<limb_t> p_hi;
+    std::vector<u128> col_lo;
+};
+
+inline ColumnBuffers gather_columns(const Limbs& a, const Limbs& b) {  // mul.cpp:12-36
+    if (a.size() != b.size()) throw std::invalid_argument("dot mul: operand lengths differ (caller pads)");
+    ColumnBuffers buf;
+    buf.m = a.size();
+    buf.m_a.resize(buf.m * buf.m);
+    buf.m_b.resize(buf.m * buf.m);
+    detail::check(dotg_gather_columns_host(buf.m_a.data(), buf.m_b.data(), a.data(), b.data(), buf.m));
+    buf.p_lo.assign(buf.m * buf.m, 0);
+    buf.p_hi.assign(buf.m * buf.m, 0);
+    buf.col_lo.assign(2 * buf.m, 0);
+    return buf;
+}
+
+inline void compute_partials(ColumnBuffers& buf, RadixConfig cfg, Width w = Width::w8) {  // mul.cpp:38-52
+    detail::validate(w);
+    buf.p_lo.resize(buf.m_a.size());
+    buf.p_hi.resize(buf.m_a.size());
+    if (buf.m_b.size() != buf.m_a.size()) throw std::invalid_argument("column buffers: m_a / m_b sizes differ");
+    detail::check(dotg_compute_partials_host(buf.p_lo.data(), buf.p_hi.data(), buf.m_a.data(), buf.m_b.data(),
+                                             buf.m_a.size(), static_cast<int>(cfg.limb_bits)));
+}
+
+inline std::span<const u128> align_and_reduce(ColumnBuffers& buf) {  // mul.cpp:54-68
+    std::vector<limb_t> cols(4 * buf.m);
+    detail::check(dotg_align_and_reduce_host(cols.data(), buf.p_lo.data(), buf.p_hi.data(), buf.m));
+    buf.col_lo.resize(2 * buf.m);
+    for (std::size_t c = 0; c < 2 * buf.m; ++c) buf.col_lo[c] = u128(cols[2 * c]) | (u128(cols[2 * c + 1]) << 64);
+    return {buf.col_lo.data(), buf.col_lo.size()};
+}
+
+inline Limbs carry_pass(std::span<const u128> columns, RadixConfig cfg) {  // mul.cpp:70-90
+    std::vector<limb_t> cols(2 * columns.size());
+    for (std::size_t c = 0; c < columns.size(); ++c) {
+        cols[2 * c] = limb_t(columns[c]);
+        cols[2 * c + 1] = limb_t(columns[c] >> 64);
+    }
+    Limbs out(columns.size() + 2);
+    std::uint32_t n = 0;
+    detail::check(dotg_carry_pass_host(out.data(), &n, out.size(), cols.data(), columns.size(),
+                                       static_cast<int>(cfg.limb_bits)));
+    out.resize(n);
+    return out;
+}
+
 // Exact product, exactly 2m limbs; equal lengths 1 <= m <= 2^24 (mul.hpp:75-76).
 inline Limbs dot_mul_words(const Limbs& a, const Limbs& b, RadixConfig cfg = kSaturated,
                            Width w = Width::w8) {

@@ -229,6 +229,34 @@ int dotg_chunk_batch(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* pha
 int dotg_chunk_host(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phase4_fired, const uint64_t* a,
                     const uint64_t* b, uint32_t carry_in, unsigned w);
 
+/* ---------------------------------------------------------------------------
+ * The column pipeline as separate stages. Replaces: gather_columns, compute_partials,
+ * align_and_reduce, carry_pass (mul.hpp:32-67, mul.cpp:12-90) - the stages dot_mul_words
+ * chains (mul.cpp:96-103; dotg_mul_batch fuses them). Same buffers, bit for bit:
+ *   gather:   m_a / m_b [batch][m*m] in column order (i + j ascending, i ascending);
+ *             1 <= m <= 2^24 (m*m buffers: device memory bounds it far lower).
+ *   partials: p_lo = (m_a*m_b) mod 2^k, p_hi = floor(m_a*m_b / 2^k) truncated to 64 bits,
+ *             limb_bits k in {64, 52} (n entries, any grouping).
+ *   reduce:   columns [batch][2m] u128 sums as (low 64, high 64) pairs of uint64.
+ *   carry:    out [batch][out_cap] limbs, out_limbs[p] = limbs written (ncols plus a
+ *             residual of at most 2): out_cap >= ncols + 2.
+ * Host forms (one operand set, host pointers) back the C++ drop-in.
+ * ------------------------------------------------------------------------- */
+int dotg_gather_columns(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                        dotg_stream_t stream);
+int dotg_compute_partials(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                          int limb_bits, dotg_stream_t stream);
+int dotg_align_and_reduce(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m, size_t batch,
+                          dotg_stream_t stream);
+int dotg_carry_pass(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
+                    size_t batch, int limb_bits, dotg_stream_t stream);
+int dotg_gather_columns_host(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m);
+int dotg_compute_partials_host(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                               int limb_bits);
+int dotg_align_and_reduce_host(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m);
+int dotg_carry_pass_host(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
+                         int limb_bits);
+
 /* Workload setup (not the hot path): out[i] = splitmix64 output for counter
  * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,

@@ -222,6 +222,60 @@ def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
     return out
 
 
+# ---- the column pipeline as separate device stages (mul.hpp:32-67, mul.cpp:12-90)
+def num_pairs(c: int, m: int) -> int:
+    """mul.hpp:36-38: pair count of column c (c = 2m - 1 is the carry slot, 0 pairs)."""
+    return min(c + 1, m, 2 * m - 1 - c)
+
+
+def gather_columns(a, b):
+    """(m_a, m_b): the m*m pairs in column order (mul.cpp:12-36), gathered on the device."""
+    a, b = _host_u64(a, "a"), _host_u64(b, "b")
+    if a.size != b.size:
+        raise InvalidArgument("dot mul: operand lengths differ (caller pads)")
+    m = a.size
+    ma, mb = np.zeros(m * m, np.uint64), np.zeros(m * m, np.uint64)
+    check(lib().dotg_gather_columns_host(_hp(ma), _hp(mb), _hp(a), _hp(b), m))
+    return ma, mb
+
+
+def compute_partials(m_a, m_b, limb_bits: int = 64):
+    """(p_lo, p_hi) = products split at bit k (mul.cpp:38-52), on the device."""
+    m_a, m_b = _host_u64(m_a, "m_a"), _host_u64(m_b, "m_b")
+    if m_a.size != m_b.size:
+        raise InvalidArgument("column buffers: m_a / m_b sizes differ")
+    lo, hi = np.zeros(m_a.size, np.uint64), np.zeros(m_a.size, np.uint64)
+    check(lib().dotg_compute_partials_host(_hp(lo), _hp(hi), _hp(m_a), _hp(m_b), m_a.size, int(limb_bits)))
+    return lo, hi
+
+
+def align_and_reduce(p_lo, p_hi, m: int) -> list:
+    """The 2m u128 column sums (mul.cpp:54-68) as Python ints, reduced on the device."""
+    p_lo, p_hi = _host_u64(p_lo, "p_lo"), _host_u64(p_hi, "p_hi")
+    if p_lo.size != m * m or p_hi.size != m * m:
+        raise InvalidArgument("column buffers: partial buffers need m*m entries")
+    cols = np.zeros(4 * m, np.uint64)
+    check(lib().dotg_align_and_reduce_host(_hp(cols), _hp(p_lo), _hp(p_hi), m))
+    return [int(cols[2 * c]) | (int(cols[2 * c + 1]) << 64) for c in range(2 * m)]
+
+
+def carry_pass(columns, limb_bits: int = 64) -> np.ndarray:
+    """Sequential renormalisation of u128 columns (mul.cpp:70-90) on the device; residual
+    carry limbs are appended."""
+    cols = list(columns)
+    if any(not 0 <= int(c) < 1 << 128 for c in cols):
+        raise InvalidArgument("columns are unsigned 128-bit values")
+    raw = np.zeros(max(1, 2 * len(cols)), np.uint64)
+    for i, c in enumerate(cols):
+        raw[2 * i] = int(c) & (2**64 - 1)
+        raw[2 * i + 1] = int(c) >> 64
+    out = np.zeros(len(cols) + 2, np.uint64)
+    n = ctypes.c_uint32(0)
+    check(lib().dotg_carry_pass_host(_hp(out), ctypes.byref(n), out.size, _hp(raw) if cols else None, len(cols),
+                                     int(limb_bits)))
+    return out[: n.value].copy()
+
+
 def dot_mul_5x5(a, b) -> np.ndarray:
     """Fixed 5-limb product over unsaturated 52-bit limbs, exactly 10 limbs
     (mul.hpp:78-80, mul.cpp:127-150)."""

@@ -814,6 +814,164 @@ int dotg_chunk_host(int sub, uint64_t* sums, uint32_t* carry_out, uint32_t* phas
     return DOTG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+int check_radix_bits(int k) {  // check_radix (limbs.cpp:21-24)
+    return (k == 64 || k == 52) ? DOTG_OK : fail(DOTG_EINVAL, "RadixConfig: limb_bits must be 64 or 52");
+}
+int check_gather(size_t m) {  // gather_columns (mul.cpp:13-18)
+    if (m == 0) return fail(DOTG_EINVAL, "dot mul: operands need at least one limb");
+    if (m > (size_t(1) << 24)) return fail(DOTG_EINVAL, "dot mul: limb count exceeds the column accumulator bound");
+    return DOTG_OK;
+}
+
+// Host form of one device stage: inputs copied in, outputs copied back, one sync.
+struct HostBuf {
+    void* host;
+    size_t bytes;
+    bool in, out;
+};
+template <typename F>
+int run_staged(std::vector<HostBuf> bufs, const char* what, F&& fn) {
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    cudaStream_t st = g_host.s[0];
+    size_t total = 0;
+    std::vector<size_t> off;
+    for (const HostBuf& b : bufs) {
+        off.push_back(total);
+        total += align_up(b.bytes, 256);
+    }
+    char* base = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), total ? total : 256, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    std::vector<void*> dev;
+    for (size_t i = 0; i < bufs.size(); ++i) {
+        dev.push_back(base + off[i]);
+        if (e == cudaSuccess && bufs[i].in && bufs[i].bytes)
+            e = cudaMemcpyAsync(dev[i], bufs[i].host, bufs[i].bytes, cudaMemcpyHostToDevice, st);
+    }
+    if (e == cudaSuccess) e = fn(dev, st);
+    for (size_t i = 0; i < bufs.size(); ++i)
+        if (e == cudaSuccess && bufs[i].out && bufs[i].bytes)
+            e = cudaMemcpyAsync(bufs[i].host, dev[i], bufs[i].bytes, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaFreeAsync(base, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    if (e == cudaErrorMemoryAllocation) return fail(DOTG_ENOMEM, std::string(what) + ": out of device memory");
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    return DOTG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int dotg_gather_columns(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                        dotg_stream_t stream) {
+    int rc = check_gather(m);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    if (!m_a || !m_b || !a || !b) return fail(DOTG_EINVAL, "gather: null operand");
+    if (batch > 65535) return fail(DOTG_EINVAL, "gather: at most 65535 operand pairs per call");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_gather_columns(m_a, m_b, a, b, m, batch, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "gather");
+}
+
+int dotg_compute_partials(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                          int limb_bits, dotg_stream_t stream) {
+    int rc = check_radix_bits(limb_bits);
+    if (rc != DOTG_OK || n == 0) return rc;
+    if (!p_lo || !p_hi || !m_a || !m_b) return fail(DOTG_EINVAL, "partials: null operand");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_partials(p_lo, p_hi, m_a, m_b, n, unsigned(limb_bits), static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "partials");
+}
+
+int dotg_align_and_reduce(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m, size_t batch,
+                          dotg_stream_t stream) {
+    int rc = check_gather(m);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    if (!columns || !p_lo || !p_hi) return fail(DOTG_EINVAL, "reduce: null operand");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_align_reduce(columns, p_lo, p_hi, m, batch, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "reduce");
+}
+
+int dotg_carry_pass(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
+                    size_t batch, int limb_bits, dotg_stream_t stream) {
+    int rc = check_radix_bits(limb_bits);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    if (out_cap < ncols + 2) return fail(DOTG_EINVAL, "carry pass: out_cap must be at least ncols + 2");
+    if (!out || !out_limbs || (ncols > 0 && !columns)) return fail(DOTG_EINVAL, "carry pass: null operand");
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_carry_pass(out, out_limbs, out_cap, columns, ncols, batch, unsigned(limb_bits),
+                                            static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "carry pass");
+}
+
+int dotg_gather_columns_host(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m) {
+    int rc = check_gather(m);
+    if (rc != DOTG_OK) return rc;
+    if (!m_a || !m_b || !a || !b) return fail(DOTG_EINVAL, "gather: null operand");
+    if (m > (size_t(1) << 14)) return fail(DOTG_ENOMEM, "gather: m*m column buffers do not fit this call");
+    const size_t ib = m * 8, ob = m * m * 8;
+    return run_staged({{const_cast<uint64_t*>(a), ib, true, false}, {const_cast<uint64_t*>(b), ib, true, false},
+                       {m_a, ob, false, true}, {m_b, ob, false, true}},
+                      "gather", [&](std::vector<void*>& d, cudaStream_t st) {
+                          return dotg::launch_gather_columns(static_cast<uint64_t*>(d[2]), static_cast<uint64_t*>(d[3]),
+                                                             static_cast<uint64_t*>(d[0]),
+                                                             static_cast<uint64_t*>(d[1]), m, 1, st);
+                      });
+}
+
+int dotg_compute_partials_host(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                               int limb_bits) {
+    int rc = check_radix_bits(limb_bits);
+    if (rc != DOTG_OK || n == 0) return rc;
+    if (!p_lo || !p_hi || !m_a || !m_b) return fail(DOTG_EINVAL, "partials: null operand");
+    const size_t nb = n * 8;
+    return run_staged({{const_cast<uint64_t*>(m_a), nb, true, false}, {const_cast<uint64_t*>(m_b), nb, true, false},
+                       {p_lo, nb, false, true}, {p_hi, nb, false, true}},
+                      "partials", [&](std::vector<void*>& d, cudaStream_t st) {
+                          return dotg::launch_partials(static_cast<uint64_t*>(d[2]), static_cast<uint64_t*>(d[3]),
+                                                       static_cast<uint64_t*>(d[0]), static_cast<uint64_t*>(d[1]), n,
+                                                       unsigned(limb_bits), st);
+                      });
+}
+
+int dotg_align_and_reduce_host(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m) {
+    int rc = check_gather(m);
+    if (rc != DOTG_OK) return rc;
+    if (!columns || !p_lo || !p_hi) return fail(DOTG_EINVAL, "reduce: null operand");
+    if (m > (size_t(1) << 14)) return fail(DOTG_ENOMEM, "reduce: m*m partial buffers do not fit this call");
+    const size_t pb = m * m * 8, cb = 2 * m * 16;
+    return run_staged({{const_cast<uint64_t*>(p_lo), pb, true, false}, {const_cast<uint64_t*>(p_hi), pb, true, false},
+                       {columns, cb, false, true}},
+                      "reduce", [&](std::vector<void*>& d, cudaStream_t st) {
+                          return dotg::launch_align_reduce(static_cast<uint64_t*>(d[2]), static_cast<uint64_t*>(d[0]),
+                                                           static_cast<uint64_t*>(d[1]), m, 1, st);
+                      });
+}
+
+int dotg_carry_pass_host(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
+                         int limb_bits) {
+    int rc = check_radix_bits(limb_bits);
+    if (rc != DOTG_OK) return rc;
+    if (out_cap < ncols + 2) return fail(DOTG_EINVAL, "carry pass: out_cap must be at least ncols + 2");
+    if (!out || !out_limbs || (ncols > 0 && !columns)) return fail(DOTG_EINVAL, "carry pass: null operand");
+    return run_staged({{const_cast<uint64_t*>(columns), ncols * 16, true, false}, {out, out_cap * 8, false, true},
+                       {out_limbs, 4, false, true}},
+                      "carry pass", [&](std::vector<void*>& d, cudaStream_t st) {
+                          return dotg::launch_carry_pass(static_cast<uint64_t*>(d[1]), static_cast<uint32_t*>(d[2]),
+                                                         out_cap, static_cast<uint64_t*>(d[0]), ncols, 1,
+                                                         unsigned(limb_bits), st);
+                      });
+}
+
 int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, int width,
                           uint32_t* carry, uint64_t* chunks, uint64_t* fires) {
     int rc = dotg_validate_width(width);

@@ -99,6 +99,16 @@ cudaError_t launch_chunk_batch(bool sub, uint64_t* sums, uint32_t* carry_out, ui
                                const uint64_t* b, const uint32_t* carry_in, unsigned w, size_t batch,
                                cudaStream_t st);
 
+// The reference's column pipeline as separate stages (columns.cu).
+cudaError_t launch_gather_columns(uint64_t* ma, uint64_t* mb, const uint64_t* a, const uint64_t* b, size_t m,
+                                  size_t batch, cudaStream_t st);
+cudaError_t launch_partials(uint64_t* plo, uint64_t* phi, const uint64_t* ma, const uint64_t* mb, size_t n,
+                            unsigned k, cudaStream_t st);
+cudaError_t launch_align_reduce(uint64_t* cols, const uint64_t* plo, const uint64_t* phi, size_t m, size_t batch,
+                                cudaStream_t st);
+cudaError_t launch_carry_pass(uint64_t* out, uint32_t* nout, size_t cap, const uint64_t* cols, size_t ncols,
+                              size_t batch, unsigned k, cudaStream_t st);
+
 // Workload setup: splitmix64 counter fill (util.cu).
 cudaError_t launch_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, cudaStream_t st);
 

@@ -137,6 +137,32 @@ int main() {
             }
         }
     });
+    run("column pipeline stages through the drop-in", [] {  // test_mul.cpp:54-252
+        std::mt19937_64 rng(11);
+        const Limbs a = uniform_limbs(rng, 5), b = uniform_limbs(rng, 5);
+        ColumnBuffers buf = gather_columns(a, b);
+        CHECK(buf.m == 5 && buf.m_a.size() == 25 && buf.col_lo.size() == 10);
+        for (std::size_t i = 0; i < 5; ++i) CHECK(buf.m_a[10 + i] == a[i] && buf.m_b[10 + i] == b[4 - i]);
+        CHECK_THROWS_AS(gather_columns(Limbs{1, 2}, Limbs{1}), std::invalid_argument);
+        CHECK_THROWS_AS(gather_columns(Limbs{}, Limbs{}), std::invalid_argument);
+        compute_partials(buf, kSaturated);
+        for (std::size_t t = 0; t < 25; ++t) {
+            const u128 p = u128(buf.m_a[t]) * buf.m_b[t];
+            CHECK(buf.p_lo[t] == limb_t(p) && buf.p_hi[t] == limb_t(p >> 64));
+        }
+        const auto cols = align_and_reduce(buf);
+        CHECK(carry_pass(cols, kSaturated) == oracle_mul_padded(a, b));
+        Limbs x(4, 0), y(4, 0);  // a lone pair: column 6 holds 2^62
+        x[2] = limb_t(1) << 63;
+        y[3] = limb_t(1) << 63;
+        ColumnBuffers lone = gather_columns(x, y);
+        compute_partials(lone, kSaturated);
+        const auto lc = align_and_reduce(lone);
+        for (std::size_t c = 0; c < lc.size(); ++c) CHECK(lc[c] == (c == 6 ? u128(limb_t(1) << 62) : u128(0)));
+        const std::vector<u128> full{~u128(0)};
+        CHECK(carry_pass(full, kUnsaturated).size() == 3);  // residual appended
+        CHECK_THROWS_AS(carry_pass(full, RadixConfig{48}), std::invalid_argument);
+    });
     run("2^512 - 1 plus 1 rolls over into the flag", [] {  // test_addsub.cpp:124-130
         const WordsResult r = dot_add_words(Limbs(8, kMax), Limbs{1});
         CHECK(r.limbs == Limbs(8, 0));
