@@ -160,6 +160,17 @@ inline WordsResult dot_sub_words(const Limbs& a, const Limbs& b, Width w = Width
     return detail::run_limbs(true, a, b, w, stats);
 }
 
+// Value ordering ignoring high zero limbs: -1 / 0 / +1 (limbs.hpp:84, limbs.cpp:46-53).
+inline int compare(const Limbs& a, const Limbs& b) {
+    const std::size_t m = a.size() > b.size() ? a.size() : b.size();
+    Limbs pa = a, pb = b;
+    pa.resize(m, 0);
+    pb.resize(m, 0);
+    std::int32_t r = 0;
+    detail::check(dotg_compare_host(&r, pa.data(), pb.data(), m, 1));
+    return r;
+}
+
 // ---- The column pipeline as separate stages (mul.hpp:32-67, mul.cpp:12-90), each run on
 // the device (dotg_*_host stages of dotg.h); dot_mul_words below does not go through them
 // (its kernels fuse the four stages in registers).

@@ -214,6 +214,9 @@ int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint6
  * ------------------------------------------------------------------------- */
 int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
                        dotg_stream_t stream);
+/* Host-memory form (row-major), backing the C++ drop-in's compare(a, b) (which zero-pads
+ * unequal lengths first: high zero limbs do not change the order, limbs.cpp:46-53). */
+int dotg_compare_host(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch);
 
 /* ---------------------------------------------------------------------------
  * Chunk-level operations. Replaces: add_w_limbs / sub_w_limbs (addsub.hpp:78-89,

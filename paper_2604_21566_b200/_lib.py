@@ -46,6 +46,7 @@ SIGNATURES = {
     "dotg_words_host_stats": (c_int, [c_int, _P, _P, _P, c_size_t, c_int, _P, _P, _P]),
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_compare_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
+    "dotg_compare_host": (c_int, [_P, _P, _P, c_size_t, c_size_t]),
     "dotg_gather_columns": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, _P]),
     "dotg_compute_partials": (c_int, [_P, _P, _P, _P, c_size_t, c_int, _P]),
     "dotg_align_and_reduce": (c_int, [_P, _P, _P, c_size_t, c_size_t, _P]),

@@ -222,6 +222,17 @@ def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
     return out
 
 
+def compare(a, b) -> int:
+    """-1 / 0 / +1, high zero limbs ignored (limbs.hpp:84, limbs.cpp:46-53), on the device."""
+    a, b = _host_u64(a, "a"), _host_u64(b, "b")
+    m = max(a.size, b.size)
+    pa, pb = np.zeros(max(m, 1), np.uint64), np.zeros(max(m, 1), np.uint64)
+    pa[: a.size], pb[: b.size] = a, b
+    out = np.zeros(1, np.int32)
+    check(lib().dotg_compare_host(_hp(out), _hp(pa), _hp(pb), m, 1))
+    return int(out[0])
+
+
 # ---- the column pipeline as separate device stages (mul.hpp:32-67, mul.cpp:12-90)
 def num_pairs(c: int, m: int) -> int:
     """mul.hpp:36-38: pair count of column c (c = 2m - 1 is the carry slot, 0 pairs)."""

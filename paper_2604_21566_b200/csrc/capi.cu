@@ -957,6 +957,20 @@ int dotg_align_and_reduce_host(uint64_t* columns, const uint64_t* p_lo, const ui
                       });
 }
 
+int dotg_compare_host(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch) {
+    if (batch == 0) return DOTG_OK;
+    if (out == nullptr || (m > 0 && (a == nullptr || b == nullptr))) return fail(DOTG_EINVAL, "compare: null operand");
+    if (m > SIZE_MAX / 8 / batch) return fail(DOTG_EINVAL, "compare: size overflow");
+    const size_t ib = m * batch * 8;
+    return run_staged({{const_cast<uint64_t*>(a), ib, true, false}, {const_cast<uint64_t*>(b), ib, true, false},
+                       {out, batch * 4, false, true}},
+                      "compare", [&](std::vector<void*>& d, cudaStream_t st) {
+                          return dotg::launch_compare_batch(static_cast<int32_t*>(d[2]),
+                                                            static_cast<uint64_t*>(d[0]),
+                                                            static_cast<uint64_t*>(d[1]), m, batch, 0, st);
+                      });
+}
+
 int dotg_carry_pass_host(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
                          int limb_bits) {
     int rc = check_radix_bits(limb_bits);

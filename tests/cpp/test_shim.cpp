@@ -137,6 +137,12 @@ int main() {
             }
         }
     });
+    run("compare ignores high zero limbs", [] {  // test_limbs.cpp compare cases
+        CHECK(compare(Limbs{1, 0, 0}, Limbs{1}) == 0);
+        CHECK(compare(Limbs{0, 1}, Limbs{kMax}) == 1);
+        CHECK(compare(Limbs{}, Limbs{0}) == 0);
+        CHECK(compare(Limbs{5}, Limbs{6, 0}) == -1);
+    });
     run("column pipeline stages through the drop-in", [] {  // test_mul.cpp:54-252
         std::mt19937_64 rng(11);
         const Limbs a = uniform_limbs(rng, 5), b = uniform_limbs(rng, 5);

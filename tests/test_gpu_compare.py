@@ -58,3 +58,21 @@ def test_compare_empty_and_errors(cuda):
     a = torch.zeros((3, 4), dtype=torch.int64, device="cuda")
     with pytest.raises(dg.InvalidArgument):
         dg.compare_batch(a, torch.zeros((3, 5), dtype=torch.int64, device="cuda"))
+
+
+def test_compare_value_form(cuda, oracle):
+    """compare(a, b) with unequal lengths: high zero limbs are ignored (limbs.cpp:46-53)."""
+    from paper_2604_21566_b200 import api
+
+    rng = np.random.default_rng(5)
+    for _ in range(60):
+        ma, mb = int(rng.integers(0, 9)), int(rng.integers(0, 9))
+        a = rng.integers(0, 2**64, size=ma, dtype=np.uint64)
+        b = rng.integers(0, 2**64, size=mb, dtype=np.uint64)
+        if ma and rng.random() < 0.3:
+            a[-1] = 0
+        if ma and mb and rng.random() < 0.3:
+            b = np.concatenate([a, np.zeros(int(rng.integers(0, 3)), np.uint64)])
+        assert api.compare(a, b) == oracle.compare(a, b), (a, b)
+    assert api.compare([], []) == 0 and api.compare([0, 0], [0]) == 0
+    assert api.compare([1], [0, 0, 0]) == 1 and api.compare([MAX], [0, 1]) == -1
