@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "internal.h"
@@ -453,8 +454,12 @@ cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b,
 template <bool SUB>
 cudaError_t run_interleaved_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                                 size_t batch, cudaStream_t st) {
+    // segments of 8 / 16 / 32 limbs keep up to 32 warps per strip of 32 pairs
+    // (tools/layout_timing.py: m = 512 2.0 -> 3.0 TB/s with 16-limb segments instead of 32;
+    // m = 1024 2.8 TB/s, thread per pair before)
     if (m <= 256) return run_interleaved<8, 32, SUB>(out, a, b, flags, m, batch, st);
-    return run_interleaved<32, 16, SUB>(out, a, b, flags, m, batch, st);
+    if (m <= 512) return run_interleaved<16, 32, SUB>(out, a, b, flags, m, batch, st);
+    return run_interleaved<32, 32, SUB>(out, a, b, flags, m, batch, st);
 }
 
 template <bool SUB>
@@ -550,7 +555,7 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             continue;
         }
         const int r = route(P, layouts[i]);
-        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 512) {
+        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 1024) {
             cudaError_t e = P.sub ? run_interleaved_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                                   : run_interleaved_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
             if (e != cudaSuccess) return e;

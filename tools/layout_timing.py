@@ -22,7 +22,7 @@ def t(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
-for m, B in list(W.C2_SIZES) + [(128, 1 << 15), (512, 1 << 13)]:
+for m, B in list(W.C2_SIZES) + [(128, 1 << 15), (512, 1 << 13), (1024, 1 << 12)]:
     a, b, sa, sb = W.c2_inputs(m, B)
     ai, bi = a.t().contiguous(), b.t().contiguous()
     out, fl = dg.add_batch(a, b)
