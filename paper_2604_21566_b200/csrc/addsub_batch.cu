@@ -449,8 +449,10 @@ cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b,
 
 // Interleaved problems by length (tools/layout_timing.py, B200, B x m = 2^22 limbs):
 // m < 128 thread-per-pair strided (5.2-6.6 TB/s); 128 <= m <= 256 8-limb segments, up to
-// 32 per CTA (4.0-4.3 TB/s vs 3.0 for 16-limb segments of two pairs per lane); 256 < m <=
-// 512 32-limb segments (2.0 TB/s vs 1.1 strided); longer numbers strided.
+// 32 per CTA (4.0-4.3 TB/s vs 3.0 for 16-limb segments of two pairs per lane, 3.2-3.4 for
+// 16-warp CTAs of 16-limb segments, 3.7 for 4-limb segments or 16-warp CTAs at m = 128);
+// 256 < m <= 512 16-limb segments (3.0 TB/s; 2.0 with 32-limb ones, 1.1 strided);
+// 512 < m <= 1024 32-limb segments (2.8 TB/s); longer numbers strided.
 template <bool SUB>
 cudaError_t run_interleaved_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                                 size_t batch, cudaStream_t st) {
