@@ -260,6 +260,17 @@ int dotg_align_and_reduce_host(uint64_t* columns, const uint64_t* p_lo, const ui
 int dotg_carry_pass_host(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
                          int limb_bits);
 
+/* ---------------------------------------------------------------------------
+ * Carry statistics (acceptance criterion 4, acceptance.cpp:157-170). Replaces:
+ * carry_census(k) (oracle.cpp:65-78): counts[0] = pairs (x, y) in [0, 2^k)^2 with
+ * x + y = 2^k - 1, counts[1] = pairs with x + y >= 2^k, 1 <= k <= 16 (exhaustive, on the
+ * device); and run_stats' Monte-Carlo carry frequency (bench.cpp:278-287): *carries =
+ * carry-outs of `samples` random 64-bit additions (splitmix64 stream of `seed`).
+ * Host pointers; synchronous.
+ * ------------------------------------------------------------------------- */
+int dotg_carry_census(unsigned k, uint64_t* counts);
+int dotg_mc_carry(uint64_t samples, uint64_t seed, uint64_t* carries);
+
 /* Workload setup (not the hot path): out[i] = splitmix64 output for counter
  * offset + i + 1 (device pointer, stream-ordered). Host twin: oracle/dot_oracle.c. */
 int dotg_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset,

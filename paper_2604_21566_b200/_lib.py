@@ -47,6 +47,8 @@ SIGNATURES = {
     "dotg_fill_splitmix64": (c_int, [_P, c_size_t, c_uint64, c_uint64, _P]),
     "dotg_compare_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
     "dotg_compare_host": (c_int, [_P, _P, _P, c_size_t, c_size_t]),
+    "dotg_carry_census": (c_int, [c_uint, _P]),
+    "dotg_mc_carry": (c_int, [c_uint64, c_uint64, _P]),
     "dotg_gather_columns": (c_int, [_P, _P, _P, _P, c_size_t, c_size_t, _P]),
     "dotg_compute_partials": (c_int, [_P, _P, _P, _P, c_size_t, c_int, _P]),
     "dotg_align_and_reduce": (c_int, [_P, _P, _P, c_size_t, c_size_t, _P]),

@@ -233,6 +233,32 @@ def compare(a, b) -> int:
     return int(out[0])
 
 
+def carry_census(k: int):
+    """(max_sum_pairs, carry_pairs) over all k-bit pairs (oracle.cpp:65-78), on the device."""
+    out = np.zeros(2, np.uint64)
+    check(lib().dotg_carry_census(int(k), _hp(out)))
+    return int(out[0]), int(out[1])
+
+
+def run_stats(k_max: int = 12, mc_samples: int = 10_000_000, seed: int = 1) -> dict:
+    """run_stats (bench.cpp:261-289): census rows k = 1..k_max against the closed forms
+    2^k and 2^(k-1) (2^k - 1), and the Monte-Carlo carry frequency of random 64-bit adds
+    (|f - 0.5| <= 0.001); everything counted on the device."""
+    if not 1 <= int(k_max) <= 16:
+        raise InvalidArgument("stats: k_max must be in 1..16")
+    rows = []
+    for k in range(1, int(k_max) + 1):
+        ms, cp = carry_census(k)
+        cm, cc = 1 << k, (1 << (k - 1)) * ((1 << k) - 1)
+        rows.append({"k": k, "max_sum_pairs": ms, "closed_max_sum": cm, "carry_pairs": cp, "closed_carry": cc,
+                     "match": ms == cm and cp == cc})
+    c = np.zeros(1, np.uint64)
+    check(lib().dotg_mc_carry(int(mc_samples), int(seed) & (2**64 - 1), _hp(c)))
+    freq = int(c[0]) / mc_samples if mc_samples else 0.0
+    return {"census": rows, "mc_samples": int(mc_samples), "mc_carry_freq": freq,
+            "mc_within_tolerance": bool(mc_samples) and abs(freq - 0.5) <= 0.001}
+
+
 # ---- the column pipeline as separate device stages (mul.hpp:32-67, mul.cpp:12-90)
 def num_pairs(c: int, m: int) -> int:
     """mul.hpp:36-38: pair count of column c (c = 2m - 1 is the carry slot, 0 pairs)."""

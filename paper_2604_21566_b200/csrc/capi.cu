@@ -971,6 +971,21 @@ int dotg_compare_host(int32_t* out, const uint64_t* a, const uint64_t* b, size_t
                       });
 }
 
+int dotg_carry_census(unsigned k, uint64_t* counts) {
+    if (k < 1 || k > 16) return fail(DOTG_EINVAL, "carry_census: k must be in 1..16");  // oracle.cpp:66
+    if (counts == nullptr) return fail(DOTG_EINVAL, "carry_census: null output");
+    return run_staged({{counts, 16, false, true}}, "carry census", [&](std::vector<void*>& d, cudaStream_t st) {
+        return dotg::launch_carry_census(k, static_cast<uint64_t*>(d[0]), st);
+    });
+}
+
+int dotg_mc_carry(uint64_t samples, uint64_t seed, uint64_t* carries) {
+    if (carries == nullptr) return fail(DOTG_EINVAL, "mc carry: null output");
+    return run_staged({{carries, 8, false, true}}, "mc carry", [&](std::vector<void*>& d, cudaStream_t st) {
+        return dotg::launch_mc_carry(samples, seed, static_cast<uint64_t*>(d[0]), st);
+    });
+}
+
 int dotg_carry_pass_host(uint64_t* out, uint32_t* out_limbs, size_t out_cap, const uint64_t* columns, size_t ncols,
                          int limb_bits) {
     int rc = check_radix_bits(limb_bits);

@@ -109,6 +109,10 @@ cudaError_t launch_align_reduce(uint64_t* cols, const uint64_t* plo, const uint6
 cudaError_t launch_carry_pass(uint64_t* out, uint32_t* nout, size_t cap, const uint64_t* cols, size_t ncols,
                               size_t batch, unsigned k, cudaStream_t st);
 
+// Carry statistics (run_stats / carry_census, stats.cu).
+cudaError_t launch_carry_census(unsigned k, uint64_t* counts, cudaStream_t st);
+cudaError_t launch_mc_carry(uint64_t samples, uint64_t seed, uint64_t* carries, cudaStream_t st);
+
 // Workload setup: splitmix64 counter fill (util.cu).
 cudaError_t launch_fill_splitmix64(uint64_t* out, size_t n, uint64_t seed, uint64_t offset, cudaStream_t st);
 

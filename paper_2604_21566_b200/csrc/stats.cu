@@ -57,7 +57,66 @@ __global__ void __launch_bounds__(256) k_addsub_stats(const uint64_t* out, const
     }
 }
 
+// carry_census(k) (src/oracle.cpp:65-78): over all (x, y) in [0, 2^k)^2, pairs whose sum is
+// exactly 2^k - 1 (propagate) and pairs whose sum carries out (>= 2^k). The same
+// exhaustive 2^2k enumeration as the reference (the point is to check the closed forms),
+// as a grid-stride over pair indices t = x * 2^k + y.
+__global__ void __launch_bounds__(256) k_carry_census(unsigned k, unsigned long long* counts) {
+    const uint64_t n = uint64_t(1) << k, total = n * n, max = n - 1;
+    unsigned long long ms = 0, cs = 0;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t s = (t >> k) + (t & max);
+        ms += s == max;
+        cs += s >= n;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        ms += __shfl_down_sync(0xffffffffu, ms, o);
+        cs += __shfl_down_sync(0xffffffffu, cs, o);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        atomicAdd(counts, ms);
+        atomicAdd(counts + 1, cs);
+    }
+}
+
+// Monte-Carlo carry frequency of random 64-bit limb additions (run_stats,
+// src/bench.cpp:278-287): sample n = (x_n, y_n) from the counter-based splitmix64 stream
+// (the device's workload generator) instead of mt19937_64; the check is statistical.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+__global__ void __launch_bounds__(256) k_mc_carry(uint64_t samples, uint64_t seed, unsigned long long* carries) {
+    unsigned long long c = 0;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < samples;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t x = mix64(seed + (2 * t + 1) * 0x9e3779b97f4a7c15ull);
+        const uint64_t y = mix64(seed + (2 * t + 2) * 0x9e3779b97f4a7c15ull);
+        c += (x + y) < x;
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31u) == 0) atomicAdd(carries, c);
+}
+
 }  // namespace
+
+cudaError_t launch_carry_census(unsigned k, uint64_t* counts, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(uint64_t), st);
+    if (e != cudaSuccess) return e;
+    k_carry_census<<<148 * 8, 256, 0, st>>>(k, reinterpret_cast<unsigned long long*>(counts));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_mc_carry(uint64_t samples, uint64_t seed, uint64_t* carries, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(carries, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return e;
+    k_mc_carry<<<148 * 8, 256, 0, st>>>(samples, seed, reinterpret_cast<unsigned long long*>(carries));
+    count_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_addsub_stats(bool sub, const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                                 size_t batch, int layout, unsigned lanes, uint64_t* counters, cudaStream_t st) {

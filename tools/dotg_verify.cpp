@@ -350,12 +350,67 @@ int cmd_bench(const std::vector<Case>& corpus, int width, unsigned reps, const s
 
 }  // namespace
 
+// `dotg-verify stats [--k-max K] [--samples N] [--seed S]`: dotarith stats
+// (dotarith_cli.cpp:141-156, bench.cpp:261-289) with the census and the Monte-Carlo pass
+// counted on the device. Exit 0 when every row matches its closed form and the carry
+// frequency is within 0.5 +/- 0.001, else 1.
+int cmd_stats(int argc, char** argv) {
+    unsigned k_max = 12;
+    uint64_t samples = 10000000, seed = 1;
+    for (int i = 2; i < argc; i += 2) {
+        const std::string opt = argv[i];
+        if (i + 1 >= argc) {
+            std::fprintf(stderr, "option %s needs a value\n", opt.c_str());
+            return 2;
+        }
+        const char* v = argv[i + 1];
+        if (opt == "--k-max") k_max = unsigned(std::strtoul(v, nullptr, 10));
+        else if (opt == "--samples") samples = std::strtoull(v, nullptr, 10);
+        else if (opt == "--seed") seed = std::strtoull(v, nullptr, 10);
+        else {
+            std::fprintf(stderr, "unknown option: %s\n", opt.c_str());
+            return 2;
+        }
+    }
+    if (k_max < 1 || k_max > 16) {
+        std::fprintf(stderr, "stats: k_max must be in 1..16\n");
+        return 2;
+    }
+    bool ok = true;
+    std::printf("%3s %22s %22s %s\n", "k", "max-sum (got/closed)", "carry (got/closed)", "match");
+    for (unsigned k = 1; k <= k_max; ++k) {
+        uint64_t c[2] = {0, 0};
+        if (dotg_carry_census(k, c) != DOTG_OK) {
+            std::fprintf(stderr, "error: %s\n", dotg_last_error());
+            return 2;
+        }
+        const uint64_t cm = uint64_t(1) << k, cc = (uint64_t(1) << (k - 1)) * ((uint64_t(1) << k) - 1);
+        const bool match = c[0] == cm && c[1] == cc;
+        ok = ok && match;
+        std::printf("%3u %10llu /%10llu %10llu /%10llu %s\n", k, static_cast<unsigned long long>(c[0]),
+                    static_cast<unsigned long long>(cm), static_cast<unsigned long long>(c[1]),
+                    static_cast<unsigned long long>(cc), match ? "yes" : "NO");
+    }
+    uint64_t carries = 0;
+    if (dotg_mc_carry(samples, seed, &carries) != DOTG_OK) {
+        std::fprintf(stderr, "error: %s\n", dotg_last_error());
+        return 2;
+    }
+    const double f = samples ? double(carries) / double(samples) : 0.0;
+    const bool within = samples && std::fabs(f - 0.5) <= 0.001;
+    std::printf("monte-carlo: %llu samples, carry frequency %.6f (0.5 +/- 0.001: %s)\n",
+                static_cast<unsigned long long>(samples), f, within ? "yes" : "NO");
+    return ok && within ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
     const std::string cmd = argc >= 2 ? argv[1] : "";
+    if (cmd == "stats") return cmd_stats(argc, argv);
     if (argc < 3 || (cmd != "verify" && cmd != "bench")) {
         std::fprintf(stderr,
                      "usage: dotg-verify verify <corpus.jsonl> [--width scalar|2|4|8]\n"
-                     "       dotg-verify bench <corpus.jsonl> [--width scalar|2|4|8] [--reps R] [--csv path]\n");
+                     "       dotg-verify bench <corpus.jsonl> [--width scalar|2|4|8] [--reps R] [--csv path]\n"
+                     "       dotg-verify stats [--k-max K] [--samples N] [--seed S]\n");
         return 2;
     }
     int width = 8;
