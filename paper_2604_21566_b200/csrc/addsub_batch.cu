@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* ou
                                                                      const uint64_t* b, uint32_t* flags,
                                                                      size_t m, size_t batch, bool vec_ok) {
     __shared__ uint32_t sgp[kIMaxS][32 * kPPL];  // bit 0 G, bit 1 P per (segment, pair)
+    __shared__ uint32_t scin[32 * kPPL];          // bit j: carry into segment j, per pair
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
     const int S = int(blockDim.x >> 5);
     const size_t p = size_t(blockIdx.x) * (32 * kPPL) + size_t(kPPL * lane);  // lane's first pair
@@ -307,13 +308,25 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* ou
         sgp[w][kPPL * lane + q] = c | (all << 1);
     }
     __syncthreads();
+    // carries into every segment of a pair at once: the segments' (G, P) bits as two masks
+    // and one mask addition, C = ((G << 1) + P) ^ P - the limb-level lookahead applied to
+    // segments (warp 0, lane = pair), instead of each warp folding its lower segments
+    if (w == 0) {
+#pragma unroll
+        for (int q = 0; q < kPPL; ++q) {
+            uint64_t G = 0, P = 0;
+            for (int j = 0; j < S; ++j) {
+                const uint32_t v = sgp[j][kPPL * lane + q];
+                G |= uint64_t(v & 1u) << j;
+                P |= uint64_t((v >> 1) & 1u) << j;
+            }
+            scin[kPPL * lane + q] = uint32_t(((G << 1) + P) ^ P);
+        }
+    }
+    __syncthreads();
 #pragma unroll
     for (int q = 0; q < kPPL; ++q) {
-        uint32_t cin = 0;  // carry into this segment: fold lower segments of the pair
-        for (int j = 0; j < w; ++j) {
-            const uint32_t v = sgp[j][kPPL * lane + q];
-            cin = (v & 1u) | (((v >> 1) & 1u) & cin);
-        }
+        const uint32_t cin = (scin[kPPL * lane + q] >> w) & 1u;  // carry into this segment
         uint32_t c = cin;
 #pragma unroll
         for (int k = 0; k < kIL; ++k)
