@@ -47,6 +47,15 @@ __device__ __forceinline__ uint32_t chunk_carry(uint32_t g, uint32_t p, uint32_t
     return ((uint32_t(y) ^ P) >> lane) & 1u;
 }
 
+// Both warp kernels walk a pair in 32-limb chunks whose carries chain serially; the loads
+// of kGrp chunks are issued together before their carry chain runs, so a warp keeps kGrp
+// chunks of memory traffic in flight instead of one (tools/kara_breakdown.py: the level
+// passes were 55-87% of a padded product with one chunk per step).
+#ifndef DOTG_KARA_GRP
+#define DOTG_KARA_GRP 4
+#endif
+constexpr int kGrp = DOTG_KARA_GRP;
+
 // Children of pair p, parent read as 2h limbs with zero padding above its m limbs:
 //   lo = A[0:h], hi = A[h:2h], df = |hi - lo|, sign = (hi < lo).
 __global__ void __launch_bounds__(kKaraWarps * 32) k_kara_split_w(const uint64_t* __restrict__ A, size_t m,
@@ -57,31 +66,55 @@ __global__ void __launch_bounds__(kKaraWarps * 32) k_kara_split_w(const uint64_t
     if (p >= count) return;
     const uint64_t* a = A + p * m;
     auto limb = [&](size_t i) -> uint64_t { return i < m ? __ldg(a + i) : 0ull; };
-    // highest limb where hi and lo differ decides the sign (compare, limbs.cpp:46-53)
+    uint64_t* plo = lo + p * h;
+    uint64_t* phi = hi + p * h;
+    uint64_t* pdf = df + p * h;
+    // pass 1: copy the halves out and find the highest limb where they differ, which
+    // decides the sign (compare, limbs.cpp:46-53)
     unsigned top = 0;  // 1 + index of the highest differing limb seen by this lane
-    for (size_t i = lane; i < h; i += 32)
-        if (limb(h + i) != limb(i)) top = unsigned(i) + 1;
+    for (size_t base = 0; base < h; base += 32 * kGrp) {
+        uint64_t x[kGrp], y[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const size_t i = base + 32 * u + lane;
+            x[u] = i < h ? limb(h + i) : 0ull;
+            y[u] = i < h ? limb(i) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const size_t i = base + 32 * u + lane;
+            if (i < h) {
+                plo[i] = y[u];
+                phi[i] = x[u];
+                if (x[u] != y[u]) top = unsigned(i) + 1;
+            }
+        }
+    }
     const unsigned hi_diff = __reduce_max_sync(0xffffffffu, top);
     bool neg = false;
     if (hi_diff != 0) {
         const size_t i = hi_diff - 1;
         neg = limb(h + i) < limb(i);  // every lane reads the same limb (broadcast)
     }
-    uint64_t* plo = lo + p * h;
-    uint64_t* phi = hi + p * h;
-    uint64_t* pdf = df + p * h;
+    // pass 2: larger minus smaller, borrows by chunk lookahead
     uint32_t cin = 0;
-    for (size_t base = 0; base < h; base += 32) {
-        const size_t i = base + lane;
-        const bool ok = i < h;
-        const uint64_t x = ok ? limb(h + i) : 0ull, y = ok ? limb(i) : 0ull;
-        const uint64_t u = neg ? y : x, v = neg ? x : y;  // larger minus smaller
-        const uint64_t d = u - v;
-        const uint32_t bin = chunk_carry(ok && u < v, ok && d == 0, cin, lane);
-        if (ok) {
-            plo[i] = y;
-            phi[i] = x;
-            pdf[i] = d - bin;
+    for (size_t base = 0; base < h; base += 32 * kGrp) {
+        uint64_t x[kGrp], y[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const size_t i = base + 32 * u + lane;
+            x[u] = i < h ? limb(h + i) : 0ull;
+            y[u] = i < h ? limb(i) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            if (base + 32 * u >= h) break;
+            const size_t i = base + 32 * u + lane;
+            const bool ok = i < h;
+            const uint64_t uu = neg ? y[u] : x[u], vv = neg ? x[u] : y[u];
+            const uint64_t d = uu - vv;
+            const uint32_t bin = chunk_carry(ok && uu < vv, ok && d == 0, cin, lane);
+            if (ok) pdf[i] = d - bin;
         }
     }
     if (lane == 0) sign[p] = neg ? 1u : 0u;
@@ -105,29 +138,39 @@ __global__ void __launch_bounds__(kKaraWarps * 32) k_kara_combine_w(const uint64
     uint64_t* o = out + p * n_out;
     for (size_t k = lane; k < h && k < n_out; k += 32) o[k] = __ldg(p0 + k);
     uint32_t cT = 0, cM = 0, cR = 0;
-    for (size_t base = 0; base < 3 * h; base += 32) {
-        const size_t j = base + lane, k = h + j;
-        const bool ok = j < 3 * h;
-        const bool low = j < n2;
-        const uint64_t x0 = ok && low ? __ldg(p0 + j) : 0ull, x1 = ok && low ? __ldg(p1 + j) : 0ull;
-        const uint64_t dd = ok && low ? __ldg(pd + j) : 0ull;
-        // T = P0 + P1
-        const uint64_t ts = x0 + x1;
-        const uint64_t t = ts + chunk_carry(ok && ts < x0, ok && ts == ~0ull, cT, lane);
-        // M = T -+ PD
-        uint64_t mj;
-        if (minus) {
-            const uint64_t ms = t - dd;
-            mj = ms - chunk_carry(ok && t < dd, ok && ms == 0, cM, lane);
-        } else {
-            const uint64_t ms = t + dd;
-            mj = ms + chunk_carry(ok && ms < t, ok && ms == ~0ull, cM, lane);
+    for (size_t base = 0; base < 3 * h; base += 32 * kGrp) {
+        uint64_t x0[kGrp], x1[kGrp], dd[kGrp], bk[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const size_t j = base + 32 * u + lane, k = h + j;
+            const bool ok = j < 3 * h, low = j < n2;
+            x0[u] = ok && low ? __ldg(p0 + j) : 0ull;
+            x1[u] = ok && low ? __ldg(p1 + j) : 0ull;
+            dd[u] = ok && low ? __ldg(pd + j) : 0ull;
+            bk[u] = !ok ? 0ull : (k < n2 ? __ldg(p0 + k) : __ldg(p1 + (k - n2)));
         }
-        // R[h + j] = base + M[j]
-        const uint64_t bk = !ok ? 0ull : (k < n2 ? __ldg(p0 + k) : __ldg(p1 + (k - n2)));
-        const uint64_t rs = bk + mj;
-        const uint64_t r = rs + chunk_carry(ok && rs < bk, ok && rs == ~0ull, cR, lane);
-        if (ok && k < n_out) o[k] = r;
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            if (base + 32 * u >= 3 * h) break;
+            const size_t j = base + 32 * u + lane, k = h + j;
+            const bool ok = j < 3 * h;
+            // T = P0 + P1
+            const uint64_t ts = x0[u] + x1[u];
+            const uint64_t t = ts + chunk_carry(ok && ts < x0[u], ok && ts == ~0ull, cT, lane);
+            // M = T -+ PD
+            uint64_t mj;
+            if (minus) {
+                const uint64_t ms = t - dd[u];
+                mj = ms - chunk_carry(ok && t < dd[u], ok && ms == 0, cM, lane);
+            } else {
+                const uint64_t ms = t + dd[u];
+                mj = ms + chunk_carry(ok && ms < t, ok && ms == ~0ull, cM, lane);
+            }
+            // R[h + j] = base + M[j]
+            const uint64_t rs = bk[u] + mj;
+            const uint64_t r = rs + chunk_carry(ok && rs < bk[u], ok && rs == ~0ull, cR, lane);
+            if (ok && k < n_out) o[k] = r;
+        }
     }
 }
 
@@ -209,7 +252,10 @@ unsigned flat_grid(size_t total) {
 
 // Wide when each warp would walk >= 4096 limbs and there are too few pairs to fill the
 // GPU with warps; the long-number kernels take at most 65535 numbers per launch.
-bool kara_wide(size_t h, size_t count) { return h >= 4096 && count <= 2048; }
+#ifndef DOTG_KARA_WIDE_H
+#define DOTG_KARA_WIDE_H 4096
+#endif
+bool kara_wide(size_t h, size_t count) { return h >= DOTG_KARA_WIDE_H && count <= 2048; }
 
 cudaError_t split_wide(const uint64_t* A, size_t m, size_t h, size_t count, uint64_t* lo, uint64_t* hi,
                        uint64_t* df, uint32_t* sign, cudaStream_t st) {
@@ -442,6 +488,10 @@ cudaError_t run_karatsuba_at(uint64_t* out, const uint64_t* a, const uint64_t* b
 
 cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, const KaraPlan& plan,
                           cudaStream_t st) {
+    // small runs skip the free-memory query (cudaMemGetInfo costs host time on every call)
+    const char* env_budget = std::getenv("DOTG_KARA_BUDGET_MB");
+    if (env_budget == nullptr && kara_bf_bytes(plan, 0, batch) <= (size_t(1) << 30))
+        return run_karatsuba_bf(out, a, b, batch, plan, 0, st);
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = size_t(16) << 30;
     // breadth-first while its scratch stays inside the pool's 8 GiB reserve (7 GiB, or 70%
@@ -450,7 +500,7 @@ cudaError_t run_karatsuba(uint64_t* out, const uint64_t* a, const uint64_t* b, s
     // multi-CTA long-number passes (tools/mul_max_timing.py: 2^22 limbs 140 ms vs 0.7-0.8 s,
     // 2^24 limbs 1.21 s vs 1.7-1.9 s with a 70%-of-free budget)
     size_t budget = std::min(free_b / 10 * 7, size_t(7) << 30);
-    if (const char* e = std::getenv("DOTG_KARA_BUDGET_MB")) budget = size_t(std::strtoull(e, nullptr, 10)) << 20;
+    if (env_budget != nullptr) budget = size_t(std::strtoull(env_budget, nullptr, 10)) << 20;
     return run_karatsuba_at(out, a, b, batch, plan, 0, budget, st);
 }
 
