@@ -75,6 +75,11 @@ int dotg_sub_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t
  * exactly (same pointer and pitch). */
 int dotg_addsub_batch_strided(int sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b,
                               size_t ldb, uint32_t* flags, size_t m, size_t batch, dotg_stream_t stream);
+/* Row-pitched multiply: a[p * lda + i], b[p * ldb + i], out[p * ldo + k] (k < 2m); pitches
+ * in limbs (lda, ldb >= m and ldo >= 2m when batch > 1). Non-dense pitches gather the rows
+ * into scratch and scatter the product (two extra passes). out must not overlap a or b. */
+int dotg_mul_batch_strided(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b, size_t ldb,
+                           size_t m, size_t batch, dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Grouped batched add/sub: up to any number of INDEPENDENT problems (sizes may differ)

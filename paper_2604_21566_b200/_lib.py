@@ -59,6 +59,7 @@ SIGNATURES = {
     "dotg_carry_pass_host": (c_int, [_P, _P, c_size_t, _P, c_size_t, c_int]),
     "dotg_addsub_batch_strided": (c_int, [c_int, _P, c_size_t, _P, c_size_t, _P, c_size_t, _P, c_size_t, c_size_t,
                                           _P]),
+    "dotg_mul_batch_strided": (c_int, [_P, c_size_t, _P, c_size_t, _P, c_size_t, c_size_t, c_size_t, _P]),
     "dotg_chunk_batch": (c_int, [c_int, _P, _P, _P, _P, _P, _P, c_uint, c_size_t, _P]),
     "dotg_chunk_host": (c_int, [c_int, _P, _P, _P, _P, _P, c_uint32, c_uint]),
     "dotg_kernel_launches": (c_uint64, []),

@@ -515,6 +515,21 @@ def mul_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):
     INTERLEAVED out: [2m, batch]."""
     torch = _torch()
     lay = _layout(layout)
+    views = [t for t in (a, b, out) if t is not None]
+    if lay == ROW_MAJOR and not all(t.is_contiguous() for t in views if isinstance(t, torch.Tensor)) and all(
+            _row_pitched(t) for t in views):
+        # row-pitched views (e.g. x[:, :m] of a wider tensor): dotg_mul_batch_strided
+        if a.shape != b.shape:
+            raise InvalidArgument("dot mul: operand shapes differ")
+        batch, m = a.shape
+        if out is None:
+            out = torch.empty((batch, 2 * m), dtype=a.dtype, device=a.device)
+        if tuple(out.shape) != (batch, 2 * m):
+            raise InvalidArgument("out must hold exactly 2m limbs per pair")
+        pitch = [t.stride(0) if t.shape[0] > 1 else n for t, n in ((out, 2 * m), (a, m), (b, m))]
+        check(lib().dotg_mul_batch_strided(_dptr(out), pitch[0], _dptr(a), pitch[1], _dptr(b), pitch[2], m, batch,
+                                           _stream_handle(stream)))
+        return out
     _check_dev(a, "a")
     _check_dev(b, "b")
     if a.shape != b.shape:

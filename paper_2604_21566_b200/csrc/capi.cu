@@ -560,6 +560,26 @@ int dotg_addsub_batch_strided(int sub, uint64_t* out, size_t ldo, const uint64_t
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg add/sub strided launch");
 }
 
+int dotg_mul_batch_strided(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b, size_t ldb,
+                           size_t m, size_t batch, dotg_stream_t stream) {
+    if (m == 0) return fail(DOTG_EINVAL, "dot mul: operands need at least one limb");
+    if (m > (size_t(1) << 24)) return fail(DOTG_EINVAL, "dot mul: limb count exceeds the column accumulator bound");
+    if (batch == 0) return DOTG_OK;
+    if (out == nullptr || a == nullptr || b == nullptr) return fail(DOTG_EINVAL, "dot mul: null operand");
+    if (batch > 1 && (lda < m || ldb < m || ldo < 2 * m))
+        return fail(DOTG_EINVAL, "dot mul: row pitch below the limb count");
+    const size_t mx = std::max(ldo, std::max(lda, ldb));
+    if (mx > SIZE_MAX / 8 / batch) return fail(DOTG_EINVAL, "dot mul: size overflow");
+    auto span = [&](size_t ld, size_t n) { return ((batch - 1) * ld + n) * sizeof(uint64_t); };
+    if (ranges_overlap(out, span(ldo, 2 * m), a, span(lda, m)) || ranges_overlap(out, span(ldo, 2 * m), b, span(ldb, m)))
+        return fail(DOTG_EINVAL, "dot mul: out must not overlap the operands");
+    int rc = check_device();
+    if (rc != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_mul_pitched(out, ldo, a, lda, b, ldb, m, batch, static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorMemoryAllocation) return fail(DOTG_ENOMEM, "dot mul: scratch allocation failed");
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg mul strided launch");
+}
+
 int dotg_addsub_grouped(const dotg_addsub_problem* problems, int n, dotg_stream_t stream) {
     if (n < 0 || (n > 0 && problems == nullptr)) return fail(DOTG_EINVAL, "grouped: bad problem list");
     if (n == 0) return DOTG_OK;

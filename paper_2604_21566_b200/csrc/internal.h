@@ -52,6 +52,8 @@ cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
 cudaError_t launch_addsub_pitched(bool sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,
                                   const uint64_t* b, size_t ldb, uint32_t* flags, size_t m, size_t batch,
                                   cudaStream_t stream);
+cudaError_t launch_mul_pitched(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b,
+                               size_t ldb, size_t m, size_t batch, cudaStream_t st);
 cudaError_t launch_long_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
                               size_t m, size_t batch, cudaStream_t stream);
 

@@ -552,6 +552,34 @@ cudaError_t mul_padded_rows(uint64_t* out, const uint64_t* a, const uint64_t* b,
     return e;
 }
 
+// Row-pitched operands / product (views of wider arrays): gather the rows into dense
+// scratch, run the dense route, scatter the product rows (two extra coalesced passes).
+cudaError_t launch_mul_pitched(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda, const uint64_t* b,
+                               size_t ldb, size_t m, size_t batch, cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    if (ldo == 2 * m && lda == m && ldb == m) return launch_mul_batch(out, a, b, m, batch, 0, st);
+    retain_stream_pool();
+    uint64_t *pa = nullptr, *pb = nullptr, *po = nullptr;
+    cudaError_t e = cudaMallocAsync(&pa, batch * m * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&pb, batch * m * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&po, batch * 2 * m * 8, st);
+    if (e == cudaSuccess) {
+        k_copy_2d<<<flat_grid(batch * m), 256, 0, st>>>(pa, m, 0, a, lda, 0, m, batch);
+        k_copy_2d<<<flat_grid(batch * m), 256, 0, st>>>(pb, m, 0, b, ldb, 0, m, batch);
+        count_launch(2);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = launch_mul_batch(po, pa, pb, m, batch, 0, st);
+    if (e == cudaSuccess) {
+        k_copy_2d<<<flat_grid(batch * 2 * m), 256, 0, st>>>(out, ldo, 0, po, 2 * m, 0, 2 * m, batch);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    for (void* q : {static_cast<void*>(pa), static_cast<void*>(pb), static_cast<void*>(po)})
+        if (q != nullptr) cudaFreeAsync(q, st);
+    return e;
+}
+
 // Reference recursion (kara_rec, mul.cpp:176-233): split h = ceil(m / 2) until m <= theta.
 cudaError_t launch_karatsuba_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                    size_t theta, cudaStream_t st) {

@@ -160,3 +160,25 @@ def test_config_parity_full_size(cuda, oracle, route, cfg):
     got = host(dg.mul_batch(a, b))
     want = oracle.mul_batch(ha, hb)
     assert np.array_equal(got, want)
+
+
+def test_row_pitched_views(cuda, oracle):
+    """dotg_mul_batch_strided: operands and product as row-pitched views of wider tensors."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(505)
+    for m, batch, wa, wb, wo in ((16, 300, 20, 16, 40), (64, 100, 64, 70, 128), (3, 50, 5, 4, 9), (200, 7, 210, 200, 400)):
+        A = uniform(rng, (batch, wa))
+        B = uniform(rng, (batch, wb))
+        A[0, :m] = MAX
+        B[0, :m] = MAX
+        ta = torch.from_numpy(A.view(np.int64)).cuda()[:, :m]
+        tb = torch.from_numpy(B.view(np.int64)).cuda()[:, :m]
+        O = torch.full((batch, wo), 7, dtype=torch.int64, device="cuda")
+        got = dg.mul_batch(ta, tb, out=O[:, : 2 * m])
+        want = oracle.mul_batch(np.ascontiguousarray(A[:, :m]), np.ascontiguousarray(B[:, :m]))
+        Oh = O.cpu().numpy().view(np.uint64)
+        assert np.array_equal(Oh[:, : 2 * m], want), m
+        assert (Oh[:, 2 * m:] == 7).all()  # the rest of each row untouched
+        assert np.array_equal(dg.mul_batch(ta, tb).cpu().numpy().view(np.uint64), want)
