@@ -399,13 +399,26 @@ def _torch():
 
 
 def _dptr(t):
-    return None if t is None else ctypes.c_void_p(t.data_ptr())
+    # the ctypes signatures declare c_void_p: a plain int converts without a wrapper object
+    return None if t is None else t.data_ptr()
+
+
+_raw_stream = None
 
 
 def _stream_handle(stream):
+    """The caller's stream (or the current one) as a raw cudaStream_t. The current-stream
+    query goes through torch's raw accessor when it exists (~0.3 us instead of ~3 us for
+    torch.cuda.current_stream(), which builds a Stream object)."""
+    global _raw_stream
+    if stream is not None:
+        return stream.cuda_stream
     torch = _torch()
-    s = torch.cuda.current_stream() if stream is None else stream
-    return ctypes.c_void_p(s.cuda_stream)
+    if _raw_stream is None:
+        getter = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _raw_stream = (lambda: getter(torch.cuda.current_device())) if getter else (
+            lambda: torch.cuda.current_stream().cuda_stream)
+    return _raw_stream()
 
 
 def _check_dev(t, name, elem=8):
