@@ -67,3 +67,22 @@ def test_chunk_batch_invalid_carry_and_alias(cuda):
     with pytest.raises(dg.InvalidArgument):
         dg.chunk_batch(False, torch.zeros((4, 9), dtype=torch.int64, device="cuda"),
                        torch.zeros((4, 9), dtype=torch.int64, device="cuda"))
+
+
+def test_chunk_batch_in_place(cuda, oracle):
+    """sums may alias a (or b) exactly, like the word-level forms (addsub.hpp:95-97)."""
+    import paper_2604_21566_b200 as dg
+    from paper_2604_21566_b200 import api
+
+    torch = cuda
+    rng = np.random.default_rng(88)
+    a, b = spiky(rng, (500, 8)), spiky(rng, (500, 8))
+    ta = torch.from_numpy(a.view(np.int64).copy()).cuda()
+    tb = torch.from_numpy(b.view(np.int64)).cuda()
+    co = torch.empty(500, dtype=torch.int32, device="cuda")
+    api.check(dg.lib().dotg_chunk_batch(0, api._dptr(ta), api._dptr(co), None, api._dptr(ta), api._dptr(tb), None, 8,
+                                        500, api._stream_handle(None)))
+    got = ta.cpu().numpy().view(np.uint64)
+    for p in range(0, 500, 13):
+        want, wc, _ = oracle.chunk(False, a[p], b[p], 0, 8)
+        assert np.array_equal(got[p], want) and int(co[p]) == wc

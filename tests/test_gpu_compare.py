@@ -76,3 +76,12 @@ def test_compare_value_form(cuda, oracle):
         assert api.compare(a, b) == oracle.compare(a, b), (a, b)
     assert api.compare([], []) == 0 and api.compare([0, 0], [0]) == 0
     assert api.compare([1], [0, 0, 0]) == 1 and api.compare([MAX], [0, 1]) == -1
+
+
+def test_compare_zero_limbs(cuda):
+    """m = 0 with pairs: every pair compares equal."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    z = torch.zeros((5, 0), dtype=torch.int64, device="cuda")
+    assert dg.compare_batch(z, z).tolist() == [0] * 5
