@@ -57,3 +57,36 @@ def test_routing_fuzz(cuda, oracle, seed):
                 got = out.cpu().numpy().view(np.uint64).T
             assert np.array_equal(got, want), ctx
             assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf), ctx
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_pitched_views_fuzz(cuda, oracle, seed):
+    """Row-pitched operand / result views (dotg_addsub_batch_strided, dotg_mul_batch_strided)
+    with random sizes, pitches and column offsets, against the oracle."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(777 + seed)
+    for it in range(25):
+        m = int(rng.choice(M_CHOICES))
+        batch = int(rng.integers(1, 300))
+        cat = CATEGORIES[int(rng.integers(len(CATEGORIES)))]
+        op = ["add", "sub", "mul"][it % 3]
+        a, b = category(rng, cat, "mul" if op == "mul" else op, (batch, m))
+
+        def view(x, extra):
+            wide = np.zeros((x.shape[0], x.shape[1] + extra), np.uint64)
+            off = int(rng.integers(0, extra + 1))
+            wide[:, off:off + x.shape[1]] = x
+            t = torch.from_numpy(wide.view(np.int64)).cuda()
+            return t[:, off:off + x.shape[1]]
+
+        ta, tb = view(a, int(rng.integers(0, 9))), view(b, int(rng.integers(0, 9)))
+        if op == "mul":
+            got = dg.mul_batch(ta, tb).cpu().numpy().view(np.uint64)
+            assert np.array_equal(got, oracle.mul_batch(a, b)), (seed, it, m, batch)
+        else:
+            out, fl = dg.addsub_batch(op == "sub", ta, tb)
+            want, wf = oracle.addsub_batch(op == "sub", a, b)
+            assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (seed, it, m, batch, op)
+            assert np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
