@@ -40,7 +40,8 @@ typedef enum {
     DOTG_EINVAL = 1,  /* std::invalid_argument in the reference */
     DOTG_ECUDA = 2,   /* CUDA runtime error / no sm_100 device */
     DOTG_ENOMEM = 3,  /* device or host allocation failed */
-    DOTG_ENOTSUP = 4  /* argument combination not supported */
+    DOTG_ENOTSUP = 4, /* argument combination not supported */
+    DOTG_ENCCL = 5    /* NCCL missing or a collective failed (sharded entry points) */
 } dotg_status;
 
 typedef enum { DOTG_ROW_MAJOR = 0, DOTG_INTERLEAVED = 1 } dotg_layout;
@@ -118,8 +119,8 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
  * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
  * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it
  * does not cover). Both are bit-exact; the knob exists for A/B measurement and for
- * parity tests of both kernels. Process-wide. Returns the previous route, or
- * DOTG_EINVAL for an unknown value. */
+ * parity tests of both kernels. Process-wide. Returns the previous route (>= 0), or
+ * -DOTG_EINVAL (negative, distinct from every route) for an unknown value. */
 #define DOTG_MUL_AUTO 0
 #define DOTG_MUL_IMAD 1
 #define DOTG_MUL_IMMA 2
@@ -174,6 +175,35 @@ int dotg_shard_local(int sub, uint64_t* out, const uint64_t* a, const uint64_t* 
                      void* state, uint32_t* agg, dotg_stream_t stream);
 int dotg_shard_finish(int sub, uint64_t* out, size_t m, void* state, const uint32_t* all_aggs,
                       int rank, int world, uint32_t* carry_out, dotg_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * The same protocol driven from C++ in one call per rank (SURVEY.md §8(b)
+ * dotg_add_words_sharded; §8(e)). Replaces: the serial chunk chain of one long number,
+ * dot_add_words / dot_sub_words span form over m limbs (addsub.cpp:136-170, 286-294),
+ * when the number's limbs are spread over the GPUs of one node.
+ *   dotg_add_words_sharded(out, a, b, m_local, carry_out, comm, stream)
+ * enqueues on `stream`: dotg_shard_local -> ncclAllGather of the 8-byte {G, P} -> the
+ * boundary fix-up; no host synchronisation (CUDA-graph capturable). out/a/b are this
+ * rank's m_local limbs (rank order = limb order, any split, m_local = 0 allowed);
+ * carry_out (device uint32, may be NULL) receives the carry/borrow of the WHOLE number.
+ * A dotg_comm wraps an NCCL communicator: created here from an NCCL unique id (rank 0
+ * calls dotg_comm_get_unique_id and the caller broadcasts the dotg_comm_id_bytes()
+ * bytes by any means), or wrapped around a caller-owned ncclComm_t (dotg_comm_wrap; not
+ * destroyed by dotg_comm_destroy). NCCL is loaded at run time; without it these calls
+ * return DOTG_ENCCL. The current device must be the communicator's device.
+ * ------------------------------------------------------------------------- */
+typedef struct dotg_comm dotg_comm;
+size_t dotg_comm_id_bytes(void);
+int dotg_comm_get_unique_id(void* id);
+int dotg_comm_init_rank(dotg_comm** comm, int world, const void* id, int rank);
+int dotg_comm_wrap(dotg_comm** comm, void* nccl_comm);
+int dotg_comm_destroy(dotg_comm* comm);
+int dotg_comm_rank(const dotg_comm* comm);
+int dotg_comm_size(const dotg_comm* comm);
+int dotg_add_words_sharded(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m_local,
+                           uint32_t* carry_out, const dotg_comm* comm, dotg_stream_t stream);
+int dotg_sub_words_sharded(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m_local,
+                           uint32_t* carry_out, const dotg_comm* comm, dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Host-buffer entry points (the reference-facing call: host spans in, host out).

@@ -217,3 +217,68 @@ void dotor_mul_columns52(uint64_t* out, const uint64_t* a, const uint64_t* b, si
     }
     free(col);
 }
+
+/* ---- the column pipeline as separate stages (mul.hpp:32-67, mul.cpp:12-90) ---- */
+
+/* gather_columns (mul.cpp:12-36): column order, c ascending, i ascending. */
+size_t dotor_gather_columns(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m) {
+    size_t t = 0;
+    for (size_t c = 0; c + 1 < 2 * m; ++c) {
+        const size_t i_lo = c + 1 >= m ? c + 1 - m : 0;
+        const size_t i_hi = c < m - 1 ? c : m - 1;
+        for (size_t i = i_lo; i <= i_hi; ++i, ++t) {
+            m_a[t] = a[i];
+            m_b[t] = b[c - i];
+        }
+    }
+    return t;
+}
+
+/* compute_partials (mul.cpp:38-52): split each product at bit k (k = 64 or 52). */
+void dotor_compute_partials(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                            unsigned k) {
+    const uint64_t mask = k >= 64 ? ~(uint64_t)0 : (((uint64_t)1 << k) - 1);
+    for (size_t t = 0; t < n; ++t) {
+        const u128 p = (u128)m_a[t] * m_b[t];
+        p_lo[t] = (uint64_t)p & mask;
+        p_hi[t] = (uint64_t)(p >> k);
+    }
+}
+
+/* align_and_reduce (mul.cpp:54-68): 2m u128 column sums as (low, high) word pairs. */
+void dotor_align_and_reduce(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m) {
+    u128* col = (u128*)calloc(2 * m, sizeof(u128));
+    size_t t = 0;
+    for (size_t c = 0; c + 1 < 2 * m; ++c) {
+        const size_t lo = c + 1 >= m ? c + 1 - m : 0, hi = c < m - 1 ? c : m - 1;
+        for (size_t i = lo; i <= hi; ++i, ++t) {
+            col[c] += p_lo[t];
+            col[c + 1] += p_hi[t];
+        }
+    }
+    for (size_t c = 0; c < 2 * m; ++c) {
+        columns[2 * c] = (uint64_t)col[c];
+        columns[2 * c + 1] = (uint64_t)(col[c] >> 64);
+    }
+    free(col);
+}
+
+/* carry_pass (mul.cpp:70-90): serial renormalisation to base 2^k with the 128-bit wrap
+ * fold, then residual limbs. out holds ncols + 3 limbs; returns the limbs written. */
+size_t dotor_carry_pass(uint64_t* out, const uint64_t* columns, size_t ncols, unsigned k) {
+    const uint64_t mask = k >= 64 ? ~(uint64_t)0 : (((uint64_t)1 << k) - 1);
+    u128 carry = 0;
+    size_t n = 0;
+    for (size_t c = 0; c < ncols; ++c) {
+        const u128 col = ((u128)columns[2 * c + 1] << 64) | columns[2 * c];
+        const u128 v = col + carry;
+        const u128 wrapped = v < col ? ((u128)1 << (128 - k)) : 0;
+        out[n++] = (uint64_t)v & mask;
+        carry = (v >> k) + wrapped;
+    }
+    while (carry != 0) {
+        out[n++] = (uint64_t)carry & mask;
+        carry >>= k;
+    }
+    return n;
+}

@@ -49,6 +49,16 @@ void dotor_mul_columns(uint64_t* out, const uint64_t* a, const uint64_t* b, size
 /* dot_mul_words(a, b, kUnsaturated) (mul.cpp:38-90 at k = 52): exactly 2m limbs < 2^52. */
 void dotor_mul_columns52(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m);
 
+/* The column pipeline stage by stage (u128 columns as (low, high) uint64 pairs):
+ * gather_columns (mul.cpp:12-36) -> returns m*m; compute_partials at k in {64, 52}
+ * (mul.cpp:38-52); align_and_reduce (mul.cpp:54-68) -> 2m columns; carry_pass
+ * (mul.cpp:70-90) over any ncols columns, out holds ncols + 3 limbs, returns the count. */
+size_t dotor_gather_columns(uint64_t* m_a, uint64_t* m_b, const uint64_t* a, const uint64_t* b, size_t m);
+void dotor_compute_partials(uint64_t* p_lo, uint64_t* p_hi, const uint64_t* m_a, const uint64_t* m_b, size_t n,
+                            unsigned k);
+void dotor_align_and_reduce(uint64_t* columns, const uint64_t* p_lo, const uint64_t* p_hi, size_t m);
+size_t dotor_carry_pass(uint64_t* out, const uint64_t* columns, size_t ncols, unsigned k);
+
 /* compare (src/limbs.cpp:46-53): -1 / 0 / +1 ignoring high zero limbs. */
 int dotor_compare(const uint64_t* a, size_t ma, const uint64_t* b, size_t mb);
 

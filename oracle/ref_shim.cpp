@@ -113,6 +113,68 @@ int dotref_mul_words(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, s
     });
 }
 
+// The column pipeline stages one by one (mul.hpp:32-67, mul.cpp:12-90), so the device
+// stages (dotg_gather_columns ... dotg_carry_pass) are pinned to the reference's own
+// outputs. u128 values cross the ABI as (low 64, high 64) pairs.
+namespace {
+dot::RadixConfig radix_of(int bits) { return bits == 52 ? dot::kUnsaturated : dot::kSaturated; }
+}  // namespace
+
+// gather_columns: m_a / m_b receive the m*m gathered limbs (column order). Returns m*m.
+int dotref_gather_columns(limb_t* m_a, limb_t* m_b, const limb_t* a, const limb_t* b, size_t m) {
+    return guarded([&] {
+        const dot::ColumnBuffers buf = dot::gather_columns(Limbs(a, a + m), Limbs(b, b + m));
+        std::copy(buf.m_a.begin(), buf.m_a.end(), m_a);
+        std::copy(buf.m_b.begin(), buf.m_b.end(), m_b);
+        return int(buf.m_a.size());
+    });
+}
+
+// compute_partials over n gathered pairs (any n; the reference only reads m_a / m_b).
+int dotref_compute_partials(limb_t* p_lo, limb_t* p_hi, const limb_t* m_a, const limb_t* m_b, size_t n,
+                            int limb_bits, int width) {
+    return guarded([&] {
+        dot::ColumnBuffers buf;
+        buf.m_a.assign(m_a, m_a + n);
+        buf.m_b.assign(m_b, m_b + n);
+        buf.p_lo.assign(n, 0);
+        buf.p_hi.assign(n, 0);
+        dot::compute_partials(buf, radix_of(limb_bits), width_of(width));
+        std::copy(buf.p_lo.begin(), buf.p_lo.end(), p_lo);
+        std::copy(buf.p_hi.begin(), buf.p_hi.end(), p_hi);
+        return 0;
+    });
+}
+
+// align_and_reduce of the m*m partials of an m-limb product: 2m u128 column sums.
+int dotref_align_and_reduce(limb_t* columns, const limb_t* p_lo, const limb_t* p_hi, size_t m) {
+    return guarded([&] {
+        dot::ColumnBuffers buf;
+        buf.m = m;
+        buf.p_lo.assign(p_lo, p_lo + m * m);
+        buf.p_hi.assign(p_hi, p_hi + m * m);
+        buf.col_lo.assign(2 * m, 0);
+        const std::span<const dot::u128> cols = dot::align_and_reduce(buf);
+        for (size_t c = 0; c < cols.size(); ++c) {
+            columns[2 * c] = limb_t(cols[c]);
+            columns[2 * c + 1] = limb_t(cols[c] >> 64);
+        }
+        return int(cols.size());
+    });
+}
+
+// carry_pass over ncols arbitrary u128 columns; out must hold ncols + 3 limbs. Returns the
+// number of limbs written (ncols plus the residual limbs, if any).
+int dotref_carry_pass(limb_t* out, const limb_t* columns, size_t ncols, int limb_bits) {
+    return guarded([&] {
+        std::vector<dot::u128> cols(ncols);
+        for (size_t c = 0; c < ncols; ++c) cols[c] = (dot::u128(columns[2 * c + 1]) << 64) | columns[2 * c];
+        const Limbs r = dot::carry_pass(std::span<const dot::u128>(cols.data(), cols.size()), radix_of(limb_bits));
+        std::copy(r.begin(), r.end(), out);
+        return int(r.size());
+    });
+}
+
 // 52-bit radix routes (mul.hpp:73-85): dot_mul_words(kUnsaturated), dot_mul_5x5,
 // dot_mul_4x4, and the repacking helpers (limbs.hpp:111-117). Return the output length.
 int dotref_mul_words52(limb_t* out, const limb_t* a, size_t ma, const limb_t* b, size_t mb) {

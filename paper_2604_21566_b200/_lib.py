@@ -14,7 +14,7 @@ from ctypes import c_char_p, c_int, c_size_t, c_uint, c_uint32, c_uint64, c_void
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libdotg.so")
 
-DOTG_OK, DOTG_EINVAL, DOTG_ECUDA, DOTG_ENOMEM, DOTG_ENOTSUP = range(5)
+DOTG_OK, DOTG_EINVAL, DOTG_ECUDA, DOTG_ENOMEM, DOTG_ENOTSUP, DOTG_ENCCL = range(6)
 ROW_MAJOR, INTERLEAVED = 0, 1
 
 # Every symbol include/dotg.h declares: name -> (restype, argtypes).
@@ -64,6 +64,15 @@ SIGNATURES = {
     "dotg_chunk_host": (c_int, [c_int, _P, _P, _P, _P, _P, c_uint32, c_uint]),
     "dotg_kernel_launches": (c_uint64, []),
     "dotg_set_mul_route": (c_int, [c_int]),
+    "dotg_comm_id_bytes": (c_size_t, []),
+    "dotg_comm_get_unique_id": (c_int, [_P]),
+    "dotg_comm_init_rank": (c_int, [_P, c_int, _P, c_int]),
+    "dotg_comm_wrap": (c_int, [_P, _P]),
+    "dotg_comm_destroy": (c_int, [_P]),
+    "dotg_comm_rank": (c_int, [_P]),
+    "dotg_comm_size": (c_int, [_P]),
+    "dotg_add_words_sharded": (c_int, [_P, _P, _P, c_size_t, _P, _P, _P]),
+    "dotg_sub_words_sharded": (c_int, [_P, _P, _P, c_size_t, _P, _P, _P]),
 }
 
 
@@ -84,6 +93,10 @@ class InvalidArgument(DotgError, ValueError):
 
 class DotgCudaError(DotgError):
     """CUDA failure or no sm_100 device (there is no CPU fallback)."""
+
+
+class DotgNcclError(DotgError):
+    """NCCL missing or a collective of the sharded entry points failed."""
 
 
 _lib = None
@@ -118,6 +131,8 @@ def check(rc: int) -> None:
         raise DotgCudaError(msg)
     if rc == DOTG_ENOMEM:
         raise MemoryError(msg)
+    if rc == DOTG_ENCCL:
+        raise DotgNcclError(msg)
     raise DotgError(f"dotg status {rc}: {msg}")
 
 
@@ -134,4 +149,6 @@ def set_mul_route(route: str) -> str:
     if route not in _ROUTES:
         raise InvalidArgument(f"mul route must be one of {sorted(_ROUTES)}")
     prev = int(lib().dotg_set_mul_route(_ROUTES[route]))
+    if prev < 0:
+        check(-prev)
     return {v: k for k, v in _ROUTES.items()}[prev]

@@ -569,10 +569,17 @@ def addsub_stats(sub: bool, out, a, b, *, width=Width.w8, layout=ROW_MAJOR, stre
     if not (a.shape == b.shape == out.shape):
         raise InvalidArgument("stats: operand shapes differ")
     batch, m = _batch_dims(a, lay)
-    cnt = torch.zeros(2, dtype=torch.int64, device=a.device)
-    check(lib().dotg_addsub_stats(int(sub), _dptr(out), _dptr(a), _dptr(b), m, batch, lay, int(width), _dptr(cnt),
-                                  _stream_handle(stream)))
-    ch, fi = cnt.tolist()
+    # the counters are zeroed, accumulated and read back on ONE stream (the caller's):
+    # the zero-fill runs on it as torch's current stream, and the read-back synchronises it
+    import contextlib
+
+    with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+        cnt = torch.zeros(2, dtype=torch.int64, device=a.device)
+        check(lib().dotg_addsub_stats(int(sub), _dptr(out), _dptr(a), _dptr(b), m, batch, lay, int(width),
+                                      _dptr(cnt), _stream_handle(stream)))
+        if stream is not None:
+            stream.synchronize()
+        ch, fi = cnt.tolist()
     return int(ch), int(fi)
 
 

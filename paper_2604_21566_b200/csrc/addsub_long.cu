@@ -352,6 +352,33 @@ cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const 
     return cudaGetLastError();
 }
 
+// An empty shard (m = 0) still takes part in the exchange: it is all-propagate with no
+// generate, {G, P} = {0, 1} - the identity of the (G, P) composition.
+__global__ void k_shard_identity(uint32_t* agg) {
+    agg[0] = 0u;
+    agg[1] = 1u;
+}
+
+// Whole-number carry from the gathered shard aggregates (what k_long_finish writes for a
+// non-empty shard): total = G_{w-1} | (P_{w-1} & total_{w-2}) ...
+__global__ void k_compose_aggs(const uint32_t* all_aggs, int world, uint32_t* carry_out) {
+    uint32_t total = 0;
+    for (int q = 0; q < world; ++q) total = all_aggs[2 * q] | (all_aggs[2 * q + 1] & total);
+    *carry_out = total;
+}
+
+cudaError_t launch_shard_identity(uint32_t* agg, cudaStream_t stream) {
+    k_shard_identity<<<1, 1, 0, stream>>>(agg);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compose_aggs(const uint32_t* all_aggs, int world, uint32_t* carry_out, cudaStream_t stream) {
+    k_compose_aggs<<<1, 1, 0, stream>>>(all_aggs, world, carry_out);
+    count_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
                                const uint32_t* all_aggs, int rank, int world, uint32_t* carry_out,
                                cudaStream_t stream) {

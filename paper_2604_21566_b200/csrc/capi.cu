@@ -256,6 +256,7 @@ SliceGeom geom(const HostJob& j) {
 // downloads on a third, each slice linked only by its own two events: nothing ever waits
 // for a download to free a staging slot. Used while the image fits in kFlatMax bytes.
 constexpr size_t kFlatMax = size_t(16) << 30;
+constexpr int kFlatNoMem = -1;  // run_host_jobs_flat: no room for the image, nothing enqueued
 
 struct FlatGeom {
     size_t da, db, dout, dfl;  // offsets of the job's arrays in the image
@@ -288,8 +289,11 @@ int run_host_jobs_flat(const HostJob* jobs, int n, const std::vector<FlatGeom>& 
         if (g_host.flat) cudaFree(g_host.flat);
         g_host.flat = nullptr;
         g_host.flat_cap = 0;
-        if ((e = cudaMalloc(&g_host.flat, bytes)) != cudaSuccess)
-            return fail(DOTG_ENOMEM, std::string("host pipeline image: ") + cudaGetErrorString(e));
+        if ((e = cudaMalloc(&g_host.flat, bytes)) != cudaSuccess) {
+            g_host.flat = nullptr;
+            cudaGetLastError();  // clear the (non-sticky) allocation error for the caller
+            return kFlatNoMem;   // caller falls back to the staging-slot pipeline
+        }
         g_host.flat_cap = bytes;
     }
     while (g_host.ev.size() < 2 * slices) {
@@ -362,7 +366,10 @@ int run_host_jobs(const HostJob* jobs, int n) {
         if (bytes <= kFlatMax) {
             int rc = host_prepare(256);
             if (rc != DOTG_OK) return rc;
-            return run_host_jobs_flat(jobs, n, fg, bytes, slices);
+            rc = run_host_jobs_flat(jobs, n, fg, bytes, slices);
+            if (rc != kFlatNoMem) return rc;
+            // the image did not fit next to what the device already holds: the slot
+            // pipeline below needs only kNS slices of staging
         }
     }
     size_t slot = 256;
@@ -485,6 +492,14 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
 
 }  // namespace
 
+namespace dotg {
+int api_fail(int code, const std::string& msg) { return fail(code, msg); }
+int api_check_device() { return check_device(); }
+int api_check_addsub_words(const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m) {
+    return check_addsub(const_cast<uint64_t*>(out), a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
+}
+}  // namespace dotg
+
 extern "C" {
 
 int dotg_validate_width(int width) {
@@ -507,7 +522,7 @@ uint64_t dotg_kernel_launches(void) { return dotg::g_launches.load(); }
 
 int dotg_set_mul_route(int route) {
     if (route != DOTG_MUL_AUTO && route != DOTG_MUL_IMAD && route != DOTG_MUL_IMMA)
-        return fail(DOTG_EINVAL, "set_mul_route: route must be DOTG_MUL_AUTO, DOTG_MUL_IMAD or DOTG_MUL_IMMA");
+        return -fail(DOTG_EINVAL, "set_mul_route: route must be DOTG_MUL_AUTO, DOTG_MUL_IMAD or DOTG_MUL_IMMA");
     return dotg::g_mul_route.exchange(route);
 }
 
@@ -741,6 +756,30 @@ int dotg_addsub_grouped_host(const dotg_addsub_problem* problems, int n) {
         if (q.layout != DOTG_ROW_MAJOR) return fail(DOTG_EINVAL, "grouped host: row-major only");
         int rc = check_addsub(q.out, q.a, q.b, q.flags, q.m, q.batch, q.layout);
         if (rc != DOTG_OK) return rc;
+        if (q.m > 0 && q.batch > 0) {
+            // The pipeline uploads every problem's operands on one stream while results
+            // download on another: a problem reading another's out (a chained problem) would
+            // upload stale host data. Same independence rule as dotg_addsub_grouped.
+            const size_t bytes = q.m * q.batch * 8;
+            for (int j = 0; j < i; ++j) {
+                const dotg_addsub_problem& o = problems[j];
+                const size_t ob = o.m * o.batch * 8;
+                if (!ob) continue;
+                const bool clash = ranges_overlap(q.out, bytes, o.out, ob) || ranges_overlap(q.out, bytes, o.a, ob) ||
+                                   ranges_overlap(q.out, bytes, o.b, ob) || ranges_overlap(o.out, ob, q.a, bytes) ||
+                                   ranges_overlap(o.out, ob, q.b, bytes) ||
+                                   (q.flags && (ranges_overlap(q.flags, q.batch * 4, o.out, ob) ||
+                                                ranges_overlap(q.flags, q.batch * 4, o.a, ob) ||
+                                                ranges_overlap(q.flags, q.batch * 4, o.b, ob) ||
+                                                (o.flags && ranges_overlap(q.flags, q.batch * 4, o.flags, o.batch * 4)))) ||
+                                   (o.flags && (ranges_overlap(o.flags, o.batch * 4, q.out, bytes) ||
+                                                ranges_overlap(o.flags, o.batch * 4, q.a, bytes) ||
+                                                ranges_overlap(o.flags, o.batch * 4, q.b, bytes)));
+                if (clash)
+                    return fail(DOTG_EINVAL,
+                                "grouped host: problems must be independent (an output overlaps another problem)");
+            }
+        }
         if (q.batch == 0) continue;
         if (q.m == 0) {
             if (q.flags) std::memset(q.flags, 0, q.batch * sizeof(uint32_t));

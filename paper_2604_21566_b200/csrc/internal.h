@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 namespace dotg {
 
@@ -47,6 +48,16 @@ cudaError_t launch_long_local(bool sub, uint64_t* out, const uint64_t* a, const 
 cudaError_t launch_long_finish(bool sub, uint64_t* out, size_t m, void* state,
                                const uint32_t* all_aggs, int rank, int world,
                                uint32_t* carry_out, cudaStream_t stream);
+
+// Empty shard aggregate {0, 1}; whole-number carry from gathered aggregates (comm.cu).
+cudaError_t launch_shard_identity(uint32_t* agg, cudaStream_t stream);
+cudaError_t launch_compose_aggs(const uint32_t* all_aggs, int world, uint32_t* carry_out, cudaStream_t stream);
+
+// Shared C-ABI helpers (capi.cu): set dotg_last_error and return code; the sm_100 check;
+// the span-form argument checks of one long add/sub (null operands, partial aliasing).
+int api_fail(int code, const std::string& msg);
+int api_check_device();
+int api_check_addsub_words(const uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m);
 
 // A batch of long numbers (row-major, m >= 1 tile): the tiled passes with grid.y = number.
 cudaError_t launch_addsub_pitched(bool sub, uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,

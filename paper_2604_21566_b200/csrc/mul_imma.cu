@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
     if (mr < C::M)
         for (int i = lane; i < C::RAW_WORDS; i += 32) raw[i] = 0;
     __syncwarp();
+    // the zero-fill is a generic-proxy write; the bulk copies below write the same ring
+    // through the async proxy: order the former before the latter
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
     const size_t nwarps = size_t(gridDim.x) * kImmaWarps;
     const size_t first = size_t(blockIdx.x) * kImmaWarps + warp;

@@ -75,24 +75,88 @@ class ShardedWords:
 
     def run(self, sub: bool, out, a, b, *, state=None, stream=None):
         """Returns (out, carry) where carry is an int32[1] tensor holding the carry of the
-        WHOLE number (identical on every rank)."""
+        WHOLE number (identical on every rank). Everything - the scratch zero-fills, both
+        device passes and the collective - is ordered on ``stream`` (default: the current
+        stream): the sequence runs with ``stream`` as torch's current stream, so the
+        allocations, the NCCL all-gather and the gloo host copy all wait on the passes."""
+        import contextlib
+
         import torch
 
         if a.shape != b.shape or out.shape != a.shape:
             raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")
         dev = a.device
-        if state is None:
-            state = self.state_for(a.numel(), dev) if dev.type == "cuda" else None
-        agg = torch.zeros(2, dtype=torch.int32, device=dev)
-        self.local_fn(sub, out, a, b, state, agg, stream)
-        all_aggs = torch.empty(2 * self.world, dtype=torch.int32, device=dev)
-        if dev.type == "cuda" and self.dist.get_backend(self.group) != "nccl":
-            # gloo (CPU collectives): stage the 8 bytes through host memory
-            host = torch.empty(2 * self.world, dtype=torch.int32)
-            self.dist.all_gather_into_tensor(host, agg.cpu(), group=self.group)
-            all_aggs.copy_(host)
-        else:
-            self.dist.all_gather_into_tensor(all_aggs, agg, group=self.group)
-        carry = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.finish_fn(sub, out, state, all_aggs, self.rank, self.world, carry, stream)
+        ctx = torch.cuda.stream(stream) if (stream is not None and dev.type == "cuda") else contextlib.nullcontext()
+        with ctx:
+            if state is None:
+                state = self.state_for(a.numel(), dev) if dev.type == "cuda" else None
+            agg = torch.zeros(2, dtype=torch.int32, device=dev)
+            self.local_fn(sub, out, a, b, state, agg, stream)
+            all_aggs = torch.empty(2 * self.world, dtype=torch.int32, device=dev)
+            if dev.type == "cuda" and self.dist.get_backend(self.group) != "nccl":
+                # gloo (CPU collectives): stage the 8 bytes through host memory (agg.cpu()
+                # synchronises with the current stream = the passes' stream)
+                host = torch.empty(2 * self.world, dtype=torch.int32)
+                self.dist.all_gather_into_tensor(host, agg.cpu(), group=self.group)
+                all_aggs.copy_(host)
+            else:
+                self.dist.all_gather_into_tensor(all_aggs, agg, group=self.group)
+            carry = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.finish_fn(sub, out, state, all_aggs, self.rank, self.world, carry, stream)
         return out, carry
+
+
+class CommShardedWords:
+    """The same protocol in ONE C-ABI call per rank (``dotg_add_words_sharded`` /
+    ``dotg_sub_words_sharded``): the local pass, the 8-byte ``ncclAllGather`` and the
+    boundary fix-up are enqueued by the library's C++ host code on one stream, over an
+    NCCL communicator the library owns (``dotg_comm``). ``torch.distributed`` only
+    carries the 128-byte NCCL unique id from rank 0 to the others at construction (any
+    backend). Construction is collective: every rank of ``group`` must create one."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        L = lib()
+        nid = int(L.dotg_comm_id_bytes())
+        payload = [None]
+        if self.rank == 0:
+            buf = ctypes.create_string_buffer(nid)
+            check(L.dotg_comm_get_unique_id(buf))
+            payload = [bytes(buf.raw)]
+        dist.broadcast_object_list(payload, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        uid = ctypes.create_string_buffer(payload[0], nid)
+        self._comm = ctypes.c_void_p()
+        check(L.dotg_comm_init_rank(ctypes.byref(self._comm), self.world, uid, self.rank))
+        assert L.dotg_comm_rank(self._comm) == self.rank and L.dotg_comm_size(self._comm) == self.world
+
+    def run(self, sub: bool, out, a, b, *, carry=None, stream=None):
+        """out = a +/- b over this rank's limbs; returns (out, carry) with carry an int32[1]
+        device tensor receiving the carry/borrow of the WHOLE number (every rank)."""
+        import torch
+
+        from .api import _dptr, _stream_handle
+
+        if a.shape != b.shape or out.shape != a.shape:
+            raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")
+        if carry is None:
+            carry = torch.empty(1, dtype=torch.int32, device=a.device)
+        fn = lib().dotg_sub_words_sharded if sub else lib().dotg_add_words_sharded
+        check(fn(_dptr(out), _dptr(a), _dptr(b), a.numel(), _dptr(carry), self._comm, _stream_handle(stream)))
+        return out, carry
+
+    def close(self) -> None:
+        if getattr(self, "_comm", None) is not None and self._comm.value:
+            check(lib().dotg_comm_destroy(self._comm))
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass

@@ -58,7 +58,42 @@ class Oracle:
         L.dotor_mul_columns52.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t]
         L.dotor_fill_splitmix64.restype = None
         L.dotor_fill_splitmix64.argtypes = [c_void_p, c_size_t, c_uint64, c_uint64]
+        L.dotor_gather_columns.restype = c_size_t
+        L.dotor_gather_columns.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t]
+        L.dotor_compute_partials.restype = None
+        L.dotor_compute_partials.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_uint]
+        L.dotor_align_and_reduce.restype = None
+        L.dotor_align_and_reduce.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t]
+        L.dotor_carry_pass.restype = c_size_t
+        L.dotor_carry_pass.argtypes = [c_void_p, c_void_p, c_size_t, c_uint]
         self.L = L
+
+    # the column pipeline stage by stage (mul.cpp:12-90); columns are [2m, 2] (low, high)
+    def gather_columns(self, a, b):
+        a, b = u64(a), u64(b)
+        m = a.size
+        ma, mb = np.zeros(m * m, U64), np.zeros(m * m, U64)
+        n = self.L.dotor_gather_columns(_p(ma), _p(mb), _p(a), _p(b), m)
+        assert n == m * m
+        return ma, mb
+
+    def compute_partials(self, ma, mb, k=64):
+        ma, mb = u64(ma), u64(mb)
+        lo, hi = np.zeros(ma.size, U64), np.zeros(ma.size, U64)
+        self.L.dotor_compute_partials(_p(lo), _p(hi), _p(ma), _p(mb), ma.size, k)
+        return lo, hi
+
+    def align_and_reduce(self, lo, hi, m):
+        lo, hi = u64(lo), u64(hi)
+        cols = np.zeros((2 * m, 2), U64)
+        self.L.dotor_align_and_reduce(_p(cols), _p(lo), _p(hi), m)
+        return cols
+
+    def carry_pass(self, cols, k=64):
+        cols = u64(cols).reshape(-1, 2)
+        out = np.zeros(cols.shape[0] + 3, U64)
+        n = self.L.dotor_carry_pass(_p(out), _p(cols), cols.shape[0], k)
+        return out[:n].copy()
 
     # oracle_add / oracle_sub (oracle.cpp:16-48)
     def add(self, a, b):
@@ -172,6 +207,14 @@ class Reference:
             getattr(L, fn).argtypes = [c_void_p, c_void_p, c_size_t]
         L.dotref_dispatch_note.restype = ctypes.c_char_p
         L.dotref_dispatch_note.argtypes = [c_int]
+        L.dotref_gather_columns.restype = c_int
+        L.dotref_gather_columns.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t]
+        L.dotref_compute_partials.restype = c_int
+        L.dotref_compute_partials.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_int, c_int]
+        L.dotref_align_and_reduce.restype = c_int
+        L.dotref_align_and_reduce.argtypes = [c_void_p, c_void_p, c_void_p, c_size_t]
+        L.dotref_carry_pass.restype = c_int
+        L.dotref_carry_pass.argtypes = [c_void_p, c_void_p, c_size_t, c_int]
         L.dotref_last_error.restype = ctypes.c_char_p
         self.L = L
 
@@ -220,6 +263,38 @@ class Reference:
         n = getattr(self.L, fn)(_p(out), _p(a), a.size)
         if n < 0:
             raise ValueError(self.L.dotref_last_error().decode())
+        return out[:n].copy()
+
+    # the column pipeline stages of the reference itself (mul.hpp:32-67)
+    def _ok(self, rc):
+        if rc < 0:
+            raise ValueError(self.L.dotref_last_error().decode())
+        return rc
+
+    def gather_columns(self, a, b):
+        a, b = u64(a), u64(b)
+        m = a.size
+        ma, mb = np.zeros(max(m * m, 1), U64), np.zeros(max(m * m, 1), U64)
+        n = self._ok(self.L.dotref_gather_columns(_p(ma), _p(mb), _p(a), _p(b), m))
+        return ma[:n].copy(), mb[:n].copy()
+
+    def compute_partials(self, ma, mb, k=64, width=8):
+        ma, mb = u64(ma), u64(mb)
+        lo, hi = np.zeros(ma.size, U64), np.zeros(ma.size, U64)
+        self._ok(self.L.dotref_compute_partials(_p(lo), _p(hi), _p(ma), _p(mb), ma.size, k, width))
+        return lo, hi
+
+    def align_and_reduce(self, lo, hi, m):
+        lo, hi = u64(lo), u64(hi)
+        cols = np.zeros((2 * m, 2), U64)
+        n = self._ok(self.L.dotref_align_and_reduce(_p(cols), _p(lo), _p(hi), m))
+        assert n == 2 * m
+        return cols
+
+    def carry_pass(self, cols, k=64):
+        cols = u64(cols).reshape(-1, 2)
+        out = np.zeros(cols.shape[0] + 3, U64)
+        n = self._ok(self.L.dotref_carry_pass(_p(out), _p(cols), cols.shape[0], k))
         return out[:n].copy()
 
     def oracle_addsub(self, sub, a, b):

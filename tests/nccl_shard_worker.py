@@ -15,7 +15,7 @@ def main():
     from helpers import Oracle
 
     from paper_2604_21566_b200 import workloads as W
-    from paper_2604_21566_b200.sharded import ShardedWords, shard_bounds
+    from paper_2604_21566_b200.sharded import CommShardedWords, ShardedWords, shard_bounds
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     dist.init_process_group("nccl")
@@ -28,13 +28,25 @@ def main():
         a, b = W.c5_shard_inputs(sub, lo, hi, m=m, run=run)
         ga, gb = W.c5_inputs(sub, m=m, run=run)
         assert torch.equal(ga[lo:hi], a) and torch.equal(gb[lo:hi], b)
-        out = torch.empty_like(a)
-        sw = ShardedWords()
-        out, carry = sw.run(sub, out, a, b)
         ha, hb = ga.cpu().numpy().view(np.uint64), gb.cpu().numpy().view(np.uint64)
         want, wf = orc.sub(ha, hb) if sub else orc.add(ha, hb)
+        # (1) Python-orchestrated: two C-ABI passes around torch's all_gather
+        out = torch.empty_like(a)
+        out, carry = ShardedWords().run(sub, out, a, b)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), want[lo:hi]), (rank, sub)
         assert int(carry.item()) == wf
+        # (2) C++-orchestrated: one dotg_*_words_sharded call over the library's own NCCL
+        # communicator, on a side stream
+        cs = CommShardedWords()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        out2 = torch.full_like(a, -1)
+        with torch.cuda.stream(st):
+            out2, carry2 = cs.run(sub, out2, a, b, stream=st)
+        st.synchronize()
+        assert np.array_equal(out2.cpu().numpy().view(np.uint64), want[lo:hi]), (rank, sub, "comm")
+        assert int(carry2.item()) == wf
+        cs.close()
     dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}/{world} ok")

@@ -53,6 +53,26 @@ def test_validation_before_device():
     assert rc == DOTG_EINVAL and b"alias" in L.dotg_last_error()
     assert L.dotg_shard_finish(0, None, 0, None, None, 3, 2, None, None) == DOTG_EINVAL
     assert L.dotg_shard_state_bytes(1 << 30) >= (1 << 30) // 4096 * 4
+    # sharded entry points: the comm is checked before NCCL or the device is touched
+    assert L.dotg_comm_id_bytes() == 128
+    assert L.dotg_add_words_sharded(None, None, None, 4, None, None, None) == DOTG_EINVAL
+    assert L.dotg_comm_init_rank(None, 1, None, 0) == DOTG_EINVAL
+    assert L.dotg_comm_destroy(None) == DOTG_OK
+    assert L.dotg_comm_rank(None) == -1 and L.dotg_comm_size(None) == -1
+    # grouped host problems must be independent: problem 1 reading problem 0's out is a
+    # chained call the copy pipeline cannot order
+    from paper_2604_21566_b200._lib import AddSubProblem
+
+    h = (ctypes.c_uint64 * 96)()
+    hb_ = ctypes.addressof(h)
+    probs = (AddSubProblem * 2)()
+    probs[0] = AddSubProblem(0, 0, hb_, hb_ + 256, hb_ + 512, None, 4, 8)       # out = [0, 256)
+    probs[1] = AddSubProblem(1, 0, hb_ + 512 + 256, hb_, hb_ + 256, None, 4, 1)  # reads out of 0
+    assert L.dotg_addsub_grouped_host(probs, 2) == DOTG_EINVAL
+    assert b"independent" in L.dotg_last_error()
+    # set_mul_route: an unknown route is negative, distinct from every valid route
+    assert L.dotg_set_mul_route(9) == -DOTG_EINVAL
+    assert b"route" in L.dotg_last_error()
 
 
 def test_python_validation_raises_invalid_argument():

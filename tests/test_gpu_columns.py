@@ -136,3 +136,57 @@ def test_batched_device_stages_and_chain(cuda, oracle):
         assert [int(cols_h[p][2 * c]) | int(cols_h[p][2 * c + 1]) << 64 for c in range(2 * m)] == hc
         assert nout[p] == 2 * m and np.array_equal(out[p][: 2 * m], want[p])
         assert np.array_equal(api.carry_pass(hc), want[p])
+
+
+def test_stages_match_reference_golden(cuda):
+    """Device stages against the reference's OWN stage outputs (tests/golden/
+    column_vectors.npz from oracle/_ref: gather_columns, compute_partials,
+    align_and_reduce, carry_pass), limb for limb and including the output length of
+    carry_pass (the residual limbs of raw columns, test_mul.cpp:229-252). Batched device
+    forms for the pipeline cases, the host forms for the raw carry cases."""
+    import os
+
+    from paper_2604_21566_b200 import api
+
+    torch = cuda
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "column_vectors.npz"))
+    L, s = api.lib(), api._stream_handle(None)
+
+    def dev(x):
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
+
+    def host(t):
+        return t.cpu().numpy().view(np.uint64)
+
+    for m in g["sizes"]:
+        m = int(m)
+        for k in (64, 52):
+            key = f"m{m}_k{k}"
+            A, B = g[key + "_a"], g[key + "_b"]
+            batch = A.shape[0]
+            ta, tb = dev(A), dev(B)
+            ma = torch.empty((batch, m * m), dtype=torch.int64, device="cuda")
+            mb = torch.empty_like(ma)
+            api.check(L.dotg_gather_columns(api._dptr(ma), api._dptr(mb), api._dptr(ta), api._dptr(tb), m, batch, s))
+            assert np.array_equal(host(ma), g[key + "_ma"]) and np.array_equal(host(mb), g[key + "_mb"]), key
+            lo, hi = torch.empty_like(ma), torch.empty_like(ma)
+            api.check(L.dotg_compute_partials(api._dptr(lo), api._dptr(hi), api._dptr(ma), api._dptr(mb),
+                                              batch * m * m, k, s))
+            assert np.array_equal(host(lo), g[key + "_plo"]) and np.array_equal(host(hi), g[key + "_phi"]), key
+            cols = torch.empty((batch, 4 * m), dtype=torch.int64, device="cuda")
+            api.check(L.dotg_align_and_reduce(api._dptr(cols), api._dptr(lo), api._dptr(hi), m, batch, s))
+            assert np.array_equal(host(cols).reshape(batch, 2 * m, 2), g[key + "_cols"]), key
+            cap = 2 * m + 2
+            out = torch.full((batch, cap), -1, dtype=torch.int64, device="cuda")
+            nout = torch.zeros(batch, dtype=torch.int32, device="cuda")
+            api.check(L.dotg_carry_pass(api._dptr(out), api._dptr(nout), cap, api._dptr(cols), 2 * m, batch, k, s))
+            want = g[key + "_out"]
+            assert (nout.cpu().numpy() == want.shape[1]).all(), key  # exactly the reference's length
+            assert np.array_equal(host(out)[:, : want.shape[1]], want), key
+    for k in (64, 52):
+        cols, co = g[f"carry_k{k}_cols"], g[f"carry_k{k}_col_offsets"]
+        outs, oo = g[f"carry_k{k}_out"], g[f"carry_k{k}_out_offsets"]
+        for j in range(co.size - 1):
+            c = cols[co[j]:co[j + 1]]
+            got = api.carry_pass([int(x[0]) | int(x[1]) << 64 for x in c], k)
+            assert np.array_equal(got, outs[oo[j]:oo[j + 1]]), (k, j)
