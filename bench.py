@@ -5,21 +5,25 @@ Headline workload (BASELINE.json configs[1], "C2"): the carry-stress add/sub swe
 (m, B) in (4, 2^20), (16, 2^18), (64, 2^16), (256, 2^14); each limb all-ones with p=1/2
 else uniform, 1% of pairs forced to a full-length carry chain; sub swaps pairs so a >= b.
 One step = batched add at all four sizes, then batched sub at all four sizes, through the
-device C ABI (dotg_add_batch / dotg_sub_batch). Metric: algorithmic GB/s
-(24m + 4 bytes per pair-op), roofline = measured HBM copy bandwidth.
+device C ABI (one dotg_addsub_grouped launch, replayed as a CUDA graph). Metric:
+algorithmic GB/s (24m + 4 bytes per pair-op), roofline = measured HBM copy bandwidth.
 
-The same JSON line also reports C1 (4096-bit add/sub), C3/C4 (1024/4096-bit mul,
-products/s vs the measured IMAD.WIDE roofline) and C5 (one 2^30-limb add/sub) under
-"configs".
+The same JSON line reports every other config under "configs", each with its own
+roofline, e2e (host C ABI, pinned buffers, copies timed) and reference CPU baseline:
+C1 (4096-bit add/sub), C3/C4 (1024/4096-bit mul, products/s vs the measured IMAD.WIDE
+roofline), C5 (one 2^30-limb add/sub), plus the interleaved layout.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--only C2] [--no-secondary]
+                  [--only C1,C3,C4,C5,IL] [--no-secondary]
 
-N > 1: launched by torch.distributed.run, one rank per GPU; every rank runs the full
-batch sweep on its own GPU (weak scaling, no collective on the data path); value = the
-bytes of all ranks / max-over-ranks time. --impl reference times the reference's own
-CPU implementation (oracle/_ref/libdotref.so: span-form dot_add_words / dot_sub_words
-at Width::w8 and dot_mul_words) on all host cores; under torchrun only rank 0 works.
+N > 1: launched by torch.distributed.run, one rank per GPU. Strong scaling: rank r runs
+the contiguous slice [B*r/N, B*(r+1)/N) of every named batch (no collective on the data
+path; C5 is split by limb range and exchanges 8 bytes per rank through
+dotg_add_words_sharded); value = the whole named workload / max-over-ranks time. The
+weak-scaling figure (full sweep on every rank) is reported as "weak_scaling".
+--impl reference times the reference's own CPU implementation (oracle/_ref/libdotref.so:
+span-form dot_add_words / dot_sub_words at Width::w8 and dot_mul_words) on all host
+cores; under torchrun only rank 0 works.
 """
 from __future__ import annotations
 
@@ -46,16 +50,17 @@ DATA = ("synthetic (seeded splitmix64, BASELINE.json configs[1] distribution: li
         "1% forced full carry chains, sub swapped to a>=b)")
 
 
-def c2_config(ungrouped=False, working_set=None):
-    cfg = {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
-           "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
-           "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if ungrouped else
-                    "one dotg_addsub_grouped call = one persistent launch: add at 4 sizes + sub at 4 sizes"),
-           "per_rank": "full sweep on every rank (weak scaling, no collective)"}
-    if working_set is not None:
-        cfg["l2"] = (f"inputs larger than L2: each step reads {working_set / 1e6:.0f} MB of distinct inputs "
-                     "(126 MB L2), every buffer touched once per step")
-    return cfg
+C2_WORKING_SET = sum(4 * B * m * 8 for m, B in C2_SIZES)  # distinct input bytes per step (a, b, sa, sb)
+
+
+def c2_config(ungrouped=False):
+    """The workload description, identical in both arms (ours and --impl reference)."""
+    return {"workload": "C2 carry-stress add+sub sweep (BASELINE.json configs[1])",
+            "sizes_m_batch": C2_SIZES, "layout": "row-major [batch][m] (reference Limbs layout)",
+            "step": ("8 launches: add at 4 sizes then sub at 4 sizes" if ungrouped else
+                     "add at 4 sizes + sub at 4 sizes (GPU: one dotg_addsub_grouped launch)"),
+            "l2": (f"inputs larger than L2: each step reads {C2_WORKING_SET / 1e6:.0f} MB of distinct inputs "
+                   "(126 MB L2), every buffer touched once per step")}
 
 
 # ---------------------------------------------------------------------------
@@ -200,6 +205,25 @@ class CpuRef:
             raise SystemExit("neither oracle/_ref/libdotref.so nor oracle/liboracle.so is built")
         self.L = L
 
+    def words(self, sub, out, a, b):
+        """One long number, span form (dot_add_words / dot_sub_words, Width::w8, single
+        thread: the reference's carry chain is serial). Returns the carry/borrow."""
+        P = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+        if self.kind == "reference":
+            L = self.L
+            L.dotref_words.restype = ctypes.c_int
+            L.dotref_words.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                       ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                       ctypes.c_void_p, ctypes.c_void_p]
+            c = L.dotref_words(int(sub), P(out), out.size, P(a), a.size, P(b), b.size, 8, None, None)
+            if c < 0:
+                raise RuntimeError("reference words failed")
+            return int(c)
+        self.L.dotor_words.restype = ctypes.c_uint
+        self.L.dotor_words.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_size_t, ctypes.c_uint, ctypes.c_void_p, ctypes.c_void_p]
+        return int(self.L.dotor_words(int(sub), P(out), P(a), P(b), a.size, 8, None, None))
+
     def run(self, op, a, b, out, flags):
         """op 0 add, 1 sub, 2 mul on [B, m] numpy uint64 arrays (reference DoT path)."""
         B, m = a.shape
@@ -300,9 +324,10 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs,
         "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64", "data": DATA,
         "config": c2_config(),
+        "sharding": "reference CPU path on rank 0's host (all host threads); other ranks idle",
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
                          "sample": f"full C2 step (add+sub, 4 sizes) x {args.steps} steps; route {cpu.note}"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -401,8 +426,73 @@ def timed_steps(torch, dist, world, stream, calls, steps, warmup):
     return total_ms / steps, per_call
 
 
+L2_BYTES = 126 * 1000 * 1000  # B200 L2 (126 MB): inputs per timed step must exceed it
+
+
+def rank_slice(B, rank, world):
+    """Contiguous pair range [lo, hi) of the named batch that `rank` processes (strong
+    scaling: the batch partitioned into G contiguous slices)."""
+    return B * rank // world, B * (rank + 1) // world
+
+
+def rotations(input_bytes):
+    """How many distinct copies of a per-rank input set to rotate through so that the
+    bytes read between two uses of the same copy exceed the L2 (timing rule: inputs
+    larger than L2 between timed iterations)."""
+    return max(1, -(-2 * L2_BYTES // max(1, input_bytes)))
+
+
+def make_rotating(fns):
+    """One zero-arg callable that runs fns[0], fns[1], ... in turn (one per step)."""
+    state = {"i": 0}
+
+    def call():
+        f = fns[state["i"] % len(fns)]
+        state["i"] += 1
+        return f()
+
+    return call
+
+
+def capture_graph(torch, dg, lib, stream, make_call):
+    """Capture make_call(launcher)() once into a CUDA graph; returns (replay_fn,
+    kernels per replay) or (None, None) when capture is unavailable."""
+    try:
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        call = make_call(Launcher(torch, lib, cap))
+        with torch.cuda.stream(cap):
+            assert call() == 0
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = dg.kernel_launches()
+        with torch.cuda.graph(graph, stream=cap):
+            call()
+        nk = dg.kernel_launches() - n0
+        torch.cuda.synchronize()
+        return (lambda: (graph.replay(), 0)[1]), nk, graph
+    except Exception as e:  # noqa: BLE001
+        print(f"graph capture unavailable ({e}); direct launches", file=sys.stderr)
+        return None, None, None
+
+
+def hbm_roofline(alg_bytes, launch_s, peak, kernel, peak_kind="measured (MEASURED_PEAKS.json hbm_gbs)",
+                 traffic=None, **extra):
+    achieved = alg_bytes / launch_s / 1e9
+    r = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+         "traffic": traffic, "kernel": kernel, "algorithmic_bytes_per_launch": alg_bytes,
+         "launch_us_avg": launch_s * 1e6, "peak_kind": peak_kind}
+    r.update(extra)
+    return r
+
+
+def pinned_like(torch, t):
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h
+
+
 def run_ours(args, rank, world, dist):
-    import numpy as np
     import torch
 
     import paper_2604_21566_b200 as dg
@@ -410,19 +500,15 @@ def run_ours(args, rank, world, dist):
 
     lib = dg.lib()  # raises if libdotg.so is missing: no fallback
     torch.cuda.set_device(device_index())
+    hbm_peak, peak_kind, sm_max = peaks()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    stream = torch.cuda.current_stream()
+    L = Launcher(torch, lib, stream)
     if args.only:
-        stream = torch.cuda.current_stream()
-        hbm_peak, _, sm_max = peaks()
-        sms = torch.cuda.get_device_properties(0).multi_processor_count
-        res = run_secondary(args, torch, dg, W, Launcher(torch, lib, stream), stream, world, dist, hbm_peak,
-                            sm_max, sms)
+        res = run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm_max, sms)
         if rank == 0:
             print(json.dumps({"only": args.only, "configs": res}), flush=True)
         return 0
-    stream = torch.cuda.current_stream()
-    L = Launcher(torch, lib, stream)
-    hbm_peak, peak_kind, sm_max = peaks()
-    sms = torch.cuda.get_device_properties(0).multi_processor_count
 
     # ---- headline: C2 sweep, device-resident ----
     bufs = []
@@ -434,38 +520,47 @@ def run_ours(args, rank, world, dist):
     probs = [(False, x["oa"], x["a"], x["b"], x["fa"], x["m"], x["B"]) for x in bufs]
     probs += [(True, x["os"], x["sa"], x["sb"], x["fs"], x["m"], x["B"]) for x in bufs]
     call_bytes = [x["B"] * (24 * x["m"] + 4) for x in bufs] * 2
-    step_bytes = sum(call_bytes)
-    # per-problem launches (event-bracketed breakdown, and --ungrouped timing)
-    single_calls = [L.addsub(*q) for q in probs]
-    if args.ungrouped:
-        calls = single_calls
-    else:
-        calls = [L.grouped(probs)]  # the whole sweep = one persistent launch
-    # The step as a CUDA graph (one replay per step): same kernel, same bytes, without the
-    # host launch path between consecutive steps. --no-graph keeps direct launches.
+    full_step_bytes = sum(call_bytes)
+    assert full_step_bytes == c2_bytes()
+
+    # This rank's share of every batch (strong scaling: the named batches split into G
+    # contiguous slices, no collective). At N = 1 the slice is the whole batch. With small
+    # slices several copies rotate so every step still reads more than the L2.
+    def slice_probs(copy):
+        out = []
+        for (sub, o, a_, b_, f, m, B), x in zip(probs, bufs * 2):
+            lo, hi = rank_slice(B, rank, world)
+            if copy == 0:
+                out.append((sub, o[lo:hi], a_[lo:hi], b_[lo:hi], f[lo:hi], m, hi - lo))
+            else:
+                out.append((sub, torch.empty_like(o[lo:hi]), a_[lo:hi].clone(), b_[lo:hi].clone(),
+                            torch.empty_like(f[lo:hi]), m, hi - lo))
+        return out
+
+    my_pairs = [rank_slice(B, rank, world) for m, B in C2_SIZES]
+    my_bytes = sum(2 * (hi - lo) * (24 * m + 4) for (m, B), (lo, hi) in zip(C2_SIZES, my_pairs))
+    my_inputs = sum(2 * 2 * (hi - lo) * m * 8 for (m, B), (lo, hi) in zip(C2_SIZES, my_pairs))
+    nrot = rotations(my_inputs) if world > 1 else 1
+    sets = [slice_probs(i) for i in range(nrot)]
+    single_calls = [L.addsub(*q) for q in sets[0]]
     graph_launches = None
-    if not args.ungrouped and not args.no_graph:
-        try:
-            cap = torch.cuda.Stream()
-            cap.wait_stream(stream)
-            Lc = Launcher(torch, lib, cap)
-            cap_call = Lc.grouped(probs)
-            with torch.cuda.stream(cap):
-                assert cap_call() == 0
-            torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            n0 = dg.kernel_launches()
-            with torch.cuda.graph(graph, stream=cap):
-                cap_call()
-            graph_launches = dg.kernel_launches() - n0
-            torch.cuda.synchronize()
-            calls = [lambda: (graph.replay(), 0)[1]]
-        except Exception as e:  # noqa: BLE001
-            graph_launches = None
-            print(f"graph capture unavailable ({e}); direct launches", file=sys.stderr)
-    calls_meta = list(range(len(calls)))
-    assert step_bytes == c2_bytes()
-    working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per step (a, b, sa, sb)
+    graphs = []
+    if args.ungrouped:
+        calls = [make_rotating([(lambda ps=ps: [L.addsub(*q)() for q in ps][-1]) for ps in sets])]
+    elif args.no_graph:
+        calls = [make_rotating([L.grouped(ps) for ps in sets])]
+    else:
+        replays = []
+        for ps in sets:
+            fn, nk, g = capture_graph(torch, dg, lib, stream, lambda Lc, ps=ps: Lc.grouped(ps))
+            if fn is None:
+                replays = None
+                break
+            replays.append(fn)
+            graphs.append(g)
+            graph_launches = nk
+        calls = [make_rotating(replays)] if replays else [make_rotating([L.grouped(ps) for ps in sets])]
+    working_set = sum(4 * x["a"].numel() * 8 for x in bufs)  # distinct inputs read per full step (a, b, sa, sb)
 
     sampler = ClockSampler(device_index())
     sampler.start()
@@ -479,23 +574,36 @@ def run_ours(args, rank, world, dist):
     if graph_launches is not None:
         launches = graph_launches * args.steps
     clocks = sampler.stop()
-    value = step_bytes * world / (ms_step * 1e-3) / 1e9
-    # average launch duration of the batched add/sub kernel = lean-loop step time / launches
-    # (inter-launch gaps included: conservative); per_size uses event-bracketed launches.
-    achieved = step_bytes / (ms_step * 1e-3) / 1e9
+    # value = the whole named sweep (all ranks' slices together) / max-over-ranks step time
+    value = full_step_bytes / (ms_step * 1e-3) / 1e9
+    achieved = my_bytes / (ms_step * 1e-3) / 1e9  # this rank's kernel: its bytes per launch / launch time
+    weak = None
+    if world > 1:
+        # weak scaling (extra key): every rank runs the FULL sweep on its own GPU
+        fn, nk, g = capture_graph(torch, dg, lib, stream, lambda Lc: Lc.grouped(probs))
+        graphs.append(g)
+        wcalls = [fn] if fn is not None else [L.grouped(probs)]
+        wms, _ = timed_steps(torch, dist, world, stream, wcalls, args.steps, args.warmup)
+        weak = {"value": full_step_bytes * world / (wms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": wms,
+                "per_rank": "the full C2 sweep on every rank (no collective)"}
     _, per_single = timed_steps(torch, None, 1, stream, single_calls, max(3, args.steps // 4), 2)
-    per_size = {f"m{x['m']}": {"add_gbs": call_bytes[i] / (per_single[i] * 1e-3) / 1e9,
-                               "sub_gbs": call_bytes[i] / (per_single[i + 4] * 1e-3) / 1e9}
-                for i, x in enumerate(bufs)}
+    per_size = {}
+    for i, x in enumerate(bufs):
+        lo, hi = my_pairs[i]
+        bts = (hi - lo) * (24 * x["m"] + 4)
+        per_size[f"m{x['m']}"] = {"add_gbs": bts / (per_single[i] * 1e-3) / 1e9,
+                                  "sub_gbs": bts / (per_single[i + 4] * 1e-3) / 1e9,
+                                  "add_us": per_single[i] * 1e3, "sub_us": per_single[i + 4] * 1e3,
+                                  "add_frac": bts / (per_single[i] * 1e-3) / 1e9 / hbm_peak,
+                                  "sub_frac": bts / (per_single[i + 4] * 1e-3) / 1e9 / hbm_peak,
+                                  "note": "one dotg_add_batch / dotg_sub_batch launch of this size alone"}
     traffic = traffic_table().get("C2_per_launch_bytes_grouped" if not args.ungrouped else "C2_per_launch_bytes")
     # the same byte mix without carries: a plain 2-read / 1-write streaming add measured
     # live (tools/stream_peak.cu) - the practical ceiling for this kernel's traffic
     mix_peak = None
     sp = os.path.join(ROOT, "tools", "build", "stream_peak")
-    if os.path.exists(sp) and rank == 0:
+    if os.path.exists(sp) and rank == 0 and world == 1:
         try:
-            import subprocess
-
             r = subprocess.run([sp], capture_output=True, text=True, timeout=120)
             probe = json.loads(r.stdout)
             mix_peak = {"GBps": probe["add_2r1w"]["GBps"], "frac": achieved / probe["add_2r1w"]["GBps"],
@@ -506,37 +614,34 @@ def run_ours(args, rank, world, dist):
     # stress level of the sweep: AddSubStats counters of the reference's
     # w8 chunking, derived on the device from the step's own inputs and outputs
     stress = {}
-    ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
-    for x in bufs:
-        row = {}
-        for sub, o, a_, b_ in ((0, x["oa"], x["a"], x["b"]), (1, x["os"], x["sa"], x["sb"])):
-            ctr.zero_()
-            rc = lib.dotg_addsub_stats(sub, ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a_.data_ptr()),
-                                       ctypes.c_void_p(b_.data_ptr()), x["m"], x["B"], 0, 8,
-                                       ctypes.c_void_p(ctr.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
-            if rc == 0:
-                c = ctr.cpu().tolist()
-                row["sub" if sub else "add"] = {"chunks": c[0], "phase4_triggers": c[1],
-                                                "phase4_fraction": c[1] / max(1, c[0])}
-        stress[f"m{x['m']}"] = row
+    if world == 1:
+        ctr = torch.zeros(2, dtype=torch.int64, device="cuda")
+        for x in bufs:
+            row = {}
+            for sub, o, a_, b_ in ((0, x["oa"], x["a"], x["b"]), (1, x["os"], x["sa"], x["sb"])):
+                ctr.zero_()
+                rc = lib.dotg_addsub_stats(sub, ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a_.data_ptr()),
+                                           ctypes.c_void_p(b_.data_ptr()), x["m"], x["B"], 0, 8,
+                                           ctypes.c_void_p(ctr.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+                if rc == 0:
+                    c = ctr.cpu().tolist()
+                    row["sub" if sub else "add"] = {"chunks": c[0], "phase4_triggers": c[1],
+                                                    "phase4_fraction": c[1] / max(1, c[0])}
+            stress[f"m{x['m']}"] = row
 
-    # ---- e2e: the same step through the host-buffer C ABI (pinned host arrays) ----
+    # ---- e2e: this rank's share through the host-buffer C ABI (pinned host arrays) ----
     e2e = None
     if not args.no_e2e:
-        hsets = []
-        for x in bufs:
-            hs = {}
-            for k in ("a", "b", "sa", "sb"):
-                h = torch.empty(x[k].shape, dtype=torch.int64, pin_memory=True)
-                h.copy_(x[k])
-                hs[k] = h
-            hs["o"] = torch.empty(x["a"].shape, dtype=torch.int64, pin_memory=True)
-            hs["os"] = torch.empty(x["a"].shape, dtype=torch.int64, pin_memory=True)
-            hs["f"] = torch.empty(x["B"], dtype=torch.int32, pin_memory=True)
-            hs["fs"] = torch.empty(x["B"], dtype=torch.int32, pin_memory=True)
-            hsets.append((x["m"], x["B"], hs))
         from paper_2604_21566_b200._lib import AddSubProblem
 
+        hsets = []
+        for x, (lo, hi) in zip(bufs, my_pairs):
+            hs = {k: pinned_like(torch, x[k][lo:hi]) for k in ("a", "b", "sa", "sb")}
+            hs["o"] = torch.empty(hs["a"].shape, dtype=torch.int64, pin_memory=True)
+            hs["os"] = torch.empty(hs["a"].shape, dtype=torch.int64, pin_memory=True)
+            hs["f"] = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+            hs["fs"] = torch.empty(hi - lo, dtype=torch.int32, pin_memory=True)
+            hsets.append((x["m"], hi - lo, hs))
         hprobs = (AddSubProblem * 8)()
         for i, (m, B, hs) in enumerate(hsets):
             hprobs[i] = AddSubProblem(0, 0, hs["o"].data_ptr(), hs["a"].data_ptr(), hs["b"].data_ptr(),
@@ -549,10 +654,11 @@ def run_ours(args, rank, world, dist):
             assert rc == 0, lib.dotg_last_error()
 
         e2e_step()
-        # correctness spot check of the e2e path against the device result (last call = sub m=256)
-        m, B, hs = hsets[-1]
-        assert torch.equal(hs["os"], bufs[-1]["os"].cpu()), "e2e result mismatch"
-        assert torch.equal(hsets[0][2]["o"], bufs[0]["oa"].cpu()), "e2e result mismatch"
+        # correctness spot check of the e2e path against the device result
+        lo, hi = my_pairs[-1]
+        assert torch.equal(hsets[-1][2]["os"], bufs[-1]["os"][lo:hi].cpu()), "e2e result mismatch"
+        lo, hi = my_pairs[0]
+        assert torch.equal(hsets[0][2]["o"], bufs[0]["oa"][lo:hi].cpu()), "e2e result mismatch"
         e_steps = max(3, min(args.steps, 20))
         if world > 1:
             dist.barrier()
@@ -562,12 +668,14 @@ def run_ours(args, rank, world, dist):
         dt = time.perf_counter() - t0
         if world > 1:
             dt = reduce_scalar(dist, dt, "max")
-        h2d = sum(2 * 2 * B * m * 8 for m, B in C2_SIZES)
-        d2h = sum(2 * (B * m * 8 + 4 * B) for m, B in C2_SIZES)
-        e2e = {"value": step_bytes * world * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+        h2d = sum(2 * 2 * B * m * 8 for m, B, _ in hsets)
+        d2h = sum(2 * (B * m * 8 + 4 * B) for m, B, _ in hsets)
+        e2e = {"value": full_step_bytes * e_steps / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": e_steps,
                "api": "dotg_addsub_grouped_host: the 8 host problems through one H2D / kernel / D2H stream "
-                      "pipeline (pinned host buffers)"}
+                      "pipeline (pinned host buffers)",
+               "bound": "PCIe: one integer op per byte moved; the kernel-only path runs ~85x faster than the "
+                        "link can feed it"}
         # the PCIe ceiling of this step: the same bytes moved with no kernels at all
         # (uploads on one stream, downloads concurrently on another, 24 MB chunks)
         try:
@@ -591,7 +699,7 @@ def run_ours(args, rank, world, dist):
             for _ in range(5):
                 xfer()
             tx = (time.perf_counter() - t0) / 5
-            e2e["transfer_only_GBps"] = step_bytes / tx / 1e9
+            e2e["transfer_only_GBps"] = my_bytes / tx / 1e9
             e2e["frac_of_transfer_only"] = e2e["value"] / world / e2e["transfer_only_GBps"]
             del xa, xb, ya, yb
         except Exception as ex:  # noqa: BLE001
@@ -604,35 +712,40 @@ def run_ours(args, rank, world, dist):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cpu = CpuRef()
-            sets = host_c2_inputs()
-            gbs, reps, dt = cpu_c2_measure(cpu, sets, min_seconds=args.cpu_seconds)
+            hsets_cpu = host_c2_inputs()
+            gbs, reps, dt = cpu_c2_measure(cpu, hsets_cpu, min_seconds=args.cpu_seconds)
             cpu_baseline = {"value": gbs, "unit": "GB/s", "cores": cpu.threads, "kind": cpu.kind,
                             "sample": f"full C2 step (add+sub at 4 sizes, {c2_bytes() / 1e6:.0f} MB) x {reps} reps "
                                       f"({dt:.1f} s), span-form dot_add_words/dot_sub_words route {cpu.note}"}
-            del sets
+            del hsets_cpu
         except Exception as e:  # noqa: BLE001
             cpu_baseline = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
 
     # free the headline buffers before the secondary configs
-    del bufs, calls, single_calls
+    del bufs, calls, single_calls, sets, graphs
+    torch.cuda.synchronize()
     torch.cuda.empty_cache()
 
     secondary = {}
     if not args.no_secondary:
-        secondary = run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms, rank == 0)
+        secondary = run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm_max, sms)
 
     line = {
         "metric": METRIC,
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": DATA,
-        "config": c2_config(args.ungrouped, working_set),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
-                     "algorithmic_bytes_per_launch": step_bytes / len(calls_meta),
-                     "launch_us_avg": ms_step * 1e3 / len(calls_meta), "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                     "per_size": per_size, "mix_peak": mix_peak},
+        "config": c2_config(args.ungrouped),
+        "sharding": (f"rank r of {world} runs pairs [B*r/{world}, B*(r+1)/{world}) of every C2 batch (contiguous "
+                     "slices, no collective on the data path); value = the whole named sweep / max-over-ranks step "
+                     f"time; {nrot} rotating copies of each rank's slice keep > L2 bytes per step"
+                     if world > 1 else "one GPU runs the whole named sweep"),
+        "roofline": hbm_roofline(my_bytes, ms_step * 1e-3, hbm_peak,
+                                 "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
+                                 peak_kind=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", traffic=traffic,
+                                 per_size=per_size, mix_peak=mix_peak,
+                                 note="achieved = this rank's algorithmic bytes per step launch / the launch's "
+                                      "CUDA-event time on the launching stream (one launch per step)"),
         "cpu_baseline": cpu_baseline,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -642,129 +755,251 @@ def run_ours(args, rank, world, dist):
         "carry_stress": stress,
         "configs": secondary,
     }
+    if weak is not None:
+        line["weak_scaling"] = weak
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
 
 
-def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, sms, rank0=True):
+def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm_max, sms):
+    import numpy as np
+
     out = {}
     steps = max(3, min(args.steps, 50))
     warm = max(3, args.warmup)
     dd = dist if world > 1 else None
+    lib = dg.lib()
+    rank0 = rank == 0
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def want(k):
         return not args.only or k in args.only.split(",")
 
-    # C1: 4096-bit add + sub (rotate 3 input sets -> 300 MB between reuses > L2)
-    sets = []
-    for r in range(3 if want("C1") else 0):
-        a = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 0).view(-1, 64)
-        b = W.fill(W.C1["batch"] * 64, 0xC1 + 17 * r, 1 << 40).view(-1, 64)
-        sa, sb = W.swap_for_sub(a, b)
-        sets.append((a, b, sa, sb, torch.empty_like(a), torch.empty(a.shape[0], dtype=torch.int32, device="cuda")))
-    B = W.C1["batch"]
-    calls = []
-    if not want("C1"):
-        sets = []
-    outs2 = []
-    for a, b, sa, sb, o, f in sets:
-        # add and sub of one set: one grouped launch (two problems, separate outputs)
-        o2, f2 = torch.empty_like(o), torch.empty_like(f)
-        outs2.append((o2, f2))
-        calls.append(L.grouped([(False, o, a, b, f, 64, B), (True, o2, sa, sb, f2, 64, B)]))
-    if sets:
-        ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
-    byts = B * (24 * 64 + 4)
-    if sets:
-        nops = 2 * len(calls)
-        out["C1"] = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": byts * nops * world / (ms * 1e-3) / 1e9,
-                     "unit": "GB/s", "kernel_gbs": byts * nops / (sum(per) * 1e-3) / 1e9,
-                     "frac_hbm": byts * nops / (sum(per) * 1e-3) / 1e9 / hbm_peak,
-                     "frac_hbm_back_to_back": byts * nops / (ms * 1e-3) / 1e9 / hbm_peak,
-                     "launch_us": statistics.mean(per) * 1e3,
-                     "step": "3 rotating input sets (300 MB apart > L2); per set add + sub in one dotg_addsub_grouped "
-                             "launch"}
-    del outs2
-    del sets, calls
-    torch.cuda.empty_cache()
+    def host_u64(t):
+        return t.cpu().numpy().view(np.uint64)
 
+    # ---------------- C1: 4096-bit add + sub, B = 65536 ----------------
+    if want("C1"):
+        B, m = W.C1["batch"], 64
+        lo, hi = rank_slice(B, rank, world)
+        nb = hi - lo
+        byts = nb * (24 * m + 4)  # one op over this rank's slice
+        # 3 rotating input sets (>= 2 x L2 of inputs between reuses of a set)
+        nset = max(3, rotations(2 * 2 * nb * m * 8))
+        sets = []
+        for r in range(nset):
+            a = W.fill(B * m, 0xC1 + 17 * r, 0).view(-1, m)[lo:hi].clone()
+            b = W.fill(B * m, 0xC1 + 17 * r, 1 << 40).view(-1, m)[lo:hi].clone()
+            sa, sb = W.swap_for_sub(a, b)
+            sets.append(dict(a=a, b=b, sa=sa, sb=sb, o=torch.empty_like(a), o2=torch.empty_like(a),
+                             f=torch.empty(nb, dtype=torch.int32, device="cuda"),
+                             f2=torch.empty(nb, dtype=torch.int32, device="cuda")))
+        calls = [L.grouped([(False, x["o"], x["a"], x["b"], x["f"], m, nb), (True, x["o2"], x["sa"], x["sb"], x["f2"],
+                                                                             m, nb)]) for x in sets]
+        ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
+        x0 = sets[0]
+        singles = [L.addsub(False, x0["o"], x0["a"], x0["b"], x0["f"], m, nb),
+                   L.addsub(True, x0["o2"], x0["sa"], x0["sb"], x0["f2"], m, nb)]
+        _, per1 = timed_steps(torch, None, 1, stream, singles, steps, warm)
+        launch_s = statistics.mean(per) * 1e-3
+        c1 = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": B * (24 * m + 4) * 2 * len(calls) / (ms * 1e-3)
+              / 1e9, "unit": "GB/s",
+              "step": f"{len(calls)} rotating input sets; per set add + sub in one dotg_addsub_grouped launch",
+              "roofline": hbm_roofline(2 * byts, launch_s, hbm_peak,
+                                       "k_addsub_grouped (add + sub of one C1 set, 2 problems, one launch)",
+                                       single_launch={"add_gbs": byts / (per1[0] * 1e-3) / 1e9,
+                                                      "sub_gbs": byts / (per1[1] * 1e-3) / 1e9,
+                                                      "add_frac": byts / (per1[0] * 1e-3) / 1e9 / hbm_peak,
+                                                      "sub_frac": byts / (per1[1] * 1e-3) / 1e9 / hbm_peak,
+                                                      "add_us": per1[0] * 1e3, "sub_us": per1[1] * 1e3}),
+              "frac_hbm_back_to_back": 2 * byts * len(calls) / (ms * 1e-3) / 1e9 / hbm_peak}
+        if not args.no_e2e:
+            from paper_2604_21566_b200._lib import AddSubProblem
+
+            hs = {k: pinned_like(torch, x0[k]) for k in ("a", "b", "sa", "sb")}
+            ho = torch.empty_like(hs["a"], pin_memory=True)
+            ho2 = torch.empty_like(hs["a"], pin_memory=True)
+            hf = torch.empty(nb, dtype=torch.int32, pin_memory=True)
+            hf2 = torch.empty(nb, dtype=torch.int32, pin_memory=True)
+            hp = (AddSubProblem * 2)()
+            hp[0] = AddSubProblem(0, 0, ho.data_ptr(), hs["a"].data_ptr(), hs["b"].data_ptr(), hf.data_ptr(), m, nb)
+            hp[1] = AddSubProblem(1, 0, ho2.data_ptr(), hs["sa"].data_ptr(), hs["sb"].data_ptr(), hf2.data_ptr(), m,
+                                  nb)
+            assert lib.dotg_addsub_grouped_host(hp, 2) == 0, lib.dotg_last_error()
+            torch.cuda.synchronize()
+            assert torch.equal(ho, x0["o"].cpu()) and torch.equal(ho2, x0["o2"].cpu()), "C1 e2e mismatch"
+            reps = 10
+            if dd is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                lib.dotg_addsub_grouped_host(hp, 2)
+            dt = (time.perf_counter() - t0) / reps
+            if dd is not None:
+                dt = reduce_scalar(dist, dt, "max")
+            c1["e2e"] = {"value": B * (24 * m + 4) * 2 / dt / 1e9, "unit": "GB/s",
+                         "h2d_bytes_per_step": 4 * nb * m * 8, "d2h_bytes_per_step": 2 * (nb * m * 8 + 4 * nb),
+                         "api": "dotg_addsub_grouped_host (add + sub of the whole batch, pinned host buffers)"}
+            if rank0 and world == 1 and not args.no_cpu:
+                try:
+                    cpu = CpuRef()
+                    ha, hb = hs["a"].numpy().view(np.uint64), hs["b"].numpy().view(np.uint64)
+                    hsa, hsb = hs["sa"].numpy().view(np.uint64), hs["sb"].numpy().view(np.uint64)
+                    co, cf = np.empty_like(ha), np.empty(nb, np.uint32)
+                    co2, cf2 = np.empty_like(ha), np.empty(nb, np.uint32)
+                    cpu.run(0, ha, hb, co, cf)
+                    cpu.run(1, hsa, hsb, co2, cf2)
+                    assert np.array_equal(co, ho.numpy().view(np.uint64)) and np.array_equal(
+                        co2, ho2.numpy().view(np.uint64)), "C1 cpu/gpu mismatch"
+                    assert np.array_equal(cf, hf.numpy().view(np.uint32)) and np.array_equal(
+                        cf2, hf2.numpy().view(np.uint32)), "C1 cpu/gpu flag mismatch"
+                    reps, t0 = 0, time.perf_counter()
+                    while True:
+                        cpu.run(0, ha, hb, co, cf)
+                        cpu.run(1, hsa, hsb, co2, cf2)
+                        reps += 1
+                        if time.perf_counter() - t0 >= 2.0:
+                            break
+                    cdt = (time.perf_counter() - t0) / reps
+                    c1["cpu_baseline"] = {"value": 2 * byts / cdt / 1e9, "unit": "GB/s", "cores": cpu.threads,
+                                          "kind": cpu.kind,
+                                          "sample": f"all {nb} pairs, add + sub (span-form dot_add_words / "
+                                                    f"dot_sub_words, route {cpu.note}) x {reps} reps; results "
+                                                    "bit-identical to the GPU's"}
+                except Exception as e:  # noqa: BLE001
+                    c1["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:200]}
+            del hs, ho, ho2
+        out["C1"] = c1
+        del sets, calls, singles
+        torch.cuda.empty_cache()
+
+    # ---------------- C3 / C4: batched multiply ----------------
     imad_peak_pps = sms * IMAD_WIDE_PER_CLK_SM * sm_max * 1e6  # u32 products / s at max clock
     for name, gen, m in (("C3", W.c3_inputs, 16), ("C4", W.c4_inputs, 64)):
         if not want(name):
             continue
-        a, b = gen()
-        Bn = a.shape[0]
-        o = torch.empty((Bn, 2 * m), dtype=torch.int64, device="cuda")
-        calls = [L.mul(o, a, b, m, Bn)]
+        fa, fb = gen()
+        Bn = fa.shape[0]
+        lo, hi = rank_slice(Bn, rank, world)
+        nb = hi - lo
+        nrot = rotations(2 * nb * m * 8) if world > 1 else 1
+        rot = [(fa[lo:hi].clone(), fb[lo:hi].clone()) for _ in range(nrot)] if world > 1 else [(fa, fb)]
+        outs = [torch.empty((nb, 2 * m), dtype=torch.int64, device="cuda") for _ in rot]
+        calls = [make_rotating([L.mul(o, a_, b_, m, nb) for o, (a_, b_) in zip(outs, rot)])]
         ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
-        pairs_s = Bn / (per[0] * 1e-3)
+        pairs_s = nb / (per[0] * 1e-3)
         prods = 4 * m * m
-        out[name] = {"metric": f"{64 * m}-bit mul products/s (pairs/s)", "value": Bn * world / (ms * 1e-3),
-                     "unit": "pairs/s", "kernel_pairs_s": pairs_s, "kernel_us": per[0] * 1e3,
-                     "u32_products_per_s": pairs_s * prods,
-                     "imad_roofline_u32_products_per_s": imad_peak_pps,
-                     "frac_imad": pairs_s * prods / imad_peak_pps,
-                     "hbm_gbs": Bn * 32 * m / (per[0] * 1e-3) / 1e9,
-                     "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
+        o, (a, b) = outs[0], rot[0]
+        res = {"metric": f"{64 * m}-bit mul products/s (pairs/s)", "value": Bn / (ms * 1e-3),
+               "unit": "pairs/s", "kernel_pairs_s": pairs_s, "kernel_us": per[0] * 1e3,
+               "u32_products_per_s": pairs_s * prods,
+               "imad_roofline_u32_products_per_s": imad_peak_pps,
+               "frac_imad": pairs_s * prods / imad_peak_pps,
+               "hbm_gbs": nb * 32 * m / (per[0] * 1e-3) / 1e9,
+               "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
+        roof = {"bound": "imad", "achieved": pairs_s * prods / 1e12, "peak": imad_peak_pps / 1e12,
+                "unit": "T u32-products/s", "frac": pairs_s * prods / imad_peak_pps, "traffic": None,
+                "algorithmic_units_per_launch": f"{nb} pairs x {prods} u32 products", "launch_us_avg": per[0] * 1e3}
         if m in IMMA_ROUTE_M:
             # tensor-pipe kernel (k_mul_imma): radix-2^8 products, (8m)^2 byte-MACs per pair
             imma_peak = sms * IMMA_U8_MACS_PER_CLK_SM * sm_max * 1e6
-            out[name].update({"pipe": "imma (mma.sync m16n8k32 u8, k_mul_imma)",
-                              "u8_macs_per_s": pairs_s * (8 * m) ** 2,
-                              "imma_roofline_u8_macs_per_s": imma_peak,
-                              "frac_imma": pairs_s * (8 * m) ** 2 / imma_peak,
-                              "note": "frac_imad: u32-product equivalents vs the IMAD.WIDE roofline (148 x 32/clk x "
-                                      "max clock); frac_imma: byte MACs vs the measured u8 IMMA rate (148 x 2048/clk "
-                                      "x max clock, tools/imma_peak.cu)"})
+            res.update({"pipe": "imma (mma.sync m16n8k32 u8, k_mul_imma)",
+                        "u8_macs_per_s": pairs_s * (8 * m) ** 2,
+                        "imma_roofline_u8_macs_per_s": imma_peak,
+                        "frac_imma": pairs_s * (8 * m) ** 2 / imma_peak,
+                        "note": "frac_imad: u32-product equivalents vs the IMAD.WIDE roofline (148 x 32/clk x "
+                                "max clock); frac_imma: byte MACs vs the measured u8 IMMA rate (148 x 2048/clk "
+                                "x max clock, tools/imma_peak.cu)"})
+            roof["kernel"] = "k_mul_imma<16> (mma.sync u8 column sums)"
         else:
-            out[name]["pipe"] = "imad (IMAD.WIDE.U32 96-bit column MAC)"
+            res["pipe"] = "imad (IMAD.WIDE.U32 96-bit column MAC)"
+            roof["kernel"] = "k_mul_kara16 (IMAD.WIDE.U32 columns, one in-register Karatsuba level)"
+        res["roofline"] = roof
         if not args.no_e2e:
             # e2e: pinned host arrays through dotg_mul_batch_host (copies inside the timed region)
-            ha = torch.empty(a.shape, dtype=torch.int64, pin_memory=True)
-            hb = torch.empty(b.shape, dtype=torch.int64, pin_memory=True)
+            ha, hb = pinned_like(torch, a), pinned_like(torch, b)
             ho = torch.empty(o.shape, dtype=torch.int64, pin_memory=True)
-            ha.copy_(a)
-            hb.copy_(b)
-            lib = dg.lib()
-            P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-            assert lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, Bn) == 0
+            assert lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, nb) == 0
+            torch.cuda.synchronize()
             assert torch.equal(ho, o.cpu()), "mul e2e mismatch"
             reps = 5
+            if dd is not None:
+                dist.barrier()
             t0 = time.perf_counter()
             for _ in range(reps):
-                lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, Bn)
+                lib.dotg_mul_batch_host(P(ho), P(ha), P(hb), m, nb)
             dt = (time.perf_counter() - t0) / reps
-            out[name]["e2e"] = {"value": Bn * world / dt, "unit": "pairs/s", "h2d_bytes_per_step": 2 * Bn * m * 8,
-                                "d2h_bytes_per_step": Bn * 2 * m * 8, "api": "dotg_mul_batch_host"}
+            if dd is not None:
+                dt = reduce_scalar(dist, dt, "max")
+            res["e2e"] = {"value": Bn / dt, "unit": "pairs/s", "h2d_bytes_per_step": 2 * nb * m * 8,
+                          "d2h_bytes_per_step": nb * 2 * m * 8, "api": "dotg_mul_batch_host"}
             if rank0 and world == 1 and not args.no_cpu:
                 try:
                     cpu = CpuRef()
-                    import numpy as np
-
                     nsamp = Bn // 16
-                    sa_ = ha[:nsamp].numpy().view(np.uint64)
-                    sb_ = hb[:nsamp].numpy().view(np.uint64)
+                    if name == "C4":  # half random, half all-ones pairs, as in the config
+                        idx = np.concatenate([np.arange(nsamp // 2), np.arange(Bn // 2, Bn // 2 + nsamp // 2)])
+                    else:
+                        idx = np.arange(nsamp)
+                    sa_ = np.ascontiguousarray(ha.numpy().view(np.uint64)[idx])
+                    sb_ = np.ascontiguousarray(hb.numpy().view(np.uint64)[idx])
                     so_ = np.empty((nsamp, 2 * m), np.uint64)
                     cpu.run(2, sa_, sb_, so_, None)  # warm
                     t0 = time.perf_counter()
                     cpu.run(2, sa_, sb_, so_, None)
                     cdt = time.perf_counter() - t0
-                    assert np.array_equal(so_, ho[:nsamp].numpy().view(np.uint64)), "cpu/gpu mismatch"
-                    out[name]["cpu_baseline"] = {"value": nsamp / cdt, "unit": "pairs/s", "cores": cpu.threads,
-                                                 "kind": cpu.kind,
-                                                 "sample": f"{nsamp} pairs of the same batch, dot_mul_words"}
+                    assert np.array_equal(so_, ho.numpy().view(np.uint64)[idx]), "cpu/gpu mismatch"
+                    res["cpu_baseline"] = {"value": nsamp / cdt, "unit": "pairs/s", "cores": cpu.threads,
+                                           "kind": cpu.kind,
+                                           "sample": f"{nsamp} pairs of the same batch"
+                                                     f"{' (half random, half all-ones)' if name == 'C4' else ''}, "
+                                                     "dot_mul_words; results bit-identical to the GPU's"}
                 except Exception as e:  # noqa: BLE001
-                    out[name]["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)}
+                    res["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:200]}
             del ha, hb, ho
-        del a, b, o, calls
+        out[name] = res
+        del fa, fb, rot, outs, calls, a, b, o
         torch.cuda.empty_cache()
 
+    # ---------------- interleaved layout (north star's batch-interleaved subsystem) ----------------
+    if want("IL") and world == 1 and not args.no_layouts:
+        il = {}
+        for m, B in [(64, 1 << 16)] + [(mm, (1 << 22) // mm) for mm in (4, 16, 128, 256, 512)]:
+            a = W.fill(B * m, 0x1A + m, 0).view(m, B)  # [m][batch]
+            b = W.fill(B * m, 0x1A + m, 1 << 40).view(m, B)
+            o, f = torch.empty_like(a), torch.empty(B, dtype=torch.int32, device="cuda")
+            fns = []
+            for sub in (0, 1):
+                fn = lib.dotg_sub_batch if sub else lib.dotg_add_batch
+                args_ = (P(o), P(a), P(b), P(f), m, B, 1, L.stream)
+                fns.append(lambda fn=fn, args_=args_: fn(*args_))
+            _, per = timed_steps(torch, None, 1, stream, fns, steps, warm)
+            byts = B * (24 * m + 4)
+            il[f"m{m}_B{B}"] = {"add_gbs": byts / (per[0] * 1e-3) / 1e9, "sub_gbs": byts / (per[1] * 1e-3) / 1e9,
+                                "add_frac": byts / (per[0] * 1e-3) / 1e9 / hbm_peak,
+                                "sub_frac": byts / (per[1] * 1e-3) / 1e9 / hbm_peak}
+            del a, b, o, f
+        # interleaved multiply at the C3 / C4 shapes
+        for m, B in ((16, 1 << 18), (32, 1 << 17), (64, 1 << 16)):
+            a = W.fill(B * m, 0x1B + m, 0).view(m, B)
+            b = W.fill(B * m, 0x1B + m, 1 << 40).view(m, B)
+            o = torch.empty((2 * m, B), dtype=torch.int64, device="cuda")
+            args_ = (P(o), P(a), P(b), m, B, 1, L.stream)
+            _, per = timed_steps(torch, None, 1, stream, [lambda args_=args_: lib.dotg_mul_batch(*args_)], steps,
+                                 warm)
+            il[f"mul_m{m}_B{B}"] = {"pairs_s": B / (per[0] * 1e-3), "us": per[0] * 1e3,
+                                    "frac_imad": B / (per[0] * 1e-3) * 4 * m * m / imad_peak_pps}
+            del a, b, o
+        out["interleaved"] = {"layout": "[m][batch] (limb i of pair p at i*batch + p)", "per_shape": il,
+                              "peak": hbm_peak}
+        torch.cuda.empty_cache()
+
+    # ---------------- C5: one 2^30-limb add / sub ----------------
     if not args.no_c5 and want("C5"):
-        from paper_2604_21566_b200.sharded import ShardedWords, shard_bounds
+        from paper_2604_21566_b200.sharded import CommShardedWords, ShardedWords, shard_bounds
 
         M5 = W.C5_M
-        rank = dist.get_rank() if world > 1 else 0
         lo, hi = shard_bounds(M5, rank, world)
         n_local = hi - lo
         free = torch.cuda.mem_get_info()[0]
@@ -773,36 +1008,84 @@ def run_secondary(args, torch, dg, W, L, stream, world, dist, hbm_peak, sm_max, 
         if free < 3 * n_local * 8 + (1 << 30):
             out["C5"] = {"skipped": f"needs {3 * n_local * 8 / 2**30:.0f} GiB free per GPU"}
             return out
+        shared = os.environ.get("DOTG_BENCH_SHARED_GPU") == "1"
+        comm = CommShardedWords() if world > 1 and not shared else None
         res = {}
         for sub in (False, True):
             a, b = W.c5_shard_inputs(sub, lo, hi) if world > 1 else W.c5_inputs(sub)
             o = torch.empty_like(a)
             c = torch.empty(1, dtype=torch.int32, device="cuda")
             if world == 1:
-                fn = dg.lib().dotg_sub_words if sub else dg.lib().dotg_add_words
-                args_ = (ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
-                         n_local, ctypes.c_void_p(c.data_ptr()), L.stream)
-                call = lambda: fn(*args_)  # noqa: E731
+                fn = lib.dotg_sub_words if sub else lib.dotg_add_words
+                args_ = (P(o), P(a), P(b), n_local, P(c), L.stream)
+                call = lambda fn=fn, args_=args_: fn(*args_)  # noqa: E731
+                mode = "single GPU: dotg_add_words / dotg_sub_words (tiled local pass, chunk scan, fix-up)"
+            elif comm is not None:
+                def call(sub=sub, a=a, b=b, o=o, c=c):
+                    comm.run(sub, o, a, b, carry=c, stream=stream)
+                    return 0
+                mode = (f"{world} limb-range shards: one dotg_{'sub' if sub else 'add'}_words_sharded call per "
+                        "rank (C++: local pass, 8-byte ncclAllGather, fix-up on one stream)")
             else:
-                # limb-range shards: local pass, 8-byte NCCL all-gather, boundary fix-up
                 sw = ShardedWords()
                 state = sw.state_for(n_local, a.device)
 
-                def call():
+                def call(sub=sub, a=a, b=b, o=o, sw=sw, state=state):
                     sw.run(sub, o, a, b, state=state)
                     return 0
+                mode = f"{world} limb-range shards, gloo exchange (shared-GPU rehearsal)"
             ms, per = timed_steps(torch, dd, world, stream, [call], 3, 2)
-            carry = int(c.item()) if world == 1 else None
-            res["sub" if sub else "add"] = {"ms": ms, "gbs": 24 * M5 / (ms * 1e-3) / 1e9,
-                                            "frac_hbm_per_gpu": 24 * M5 / world / (ms * 1e-3) / 1e9 / hbm_peak,
-                                            "carry": carry}
-            del a, b, o
+            carry = int(c.item()) if world == 1 or comm is not None else None
+            r = {"ms": ms, "gbs": 24 * M5 / (ms * 1e-3) / 1e9,
+                 "frac_hbm_per_gpu": 24 * n_local / (ms * 1e-3) / 1e9 / hbm_peak, "carry": carry, "mode": mode}
+            r["roofline"] = hbm_roofline(24 * n_local, per[0] * 1e-3, hbm_peak,
+                                         "k_long_local + k_long_scan_chunks + k_long_shard_agg + k_long_finish "
+                                         "(one long add/sub; k_long_local carries ~90% of the time)")
+            if world == 1 and not args.no_e2e and rank0:
+                # e2e through the host span form on pinned 8 GiB host arrays, and the
+                # reference's span-form dot_add_words on the same host arrays (1 thread)
+                ha, hb = pinned_like(torch, a), pinned_like(torch, b)
+                del a, b, o
+                torch.cuda.empty_cache()
+                ho = torch.empty(ha.shape, dtype=torch.int64, pin_memory=True)
+                hfn = lib.dotg_sub_words_host if sub else lib.dotg_add_words_host
+                hc = ctypes.c_uint32(0)
+                assert hfn(P(ho), P(ha), P(hb), M5, ctypes.byref(hc)) == 0, lib.dotg_last_error()
+                assert hc.value == carry, "C5 e2e carry mismatch"
+                reps = 2
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    hfn(P(ho), P(ha), P(hb), M5, ctypes.byref(hc))
+                dt = (time.perf_counter() - t0) / reps
+                r["e2e"] = {"value": 24 * M5 / dt / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 * M5,
+                            "d2h_bytes_per_step": 8 * M5 + 4,
+                            "api": f"dotg_{'sub' if sub else 'add'}_words_host (pinned 8 GiB host operands)"}
+                if not args.no_cpu:
+                    try:
+                        cpu = CpuRef()
+                        hav, hbv = ha.numpy().view(np.uint64), hb.numpy().view(np.uint64)
+                        co = np.empty(M5, np.uint64)
+                        t0 = time.perf_counter()
+                        cc = cpu.words(int(sub), co, hav, hbv)
+                        cdt = time.perf_counter() - t0
+                        assert cc == carry and np.array_equal(co, ho.numpy().view(np.uint64)), "C5 cpu/gpu mismatch"
+                        r["cpu_baseline"] = {"value": 24 * M5 / cdt / 1e9, "unit": "GB/s", "cores": 1,
+                                             "kind": cpu.kind,
+                                             "sample": f"all 2^30 limbs, one span-form dot_{'sub' if sub else 'add'}"
+                                                       f"_words call (route {cpu.note}; the reference's carry "
+                                                       "chain is serial, so 1 thread); bit-identical to the GPU"}
+                        del co
+                    except Exception as e:  # noqa: BLE001
+                        r["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:200]}
+                del ha, hb, ho
+            else:
+                del a, b, o
+            res["sub" if sub else "add"] = r
             torch.cuda.empty_cache()
+        if comm is not None:
+            comm.close()
         out["C5"] = {"metric": "one 2^30-limb add/sub GB/s (whole number, all GPUs)", "unit": "GB/s",
-                     "n_limbs": M5, "shard_limbs": n_local, "run": list(W.C5_RUN),
-                     "mode": "single GPU tiled path" if world == 1 else
-                             f"{world} limb-range shards, NCCL all_gather of 8-byte (G,P) per rank",
-                     **res}
+                     "n_limbs": M5, "shard_limbs": n_local, "run": list(W.C5_RUN), **res}
     return out
 
 
@@ -939,6 +1222,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-layouts", action="store_true", help="skip the interleaved-layout rows")
     ap.add_argument("--only", default="", help="comma list of C1,C3,C4,C5: run only those secondary configs")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
     ap.add_argument("--no-graph", action="store_true", help="direct launches instead of one CUDA-graph replay per step")
