@@ -486,6 +486,33 @@ def hbm_roofline(alg_bytes, launch_s, peak, kernel, peak_kind="measured (MEASURE
     return r
 
 
+def per_launch_us(torch, dg, lib, stream, make_calls, reps=4):
+    """Device time of ONE launch when launches run back to back (the GPU never waits for
+    the host): the calls make_calls(launcher) returns - one per rotating input set - are
+    captured `reps` times into one CUDA graph; per launch = graph time / launches, CUDA
+    events on the launching stream, best of 3 replays. (Bracketing a single launch with
+    events from Python also times the host's launch submission when the GPU is idle -
+    ~6 us on a ~17 us kernel.)"""
+    fn, nk, graph = capture_graph(torch, dg, lib, stream,
+                                  lambda Lc: (lambda cs=make_calls(Lc): [c() for _ in range(reps) for c in cs][-1]))
+    if fn is None:
+        return None
+    n = reps * len(make_calls(Launcher(torch, lib, stream)))
+    fn()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e3 / n
+        best = t if best is None else min(best, t)
+    del graph
+    return best
+
+
 def pinned_like(torch, t):
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     h.copy_(t)
@@ -586,17 +613,28 @@ def run_ours(args, rank, world, dist):
         wms, _ = timed_steps(torch, dist, world, stream, wcalls, args.steps, args.warmup)
         weak = {"value": full_step_bytes * world / (wms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": wms,
                 "per_rank": "the full C2 sweep on every rank (no collective)"}
-    _, per_single = timed_steps(torch, None, 1, stream, single_calls, max(3, args.steps // 4), 2)
+    # one size alone per launch: dotg_add_batch / dotg_sub_batch of this rank's slice,
+    # back to back over 3 rotating copies of the inputs (> L2 between reuses)
     per_size = {}
     for i, x in enumerate(bufs):
         lo, hi = my_pairs[i]
         bts = (hi - lo) * (24 * x["m"] + 4)
-        per_size[f"m{x['m']}"] = {"add_gbs": bts / (per_single[i] * 1e-3) / 1e9,
-                                  "sub_gbs": bts / (per_single[i + 4] * 1e-3) / 1e9,
-                                  "add_us": per_single[i] * 1e3, "sub_us": per_single[i + 4] * 1e3,
-                                  "add_frac": bts / (per_single[i] * 1e-3) / 1e9 / hbm_peak,
-                                  "sub_frac": bts / (per_single[i + 4] * 1e-3) / 1e9 / hbm_peak,
-                                  "note": "one dotg_add_batch / dotg_sub_batch launch of this size alone"}
+        row = {}
+        for op, (o, a_, b_, f) in (("add", (x["oa"], x["a"], x["b"], x["fa"])),
+                                   ("sub", (x["os"], x["sa"], x["sb"], x["fs"]))):
+            copies = [(o[lo:hi], a_[lo:hi], b_[lo:hi], f[lo:hi])]
+            copies += [(torch.empty_like(o[lo:hi]), a_[lo:hi].clone(), b_[lo:hi].clone(), torch.empty_like(f[lo:hi]))
+                       for _ in range(max(2, rotations(2 * (hi - lo) * x["m"] * 8)) - 1)]
+            us = per_launch_us(torch, dg, lib, stream,
+                               lambda Lc, cp=copies, sub=op == "sub": [Lc.addsub(sub, *c_, x["m"], hi - lo)
+                                                                      for c_ in cp])
+            del copies
+            if us is not None:
+                row.update({f"{op}_gbs": bts / (us * 1e-6) / 1e9, f"{op}_us": us,
+                            f"{op}_frac": bts / (us * 1e-6) / 1e9 / hbm_peak})
+        row["note"] = ("one dotg_add_batch / dotg_sub_batch launch of this size alone, launches back to back "
+                       "over rotating input copies (CUDA graph, events on the stream)")
+        per_size[f"m{x['m']}"] = row
     traffic = traffic_table().get("C2_per_launch_bytes_grouped" if not args.ungrouped else "C2_per_launch_bytes")
     # the same byte mix without carries: a plain 2-read / 1-write streaming add measured
     # live (tools/stream_peak.cu) - the practical ceiling for this kernel's traffic
@@ -799,10 +837,14 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                                                                              m, nb)]) for x in sets]
         ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
         x0 = sets[0]
-        singles = [L.addsub(False, x0["o"], x0["a"], x0["b"], x0["f"], m, nb),
-                   L.addsub(True, x0["o2"], x0["sa"], x0["sb"], x0["f2"], m, nb)]
-        _, per1 = timed_steps(torch, None, 1, stream, singles, steps, warm)
-        launch_s = statistics.mean(per) * 1e-3
+        # back-to-back launch times (graph over the rotating sets): add+sub grouped, add, sub
+        us_g = per_launch_us(torch, dg, lib, stream, lambda Lc: [
+            Lc.grouped([(False, x["o"], x["a"], x["b"], x["f"], m, nb), (True, x["o2"], x["sa"], x["sb"], x["f2"], m,
+                                                                         nb)]) for x in sets])
+        per1 = [per_launch_us(torch, dg, lib, stream, lambda Lc, sub=sub: [
+            Lc.addsub(sub, x["o2" if sub else "o"], x["sa" if sub else "a"], x["sb" if sub else "b"],
+                      x["f2" if sub else "f"], m, nb) for x in sets]) * 1e-3 for sub in (False, True)]
+        launch_s = (us_g * 1e-6) if us_g is not None else statistics.mean(per) * 1e-3
         c1 = {"metric": "add/sub GB/s (4096-bit, B=65536)", "value": B * (24 * m + 4) * 2 * len(calls) / (ms * 1e-3)
               / 1e9, "unit": "GB/s",
               "step": f"{len(calls)} rotating input sets; per set add + sub in one dotg_addsub_grouped launch",
@@ -871,7 +913,7 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                     c1["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:200]}
             del hs, ho, ho2
         out["C1"] = c1
-        del sets, calls, singles
+        del sets, calls
         torch.cuda.empty_cache()
 
     # ---------------- C3 / C4: batched multiply ----------------

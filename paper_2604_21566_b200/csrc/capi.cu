@@ -431,9 +431,12 @@ int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint
     return run_host_jobs(&j, 1);
 }
 
-// Single long number from host spans: slices are independent shards (dotg_shard_*),
-// so H2D of slice k+1 overlaps the streaming pass of slice k; one finish pass per
-// slice then resolves the slice carry-ins from the gathered slice aggregates.
+// Single long number from host spans: slices are independent shards (dotg_shard_*). H2D
+// of slice k+1 overlaps the streaming pass of slice k (two upload streams), and slice k's
+// fix-up needs only the aggregates of slices 0..k - a carry scan ACROSS slices, in slice
+// order - so it runs on a third stream as soon as slice k's local pass is done, followed
+// by slice k's D2H: downloads overlap the remaining uploads (the two copy engines work at
+// once) instead of waiting for the whole number to be resident.
 int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
     int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
     if (rc != DOTG_OK) return rc;
@@ -449,7 +452,7 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
     const size_t sb = align_up(dotg::long_state_bytes(slice), 256);
     const size_t ab = align_up(m * 8, 256);
     char* base = nullptr;
-    cudaStream_t s0 = g_host.s[0], s1 = g_host.s[1];
+    cudaStream_t s0 = g_host.s[0], s1 = g_host.s[1], sf = g_host.s[2];
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * ab + nsl * sb + align_up(nsl * 8, 256) + 256, s0);
     if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("words_host: ") + cudaGetErrorString(e));
     uint64_t* da = reinterpret_cast<uint64_t*>(base);
@@ -458,10 +461,15 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
     char* states = base + 3 * ab;
     uint32_t* aggs = reinterpret_cast<uint32_t*>(states + nsl * sb);
     uint32_t* dcarry = aggs + 2 * nsl;
-    cudaEvent_t ev = nullptr;
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventRecord(ev, s0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev, 0);  // allocation visible on s1
+    while (e == cudaSuccess && g_host.ev.size() < nsl + 1) {
+        cudaEvent_t ev;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) g_host.ev.push_back(ev);
+    }
+    cudaEvent_t ev_alloc = e == cudaSuccess ? g_host.ev[nsl] : nullptr;
+    if (e == cudaSuccess) e = cudaEventRecord(ev_alloc, s0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev_alloc, 0);  // allocation visible on s1 and sf
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sf, ev_alloc, 0);
     for (size_t k = 0; k < nsl && e == cudaSuccess; ++k) {
         const size_t l0 = k * slice, n = std::min(slice, m - l0);
         cudaStream_t st = (k & 1) ? s1 : s0;
@@ -469,20 +477,23 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
         if (e == cudaSuccess) e = cudaMemcpyAsync(db + l0, b + l0, n * 8, cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess)
             e = dotg::launch_long_local(sub, dout + l0, da + l0, db + l0, n, states + k * sb, aggs + 2 * k, st);
-    }
-    if (e == cudaSuccess) e = cudaEventRecord(ev, s1);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s0, ev, 0);
-    for (size_t k = 0; k < nsl && e == cudaSuccess; ++k) {
-        const size_t l0 = k * slice, n = std::min(slice, m - l0);
-        e = dotg::launch_long_finish(sub, dout + l0, n, states + k * sb, aggs, int(k), int(nsl),
-                                     k == 0 ? dcarry : nullptr, s0);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(out + l0, dout + l0, n * 8, cudaMemcpyDeviceToHost, s0);
+        if (e == cudaSuccess) e = cudaEventRecord(g_host.ev[k], st);
+        // fix-up of slice k: carry-in = (G, P) scan over slices 0..k-1, whose local passes
+        // sf has already waited for (it handles the slices in order)
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sf, g_host.ev[k], 0);
+        if (e == cudaSuccess)
+            e = dotg::launch_long_finish(sub, dout + l0, n, states + k * sb, aggs, int(k), int(k + 1),
+                                         k + 1 == nsl ? dcarry : nullptr, sf);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out + l0, dout + l0, n * 8, cudaMemcpyDeviceToHost, sf);
     }
     uint32_t hc = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hc, dcarry, 4, cudaMemcpyDeviceToHost, s0);
-    cudaError_t e2 = cudaFreeAsync(base, s0);
-    cudaError_t e3 = cudaStreamSynchronize(s0);
-    if (ev) cudaEventDestroy(ev);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hc, dcarry, 4, cudaMemcpyDeviceToHost, sf);
+    cudaError_t e2 = cudaFreeAsync(base, sf);  // sf has waited for every upload stream's work
+    cudaError_t e3 = cudaSuccess;
+    for (cudaStream_t x : {s0, s1, sf}) {
+        cudaError_t y = cudaStreamSynchronize(x);
+        if (e3 == cudaSuccess) e3 = y;
+    }
     if (e != cudaSuccess) return cuda_fail(e, "dotg words host");
     if (e2 != cudaSuccess) return cuda_fail(e2, "free");
     if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
