@@ -666,6 +666,23 @@ def run_ours(args, rank, world, dist):
                     row["sub" if sub else "add"] = {"chunks": c[0], "phase4_triggers": c[1],
                                                     "phase4_fraction": c[1] / max(1, c[0])}
             stress[f"m{x['m']}"] = row
+    # phase split (the reference's collect_ticks pass, bench.cpp:227-247): %clock64 laps
+    # of the timed team kernel over the same inputs, in AddSubStats buckets
+    phase_split = {}
+    if world == 1 and not args.no_phase:
+        for x in bufs:
+            row = {}
+            for op, (a_, b_) in (("add", (x["a"], x["b"])), ("sub", (x["sa"], x["sb"]))):
+                try:
+                    r = dg.addsub_phase_ticks(op == "sub", a_, b_)
+                    row[op] = {"pct": {k: round(v, 2) for k, v in r["pct"].items()},
+                               "carry_to_add_ratio": r["carry_to_add_ratio"]}
+                except Exception as e:  # noqa: BLE001
+                    row[op] = {"error": str(e)[:200]}
+            phase_split[f"m{x['m']}"] = row
+        phase_split["unit"] = ("share of SM-clock cycles per warp task (timed team kernel, laps at phase "
+                               "boundaries); reference (PAPER.md:754-761, EMR 512-bit add): load 18.7 / add 13.8 / "
+                               "carry_gen 25.8 / carry_add 20.7 / store 21.0 %, carry-to-add 4.9 random")
 
     # ---- e2e: this rank's share through the host-buffer C ABI (pinned host arrays) ----
     e2e = None
@@ -791,6 +808,7 @@ def run_ours(args, rank, world, dist):
                         if graph_launches is not None else "direct C-ABI launches"),
         "clocks": clocks,
         "carry_stress": stress,
+        "phase_split": phase_split,
         "configs": secondary,
     }
     if weak is not None:
@@ -1265,6 +1283,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-layouts", action="store_true", help="skip the interleaved-layout rows")
+    ap.add_argument("--no-phase", action="store_true", help="skip the phase-tick split")
     ap.add_argument("--only", default="", help="comma list of C1,C3,C4,C5: run only those secondary configs")
     ap.add_argument("--ungrouped", action="store_true", help="one launch per (size, op) instead of one grouped launch")
     ap.add_argument("--no-graph", action="store_true", help="direct launches instead of one CUDA-graph replay per step")

@@ -10,7 +10,9 @@
 //
 // Differences, by design:
 //   * AddSubStats (addsub.hpp:53-72): chunks_processed / phase4_triggers are produced
-//     (derived on the device); the rdtsc phase ticks are not (collect_ticks throws).
+//     (derived on the device); collect_ticks fills the phase ticks with SM-clock laps of
+//     the timed team kernel (dotg_addsub_phase_ticks_host; power-of-two m <= 256, other
+//     lengths throw std::logic_error).
 //   * dot_mul_4x4 computes the 64-bit product directly (the reference routes it through
 //     52-bit repacking and dot_mul_5x5; the 8 result limbs are identical).
 //   * Partial aliasing of out with a/b (undefined in the reference) throws.
@@ -54,12 +56,30 @@ struct AddSubStats {
     std::uint64_t chunks_processed = 0;
     std::uint64_t phase4_triggers = 0;
     bool collect_ticks = false;
+    // addsub.hpp:57-63, in SM clock cycles summed over the kernel's warps (see dotg.h)
+    std::uint64_t load_ticks = 0;
+    std::uint64_t add_ticks = 0;
+    std::uint64_t carry_gen_ticks = 0;
+    std::uint64_t carry_add_ticks = 0;
+    std::uint64_t store_ticks = 0;
+    std::uint64_t overflow_ticks = 0;
     double phase4_rate() const {
         return chunks_processed ? double(phase4_triggers) / double(chunks_processed) : 0.0;
+    }
+    // addsub.cpp:258-263
+    double carry_to_add_ratio() const {
+        if (add_ticks == 0) return 0.0;
+        return double(carry_gen_ticks + carry_add_ticks + store_ticks + overflow_ticks) / double(add_ticks);
     }
     void merge(const AddSubStats& o) {
         chunks_processed += o.chunks_processed;
         phase4_triggers += o.phase4_triggers;
+        load_ticks += o.load_ticks;
+        add_ticks += o.add_ticks;
+        carry_gen_ticks += o.carry_gen_ticks;
+        carry_add_ticks += o.carry_add_ticks;
+        store_ticks += o.store_ticks;
+        overflow_ticks += o.overflow_ticks;
     }
 };
 
@@ -70,19 +90,40 @@ inline void check(int rc) {
     if (rc == DOTG_EINVAL) throw std::invalid_argument(msg);
     throw std::runtime_error("dotg: " + msg);
 }
-inline void no_ticks(const AddSubStats* st) {
-    if (st != nullptr && st->collect_ticks)
-        throw std::logic_error("AddSubStats::collect_ticks (rdtsc phase ticks) has no device equivalent");
+inline bool ticks_supported(std::size_t m) { return m != 0 && m <= 256 && (m & (m - 1)) == 0; }
+inline void no_ticks(const AddSubStats* st, std::size_t m) {
+    if (st != nullptr && st->collect_ticks && !ticks_supported(m))
+        throw std::logic_error("AddSubStats::collect_ticks: the timed device kernel covers power-of-two m <= 256");
 }
 inline void validate(Width w) { check(dotg_validate_width(static_cast<int>(w))); }
 
 inline unsigned run_words(bool sub, std::span<limb_t> out, std::span<const limb_t> a,
                           std::span<const limb_t> b, Width w, AddSubStats* st) {
     validate(w);
-    no_ticks(st);
     if (a.size() != b.size() || out.size() != a.size())  // addsub.cpp:139-140
         throw std::invalid_argument("dot add/sub: operand lengths differ (caller pads)");
+    no_ticks(st, a.size());
     std::uint32_t carry = 0;
+    if (st != nullptr && st->collect_ticks) {
+        // the counters first (into scratch: out may alias a or b), then the phase laps of
+        // the timed team kernel, which writes out
+        std::uint64_t ch = 0, fi = 0;
+        std::uint32_t c2 = 0;
+        std::vector<limb_t> scratch(a.size());
+        check(dotg_words_host_stats(sub ? 1 : 0, scratch.data(), a.data(), b.data(), a.size(), static_cast<int>(w),
+                                    &c2, &ch, &fi));
+        st->chunks_processed += ch;
+        st->phase4_triggers += fi;
+        std::uint64_t t[6] = {};
+        check(dotg_addsub_phase_ticks_host(sub ? 1 : 0, out.data(), a.data(), b.data(), &carry, a.size(), 1, t));
+        st->load_ticks += t[0];
+        st->add_ticks += t[1];
+        st->carry_gen_ticks += t[2];
+        st->carry_add_ticks += t[3];
+        st->store_ticks += t[4];
+        st->overflow_ticks += t[5];
+        return carry;
+    }
     if (st != nullptr) {
         std::uint64_t ch = 0, fi = 0;
         check(dotg_words_host_stats(sub ? 1 : 0, out.data(), a.data(), b.data(), a.size(), static_cast<int>(w),

@@ -242,6 +242,20 @@ int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uin
 int dotg_words_host_stats(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                           int width, uint32_t* carry, uint64_t* chunks, uint64_t* fires);
 
+/* Phase ticks (AddSubStats::collect_ticks, addsub.hpp:57-63; the reference's PhaseTimer
+ * laps, kernels.hpp:20-37, and the phase-% / carry-to-add pass of bench.cpp:227-247):
+ * runs the batched add/sub with per-phase %clock64 laps compiled into the same team
+ * kernel and ADDS SM-clock cycles, summed over warps, into ticks[6] in AddSubStats order
+ * {load, add, carry_gen, carry_add, store, overflow} (overflow stays 0: cascades are
+ * resolved by the same mask addition as every other carry). out/flags are computed as by
+ * dotg_add_batch / dotg_sub_batch. Row-major, power-of-two m <= 256 (else DOTG_ENOTSUP).
+ * Device form: device pointers, ticks a device uint64[6]. Host form: host arrays, ticks a
+ * host uint64[6]. Off the hot path (the laps serialise each warp's phases). */
+int dotg_addsub_phase_ticks(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                            size_t batch, uint64_t* ticks, dotg_stream_t stream);
+int dotg_addsub_phase_ticks_host(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                                 size_t m, size_t batch, uint64_t* ticks);
+
 /* ---------------------------------------------------------------------------
  * Batched comparison. Replaces: compare(a, b) per pair (limbs.hpp:84, limbs.cpp:46-53),
  * the a >= b check of the sub configs. out[p] = -1 / 0 / +1 for a[p] < = > b[p] (equal

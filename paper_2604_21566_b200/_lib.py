@@ -64,6 +64,8 @@ SIGNATURES = {
     "dotg_chunk_host": (c_int, [c_int, _P, _P, _P, _P, _P, c_uint32, c_uint]),
     "dotg_kernel_launches": (c_uint64, []),
     "dotg_set_mul_route": (c_int, [c_int]),
+    "dotg_addsub_phase_ticks": (c_int, [c_int, _P, _P, _P, _P, c_size_t, c_size_t, _P, _P]),
+    "dotg_addsub_phase_ticks_host": (c_int, [c_int, _P, _P, _P, _P, c_size_t, c_size_t, _P]),
     "dotg_comm_id_bytes": (c_size_t, []),
     "dotg_comm_get_unique_id": (c_int, [_P]),
     "dotg_comm_init_rank": (c_int, [_P, c_int, _P, c_int]),

@@ -45,22 +45,35 @@ def lane_count(w: int) -> int:
 
 
 class AddSubStats:
-    """Counters of the reference's AddSubStats (include/dot/addsub.hpp:53-72) that the
-    device path reproduces: chunks_processed and phase4_triggers (derived on the device,
-    see csrc/stats.cu). Accumulated across calls like the reference. The rdtsc phase
-    ticks (collect_ticks) have no device equivalent and are rejected."""
+    """The reference's AddSubStats (include/dot/addsub.hpp:53-72): chunks_processed and
+    phase4_triggers (derived on the device, csrc/stats.cu) and, with collect_ticks, the
+    six phase-tick buckets - SM clock cycles from the %clock64 laps of the timed team
+    kernel (dotg_addsub_phase_ticks; power-of-two m <= 256), summed over warps.
+    Accumulated across calls like the reference."""
+
+    TICKS = ("load_ticks", "add_ticks", "carry_gen_ticks", "carry_add_ticks", "store_ticks", "overflow_ticks")
 
     def __init__(self):
         self.chunks_processed = 0
         self.phase4_triggers = 0
         self.collect_ticks = False
+        for k in self.TICKS:
+            setattr(self, k, 0)
 
     def phase4_rate(self) -> float:
         return self.phase4_triggers / self.chunks_processed if self.chunks_processed else 0.0
 
+    def carry_to_add_ratio(self) -> float:
+        """addsub.cpp:258-263: carry-handling ticks over the lane-add ticks."""
+        if self.add_ticks == 0:
+            return 0.0
+        return (self.carry_gen_ticks + self.carry_add_ticks + self.store_ticks + self.overflow_ticks) / self.add_ticks
+
     def merge(self, other: "AddSubStats") -> None:
         self.chunks_processed += other.chunks_processed
         self.phase4_triggers += other.phase4_triggers
+        for k in self.TICKS:
+            setattr(self, k, getattr(self, k) + getattr(other, k))
 
 
 class WordsResult(NamedTuple):
@@ -107,13 +120,22 @@ def _words_span(sub: bool, out: np.ndarray, a, b, width, stats=None) -> int:
         raise InvalidArgument("dot add/sub: operand lengths differ (caller pads)")  # addsub.cpp:139-140
     carry = ctypes.c_uint32(0)
     if stats is not None:
-        if stats.collect_ticks:
-            raise _lib.DotgError("AddSubStats.collect_ticks (rdtsc phase ticks) has no device equivalent")
+        m = a.size
+        if stats.collect_ticks and not (0 < m <= 256 and m & (m - 1) == 0):
+            raise _lib.DotgError("AddSubStats.collect_ticks: the timed device kernel covers power-of-two m <= 256")
         ch, fi = ctypes.c_uint64(0), ctypes.c_uint64(0)
-        check(lib().dotg_words_host_stats(int(sub), _hp(out), _hp(a), _hp(b), a.size, int(width),
+        dst = np.empty_like(out) if stats.collect_ticks else out  # out may alias a or b
+        check(lib().dotg_words_host_stats(int(sub), _hp(dst), _hp(a), _hp(b), a.size, int(width),
                                           ctypes.byref(carry), ctypes.byref(ch), ctypes.byref(fi)))
         stats.chunks_processed += int(ch.value)
         stats.phase4_triggers += int(fi.value)
+        if stats.collect_ticks:
+            t = np.zeros(6, np.uint64)
+            c32 = np.zeros(1, np.uint32)
+            check(lib().dotg_addsub_phase_ticks_host(int(sub), _hp(out), _hp(a), _hp(b), _hp(c32), m, 1, _hp(t)))
+            for k, v in zip(AddSubStats.TICKS, t.tolist()):
+                setattr(stats, k, getattr(stats, k) + int(v))
+            return int(c32[0])
         return int(carry.value)
     fn = lib().dotg_sub_words_host if sub else lib().dotg_add_words_host
     check(fn(_hp(out), _hp(a), _hp(b), a.size, ctypes.byref(carry)))
@@ -581,6 +603,38 @@ def addsub_stats(sub: bool, out, a, b, *, width=Width.w8, layout=ROW_MAJOR, stre
             stream.synchronize()
         ch, fi = cnt.tolist()
     return int(ch), int(fi)
+
+
+def addsub_phase_ticks(sub: bool, a, b, out=None, flags=None, *, stream=None) -> dict:
+    """Phase split of the batched add/sub on the device (the GPU counterpart of the
+    reference's collect_ticks pass, bench.cpp:227-247): runs the team kernel with
+    %clock64 laps compiled in over row-major [batch, m] device tensors (power-of-two
+    m <= 256), writes out / flags like add_batch / sub_batch, and returns the six tick
+    buckets (SM cycles summed over warps), their percentages and carry_to_add_ratio."""
+    torch = _torch()
+    import contextlib
+
+    _check_dev(a, "a")
+    _check_dev(b, "b")
+    if a.shape != b.shape or a.dim() != 2:
+        raise InvalidArgument("phase ticks: a, b must be [batch, m] tensors of one shape")
+    batch, m = a.shape
+    if out is None:
+        out = torch.empty_like(a)
+    if flags is None:
+        flags = torch.empty(batch, dtype=torch.int32, device=a.device)
+    with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+        t = torch.zeros(6, dtype=torch.int64, device=a.device)
+        check(lib().dotg_addsub_phase_ticks(int(sub), _dptr(out), _dptr(a), _dptr(b), _dptr(flags), m, batch,
+                                            _dptr(t), _stream_handle(stream)))
+        if stream is not None:
+            stream.synchronize()
+        ticks = [int(x) for x in t.tolist()]
+    res = dict(zip(AddSubStats.TICKS, ticks))
+    total = sum(ticks)
+    res["pct"] = {k.replace("_ticks", ""): (100.0 * v / total if total else 0.0) for k, v in zip(AddSubStats.TICKS, ticks)}
+    res["carry_to_add_ratio"] = (sum(ticks[2:]) / ticks[1]) if ticks[1] else 0.0
+    return res
 
 
 def compare_batch(a, b, out=None, *, layout=ROW_MAJOR, stream=None):

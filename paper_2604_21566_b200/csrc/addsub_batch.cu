@@ -55,8 +55,34 @@ __host__ __device__ constexpr uint64_t numbers_per_task(uint32_t m) {
     return uint64_t(32 / ((m / team_v(m)) < 32 ? (m / team_v(m)) : 32)) * uint64_t(team_u(m));
 }
 
-template <bool SUB, int M, int V, int U>
-__device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task) {
+// Phase ticks of the timed instantiation (the GPU counterpart of the reference's
+// AddSubStats::collect_ticks laps, PhaseTimer in kernels.hpp:20-37): SM clock cycles per
+// warp, lane 0 accumulating. Buckets in AddSubStats order: load, add, carry_gen,
+// carry_add, store, overflow. "overflow" (the reference's Phase-4 cascade) stays 0: the
+// mask addition of carry_gen resolves cascades with the same instructions as the common
+// case. A lap reads %clock64 only after a value depending on the previous phase's
+// results, so outstanding loads are charged to the phase that waits for them.
+enum TickBucket { kTickLoad = 0, kTickAdd, kTickCarryGen, kTickCarryAdd, kTickStore, kTickOverflow, kTicks };
+template <bool TIMED>
+struct WarpTimer {
+    uint64_t t0 = 0;
+    uint64_t acc[kTicks] = {};
+    __device__ __forceinline__ void start() {
+        if constexpr (TIMED) asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0)::"memory");
+    }
+    // dep: any value produced by the phase (forces its completion before the clock read)
+    __device__ __forceinline__ void lap(int bucket, uint64_t dep) {
+        if constexpr (TIMED) {
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1) : "l"(dep) : "memory");
+            acc[bucket] += t1 - t0;
+            t0 = t1;
+        }
+    }
+};
+
+template <bool SUB, int M, int V, int U, bool TIMED = false>
+__device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task, WarpTimer<TIMED>& tm) {
     using C = TeamCfg<M, V>;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned team = lane / C::T;
@@ -68,6 +94,7 @@ __device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task)
 
     uint64_t s[U][C::R][V];
     uint64_t bv[U][C::R][V];
+    tm.start();
     // Issue every load of the task before any arithmetic (MLP).
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -86,6 +113,16 @@ __device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task)
         }
     }
 
+    if constexpr (TIMED) {
+        uint64_t dep = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < C::R; ++r)
+#pragma unroll
+                for (int k = 0; k < V; ++k) dep ^= s[u][r][k] ^ bv[u][r][k];
+        tm.lap(kTickLoad, dep);
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint64_t num = base_num + uint64_t(u * C::NPW) + team;
@@ -95,10 +132,25 @@ __device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task)
 #pragma unroll
         for (int w = 0; w < C::W; ++w) Gm[w] = Pm[w] = 0;
 #pragma unroll
+        if constexpr (TIMED) {  // phase 1 (lane sums) timed on its own, as in chunk_generic
+#pragma unroll
+            for (int r = 0; r < C::R; ++r)
+#pragma unroll
+                for (int k = 0; k < V; ++k) s[u][r][k] = lane_op<SUB>(s[u][r][k], bv[u][r][k], g[r][k], p[r][k]);
+            uint64_t dep = 0;
+#pragma unroll
+            for (int r = 0; r < C::R; ++r)
+#pragma unroll
+                for (int k = 0; k < V; ++k) dep += s[u][r][k] + g[r][k] + p[r][k];
+            tm.lap(kTickAdd, dep);
+        }
+#pragma unroll
         for (int r = 0; r < C::R; ++r) {
             // Phase 1 + 2.
+            if constexpr (!TIMED) {
 #pragma unroll
-            for (int k = 0; k < V; ++k) s[u][r][k] = lane_op<SUB>(s[u][r][k], bv[u][r][k], g[r][k], p[r][k]);
+                for (int k = 0; k < V; ++k) s[u][r][k] = lane_op<SUB>(s[u][r][k], bv[u][r][k], g[r][k], p[r][k]);
+            }
             uint32_t G, P2;
             fold_gp<V>(g[r], p[r], G, P2);
             const uint32_t gw = __ballot_sync(0xffffffffu, G);
@@ -123,31 +175,47 @@ __device__ __forceinline__ void team_task(const AddSubProblem& P, uint64_t task)
         uint32_t flag;
         if constexpr (C::SL % 64 == 0) flag = uint32_t(Gm[C::W - 1] >> 63) | k;
         else flag = uint32_t(Cm[C::W - 1] >> (C::SL % 64)) & 1u;
+        tm.lap(kTickCarryGen, Cm[0] + flag);
 
         // Phase 4: apply carries inside each super-lane, store.
+        if constexpr (TIMED) {
+            uint64_t dep = 0;
+#pragma unroll
+            for (int r = 0; r < C::R; ++r) {
+                const unsigned j = unsigned(r * C::T) + t;
+                const uint32_t c = uint32_t(Cm[j / 64] >> (j % 64)) & 1u;
+                apply_superlane<SUB, V>(s[u][r], g[r], p[r], c);
+#pragma unroll
+                for (int k = 0; k < V; ++k) dep += s[u][r][k];
+            }
+            tm.lap(kTickCarryAdd, dep);
+        }
 #pragma unroll
         for (int r = 0; r < C::R; ++r) {
-            const unsigned j = unsigned(r * C::T) + t;
-            const uint32_t c = uint32_t(Cm[j / 64] >> (j % 64)) & 1u;
-            apply_superlane<SUB, V>(s[u][r], g[r], p[r], c);
+            if constexpr (!TIMED) {
+                const unsigned j = unsigned(r * C::T) + t;
+                const uint32_t c = uint32_t(Cm[j / 64] >> (j % 64)) & 1u;
+                apply_superlane<SUB, V>(s[u][r], g[r], p[r], c);
+            }
             if (ok) st_stream<V>(P.out + num * M + uint64_t(r * V * C::T + t * V), s[u][r]);
         }
         if (P.flags != nullptr && ok && t == 0) P.flags[num] = flag;
+        tm.lap(kTickStore, 0);
     }
 }
 
-template <bool SUB>
-__device__ __forceinline__ void dispatch_small(const AddSubProblem& P, uint64_t task) {
+template <bool SUB, bool TIMED = false>
+__device__ __forceinline__ void dispatch_small(const AddSubProblem& P, uint64_t task, WarpTimer<TIMED>& tm) {
     switch (P.m) {
-        case 1: team_task<SUB, 1, 1, 2>(P, task); break;
-        case 2: team_task<SUB, 2, 2, 2>(P, task); break;
-        case 4: team_task<SUB, 4, 4, 2>(P, task); break;
-        case 8: team_task<SUB, 8, 4, 2>(P, task); break;
-        case 16: team_task<SUB, 16, 4, 2>(P, task); break;
-        case 32: team_task<SUB, 32, 4, 2>(P, task); break;
-        case 64: team_task<SUB, 64, 4, 2>(P, task); break;
-        case 128: team_task<SUB, 128, 4, 2>(P, task); break;
-        case 256: team_task<SUB, 256, 4, 1>(P, task); break;
+        case 1: team_task<SUB, 1, 1, 2, TIMED>(P, task, tm); break;
+        case 2: team_task<SUB, 2, 2, 2, TIMED>(P, task, tm); break;
+        case 4: team_task<SUB, 4, 4, 2, TIMED>(P, task, tm); break;
+        case 8: team_task<SUB, 8, 4, 2, TIMED>(P, task, tm); break;
+        case 16: team_task<SUB, 16, 4, 2, TIMED>(P, task, tm); break;
+        case 32: team_task<SUB, 32, 4, 2, TIMED>(P, task, tm); break;
+        case 64: team_task<SUB, 64, 4, 2, TIMED>(P, task, tm); break;
+        case 128: team_task<SUB, 128, 4, 2, TIMED>(P, task, tm); break;
+        case 256: team_task<SUB, 256, 4, 1, TIMED>(P, task, tm); break;
         default: break;
     }
 }
@@ -158,19 +226,59 @@ template <bool BIG>
 __global__ void __launch_bounds__(256) k_addsub_grouped(const __grid_constant__ AddSubGroup grp) {
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    WarpTimer<false> tm;
     int pi = 0;
     for (uint64_t t = warp; t < grp.total_tasks; t += nw) {
         while (pi + 1 < grp.n && grp.p[pi + 1].task_begin <= t) ++pi;
         const AddSubProblem& P = grp.p[pi];
         const uint64_t task = t - P.task_begin;
         if constexpr (BIG) {
-            if (P.sub) team_task<true, 512, 4, 1>(P, task);
-            else team_task<false, 512, 4, 1>(P, task);
+            if (P.sub) team_task<true, 512, 4, 1>(P, task, tm);
+            else team_task<false, 512, 4, 1>(P, task, tm);
         } else {
-            if (P.sub) dispatch_small<true>(P, task);
-            else dispatch_small<false>(P, task);
+            if (P.sub) dispatch_small<true>(P, task, tm);
+            else dispatch_small<false>(P, task, tm);
         }
     }
+}
+
+// The same persistent task loop with the phase laps compiled in (one problem, m a power of
+// two <= 256, row-major): results identical to k_addsub_grouped; ticks = device uint64[6]
+// accumulated (AddSubStats bucket order), summed over warps.
+__global__ void __launch_bounds__(256) k_addsub_timed(const AddSubProblem P, uint64_t ntasks, uint64_t* ticks) {
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    WarpTimer<true> tm;
+    for (uint64_t t = warp; t < ntasks; t += nw) {
+        if (P.sub) dispatch_small<true, true>(P, t, tm);
+        else dispatch_small<false, true>(P, t, tm);
+    }
+    if ((threadIdx.x & 31u) == 0)
+        for (int i = 0; i < kTicks; ++i)
+            if (tm.acc[i]) atomicAdd(reinterpret_cast<unsigned long long*>(ticks + i), (unsigned long long)tm.acc[i]);
+}
+
+cudaError_t launch_addsub_timed(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                                size_t m, size_t batch, uint64_t* ticks, cudaStream_t st) {
+    if (m == 0 || m > 256 || (m & (m - 1)) != 0) return cudaErrorNotSupported;
+    AddSubProblem P{};
+    P.out = out;
+    P.a = a;
+    P.b = b;
+    P.flags = flags;
+    P.batch = batch;
+    P.m = uint32_t(m);
+    P.sub = sub ? 1u : 0u;
+    const uint64_t ntasks = (batch + numbers_per_task(uint32_t(m)) - 1) / numbers_per_task(uint32_t(m));
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_addsub_timed, 256, 0);
+    const uint64_t cap = uint64_t(sms) * uint64_t(per > 0 ? per : 1);
+    const uint64_t need = (ntasks + 7) / 8;
+    k_addsub_timed<<<unsigned(need < cap ? (need ? need : 1) : cap), 256, 0, st>>>(P, ntasks, ticks);
+    count_launch();
+    return cudaGetLastError();
 }
 
 // Thread per pair, any m and any strides: pair p, limb i at p*sp + i*si. Interleaved
@@ -236,123 +344,185 @@ __global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ld
     if (flags != nullptr) flags[pidx] = c;
 }
 
-// Interleaved layout [m][batch], limb-segmented: a CTA owns 32 * PPL consecutive pairs;
-// warp w of the CTA owns limbs [w*L, w*L + L) of those pairs, lane l the pairs
-// PPL*l .. PPL*l + PPL - 1 (for PPL = 2 one 128-bit load per limb row covers both).
-// Each thread resolves its segment with carry-in 0 keeping the sums and g/p bits in
-// registers, publishes the segment's (G, P) per pair in shared memory, folds the (G, P)
-// of the lower segments of its pair into its carry-in, and only then stores - every
-// output written once. A batch of few long numbers gets S = ceil(m / L) warps per strip
-// of pairs instead of one serial thread per pair.
-constexpr int kPPL = 1;  // pairs per lane (2 with 128-bit row loads measured slower)
+// Interleaved layout [m][batch], limb-segmented: a CTA owns 32 consecutive pairs (lane =
+// pair); warp w of the CTA owns limbs [w*L, w*L + L) of those pairs. Each thread resolves
+// its segment with carry-in 0 keeping the sums and g/p bits in registers. The segments'
+// (G, P) are published per warp as two 32-bit ballot masks over the pairs; after ONE
+// barrier every warp folds the masks of the lower segments, bit-parallel over its 32
+// pairs (c = G_j | (P_j & c), j < w), applies its carry-in and stores - every output
+// written once. (r01 version: a second barrier and warp 0 folding the segments per pair
+// while the other warps waited - 0.43-0.61 of HBM at m = 128-512.) A batch of few long
+// numbers gets S = ceil(m / L) warps per strip of pairs instead of one serial thread per
+// pair.
 template <int kIL, int kIMaxS, bool SUB>  // limbs per thread-segment, segments per CTA
-__global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* out, const uint64_t* a,
-                                                                     const uint64_t* b, uint32_t* flags,
-                                                                     size_t m, size_t batch, bool vec_ok) {
-    __shared__ uint32_t sgp[kIMaxS][32 * kPPL];  // bit 0 G, bit 1 P per (segment, pair)
-    __shared__ uint32_t scin[32 * kPPL];          // bit j: carry into segment j, per pair
+__global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* __restrict__ out,
+                                                                     const uint64_t* __restrict__ a,
+                                                                     const uint64_t* __restrict__ b, uint32_t* flags,
+                                                                     size_t m, size_t batch) {
+    __shared__ uint32_t sG[kIMaxS], sP[kIMaxS];  // per segment: bit p = G / P of pair p
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
-    const int S = int(blockDim.x >> 5);
-    const size_t p = size_t(blockIdx.x) * (32 * kPPL) + size_t(kPPL * lane);  // lane's first pair
+    const size_t p = size_t(blockIdx.x) * 32 + size_t(lane);
     const size_t i0 = size_t(w) * kIL;
     const int L = int(m - i0 < size_t(kIL) ? m - i0 : size_t(kIL));
-    bool ok[kPPL];
-#pragma unroll
-    for (int q = 0; q < kPPL; ++q) ok[q] = p + q < batch;
-    const bool vec = kPPL == 2 && ok[kPPL - 1] && vec_ok;  // batch even, 16-byte aligned bases
-    uint64_t s[kPPL][kIL];
-    uint32_t gm[kPPL], pm[kPPL];  // per-limb generate / propagate bits
-#pragma unroll
-    for (int q = 0; q < kPPL; ++q) gm[q] = pm[q] = 0;
+    const bool ok = p < batch;
+    uint64_t s[kIL], y[kIL];
+    uint32_t gm = 0, pm = 0;  // per-limb generate / propagate bits
+    // every load of the segment in flight before any arithmetic
 #pragma unroll
     for (int k = 0; k < kIL; ++k) {
-        if (k < L) {
+        s[k] = y[k] = 0;
+        if (k < L && ok) {
             const size_t off = (i0 + size_t(k)) * batch + p;
-            uint64_t x[kPPL], y[kPPL];
-#pragma unroll
-            for (int q = 0; q < kPPL; ++q) x[q] = y[q] = 0;
-            if constexpr (kPPL == 2) {
-                if (vec) {
-                    asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
-                                 : "=l"(x[0]), "=l"(x[kPPL - 1]) : "l"(a + off));
-                    asm volatile("ld.global.L1::no_allocate.v2.u64 {%0,%1}, [%2];"
-                                 : "=l"(y[0]), "=l"(y[kPPL - 1]) : "l"(b + off));
-                }
-            }
-            if (!vec) {
-#pragma unroll
-                for (int q = 0; q < kPPL; ++q)
-                    if (ok[q]) {
-                        x[q] = a[off + q];
-                        y[q] = b[off + q];
-                    }
-            }
-#pragma unroll
-            for (int q = 0; q < kPPL; ++q) {
-                uint32_t gq, pq;
-                s[q][k] = lane_op<SUB>(x[q], y[q], gq, pq);
-                gm[q] |= gq << k;
-                pm[q] |= pq << k;
-            }
+            s[k] = __ldcs(a + off);
+            y[k] = __ldcs(b + off);
         }
-    }
-#pragma unroll
-    for (int q = 0; q < kPPL; ++q) {
-        uint32_t c = 0, all = 1;
-#pragma unroll
-        for (int k = 0; k < kIL; ++k)
-            if (k < L) {
-                c = ((gm[q] >> k) & 1u) | (((pm[q] >> k) & 1u) & c);
-                all &= (pm[q] >> k) & 1u;
-            }
-        sgp[w][kPPL * lane + q] = c | (all << 1);
-    }
-    __syncthreads();
-    // carries into every segment of a pair at once: the segments' (G, P) bits as two masks
-    // and one mask addition, C = ((G << 1) + P) ^ P - the limb-level lookahead applied to
-    // segments (warp 0, lane = pair), instead of each warp folding its lower segments
-    if (w == 0) {
-#pragma unroll
-        for (int q = 0; q < kPPL; ++q) {
-            uint64_t G = 0, P = 0;
-            for (int j = 0; j < S; ++j) {
-                const uint32_t v = sgp[j][kPPL * lane + q];
-                G |= uint64_t(v & 1u) << j;
-                P |= uint64_t((v >> 1) & 1u) << j;
-            }
-            scin[kPPL * lane + q] = uint32_t(((G << 1) + P) ^ P);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kPPL; ++q) {
-        const uint32_t cin = (scin[kPPL * lane + q] >> w) & 1u;  // carry into this segment
-        uint32_t c = cin;
-#pragma unroll
-        for (int k = 0; k < kIL; ++k)
-            if (k < L) {
-                s[q][k] = apply_carry<SUB>(s[q][k], c);
-                c = ((gm[q] >> k) & 1u) | (((pm[q] >> k) & 1u) & c);
-            }
-        if (w == S - 1 && flags != nullptr && ok[q]) flags[p + q] = c;
     }
 #pragma unroll
     for (int k = 0; k < kIL; ++k) {
         if (k < L) {
-            const size_t off = (i0 + size_t(k)) * batch + p;
-            if constexpr (kPPL == 2) {
-                if (vec) {
-                    asm volatile("st.global.L1::no_allocate.v2.u64 [%0], {%1,%2};" ::"l"(out + off), "l"(s[0][k]),
-                                 "l"(s[kPPL - 1][k])
-                                 : "memory");
-                    continue;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < kPPL; ++q)
-                if (ok[q]) out[off + q] = s[q][k];
+            uint32_t gq, pq;
+            s[k] = lane_op<SUB>(s[k], y[k], gq, pq);
+            gm |= gq << k;
+            pm |= pq << k;
         }
     }
+    uint32_t c = 0, all = 1;
+#pragma unroll
+    for (int k = 0; k < kIL; ++k)
+        if (k < L) {
+            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+            all &= (pm >> k) & 1u;
+        }
+    const uint32_t Gm = __ballot_sync(0xffffffffu, c), Pm = __ballot_sync(0xffffffffu, all);
+    if (lane == 0) {
+        sG[w] = Gm;
+        sP[w] = Pm;
+    }
+    __syncthreads();
+    uint32_t cm = 0;  // carries into segment w, one bit per pair
+#pragma unroll
+    for (int j = 0; j < kIMaxS; ++j)
+        if (j < w) cm = sG[j] | (sP[j] & cm);
+    c = (cm >> lane) & 1u;
+#pragma unroll
+    for (int k = 0; k < kIL; ++k)
+        if (k < L) {
+            s[k] = apply_carry<SUB>(s[k], c);
+            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+        }
+    if (!ok) return;
+    if (w == int(blockDim.x >> 5) - 1 && flags != nullptr) flags[p] = c;
+#pragma unroll
+    for (int k = 0; k < kIL; ++k)
+        if (k < L) __stcs(out + (i0 + size_t(k)) * batch + p, s[k]);
+}
+
+// Interleaved layout, two streaming passes (no barrier, no register holding): the
+// long-number scheme of addsub_long.cu applied to segments of kSL limbs x 32 pairs.
+//   pass 1 (k_il_local): warp = (strip of 32 pairs, segment of kSL limb rows); every
+//     load of the segment in flight, then the segment resolved with carry-in 0 and
+//     stored at once; per (segment, pair) one state byte: G (carry out for carry-in 0),
+//     P (every limb propagates), pt (first non-propagating limb, kSL if none). Only
+//     limbs [0, pt] of a segment depend on its carry-in.
+//   pass 2 (k_il_finish): thread per pair walks its S state bytes (coalesced across the
+//     pairs), c_{j+1} = G_j | (P_j & c_j), and where c_j = 1 rewrites limbs [0, pt] of
+//     segment j (propagate value below pt, +-1 at pt): on random data one 8-byte RMW per
+//     segment with carry-in 1, mostly in the same limb row across a warp.
+// Warps are numbered strip-fastest so concurrently running warps stream contiguous
+// stretches of each limb row.
+constexpr int kSL = 8;  // limbs per segment
+// A batch of numbers of <= kSL limbs is one segment per pair: the flag is final in pass 1
+// and the finish pass is skipped. (Measured r02, tools/il_modes.py, B x m = 2^22: pass 1
+// with 4 pairs per lane and 256-bit row loads ran 2.6-3.9 TB/s, below 1 pair per lane.)
+template <bool SUB>
+__global__ void __launch_bounds__(256) k_il_local(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                  const uint64_t* __restrict__ b, uint8_t* __restrict__ state,
+                                                  uint32_t* __restrict__ flags, size_t m, size_t batch,
+                                                  size_t nstrips, size_t nwarps) {
+    const size_t gw = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (gw >= nwarps) return;
+    const size_t strip = gw % nstrips, seg = gw / nstrips;
+    constexpr int PPL = 1;
+    const size_t p = strip * 32 + (threadIdx.x & 31u);
+    if (p >= batch) return;
+    const size_t i0 = seg * kSL;
+    const int L = int(m - i0 < size_t(kSL) ? m - i0 : size_t(kSL));
+    uint64_t s[kSL][PPL], y[kSL][PPL];
+#pragma unroll
+    for (int k = 0; k < kSL; ++k) {
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) s[k][q] = y[k][q] = 0;
+        if (k < L) {
+            const size_t off = (i0 + size_t(k)) * batch + p;
+            s[k][0] = __ldcs(a + off);
+            y[k][0] = __ldcs(b + off);
+        }
+    }
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) {
+        uint32_t c = 0, all = 1, pt = kSL;
+#pragma unroll
+        for (int k = 0; k < kSL; ++k)
+            if (k < L) {
+                uint32_t g, pr;
+                const uint64_t v = lane_op<SUB>(s[k][q], y[k][q], g, pr);
+                s[k][q] = apply_carry<SUB>(v, c);
+                if (!pr && pt == kSL) pt = uint32_t(k);
+                c = g | (pr & c);
+                all &= pr;
+            }
+        if (pt > uint32_t(L)) pt = uint32_t(L);
+        word |= (c | (all << 1) | (pt << 2)) << (8 * q);
+        if (m <= size_t(kSL) && flags != nullptr) flags[p + q] = c;
+    }
+#pragma unroll
+    for (int k = 0; k < kSL; ++k)
+        if (k < L) {
+            const size_t off = (i0 + size_t(k)) * batch + p;
+            __stcs(out + off, s[k][0]);
+        }
+    if (m > size_t(kSL)) state[seg * batch + p] = uint8_t(word);
+}
+
+template <bool SUB>
+__global__ void __launch_bounds__(256) k_il_finish(uint64_t* __restrict__ out, const uint8_t* __restrict__ state,
+                                                   uint32_t* flags, size_t m, size_t batch, size_t nseg) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= batch) return;
+    constexpr int CH = 16;  // segments per round: their state loads, then their fix-up loads, in flight together
+    uint32_t c = 0;
+    for (size_t j0 = 0; j0 < nseg; j0 += CH) {
+        uint32_t st[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k)  // past the last segment: the identity {G, P} = {0, 1}
+            st[k] = j0 + k < nseg ? uint32_t(__ldcs(state + (j0 + k) * batch + p)) : 2u;
+        uint32_t cin = 0;  // bit k: carry into segment j0 + k
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            cin |= c << k;
+            c = (st[k] & 1u) | ((st[k] >> 1) & 1u & c);
+        }
+        if (j0 + CH > nseg) cin &= (1u << (nseg - j0)) - 1u;  // no fix-ups past the last segment
+        if (cin == 0) continue;
+        uint64_t v[CH];
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            v[k] = 0;
+            const size_t i0 = (j0 + k) * kSL;
+            const uint32_t pt = st[k] >> 2;
+            if (((cin >> k) & 1u) && i0 + pt < m && pt < uint32_t(kSL)) v[k] = out[(i0 + pt) * batch + p];
+        }
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            if (!((cin >> k) & 1u)) continue;
+            const size_t i0 = (j0 + k) * kSL;
+            const uint32_t pt = st[k] >> 2;
+            for (uint32_t q = 0; q < pt; ++q) out[(i0 + q) * batch + p] = prop_value<SUB>(1u);
+            if (i0 + pt < m && pt < uint32_t(kSL)) out[(i0 + pt) * batch + p] = apply_carry<SUB>(v[k], 1u);
+        }
+    }
+    if (flags != nullptr) flags[p] = c;
 }
 
 // Row-major, any m (no power-of-two team shape): the batch is one flat limb array, so a
@@ -450,12 +620,9 @@ template <int kIL, int kIMaxS, bool SUB>
 cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                             size_t batch, cudaStream_t st) {
     const size_t S = (m + kIL - 1) / kIL;
-    const size_t blocks = (batch + 32 * kPPL - 1) / (32 * kPPL);
-    const bool vec_ok = batch % 2 == 0 &&
-                        ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
-                          reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
+    const size_t blocks = (batch + 31) / 32;
     k_addsub_interleaved<kIL, kIMaxS, SUB><<<unsigned(blocks), unsigned(S * 32), 0, st>>>(out, a, b, flags, m,
-                                                                                        batch, vec_ok);
+                                                                                        batch);
     count_launch();
     return cudaGetLastError();
 }
@@ -466,6 +633,58 @@ cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b,
 // 16-warp CTAs of 16-limb segments, 3.7 for 4-limb segments or 16-warp CTAs at m = 128);
 // 256 < m <= 512 16-limb segments (3.0 TB/s; 2.0 with 32-limb ones, 1.1 strided);
 // 512 < m <= 1024 32-limb segments (2.8 TB/s); longer numbers strided.
+// segment state fits a modest scratch, and the grid fits 32-bit block counts
+bool nseg_fits(size_t m, size_t batch) {
+    const size_t nseg = (m + kSL - 1) / kSL;
+    return nseg * batch <= (size_t(1) << 32) && (nseg * ((batch + 31) / 32) + 7) / 8 < (size_t(1) << 31);
+}
+
+template <bool SUB>
+cudaError_t run_interleaved_2pass(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                                  size_t batch, cudaStream_t st) {
+    const size_t nseg = (m + kSL - 1) / kSL, nstrips = (batch + 31) / 32;
+    const size_t nwarps = nseg * nstrips;
+    uint8_t* state = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (nseg > 1) {
+        retain_stream_pool();
+        e = cudaMallocAsync(reinterpret_cast<void**>(&state), nseg * batch, st);
+        if (e != cudaSuccess) return e;
+    }
+    k_il_local<SUB><<<unsigned((nwarps + 7) / 8), 256, 0, st>>>(out, a, b, state, flags, m, batch, nstrips, nwarps);
+    count_launch();
+    e = cudaGetLastError();
+    if (nseg == 1) return e;
+    if (e == cudaSuccess) {
+        k_il_finish<SUB><<<unsigned((batch + 255) / 256), 256, 0, st>>>(out, state, flags, m, batch, nseg);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    cudaError_t e2 = cudaFreeAsync(state, st);
+    return e != cudaSuccess ? e : e2;
+}
+
+// Interleaved routes (tools/il_modes.py, B200, B x m = 2^22 limbs, GB/s at m = 4 / 16 / 32
+// / 64 / 128 / 256 / 512 / 1024): thread per pair 4560 / 5130 / 5360 / 4410 / 3230 / 1910 /
+// 1060 / 560; one-pass segmented CTAs - / - / - / - / 4030 / 3050 / 3240 / 2320; two-pass
+// 3860 (m = 4) ... 3730 / 3250 / 2710 / 2020 (m = 128 ... 1024). Auto: thread per pair below
+// 128 limbs, one-pass CTAs up to 1024, two-pass above. DOTG_IL_MODE (A/B knob): 0 auto,
+// 1 one-pass where it applies, 2 thread per pair; DOTG_IL_MIN moves the two-pass bound.
+int il_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("DOTG_IL_MODE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+bool il_two_pass(size_t m, size_t batch) {
+    static const size_t lo = [] {
+        const char* e = std::getenv("DOTG_IL_MIN");
+        return size_t(e ? std::atol(e) : 1025);
+    }();
+    return il_mode() == 0 && m >= lo && nseg_fits(m, batch);
+}
+
 template <bool SUB>
 cudaError_t run_interleaved_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                                 size_t batch, cudaStream_t st) {
@@ -570,7 +789,13 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             continue;
         }
         const int r = route(P, layouts[i]);
-        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 1024) {
+        if (r == 2 && layouts[i] == 1 && il_two_pass(P.m, P.batch)) {
+            cudaError_t e = P.sub ? run_interleaved_2pass<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                                  : run_interleaved_2pass<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+            if (e != cudaSuccess) return e;
+            continue;
+        }
+        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 1024 && il_mode() != 2) {
             cudaError_t e = P.sub ? run_interleaved_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                                   : run_interleaved_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
             if (e != cudaSuccess) return e;

@@ -819,6 +819,56 @@ int dotg_addsub_stats(int sub, const uint64_t* out, const uint64_t* a, const uin
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "stats");
 }
 
+int dotg_addsub_phase_ticks(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                            size_t batch, uint64_t* ticks, dotg_stream_t stream) {
+    int rc = check_addsub(out, a, b, flags, m, batch, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if (ticks == nullptr) return fail(DOTG_EINVAL, "phase ticks: null ticks");
+    if (m == 0 || m > 256 || (m & (m - 1)) != 0)
+        return fail(DOTG_ENOTSUP, "phase ticks: the timed kernel covers power-of-two m <= 256 (row-major)");
+    if (batch == 0) return DOTG_OK;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_addsub_timed(sub != 0, out, a, b, flags, m, batch, ticks,
+                                              static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "phase ticks");
+}
+
+int dotg_addsub_phase_ticks_host(int sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                                 size_t m, size_t batch, uint64_t* ticks) {
+    int rc = check_addsub(out, a, b, flags, m, batch, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK) return rc;
+    if (ticks == nullptr) return fail(DOTG_EINVAL, "phase ticks: null ticks");
+    if (m == 0 || m > 256 || (m & (m - 1)) != 0)
+        return fail(DOTG_ENOTSUP, "phase ticks: the timed kernel covers power-of-two m <= 256 (row-major)");
+    if (batch == 0) return DOTG_OK;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    std::lock_guard<std::mutex> lk(g_host.mu);
+    if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    cudaStream_t st = g_host.s[0];
+    const size_t ib = align_up(m * batch * 8, 256), fb = align_up(batch * 4, 256);
+    char* base = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * ib + fb + 64, st);
+    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("phase ticks: ") + cudaGetErrorString(e));
+    uint64_t* da = reinterpret_cast<uint64_t*>(base);
+    uint64_t* db = reinterpret_cast<uint64_t*>(base + ib);
+    uint64_t* dout = reinterpret_cast<uint64_t*>(base + 2 * ib);
+    uint32_t* dfl = reinterpret_cast<uint32_t*>(base + 3 * ib);
+    uint64_t* dt = reinterpret_cast<uint64_t*>(base + 3 * ib + fb);
+    e = cudaMemcpyAsync(da, a, m * batch * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db, b, m * batch * 8, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dt, ticks, 6 * 8, cudaMemcpyHostToDevice, st);  // accumulate
+    if (e == cudaSuccess) e = dotg::launch_addsub_timed(sub != 0, dout, da, db, dfl, m, batch, dt, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, m * batch * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && flags) e = cudaMemcpyAsync(flags, dfl, batch * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ticks, dt, 6 * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e2 = cudaFreeAsync(base, st);
+    cudaError_t e3 = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "phase ticks host");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
+    return DOTG_OK;
+}
+
 int dotg_compare_batch(int32_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch, int layout,
                        dotg_stream_t stream) {
     if (layout != DOTG_ROW_MAJOR && layout != DOTG_INTERLEAVED) return fail(DOTG_EINVAL, "unknown layout");

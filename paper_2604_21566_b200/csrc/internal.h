@@ -36,6 +36,11 @@ struct AddSubGroup {  // passed by value as a __grid_constant__ kernel parameter
 // Grouped batched add/sub: every problem independent; layouts[i] per problem.
 cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, int n, cudaStream_t stream);
 
+// Batched add/sub with the phase-tick laps compiled in (row-major, power-of-two m <= 256):
+// ticks = device uint64[6] {load, add, carry_gen, carry_add, store, overflow}, accumulated.
+cudaError_t launch_addsub_timed(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
+                                size_t m, size_t batch, uint64_t* ticks, cudaStream_t st);
+
 // Batched add/sub. layout 0 = row-major [batch][m], 1 = interleaved [m][batch].
 cudaError_t launch_addsub_batch(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b,
                                 uint32_t* flags, size_t m, size_t batch, int layout,
@@ -78,6 +83,9 @@ cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b,
                             cudaStream_t st);
 // Even 16 < m < 128, 16-byte aligned rows: zero-extended to the next tensor-pipe size.
 cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st);
+// Interleaved [m][batch] operands / product in place: even 16 < m <= 128.
+cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st);
 // Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
 extern std::atomic<int> g_mul_route;

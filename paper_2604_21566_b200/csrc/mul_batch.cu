@@ -726,7 +726,11 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
                              int layout, cudaStream_t stream) {
     if (batch == 0) return cudaSuccess;
     const bool al = aligned32(out) && aligned32(a) && aligned32(b);
-    // interleaved m > 16, and 4 < m < 16 off the powers of two (no interleaved register
+    // interleaved even 16 < m <= 128: the tensor-pipe kernel reads and writes the
+    // interleaved layout in place (tools/mul_layout_timing.py)
+    if (layout == 1 && m > 16 && m <= 128 && m % 2 == 0 && g_mul_route.load(std::memory_order_relaxed) != 1)
+        return launch_mul_imma_il(out, a, b, m, batch, stream);
+    // other interleaved m > 16, and 4 < m < 16 off the powers of two (no interleaved register
     // kernel for those): transpose around the row-major route
     if (layout == 1 && (m > 16 || (m > 4 && (m & (m - 1)) != 0)) && g_mul_route.load(std::memory_order_relaxed) != 1 &&
         batch <= (size_t(65535) * 32))

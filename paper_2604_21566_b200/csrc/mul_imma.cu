@@ -156,7 +156,14 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 #ifndef DOTG_IMMA_MINB16
 #define DOTG_IMMA_MINB16 1
 #endif
-template <int NB>
+// IL = true: the batch-interleaved layout [m][batch] (limb i of pair p at i * batch + p),
+// read in place - no transposes. A warp's operand words come straight from global memory
+// with one 8-byte load per limb (the 4 warps of a CTA take 4 consecutive pairs, so every
+// 32-byte sector is used whole across them in L1 / L2 and DRAM sees each byte once), held
+// one pair ahead in registers instead of the bulk-copy ring; products are stored at
+// out[L * batch + p] (the 4 warps again fill the sectors). Row-major (IL = false) uses the
+// mbarrier ring of cp.async.bulk copies.
+template <int NB, bool IL>
 __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b, size_t batch,
@@ -168,14 +175,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
     extern __shared__ __align__(16) uint32_t smem_dyn[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    uint32_t* raw = smem_dyn + size_t(warp) * C::WARP_WORDS;  // ST x (a words, b words)
-    uint32_t* cp = raw + C::RAW_WORDS;                        // 4 shifted copies of bpad
+    uint32_t* raw = smem_dyn + size_t(warp) * (IL ? C::WARP_WORDS - C::RAW_WORDS : C::WARP_WORDS);
+    uint32_t* cp = raw + (IL ? 0 : C::RAW_WORDS);            // 4 shifted copies of bpad
     uint32_t* sa = cp + C::COPY_WORDS;                        // byte-reversed a words
     int* S = reinterpret_cast<int*>(sa + C::A_WORDS);         // column sums
     __shared__ uint64_t bars[kImmaWarps][C::ST];
     uint64_t* bar = bars[warp];
     for (int i = lane; i < C::COPY_WORDS + C::A_WORDS; i += 32) cp[i] = 0;  // padding stays zero
-    if (mr < C::M)
+    if (!IL && mr < C::M)
         for (int i = lane; i < C::RAW_WORDS; i += 32) raw[i] = 0;
     __syncwarp();
     // the zero-fill is a generic-proxy write; the bulk copies below write the same ring
@@ -191,24 +198,47 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
         bulk_load(dst, a + p * size_t(mr), kOpBytes, &bar[stage]);
         bulk_load(dst + C::NW, b + p * size_t(mr), kOpBytes, &bar[stage]);
     };
-    if (lane == 0) {
+    if (!IL && lane == 0) {
         for (int st = 0; st < C::ST; ++st) mbar_init(&bar[st]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int st = 0; st < C::ST; ++st)
             if (first + size_t(st) * nwarps < batch) issue(st, first + size_t(st) * nwarps);
     }
     __syncwarp();
+    // IL: lane's VW operand words of a pair = limbs VW/2 * lane ... (VW even for m >= 32)
+    static_assert(!IL || (C::VW % 2 == 0), "interleaved route needs two or more words per lane");
+    constexpr int LL = C::VW / 2 > 0 ? C::VW / 2 : 1;  // limbs per lane
+    uint64_t na[LL], nb[LL];
+    auto il_load = [&](size_t pr) {
+#pragma unroll
+        for (int e = 0; e < LL; ++e) {
+            const size_t L = size_t(lane) * LL + e;
+            const bool okl = pr < batch && lane < C::LD_LANES && int(L) < mr;
+            na[e] = okl ? __ldg(a + L * batch + pr) : 0ull;
+            nb[e] = okl ? __ldg(b + L * batch + pr) : 0ull;
+        }
+    };
+    if (IL) il_load(first);
     int stage = 0;
     uint32_t parity = 0;
     for (size_t pair = first; pair < batch; pair += nwarps) {
-        mbar_wait(&bar[stage], parity);
+        if (!IL) mbar_wait(&bar[stage], parity);
         // ---- stage: copy_s[i] = bytes bpad[4i + s ..], bpad[y] = b[y - 31]; word j of b
         // feeds copy index i = j + 8 (with word j + 1), and i = 7 takes (0, b[0]).
         {
             const uint32_t* ra = raw + stage * 2 * C::NW;
             const uint32_t* rb = ra + C::NW;
             uint32_t bv[C::VW + 1], av[C::VW];
-            if (lane < C::LD_LANES) {
+            if constexpr (IL) {
+#pragma unroll
+                for (int e = 0; e < LL; ++e) {
+                    av[2 * e] = uint32_t(na[e]);
+                    av[2 * e + 1] = uint32_t(na[e] >> 32);
+                    bv[2 * e] = uint32_t(nb[e]);
+                    bv[2 * e + 1] = uint32_t(nb[e] >> 32);
+                }
+                il_load(pair + nwarps);  // next pair's operands in flight during this one
+            } else if (lane < C::LD_LANES) {
                 lds_vec<C::VW>(rb + lane * C::VW, bv);
                 lds_vec<C::VW>(ra + lane * C::VW, av);
             }
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
         }
         __syncwarp();
         // ---- the raw slot is consumed: refill it with the pair ST steps ahead
-        if (lane == 0) {
+        if (!IL && lane == 0) {
             const size_t ahead = pair + size_t(C::ST) * nwarps;
             if (ahead < batch) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -339,18 +369,24 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
             lo[k] = sv;
         }
         if (active) {
-            uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
+            if constexpr (IL) {
 #pragma unroll
-            for (int k = 0; k < C::LPL; ++k)
-                if (lane + 32 * k < 2 * mr) po[32 * k] = lo[k];
+                for (int k = 0; k < C::LPL; ++k)
+                    if (lane + 32 * k < 2 * mr) out[size_t(lane + 32 * k) * batch + pair] = lo[k];
+            } else {
+                uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
+#pragma unroll
+                for (int k = 0; k < C::LPL; ++k)
+                    if (lane + 32 * k < 2 * mr) po[32 * k] = lo[k];
+            }
         }
     }
 }
 
-template <int NB>
+template <int NB, bool IL = false>
 cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch, int mr, cudaStream_t st) {
     using C = ImmaCfg<NB>;
-    const size_t smem = size_t(kImmaWarps) * C::WARP_WORDS * sizeof(uint32_t);
+    const size_t smem = size_t(kImmaWarps) * (IL ? C::WARP_WORDS - C::RAW_WORDS : C::WARP_WORDS) * sizeof(uint32_t);
     // per (host thread, device): the smem opt-in is a per-device function attribute
     static thread_local struct { int dev = -1, grid_cap = 0; } di;
     int dev = 0;
@@ -359,17 +395,17 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(k_mul_imma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            cudaError_t e = cudaFuncSetAttribute(k_mul_imma<NB, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             if (e != cudaSuccess) return e;
         }
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mul_imma<NB>, kImmaWarps * 32, smem);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mul_imma<NB, IL>, kImmaWarps * 32, smem);
         if (e != cudaSuccess) return e;
         di.grid_cap = sms * (per_sm > 0 ? per_sm : 1);
         di.dev = dev;
     }
     const size_t need = (batch + kImmaWarps - 1) / kImmaWarps;
     const size_t grid = need < size_t(di.grid_cap) ? need : size_t(di.grid_cap);
-    k_mul_imma<NB><<<unsigned(grid), kImmaWarps * 32, smem, st>>>(out, a, b, batch, mr);
+    k_mul_imma<NB, IL><<<unsigned(grid), kImmaWarps * 32, smem, st>>>(out, a, b, batch, mr);
     count_launch();
     return cudaGetLastError();
 }
@@ -390,6 +426,18 @@ cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b,
         case 128: return run_imma<32>(out, a, b, batch, mr, st);
         default: return cudaErrorNotSupported;
     }
+}
+
+// Interleaved [m][batch] operands and product, read and written in place (m in {32, 64,
+// 128}, and even 16 < m < 128 zero-extended in registers).
+cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                               cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    if (m % 2 != 0 || m <= 16 || m > 128) return cudaErrorNotSupported;
+    const int mr = int(m);
+    if (m <= 32) return run_imma<8, true>(out, a, b, batch, mr, st);
+    if (m <= 64) return run_imma<16, true>(out, a, b, batch, mr, st);
+    return run_imma<32, true>(out, a, b, batch, mr, st);
 }
 
 // Even 16 < m < 128 with 16-byte aligned rows: the next tensor-pipe size's kernel with the

@@ -299,10 +299,33 @@ int main() {
             CHECK(sb.phase4_rate() == 1.0);
         }
     });
-    run("tick collection is rejected, counters without ticks work", [] {
-        AddSubStats st;
+    run("tick collection: phase laps of the timed kernel, results and counters unchanged", [] {
+        // (addsub.hpp:57-63; acceptance-style check of bench.cpp:227-247's phase split)
+        std::mt19937_64 rng(41);
+        for (const std::size_t m : {4u, 64u, 256u}) {
+            Limbs a(m), b(m);
+            for (auto& x : a) x = rng();
+            for (auto& x : b) x = rng();
+            AddSubStats st, plain;
+            st.collect_ticks = true;
+            const WordsResult r = dot_add_words(a, b, Width::w8, &st);
+            const WordsResult q = dot_add_words(a, b, Width::w8, &plain);
+            CHECK(r.limbs == q.limbs && r.flag == q.flag);
+            CHECK(st.chunks_processed == plain.chunks_processed && st.phase4_triggers == plain.phase4_triggers);
+            CHECK(st.load_ticks > 0 && st.add_ticks > 0 && st.carry_gen_ticks > 0 && st.carry_add_ticks > 0 &&
+                  st.store_ticks > 0 && st.overflow_ticks == 0);
+            CHECK(st.carry_to_add_ratio() > 0.0);
+            Limbs o(m);  // span form, exact aliasing out == a
+            Limbs a2 = a;
+            AddSubStats sa;
+            sa.collect_ticks = true;
+            CHECK(dot_add_words(std::span<limb_t>(a2), std::span<const limb_t>(a2), std::span<const limb_t>(b),
+                                Width::w8, &sa) == r.flag);
+            CHECK(a2 == r.limbs && sa.chunks_processed == plain.chunks_processed);
+        }
+        AddSubStats st;  // lengths outside the timed kernel's cover are rejected
         st.collect_ticks = true;
-        CHECK_THROWS_AS(dot_add_words(Limbs(4, 1), Limbs(4, 1), Width::w8, &st), std::logic_error);
+        CHECK_THROWS_AS(dot_add_words(Limbs(5, 1), Limbs(5, 1), Width::w8, &st), std::logic_error);
     });
     run("one-limb product is exactly the two-limb scalar product", [] {  // test_mul.cpp:323-331
         std::mt19937_64 rng(21);

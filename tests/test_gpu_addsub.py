@@ -41,6 +41,25 @@ def test_batch_matches_oracle(cuda, oracle, m):
                 assert np.array_equal(gf, wf), (m, cat, op, layout)
 
 
+@pytest.mark.parametrize("m,batch", [(1025, 64), (1500, 33), (4100, 40), (8200, 3)])
+def test_interleaved_two_pass(cuda, oracle, m, batch):
+    """Interleaved numbers longer than 1024 limbs: the two streaming passes (segments of 8
+    limbs resolved with carry-in 0, then the per-pair carry scan and prefix fix-up),
+    including propagate runs across many segments and the flags."""
+    rng = np.random.default_rng(7000 + m)
+    for cat in ("random", "full_propagation", "spiky", "maxed_limbs"):
+        for op in ("add", "sub"):
+            a, b = category(rng, cat, op, (batch, m))
+            if cat == "random":  # a long propagate run straddling segments in some pairs
+                a[::3, 5:m - 7] = np.uint64(0xFFFFFFFFFFFFFFFF) if op == "add" else b[::3, 5:m - 7]
+                if op == "add":
+                    b[::3, 5:m - 7] = 0
+            want, wf = oracle.addsub_batch(op == "sub", a, b)
+            got, gf = run(cuda, op == "sub", a, b, "interleaved")
+            assert np.array_equal(got, want), (m, cat, op)
+            assert np.array_equal(gf, wf), (m, cat, op)
+
+
 @pytest.mark.parametrize("m,batch", [(128, 128), (200, 130), (256, 64), (256, 190), (129, 66), (257, 40),
                                      (300, 65), (384, 32), (512, 33), (513, 31), (777, 40), (1024, 33)])
 def test_interleaved_segmented(cuda, oracle, m, batch):

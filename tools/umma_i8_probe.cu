@@ -43,12 +43,12 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {  // u8 x u8 -> s
     return (2u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
-template <int N, bool TS, int NA>
+template <int N, bool TS, int NA, int NCH>
 __global__ void __launch_bounds__(128, 1) k_umma(const uint8_t* gA, const uint8_t* gB, int32_t* gD, long long* cyc,
                                                  long long* ldcyc, int iters) {
     constexpr int M = 128;
     constexpr int ATILE = M * 32;
-    constexpr int DCOLS = N;
+    constexpr int DCOLS = N * NCH;  // NCH independent accumulators, MMA i into accumulator i % NCH
     constexpr int COLS = (DCOLS + (TS ? 8 : 0)) <= 32 ? 32 : (DCOLS + (TS ? 8 : 0)) <= 64 ? 64 : (DCOLS + (TS ? 8 : 0)) <= 128 ? 128 : (DCOLS + (TS ? 8 : 0)) <= 256 ? 256 : 512;
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* sA = sm;                 // NA tiles
@@ -86,18 +86,19 @@ __global__ void __launch_bounds__(128, 1) k_umma(const uint8_t* gA, const uint8_
         }
         long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
-            const uint32_t acc = i > 0;
+            const uint32_t acc = i >= NCH;
+            const uint32_t dti = dt + uint32_t((i % NCH) * N);
             if (TS) {
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dti),
                     "r"(at), "l"(bd), "r"(id), "r"(acc)
                     : "memory");
             } else {
                 const uint64_t ad = sdesc(smem_u32(sA + (i % NA) * ATILE), 128, 256);
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(dti),
                     "l"(ad), "l"(bd), "r"(id), "r"(acc)
                     : "memory");
             }
@@ -129,8 +130,8 @@ __global__ void __launch_bounds__(128, 1) k_umma(const uint8_t* gA, const uint8_
               "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(dt + (uint32_t(warp * 32) << 16) + uint32_t(c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (blockIdx.x == 0)
-            for (int j = 0; j < 16; ++j) gD[(warp * 32 + (tid & 31)) * N + c0 + j] = int32_t(v[j]);
+        if (blockIdx.x == 0 && c0 < N)
+            for (int j = 0; j < 16 && c0 + j < N; ++j) gD[(warp * 32 + (tid & 31)) * N + c0 + j] = int32_t(v[j]);
         acc ^= v[0];
     }
     // TMEM read throughput: 64 more x16 loads per warp, all 4 warps at once
@@ -157,8 +158,8 @@ __global__ void __launch_bounds__(128, 1) k_umma(const uint8_t* gA, const uint8_
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(COLS) : "memory");
 }
 
-template <int N, bool TS, int NA>
-void run(int sms, int clk_mhz) {
+template <int N, bool TS, int NA, int NCH = 1>
+void run(int sms, int clk_mhz, int per_sm = 1) {
     constexpr int M = 128;
     const int iters = 2048;
     std::vector<uint8_t> A(M * 32), B(N * 32);
@@ -171,46 +172,52 @@ void run(int sms, int clk_mhz) {
     CK(cudaMalloc(&dA, A.size()));
     CK(cudaMalloc(&dB, B.size()));
     CK(cudaMalloc(&dD, sizeof(int32_t) * M * N));
-    CK(cudaMalloc(&dc, sizeof(long long) * sms));
-    CK(cudaMalloc(&dl, sizeof(long long) * sms));
+    CK(cudaMalloc(&dc, sizeof(long long) * sms * per_sm));
+    CK(cudaMalloc(&dl, sizeof(long long) * sms * per_sm));
     CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
     const int smem = NA * M * 32 + N * 32;
-    CK(cudaFuncSetAttribute(k_umma<N, TS, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_umma<N, TS, NA><<<sms, 128, smem>>>(dA, dB, dD, dc, dl, iters);  // warm
+    CK(cudaFuncSetAttribute(k_umma<N, TS, NA, NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_umma<N, TS, NA, NCH><<<sms * per_sm, 128, smem>>>(dA, dB, dD, dc, dl, iters);  // warm
     CK(cudaDeviceSynchronize());
-    k_umma<N, TS, NA><<<sms, 128, smem>>>(dA, dB, dD, dc, dl, iters);
+    k_umma<N, TS, NA, NCH><<<sms * per_sm, 128, smem>>>(dA, dB, dD, dc, dl, iters);
     CK(cudaDeviceSynchronize());
     std::vector<int32_t> D(M * N);
-    std::vector<long long> c(sms), l(sms);
+    const int nct = sms * per_sm;
+    std::vector<long long> c(nct), l(nct);
     CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(c.data(), dc, sms * 8, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(l.data(), dl, sms * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(c.data(), dc, nct * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(l.data(), dl, nct * 8, cudaMemcpyDeviceToHost));
     long long bad = 0;
     for (int r = 0; r < M; ++r)
         for (int n = 0; n < N; ++n) {
             long long want = 0;
-            const int na = TS ? 1 : NA;  // MMA i uses A tile i % na: iters / na MMAs per tile
-            for (int t = 0; t < na; ++t) {
+            const int na = TS ? 1 : NA;  // accumulator 0 takes MMAs i = 0, NCH, ...: A tile i % na
+            for (int i = 0; i < iters; i += NCH) {
+                const int t = i % na;
                 int dot = 0;
                 for (int k = 0; k < 32; ++k) dot += int(uint8_t(A[r * 32 + k] + t)) * int(B[n * 32 + k]);
-                want += (long long)dot * (iters / na);
+                want += dot;
+                if (na == 1) {
+                    want = (long long)dot * (iters / NCH);
+                    break;
+                }
             }
             if (D[r * N + n] != int32_t(want)) ++bad;
         }
     double cm = 0, lm = 0;
-    for (int i = 0; i < sms; ++i) cm += c[i], lm += l[i];
-    cm /= sms;
-    lm /= sms;
+    for (int i = 0; i < nct; ++i) cm += c[i], lm += l[i];
+    cm /= nct;
+    lm /= nct;
     const double clk_per_mma = cm / iters;
     const double macs = double(M) * N * 32;
     // TMEM read: 4 warps x 64 loads x 32 lanes x 16 words x 4 B
     const double ld_bytes = 4.0 * 64 * 32 * 16 * 4;
     std::printf(
-        "{\"M\": %d, \"N\": %d, \"K\": 32, \"mode\": \"%s\", \"distinct_A_tiles\": %d, \"clk_per_mma\": %.2f, "
+        "{\"M\": %d, \"N\": %d, \"K\": 32, \"mode\": \"%s\", \"distinct_A_tiles\": %d, \"accumulators\": %d, \"ctas_per_sm\": %d, \"clk_per_mma\": %.2f, "
         "\"macs_per_clk_sm\": %.1f, \"smem_bytes_per_mma\": %d, \"smem_B_per_clk\": %.1f, "
         "\"tmem_ld_B_per_clk\": %.1f, \"check\": \"%s\", \"mismatches\": %lld}\n",
-        M, N, TS ? "TS (A in TMEM)" : "SS (A, B in smem)", TS ? 1 : NA, clk_per_mma, macs / clk_per_mma,
+        M, N, TS ? "TS (A in TMEM)" : "SS (A, B in smem)", TS ? 1 : NA, NCH, per_sm, clk_per_mma, per_sm * macs / clk_per_mma,
         (TS ? 0 : M * 32) + N * 32, ((TS ? 0 : M * 32) + N * 32) / clk_per_mma, ld_bytes / lm, bad ? "FAIL" : "ok", bad);
     (void)clk_mhz;
     cudaFree(dA);
@@ -239,5 +246,18 @@ int main() {
     run<256, false, 1>(sms, clk);
     run<256, false, 4>(sms, clk);
     run<256, true, 1>(sms, clk);
+    // independent accumulators (no dependent accumulate between consecutive MMAs)
+    run<16, false, 4, 8>(sms, clk);
+    run<16, true, 1, 8>(sms, clk);
+    run<16, true, 1, 16>(sms, clk);
+    run<32, false, 4, 8>(sms, clk);
+    run<32, true, 1, 8>(sms, clk);
+    run<64, false, 4, 4>(sms, clk);
+    run<64, true, 1, 4>(sms, clk);
+    // several CTAs per SM, each with its own issuing thread and accumulators
+    run<16, false, 4, 8>(sms, clk, 4);
+    run<16, true, 1, 8>(sms, clk, 4);
+    run<32, true, 1, 4>(sms, clk, 4);
+    run<16, true, 1, 1>(sms, clk, 4);
     return 0;
 }
