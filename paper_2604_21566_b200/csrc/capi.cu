@@ -178,6 +178,18 @@ size_t mul_slice_bytes() {
     return v;
 }
 
+// Long-number host calls stream larger slices than batches (tools/c5_host_probe.py, 2^30
+// limbs, pinned: 8 MB 62.6, 24 MB 64.3, 48 MB 74.1 GB/s vs 74.7 GB/s moving the same bytes
+// with no kernels). DOTG_HOST_WORDS_SLICE_MB, input MB per slice (a and b), default 48.
+size_t words_slice_bytes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("DOTG_HOST_WORDS_SLICE_MB");
+        const long x = e ? std::atol(e) : 48;
+        return size_t(x < 1 ? 1 : x) << 20;
+    }();
+    return v;
+}
+
 struct HostCtx {
     std::mutex mu;
     int device = -1;
@@ -186,6 +198,8 @@ struct HostCtx {
     size_t cap = 0;  // bytes per slot
     char* flat = nullptr;  // whole-call device image (flat pipeline)
     size_t flat_cap = 0;
+    char* ring = nullptr;  // long-number slice ring (words_host)
+    size_t ring_cap = 0;
     std::vector<cudaEvent_t> ev;
 };
 HostCtx g_host;
@@ -203,6 +217,9 @@ int host_prepare(size_t bytes_per_slot) {
         if (g_host.flat) cudaFree(g_host.flat);
         g_host.flat = nullptr;
         g_host.flat_cap = 0;
+        if (g_host.ring) cudaFree(g_host.ring);
+        g_host.ring = nullptr;
+        g_host.ring_cap = 0;
         for (cudaEvent_t ev : g_host.ev) cudaEventDestroy(ev);
         g_host.ev.clear();  // events belong to the previous device
         for (int i = 0; i < kNS; ++i) {
@@ -431,12 +448,15 @@ int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint
     return run_host_jobs(&j, 1);
 }
 
-// Single long number from host spans: slices are independent shards (dotg_shard_*). H2D
-// of slice k+1 overlaps the streaming pass of slice k (two upload streams), and slice k's
-// fix-up needs only the aggregates of slices 0..k - a carry scan ACROSS slices, in slice
-// order - so it runs on a third stream as soon as slice k's local pass is done, followed
-// by slice k's D2H: downloads overlap the remaining uploads (the two copy engines work at
-// once) instead of waiting for the whole number to be resident.
+// Single long number from host spans through a RING of kRing device slots (a slice of a,
+// b, out and its tile state each), never a whole device image: the number can exceed
+// device memory, and nothing is mapped per call. Slices are independent shards
+// (dotg_shard_*): uploads in order on one stream, the streaming pass of slice k on a second
+// (as soon as its upload lands), and - because slice k's fix-up needs only the aggregates
+// of slices 0..k, a carry scan ACROSS slices in slice order - its fix-up and download on a
+// third right after its pass. The upload of slice k + kRing waits only for the download of
+// slice k (same slot). H2D, kernels and D2H of different slices run concurrently.
+constexpr int kRing = 6;
 int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
     int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
     if (rc != DOTG_OK) return rc;
@@ -447,55 +467,65 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
     if ((rc = check_device()) != DOTG_OK) return rc;
     std::lock_guard<std::mutex> lk(g_host.mu);
     if ((rc = host_prepare(256)) != DOTG_OK) return rc;
-    const size_t slice = std::max<size_t>(4096, (slice_bytes() / 16) / 4096 * 4096);
+    const size_t slice = std::max<size_t>(4096, (words_slice_bytes() / 16) / 4096 * 4096);
     const size_t nsl = (m + slice - 1) / slice;
     const size_t sb = align_up(dotg::long_state_bytes(slice), 256);
-    const size_t ab = align_up(m * 8, 256);
-    char* base = nullptr;
-    cudaStream_t s0 = g_host.s[0], s1 = g_host.s[1], sf = g_host.s[2];
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&base), 3 * ab + nsl * sb + align_up(nsl * 8, 256) + 256, s0);
-    if (e != cudaSuccess) return fail(DOTG_ENOMEM, std::string("words_host: ") + cudaGetErrorString(e));
-    uint64_t* da = reinterpret_cast<uint64_t*>(base);
-    uint64_t* db = reinterpret_cast<uint64_t*>(base + ab);
-    uint64_t* dout = reinterpret_cast<uint64_t*>(base + 2 * ab);
-    char* states = base + 3 * ab;
-    uint32_t* aggs = reinterpret_cast<uint32_t*>(states + nsl * sb);
+    const size_t ab = align_up(slice * 8, 256);
+    const size_t slot_bytes = 3 * ab + sb;
+    const size_t ring_bytes = size_t(kRing) * slot_bytes + align_up(nsl * 8, 256) + 256;
+    cudaError_t e = cudaSuccess;
+    if (g_host.ring_cap < ring_bytes) {
+        if (g_host.ring) cudaFree(g_host.ring);
+        g_host.ring = nullptr;
+        g_host.ring_cap = 0;
+        if ((e = cudaMalloc(&g_host.ring, ring_bytes)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(DOTG_ENOMEM, std::string("words_host ring: ") + cudaGetErrorString(e));
+        }
+        g_host.ring_cap = ring_bytes;
+    }
+    char* base = g_host.ring;
+    uint32_t* aggs = reinterpret_cast<uint32_t*>(base + size_t(kRing) * slot_bytes);
     uint32_t* dcarry = aggs + 2 * nsl;
-    while (e == cudaSuccess && g_host.ev.size() < nsl + 1) {
+    // events: [0, kRing) upload done per slot, [kRing, 2 kRing) pass done per slot,
+    // [2 kRing, 3 kRing) download done per slot
+    while (e == cudaSuccess && g_host.ev.size() < size_t(3 * kRing)) {
         cudaEvent_t ev;
         e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         if (e == cudaSuccess) g_host.ev.push_back(ev);
     }
-    cudaEvent_t ev_alloc = e == cudaSuccess ? g_host.ev[nsl] : nullptr;
-    if (e == cudaSuccess) e = cudaEventRecord(ev_alloc, s0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s1, ev_alloc, 0);  // allocation visible on s1 and sf
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(sf, ev_alloc, 0);
+    cudaStream_t su = g_host.s[0], sk = g_host.s[1], sf = g_host.s[2];
     for (size_t k = 0; k < nsl && e == cudaSuccess; ++k) {
         const size_t l0 = k * slice, n = std::min(slice, m - l0);
-        cudaStream_t st = (k & 1) ? s1 : s0;
-        e = cudaMemcpyAsync(da + l0, a + l0, n * 8, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(db + l0, b + l0, n * 8, cudaMemcpyHostToDevice, st);
+        const int q = int(k % kRing);
+        char* slot = base + size_t(q) * slot_bytes;
+        uint64_t* da = reinterpret_cast<uint64_t*>(slot);
+        uint64_t* db = reinterpret_cast<uint64_t*>(slot + ab);
+        uint64_t* dout = reinterpret_cast<uint64_t*>(slot + 2 * ab);
+        void* state = slot + 3 * ab;
+        cudaEvent_t ev_up = g_host.ev[q], ev_pass = g_host.ev[kRing + q], ev_down = g_host.ev[2 * kRing + q];
+        if (k >= size_t(kRing)) e = cudaStreamWaitEvent(su, ev_down, 0);  // slot free again
+        if (e == cudaSuccess) e = cudaMemcpyAsync(da, a + l0, n * 8, cudaMemcpyHostToDevice, su);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db, b + l0, n * 8, cudaMemcpyHostToDevice, su);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_up, su);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, ev_up, 0);
+        if (e == cudaSuccess) e = dotg::launch_long_local(sub, dout, da, db, n, state, aggs + 2 * k, sk);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_pass, sk);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sf, ev_pass, 0);
         if (e == cudaSuccess)
-            e = dotg::launch_long_local(sub, dout + l0, da + l0, db + l0, n, states + k * sb, aggs + 2 * k, st);
-        if (e == cudaSuccess) e = cudaEventRecord(g_host.ev[k], st);
-        // fix-up of slice k: carry-in = (G, P) scan over slices 0..k-1, whose local passes
-        // sf has already waited for (it handles the slices in order)
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(sf, g_host.ev[k], 0);
-        if (e == cudaSuccess)
-            e = dotg::launch_long_finish(sub, dout + l0, n, states + k * sb, aggs, int(k), int(k + 1),
-                                         k + 1 == nsl ? dcarry : nullptr, sf);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(out + l0, dout + l0, n * 8, cudaMemcpyDeviceToHost, sf);
+            e = dotg::launch_long_finish(sub, dout, n, state, aggs, int(k), int(k + 1), k + 1 == nsl ? dcarry : nullptr,
+                                         sf);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out + l0, dout, n * 8, cudaMemcpyDeviceToHost, sf);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_down, sf);
     }
     uint32_t hc = 0;
     if (e == cudaSuccess) e = cudaMemcpyAsync(&hc, dcarry, 4, cudaMemcpyDeviceToHost, sf);
-    cudaError_t e2 = cudaFreeAsync(base, sf);  // sf has waited for every upload stream's work
     cudaError_t e3 = cudaSuccess;
-    for (cudaStream_t x : {s0, s1, sf}) {
+    for (cudaStream_t x : {su, sk, sf}) {
         cudaError_t y = cudaStreamSynchronize(x);
         if (e3 == cudaSuccess) e3 = y;
     }
     if (e != cudaSuccess) return cuda_fail(e, "dotg words host");
-    if (e2 != cudaSuccess) return cuda_fail(e2, "free");
     if (e3 != cudaSuccess) return cuda_fail(e3, "sync");
     if (carry) *carry = hc;
     return DOTG_OK;
