@@ -157,14 +157,16 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 #define DOTG_IMMA_MINB16 1
 #endif
 // IL = true: the batch-interleaved layout [m][batch] (limb i of pair p at i * batch + p),
-// read in place - no transposes. A warp's operand words come straight from global memory
-// with one 8-byte load per limb (the 4 warps of a CTA take 4 consecutive pairs, so every
-// 32-byte sector is used whole across them in L1 / L2 and DRAM sees each byte once), held
-// one pair ahead in registers instead of the bulk-copy ring; products are stored at
-// out[L * batch + p] (the 4 warps again fill the sectors). Row-major (IL = false) uses the
-// mbarrier ring of cp.async.bulk copies.
+// read and written in place - no transposes. The 4 warps of a CTA take 4 consecutive
+// pairs at a time; the CTA loads their [m][4] operand tiles cooperatively (4 lanes per
+// 32-byte limb row: 8 sectors per warp instruction, where a warp loading its own pair
+// touched 32), one group ahead in registers, into padded shared tiles each warp reads its
+// pair from; products go back the same way through a [2m][4] tile. (r02 first version,
+// every warp loading its own pair: L1 92% busy, 139 us at m = 64.) Row-major (IL = false)
+// uses the per-warp mbarrier ring of cp.async.bulk copies.
+constexpr int kTileP = 9;  // words per [.][4 pairs] tile row: 8 + 1 pad (odd: conflict-free columns)
 template <int NB, bool IL>
-__global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 : 1) k_mul_imma(uint64_t* __restrict__ out,
+__global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMMA_MINB16) : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b, size_t batch,
                                                               int mr) {
@@ -181,6 +183,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
     int* S = reinterpret_cast<int*>(sa + C::A_WORDS);         // column sums
     __shared__ uint64_t bars[kImmaWarps][C::ST];
     uint64_t* bar = bars[warp];
+    // IL tiles: operands [2][M][kTileP], product [2M][kTileP] (u32 words)
+    __shared__ uint32_t til[IL ? 2 * C::M * kTileP : 1], tol[IL ? 2 * C::M * kTileP : 1];
     for (int i = lane; i < C::COPY_WORDS + C::A_WORDS; i += 32) cp[i] = 0;  // padding stays zero
     if (!IL && mr < C::M)
         for (int i = lane; i < C::RAW_WORDS; i += 32) raw[i] = 0;
@@ -208,20 +212,25 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
     // IL: lane's VW operand words of a pair = limbs VW/2 * lane ... (VW even for m >= 32)
     static_assert(!IL || (C::VW % 2 == 0), "interleaved route needs two or more words per lane");
     constexpr int LL = C::VW / 2 > 0 ? C::VW / 2 : 1;  // limbs per lane
-    uint64_t na[LL], nb[LL];
-    auto il_load = [&](size_t pr) {
+    constexpr int RP = C::M / 32 > 0 ? C::M / 32 : 1;  // tile rows per thread per operand
+    const int trow = threadIdx.x >> 2, tp = threadIdx.x & 3;  // cooperative load: row, pair in group
+    const size_t ngroups = (batch + 3) / 4;
+    uint64_t na[RP], nb[RP];
+    auto il_load = [&](size_t grp) {
+        const size_t pr = grp * 4 + size_t(tp);
 #pragma unroll
-        for (int e = 0; e < LL; ++e) {
-            const size_t L = size_t(lane) * LL + e;
-            const bool okl = pr < batch && lane < C::LD_LANES && int(L) < mr;
-            na[e] = okl ? __ldg(a + L * batch + pr) : 0ull;
-            nb[e] = okl ? __ldg(b + L * batch + pr) : 0ull;
+        for (int j = 0; j < RP; ++j) {
+            const int r = trow + 32 * j;
+            const bool okl = grp < ngroups && pr < batch && r < mr;
+            na[j] = okl ? __ldg(a + size_t(r) * batch + pr) : 0ull;
+            nb[j] = okl ? __ldg(b + size_t(r) * batch + pr) : 0ull;
         }
     };
-    if (IL) il_load(first);
+    if (IL) il_load(blockIdx.x);
     int stage = 0;
     uint32_t parity = 0;
-    for (size_t pair = first; pair < batch; pair += nwarps) {
+    for (size_t grp = blockIdx.x, pair = IL ? size_t(blockIdx.x) * 4 + warp : first; IL ? grp < ngroups : pair < batch;
+         grp += gridDim.x, pair += nwarps) {
         if (!IL) mbar_wait(&bar[stage], parity);
         // ---- stage: copy_s[i] = bytes bpad[4i + s ..], bpad[y] = b[y - 31]; word j of b
         // feeds copy index i = j + 8 (with word j + 1), and i = 7 takes (0, b[0]).
@@ -231,13 +240,25 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
             uint32_t bv[C::VW + 1], av[C::VW];
             if constexpr (IL) {
 #pragma unroll
-                for (int e = 0; e < LL; ++e) {
-                    av[2 * e] = uint32_t(na[e]);
-                    av[2 * e + 1] = uint32_t(na[e] >> 32);
-                    bv[2 * e] = uint32_t(nb[e]);
-                    bv[2 * e + 1] = uint32_t(nb[e] >> 32);
+                for (int j = 0; j < RP; ++j) {
+                    const int r = trow + 32 * j;
+                    uint32_t* ta = til + r * kTileP + 2 * tp;
+                    uint32_t* tb = til + (C::M + r) * kTileP + 2 * tp;
+                    ta[0] = uint32_t(na[j]);
+                    ta[1] = uint32_t(na[j] >> 32);
+                    tb[0] = uint32_t(nb[j]);
+                    tb[1] = uint32_t(nb[j] >> 32);
                 }
-                il_load(pair + nwarps);  // next pair's operands in flight during this one
+                __syncthreads();
+                il_load(grp + gridDim.x);  // the next group's operands in flight during this one
+#pragma unroll
+                for (int e = 0; e < LL; ++e) {
+                    const int L = lane * LL + e;
+                    av[2 * e] = til[L * kTileP + 2 * warp];
+                    av[2 * e + 1] = til[L * kTileP + 2 * warp + 1];
+                    bv[2 * e] = til[(C::M + L) * kTileP + 2 * warp];
+                    bv[2 * e + 1] = til[(C::M + L) * kTileP + 2 * warp + 1];
+                }
             } else if (lane < C::LD_LANES) {
                 lds_vec<C::VW>(rb + lane * C::VW, bv);
                 lds_vec<C::VW>(ra + lane * C::VW, av);
@@ -368,12 +389,27 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? DOTG_IMMA_MINB16 :
             sv += (C >> lane) & 1u;
             lo[k] = sv;
         }
-        if (active) {
-            if constexpr (IL) {
+        if constexpr (IL) {
+            // product limbs into the [2M][4] tile, then the CTA stores whole 32-byte rows
+            if (active)
 #pragma unroll
-                for (int k = 0; k < C::LPL; ++k)
-                    if (lane + 32 * k < 2 * mr) out[size_t(lane + 32 * k) * batch + pair] = lo[k];
-            } else {
+                for (int k = 0; k < C::LPL; ++k) {
+                    uint32_t* to = tol + (lane + 32 * k) * kTileP + 2 * warp;
+                    to[0] = uint32_t(lo[k]);
+                    to[1] = uint32_t(lo[k] >> 32);
+                }
+            __syncthreads();
+            const size_t pr = grp * 4 + size_t(tp);
+#pragma unroll
+            for (int j = 0; j < 2 * RP; ++j) {
+                const int r = trow + 32 * j;
+                if (r < 2 * mr && pr < batch) {
+                    const uint32_t* to = tol + r * kTileP + 2 * tp;
+                    out[size_t(r) * batch + pr] = uint64_t(to[0]) | (uint64_t(to[1]) << 32);
+                }
+            }
+        } else if (active) {
+            {
                 uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
 #pragma unroll
                 for (int k = 0; k < C::LPL; ++k)
