@@ -223,8 +223,9 @@ def sub_w_limbs(a, b, borrow_in: int, w: int) -> ChunkResult:
 
 def dot_mul_words(a, b, cfg: int = 64, width=Width.w8) -> np.ndarray:
     """Exact product, exactly 2m limbs (include/dot/mul.hpp:75-76, src/mul.cpp:96-103).
-    Equal limb counts 1 <= m <= 2^24 (mul.cpp:13-18). Only the saturated 64-bit radix is
-    on the device path (the 52-bit route is out of scope)."""
+    Equal limb counts 1 <= m <= 2^24 (mul.cpp:13-18). cfg = 64 (kSaturated) runs the
+    batched column / tensor-pipe / Karatsuba routes; cfg = 52 (kUnsaturated, limbs
+    < 2^52) runs k_mul52 (dotg_mul52_batch_host), both on the device."""
     if int(cfg) not in (64, 52):
         raise InvalidArgument("RadixConfig: limb_bits must be 64 or 52")  # limbs.cpp:22-24
     _validate_width(width)
