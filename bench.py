@@ -776,6 +776,59 @@ def run_ours(args, rank, world, dist):
         except Exception as e:  # noqa: BLE001
             cpu_baseline = {"value": None, "unit": "GB/s", "cores": 0, "kind": "unavailable", "sample": str(e)}
 
+    # per-call latency of the drop-in span form on ONE 4096-bit number (how the reference's
+    # own callers use dot_add_words, e.g. Karatsuba's add_at, mul.cpp:169-174), beside the
+    # reference's span call on one core; and one device-resident call (batch of 1)
+    latency = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            import numpy as np
+
+            m1 = 64
+            ha1 = np.ascontiguousarray(bufs[2]["a"][0].cpu().numpy().view(np.uint64))
+            hb1 = np.ascontiguousarray(bufs[2]["b"][0].cpu().numpy().view(np.uint64))
+            ho1 = np.empty(m1, np.uint64)
+            c1 = ctypes.c_uint32(0)
+            P1 = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+            for _ in range(20):
+                lib.dotg_add_words_host(P1(ho1), P1(ha1), P1(hb1), m1, ctypes.byref(c1))
+            n1 = 2000
+            t0 = time.perf_counter()
+            for _ in range(n1):
+                lib.dotg_add_words_host(P1(ho1), P1(ha1), P1(hb1), m1, ctypes.byref(c1))
+            host_us = (time.perf_counter() - t0) / n1 * 1e6
+            d_o = torch.empty(m1, dtype=torch.int64, device="cuda")
+            d_c = torch.empty(1, dtype=torch.int32, device="cuda")
+            da1, db1 = bufs[2]["a"][0], bufs[2]["b"][0]
+            dcall = lambda: lib.dotg_add_batch(ctypes.c_void_p(d_o.data_ptr()), ctypes.c_void_p(da1.data_ptr()),  # noqa: E731
+                                               ctypes.c_void_p(db1.data_ptr()), ctypes.c_void_p(d_c.data_ptr()), m1,
+                                               1, 0, L.stream)
+            for _ in range(20):
+                dcall()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(n1):
+                dcall()
+            torch.cuda.synchronize()
+            dev_us = (time.perf_counter() - t0) / n1 * 1e6
+            cpu = CpuRef()
+            ref_ns = None
+            if cpu.kind == "reference":
+                co = np.empty(m1, np.uint64)
+                cpu.words(0, co, ha1, hb1)
+                t0 = time.perf_counter()
+                for _ in range(n1):
+                    cpu.words(0, co, ha1, hb1)
+                ref_ns = (time.perf_counter() - t0) / n1 * 1e9
+            latency = {"m": m1, "dropin_host_span_us": host_us, "device_call_us": dev_us,
+                       "reference_span_ns_incl_ctypes": ref_ns,
+                       "note": "one 4096-bit add per call: host span form (H2D, kernel, D2H, sync) and the "
+                               "device-pointer C ABI back to back (launch-bound), vs the reference's span call "
+                               "through ctypes on one core (~53 ns natively, profiles/r01_cpu_table.json). Single "
+                               "small numbers belong on the CPU or in a batch / CUDA graph."}
+        except Exception as e:  # noqa: BLE001
+            latency = {"error": str(e)[:200]}
+
     # free the headline buffers before the secondary configs
     del bufs, calls, single_calls, sets, graphs
     torch.cuda.synchronize()
@@ -809,6 +862,7 @@ def run_ours(args, rank, world, dist):
         "clocks": clocks,
         "carry_stress": stress,
         "phase_split": phase_split,
+        "call_latency": latency,
         "configs": secondary,
     }
     if weak is not None:
