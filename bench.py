@@ -1109,6 +1109,32 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                               "peak": hbm_peak}
         torch.cuda.empty_cache()
 
+    # ---------------- 256-bit base cases: dot_mul_5x5 / dot_mul_4x4 shapes ----------------
+    if want("R52") and world == 1 and not args.no_layouts:
+        r52 = {}
+        Bq = 1 << 21
+        for name, m, fn, mask in (("mul52_5x5", 5, lib.dotg_mul52_batch, (1 << 52) - 1),
+                                  ("mul64_4x4", 4, None, None)):
+            a = W.fill(Bq * m, 0x52 + m, 0).view(Bq, m)
+            b = W.fill(Bq * m, 0x52 + m, 1 << 40).view(Bq, m)
+            if mask is not None:
+                a &= mask
+                b &= mask
+            o = torch.empty((Bq, 2 * m), dtype=torch.int64, device="cuda")
+
+            def mk(Lc, fn=fn, o=o, a=a, b=b, m=m):
+                if fn is None:
+                    return [Lc.mul(o, a, b, m, Bq)]
+                args_ = (P(o), P(a), P(b), m, Bq, Lc.stream)
+                return [lambda: fn(*args_)]
+            us = per_launch_us(torch, dg, lib, stream, mk)
+            byts = Bq * 32 * m
+            r52[name] = {"pairs_s": Bq / (us * 1e-6), "us": us, "hbm_gbs": byts / (us * 1e-6) / 1e9,
+                         "frac_hbm": byts / (us * 1e-6) / 1e9 / hbm_peak, "batch": Bq}
+            del a, b, o
+        out["base_case_256bit"] = r52
+        torch.cuda.empty_cache()
+
     # ---------------- C5: one 2^30-limb add / sub ----------------
     if not args.no_c5 and want("C5"):
         from paper_2604_21566_b200.sharded import CommShardedWords, ShardedWords, shard_bounds

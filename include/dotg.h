@@ -131,6 +131,11 @@ int dotg_set_mul_route(int route);
  * limb must be < 2^52 (check_limbs, limbs.cpp:26-33 -> DOTG_EINVAL); exactly 2m output
  * limbs, each < 2^52. */
 int dotg_mul52_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch);
+/* Device-pointer form (stream-ordered): the caller guarantees every limb < 2^52 (the host
+ * form above validates them like check_limbs); a wider limb yields an unspecified
+ * product. Row-major [batch][m] -> [batch][2m]. */
+int dotg_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                     dotg_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * Batched Karatsuba (reference karatsuba_mul / kara_rec, mul.hpp:87-102,

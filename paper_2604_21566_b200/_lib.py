@@ -29,6 +29,7 @@ SIGNATURES = {
     "dotg_addsub_grouped": (c_int, [_P, c_int, _P]),
     "dotg_mul_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_int, _P]),
     "dotg_mul52_batch_host": (c_int, [_P, _P, _P, c_size_t, c_size_t]),
+    "dotg_mul52_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, _P]),
     "dotg_karatsuba_batch": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_size_t, _P]),
     "dotg_karatsuba_batch_host": (c_int, [_P, _P, _P, c_size_t, c_size_t, c_size_t]),
     "dotg_add_words": (c_int, [_P, _P, _P, c_size_t, _P, _P]),

@@ -457,6 +457,7 @@ int batch_host(int op, uint64_t* out, const uint64_t* a, const uint64_t* b, uint
 // third right after its pass. The upload of slice k + kRing waits only for the download of
 // slice k (same slot). H2D, kernels and D2H of different slices run concurrently.
 constexpr int kRing = 6;
+constexpr size_t kWordsSmall = size_t(1) << 16;  // limbs: below, one stream and the team kernel
 int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, uint32_t* carry) {
     int rc = check_addsub(out, a, b, nullptr, m, 1, DOTG_ROW_MAJOR);
     if (rc != DOTG_OK) return rc;
@@ -467,6 +468,38 @@ int words_host(bool sub, uint64_t* out, const uint64_t* a, const uint64_t* b, si
     if ((rc = check_device()) != DOTG_OK) return rc;
     std::lock_guard<std::mutex> lk(g_host.mu);
     if ((rc = host_prepare(256)) != DOTG_OK) return rc;
+    if (m <= kWordsSmall) {
+        // one short number (the reference's per-call use, e.g. Karatsuba's add_at): one
+        // stream, the batched team kernel with batch 1, one synchronisation
+        const size_t ab = align_up(m * 8, 256);
+        if (g_host.ring_cap < 3 * ab + 256) {
+            if (g_host.ring) cudaFree(g_host.ring);
+            g_host.ring = nullptr;
+            g_host.ring_cap = 0;
+            cudaError_t ea = cudaMalloc(&g_host.ring, size_t(4) << 20);
+            if (ea != cudaSuccess) {
+                cudaGetLastError();
+                return fail(DOTG_ENOMEM, std::string("words_host: ") + cudaGetErrorString(ea));
+            }
+            g_host.ring_cap = size_t(4) << 20;
+        }
+        uint64_t* da = reinterpret_cast<uint64_t*>(g_host.ring);
+        uint64_t* db = reinterpret_cast<uint64_t*>(g_host.ring + ab);
+        uint64_t* dout = reinterpret_cast<uint64_t*>(g_host.ring + 2 * ab);
+        uint32_t* dfl = reinterpret_cast<uint32_t*>(g_host.ring + 3 * ab);
+        cudaStream_t s0 = g_host.s[0];
+        uint32_t hc = 0;
+        cudaError_t e = cudaMemcpyAsync(da, a, m * 8, cudaMemcpyHostToDevice, s0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(db, b, m * 8, cudaMemcpyHostToDevice, s0);
+        if (e == cudaSuccess) e = dotg::launch_addsub_batch(sub, dout, da, db, dfl, m, 1, 0, s0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, dout, m * 8, cudaMemcpyDeviceToHost, s0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&hc, dfl, 4, cudaMemcpyDeviceToHost, s0);
+        cudaError_t e2 = cudaStreamSynchronize(s0);
+        if (e != cudaSuccess) return cuda_fail(e, "dotg words host");
+        if (e2 != cudaSuccess) return cuda_fail(e2, "sync");
+        if (carry) *carry = hc;
+        return DOTG_OK;
+    }
     const size_t slice = std::max<size_t>(4096, (words_slice_bytes() / 16) / 4096 * 4096);
     const size_t nsl = (m + slice - 1) / slice;
     const size_t sb = align_up(dotg::long_state_bytes(slice), 256);
@@ -682,6 +715,15 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
     if ((rc = check_device()) != DOTG_OK) return rc;
     cudaError_t e = dotg::launch_mul_batch(out, a, b, m, batch, layout, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg mul batch launch");
+}
+
+int dotg_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                     dotg_stream_t stream) {
+    int rc = check_mul(out, a, b, m, batch, DOTG_ROW_MAJOR);
+    if (rc != DOTG_OK || batch == 0) return rc;
+    if ((rc = check_device()) != DOTG_OK) return rc;
+    cudaError_t e = dotg::launch_mul52_batch(out, a, b, m, batch, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DOTG_OK : cuda_fail(e, "dotg mul52 batch");
 }
 
 int dotg_mul52_batch_host(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch) {

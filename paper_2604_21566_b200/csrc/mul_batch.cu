@@ -636,6 +636,62 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // then one carry pass in radix 2^52. Thread per pair, 128-bit column accumulators
 // (a column of m pairs sums below 2m * 2^52). Exactly 2m output limbs, each < 2^52.
 // ---------------------------------------------------------------------------
+// Small m (dot_mul_5x5's m = 5, the 4x4 route's 5 after repacking, up to 16): thread per
+// pair with both operands in registers (staged by the CTA through shared memory) and
+// every 52 x 52-bit product taken ONCE (mul.lo /
+// mul.hi of the 64-bit limbs, split at bit 52: low part into column i + j, high part into
+// i + j + 1). A column of M low parts plus M high parts is < 2M * 2^52, so plain 64-bit
+// column sums are exact; one radix-2^52 carry pass (mul.cpp:70-90 at k = 52). Rows are
+// zero-extended to M limbs (zero limbs add nothing), only 2m limbs are stored.
+template <int M>
+__global__ void __launch_bounds__(128) k_mul52_regs(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                    const uint64_t* __restrict__ b, int m, size_t batch) {
+    // the CTA's 128 rows of a and b (and later its 128 products) are contiguous: staged
+    // through shared memory with coalesced loads / stores (rows of 5 limbs are 40 bytes)
+    __shared__ uint64_t buf[2 * 128 * M];  // a rows | b rows, then the products
+    uint64_t* sa = buf;
+    uint64_t* sb = buf + 128 * M;
+    uint64_t* so = buf;
+    const size_t p0 = size_t(blockIdx.x) * 128;
+    const size_t np = batch - p0 < 128 ? batch - p0 : 128;
+    const size_t nin = np * size_t(m), nout = 2 * nin;
+    for (size_t i = threadIdx.x; i < nin; i += 128) {
+        sa[i] = __ldcs(a + p0 * size_t(m) + i);
+        sb[i] = __ldcs(b + p0 * size_t(m) + i);
+    }
+    __syncthreads();
+    constexpr uint64_t kMask = (uint64_t(1) << 52) - 1;
+    uint64_t x[M], y[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        x[i] = (threadIdx.x < np && i < m) ? sa[threadIdx.x * m + i] : 0ull;
+        y[i] = (threadIdx.x < np && i < m) ? sb[threadIdx.x * m + i] : 0ull;
+    }
+    __syncthreads();  // the operand rows are in registers: the buffer takes the products
+    if (threadIdx.x < np) {
+        uint64_t col[2 * M];
+#pragma unroll
+        for (int c = 0; c < 2 * M; ++c) col[c] = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                const uint64_t lo = x[i] * y[j], hi = __umul64hi(x[i], y[j]);
+                col[i + j] += lo & kMask;
+                col[i + j + 1] += (hi << 12) | (lo >> 52);  // floor(product / 2^52) < 2^52
+            }
+        uint64_t carry = 0;
+#pragma unroll
+        for (int c = 0; c < 2 * M; ++c) {
+            const uint64_t v = col[c] + carry;  // < 2^(52 + log2(2M) + 1): no wrap
+            if (c < 2 * m) so[threadIdx.x * 2 * m + c] = v & kMask;
+            carry = v >> 52;
+        }
+    }
+    __syncthreads();
+    for (size_t i = threadIdx.x; i < nout; i += 128) __stcs(out + p0 * 2 * size_t(m) + i, so[i]);
+}
+
 __global__ void __launch_bounds__(128) k_mul52(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m,
                                                size_t batch) {
     const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -666,7 +722,12 @@ __global__ void __launch_bounds__(128) k_mul52(uint64_t* out, const uint64_t* a,
 cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
-    k_mul52<<<unsigned((batch + 127) / 128), 128, 0, st>>>(out, a, b, m, batch);
+    const unsigned grid = unsigned((batch + 127) / 128);
+    if (m <= 4) k_mul52_regs<4><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    else if (m <= 5) k_mul52_regs<5><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    else if (m <= 8) k_mul52_regs<8><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    else if (m <= 16) k_mul52_regs<16><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    else k_mul52<<<grid, 128, 0, st>>>(out, a, b, m, batch);
     count_launch();
     return cudaGetLastError();
 }
