@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "internal.h"
@@ -523,6 +524,179 @@ __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint
 }
 
 // ---------------------------------------------------------------------------
+// C3 hybrid: the Karatsuba middle product z1 = |a_hi - a_lo| * |b_hi - b_lo| (512 x 512
+// bits) on the otherwise idle FP64 pipe, z0 and z2 on the IMAD pipe as above. Exact 52 x
+// 52-bit products on FP64 (tools/dfma_sweep.cu, 2^20 cases checked): with x, y < 2^52,
+//   h = fma.rz(x, y, 2^104)  -> bits(h) = bits(2^104) + floor(xy / 2^52)
+//   l = fma.rn(x, y, (2^104 + 2^52) - h) -> bits(l) = bits(2^52) + (xy mod 2^52)
+// so the raw bit patterns are accumulated as 64-bit integers into radix-2^52 columns and
+// the constant biases (a compile-time count per column) are subtracted once. Per pair the
+// IMAD pipe issues 512 column MACs instead of 768; the FP64 pipe takes 100 products.
+// ---------------------------------------------------------------------------
+template <int V>
+__device__ __forceinline__ void ld_cached(const uint64_t* p, uint64_t (&v)[V]) {
+    static_assert(V == 4, "V = 4");
+    asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+
+// Z = X * Y for 16-word (512-bit) operands, on the FP64 pipe. Z has 32 words.
+__device__ __forceinline__ void mul16_words_fp64(const uint32_t (&X)[16], const uint32_t (&Y)[16],
+                                                 uint32_t (&Z)[32]) {
+    constexpr uint64_t kM52 = (uint64_t(1) << 52) - 1;
+    constexpr int NL = 10;  // 52-bit limbs per 512-bit operand
+    double x[NL], y[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        const int o = 52 * k, w = o / 32, sh = o % 32;
+        auto word = [](const uint32_t (&W)[16], int i) -> uint64_t { return i < 16 ? W[i < 16 ? i : 0] : 0u; };
+        const uint64_t vx = ((word(X, w) | (word(X, w + 1) << 32)) >> sh | (sh ? word(X, w + 2) << (64 - sh) : 0)) & kM52;
+        const uint64_t vy = ((word(Y, w) | (word(Y, w + 1) << 32)) >> sh | (sh ? word(Y, w + 2) << (64 - sh) : 0)) & kM52;
+        x[k] = double(vx);  // exact: < 2^52
+        y[k] = double(vy);
+    }
+    const double C104 = 20282409603651670423947251286016.0;                     // 2^104
+    const double C104p52 = 20282409603651670423947251286016.0 + 4503599627370496.0;  // 2^104 + 2^52
+    uint64_t col[2 * NL];
+#pragma unroll
+    for (int c = 0; c < 2 * NL; ++c) col[c] = 0;
+#pragma unroll
+    for (int i = 0; i < NL; ++i)
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            double h, cc, l;
+            asm("fma.rz.f64 %0, %1, %2, %3;" : "=d"(h) : "d"(x[i]), "d"(y[j]), "d"(C104));
+            asm("sub.rn.f64 %0, %1, %2;" : "=d"(cc) : "d"(C104p52), "d"(h));
+            asm("fma.rn.f64 %0, %1, %2, %3;" : "=d"(l) : "d"(x[i]), "d"(y[j]), "d"(cc));
+            col[i + j] += uint64_t(__double_as_longlong(l));
+            col[i + j + 1] += uint64_t(__double_as_longlong(h));
+        }
+    // remove the biases (mod 2^64: the true column sums are < 20 * 2^52), carry in radix 2^52
+    constexpr uint64_t kB52 = 0x4330000000000000ull, kB104 = 0x4670000000000000ull;
+    uint64_t r[2 * NL];
+    uint64_t carry = 0;
+#pragma unroll
+    for (int c = 0; c < 2 * NL; ++c) {
+        const int nlo = c < NL ? c + 1 : (c <= 2 * NL - 2 ? 2 * NL - 1 - c : 0);  // pairs with i + j = c
+        const int nhi = c == 0 ? 0 : (c - 1 < NL ? c : 2 * NL - c);            // pairs with i + j = c - 1
+        const uint64_t v = col[c] - uint64_t(nlo) * kB52 - uint64_t(nhi) * kB104 + carry;
+        r[c] = v & kM52;
+        carry = v >> 52;
+    }
+    // repack 20 x 52 bits into 32 words (the product is < 2^1024)
+#pragma unroll
+    for (int w = 0; w < 32; ++w) {
+        const int o = 32 * w, k = o / 52, sh = o % 52;
+        uint64_t v = r[k] >> sh;
+        if (k + 1 < 2 * NL) v |= r[k + 1 < 2 * NL ? k + 1 : 0] << (52 - sh);
+        Z[w] = uint32_t(v);
+    }
+}
+
+#ifndef DOTG_K16H_MINB
+#define DOTG_K16H_MINB 16
+#endif
+__global__ void __launch_bounds__(32, DOTG_K16H_MINB) k_mul_kara16h(uint64_t* out, const uint64_t* a, const uint64_t* b,
+                                                                   size_t batch) {
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    const uint64_t* pa = a + pidx * 16;
+    const uint64_t* pb = b + pidx * 16;
+    // z1 first, from |a_hi - a_lo| and |b_hi - b_lo|; the halves are reloaded (L1) later
+    uint32_t Z1[2 * kK];
+    uint32_t sa, sb;
+    {
+        uint32_t Al[kK], Ah[kK], Bl[kK], Bh[kK];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            uint64_t x[4], y[4];
+            ld_cached<4>(pa + 4 * v, x);
+            ld_cached<4>(pb + 4 * v, y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int w = 8 * v + 2 * k;
+                uint32_t* qa = w < kK ? &Al[w] : &Ah[w - kK];
+                uint32_t* qb = w < kK ? &Bl[w] : &Bh[w - kK];
+                qa[0] = lo32(x[k]);
+                qa[1] = hi32(x[k]);
+                qb[0] = lo32(y[k]);
+                qb[1] = hi32(y[k]);
+            }
+        }
+        uint32_t Da[kK], Db[kK];
+        sa = absdiff16(Ah, Al, Da);
+        sb = absdiff16(Bh, Bl, Db);
+        mul16_words_fp64(Da, Db, Z1);
+    }
+    auto load_half = [&](const uint64_t* p, int half, uint32_t (&W)[kK]) {
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            uint64_t x[4];
+            ld_cached<4>(p + 8 * half + 4 * v, x);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                W[8 * v + 2 * k] = lo32(x[k]);
+                W[8 * v + 2 * k + 1] = hi32(x[k]);
+            }
+        }
+    };
+    uint32_t Z0[2 * kK], Z2[2 * kK];
+    {
+        uint32_t X[kK], Y[kK];
+        load_half(pa, 0, X);
+        load_half(pb, 0, Y);
+        mul16_words(X, Y, Z0);
+    }
+    uint64_t* po = out + pidx * 32;
+    {  // R[0, 16) = z0[0, 16)
+        uint64_t o0[4], o1[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            o0[k] = uint64_t(Z0[2 * k]) | (uint64_t(Z0[2 * k + 1]) << 32);
+            o1[k] = uint64_t(Z0[8 + 2 * k]) | (uint64_t(Z0[8 + 2 * k + 1]) << 32);
+        }
+        st_stream<4>(po, o0);
+        st_stream<4>(po + 4, o1);
+    }
+    {
+        uint32_t X[kK], Y[kK];
+        load_half(pa, 1, X);
+        load_half(pb, 1, Y);
+        mul16_words(X, Y, Z2);
+    }
+    // mid = z0 + z2 - z1 (same signs) or + z1, then R[16, 64) as in k_mul_kara16
+    const uint32_t neg = sa == sb ? 1u : 0u, mask = 0u - neg;
+    uint32_t mid[2 * kK + 1];
+    {
+        uint32_t c = neg;
+#pragma unroll
+        for (int i = 0; i < 2 * kK; ++i) {
+            const uint64_t t = uint64_t(Z0[i]) + Z2[i] + (Z1[i] ^ mask) + c;
+            mid[i] = uint32_t(t);
+            c = uint32_t(t >> 32);
+        }
+        mid[2 * kK] = c + mask;
+    }
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        uint32_t r[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int i = 8 * q + e;
+            const uint32_t base = i < kK ? Z0[kK + i] : Z2[i - kK];
+            const uint32_t add = i <= 2 * kK ? mid[i <= 2 * kK ? i : 0] : 0u;
+            const uint64_t t = uint64_t(base) + add + c;
+            r[e] = uint32_t(t);
+            c = uint32_t(t >> 32);
+        }
+        uint64_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[k] = uint64_t(r[2 * k]) | (uint64_t(r[2 * k + 1]) << 32);
+        st_stream<4>(po + 8 + 4 * q, o);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Generic: any m, any layout (pair p, limb i at p*sp + i*si; out limb k at p*so + k*sio).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t word_at(const uint64_t* base, size_t si, size_t w) {
@@ -839,8 +1013,20 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
             break;
         case 16:
             if (al) {  // C3: 40.0 us vs 42.1 us for the plain 16-column kernel (tools/mul_timing.py)
-                k_mul_kara16<<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0, stream>>>(
-                    out, a, b, batch);
+                // A/B knob: DOTG_K16_HYBRID=1 takes z1 on the FP64 pipe (k_mul_kara16h).
+                // Measured r02 (tools/c3_probe.py): 41.6 vs 39.4 us at 2^18 pairs, 0.873 vs
+                // 0.903 of the roofline at 2^21 - the kernel is latency-bound at 16 warps/SM,
+                // not IMAD-pipe-bound, so moving a third of the MACs to another pipe loses
+                // to the extra instructions. Default off.
+                static const int hybrid = [] {
+                    const char* e = std::getenv("DOTG_K16_HYBRID");
+                    return e ? std::atoi(e) : 0;
+                }();
+                if (hybrid)
+                    k_mul_kara16h<<<unsigned((batch + 31) / 32), 32, 0, stream>>>(out, a, b, batch);
+                else
+                    k_mul_kara16<<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0, stream>>>(
+                        out, a, b, batch);
                 count_launch();
                 return cudaGetLastError();
             }

@@ -182,3 +182,17 @@ def test_row_pitched_views(cuda, oracle):
         assert np.array_equal(Oh[:, : 2 * m], want), m
         assert (Oh[:, 2 * m:] == 7).all()  # the rest of each row untouched
         assert np.array_equal(dg.mul_batch(ta, tb).cpu().numpy().view(np.uint64), want)
+
+
+@pytest.mark.parametrize("m", [18, 32, 64, 126, 128])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 9, 1031])
+def test_interleaved_tensor_pipe_in_place(cuda, oracle, m, n):
+    """The interleaved tensor-pipe route reads and writes [m][batch] in place through
+    CTA tiles of 4 consecutive pairs: partial last groups (batch % 4 != 0, batch < 4),
+    zero-extended rows (m < the kernel's size), all-ones operands."""
+    rng = np.random.default_rng(7 * m + n)
+    a, b = category(rng, "random", "mul", (n, m))
+    a[::3] = MAX
+    b[1::4] = MAX
+    want = oracle.mul_batch(a, b)
+    assert np.array_equal(mul(cuda, a, b, "interleaved"), want), (m, n)

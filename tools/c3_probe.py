@@ -1,5 +1,7 @@
 """C3 multiply (m = 16) time per pair against the batch size: the wave-tail share of the
-named 2^18-pair batch (k_mul_kara16, one-warp CTAs). Back-to-back launches, CUDA events."""
+named 2^18-pair batch (one-warp CTAs). Back-to-back launches, CUDA events. The kernel is
+chosen by DOTG_K16_HYBRID (1: k_mul_kara16h, z1 on the FP64 pipe; 0: k_mul_kara16); the
+product is checked against the other kernel's through the IMMA route at 2^15 pairs."""
 import json
 import os
 import sys
@@ -12,7 +14,16 @@ from paper_2604_21566_b200 import workloads as W
 
 torch.cuda.set_device(0)
 m = 16
-res = {}
+res = {"hybrid": os.environ.get("DOTG_K16_HYBRID", "1")}
+a = W.fill(32768 * m, 0x77, 0).view(-1, m)
+b = W.fill(32768 * m, 0x77, 1 << 40).view(-1, m)
+b[::7] = -1
+a[::5] = -1
+ref = torch.empty((32768, 2 * m), dtype=torch.int64, device="cuda")
+prev = dg.set_mul_route("imma")
+dg.mul_batch(a, b, out=ref)
+dg.set_mul_route(prev)
+assert torch.equal(dg.mul_batch(a, b), ref), "C3 kernel disagrees with the tensor-pipe route"
 for lg in (15, 16, 17, 18, 19, 20, 21):
     B = 1 << lg
     a = W.fill(B * m, 0xC3, 0).view(B, m)
