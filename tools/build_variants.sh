@@ -14,6 +14,6 @@ while [ $# -ge 2 ]; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I"$ROOT/include" \
        -Xptxas -v $flags -c "$CS/$SRC.cu" -o "$ROOT/tools/build/${SRC}_$name.o" 2> "$ROOT/tools/build/$name.ptxas.log"
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o "$ROOT/tools/build/libdotg_$name.so" \
-       $OBJS "$ROOT/tools/build/${SRC}_$name.o"
-  echo "$name: $(grep -A3 'ILi16' "$ROOT/tools/build/$name.ptxas.log" | grep -E 'registers|spill' | head -2 | tr '\n' ' ')"
+       $OBJS "$ROOT/tools/build/${SRC}_$name.o" -ldl
+  echo "$name: $(grep -A3 "${KERNEL:-ILi16}" "$ROOT/tools/build/$name.ptxas.log" | grep -E 'registers|spill' | head -2 | tr '\n' ' ')"
 done
