@@ -29,6 +29,7 @@
 // kernel with the same carry semantics.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -344,56 +345,61 @@ __global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ld
     if (flags != nullptr) flags[pidx] = c;
 }
 
-// Interleaved layout [m][batch], limb-segmented: a CTA owns 32 consecutive pairs (lane =
-// pair); warp w of the CTA owns limbs [w*L, w*L + L) of those pairs. Each thread resolves
-// its segment with carry-in 0 keeping the sums and g/p bits in registers. The segments'
-// (G, P) are published per warp as two 32-bit ballot masks over the pairs; after ONE
-// barrier every warp folds the masks of the lower segments, bit-parallel over its 32
-// pairs (c = G_j | (P_j & c), j < w), applies its carry-in and stores - every output
-// written once. (r01 version: a second barrier and warp 0 folding the segments per pair
-// while the other warps waited - 0.43-0.61 of HBM at m = 128-512.) A batch of few long
-// numbers gets S = ceil(m / L) warps per strip of pairs instead of one serial thread per
-// pair.
-template <int kIL, int kIMaxS, bool SUB>  // limbs per thread-segment, segments per CTA
-__global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* __restrict__ out,
-                                                                     const uint64_t* __restrict__ a,
-                                                                     const uint64_t* __restrict__ b, uint32_t* flags,
-                                                                     size_t m, size_t batch) {
-    __shared__ uint32_t sG[kIMaxS], sP[kIMaxS];  // per segment: bit p = G / P of pair p
+// Interleaved layout, one launch, nothing held across the barrier: a CTA of W warps owns
+// a strip of 32 pairs (lane = pair); warp w owns limb rows [w*L, (w+1)*L) with L = m / W.
+//   phase 1: stream the warp's rows in chunks of 8 (16 loads in flight), fold every
+//            chunk's generate / propagate bits into the segment's (G, P) - nothing stored,
+//            no operand kept in registers;
+//   fold:    (G, P) per pair as two ballot masks per warp, ONE barrier, each warp folds
+//            the lower segments bit-parallel over its 32 pairs;
+//   phase 2: stream the rows again (the strip was just read: L2 hits), add with the known
+//            carry-in, store.
+// DRAM sees the operands once; registers stay small, so 8-warp CTAs fit 8 per SM and
+// the whole B x m = 2^22 batch is resident in ONE wave (the register-holding kernel above
+// needs 1.73 waves at m = 256).
+// W warps (segments) per CTA, chosen per call so that ceil(batch / 32) CTAs at <= 64
+// registers (1024 threads per SM) fit in one wave: W <= 148 * 1024 / batch.
+#ifndef DOTG_IL2_OCC
+#define DOTG_IL2_OCC 1024  // resident threads per SM the register budget is sized for
+#endif
+template <bool SUB, int kIL2W>
+__global__ void __launch_bounds__(kIL2W * 32, DOTG_IL2_OCC / 32 / kIL2W) k_addsub_il2(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                           const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
+                                                           size_t batch) {
+    __shared__ uint32_t sG[kIL2W], sP[kIL2W];
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
     const size_t p = size_t(blockIdx.x) * 32 + size_t(lane);
-    const size_t i0 = size_t(w) * kIL;
-    const int L = int(m - i0 < size_t(kIL) ? m - i0 : size_t(kIL));
     const bool ok = p < batch;
-    uint64_t s[kIL], y[kIL];
-    uint32_t gm = 0, pm = 0;  // per-limb generate / propagate bits
-    // every load of the segment in flight before any arithmetic
+    const size_t L = (m + kIL2W - 1) / kIL2W;  // rows per warp
+    const size_t r0 = size_t(w) * L;
+    const size_t r1 = r0 + L < m ? r0 + L : m;
+#ifndef DOTG_IL2_CH
+#define DOTG_IL2_CH 4
+#endif
+    constexpr int CH = DOTG_IL2_CH;
+    // phase 1: segment (G, P) with carry-in 0, chunk by chunk
+    uint32_t G = 0, P = 1;
+    for (size_t c0 = r0; c0 < r1; c0 += CH) {
+        uint64_t x[CH], y[CH];
 #pragma unroll
-    for (int k = 0; k < kIL; ++k) {
-        s[k] = y[k] = 0;
-        if (k < L && ok) {
-            const size_t off = (i0 + size_t(k)) * batch + p;
-            s[k] = __ldcs(a + off);
-            y[k] = __ldcs(b + off);
+        for (int k = 0; k < CH; ++k) {
+            x[k] = y[k] = 0;
+            if (ok && c0 + k < r1) {
+                x[k] = __ldcg(a + (c0 + k) * batch + p);
+                y[k] = __ldcg(b + (c0 + k) * batch + p);
+            }
         }
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+            if (c0 + k < r1) {
+                uint32_t g, pr;
+                lane_op<SUB>(x[k], y[k], g, pr);
+                G = g | (pr & G);
+                P &= pr;
+            }
     }
-#pragma unroll
-    for (int k = 0; k < kIL; ++k) {
-        if (k < L) {
-            uint32_t gq, pq;
-            s[k] = lane_op<SUB>(s[k], y[k], gq, pq);
-            gm |= gq << k;
-            pm |= pq << k;
-        }
-    }
-    uint32_t c = 0, all = 1;
-#pragma unroll
-    for (int k = 0; k < kIL; ++k)
-        if (k < L) {
-            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
-            all &= (pm >> k) & 1u;
-        }
-    const uint32_t Gm = __ballot_sync(0xffffffffu, c), Pm = __ballot_sync(0xffffffffu, all);
+    const uint32_t Gm = __ballot_sync(0xffffffffu, ok && r0 < r1 ? G : 0u);
+    const uint32_t Pm = __ballot_sync(0xffffffffu, !ok || r0 >= r1 || P);
     if (lane == 0) {
         sG[w] = Gm;
         sP[w] = Pm;
@@ -401,20 +407,60 @@ __global__ void __launch_bounds__(kIMaxS * 32) k_addsub_interleaved(uint64_t* __
     __syncthreads();
     uint32_t cm = 0;  // carries into segment w, one bit per pair
 #pragma unroll
-    for (int j = 0; j < kIMaxS; ++j)
+    for (int j = 0; j < kIL2W; ++j)
         if (j < w) cm = sG[j] | (sP[j] & cm);
-    c = (cm >> lane) & 1u;
+    uint32_t c = (cm >> lane) & 1u;
+    // phase 2: the same rows again, with the carry
+    for (size_t c0 = r0; c0 < r1; c0 += CH) {
+        uint64_t x[CH], y[CH];
 #pragma unroll
-    for (int k = 0; k < kIL; ++k)
-        if (k < L) {
-            s[k] = apply_carry<SUB>(s[k], c);
-            c = ((gm >> k) & 1u) | (((pm >> k) & 1u) & c);
+        for (int k = 0; k < CH; ++k) {
+            x[k] = y[k] = 0;
+            if (ok && c0 + k < r1) {
+                x[k] = __ldcs(a + (c0 + k) * batch + p);
+                y[k] = __ldcs(b + (c0 + k) * batch + p);
+            }
         }
-    if (!ok) return;
-    if (w == int(blockDim.x >> 5) - 1 && flags != nullptr) flags[p] = c;
 #pragma unroll
-    for (int k = 0; k < kIL; ++k)
-        if (k < L) __stcs(out + (i0 + size_t(k)) * batch + p, s[k]);
+        for (int k = 0; k < CH; ++k)
+            if (ok && c0 + k < r1) {
+                uint32_t g, pr;
+                const uint64_t v = lane_op<SUB>(x[k], y[k], g, pr);
+                __stcs(out + (c0 + k) * batch + p, apply_carry<SUB>(v, c));
+                c = g | (pr & c);
+            }
+    }
+    if (ok && flags != nullptr && r1 == m && r0 < r1) flags[p] = c;
+}
+
+template <bool SUB>
+cudaError_t run_interleaved_il2(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                                size_t batch, cudaStream_t st) {
+    static thread_local struct { int dev = -1, sms = 148; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        di.dev = dev;
+    }
+    const size_t ctas = (batch + 31) / 32;
+    static const int wdiv = [] {
+        const char* e = std::getenv("DOTG_IL2_WDIV");  // A/B knob: fewer, longer segments
+        return e ? std::atoi(e) : 1;
+    }();
+    int W = 32;
+    while (W > 2 && (size_t(W) * ctas > size_t(di.sms) * (DOTG_IL2_OCC / 32) || size_t(W) * 8 > m)) W /= 2;
+    for (int d = wdiv; d > 1 && W > 2; d /= 2) W /= 2;
+    const unsigned grid = unsigned(ctas);
+    switch (W) {
+        case 32: k_addsub_il2<SUB, 32><<<grid, 32 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+        case 16: k_addsub_il2<SUB, 16><<<grid, 16 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+        case 8: k_addsub_il2<SUB, 8><<<grid, 8 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+        case 4: k_addsub_il2<SUB, 4><<<grid, 4 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+        default: k_addsub_il2<SUB, 2><<<grid, 2 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+    }
+    count_launch();
+    return cudaGetLastError();
 }
 
 // Interleaved layout, two streaming passes (no barrier, no register holding): the
@@ -616,23 +662,6 @@ __global__ void __launch_bounds__(256) k_addsub_rows_any(uint64_t* __restrict__ 
 
 namespace {
 
-template <int kIL, int kIMaxS, bool SUB>
-cudaError_t run_interleaved(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
-                            size_t batch, cudaStream_t st) {
-    const size_t S = (m + kIL - 1) / kIL;
-    const size_t blocks = (batch + 31) / 32;
-    k_addsub_interleaved<kIL, kIMaxS, SUB><<<unsigned(blocks), unsigned(S * 32), 0, st>>>(out, a, b, flags, m,
-                                                                                        batch);
-    count_launch();
-    return cudaGetLastError();
-}
-
-// Interleaved problems by length (tools/layout_timing.py, B200, B x m = 2^22 limbs):
-// m < 128 thread-per-pair strided (5.2-6.6 TB/s); 128 <= m <= 256 8-limb segments, up to
-// 32 per CTA (4.0-4.3 TB/s vs 3.0 for 16-limb segments of two pairs per lane, 3.2-3.4 for
-// 16-warp CTAs of 16-limb segments, 3.7 for 4-limb segments or 16-warp CTAs at m = 128);
-// 256 < m <= 512 16-limb segments (3.0 TB/s; 2.0 with 32-limb ones, 1.1 strided);
-// 512 < m <= 1024 32-limb segments (2.8 TB/s); longer numbers strided.
 // segment state fits a modest scratch, and the grid fits 32-bit block counts
 bool nseg_fits(size_t m, size_t batch) {
     const size_t nseg = (m + kSL - 1) / kSL;
@@ -666,10 +695,15 @@ cudaError_t run_interleaved_2pass(uint64_t* out, const uint64_t* a, const uint64
 
 // Interleaved routes (tools/il_modes.py, B200, B x m = 2^22 limbs, GB/s at m = 4 / 16 / 32
 // / 64 / 128 / 256 / 512 / 1024): thread per pair 4560 / 5130 / 5360 / 4410 / 3230 / 1910 /
-// 1060 / 560; one-pass segmented CTAs - / - / - / - / 4030 / 3050 / 3240 / 2320; two-pass
-// 3860 (m = 4) ... 3730 / 3250 / 2710 / 2020 (m = 128 ... 1024). Auto: thread per pair below
-// 128 limbs, one-pass CTAs up to 1024, two-pass above. DOTG_IL_MODE (A/B knob): 0 auto,
-// 1 one-pass where it applies, 2 thread per pair; DOTG_IL_MIN moves the two-pass bound.
+// 1060 / 560; re-read segmented CTAs (k_addsub_il2) - / 4060 / 4320 / 4370 / 4390 / 4040 /
+// 4030 / 3930; two-pass 3860 (m = 4) ... 3730 / 3250 / 2710 / 2020 (m = 128 ... 1024); the
+// r01 register-holding segmented CTAs (removed) 4030 / 3050 / 3240 / 2320 at 128-1024.
+// Auto (0 = not interleaved-special, i.e. thread per pair; 3 = k_addsub_il2; 4 = two-pass):
+// up to 8 limbs the two-pass route's first pass alone (one segment: 4907 GB/s at m = 4);
+// below 128 limbs thread per pair; from 128 limbs the re-read CTAs while they give every SM
+// at least 8 warps, else the two-pass route (its warps are (strip, segment) pairs, so a
+// few long numbers still fill the GPU). DOTG_IL_MODE (A/B
+// knob) forces 2 (thread per pair), 3 or 4 where they apply.
 int il_mode() {
     static const int v = [] {
         const char* e = std::getenv("DOTG_IL_MODE");
@@ -677,23 +711,23 @@ int il_mode() {
     }();
     return v;
 }
-bool il_two_pass(size_t m, size_t batch) {
-    static const size_t lo = [] {
-        const char* e = std::getenv("DOTG_IL_MIN");
-        return size_t(e ? std::atol(e) : 1025);
-    }();
-    return il_mode() == 0 && m >= lo && nseg_fits(m, batch);
-}
-
-template <bool SUB>
-cudaError_t run_interleaved_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
-                                size_t batch, cudaStream_t st) {
-    // segments of 8 / 16 / 32 limbs keep up to 32 warps per strip of 32 pairs
-    // (tools/layout_timing.py: m = 512 2.0 -> 3.0 TB/s with 16-limb segments instead of 32;
-    // m = 1024 2.8 TB/s, thread per pair before)
-    if (m <= 256) return run_interleaved<8, 32, SUB>(out, a, b, flags, m, batch, st);
-    if (m <= 512) return run_interleaved<16, 32, SUB>(out, a, b, flags, m, batch, st);
-    return run_interleaved<32, 32, SUB>(out, a, b, flags, m, batch, st);
+int il_route(size_t m, size_t batch) {
+    const int mode = il_mode();
+    if (mode == 2) return 0;
+    if (mode == 3) return m >= 16 ? 3 : 0;
+    if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
+    if (m <= size_t(kSL)) return nseg_fits(m, batch) ? 4 : 0;  // one segment: pass 1 alone
+    if (m < 128) return 0;
+    static thread_local struct { int dev = -1, sms = 148; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        di.dev = dev;
+    }
+    const size_t warps = (batch + 31) / 32 * std::min<size_t>(32, m / 8);  // k_addsub_il2's warps
+    if (warps >= size_t(8) * size_t(di.sms)) return 3;
+    return nseg_fits(m, batch) ? 4 : 0;
 }
 
 template <bool SUB>
@@ -789,17 +823,19 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             continue;
         }
         const int r = route(P, layouts[i]);
-        if (r == 2 && layouts[i] == 1 && il_two_pass(P.m, P.batch)) {
-            cudaError_t e = P.sub ? run_interleaved_2pass<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
-                                  : run_interleaved_2pass<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
-            if (e != cudaSuccess) return e;
-            continue;
-        }
-        if (r == 2 && layouts[i] == 1 && P.m >= 128 && P.m <= 1024 && il_mode() != 2) {
-            cudaError_t e = P.sub ? run_interleaved_any<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
-                                  : run_interleaved_any<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
-            if (e != cudaSuccess) return e;
-            continue;
+        if (r == 2 && layouts[i] == 1) {
+            const int ir = il_route(P.m, P.batch);
+            if (ir != 0) {
+                cudaError_t e;
+                if (ir == 3)
+                    e = P.sub ? run_interleaved_il2<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                              : run_interleaved_il2<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                else
+                    e = P.sub ? run_interleaved_2pass<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                              : run_interleaved_2pass<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                if (e != cudaSuccess) return e;
+                continue;
+            }
         }
         // long numbers: two tiles (8192 limbs) or more each -> the tiled long-number passes
         // for the whole batch (a warp walking a pair's chunks serially would leave the GPU

@@ -1,5 +1,5 @@
-"""A/B of the interleaved add/sub routes (DOTG_IL_MODE: 0 auto/two-pass, 1 one-pass
-segmented CTAs, 2 thread per pair) at B x m = 2^22 limbs: back-to-back launches over 3
+"""A/B of the interleaved add/sub routes (DOTG_IL_MODE: 0 auto, 4 two-pass
+2 thread per pair, 3 re-read segmented CTAs) at B x m = 2^22 limbs: back-to-back launches over 3
 rotating input copies (> L2 between reuses), CUDA events. Each mode in its own process
 (the knob is read once). Prints one JSON line per (mode, m)."""
 import json
@@ -44,7 +44,8 @@ for m in (4, 16, 32, 64, 128, 256, 512, 1024):
 print(json.dumps(res))
 '''.replace("ROOT", repr(ROOT))
 
-for mode in ("0", "1", "2"):
+modes = sys.argv[sys.argv.index("--only") + 1].split(",") if "--only" in sys.argv else ["0", "2", "3", "4"]
+for mode in modes:
     env = {**os.environ, "DOTG_IL_MODE": mode}
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
     if r.returncode != 0:
