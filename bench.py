@@ -1079,34 +1079,45 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
     # ---------------- interleaved layout (north star's batch-interleaved subsystem) ----------------
     if want("IL") and world == 1 and not args.no_layouts:
         il = {}
+        # back-to-back launches over 3 rotating input copies (> L2 between reuses)
         for m, B in [(64, 1 << 16)] + [(mm, (1 << 22) // mm) for mm in (4, 16, 128, 256, 512)]:
-            a = W.fill(B * m, 0x1A + m, 0).view(m, B)  # [m][batch]
-            b = W.fill(B * m, 0x1A + m, 1 << 40).view(m, B)
-            o, f = torch.empty_like(a), torch.empty(B, dtype=torch.int32, device="cuda")
-            fns = []
+            sets = []
+            for r in range(3):
+                a = W.fill(B * m, 0x1A + m + 7 * r, 0).view(m, B)  # [m][batch]
+                b = W.fill(B * m, 0x1A + m + 7 * r, 1 << 40).view(m, B)
+                sets.append((a, b, torch.empty_like(a), torch.empty(B, dtype=torch.int32, device="cuda")))
+            byts = B * (24 * m + 4)
+            row = {}
             for sub in (0, 1):
                 fn = lib.dotg_sub_batch if sub else lib.dotg_add_batch
-                args_ = (P(o), P(a), P(b), P(f), m, B, 1, L.stream)
-                fns.append(lambda fn=fn, args_=args_: fn(*args_))
-            _, per = timed_steps(torch, None, 1, stream, fns, steps, warm)
-            byts = B * (24 * m + 4)
-            il[f"m{m}_B{B}"] = {"add_gbs": byts / (per[0] * 1e-3) / 1e9, "sub_gbs": byts / (per[1] * 1e-3) / 1e9,
-                                "add_frac": byts / (per[0] * 1e-3) / 1e9 / hbm_peak,
-                                "sub_frac": byts / (per[1] * 1e-3) / 1e9 / hbm_peak}
-            del a, b, o, f
+
+                def mk(Lc, fn=fn, sets=sets):
+                    return [(lambda args_=(P(o), P(a), P(b), P(f), m, B, 1, Lc.stream): fn(*args_))
+                            for a, b, o, f in sets]
+                us = per_launch_us(torch, dg, lib, stream, mk)
+                op = "sub" if sub else "add"
+                row[f"{op}_gbs"] = byts / (us * 1e-6) / 1e9
+                row[f"{op}_frac"] = byts / (us * 1e-6) / 1e9 / hbm_peak
+            il[f"m{m}_B{B}"] = row
+            del sets
         # interleaved multiply at the C3 / C4 shapes
         for m, B in ((16, 1 << 18), (32, 1 << 17), (64, 1 << 16)):
-            a = W.fill(B * m, 0x1B + m, 0).view(m, B)
-            b = W.fill(B * m, 0x1B + m, 1 << 40).view(m, B)
-            o = torch.empty((2 * m, B), dtype=torch.int64, device="cuda")
-            args_ = (P(o), P(a), P(b), m, B, 1, L.stream)
-            _, per = timed_steps(torch, None, 1, stream, [lambda args_=args_: lib.dotg_mul_batch(*args_)], steps,
-                                 warm)
-            il[f"mul_m{m}_B{B}"] = {"pairs_s": B / (per[0] * 1e-3), "us": per[0] * 1e3,
-                                    "frac_imad": B / (per[0] * 1e-3) * 4 * m * m / imad_peak_pps}
-            del a, b, o
+            sets = []
+            for r in range(2):
+                a = W.fill(B * m, 0x1B + m + 7 * r, 0).view(m, B)
+                b = W.fill(B * m, 0x1B + m + 7 * r, 1 << 40).view(m, B)
+                sets.append((a, b, torch.empty((2 * m, B), dtype=torch.int64, device="cuda")))
+
+            def mk(Lc, sets=sets, m=m, B=B):
+                return [(lambda args_=(P(o), P(a), P(b), m, B, 1, Lc.stream): lib.dotg_mul_batch(*args_))
+                        for a, b, o in sets]
+            us = per_launch_us(torch, dg, lib, stream, mk)
+            il[f"mul_m{m}_B{B}"] = {"pairs_s": B / (us * 1e-6), "us": us,
+                                    "frac_imad": B / (us * 1e-6) * 4 * m * m / imad_peak_pps}
+            del sets
         out["interleaved"] = {"layout": "[m][batch] (limb i of pair p at i*batch + p)", "per_shape": il,
-                              "peak": hbm_peak}
+                              "peak": hbm_peak, "timing": "back-to-back launches over rotating input copies "
+                                                          "(CUDA graph, events on the stream)"}
         torch.cuda.empty_cache()
 
     # ---------------- 256-bit base cases: dot_mul_5x5 / dot_mul_4x4 shapes ----------------
