@@ -922,6 +922,7 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
               "step": f"{len(calls)} rotating input sets; per set add + sub in one dotg_addsub_grouped launch",
               "roofline": hbm_roofline(2 * byts, launch_s, hbm_peak,
                                        "k_addsub_grouped (add + sub of one C1 set, 2 problems, one launch)",
+                                       traffic=traffic_table().get("C1_per_launch_bytes") if world == 1 else None,
                                        single_launch={"add_gbs": byts / (per1[0] * 1e-3) / 1e9,
                                                       "sub_gbs": byts / (per1[1] * 1e-3) / 1e9,
                                                       "add_frac": byts / (per1[0] * 1e-3) / 1e9 / hbm_peak,
@@ -1191,7 +1192,8 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                  "frac_hbm_per_gpu": 24 * n_local / (ms * 1e-3) / 1e9 / hbm_peak, "carry": carry, "mode": mode}
             r["roofline"] = hbm_roofline(24 * n_local, per[0] * 1e-3, hbm_peak,
                                          "k_long_local + k_long_scan_chunks + k_long_shard_agg + k_long_finish "
-                                         "(one long add/sub; k_long_local carries ~90% of the time)")
+                                         "(one long add/sub; k_long_local carries ~90% of the time)",
+                                         traffic=traffic_table().get("C5_per_op_bytes") if world == 1 else None)
             if world == 1 and not args.no_e2e and rank0:
                 # e2e through the host span form on pinned 8 GiB host arrays, and the
                 # reference's span-form dot_add_words on the same host arrays (1 thread)
