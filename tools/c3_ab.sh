@@ -1,5 +1,9 @@
-for h in 0 1; do DOTG_K16_HYBRID=$h python tools/c3_probe.py; done > gpurun_out/c3_ab.jsonl 2>&1
-echo rc=$?
-DOTG_K16_HYBRID=0 python -m pytest tests -m gpu -x -q -k "test_gpu_mul and (m16 or 16 or config)" > gpurun_out/pt_c3_old.log 2>&1; echo rc_old=$?
-python -m pytest tests -m gpu -x -q -k "test_gpu_mul or acceptance or fuzz or kara" > gpurun_out/pt_c3.log 2>&1; echo rc_new=$?
-tail -1 gpurun_out/pt_c3_old.log; tail -1 gpurun_out/pt_c3.log
+#!/bin/bash
+# C3 A/B: DOTG_K16_HYBRID (FP64-pipe middle product) through tools/c3_probe.py, each
+# setting in its own process; then the C3-shape parity tests. (r02 also measured a
+# two-threads-per-pair last wave this way: profiles/r02_c3_split_tail_ab.txt.)
+for cfg in "DOTG_K16_HYBRID=0" "DOTG_K16_HYBRID=1"; do
+  echo "{\"cfg\": \"$cfg\", \"r\": $(env $cfg python tools/c3_probe.py 2>&1 | tail -1)}"
+done
+DOTG_K16_HYBRID=1 python -m pytest tests -m gpu -x -q -k "test_gpu_mul or acceptance" 2>&1 | tail -1
+python -m pytest tests -m gpu -x -q -k "test_gpu_mul or acceptance or fuzz or graphs" 2>&1 | tail -1
