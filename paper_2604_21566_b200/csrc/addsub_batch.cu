@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ld
 }
 
 // Interleaved layout, one launch, nothing held across the barrier: a CTA of W warps owns
-// a strip of 32 pairs (lane = pair); warp w owns limb rows [w*L, (w+1)*L) with L = m / W.
+// a strip of 32 (or 64: two per lane) pairs; warp w owns limb rows [w*L, (w+1)*L), L = m / W.
 //   phase 1: stream the warp's rows in chunks of 8 (16 loads in flight), fold every
 //            chunk's generate / propagate bits into the segment's (G, P) - nothing stored,
 //            no operand kept in registers;
@@ -362,14 +362,15 @@ __global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ld
 #ifndef DOTG_IL2_OCC
 #define DOTG_IL2_OCC 1024  // resident threads per SM the register budget is sized for
 #endif
-template <bool SUB, int kIL2W>
+template <bool SUB, int kIL2W, int PPL>
 __global__ void __launch_bounds__(kIL2W * 32, DOTG_IL2_OCC / 32 / kIL2W) k_addsub_il2(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                                                            const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
                                                            size_t batch) {
-    __shared__ uint32_t sG[kIL2W], sP[kIL2W];
+    // PPL pairs per lane (2: one 16-byte load per limb row covers two adjacent pairs)
+    __shared__ uint32_t sG[kIL2W][PPL], sP[kIL2W][PPL];
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
-    const size_t p = size_t(blockIdx.x) * 32 + size_t(lane);
-    const bool ok = p < batch;
+    const size_t p = (size_t(blockIdx.x) * 32 + size_t(lane)) * PPL;
+    const bool ok = p < batch;  // PPL = 2: batch is even, a lane has both pairs or none
     const size_t L = (m + kIL2W - 1) / kIL2W;  // rows per warp
     const size_t r0 = size_t(w) * L;
     const size_t r1 = r0 + L < m ? r0 + L : m;
@@ -377,60 +378,93 @@ __global__ void __launch_bounds__(kIL2W * 32, DOTG_IL2_OCC / 32 / kIL2W) k_addsu
 #define DOTG_IL2_CH 4
 #endif
     constexpr int CH = DOTG_IL2_CH;
+    auto load = [&](const uint64_t* base, size_t row, uint64_t (&v)[PPL], bool stream) {
+        if constexpr (PPL == 2) {
+            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(base + row * batch + p);
+            const ulonglong2 t = stream ? __ldcs(q) : __ldcg(q);
+            v[0] = t.x;
+            v[1] = t.y;
+        } else {
+            v[0] = stream ? __ldcs(base + row * batch + p) : __ldcg(base + row * batch + p);
+        }
+    };
     // phase 1: segment (G, P) with carry-in 0, chunk by chunk
-    uint32_t G = 0, P = 1;
+    uint32_t G[PPL], P[PPL];
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) G[q] = 0, P[q] = 1;
     for (size_t c0 = r0; c0 < r1; c0 += CH) {
-        uint64_t x[CH], y[CH];
+        uint64_t x[CH][PPL], y[CH][PPL];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
-            x[k] = y[k] = 0;
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) x[k][q] = y[k][q] = 0;
             if (ok && c0 + k < r1) {
-                x[k] = __ldcg(a + (c0 + k) * batch + p);
-                y[k] = __ldcg(b + (c0 + k) * batch + p);
+                load(a, c0 + k, x[k], false);
+                load(b, c0 + k, y[k], false);
             }
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k)
-            if (c0 + k < r1) {
-                uint32_t g, pr;
-                lane_op<SUB>(x[k], y[k], g, pr);
-                G = g | (pr & G);
-                P &= pr;
-            }
+            if (c0 + k < r1)
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    uint32_t g, pr;
+                    lane_op<SUB>(x[k][q], y[k][q], g, pr);
+                    G[q] = g | (pr & G[q]);
+                    P[q] &= pr;
+                }
     }
-    const uint32_t Gm = __ballot_sync(0xffffffffu, ok && r0 < r1 ? G : 0u);
-    const uint32_t Pm = __ballot_sync(0xffffffffu, !ok || r0 >= r1 || P);
-    if (lane == 0) {
-        sG[w] = Gm;
-        sP[w] = Pm;
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) {
+        const uint32_t Gm = __ballot_sync(0xffffffffu, ok && r0 < r1 ? G[q] : 0u);
+        const uint32_t Pm = __ballot_sync(0xffffffffu, !ok || r0 >= r1 || P[q]);
+        if (lane == 0) {
+            sG[w][q] = Gm;
+            sP[w][q] = Pm;
+        }
     }
     __syncthreads();
-    uint32_t cm = 0;  // carries into segment w, one bit per pair
+    uint32_t c[PPL];
 #pragma unroll
-    for (int j = 0; j < kIL2W; ++j)
-        if (j < w) cm = sG[j] | (sP[j] & cm);
-    uint32_t c = (cm >> lane) & 1u;
+    for (int q = 0; q < PPL; ++q) {
+        uint32_t cm = 0;  // carries into segment w, one bit per lane
+#pragma unroll
+        for (int j = 0; j < kIL2W; ++j)
+            if (j < w) cm = sG[j][q] | (sP[j][q] & cm);
+        c[q] = (cm >> lane) & 1u;
+    }
     // phase 2: the same rows again, with the carry
     for (size_t c0 = r0; c0 < r1; c0 += CH) {
-        uint64_t x[CH], y[CH];
+        uint64_t x[CH][PPL], y[CH][PPL];
 #pragma unroll
         for (int k = 0; k < CH; ++k) {
-            x[k] = y[k] = 0;
+#pragma unroll
+            for (int q = 0; q < PPL; ++q) x[k][q] = y[k][q] = 0;
             if (ok && c0 + k < r1) {
-                x[k] = __ldcs(a + (c0 + k) * batch + p);
-                y[k] = __ldcs(b + (c0 + k) * batch + p);
+                load(a, c0 + k, x[k], true);
+                load(b, c0 + k, y[k], true);
             }
         }
 #pragma unroll
         for (int k = 0; k < CH; ++k)
             if (ok && c0 + k < r1) {
-                uint32_t g, pr;
-                const uint64_t v = lane_op<SUB>(x[k], y[k], g, pr);
-                __stcs(out + (c0 + k) * batch + p, apply_carry<SUB>(v, c));
-                c = g | (pr & c);
+                uint64_t r[PPL];
+#pragma unroll
+                for (int q = 0; q < PPL; ++q) {
+                    uint32_t g, pr;
+                    const uint64_t v = lane_op<SUB>(x[k][q], y[k][q], g, pr);
+                    r[q] = apply_carry<SUB>(v, c[q]);
+                    c[q] = g | (pr & c[q]);
+                }
+                if constexpr (PPL == 2)
+                    __stcs(reinterpret_cast<ulonglong2*>(out + (c0 + k) * batch + p), make_ulonglong2(r[0], r[1]));
+                else
+                    __stcs(out + (c0 + k) * batch + p, r[0]);
             }
     }
-    if (ok && flags != nullptr && r1 == m && r0 < r1) flags[p] = c;
+    if (ok && flags != nullptr && r1 == m && r0 < r1)
+#pragma unroll
+        for (int q = 0; q < PPL; ++q) flags[p + q] = c[q];
 }
 
 template <bool SUB>
@@ -443,7 +477,16 @@ cudaError_t run_interleaved_il2(uint64_t* out, const uint64_t* a, const uint64_t
         cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
         di.dev = dev;
     }
-    const size_t ctas = (batch + 31) / 32;
+    static const int ppl_knob = [] {
+        const char* e = std::getenv("DOTG_IL2_PPL");  // A/B knob: pairs per lane (1 or 2)
+        return e ? std::atoi(e) : 2;
+    }();
+    // two pairs per lane (16-byte row loads) while that still leaves a strip per SM
+    // (tools/il2_ab.sh: m = 16 ... 256 +1-9%, m = 1024 at B = 4096 -27% with half the CTAs)
+    const bool two = ppl_knob == 2 && batch % 2 == 0 && (batch + 63) / 64 >= size_t(di.sms) &&
+                     ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                       reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
+    const size_t ctas = (batch + (two ? 63 : 31)) / (two ? 64 : 32);
     static const int wdiv = [] {
         const char* e = std::getenv("DOTG_IL2_WDIV");  // A/B knob: fewer, longer segments
         return e ? std::atoi(e) : 1;
@@ -452,13 +495,17 @@ cudaError_t run_interleaved_il2(uint64_t* out, const uint64_t* a, const uint64_t
     while (W > 2 && (size_t(W) * ctas > size_t(di.sms) * (DOTG_IL2_OCC / 32) || size_t(W) * 8 > m)) W /= 2;
     for (int d = wdiv; d > 1 && W > 2; d /= 2) W /= 2;
     const unsigned grid = unsigned(ctas);
+#define DOTG_IL2_LAUNCH(WW)                                                                                   \
+    (two ? (k_addsub_il2<SUB, WW, 2><<<grid, WW * 32, 0, st>>>(out, a, b, flags, m, batch), 0)              \
+         : (k_addsub_il2<SUB, WW, 1><<<grid, WW * 32, 0, st>>>(out, a, b, flags, m, batch), 0))
     switch (W) {
-        case 32: k_addsub_il2<SUB, 32><<<grid, 32 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
-        case 16: k_addsub_il2<SUB, 16><<<grid, 16 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
-        case 8: k_addsub_il2<SUB, 8><<<grid, 8 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
-        case 4: k_addsub_il2<SUB, 4><<<grid, 4 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
-        default: k_addsub_il2<SUB, 2><<<grid, 2 * 32, 0, st>>>(out, a, b, flags, m, batch); break;
+        case 32: DOTG_IL2_LAUNCH(32); break;
+        case 16: DOTG_IL2_LAUNCH(16); break;
+        case 8: DOTG_IL2_LAUNCH(8); break;
+        case 4: DOTG_IL2_LAUNCH(4); break;
+        default: DOTG_IL2_LAUNCH(2); break;
     }
+#undef DOTG_IL2_LAUNCH
     count_launch();
     return cudaGetLastError();
 }
