@@ -114,14 +114,27 @@ class CommShardedWords:
     carries the 128-byte NCCL unique id from rank 0 to the others at construction (any
     backend). Construction is collective: every rank of ``group`` must create one."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, *, wrap_torch_comm: bool = False):
+        """wrap_torch_comm: reuse the NCCL communicator of the group's ProcessGroupNCCL
+        (dotg_comm_wrap; no second communicator) instead of creating one from a unique id."""
         import ctypes
 
+        import torch
         import torch.distributed as dist
 
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         L = lib()
+        if wrap_torch_comm:
+            pg = group if group is not None else dist.distributed_c10d._get_default_group()
+            backend = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+            probe = torch.zeros(1, device="cuda")
+            dist.all_reduce(probe, group=group)  # the communicator is created lazily
+            torch.cuda.synchronize()
+            self._comm = ctypes.c_void_p()
+            check(L.dotg_comm_wrap(ctypes.byref(self._comm), ctypes.c_void_p(int(backend._comm_ptr()))))
+            assert L.dotg_comm_rank(self._comm) == self.rank and L.dotg_comm_size(self._comm) == self.world
+            return
         nid = int(L.dotg_comm_id_bytes())
         payload = [None]
         if self.rank == 0:

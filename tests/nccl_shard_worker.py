@@ -47,6 +47,13 @@ def main():
         assert np.array_equal(out2.cpu().numpy().view(np.uint64), want[lo:hi]), (rank, sub, "comm")
         assert int(carry2.item()) == wf
         cs.close()
+        # (3) the same C++ call over torch's own NCCL communicator (dotg_comm_wrap)
+        cw = CommShardedWords(wrap_torch_comm=True)
+        out3, carry3 = cw.run(sub, torch.full_like(a, -1), a, b)
+        torch.cuda.synchronize()
+        assert np.array_equal(out3.cpu().numpy().view(np.uint64), want[lo:hi]), (rank, sub, "wrap")
+        assert int(carry3.item()) == wf
+        cw.close()
     dist.barrier()
     dist.destroy_process_group()
     print(f"rank {rank}/{world} ok")
