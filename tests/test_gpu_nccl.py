@@ -66,3 +66,16 @@ def test_comm_sharded_entry_single_rank(cuda):
         assert L.dotg_add_words_sharded(None, None, None, 0, None, None, None) == dg._lib.DOTG_EINVAL
     finally:
         check(L.dotg_comm_destroy(comm))
+
+
+def test_device_shards_two_ranks_gloo(cuda):
+    """World size 2 with the product's device passes (not CPU stand-ins): both ranks on the
+    box's GPU, the 8-byte exchange host-staged over gloo, results checked per rank."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29577",
+                        os.path.join(ROOT, "tests", "gloo_gpu_shard_worker.py")],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "MASTER_ADDR": "127.0.0.1"})
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count(" ok") == 2
