@@ -298,7 +298,10 @@ __global__ void __launch_bounds__(256) k_addsub_strided(uint64_t* out, const uin
     uint64_t* po = out + pidx * sp;
     uint32_t c = 0;
     size_t i = 0;
-    constexpr int UN = 8;
+#ifndef DOTG_TPP_UN
+#define DOTG_TPP_UN 8
+#endif
+    constexpr int UN = DOTG_TPP_UN;
     for (; i + UN <= m; i += UN) {
         uint64_t x[UN], y[UN];
 #pragma unroll
@@ -506,6 +509,201 @@ cudaError_t run_interleaved_il2(uint64_t* out, const uint64_t* a, const uint64_t
         default: DOTG_IL2_LAUNCH(2); break;
     }
 #undef DOTG_IL2_LAUNCH
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Interleaved layout, one streaming pass with an in-CTA fix-up (nothing re-read, nothing
+// held): a CTA of W warps owns a strip of 32 * PPL pairs, warp w the limb rows
+// [w*L, (w+1)*L). Each warp streams its rows UN at a time (2 * UN * PPL loads in flight
+// per lane, like the thread-per-pair kernel) and stores them resolved with carry-in 0 -
+// except its first row, which it keeps in a register - while recording, per pair, the
+// first row whose provisional limb is not the propagating value (~0 for add, 0 for sub)
+// and that limb. After ONE barrier (the warps' (G, P) as ballot masks, folded bit-parallel
+// as in k_addsub_il2), a carry-in of 1 changes exactly the rows up to that first
+// non-propagating one: rows before it become the opposite propagating value (stored
+// without reading), that row becomes limb + 1 (- 1 for sub) from the register. With
+// random limbs that is the held first row alone. (G, P) of a segment: G = its provisional
+// carry out, P = every provisional limb propagating - exclusive, since all-~0 limbs with a
+// carry out would exceed a + b.
+template <bool SUB, int UN, int PPL, bool DB>
+__global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                    const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
+                                                    size_t batch, uint32_t L) {
+    __shared__ uint32_t sG[16][PPL], sP[16][PPL];
+    const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
+    const size_t p = (size_t(blockIdx.x) * 32 + size_t(lane)) * PPL;
+    const bool ok = p < batch;  // PPL = 2: batch is even, a lane has both pairs or none
+    const size_t r0 = size_t(w) * L < m ? size_t(w) * L : m;
+    const size_t r1 = r0 + L < m ? r0 + L : m;
+    constexpr uint64_t kProp = SUB ? 0ull : ~0ull;
+    uint64_t first[PPL], qv[PPL];
+    uint32_t c[PPL], allp[PPL], q[PPL];
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) first[j] = qv[j] = 0, c[j] = 0, allp[j] = 1, q[j] = 0;
+    using Chunk = uint64_t[UN][PPL];
+    auto ld = [&](Chunk& x, Chunk& y, size_t c0) {
+#pragma unroll
+        for (int k = 0; k < UN; ++k)
+            if (c0 + k < r1) {
+                if constexpr (PPL == 2) {
+                    const ulonglong2 u = __ldcs(reinterpret_cast<const ulonglong2*>(a + (c0 + k) * batch + p));
+                    const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(b + (c0 + k) * batch + p));
+                    x[k][0] = u.x, x[k][1] = u.y, y[k][0] = v.x, y[k][1] = v.y;
+                } else {
+                    x[k][0] = __ldcs(a + (c0 + k) * batch + p);
+                    y[k][0] = __ldcs(b + (c0 + k) * batch + p);
+                }
+            }
+    };
+    auto proc = [&](Chunk& x, Chunk& y, size_t c0) {
+#pragma unroll
+        for (int k = 0; k < UN; ++k)
+            if (c0 + k < r1) {
+                const uint32_t rel = uint32_t(c0 + k - r0);
+#pragma unroll
+                for (int j = 0; j < PPL; ++j) {
+                    uint32_t g, pr;
+                    const uint64_t v = apply_carry<SUB>(lane_op<SUB>(x[k][j], y[k][j], g, pr), c[j]);
+                    c[j] = g | (pr & c[j]);
+                    const uint32_t isp = v == kProp;
+                    if (allp[j] && !isp) q[j] = rel, qv[j] = v;
+                    allp[j] &= isp;
+                    x[k][j] = v;
+                }
+                if (rel == 0) {
+#pragma unroll
+                    for (int j = 0; j < PPL; ++j) first[j] = x[k][j];
+                } else if constexpr (PPL == 2) {
+                    __stcs(reinterpret_cast<ulonglong2*>(out + (c0 + k) * batch + p), make_ulonglong2(x[k][0], x[k][1]));
+                } else {
+                    __stcs(out + (c0 + k) * batch + p, x[k][0]);
+                }
+            }
+    };
+    if (ok && r0 < r1) {
+        Chunk x0, y0;
+        if constexpr (DB) {
+            // two chunks in flight: the next chunk's loads are issued before this one is resolved
+            Chunk x1, y1;
+            size_t c0 = r0;
+            ld(x0, y0, c0);
+            while (true) {
+                if (c0 + UN < r1) ld(x1, y1, c0 + UN);
+                proc(x0, y0, c0);
+                c0 += UN;
+                if (c0 >= r1) break;
+                if (c0 + UN < r1) ld(x0, y0, c0 + UN);
+                proc(x1, y1, c0);
+                c0 += UN;
+                if (c0 >= r1) break;
+            }
+        } else {
+            for (size_t c0 = r0; c0 < r1; c0 += UN) {
+                ld(x0, y0, c0);
+                proc(x0, y0, c0);
+            }
+        }
+    }
+    const bool has = ok && r0 < r1;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) {
+        const uint32_t Gm = __ballot_sync(0xffffffffu, has && c[j]);
+        const uint32_t Pm = __ballot_sync(0xffffffffu, !has || allp[j]);
+        if (lane == 0) sG[w][j] = Gm, sP[w][j] = Pm;
+    }
+    __syncthreads();
+    if (!has) return;
+#pragma unroll
+    for (int j = 0; j < PPL; ++j) {
+        uint32_t cm = 0;  // carries into segment w, one bit per lane
+        for (int i = 0; i < w; ++i) cm = sG[i][j] | (sP[i][j] & cm);
+        const uint32_t cin = (cm >> lane) & 1u;
+        uint64_t* po = out + r0 * batch + p + j;
+        if (!cin) {
+            po[0] = first[j];
+        } else if (!allp[j] && q[j] == 0) {
+            po[0] = apply_carry<SUB>(first[j], 1u);
+        } else {
+            // rows [0, q) were all propagating (held row 0 among them): they flip; row q
+            // (if any) takes the carry
+            const uint32_t n = allp[j] ? uint32_t(r1 - r0) : q[j];
+            for (uint32_t i = 0; i < n; ++i) po[size_t(i) * batch] = prop_value<SUB>(1u);
+            if (!allp[j]) po[size_t(n) * batch] = apply_carry<SUB>(qv[j], 1u);
+        }
+        if (flags != nullptr && r1 == m) flags[p + j] = c[j] | (allp[j] & cin);
+    }
+}
+
+// Rows per warp and warps per CTA for k_addsub_ilf: enough warps to cover the GPU in ONE
+// wave (warps stream their rows; a second wave would start late and end the launch with a
+// tail), rows per warp at least one unrolled chunk.
+template <bool SUB>
+cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                                size_t batch, cudaStream_t st) {
+    static thread_local struct { int dev = -1, sms = 148; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        di.dev = dev;
+    }
+    static const int ppl_knob = [] {
+        const char* e = std::getenv("DOTG_ILF_PPL");  // A/B knob: pairs per lane (1 or 2; 0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int un_knob = [] {
+        const char* e = std::getenv("DOTG_ILF_UN");  // A/B knob: rows per chunk (8 or 16, single-buffered)
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int db_knob = [] {
+        const char* e = std::getenv("DOTG_ILF_DB");  // A/B knob: 1 = two chunks in flight
+        return e ? std::atoi(e) : 1;
+    }();
+    static const int wdiv = [] {
+        const char* e = std::getenv("DOTG_ILF_WDIV");  // A/B knob: fewer, longer segments
+        return e ? std::atoi(e) : 1;
+    }();
+    // variants (chunk rows x pairs per lane, double-buffered?): 32 operand words in
+    // registers each (16 x 1 double-buffered would spill)
+    using KFn = void (*)(uint64_t*, const uint64_t*, const uint64_t*, uint32_t*, size_t, size_t, uint32_t);
+    static constexpr int kNV = 5;
+    static const KFn kfn[kNV] = {k_addsub_ilf<SUB, 16, 1, false>, k_addsub_ilf<SUB, 8, 1, false>,
+                                 k_addsub_ilf<SUB, 8, 2, false>,  k_addsub_ilf<SUB, 8, 1, true>,
+                                 k_addsub_ilf<SUB, 4, 2, true>};
+    static constexpr int kUN[kNV] = {16, 8, 8, 8, 4};
+    // resident CTAs per SM for each (variant, W = 1 ... 16)
+    static thread_local struct { int dev = -1; int per[kNV][5]; } oc;
+    if (oc.dev != dev) {
+        for (int v = 0; v < kNV; ++v)
+            for (int i = 0; i < 5; ++i) {
+                int n = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(kfn[v]), 32 << i, 0);
+                oc.per[v][i] = n > 0 ? n : 1;
+            }
+        oc.dev = dev;
+    }
+    // the widest CTA (most warps per strip, W = 2^wi) whose grid still fits one wave
+    auto split = [&](int kv, size_t strips) {
+        int wi = 4;
+        while (wi > 0 && (strips > size_t(oc.per[kv][wi]) * size_t(di.sms) || (size_t(kUN[kv]) << wi) > m)) --wi;
+        for (int d = wdiv; d > 1 && wi > 0; d /= 2) --wi;
+        return wi;
+    };
+    const bool can2 = batch % 2 == 0 && ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                                          reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
+    const size_t strips1 = (batch + 31) / 32, strips2 = (batch + 63) / 64;
+    const int v1 = db_knob ? 3 : (un_knob == 8 ? 1 : 0), v2 = db_knob ? 4 : 2;
+    bool two;
+    if (ppl_knob == 1 || !can2) two = false;
+    else if (ppl_knob == 2) two = true;
+    else  // 16-byte rows unless they leave fewer warps (B200: m = 1024 at B = 4096 0.72 vs 0.59 of HBM)
+        two = (strips2 << split(v2, strips2)) >= (strips1 << split(v1, strips1));
+    const int kv = two ? v2 : v1;
+    const size_t strips = two ? strips2 : strips1;
+    const int W = 1 << split(kv, strips);
+    const uint32_t L = uint32_t((m + W - 1) / W);
+    kfn[kv]<<<unsigned(strips), W * 32, 0, st>>>(out, a, b, flags, m, batch, L);
     count_launch();
     return cudaGetLastError();
 }
@@ -740,17 +938,18 @@ cudaError_t run_interleaved_2pass(uint64_t* out, const uint64_t* a, const uint64
     return e != cudaSuccess ? e : e2;
 }
 
-// Interleaved routes (tools/il_modes.py, B200, B x m = 2^22 limbs, GB/s at m = 4 / 16 / 32
-// / 64 / 128 / 256 / 512 / 1024): thread per pair 4560 / 5130 / 5360 / 4410 / 3230 / 1910 /
-// 1060 / 560; re-read segmented CTAs (k_addsub_il2) - / 4060 / 4320 / 4370 / 4390 / 4040 /
-// 4030 / 3930; two-pass 3860 (m = 4) ... 3730 / 3250 / 2710 / 2020 (m = 128 ... 1024); the
-// r01 register-holding segmented CTAs (removed) 4030 / 3050 / 3240 / 2320 at 128-1024.
-// Auto (0 = not interleaved-special, i.e. thread per pair; 3 = k_addsub_il2; 4 = two-pass):
-// up to 8 limbs the two-pass route's first pass alone (one segment: 4907 GB/s at m = 4);
-// below 128 limbs thread per pair; from 128 limbs the re-read CTAs while they give every SM
-// at least 8 warps, else the two-pass route (its warps are (strip, segment) pairs, so a
-// few long numbers still fill the GPU). DOTG_IL_MODE (A/B
-// knob) forces 2 (thread per pair), 3 or 4 where they apply.
+// Interleaved routes, per-launch fraction of HBM when launches run back to back (CUDA
+// graph over 3 rotating input copies, tools/il_graph.py; B200, B x m = 2^22 limbs) at
+// m = 4 / 16 / 32 / 64 / 128 / 256 / 512 / 1024 (profiles/r02_il_graph*.jsonl):
+//   thread per pair           0.77 / 0.86 / 0.90 / 0.75 / 0.52 / 0.30 / 0.17 / 0.09
+//   re-read CTAs (il2)        0.77 / 0.73 / 0.74 / 0.74 / 0.71 / 0.69 / 0.67 / 0.64
+//   two passes                0.82 / 0.56 / 0.64 / 0.71 / 0.69 / 0.60 / 0.48 / 0.35
+//   streaming + fix-up (ilf)     - / 0.84 / 0.83 / 0.82 / 0.80 / 0.80 / 0.77 / 0.72
+// Auto: up to 8 limbs the two-pass route's first pass alone (one segment); below 48 limbs
+// thread per pair; then k_addsub_ilf, except a few very long numbers (m > 2048 and fewer
+// than 4096 pairs), which take the two-pass route (its warps are (strip, segment) pairs,
+// so they still fill the GPU). DOTG_IL_MODE (A/B knob) forces 2 (thread per pair), 3
+// (il2), 4 (two passes) or 5 (ilf) where they apply.
 int il_mode() {
     static const int v = [] {
         const char* e = std::getenv("DOTG_IL_MODE");
@@ -763,25 +962,23 @@ int il_route(size_t m, size_t batch) {
     if (mode == 2) return 0;
     if (mode == 3) return m >= 16 ? 3 : 0;
     if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
+    if (mode == 5) return m >= 2 ? 5 : 0;
     if (m <= size_t(kSL)) return nseg_fits(m, batch) ? 4 : 0;  // one segment: pass 1 alone
-    if (m < 128) return 0;
-    static thread_local struct { int dev = -1, sms = 148; } di;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (di.dev != dev) {
-        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
-        di.dev = dev;
-    }
-    const size_t warps = (batch + 31) / 32 * std::min<size_t>(32, m / 8);  // k_addsub_il2's warps
-    if (warps >= size_t(8) * size_t(di.sms)) return 3;
-    return nseg_fits(m, batch) ? 4 : 0;
+    if (m < 48) return 0;                                      // thread per pair
+    if (m <= 2048 || batch >= 4096) return 5;                  // streaming pass + in-CTA fix-up
+    return nseg_fits(m, batch) ? 4 : 5;  // a few very long numbers: (strip, segment) warps fill the GPU
 }
 
 template <bool SUB>
 cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags,
                         size_t m, size_t batch, size_t sp, size_t si, cudaStream_t st) {
-    const size_t blocks = (batch + 255) / 256;
-    k_addsub_strided<SUB><<<unsigned(blocks), 256, 0, st>>>(out, a, b, flags, m, batch, sp, si);
+    static const unsigned bs = [] {
+        const char* e = std::getenv("DOTG_TPP_BLOCK");  // A/B knob: threads per CTA (32 ... 256)
+        const int v = e ? std::atoi(e) : 256;
+        return unsigned(v >= 32 && v <= 256 ? v : 256);
+    }();
+    const size_t blocks = (batch + bs - 1) / bs;
+    k_addsub_strided<SUB><<<unsigned(blocks), bs, 0, st>>>(out, a, b, flags, m, batch, sp, si);
     count_launch();
     return cudaGetLastError();
 }
@@ -877,6 +1074,9 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
                 if (ir == 3)
                     e = P.sub ? run_interleaved_il2<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_il2<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                else if (ir == 5)
+                    e = P.sub ? run_interleaved_ilf<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                              : run_interleaved_ilf<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
                 else
                     e = P.sub ? run_interleaved_2pass<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_2pass<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);

@@ -1,0 +1,78 @@
+"""Every interleaved add/sub route, forced one at a time, against the oracle (bit-exact).
+
+The route for an interleaved [m][batch] problem is picked inside the library
+(csrc/addsub_batch.cu il_route); DOTG_IL_MODE forces one, read once per process, so each
+route runs in its own child: 2 thread per pair, 3 re-read segmented CTAs (k_addsub_il2),
+4 two streaming passes, 5 streaming pass with in-CTA fix-up (k_addsub_ilf, in each of its
+chunk / pairs-per-lane / double-buffering variants). Shapes cover ragged m, partial strips,
+segments with no rows, and the carry-stress categories whose propagate runs cross
+segment boundaries (the fix-up's rare multi-row branch)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import json, sys
+sys.path.insert(0, ROOT + "/tests")
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+import paper_2604_21566_b200 as dg
+from helpers import CATEGORIES, Oracle, category
+orc = Oracle()
+bad = []
+n = 0
+for m, batch in SHAPES:
+    rng = np.random.default_rng(9100 + 7 * m + batch)
+    for cat in CATEGORIES:
+        for op in ("add", "sub"):
+            a, b = category(rng, cat, op, (batch, m))
+            if cat == "random" and m > 12:  # a propagate run across segment boundaries
+                lo, hi = 3, m - 2
+                if op == "add":
+                    a[::3, lo:hi] = np.uint64(0xFFFFFFFFFFFFFFFF); b[::3, lo:hi] = 0
+                else:
+                    a[::3, lo:hi] = b[::3, lo:hi]
+            want, wf = orc.addsub_batch(op == "sub", a, b)
+            ta = torch.from_numpy(np.ascontiguousarray(a.T).view(np.int64)).cuda()
+            tb = torch.from_numpy(np.ascontiguousarray(b.T).view(np.int64)).cuda()
+            out, fl = dg.addsub_batch(op == "sub", ta, tb, layout="interleaved")
+            got = out.cpu().numpy().view(np.uint64).T
+            gf = fl.cpu().numpy().view(np.uint32)
+            n += 1
+            if not (np.array_equal(got, want) and np.array_equal(gf, wf)):
+                bad.append([m, batch, cat, op])
+print(json.dumps({"cases": n, "bad": bad[:10]}))
+'''.replace("ROOT", repr(ROOT))
+
+SHAPES = [(2, 70), (5, 33), (16, 64), (33, 40), (64, 96), (100, 65), (128, 128), (200, 130), (256, 190),
+          (257, 40), (512, 66), (777, 33), (1024, 64), (1500, 40)]
+
+SETTINGS = {
+    "tpp": {"DOTG_IL_MODE": "2"},
+    "il2": {"DOTG_IL_MODE": "3"},
+    "two_pass": {"DOTG_IL_MODE": "4"},
+    "ilf": {"DOTG_IL_MODE": "5"},
+    "ilf_ppl2": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "2"},
+    "ilf_un8": {"DOTG_IL_MODE": "5", "DOTG_ILF_UN": "8", "DOTG_ILF_DB": "0"},
+    "ilf_un16": {"DOTG_IL_MODE": "5", "DOTG_ILF_UN": "16", "DOTG_ILF_DB": "0"},
+    "ilf_ppl2_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "2", "DOTG_ILF_DB": "0"},
+    "ilf_wdiv4": {"DOTG_IL_MODE": "5", "DOTG_ILF_WDIV": "4"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(SETTINGS))
+def test_forced_route(cuda, name):
+    env = {**os.environ, **SETTINGS[name]}
+    code = CHILD.replace("SHAPES", repr(SHAPES))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["cases"] > 0 and not res["bad"], (name, res)
