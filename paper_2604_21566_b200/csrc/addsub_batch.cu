@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, 
     __shared__ uint32_t sG[16][PPL], sP[16][PPL];
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
     const size_t p = (size_t(blockIdx.x) * 32 + size_t(lane)) * PPL;
-    const bool ok = p < batch;  // PPL = 2: batch is even, a lane has both pairs or none
+    const bool ok = p < batch;  // PPL > 1: batch % PPL == 0, a lane has all its pairs or none
     const size_t r0 = size_t(w) * L < m ? size_t(w) * L : m;
     const size_t r1 = r0 + L < m ? r0 + L : m;
     constexpr uint64_t kProp = SUB ? 0ull : ~0ull;
@@ -546,7 +546,16 @@ __global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, 
 #pragma unroll
         for (int k = 0; k < UN; ++k)
             if (c0 + k < r1) {
-                if constexpr (PPL == 2) {
+                if constexpr (PPL == 4) {  // one 32-byte load per row and operand
+                    const uint64_t* pa = a + (c0 + k) * batch + p;
+                    const uint64_t* pb = b + (c0 + k) * batch + p;
+                    asm("ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+                        : "=l"(x[k][0]), "=l"(x[k][1]), "=l"(x[k][2]), "=l"(x[k][3])
+                        : "l"(pa));
+                    asm("ld.global.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
+                        : "=l"(y[k][0]), "=l"(y[k][1]), "=l"(y[k][2]), "=l"(y[k][3])
+                        : "l"(pb));
+                } else if constexpr (PPL == 2) {
                     const ulonglong2 u = __ldcs(reinterpret_cast<const ulonglong2*>(a + (c0 + k) * batch + p));
                     const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(b + (c0 + k) * batch + p));
                     x[k][0] = u.x, x[k][1] = u.y, y[k][0] = v.x, y[k][1] = v.y;
@@ -574,6 +583,8 @@ __global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, 
                 if (rel == 0) {
 #pragma unroll
                     for (int j = 0; j < PPL; ++j) first[j] = x[k][j];
+                } else if constexpr (PPL == 4) {
+                    st_stream<4>(out + (c0 + k) * batch + p, x[k]);
                 } else if constexpr (PPL == 2) {
                     __stcs(reinterpret_cast<ulonglong2*>(out + (c0 + k) * batch + p), make_ulonglong2(x[k][0], x[k][1]));
                 } else {
@@ -667,11 +678,12 @@ cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t
     // variants (chunk rows x pairs per lane, double-buffered?): 32 operand words in
     // registers each (16 x 1 double-buffered would spill)
     using KFn = void (*)(uint64_t*, const uint64_t*, const uint64_t*, uint32_t*, size_t, size_t, uint32_t);
-    static constexpr int kNV = 5;
+    static constexpr int kNV = 7;
     static const KFn kfn[kNV] = {k_addsub_ilf<SUB, 16, 1, false>, k_addsub_ilf<SUB, 8, 1, false>,
                                  k_addsub_ilf<SUB, 8, 2, false>,  k_addsub_ilf<SUB, 8, 1, true>,
-                                 k_addsub_ilf<SUB, 4, 2, true>};
-    static constexpr int kUN[kNV] = {16, 8, 8, 8, 4};
+                                 k_addsub_ilf<SUB, 4, 2, true>,   k_addsub_ilf<SUB, 4, 4, false>,
+                                 k_addsub_ilf<SUB, 2, 4, true>};
+    static constexpr int kUN[kNV] = {16, 8, 8, 8, 4, 4, 2};
     // resident CTAs per SM for each (variant, W = 1 ... 16)
     static thread_local struct { int dev = -1; int per[kNV][5]; } oc;
     if (oc.dev != dev) {
@@ -690,17 +702,20 @@ cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t
         for (int d = wdiv; d > 1 && wi > 0; d /= 2) --wi;
         return wi;
     };
-    const bool can2 = batch % 2 == 0 && ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
-                                          reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
-    const size_t strips1 = (batch + 31) / 32, strips2 = (batch + 63) / 64;
-    const int v1 = db_knob ? 3 : (un_knob == 8 ? 1 : 0), v2 = db_knob ? 4 : 2;
-    bool two;
-    if (ppl_knob == 1 || !can2) two = false;
-    else if (ppl_knob == 2) two = true;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                         reinterpret_cast<uintptr_t>(b);
+    const bool can2 = batch % 2 == 0 && (al & 15u) == 0;
+    const bool can4 = batch % 4 == 0 && (al & 31u) == 0;
+    const size_t strips1 = (batch + 31) / 32, strips2 = (batch + 63) / 64, strips4 = (batch + 127) / 128;
+    const int v1 = db_knob ? 3 : (un_knob == 8 ? 1 : 0), v2 = db_knob ? 4 : 2, v4 = db_knob ? 6 : 5;
+    int ppl;
+    if (ppl_knob == 4 && can4) ppl = 4;
+    else if (ppl_knob == 2 && can2) ppl = 2;
+    else if (ppl_knob == 1 || !can2) ppl = 1;
     else  // 16-byte rows unless they leave fewer warps (B200: m = 1024 at B = 4096 0.72 vs 0.59 of HBM)
-        two = (strips2 << split(v2, strips2)) >= (strips1 << split(v1, strips1));
-    const int kv = two ? v2 : v1;
-    const size_t strips = two ? strips2 : strips1;
+        ppl = (strips2 << split(v2, strips2)) >= (strips1 << split(v1, strips1)) ? 2 : 1;
+    const int kv = ppl == 4 ? v4 : (ppl == 2 ? v2 : v1);
+    const size_t strips = ppl == 4 ? strips4 : (ppl == 2 ? strips2 : strips1);
     const int W = 1 << split(kv, strips);
     const uint32_t L = uint32_t((m + W - 1) / W);
     kfn[kv]<<<unsigned(strips), W * 32, 0, st>>>(out, a, b, flags, m, batch, L);

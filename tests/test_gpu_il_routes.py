@@ -52,7 +52,7 @@ print(json.dumps({"cases": n, "bad": bad[:10]}))
 '''.replace("ROOT", repr(ROOT))
 
 SHAPES = [(2, 70), (5, 33), (16, 64), (33, 40), (64, 96), (100, 65), (128, 128), (200, 130), (256, 190),
-          (257, 40), (512, 66), (777, 33), (1024, 64), (1500, 40)]
+          (257, 40), (512, 66), (777, 33), (1024, 64), (1500, 40), (2048, 6), (3000, 2)]
 
 SETTINGS = {
     "tpp": {"DOTG_IL_MODE": "2"},
@@ -64,6 +64,8 @@ SETTINGS = {
     "ilf_un16": {"DOTG_IL_MODE": "5", "DOTG_ILF_UN": "16", "DOTG_ILF_DB": "0"},
     "ilf_ppl2_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "2", "DOTG_ILF_DB": "0"},
     "ilf_wdiv4": {"DOTG_IL_MODE": "5", "DOTG_ILF_WDIV": "4"},
+    "ilf_ppl4": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "4"},
+    "ilf_ppl4_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "4", "DOTG_ILF_DB": "0"},
 }
 
 
