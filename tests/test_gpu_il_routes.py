@@ -5,7 +5,7 @@ The route for an interleaved [m][batch] problem is picked inside the library
 route runs in its own child: 2 thread per pair, 3 re-read segmented CTAs (k_addsub_il2),
 4 two streaming passes, 5 streaming pass with in-CTA fix-up (k_addsub_ilf, in each of its
 chunk / pairs-per-lane / double-buffering variants). Shapes cover ragged m, partial strips,
-segments with no rows, and the carry-stress categories whose propagate runs cross
+segments with no rows, in-place calls (out = a), and the carry-stress categories whose propagate runs cross
 segment boundaries (the fix-up's rare multi-row branch)."""
 import json
 import os
@@ -48,6 +48,11 @@ for m, batch in SHAPES:
             n += 1
             if not (np.array_equal(got, want) and np.array_equal(gf, wf)):
                 bad.append([m, batch, cat, op])
+            # in place: out aliases a (every route reads a row before it rewrites it)
+            dg.addsub_batch(op == "sub", ta, tb, out=ta, flags=fl, layout="interleaved")
+            if not (np.array_equal(ta.cpu().numpy().view(np.uint64).T, want)
+                    and np.array_equal(fl.cpu().numpy().view(np.uint32), wf)):
+                bad.append([m, batch, cat, op, "in place"])
 print(json.dumps({"cases": n, "bad": bad[:10]}))
 '''.replace("ROOT", repr(ROOT))
 
