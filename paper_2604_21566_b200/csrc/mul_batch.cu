@@ -451,16 +451,36 @@ __device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uin
 #ifndef DOTG_K16_MINB
 #define DOTG_K16_MINB 16
 #endif
+// IL = true: the interleaved [m][batch] layout (limb i of pair p at i * batch + p), every
+// load / store coalesced across the warp's 32 consecutive pairs.
+template <bool IL>
 __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint64_t* out, const uint64_t* a,
                                                                            const uint64_t* b, size_t batch) {
     const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (pidx >= batch) return;
+    // output limbs [l0, l0 + 4) of this pair
+    auto put4 = [&](size_t l0, const uint64_t (&o)[4]) {
+        if constexpr (IL) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) __stcs(out + (l0 + k) * batch + pidx, o[k]);
+        } else {
+            st_stream<4>(out + pidx * 32 + l0, o);
+        }
+    };
     uint32_t Al[kK], Ah[kK], Bl[kK], Bh[kK];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
         uint64_t x[4], y[4];
-        ld_stream<4>(a + pidx * 16 + 4 * v, x);
-        ld_stream<4>(b + pidx * 16 + 4 * v, y);
+        if constexpr (IL) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                x[k] = __ldcs(a + size_t(4 * v + k) * batch + pidx);
+                y[k] = __ldcs(b + size_t(4 * v + k) * batch + pidx);
+            }
+        } else {
+            ld_stream<4>(a + pidx * 16 + 4 * v, x);
+            ld_stream<4>(b + pidx * 16 + 4 * v, y);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int w = 8 * v + 2 * k;  // word index 0..31
@@ -478,7 +498,6 @@ __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint
     mul16_words(Da, Db, Z1);
     mul16_words(Al, Bl, Z0);
     mul16_words(Ah, Bh, Z2);
-    uint64_t* po = out + pidx * 32;
     {  // R[0, 16) = z0[0, 16)
         uint64_t o0[4], o1[4];
 #pragma unroll
@@ -486,8 +505,8 @@ __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint
             o0[k] = uint64_t(Z0[2 * k]) | (uint64_t(Z0[2 * k + 1]) << 32);
             o1[k] = uint64_t(Z0[8 + 2 * k]) | (uint64_t(Z0[8 + 2 * k + 1]) << 32);
         }
-        st_stream<4>(po, o0);
-        st_stream<4>(po + 4, o1);
+        put4(0, o0);
+        put4(4, o1);
     }
     // mid = z0 + z2 - z1 (same signs) or + z1 (33 words; the true value is < 2^1025)
     const uint32_t neg = sa == sb ? 1u : 0u, mask = 0u - neg;
@@ -519,7 +538,7 @@ __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint
         uint64_t o[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[k] = uint64_t(r[2 * k]) | (uint64_t(r[2 * k + 1]) << 32);
-        st_stream<4>(po + 8 + 4 * q, o);
+        put4(size_t(8 + 4 * q), o);
     }
 }
 
@@ -996,7 +1015,14 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
             case 2: return run_regs<2, 1>(out, a, b, batch, stream);
             case 4: return run_regs<4, 1>(out, a, b, batch, stream);
             case 8: return run_regs<8, 1>(out, a, b, batch, stream);
-            case 16: return run_regs<16, 1>(out, a, b, batch, stream);
+            case 16:
+                if (route != 1) {  // the C3 kernel on the interleaved layout (one Karatsuba level)
+                    k_mul_kara16<true><<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0,
+                                         stream>>>(out, a, b, batch);
+                    count_launch();
+                    return cudaGetLastError();
+                }
+                return run_regs<16, 1>(out, a, b, batch, stream);
             default: return run_strided(out, a, b, m, batch, 1, stream);
         }
     }
@@ -1025,7 +1051,7 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
                 if (hybrid)
                     k_mul_kara16h<<<unsigned((batch + 31) / 32), 32, 0, stream>>>(out, a, b, batch);
                 else
-                    k_mul_kara16<<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0, stream>>>(
+                    k_mul_kara16<false><<<unsigned((batch + DOTG_K16_TPB - 1) / DOTG_K16_TPB), DOTG_K16_TPB, 0, stream>>>(
                         out, a, b, batch);
                 count_launch();
                 return cudaGetLastError();
