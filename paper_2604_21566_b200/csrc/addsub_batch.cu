@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cmath>
 #include <cstdlib>
 
 #include "device.cuh"
@@ -529,12 +530,16 @@ cudaError_t run_interleaved_il2(uint64_t* out, const uint64_t* a, const uint64_t
 template <bool SUB, int UN, int PPL, bool DB>
 __global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                                                     const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
-                                                    size_t batch, uint32_t L) {
-    __shared__ uint32_t sG[16][PPL], sP[16][PPL];
+                                                    size_t batch, uint32_t L, uint32_t G) {
+    // G lanes per segment (32, 16 or 8): a warp holds 32 / G segments of the strip's G * PPL
+    // pairs (narrower strips: more CTAs when the batch is small)
+    __shared__ uint32_t sG[64][PPL], sP[64][PPL];
     const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31u);
-    const size_t p = (size_t(blockIdx.x) * 32 + size_t(lane)) * PPL;
+    const uint32_t spw = 32u / G, ls = uint32_t(lane) % G;     // segments per warp, lane in segment
+    const uint32_t seg = uint32_t(w) * spw + uint32_t(lane) / G;  // segment index in the CTA
+    const size_t p = (size_t(blockIdx.x) * G + ls) * PPL;
     const bool ok = p < batch;  // PPL > 1: batch % PPL == 0, a lane has all its pairs or none
-    const size_t r0 = size_t(w) * L < m ? size_t(w) * L : m;
+    const size_t r0 = size_t(seg) * L < m ? size_t(seg) * L : m;
     const size_t r1 = r0 + L < m ? r0 + L : m;
     constexpr uint64_t kProp = SUB ? 0ull : ~0ull;
     uint64_t first[PPL], qv[PPL];
@@ -617,19 +622,24 @@ __global__ void __launch_bounds__(512) k_addsub_ilf(uint64_t* __restrict__ out, 
         }
     }
     const bool has = ok && r0 < r1;
+    const uint32_t gmask = G == 32 ? 0xffffffffu : (1u << G) - 1u;
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
         const uint32_t Gm = __ballot_sync(0xffffffffu, has && c[j]);
         const uint32_t Pm = __ballot_sync(0xffffffffu, !has || allp[j]);
-        if (lane == 0) sG[w][j] = Gm, sP[w][j] = Pm;
+        if (uint32_t(lane) < spw) {  // lane k stores the warp's k-th segment's masks
+            const uint32_t sh = uint32_t(lane) * G;
+            sG[uint32_t(w) * spw + uint32_t(lane)][j] = (Gm >> sh) & gmask;
+            sP[uint32_t(w) * spw + uint32_t(lane)][j] = (Pm >> sh) & gmask;
+        }
     }
     __syncthreads();
     if (!has) return;
 #pragma unroll
     for (int j = 0; j < PPL; ++j) {
-        uint32_t cm = 0;  // carries into segment w, one bit per lane
-        for (int i = 0; i < w; ++i) cm = sG[i][j] | (sP[i][j] & cm);
-        const uint32_t cin = (cm >> lane) & 1u;
+        uint32_t cm = 0;  // carries into this segment, one bit per pair lane
+        for (uint32_t i = 0; i < seg; ++i) cm = sG[i][j] | (sP[i][j] & cm);
+        const uint32_t cin = (cm >> ls) & 1u;
         uint64_t* po = out + r0 * batch + p + j;
         if (!cin) {
             po[0] = first[j];
@@ -677,7 +687,7 @@ cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t
     }();
     // variants (chunk rows x pairs per lane, double-buffered?): 32 operand words in
     // registers each (16 x 1 double-buffered would spill)
-    using KFn = void (*)(uint64_t*, const uint64_t*, const uint64_t*, uint32_t*, size_t, size_t, uint32_t);
+    using KFn = void (*)(uint64_t*, const uint64_t*, const uint64_t*, uint32_t*, size_t, size_t, uint32_t, uint32_t);
     static constexpr int kNV = 7;
     static const KFn kfn[kNV] = {k_addsub_ilf<SUB, 16, 1, false>, k_addsub_ilf<SUB, 8, 1, false>,
                                  k_addsub_ilf<SUB, 8, 2, false>,  k_addsub_ilf<SUB, 8, 1, true>,
@@ -695,30 +705,56 @@ cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t
             }
         oc.dev = dev;
     }
-    // the widest CTA (most warps per strip, W = 2^wi) whose grid still fits one wave
-    auto split = [&](int kv, size_t strips) {
-        int wi = 4;
-        while (wi > 0 && (strips > size_t(oc.per[kv][wi]) * size_t(di.sms) || (size_t(kUN[kv]) << wi) > m)) --wi;
-        for (int d = wdiv; d > 1 && wi > 0; d /= 2) --wi;
-        return wi;
+    static const int g_knob = [] {
+        const char* e = std::getenv("DOTG_ILF_G");  // A/B knob: lanes per segment (32, 16, 8; 0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    // Shape: lanes per segment G, W = 2^wi warps per CTA, strips of G * PPL pairs, S = W * 32
+    // / G segments per strip. Every segment streams at least one chunk and the grid is ONE
+    // wave (warps stream their rows; a second wave would start late and end the launch
+    // with a tail); among those, the most warps weighted by the share of SMs given a CTA
+    // (ncu: with fewer strips than SMs the rest idle). Ties keep G = 32 (whole 128-byte
+    // lines per warp row) and 16-byte rows.
+    struct Shape { int kv = 0, wi = 0; uint32_t G = 32; size_t strips = 0; double score = -1.0; };
+    auto consider = [&](Shape& best, int kv, int ppl) {
+        for (uint32_t G = 32; G >= 8; G /= 2) {
+            if (g_knob != 0 && uint32_t(g_knob) != G) continue;
+            const size_t strips = (batch + size_t(G) * ppl - 1) / (size_t(G) * ppl);
+            int wi = 4;
+            while (wi > 0 && (strips > size_t(oc.per[kv][wi]) * size_t(di.sms) ||
+                              ((size_t(kUN[kv]) << wi) * (32 / G)) > m))
+                --wi;
+            for (int d = wdiv; d > 1 && wi > 0; d /= 2) --wi;
+            // resident warps x share of SMs with a CTA x whole-wave efficiency (a grid that
+            // does not fit one wave even at W = 1 ends with a partial wave)
+            const double cap = double(oc.per[kv][wi]) * double(di.sms);
+            const double waves = double(strips) / cap;
+            const double sc = std::min(double(strips), cap) * double(1 << wi) *
+                              std::min(1.0, double(strips) / double(di.sms)) *
+                              (waves <= 1.0 ? 1.0 : waves / std::ceil(waves));
+            if (sc > best.score * 1.0001) best = Shape{kv, wi, G, strips, sc};
+        }
     };
     const uintptr_t al = reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
                          reinterpret_cast<uintptr_t>(b);
     const bool can2 = batch % 2 == 0 && (al & 15u) == 0;
     const bool can4 = batch % 4 == 0 && (al & 31u) == 0;
-    const size_t strips1 = (batch + 31) / 32, strips2 = (batch + 63) / 64, strips4 = (batch + 127) / 128;
     const int v1 = db_knob ? 3 : (un_knob == 8 ? 1 : 0), v2 = db_knob ? 4 : 2, v4 = db_knob ? 6 : 5;
-    int ppl;
-    if (ppl_knob == 4 && can4) ppl = 4;
-    else if (ppl_knob == 2 && can2) ppl = 2;
-    else if (ppl_knob == 1 || !can2) ppl = 1;
-    else  // 16-byte rows unless they leave fewer warps (B200: m = 1024 at B = 4096 0.72 vs 0.59 of HBM)
-        ppl = (strips2 << split(v2, strips2)) >= (strips1 << split(v1, strips1)) ? 2 : 1;
-    const int kv = ppl == 4 ? v4 : (ppl == 2 ? v2 : v1);
-    const size_t strips = ppl == 4 ? strips4 : (ppl == 2 ? strips2 : strips1);
-    const int W = 1 << split(kv, strips);
-    const uint32_t L = uint32_t((m + W - 1) / W);
-    kfn[kv]<<<unsigned(strips), W * 32, 0, st>>>(out, a, b, flags, m, batch, L);
+    Shape sh;
+    if (ppl_knob == 4 && can4) {
+        consider(sh, v4, 4);
+    } else if (ppl_knob == 2 && can2) {
+        consider(sh, v2, 2);
+    } else if (ppl_knob == 1 || !can2) {
+        consider(sh, v1, 1);
+    } else {  // 16-byte rows unless 8-byte rows give more warps on more SMs
+        consider(sh, v2, 2);
+        consider(sh, v1, 1);
+    }
+    const int W = 1 << sh.wi;
+    const uint32_t S = uint32_t(W) * (32u / sh.G);
+    const uint32_t L = uint32_t((m + S - 1) / S);
+    kfn[sh.kv]<<<unsigned(sh.strips), W * 32, 0, st>>>(out, a, b, flags, m, batch, L, sh.G);
     count_launch();
     return cudaGetLastError();
 }

@@ -70,6 +70,8 @@ SETTINGS = {
     "ilf_ppl2_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "2", "DOTG_ILF_DB": "0"},
     "ilf_wdiv4": {"DOTG_IL_MODE": "5", "DOTG_ILF_WDIV": "4"},
     "ilf_ppl4": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "4"},
+    "ilf_g16": {"DOTG_IL_MODE": "5", "DOTG_ILF_G": "16"},
+    "ilf_g8_ppl1": {"DOTG_IL_MODE": "5", "DOTG_ILF_G": "8", "DOTG_ILF_PPL": "1"},
     "ilf_ppl4_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "4", "DOTG_ILF_DB": "0"},
 }
 
