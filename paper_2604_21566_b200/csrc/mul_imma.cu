@@ -157,14 +157,22 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 #define DOTG_IMMA_MINB16 1
 #endif
 // IL = true: the batch-interleaved layout [m][batch] (limb i of pair p at i * batch + p),
-// read and written in place - no transposes. The 4 warps of a CTA take 4 consecutive
-// pairs at a time; the CTA loads their [m][4] operand tiles cooperatively (4 lanes per
-// 32-byte limb row: 8 sectors per warp instruction, where a warp loading its own pair
-// touched 32), one group ahead in registers, into padded shared tiles each warp reads its
-// pair from; products go back the same way through a [2m][4] tile. (r02 first version,
-// every warp loading its own pair: L1 92% busy, 139 us at m = 64.) Row-major (IL = false)
-// uses the per-warp mbarrier ring of cp.async.bulk copies.
-constexpr int kTileP = 9;  // words per [.][4 pairs] tile row: 8 + 1 pad (odd: conflict-free columns)
+// read and written in place - no transposes. A CTA takes kGP = 16 consecutive pairs at a
+// time (4 per warp): it loads their [m][16] operand tiles with whole 128-byte rows (16
+// threads per limb row) into one padded shared tile, each warp runs its 4 pairs from
+// their tile columns and writes each product back into its own pair's column (2m limbs:
+// the operand rows it replaces are already staged), and the CTA stores the [2m][16]
+// product tile with whole rows. Two barriers per 16 pairs. (r02: a [m][4] tile per 4
+// pairs, 32-byte rows, two barriers per 4 pairs: 105 us at m = 64; every warp loading
+// its own pair: 139 us, L1 92% busy.) Row-major (IL = false) uses the per-warp mbarrier
+// ring of cp.async.bulk copies.
+#ifndef DOTG_IMMA_GP16
+#define DOTG_IMMA_GP16 16
+#endif
+// pairs per interleaved CTA group (NB = 16: DOTG_IMMA_GP16) and words per tile row (2 per
+// pair + 1 pad: odd, so the warps' column reads are conflict-free)
+template <int NB> __host__ __device__ constexpr int il_gp() { return NB == 16 ? DOTG_IMMA_GP16 : 16; }
+template <int NB> __host__ __device__ constexpr int il_pitch() { return 2 * il_gp<NB>() + 1; }
 template <int NB, bool IL>
 __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMMA_MINB16) : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
@@ -183,8 +191,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
     int* S = reinterpret_cast<int*>(sa + C::A_WORDS);         // column sums
     __shared__ uint64_t bars[kImmaWarps][C::ST];
     uint64_t* bar = bars[warp];
-    // IL tiles: operands [2][M][kTileP], product [2M][kTileP] (u32 words)
-    __shared__ uint32_t til[IL ? 2 * C::M * kTileP : 1], tol[IL ? 2 * C::M * kTileP : 1];
+    // IL tile: rows [0, M) operand a, [M, 2M) operand b, later rows [0, 2M) the products
+    constexpr int kGP = il_gp<NB>(), kTileP = il_pitch<NB>();
+    __shared__ uint32_t tile[IL ? 2 * C::M * kTileP : 1];
     for (int i = lane; i < C::COPY_WORDS + C::A_WORDS; i += 32) cp[i] = 0;  // padding stays zero
     if (!IL && mr < C::M)
         for (int i = lane; i < C::RAW_WORDS; i += 32) raw[i] = 0;
@@ -209,101 +218,45 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
             if (first + size_t(st) * nwarps < batch) issue(st, first + size_t(st) * nwarps);
     }
     __syncwarp();
-    // IL: lane's VW operand words of a pair = limbs VW/2 * lane ... (VW even for m >= 32)
-    static_assert(!IL || (C::VW % 2 == 0), "interleaved route needs two or more words per lane");
-    constexpr int LL = C::VW / 2 > 0 ? C::VW / 2 : 1;  // limbs per lane
-    constexpr int RP = C::M / 32 > 0 ? C::M / 32 : 1;  // tile rows per thread per operand
-    const int trow = threadIdx.x >> 2, tp = threadIdx.x & 3;  // cooperative load: row, pair in group
-    const size_t ngroups = (batch + 3) / 4;
-    uint64_t na[RP], nb[RP];
-    auto il_load = [&](size_t grp) {
-        const size_t pr = grp * 4 + size_t(tp);
+
+    // ---- stage: copy_s[i] = bytes bpad[4i + s ..], bpad[y] = b[y - 31]; word j of b feeds
+    // copy index i = j + 8 (with word j + 1), and i = 7 takes (0, b[0]). av / bv: the lane's
+    // VW operand words (lanes < LD_LANES).
+    auto stage_pair = [&](uint32_t (&av)[C::VW], uint32_t (&bv)[C::VW + 1]) {
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, bv[0], 1);
+        if (lane < C::LD_LANES) {
+            bv[C::VW] = lane + 1 < C::LD_LANES ? nxt : 0u;
+            const int j0 = lane * C::VW;  // copy index j0 + 8 is VW-aligned
+            uint32_t c0[C::VW], c1[C::VW], c2[C::VW], c3[C::VW], sv[C::VW];
 #pragma unroll
-        for (int j = 0; j < RP; ++j) {
-            const int r = trow + 32 * j;
-            const bool okl = grp < ngroups && pr < batch && r < mr;
-            na[j] = okl ? __ldg(a + size_t(r) * batch + pr) : 0ull;
-            nb[j] = okl ? __ldg(b + size_t(r) * batch + pr) : 0ull;
-        }
-    };
-    if (IL) il_load(blockIdx.x);
-    int stage = 0;
-    uint32_t parity = 0;
-    for (size_t grp = blockIdx.x, pair = IL ? size_t(blockIdx.x) * 4 + warp : first; IL ? grp < ngroups : pair < batch;
-         grp += gridDim.x, pair += nwarps) {
-        if (!IL) mbar_wait(&bar[stage], parity);
-        // ---- stage: copy_s[i] = bytes bpad[4i + s ..], bpad[y] = b[y - 31]; word j of b
-        // feeds copy index i = j + 8 (with word j + 1), and i = 7 takes (0, b[0]).
-        {
-            const uint32_t* ra = raw + stage * 2 * C::NW;
-            const uint32_t* rb = ra + C::NW;
-            uint32_t bv[C::VW + 1], av[C::VW];
-            if constexpr (IL) {
-#pragma unroll
-                for (int j = 0; j < RP; ++j) {
-                    const int r = trow + 32 * j;
-                    uint32_t* ta = til + r * kTileP + 2 * tp;
-                    uint32_t* tb = til + (C::M + r) * kTileP + 2 * tp;
-                    ta[0] = uint32_t(na[j]);
-                    ta[1] = uint32_t(na[j] >> 32);
-                    tb[0] = uint32_t(nb[j]);
-                    tb[1] = uint32_t(nb[j] >> 32);
-                }
-                __syncthreads();
-                il_load(grp + gridDim.x);  // the next group's operands in flight during this one
-#pragma unroll
-                for (int e = 0; e < LL; ++e) {
-                    const int L = lane * LL + e;
-                    av[2 * e] = til[L * kTileP + 2 * warp];
-                    av[2 * e + 1] = til[L * kTileP + 2 * warp + 1];
-                    bv[2 * e] = til[(C::M + L) * kTileP + 2 * warp];
-                    bv[2 * e + 1] = til[(C::M + L) * kTileP + 2 * warp + 1];
-                }
-            } else if (lane < C::LD_LANES) {
-                lds_vec<C::VW>(rb + lane * C::VW, bv);
-                lds_vec<C::VW>(ra + lane * C::VW, av);
+            for (int e = 0; e < C::VW; ++e) {
+                const uint32_t lo = bv[e], hi = bv[e + 1];
+                c0[e] = __funnelshift_r(lo, hi, 8);
+                c1[e] = __funnelshift_r(lo, hi, 16);
+                c2[e] = __funnelshift_r(lo, hi, 24);
+                c3[e] = hi;
+                sv[e] = bswap32(av[e]);
             }
-            const uint32_t nxt = __shfl_down_sync(0xffffffffu, bv[0], 1);
-            if (lane < C::LD_LANES) {
-                bv[C::VW] = lane + 1 < C::LD_LANES ? nxt : 0u;
-                const int j0 = lane * C::VW;  // copy index j0 + 8 is VW-aligned
-                uint32_t c0[C::VW], c1[C::VW], c2[C::VW], c3[C::VW], sv[C::VW];
-#pragma unroll
-                for (int e = 0; e < C::VW; ++e) {
-                    const uint32_t lo = bv[e], hi = bv[e + 1];
-                    c0[e] = __funnelshift_r(lo, hi, 8);
-                    c1[e] = __funnelshift_r(lo, hi, 16);
-                    c2[e] = __funnelshift_r(lo, hi, 24);
-                    c3[e] = hi;
-                    sv[e] = bswap32(av[e]);
-                }
-                sts_vec<C::VW>(cp + 0 * C::CLP + j0 + 8, c0);
-                sts_vec<C::VW>(cp + 1 * C::CLP + j0 + 8, c1);
-                sts_vec<C::VW>(cp + 2 * C::CLP + j0 + 8, c2);
-                sts_vec<C::VW>(cp + 3 * C::CLP + j0 + 8, c3);
-                sts_vec<C::VW>(sa + aidx(j0), sv);
-                if (lane == 0) {
-                    cp[0 * C::CLP + 7] = bv[0] << 24;
-                    cp[1 * C::CLP + 7] = bv[0] << 16;
-                    cp[2 * C::CLP + 7] = bv[0] << 8;
-                    cp[3 * C::CLP + 7] = bv[0];
-                }
+            sts_vec<C::VW>(cp + 0 * C::CLP + j0 + 8, c0);
+            sts_vec<C::VW>(cp + 1 * C::CLP + j0 + 8, c1);
+            sts_vec<C::VW>(cp + 2 * C::CLP + j0 + 8, c2);
+            sts_vec<C::VW>(cp + 3 * C::CLP + j0 + 8, c3);
+            sts_vec<C::VW>(sa + aidx(j0), sv);
+            if (lane == 0) {
+                cp[0 * C::CLP + 7] = bv[0] << 24;
+                cp[1 * C::CLP + 7] = bv[0] << 16;
+                cp[2 * C::CLP + 7] = bv[0] << 8;
+                cp[3 * C::CLP + 7] = bv[0];
             }
         }
         __syncwarp();
-        // ---- the raw slot is consumed: refill it with the pair ST steps ahead
-        if (!IL && lane == 0) {
-            const size_t ahead = pair + size_t(C::ST) * nwarps;
-            if (ahead < batch) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(stage, ahead);
-            }
-        }
-        if (++stage == C::ST) {
-            stage = 0;
-            parity ^= 1u;
-        }
-        // ---- a-blocks in registers: Q[m] = block (g - m), words 7 - t and 3 - t
+    };
+
+    // ---- tensor-core column sums of the staged pair, then the deferred carry pass:
+    // lo[k] = product limb lane + 32 k (lanes < LANES)
+    const bool active = lane < C::LANES;
+    auto multiply_staged = [&](uint64_t (&lo)[C::LPL]) {
+        // a-blocks in registers: Q[m] = block (g - m), words 7 - t and 3 - t
         uint32_t Q0[C::NQ], Q1[C::NQ];
         const uint32_t* qb = sa + 12 * (g + 7 + NB - 1) + 3 - t;  // block g - m, m = q - (NB - 1)
 #pragma unroll
@@ -311,7 +264,6 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
             Q0[q] = qb[4 - 12 * q];
             Q1[q] = qb[-12 * q];
         }
-        // ---- tensor-core column sums
         int D[2][C::NC0][4];
 #pragma unroll
         for (int r = 0; r < 2; ++r)
@@ -332,9 +284,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
                 imma(D[1][c], y0, y1, z0, z1, Q0[q], Q1[q]);
             }
         }
-        // ---- column sums to shared memory: tile (R0 = 16 r, c0 = 8 c): d0 -> x,
-        // d1 -> x + 32, d2 -> x + 8, d3 -> x + 40, x = R0 + g + 32 (c0 + 2t); padded index
-        // x + 4 (x >> 5) keeps these stores and the limb reads below conflict-free.
+        // column sums to shared memory: tile (R0 = 16 r, c0 = 8 c): d0 -> x, d1 -> x + 32,
+        // d2 -> x + 8, d3 -> x + 40, x = R0 + g + 32 (c0 + 2t); padded index x + 4 (x >> 5)
+        // keeps these stores and the limb reads below conflict-free.
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -349,13 +301,12 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
                 }
             }
         __syncwarp();
-        // ---- deferred carry normalisation. Lane l owns limbs L = l + 32k; limb value
+        // deferred carry normalisation. Lane l owns limbs L = l + 32k; limb value
         // sum_e S[8L + e] 2^(8e) < 2^83 as (lo, hi); t_L = lo_L + hi_{L-1} with generate =
         // carry out of that add and propagate = (t_L == ~0), then one ballot lookahead per
         // 32-limb segment, segments chained through their carry-out.
         typedef unsigned __int128 u128;
-        const bool active = lane < C::LANES;
-        uint64_t lo[C::LPL], hi[C::LPL];
+        uint64_t hi[C::LPL];
 #pragma unroll
         for (int k = 0; k < C::LPL; ++k) {
             const int L = lane + 32 * k;
@@ -384,32 +335,109 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
             const uint32_t gk = active && sv < h, pk = active && sv == ~0ull;
             const uint32_t Gm = __ballot_sync(0xffffffffu, gk), Pm = __ballot_sync(0xffffffffu, pk);
             const uint64_t y = ((uint64_t(Gm) << 1) | cseg) + uint64_t(Pm);
-            const uint32_t C = uint32_t(y) ^ Pm;
+            const uint32_t Cm = uint32_t(y) ^ Pm;
             cseg = uint32_t(y >> 32);
-            sv += (C >> lane) & 1u;
+            sv += (Cm >> lane) & 1u;
             lo[k] = sv;
         }
-        if constexpr (IL) {
-            // product limbs into the [2M][4] tile, then the CTA stores whole 32-byte rows
-            if (active)
+    };
+
+    if constexpr (IL) {
+        // IL: lane's VW operand words of a pair = limbs VW/2 * lane ... (VW even for m >= 32)
+        static_assert(C::VW % 2 == 0, "interleaved route needs two or more words per lane");
+        constexpr int LL = C::VW / 2;                       // limbs per lane
+        constexpr int NE = 2 * C::M * kGP / (kImmaWarps * 32);  // tile elements per thread
+        static_assert((2 * C::M * kGP) % (kImmaWarps * 32) == 0, "tile split");
+        const size_t ngroups = (batch + kGP - 1) / kGP;
+        // element e = threadIdx.x + 128 i of a tile: row e / 16, pair column e % 16 (16
+        // consecutive threads: one 128-byte limb row)
+        for (size_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+            {
+                uint64_t v[NE];
 #pragma unroll
-                for (int k = 0; k < C::LPL; ++k) {
-                    uint32_t* to = tol + (lane + 32 * k) * kTileP + 2 * warp;
-                    to[0] = uint32_t(lo[k]);
-                    to[1] = uint32_t(lo[k] >> 32);
+                for (int i = 0; i < NE; ++i) {
+                    const int e = threadIdx.x + kImmaWarps * 32 * i;
+                    const int r = e / kGP, col = e % kGP;
+                    const int lr = r < C::M ? r : r - C::M;  // rows [0, M): a, [M, 2M): b
+                    const size_t pr = grp * kGP + size_t(col);
+                    v[i] = (pr < batch && lr < mr) ? __ldg((r < C::M ? a : b) + size_t(lr) * batch + pr) : 0ull;
                 }
-            __syncthreads();
-            const size_t pr = grp * 4 + size_t(tp);
 #pragma unroll
-            for (int j = 0; j < 2 * RP; ++j) {
-                const int r = trow + 32 * j;
-                if (r < 2 * mr && pr < batch) {
-                    const uint32_t* to = tol + r * kTileP + 2 * tp;
-                    out[size_t(r) * batch + pr] = uint64_t(to[0]) | (uint64_t(to[1]) << 32);
+                for (int i = 0; i < NE; ++i) {
+                    const int e = threadIdx.x + kImmaWarps * 32 * i;
+                    uint32_t* tp = tile + (e / kGP) * kTileP + 2 * (e % kGP);
+                    tp[0] = uint32_t(v[i]);
+                    tp[1] = uint32_t(v[i] >> 32);
                 }
             }
-        } else if (active) {
+            __syncthreads();
+#pragma unroll 1
+            for (int j = 0; j < kGP / kImmaWarps; ++j) {
+                const int col = warp * (kGP / kImmaWarps) + j;
+                uint32_t bv[C::VW + 1], av[C::VW];
+#pragma unroll
+                for (int e = 0; e < LL; ++e) {
+                    const int L = lane * LL + e;
+                    av[2 * e] = tile[L * kTileP + 2 * col];
+                    av[2 * e + 1] = tile[L * kTileP + 2 * col + 1];
+                    bv[2 * e] = tile[(C::M + L) * kTileP + 2 * col];
+                    bv[2 * e + 1] = tile[(C::M + L) * kTileP + 2 * col + 1];
+                }
+                stage_pair(av, bv);  // the column's operand rows are free from here on
+                uint64_t lo[C::LPL];
+                multiply_staged(lo);
+                if (active)
+#pragma unroll
+                    for (int k = 0; k < C::LPL; ++k) {
+                        uint32_t* to = tile + (lane + 32 * k) * kTileP + 2 * col;
+                        to[0] = uint32_t(lo[k]);
+                        to[1] = uint32_t(lo[k] >> 32);
+                    }
+            }
+            __syncthreads();
+            // the products, whole rows; the same element mapping as the load above, so the
+            // next group's tile writes need no barrier after these reads
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int e = threadIdx.x + kImmaWarps * 32 * i;
+                const int r = e / kGP, col = e % kGP;
+                const size_t pr = grp * kGP + size_t(col);
+                if (pr < batch && r < 2 * mr) {
+                    const uint32_t* tp = tile + r * kTileP + 2 * col;
+                    out[size_t(r) * batch + pr] = uint64_t(tp[0]) | (uint64_t(tp[1]) << 32);
+                }
+            }
+        }
+    } else {
+        int stage = 0;
+        uint32_t parity = 0;
+        for (size_t pair = first; pair < batch; pair += nwarps) {
+            mbar_wait(&bar[stage], parity);
             {
+                const uint32_t* ra = raw + stage * 2 * C::NW;
+                const uint32_t* rb = ra + C::NW;
+                uint32_t bv[C::VW + 1], av[C::VW];
+                if (lane < C::LD_LANES) {
+                    lds_vec<C::VW>(rb + lane * C::VW, bv);
+                    lds_vec<C::VW>(ra + lane * C::VW, av);
+                }
+                stage_pair(av, bv);
+            }
+            // the raw slot is consumed: refill it with the pair ST steps ahead
+            if (lane == 0) {
+                const size_t ahead = pair + size_t(C::ST) * nwarps;
+                if (ahead < batch) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(stage, ahead);
+                }
+            }
+            if (++stage == C::ST) {
+                stage = 0;
+                parity ^= 1u;
+            }
+            uint64_t lo[C::LPL];
+            multiply_staged(lo);
+            if (active) {
                 uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
 #pragma unroll
                 for (int k = 0; k < C::LPL; ++k)
@@ -430,7 +458,7 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
     if (di.dev != dev) {
         int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (smem > 48 * 1024) {
+        {  // dynamic + static (the interleaved tile) may pass the 48 KB default either way
             cudaError_t e = cudaFuncSetAttribute(k_mul_imma<NB, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             if (e != cudaSuccess) return e;
         }
