@@ -169,12 +169,18 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
 #ifndef DOTG_IMMA_GP16
 #define DOTG_IMMA_GP16 16
 #endif
+#ifndef DOTG_IMMA_IL_PREFETCH
+#define DOTG_IMMA_IL_PREFETCH 1  // the next group's tile loads in flight during this one (0: load on arrival)
+#endif
+#ifndef DOTG_IMMA_IL_MINB16
+#define DOTG_IMMA_IL_MINB16 3  // 150 registers for the prefetch (4 CTAs/SM would spill)
+#endif
 // pairs per interleaved CTA group (NB = 16: DOTG_IMMA_GP16) and words per tile row (2 per
 // pair + 1 pad: odd, so the warps' column reads are conflict-free)
 template <int NB> __host__ __device__ constexpr int il_gp() { return NB == 16 ? DOTG_IMMA_GP16 : 16; }
 template <int NB> __host__ __device__ constexpr int il_pitch() { return 2 * il_gp<NB>() + 1; }
 template <int NB, bool IL>
-__global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMMA_MINB16) : 1) k_mul_imma(uint64_t* __restrict__ out,
+__global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL_MINB16 : DOTG_IMMA_MINB16) : 1) k_mul_imma(uint64_t* __restrict__ out,
                                                               const uint64_t* __restrict__ a,
                                                               const uint64_t* __restrict__ b, size_t batch,
                                                               int mr) {
@@ -351,26 +357,30 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? 4 : DOTG_IMM
         const size_t ngroups = (batch + kGP - 1) / kGP;
         // element e = threadIdx.x + 128 i of a tile: row e / 16, pair column e % 16 (16
         // consecutive threads: one 128-byte limb row)
+        uint64_t v[NE];
+        auto fetch = [&](size_t grp) {
+#pragma unroll
+            for (int i = 0; i < NE; ++i) {
+                const int e = threadIdx.x + kImmaWarps * 32 * i;
+                const int r = e / kGP, col = e % kGP;
+                const int lr = r < C::M ? r : r - C::M;  // rows [0, M): a, [M, 2M): b
+                const size_t pr = grp * kGP + size_t(col);
+                v[i] = (grp < ngroups && pr < batch && lr < mr) ? __ldg((r < C::M ? a : b) + size_t(lr) * batch + pr)
+                                                                 : 0ull;
+            }
+        };
+        if (DOTG_IMMA_IL_PREFETCH) fetch(blockIdx.x);
         for (size_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-            {
-                uint64_t v[NE];
+            if (!DOTG_IMMA_IL_PREFETCH) fetch(grp);
 #pragma unroll
-                for (int i = 0; i < NE; ++i) {
-                    const int e = threadIdx.x + kImmaWarps * 32 * i;
-                    const int r = e / kGP, col = e % kGP;
-                    const int lr = r < C::M ? r : r - C::M;  // rows [0, M): a, [M, 2M): b
-                    const size_t pr = grp * kGP + size_t(col);
-                    v[i] = (pr < batch && lr < mr) ? __ldg((r < C::M ? a : b) + size_t(lr) * batch + pr) : 0ull;
-                }
-#pragma unroll
-                for (int i = 0; i < NE; ++i) {
-                    const int e = threadIdx.x + kImmaWarps * 32 * i;
-                    uint32_t* tp = tile + (e / kGP) * kTileP + 2 * (e % kGP);
-                    tp[0] = uint32_t(v[i]);
-                    tp[1] = uint32_t(v[i] >> 32);
-                }
+            for (int i = 0; i < NE; ++i) {
+                const int e = threadIdx.x + kImmaWarps * 32 * i;
+                uint32_t* tp = tile + (e / kGP) * kTileP + 2 * (e % kGP);
+                tp[0] = uint32_t(v[i]);
+                tp[1] = uint32_t(v[i] >> 32);
             }
             __syncthreads();
+            if (DOTG_IMMA_IL_PREFETCH) fetch(grp + gridDim.x);  // in flight during this group
 #pragma unroll 1
             for (int j = 0; j < kGP / kImmaWarps; ++j) {
                 const int col = warp * (kGP / kImmaWarps) + j;
