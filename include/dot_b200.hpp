@@ -24,6 +24,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "dotg.h"
@@ -49,9 +50,10 @@ constexpr unsigned lane_count(Width w) { return w == Width::scalar ? 8u : static
 
 inline constexpr std::size_t kMaxMulLimbs = std::size_t(1) << 24;  // mul.hpp:30
 
-// The counters of the reference's AddSubStats (addsub.hpp:53-72) that the device path
-// reproduces (derived on the device from a, b and the result, csrc/stats.cu). The rdtsc
-// phase ticks have no device equivalent: collect_ticks = true throws std::logic_error.
+// The reference's AddSubStats (addsub.hpp:53-72): the counters are derived on the device
+// from a, b and the result (csrc/stats.cu); collect_ticks fills the phase ticks from the
+// timed team kernel (SM clock laps) for power-of-two m <= 256 and throws
+// std::logic_error otherwise.
 struct AddSubStats {
     std::uint64_t chunks_processed = 0;
     std::uint64_t phase4_triggers = 0;
@@ -210,6 +212,58 @@ inline int compare(const Limbs& a, const Limbs& b) {
     std::int32_t r = 0;
     detail::check(dotg_compare_host(&r, pa.data(), pb.data(), m, 1));
     return r;
+}
+inline int compare(std::span<const limb_t> a, std::span<const limb_t> b) {  // limbs.hpp:83
+    return compare(Limbs(a.begin(), a.end()), Limbs(b.begin(), b.end()));
+}
+
+// The host-side value helpers of limbs.hpp:51-89 (lengths, zeros and headroom bits only;
+// nothing here is arithmetic on the path).
+inline std::size_t sig_limbs(std::span<const limb_t> a) {  // limbs.hpp:80
+    std::size_t n = a.size();
+    for (; n != 0 && a[n - 1] == 0; --n) {
+    }
+    return n;
+}
+inline Limbs normalized(Limbs a) {  // limbs.hpp:81
+    a.resize(sig_limbs(a));
+    return a;
+}
+inline bool eq(const Limbs& a, const Limbs& b) { return compare(a, b) == 0; }  // limbs.hpp:88
+inline bool is_zero(const Limbs& a) { return sig_limbs(a) == 0; }           // limbs.hpp:89
+inline void check_radix(RadixConfig cfg) {                                   // limbs.hpp:51-52
+    if (cfg.limb_bits != 64 && cfg.limb_bits != 52)
+        throw std::invalid_argument("RadixConfig: limb_bits must be 64 or 52");
+}
+inline void check_limbs(const Limbs& a, RadixConfig cfg) {  // limbs.hpp:54-55
+    check_radix(cfg);
+    if (cfg.limb_bits == 64) return;
+    for (std::size_t i = 0; i < a.size(); ++i)
+        if (a[i] >> cfg.limb_bits)
+            throw std::invalid_argument("limb " + std::to_string(i) + " exceeds the configured limb width");
+}
+
+// Width names (addsub.hpp:39-44). The widths select nothing on the device; dispatch_note
+// names what actually runs.
+inline std::string_view to_string(Width w) {
+    switch (w) {
+        case Width::scalar: return "scalar";
+        case Width::w2: return "2";
+        case Width::w4: return "4";
+        case Width::w8: return "8";
+    }
+    return "?";
+}
+inline Width width_from_string(std::string_view s) {
+    if (s == "scalar") return Width::scalar;
+    if (s == "2") return Width::w2;
+    if (s == "4") return Width::w4;
+    if (s == "8") return Width::w8;
+    throw std::invalid_argument("unknown width: expected one of 2, 4, 8, scalar");
+}
+inline std::string_view dispatch_note(Width w) {
+    detail::validate(w);
+    return "sm_100a";  // every width runs the same B200 kernels
 }
 
 // ---- The column pipeline as separate stages (mul.hpp:32-67, mul.cpp:12-90), each run on

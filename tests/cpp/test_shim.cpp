@@ -40,6 +40,16 @@ const char* g_case = "";
         }                                 \
         CHECK(thrown_ && #expr);          \
     } while (0)
+#define CHECK_NOTHROW(expr)               \
+    do {                                  \
+        bool ok_ = true;                  \
+        try {                             \
+            (void)(expr);                 \
+        } catch (...) {                   \
+            ok_ = false;                  \
+        }                                 \
+        CHECK(ok_ && #expr);              \
+    } while (0)
 
 constexpr limb_t kMax = ~limb_t(0);
 
@@ -76,7 +86,7 @@ Limbs oracle_mul_padded(const Limbs& a, const Limbs& b) {
     dotor_mul(r.data(), a.data(), a.size(), b.data(), b.size());
     return r;
 }
-bool eq(const Limbs& a, const Limbs& b) {
+bool oracle_eq(const Limbs& a, const Limbs& b) {
     return dotor_compare(a.data(), a.size(), b.data(), b.size()) == 0;
 }
 
@@ -221,7 +231,7 @@ int main() {
             wide_b.resize(wide.size(), 0);
             const WordsResult back = dot_sub_words(wide, wide_b);
             CHECK(back.flag == 0);
-            CHECK(eq(back.limbs, a));
+            CHECK(oracle_eq(back.limbs, a));
         }
     });
     run("unequal lengths are padded like the oracle with an equal pad", [] {  // 201-217
@@ -355,9 +365,9 @@ int main() {
             CHECK(dot_mul_words(a, b) == dot_mul_words(b, a));
             Limbs one(m, 0);
             one[0] = 1;
-            CHECK(eq(dot_mul_words(a, one), a));
+            CHECK(oracle_eq(dot_mul_words(a, one), a));
             const Limbs z = dot_mul_words(a, Limbs(m, 0));
-            CHECK(eq(z, Limbs{}));
+            CHECK(oracle_eq(z, Limbs{}));
         }
     });
     run("product distributes over addition", [] {  // 391-411
@@ -374,7 +384,7 @@ int main() {
             WordsResult r = dot_add_words(dot_mul_words(a, b), dot_mul_words(a, c));
             Limbs rhs = r.limbs;
             rhs.push_back(r.flag);
-            CHECK(eq(lhs, rhs));
+            CHECK(oracle_eq(lhs, rhs));
         }
     });
     run("mul argument validation", [] {  // test_mul.cpp:97-101
@@ -441,6 +451,29 @@ int main() {
             Limbs pa(a.begin() + p * m, a.begin() + (p + 1) * m), pb(b.begin() + p * m, b.begin() + (p + 1) * m);
             const WordsResult w = oracle_sub(pa, pb);
             CHECK(Limbs(out.begin() + p * m, out.begin() + (p + 1) * m) == w.limbs && fl[p] == w.flag);
+        }
+    });
+    run("value helpers, radix checks and width names (limbs.hpp:51-89, addsub.hpp:39-44)", [] {
+        // test_limbs.cpp:149-153, test_addsub.cpp:369-370, test_mul.cpp:387
+        CHECK_NOTHROW(check_limbs(Limbs{~limb_t(0)}, kSaturated));
+        CHECK_NOTHROW(check_limbs(Limbs{(limb_t(1) << 52) - 1}, kUnsaturated));
+        CHECK_THROWS_AS(check_limbs(Limbs{limb_t(1) << 52}, kUnsaturated), std::invalid_argument);
+        CHECK_THROWS_AS(check_radix(RadixConfig{32}), std::invalid_argument);
+        for (const Width w : {Width::scalar, Width::w2, Width::w4, Width::w8}) {
+            CHECK(width_from_string(to_string(w)) == w);
+            CHECK(dispatch_note(w) == "sm_100a");
+        }
+        CHECK_THROWS_AS(width_from_string("w16"), std::invalid_argument);
+        const Limbs x{5, 0, 7, 0, 0};
+        CHECK(sig_limbs(x) == 3 && normalized(x) == (Limbs{5, 0, 7}));
+        CHECK(is_zero(Limbs{0, 0}) && is_zero(Limbs{}) && !is_zero(x));
+        CHECK(dot_b200::eq(x, Limbs{5, 0, 7}) && !dot_b200::eq(x, Limbs{5, 0, 8}));
+        CHECK(compare(std::span<const limb_t>(x), std::span<const limb_t>(Limbs{6})) == 1);
+        std::mt19937_64 rng(321);
+        for (std::size_t m : {1u, 16u, 64u}) {
+            Limbs a(m);
+            for (auto& v : a) v = rng();
+            CHECK(is_zero(dot_mul_words(a, Limbs(m, 0))));
         }
     });
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
