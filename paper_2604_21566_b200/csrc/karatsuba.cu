@@ -58,12 +58,24 @@ constexpr int kGrp = DOTG_KARA_GRP;
 
 // Children of pair p, parent read as 2h limbs with zero padding above its m limbs:
 //   lo = A[0:h], hi = A[h:2h], df = |hi - lo|, sign = (hi < lo).
-__global__ void __launch_bounds__(kKaraWarps * 32) k_kara_split_w(const uint64_t* __restrict__ A, size_t m,
-                                                                  size_t h, size_t count, uint64_t* lo,
-                                                                  uint64_t* hi, uint64_t* df, uint32_t* sign) {
+// Both operands of a level in one launch: blockIdx.y picks the operand (its own output set).
+struct KaraSplitArgs {
+    const uint64_t* A;
+    uint64_t *lo, *hi, *df;
+    uint32_t* sign;
+};
+__global__ void __launch_bounds__(kKaraWarps * 32) k_kara_split_w(const __grid_constant__ KaraSplitArgs x0,
+                                                                  const __grid_constant__ KaraSplitArgs x1, size_t m,
+                                                                  size_t h, size_t count) {
     const int lane = threadIdx.x & 31;
     const size_t p = size_t(blockIdx.x) * kKaraWarps + (threadIdx.x >> 5);
     if (p >= count) return;
+    const KaraSplitArgs& xa = blockIdx.y == 0 ? x0 : x1;
+    const uint64_t* __restrict__ A = xa.A;
+    uint64_t* lo = xa.lo;
+    uint64_t* hi = xa.hi;
+    uint64_t* df = xa.df;
+    uint32_t* sign = xa.sign;
     const uint64_t* a = A + p * m;
     auto limb = [&](size_t i) -> uint64_t { return i < m ? __ldg(a + i) : 0ull; };
     uint64_t* plo = lo + p * h;
@@ -320,11 +332,20 @@ cudaError_t combine_wide(const uint64_t* P, size_t h, size_t count, const uint32
     return e;
 }
 
-cudaError_t kara_split(const uint64_t* A, size_t m, size_t h, size_t count, uint64_t* lo, uint64_t* hi,
-                       uint64_t* df, uint32_t* sign, cudaStream_t st) {
-    if (kara_wide(h, count)) return split_wide(A, m, h, count, lo, hi, df, sign, st);
-    const unsigned grid = unsigned((count + kKaraWarps - 1) / kKaraWarps);
-    k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(A, m, h, count, lo, hi, df, sign);
+// Children of both operands of a level: [lo; hi; |hi - lo|] of A into nA (signs sa), of B
+// into nB (signs sb). The warp kernel takes both in one launch (the level's pairs are
+// latency-bound warps: twice the warps in flight at once).
+cudaError_t kara_split2(const uint64_t* A, const uint64_t* B, size_t m, size_t h, size_t count, uint64_t* nA,
+                        uint64_t* nB, uint32_t* sa, uint32_t* sb, cudaStream_t st) {
+    if (kara_wide(h, count)) {
+        cudaError_t e = split_wide(A, m, h, count, nA, nA + count * h, nA + 2 * count * h, sa, st);
+        if (e == cudaSuccess) e = split_wide(B, m, h, count, nB, nB + count * h, nB + 2 * count * h, sb, st);
+        return e;
+    }
+    const KaraSplitArgs xa{A, nA, nA + count * h, nA + 2 * count * h, sa};
+    const KaraSplitArgs xb{B, nB, nB + count * h, nB + 2 * count * h, sb};
+    const dim3 grid(unsigned((count + kKaraWarps - 1) / kKaraWarps), 2);
+    k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(xa, xb, m, h, count);
     count_launch();
     return cudaGetLastError();
 }
@@ -409,8 +430,7 @@ cudaError_t run_karatsuba_bf(uint64_t* out, const uint64_t* a, const uint64_t* b
             cleanup();
             return cudaErrorMemoryAllocation;
         }
-        cudaError_t es = kara_split(A, L.m, h, count, nA, nA + count * h, nA + 2 * count * h, L.sa, st);
-        if (es == cudaSuccess) es = kara_split(B, L.m, h, count, nB, nB + count * h, nB + 2 * count * h, L.sb, st);
+        cudaError_t es = kara_split2(A, B, L.m, h, count, nA, nB, L.sa, L.sb, st);
         if (d > d0) {
             release(A);
             release(B);
@@ -472,8 +492,7 @@ cudaError_t run_karatsuba_at(uint64_t* out, const uint64_t* a, const uint64_t* b
     if (e == cudaSuccess) e = cudaMallocAsync(&sb, batch * 4 < 256 ? 256 : batch * 4, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&P, 3 * batch * 2 * h * 8, st);
     if (e == cudaSuccess) {
-        e = kara_split(a, m, h, batch, nA, nA + batch * h, nA + 2 * batch * h, sa, st);
-        if (e == cudaSuccess) e = kara_split(b, m, h, batch, nB, nB + batch * h, nB + 2 * batch * h, sb, st);
+        e = kara_split2(a, b, m, h, batch, nA, nB, sa, sb, st);
         // the next level's plan entry describes a child of h limbs (pm[d0 + 1] == h)
         for (int k = 0; k < 3 && e == cudaSuccess; ++k)
             e = run_karatsuba_at(P + size_t(k) * batch * 2 * h, nA + size_t(k) * batch * h,
