@@ -186,6 +186,91 @@ __global__ void __launch_bounds__(kKaraWarps * 32) k_kara_combine_w(const uint64
     }
 }
 
+// CTA-per-pair combine for levels with few pairs (a warp per pair leaves most SMs idle
+// and walks 3h limbs serially): the same three chains, one after the other over the whole
+// CTA, each a segmented add - warp w streams its share of the 32-limb chunks resolved with
+// carry-in 0 and stores them, the warps' (G, P) meet in shared memory behind one barrier,
+// and a warp whose carry-in is 1 rewrites its segment's carry-dependent prefix (the
+// propagating limbs up to the first non-propagating one, which takes +-1; with random
+// limbs one chunk). T = P0 + P1 goes to scratch, M = T -+ PD in place, then R[h + j] =
+// base + M into the output.
+constexpr int kComboWarps = 16;
+// x[j] = j < na ? xa[j] : (j - na < nb ? xb[j - na] : 0)
+__device__ __forceinline__ uint64_t cat_limb(const uint64_t* xa, size_t na, const uint64_t* xb, size_t nb, size_t j) {
+    if (j < na) return xa[j];
+    return j - na < nb ? xb[j - na] : 0ull;
+}
+__device__ void cta_chain(bool sub, uint64_t* d, const uint64_t* xa, size_t na, const uint64_t* xb, size_t nb,
+                          const uint64_t* y, size_t ny, size_t n, uint32_t* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const uint64_t prop = sub ? 0ull : ~0ull;  // a limb that passes a carry / borrow on
+    const size_t nch = (n + 31) / 32, cpw = (nch + W - 1) / W;
+    const size_t c0 = size_t(w) * cpw < nch ? size_t(w) * cpw : nch;
+    const size_t c1 = c0 + cpw < nch ? c0 + cpw : nch;
+    uint32_t cin = 0, allp = 1;
+    for (size_t cb = c0; cb < c1; cb += kGrp) {
+        uint64_t xv[kGrp], yv[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            const size_t j = (cb + u) * 32 + lane;
+            const bool ok = cb + u < c1 && j < n;
+            xv[u] = ok ? cat_limb(xa, na, xb, nb, j) : 0ull;
+            yv[u] = ok && j < ny ? y[j] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+            if (cb + u >= c1) break;
+            const size_t j = (cb + u) * 32 + lane;
+            const bool ok = j < n;
+            const uint64_t sv = sub ? xv[u] - yv[u] : xv[u] + yv[u];
+            const uint32_t g = ok && (sub ? xv[u] < yv[u] : sv < xv[u]), pp = ok && sv == prop;
+            const uint32_t ci = chunk_carry(g, pp, cin, lane);
+            const uint64_t r = sub ? sv - ci : sv + ci;
+            if (ok) d[j] = r;
+            allp &= __ballot_sync(0xffffffffu, ok && r != prop) == 0u;
+        }
+    }
+    if (lane == 0) {
+        sh[w] = c0 < c1 ? cin : 0u;
+        sh[32 + w] = c0 < c1 ? allp : 1u;
+    }
+    __syncthreads();
+    uint32_t c = 0;  // carry into this warp's segment
+    for (int i = 0; i < w; ++i) c = sh[i] | (sh[32 + i] & c);
+    if (c != 0u) {
+        for (size_t cb = c0; cb < c1; ++cb) {
+            const size_t j = cb * 32 + lane;
+            const bool ok = j < n;
+            const uint64_t r = ok ? d[j] : prop;
+            const uint32_t np = __ballot_sync(0xffffffffu, r != prop);
+            const int q = np ? __ffs(np) - 1 : 32;
+            if (ok && lane < q) d[j] = ~prop;  // the propagating limbs flip
+            if (lane == q) d[j] = sub ? r - 1 : r + 1;
+            if (np) break;
+        }
+    }
+    __syncthreads();  // results visible to the next chain, shared words reusable
+}
+__global__ void __launch_bounds__(kComboWarps * 32) k_kara_combine_cta(const uint64_t* __restrict__ P, size_t h,
+                                                                       size_t count, const uint32_t* sa,
+                                                                       const uint32_t* sb, uint64_t* out, size_t m,
+                                                                       uint64_t* scratch) {
+    __shared__ uint32_t sh[64];
+    const size_t p = blockIdx.x;
+    const size_t n2 = 2 * h, n3 = 3 * h, n_out = 2 * m;
+    const uint64_t* p0 = P + p * n2;
+    const uint64_t* p1 = P + (count + p) * n2;
+    const uint64_t* pd = P + (2 * count + p) * n2;
+    uint64_t* T = scratch + p * n3;
+    uint64_t* o = out + p * n_out;
+    const bool minus = sa[p] == sb[p];  // same-sign differences: mid = P0 + P1 - PD
+    for (size_t k = threadIdx.x; k < h && k < n_out; k += blockDim.x) o[k] = p0[k];
+    cta_chain(false, T, p0, n2, nullptr, 0, p1, n2, n3, sh);  // T = P0 + P1
+    cta_chain(minus, T, T, n3, nullptr, 0, pd, n2, n3, sh);   // M = T -+ PD (>= 0)
+    if (n_out > h)                                            // R[h + j] = (P0[h:2h) ++ P1) + M
+        cta_chain(false, o + h, p0 + h, h, p1, n2, T, n3, n3 < n_out - h ? n3 : n_out - h, sh);
+}
+
 // dst[r][0:nd) = src[r][0:ns) zero-extended or truncated: one thread per destination
 // limb over the flat [rows][nd] array (coalesced stores; the row index comes from a 32-bit
 // division when the array is small enough, which covers every batch that fits in HBM
@@ -350,9 +435,26 @@ cudaError_t kara_split2(const uint64_t* A, const uint64_t* B, size_t m, size_t h
     return cudaGetLastError();
 }
 
+#ifndef DOTG_KARA_CTA_PAIRS
+#define DOTG_KARA_CTA_PAIRS 512  // below this many pairs a level's combine takes a CTA per pair
+#endif
 cudaError_t kara_combine(const uint64_t* P, size_t h, size_t count, const uint32_t* sa, const uint32_t* sb,
                          uint64_t* out, size_t m, cudaStream_t st) {
     if (kara_wide(h, count)) return combine_wide(P, h, count, sa, sb, out, m, st);
+    static const size_t cta_pairs = [] {
+        const char* e = std::getenv("DOTG_KARA_CTA_PAIRS");  // A/B knob
+        return e ? size_t(std::atoll(e)) : size_t(DOTG_KARA_CTA_PAIRS);
+    }();
+    if (count < cta_pairs && h >= 64) {
+        uint64_t* T = nullptr;
+        cudaError_t e = cudaMallocAsync(&T, count * 3 * h * 8, st);
+        if (e != cudaSuccess) return e;
+        k_kara_combine_cta<<<unsigned(count), kComboWarps * 32, 0, st>>>(P, h, count, sa, sb, out, m, T);
+        count_launch();
+        e = cudaGetLastError();
+        cudaError_t e2 = cudaFreeAsync(T, st);
+        return e != cudaSuccess ? e : e2;
+    }
     k_kara_combine_w<<<unsigned((count + kKaraWarps - 1) / kKaraWarps), kKaraWarps * 32, 0, st>>>(P, h, count, sa,
                                                                                                    sb, out, m);
     count_launch();

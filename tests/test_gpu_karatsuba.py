@@ -106,3 +106,43 @@ def test_padded_mul_batch_route(cuda, oracle, m):
         b[0] = MAX
         got = dg.mul_batch(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
         assert np.array_equal(got.cpu().numpy().view(np.uint64), oracle.mul_batch(a, b)), m
+
+
+_COMBINE_CHILD = r'''
+import sys
+sys.path.insert(0, ROOT + "/tests")
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+import paper_2604_21566_b200 as dg
+from helpers import MAX, Oracle, spiky, uniform
+orc = Oracle()
+bad = []
+for m, n in ((256, 7), (512, 5), (1024, 3), (2000, 2)):
+    rng = np.random.default_rng(4400 + m)
+    a, b = spiky(rng, (n, m)), uniform(rng, (n, m))
+    a[0] = MAX
+    b[0] = MAX
+    a[1, m // 2:2 * (m // 2)] = a[1, :m // 2]
+    got = dg.mul_batch(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
+    if not np.array_equal(got.cpu().numpy().view(np.uint64), orc.mul_batch(a, b)):
+        bad.append(m)
+print("BAD", bad)
+'''
+
+
+@pytest.mark.parametrize("cta_pairs", ["0", "1000000"])
+def test_combine_kernels_forced(cuda, cta_pairs):
+    """Both Karatsuba combine kernels - a warp per pair (DOTG_KARA_CTA_PAIRS=0) and a CTA per
+    pair with segmented chains (every level below 10^6 pairs) - exact on all-ones rows
+    (longest carry runs), equal halves and random rows, m up to 2000."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _COMBINE_CHILD.replace("ROOT", repr(root))],
+                       env={**os.environ, "DOTG_KARA_CTA_PAIRS": cta_pairs}, capture_output=True, text=True,
+                       cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-500:]
