@@ -271,6 +271,44 @@ __global__ void __launch_bounds__(kComboWarps * 32) k_kara_combine_cta(const uin
         cta_chain(false, o + h, p0 + h, h, p1, n2, T, n3, n3 < n_out - h ? n3 : n_out - h, sh);
 }
 
+// CTA-per-pair split for the same few-pair levels: the halves copied out and the highest
+// differing limb found by every warp over its share (one barrier), then |hi - lo| as one
+// segmented chain (larger minus smaller). blockIdx.y picks the operand as in the warp kernel.
+__global__ void __launch_bounds__(kComboWarps * 32) k_kara_split_cta(const __grid_constant__ KaraSplitArgs x0,
+                                                                     const __grid_constant__ KaraSplitArgs x1,
+                                                                     size_t m, size_t h, size_t count) {
+    __shared__ uint32_t sh[64];
+    __shared__ unsigned top;
+    const KaraSplitArgs& xa = blockIdx.y == 0 ? x0 : x1;
+    const size_t p = blockIdx.x;
+    const uint64_t* a = xa.A + p * m;
+    uint64_t* plo = xa.lo + p * h;
+    uint64_t* phi = xa.hi + p * h;
+    if (threadIdx.x == 0) top = 0;
+    __syncthreads();
+    unsigned mine = 0;  // 1 + highest index where the halves differ, this thread's limbs
+    for (size_t i = threadIdx.x; i < h; i += blockDim.x) {
+        const uint64_t y = a[i], x = h + i < m ? a[h + i] : 0ull;
+        plo[i] = y;
+        phi[i] = x;
+        if (x != y) mine = unsigned(i) + 1;
+    }
+    mine = __reduce_max_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicMax(&top, mine);
+    __syncthreads();
+    bool neg = false;
+    if (top != 0) {
+        const size_t i = top - 1;
+        neg = (h + i < m ? a[h + i] : 0ull) < a[i];
+    }
+    const size_t nh = m > h ? m - h : 0;  // limbs of the upper half actually stored
+    if (neg)
+        cta_chain(true, xa.df + p * h, a, h, nullptr, 0, a + h, nh, h, sh);  // lo - hi
+    else
+        cta_chain(true, xa.df + p * h, a + h, nh, nullptr, 0, a, h, h, sh);  // hi - lo
+    if (threadIdx.x == 0) xa.sign[p] = neg ? 1u : 0u;
+}
+
 // dst[r][0:nd) = src[r][0:ns) zero-extended or truncated: one thread per destination
 // limb over the flat [rows][nd] array (coalesced stores; the row index comes from a 32-bit
 // division when the array is small enough, which covers every batch that fits in HBM
@@ -417,6 +455,17 @@ cudaError_t combine_wide(const uint64_t* P, size_t h, size_t count, const uint32
     return e;
 }
 
+#ifndef DOTG_KARA_CTA_PAIRS
+#define DOTG_KARA_CTA_PAIRS 512  // below this many pairs a level's split / combine take a CTA per pair
+#endif
+size_t kara_cta_pairs() {
+    static const size_t v = [] {
+        const char* e = std::getenv("DOTG_KARA_CTA_PAIRS");  // A/B knob
+        return e ? size_t(std::atoll(e)) : size_t(DOTG_KARA_CTA_PAIRS);
+    }();
+    return v;
+}
+
 // Children of both operands of a level: [lo; hi; |hi - lo|] of A into nA (signs sa), of B
 // into nB (signs sb). The warp kernel takes both in one launch (the level's pairs are
 // latency-bound warps: twice the warps in flight at once).
@@ -429,23 +478,20 @@ cudaError_t kara_split2(const uint64_t* A, const uint64_t* B, size_t m, size_t h
     }
     const KaraSplitArgs xa{A, nA, nA + count * h, nA + 2 * count * h, sa};
     const KaraSplitArgs xb{B, nB, nB + count * h, nB + 2 * count * h, sb};
-    const dim3 grid(unsigned((count + kKaraWarps - 1) / kKaraWarps), 2);
-    k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(xa, xb, m, h, count);
+    if (count < kara_cta_pairs() && h >= 64) {
+        k_kara_split_cta<<<dim3(unsigned(count), 2), kComboWarps * 32, 0, st>>>(xa, xb, m, h, count);
+    } else {
+        const dim3 grid(unsigned((count + kKaraWarps - 1) / kKaraWarps), 2);
+        k_kara_split_w<<<grid, kKaraWarps * 32, 0, st>>>(xa, xb, m, h, count);
+    }
     count_launch();
     return cudaGetLastError();
 }
 
-#ifndef DOTG_KARA_CTA_PAIRS
-#define DOTG_KARA_CTA_PAIRS 512  // below this many pairs a level's combine takes a CTA per pair
-#endif
 cudaError_t kara_combine(const uint64_t* P, size_t h, size_t count, const uint32_t* sa, const uint32_t* sb,
                          uint64_t* out, size_t m, cudaStream_t st) {
     if (kara_wide(h, count)) return combine_wide(P, h, count, sa, sb, out, m, st);
-    static const size_t cta_pairs = [] {
-        const char* e = std::getenv("DOTG_KARA_CTA_PAIRS");  // A/B knob
-        return e ? size_t(std::atoll(e)) : size_t(DOTG_KARA_CTA_PAIRS);
-    }();
-    if (count < cta_pairs && h >= 64) {
+    if (count < kara_cta_pairs() && h >= 64) {
         uint64_t* T = nullptr;
         cudaError_t e = cudaMallocAsync(&T, count * 3 * h * 8, st);
         if (e != cudaSuccess) return e;

@@ -133,7 +133,7 @@ print("BAD", bad)
 
 @pytest.mark.parametrize("cta_pairs", ["0", "1000000"])
 def test_combine_kernels_forced(cuda, cta_pairs):
-    """Both Karatsuba combine kernels - a warp per pair (DOTG_KARA_CTA_PAIRS=0) and a CTA per
+    """Both Karatsuba split / combine kernel pairs - a warp per pair (DOTG_KARA_CTA_PAIRS=0) and a CTA per
     pair with segmented chains (every level below 10^6 pairs) - exact on all-ones rows
     (longest carry runs), equal halves and random rows, m up to 2000."""
     import os
