@@ -1013,9 +1013,10 @@ int il_route(size_t m, size_t batch) {
     if (mode == 2) return 0;
     if (mode == 3) return m >= 16 ? 3 : 0;
     if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
-    if (mode == 5) return m >= 2 ? 5 : 0;
+    if (mode == 5) return m >= 2 && (batch + 7) / 8 <= size_t(0x7fffffff) ? 5 : 0;
     if (m <= size_t(kSL)) return nseg_fits(m, batch) ? 4 : 0;  // one segment: pass 1 alone
     if (m < 48) return 0;                                      // thread per pair
+    if ((batch + 7) / 8 > size_t(0x7fffffff)) return 0;        // ilf's grid has a CTA per strip
     if (m <= 2048 || batch >= 4096) return 5;                  // streaming pass + in-CTA fix-up
     return nseg_fits(m, batch) ? 4 : 5;  // a few very long numbers: (strip, segment) warps fill the GPU
 }
