@@ -996,10 +996,11 @@ cudaError_t run_interleaved_2pass(uint64_t* out, const uint64_t* a, const uint64
 //   re-read CTAs (il2)        0.77 / 0.73 / 0.74 / 0.74 / 0.71 / 0.69 / 0.67 / 0.64
 //   two passes                0.82 / 0.56 / 0.64 / 0.71 / 0.69 / 0.60 / 0.48 / 0.35
 //   streaming + fix-up (ilf)     - / 0.84 / 0.83 / 0.82 / 0.80 / 0.80 / 0.77 / 0.72
-// Auto: up to 8 limbs the two-pass route's first pass alone (one segment); below 48 limbs
-// thread per pair; then k_addsub_ilf, except a few very long numbers (m > 2048 and fewer
-// than 4096 pairs), which take the two-pass route (its warps are (strip, segment) pairs,
-// so they still fill the GPU). DOTG_IL_MODE (A/B knob) forces 2 (thread per pair), 3
+// Auto: k_addsub_ilf up to 4 limbs (one warp per strip: add and sub 0.82 at m = 4, where
+// the two-pass route's first pass alone gave add 0.82 / sub 0.77), thread per pair below
+// 48 limbs (0.90 at m = 8), then k_addsub_ilf, except a few very long numbers (m > 2048
+// and fewer than 4096 pairs), which take the two-pass route (its warps are (strip,
+// segment) pairs, so they still fill the GPU). DOTG_IL_MODE (A/B knob) forces 2 (thread per pair), 3
 // (il2), 4 (two passes) or 5 (ilf) where they apply.
 int il_mode() {
     static const int v = [] {
@@ -1014,9 +1015,9 @@ int il_route(size_t m, size_t batch) {
     if (mode == 3) return m >= 16 ? 3 : 0;
     if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
     if (mode == 5) return m >= 2 && (batch + 7) / 8 <= size_t(0x7fffffff) ? 5 : 0;
-    if (m <= size_t(kSL)) return nseg_fits(m, batch) ? 4 : 0;  // one segment: pass 1 alone
-    if (m < 48) return 0;                                      // thread per pair
     if ((batch + 7) / 8 > size_t(0x7fffffff)) return 0;        // ilf's grid has a CTA per strip
+    if (m <= 4) return 5;                                      // ilf, one warp per strip
+    if (m < 48) return 0;                                      // thread per pair
     if (m <= 2048 || batch >= 4096) return 5;                  // streaming pass + in-CTA fix-up
     return nseg_fits(m, batch) ? 4 : 5;  // a few very long numbers: (strip, segment) warps fill the GPU
 }
