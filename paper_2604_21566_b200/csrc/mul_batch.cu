@@ -836,7 +836,12 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 // i + j + 1). A column of M low parts plus M high parts is < 2M * 2^52, so plain 64-bit
 // column sums are exact; one radix-2^52 carry pass (mul.cpp:70-90 at k = 52). Rows are
 // zero-extended to M limbs (zero limbs add nothing), only 2m limbs are stored.
-template <int M>
+// FP = true: the 52 x 52-bit products on the FP64 pipe, exactly (the fma.rz / fma.rn pair
+// of k_mul_kara16h below: bits(h) = bits(2^104) + floor(xy / 2^52), bits(l) = bits(2^52) +
+// (xy mod 2^52)), the raw bit patterns summed per column and the biases removed once -
+// three FP64 operations per product instead of a 64-bit multiply and multiply-high on the
+// IMAD pipe.
+template <int M, bool FP>
 __global__ void __launch_bounds__(128) k_mul52_regs(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                                                     const uint64_t* __restrict__ b, int m, size_t batch) {
     // the CTA's 128 rows of a and b (and later its 128 products) are contiguous: staged
@@ -848,9 +853,25 @@ __global__ void __launch_bounds__(128) k_mul52_regs(uint64_t* __restrict__ out, 
     const size_t p0 = size_t(blockIdx.x) * 128;
     const size_t np = batch - p0 < 128 ? batch - p0 : 128;
     const size_t nin = np * size_t(m), nout = 2 * nin;
-    for (size_t i = threadIdx.x; i < nin; i += 128) {
-        sa[i] = __ldcs(a + p0 * size_t(m) + i);
-        sb[i] = __ldcs(b + p0 * size_t(m) + i);
+    if (np == 128 && m == M) {
+        // a full CTA: every load of the tile in flight at once (2M per thread), then the
+        // shared-memory stores (the plain loop waits for each pair of loads)
+        uint64_t va[M], vb[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            va[k] = __ldcs(a + p0 * M + threadIdx.x + 128 * k);
+            vb[k] = __ldcs(b + p0 * M + threadIdx.x + 128 * k);
+        }
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            sa[threadIdx.x + 128 * k] = va[k];
+            sb[threadIdx.x + 128 * k] = vb[k];
+        }
+    } else {
+        for (size_t i = threadIdx.x; i < nin; i += 128) {
+            sa[i] = __ldcs(a + p0 * size_t(m) + i);
+            sb[i] = __ldcs(b + p0 * size_t(m) + i);
+        }
     }
     __syncthreads();
     constexpr uint64_t kMask = (uint64_t(1) << 52) - 1;
@@ -865,14 +886,42 @@ __global__ void __launch_bounds__(128) k_mul52_regs(uint64_t* __restrict__ out, 
         uint64_t col[2 * M];
 #pragma unroll
         for (int c = 0; c < 2 * M; ++c) col[c] = 0;
+        if constexpr (FP) {
+            const double C104 = 20282409603651670423947251286016.0;                          // 2^104
+            const double C104p52 = 20282409603651670423947251286016.0 + 4503599627370496.0;  // 2^104 + 2^52
+            double xd[M], yd[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i)
+            for (int i = 0; i < M; ++i) xd[i] = double(x[i]), yd[i] = double(y[i]);  // exact below 2^52
 #pragma unroll
-            for (int j = 0; j < M; ++j) {
-                const uint64_t lo = x[i] * y[j], hi = __umul64hi(x[i], y[j]);
-                col[i + j] += lo & kMask;
-                col[i + j + 1] += (hi << 12) | (lo >> 52);  // floor(product / 2^52) < 2^52
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    double h, cc, l;
+                    asm("fma.rz.f64 %0, %1, %2, %3;" : "=d"(h) : "d"(xd[i]), "d"(yd[j]), "d"(C104));
+                    asm("sub.rn.f64 %0, %1, %2;" : "=d"(cc) : "d"(C104p52), "d"(h));
+                    asm("fma.rn.f64 %0, %1, %2, %3;" : "=d"(l) : "d"(xd[i]), "d"(yd[j]), "d"(cc));
+                    col[i + j] += uint64_t(__double_as_longlong(l));
+                    col[i + j + 1] += uint64_t(__double_as_longlong(h));
+                }
+            // biases: column c holds one bits(2^52) per pair with i + j = c and one
+            // bits(2^104) per pair with i + j = c - 1 (mod 2^64; the true sums are < 2M 2^52)
+            constexpr uint64_t kB52 = 0x4330000000000000ull, kB104 = 0x4670000000000000ull;
+#pragma unroll
+            for (int c = 0; c < 2 * M; ++c) {
+                const int nlo = c < M ? c + 1 : (c <= 2 * M - 2 ? 2 * M - 1 - c : 0);
+                const int nhi = c == 0 ? 0 : (c - 1 < M ? c : 2 * M - c);
+                col[c] -= uint64_t(nlo) * kB52 + uint64_t(nhi) * kB104;
             }
+        } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+                for (int j = 0; j < M; ++j) {
+                    const uint64_t lo = x[i] * y[j], hi = __umul64hi(x[i], y[j]);
+                    col[i + j] += lo & kMask;
+                    col[i + j + 1] += (hi << 12) | (lo >> 52);  // floor(product / 2^52) < 2^52
+                }
+        }
         uint64_t carry = 0;
 #pragma unroll
         for (int c = 0; c < 2 * M; ++c) {
@@ -916,11 +965,22 @@ cudaError_t launch_mul52_batch(uint64_t* out, const uint64_t* a, const uint64_t*
                                cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
     const unsigned grid = unsigned((batch + 127) / 128);
-    if (m <= 4) k_mul52_regs<4><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
-    else if (m <= 5) k_mul52_regs<5><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
-    else if (m <= 8) k_mul52_regs<8><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
-    else if (m <= 16) k_mul52_regs<16><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
-    else k_mul52<<<grid, 128, 0, st>>>(out, a, b, m, batch);
+    static const bool fp = [] {  // A/B knob: 52 x 52-bit products on the FP64 pipe (1) or the IMAD pipe (0)
+        const char* e = std::getenv("DOTG_MUL52_FP");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (m > 16) k_mul52<<<grid, 128, 0, st>>>(out, a, b, m, batch);
+    else if (fp) {
+        if (m <= 4) k_mul52_regs<4, true><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else if (m <= 5) k_mul52_regs<5, true><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else if (m <= 8) k_mul52_regs<8, true><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else k_mul52_regs<16, true><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    } else {
+        if (m <= 4) k_mul52_regs<4, false><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else if (m <= 5) k_mul52_regs<5, false><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else if (m <= 8) k_mul52_regs<8, false><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+        else k_mul52_regs<16, false><<<grid, 128, 0, st>>>(out, a, b, int(m), batch);
+    }
     count_launch();
     return cudaGetLastError();
 }

@@ -65,3 +65,58 @@ def test_device_52bit_products(cuda, golden):
     ones = np.full(4, 2**64 - 1, np.uint64)
     v = sum(int(x) << (64 * k) for k, x in enumerate(dg.api.dot_mul_4x4(ones, ones)))
     assert v == ((1 << 256) - 1) ** 2
+
+
+_MUL52_CHILD = r'''
+import ctypes, sys
+sys.path.insert(0, ROOT + "/tests")
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+import paper_2604_21566_b200 as dg
+from helpers import Oracle
+orc = Oracle()
+L = dg.lib()
+M52 = (1 << 52) - 1
+bad = []
+for m in (1, 2, 3, 4, 5, 6, 8, 11, 16, 17):
+    for batch in (1, 127, 128, 300):
+        rng = np.random.default_rng(5200 + 31 * m + batch)
+        a = rng.integers(0, 1 << 52, size=(batch, m), dtype=np.uint64)
+        b = rng.integers(0, 1 << 52, size=(batch, m), dtype=np.uint64)
+        a[0] = M52                     # every product and every column at its maximum
+        b[0] = M52
+        if batch > 2:
+            a[1] = 0
+            b[2, : m // 2] = M52
+        da = torch.from_numpy(a.view(np.int64)).cuda()
+        db = torch.from_numpy(b.view(np.int64)).cuda()
+        do = torch.empty((batch, 2 * m), dtype=torch.int64, device="cuda")
+        rc = L.dotg_mul52_batch(do.data_ptr(), da.data_ptr(), db.data_ptr(), m, batch, None)
+        assert rc == 0, rc
+        got = do.cpu().numpy().view(np.uint64)
+        for i in range(batch):
+            if not np.array_equal(got[i], orc.mul_columns52(a[i], b[i])):
+                bad.append((m, batch, i))
+                break
+print("BAD", bad)
+'''
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fp", ["1", "0"])
+def test_device_52bit_batch_both_pipes(cuda, fp):
+    """dotg_mul52_batch on the FP64 pipe (exact fma.rz / fma.rn products, the default) and
+    on the IMAD pipe (DOTG_MUL52_FP=0) against the oracle's radix-2^52 column product: all
+    limbs 2^52 - 1 (largest columns), zeros, half-maximal rows, partial and full CTAs,
+    m = 1 ... 17 (17: the generic kernel)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _MUL52_CHILD.replace("ROOT", repr(root))],
+                       env={**os.environ, "DOTG_MUL52_FP": fp}, capture_output=True, text=True, cwd=root,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-500:]
