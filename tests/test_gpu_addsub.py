@@ -63,8 +63,8 @@ def test_interleaved_two_pass(cuda, oracle, m, batch):
 @pytest.mark.parametrize("m,batch", [(128, 128), (200, 130), (256, 64), (256, 190), (129, 66), (257, 40),
                                      (300, 65), (384, 32), (512, 33), (513, 31), (777, 40), (1024, 33)])
 def test_interleaved_segmented(cuda, oracle, m, batch):
-    # 128 <= m <= 1024 take k_addsub_interleaved (8-limb segments up to m = 256, 16 up to
-    # 512, 32 up to 1024): ragged m the partial last segment, batch % 32 != 0 the partial CTA
+    # 128 <= m <= 1024 take k_addsub_ilf (row segments per warp, one CTA per strip of
+    # pairs): ragged m the partial last segment, batch % 32 != 0 the partial strip
     rng = np.random.default_rng(7000 + m + batch)
     for cat in CATEGORIES:
         for op in ("add", "sub"):
