@@ -822,7 +822,7 @@ def run_ours(args, rank, world, dist):
                 ref_ns = (time.perf_counter() - t0) / n1 * 1e9
             latency = {"m": m1, "dropin_host_span_us": host_us, "device_call_us": dev_us,
                        "reference_span_ns_incl_ctypes": ref_ns,
-                       "note": "one 4096-bit add per call: host span form (H2D, kernel, D2H, sync) and the "
+                       "note": "one 4096-bit add per call: host span form (operands through mapped pinned memory, one launch, one sync) and the "
                                "device-pointer C ABI back to back (launch-bound), vs the reference's span call "
                                "through ctypes on one core (~53 ns natively, profiles/r01_cpu_table.json). Single "
                                "small numbers belong on the CPU or in a batch / CUDA graph."}
