@@ -87,6 +87,13 @@ cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t*
 // Interleaved [m][batch] operands / product in place: even 16 < m <= 128.
 cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st);
+// Wide operands on the 5th-generation tensor core (mul_umma.cu): row-major, 16-byte
+// aligned rows, 256 <= m <= 4096, m % 16 == 0 (DOTG_MUL_UMMA=0 disables the route).
+bool mul_umma_supported(size_t m);
+cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                            cudaStream_t st);
+// Karatsuba leaf size above the tcgen05 range (DOTG_UMMA_LEAF, default 2048).
+size_t mul_umma_leaf();
 // Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
 extern std::atomic<int> g_mul_route;
 

@@ -1,0 +1,402 @@
+// mul_umma.cu - batched column multiplication of WIDE operands on the 5th-generation
+// tensor core (tcgen05.mma kind::i8, accumulators in tensor memory).
+//
+// Same contract as every product kernel here (dot_mul_words, include/dot/mul.hpp:75-76,
+// src/mul.cpp:96-103: all column sums, one deferred carry pass, exactly 2m limbs), for
+// 256 <= m <= 4096 limbs (m % 16 == 0), and the leaves of the Karatsuba route above.
+//
+// Why tcgen05 here and mma.sync below 256 limbs: a UMMA with M = 128 reads its A tile
+// (4 KB) from shared memory for every instruction, so it only pays when N (the columns
+// sharing that tile) is large. One pair's column product offers N = number of a-chunks
+// of 128 bytes sharing a b-window - 16 for m = 128, 64 for m = 1024, 256 for m = 4096
+// (tools/umma_i8_probe.cu measured the small-N ceiling).
+//
+// Formulation (bytes; a, b of n = 8m bytes; x = i + j; S[x] = sum a[j] b[i]):
+//   j = 128 J + 32 p + (31 - k)        J a-chunk, p in 0..3 its 32-byte block, k the MMA K
+//   i = 128 s - 32 p + r + k - 31      s the b-window step, r in 0..127 the TMEM lane
+//   => x = 128 (s + J) + r             independent of p and k
+// MMA (s, p) over the D tile of output chunks [C0, C0 + NT):
+//   A[r][k] = b[128 s - 32 p + r + k - 31]              (Hankel window of b)
+//   B[k][c] = a[128 (C0 + c - s) + 32 p + 31 - k]       (a-block 4J + p, byte-reversed)
+//   D[r][c] += sum_k A[r][k] B[k][c]    -> D[r][c] = S[128 (C0 + c) + r], no redundancy:
+// every (i, j) byte pair is issued exactly once, into the one D entry of its column.
+// Only the columns c whose a-chunk exists are issued (N' = that range rounded out to 16,
+// zero-padded chunks), so a tile's MMAs are ~90-100 % useful.
+//
+// Shared-memory operands, K-major, no swizzle (core matrix = 8 rows x 16 bytes):
+//   * A: core matrix (g, kk) of MMA (s, p) is C_t with t = 16 s - 4 p + g + 2 kk, where
+//     C_t[rr][jj] = b[8 t + rr + jj - 31]. So the Hankel tiles of all (s, p) are windows
+//     of ONE array of core matrices (SBO 128 B, LBO 256 B): 16x the b bytes, built per
+//     block of s-steps into a 2-slot ring by funnel shifts from b staged in shared memory.
+//   * B: per (p, kk) an array of 16-byte rows indexed by J (reversed half-blocks), so
+//     shifting the a-chunk range by one (next s) is a 16-byte step of the start address
+//     (SBO 128 B, LBO = the array length).
+// Accumulation: s32 column sums < n * 255^2 < 2^31 for n <= 32 KB (m <= 4096).
+// Epilogue: tcgen05.ld (warp w holds lanes 32w..32w+31 = bytes of 4 limbs per chunk), a
+// 3-step shuffle fold of 8 byte columns per limb into lo64 + hi (< 2^25), lo to `out`,
+// hi to the next limb of a scratch row; one batched add (the add/sub kernel) then
+// resolves every inter-limb carry: product = LO + HI * 2^64.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "internal.h"
+
+namespace dotg {
+
+namespace {
+
+constexpr int kPadJ = 16;            // zero a-chunks on each side of the B arrays
+constexpr int kPadB = 160;           // zero bytes on each side of the staged b
+constexpr int kSB = 4;               // s-steps per ring slot
+constexpr int kTC = 16 * kSB + 16;   // core matrices per ring slot
+constexpr int kSlots = 3;            // ring slots
+constexpr int kWorkers = 128;        // builder / epilogue warps 0-3 (TMEM lane quarters)
+constexpr int kThreads = 160;        // + warp 4: the MMA issuer
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+// Shared-memory matrix descriptor: K-major, no swizzle, version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+// Instruction descriptor kind::i8: u8 x u8 -> s32, both K-major, M = 128.
+__device__ __forceinline__ uint32_t idesc_u8(uint32_t n) { return (2u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\nUMMA_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra UMMA_WAIT_%=;\n}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+struct UmmaGeom {
+    int na;      // a-chunks (128 bytes) per operand = m / 16
+    int nt;      // D tile width in chunks (TMEM columns)
+    int tiles;   // tiles per pair
+    int cols;    // TMEM columns allocated (power of two >= 32)
+    uint32_t la; // bytes of one B array
+    uint32_t off_ring, off_b, smem;
+};
+
+__host__ __device__ inline UmmaGeom umma_geom(int m) {
+    UmmaGeom g{};
+    g.na = m / 16;
+    g.nt = 2 * g.na < 256 ? (2 * g.na + 15) & ~15 : 256;
+    g.tiles = (2 * g.na + g.nt - 1) / g.nt;
+    g.cols = g.nt <= 32 ? 32 : (g.nt <= 64 ? 64 : (g.nt <= 128 ? 128 : 256));
+    g.la = uint32_t(g.na + 2 * kPadJ) * 16;
+    g.off_ring = 8 * g.la;
+    g.off_b = g.off_ring + kSlots * kTC * 128;
+    g.smem = g.off_b + uint32_t(8 * m + 2 * kPadB);
+    const uint32_t epi = uint32_t(12 * 16 * g.nt + 4 * 16 * 32 * 4);  // LO, HI, per-warp transpose
+    if (g.smem < epi) g.smem = epi;
+    return g;
+}
+
+__global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ out, uint64_t* __restrict__ carry_words,
+                                                     const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                                     int m) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots], done;
+    __shared__ uint32_t tbase_sh;
+    const UmmaGeom G = umma_geom(m);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t pair = blockIdx.x / unsigned(G.tiles);
+    const int C0 = int(blockIdx.x % unsigned(G.tiles)) * G.nt;
+    const int na = G.na, nb = G.na, n = 8 * m;
+    uint8_t* bh = sm;                       // 8 arrays [p][kk], (na + 2 kPadJ) rows of 16 B
+    uint8_t* ring = sm + G.off_ring;        // 2 slots x kTC core matrices
+    uint8_t* bs = sm + G.off_b;             // kPadB zeros | b | kPadB zeros
+    const uint4* ga = reinterpret_cast<const uint4*>(a + pair * size_t(m));
+    const uint4* gb = reinterpret_cast<const uint4*>(b + pair * size_t(m));
+
+    // a -> B arrays: 16-byte segment g of the operand is half (g & 1) of block 4J + p,
+    // J = g / 8, p = (g / 2) % 4; stored byte-reversed as row J of array (p, kk = 1 - half).
+    for (int g0 = tid; g0 < n / 16; g0 += 4 * kThreads) {  // n / 16 is a multiple of 128: 4 loads in flight
+        uint4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < n / 16 ? __ldg(ga + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int g = g0 + u * kThreads;
+            if (g >= n / 16) break;
+            const int J = g >> 3, p = (g >> 1) & 3, kk = 1 - (g & 1);
+            *reinterpret_cast<uint4*>(bh + (2 * p + kk) * G.la + (J + kPadJ) * 16) =
+                make_uint4(bswap32(w[u].w), bswap32(w[u].z), bswap32(w[u].y), bswap32(w[u].x));
+        }
+    }
+    for (int e = tid; e < 8 * 2 * kPadJ; e += kThreads) {  // zero chunks on both sides
+        const int arr = e / (2 * kPadJ), q = e % (2 * kPadJ);
+        const int row = q < kPadJ ? q : na + q;
+        *reinterpret_cast<uint4*>(bh + arr * G.la + row * 16) = make_uint4(0, 0, 0, 0);
+    }
+    for (int g0 = tid; g0 < n / 16; g0 += 4 * kThreads) {
+        uint4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < n / 16 ? __ldg(gb + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (g0 + u * kThreads < n / 16) reinterpret_cast<uint4*>(bs + kPadB)[g0 + u * kThreads] = w[u];
+    }
+    for (int e = tid; e < 2 * kPadB / 16; e += kThreads) {
+        const int off = e < kPadB / 16 ? e * 16 : kPadB + n + (e - kPadB / 16) * 16;
+        *reinterpret_cast<uint4*>(bs + off) = make_uint4(0, 0, 0, 0);
+    }
+    // barriers: full[q] (4 builder warps arrive), empty[q] (MMA commit), done (last commit)
+    if (tid == 0) {
+        for (int q = 0; q < kSlots; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(&full[q])) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[q])) : "memory");
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase_sh)),
+                     "r"(G.cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = tbase_sh;
+    if (warp < 4) {  // zero the accumulator tile (every MMA accumulates)
+        const uint32_t z = 0;
+        for (int c = 0; c < G.nt; c += 16)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                    tm + (uint32_t(warp * 32) << 16) + uint32_t(c)),
+                "r"(z)
+                : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+
+    const int nblocks = (nb + 1 + kSB - 1) / kSB;  // s = 0 .. nb in blocks of kSB steps
+    if (warp < 4) {
+        // builders: ring slot q % kSlots <- core matrices t = 16 s0 - 12 + (row / 8), row rr = row % 8
+        const uint32_t* bw = reinterpret_cast<const uint32_t*>(bs);
+        for (int q = 0; q < nblocks; ++q) {
+            const int slot = q % kSlots, s0 = q * kSB;
+            if (q >= kSlots) mbar_wait(smem_u32(&empty[slot]), uint32_t(q / kSlots - 1) & 1u);
+            uint8_t* rs = ring + slot * (kTC * 128);
+            const int t0 = 16 * s0 - 12;
+#pragma unroll 2
+            for (int row = tid; row < kTC * 8; row += kWorkers) {
+                const int o = 8 * (t0 + (row >> 3)) + (row & 7) - 31 + kPadB;  // byte offset in bs
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (o + 16 > kPadB && o < kPadB + n) {
+                    const int w0 = o >> 2, sh = (o & 3) * 8;
+                    const uint32_t x0 = bw[w0], x1 = bw[w0 + 1], x2 = bw[w0 + 2], x3 = bw[w0 + 3], x4 = bw[w0 + 4];
+                    v = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh),
+                                   __funnelshift_r(x2, x3, sh), __funnelshift_r(x3, x4, sh));
+                }
+                *reinterpret_cast<uint4*>(rs + row * 16) = v;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
+        }
+    } else if (lane == 0) {
+        // issuer: one thread, MMAs of a slot once its 4 builder warps arrived
+        for (int q = 0; q < nblocks; ++q) {
+            const int slot = q % kSlots, s0 = q * kSB;
+            mbar_wait(smem_u32(&full[slot]), uint32_t(q / kSlots) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint8_t* rs = ring + slot * (kTC * 128);
+            const int s1 = s0 + kSB < nb + 1 ? s0 + kSB : nb + 1;
+            for (int s = s0; s < s1; ++s) {
+                int lo = s - C0, hi = s - C0 + na;
+                if (lo < 0) lo = 0;
+                if (hi > G.nt) hi = G.nt;
+                if (hi <= lo) continue;
+                const int lo16 = lo & ~15, hi16 = (hi + 15) & ~15;
+                const uint32_t id = idesc_u8(uint32_t(hi16 - lo16));
+                const uint32_t dcol = tm + uint32_t(lo16);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const uint64_t ad = sdesc(smem_u32(rs + (16 * (s - s0) + 12 - 4 * p) * 128), 256, 128);
+                    const uint64_t bd = sdesc(smem_u32(bh + (2 * p) * G.la + (C0 + lo16 - s + kPadJ) * 16), G.la, 128);
+                    asm volatile(
+                        "{\n\t.reg .pred pa;\n\tsetp.ne.b32 pa, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pa;\n\t}" ::"r"(dcol),
+                        "l"(ad), "l"(bd), "r"(id), "r"(1u)
+                        : "memory");
+                }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(q == nblocks - 1 ? &done : &empty[slot]))
+                         : "memory");
+        }
+    }
+    mbar_wait(smem_u32(&done), 0u);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // Epilogue (all operand shared memory is free now).
+    // E1: per 16 columns, warp w's lanes hold byte 32w + lane of each output chunk; a
+    // per-warp transpose through shared memory gives each thread all 8 byte columns of
+    // one limb: V = sum_u S[u] 2^(8u) = lo + hi 2^64 (hi < 2^25), kept as LO / HI.
+    const int xend = 2 * na - C0 < G.nt ? 2 * na - C0 : G.nt;  // columns inside the product
+    const int xe16 = (xend + 15) & ~15;                         // + zero columns up to 16
+    const int nl = 16 * xe16;                                   // limbs resolved (multiple of 256)
+    uint64_t* LO = reinterpret_cast<uint64_t*>(sm);
+    uint32_t* HI = reinterpret_cast<uint32_t*>(sm + 8 * 16 * G.nt);
+    uint32_t* Tw = reinterpret_cast<uint32_t*>(sm + 12 * 16 * G.nt) + warp * (16 * 32);
+    for (int c0 = 0; c0 < (warp < 4 ? xe16 : 0); c0 += 16) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tm + (uint32_t(warp * 32) << 16) + uint32_t(c0)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) Tw[j * 32 + lane] = v[j];
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int task = lane + 32 * h, c = task >> 2, u = task & 3;
+            {
+                const uint4 q0 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u);
+                const uint4 q1 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u + 4);
+                const uint64_t x = uint64_t(q0.x) + (uint64_t(q0.y) << 8) + (uint64_t(q0.z) << 16) + (uint64_t(q0.w) << 24);
+                const uint64_t y = uint64_t(q1.x) + (uint64_t(q1.y) << 8) + (uint64_t(q1.z) << 16) + (uint64_t(q1.w) << 24);
+                const uint64_t lo = x + (y << 32);
+                const int L = 16 * (c0 + c) + 4 * warp + u;
+                LO[L] = lo;
+                HI[L] = uint32_t(y >> 32) + (lo < x ? 1u : 0u);
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
+    // add kernel's generate / propagate algebra. Warp w owns limbs [w nl/4, (w+1) nl/4) in
+    // rounds of 32 consecutive limbs (lane = limb, conflict-free): pass 1 folds the rounds
+    // into the warp's (carry-out, all-propagate), pass 2 applies the carries.
+    {
+        const int per_warp = nl / 4, rounds = per_warp / 32;  // nl = 16 * xe16 -> rounds >= 2
+        const int base = warp * per_warp;
+        __shared__ uint32_t wagg[4][2];
+        if (warp < 4) {
+            uint32_t Gw = 0, Pw = 1;
+            for (int r = 0; r < rounds; ++r) {
+                const int L = base + 32 * r + lane;
+                const uint64_t lo = LO[L];
+                const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
+                Gw = go | ((pp == 0xffffffffu) & Gw);
+                Pw &= pp == 0xffffffffu;
+            }
+            if (lane == 0) {
+                wagg[warp][0] = Gw;
+                wagg[warp][1] = Pw;
+            }
+        }
+        __syncthreads();
+        if (warp < 4) {
+            uint32_t c = 0;
+            for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
+            for (int r = 0; r < rounds; ++r) {
+                const int L = base + 32 * r + lane;
+                const uint64_t lo = LO[L];
+                const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
+                LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
+                c = uint32_t(y >> 32);
+            }
+            if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
+                carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
+        }
+    }
+    __syncthreads();
+    {
+        uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
+        for (int e = tid; e < 8 * xend; e += kThreads)
+            reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(G.cols) : "memory");
+}
+
+// Tiles after the first were resolved with carry-in 0: add each tile's carry word at the
+// next tile's first limb, propagating (one thread per pair; the additions commute).
+__global__ void k_umma_tile_carries(uint64_t* __restrict__ out, const uint64_t* __restrict__ cw, size_t m,
+                                    size_t batch, int tiles, int tile_limbs) {
+    const size_t pair = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pair >= batch) return;
+    uint64_t* row = out + pair * 2 * m;
+    for (int t = 1; t < tiles; ++t) {
+        uint64_t add = cw[pair * tiles + t - 1];
+        for (size_t L = size_t(t) * tile_limbs; add != 0 && L < 2 * m; ++L) {
+            const uint64_t s = row[L] + add;
+            add = s < add ? 1u : 0u;
+            row[L] = s;
+        }
+    }
+}
+
+}  // namespace
+
+bool mul_umma_supported(size_t m) {
+    static const int enabled = [] {
+        const char* e = std::getenv("DOTG_MUL_UMMA");
+        return e ? std::atoi(e) : 1;
+    }();
+    return enabled != 0 && m >= 256 && m <= 4096 && m % 16 == 0;
+}
+
+size_t mul_umma_leaf() {
+    static const size_t leaf = [] {
+        const char* e = std::getenv("DOTG_UMMA_LEAF");
+        const long v = e ? std::atol(e) : 2048;
+        return size_t(v >= 256 && v <= 4096 && (v & (v - 1)) == 0 ? v : 2048);
+    }();
+    return leaf;
+}
+
+cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
+                            cudaStream_t st) {
+    if (batch == 0) return cudaSuccess;
+    if (!(m >= 256 && m <= 4096 && m % 16 == 0)) return cudaErrorInvalidValue;
+    const UmmaGeom G = umma_geom(int(m));
+    // occupancy: TMEM holds 512 columns per SM, so ask for enough shared memory that no
+    // more CTAs than that fit (a CTA waiting in tcgen05.alloc would hold its SM slot)
+    const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
+    const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
+    const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
+    cudaError_t e = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const size_t ctas = batch * size_t(G.tiles);
+    if (ctas > size_t(0x7fffffff)) return cudaErrorInvalidConfiguration;
+    uint64_t* cw = nullptr;
+    if (G.tiles > 1) {
+        retain_stream_pool();
+        e = cudaMallocAsync(&cw, batch * size_t(G.tiles) * 8, st);
+        if (e != cudaSuccess) return e;
+    }
+    k_mul_umma<<<unsigned(ctas), kThreads, smem, st>>>(out, cw, a, b, int(m));
+    count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess && G.tiles > 1) {
+        k_umma_tile_carries<<<unsigned((batch + 127) / 128), 128, 0, st>>>(out, cw, m, batch, G.tiles, 16 * G.nt);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    if (cw != nullptr) cudaFreeAsync(cw, st);
+    return e;
+}
+
+}  // namespace dotg
