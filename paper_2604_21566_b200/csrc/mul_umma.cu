@@ -75,6 +75,54 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait for warps off the critical path: suspended in hardware until the phase completes
+// (or the hint elapses), so spinning waiters do not take issue slots from the MMA issuer.
+__device__ __forceinline__ void mbar_sleep(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\nUMMA_SLEEP_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra UMMA_SLEEP_%=;\n}" ::"r"(bar),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
+// The MMAs of one ring slot (s-steps s0 .. s1-1), issued by ONE elected lane of a
+// converged warp. Descriptors are linear in the address (14-bit field, 16-byte units):
+// A of (s, p) = slot base + 8 (16 (s - s0) + 12 - 4 p); B of (p, row j) = b_p0 + p b_dp + j.
+__device__ __forceinline__ void issue_block(uint32_t slot_addr, int s0, int s1, int C0, int na, int nt, uint32_t dbase,
+                                            uint64_t b_p0, uint64_t b_dp) {
+    const uint64_t a_s0 = sdesc(slot_addr + 12 * 128, 256, 128);
+    for (int s = s0; s < s1; ++s) {
+        int lo = s - C0, hi = s - C0 + na;
+        if (lo < 0) lo = 0;
+        if (hi > nt) hi = nt;
+        if (hi <= lo) continue;
+        const int lo16 = lo & ~15, hi16 = (hi + 15) & ~15;
+        const uint32_t id = idesc_u8(uint32_t(hi16 - lo16));
+        const uint32_t dcol = dbase + uint32_t(lo16);
+        const uint64_t ad = a_s0 + uint64_t(128 * (s - s0));
+        const uint64_t bd = b_p0 + uint64_t(C0 + lo16 - s);
+        asm volatile(
+            "{\n\t.reg .pred pe;\n\t.reg .pred pa;\n\t"
+            "elect.sync _|pe, 0xffffffff;\n\t"
+            "setp.ne.b32 pa, %4, 0;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pa;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::i8 [%0], %5, %6, %3, pa;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::i8 [%0], %7, %8, %3, pa;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::i8 [%0], %9, %10, %3, pa;\n\t}" ::"r"(dcol),
+            "l"(ad), "l"(bd), "r"(id), "r"(1u), "l"(ad - 32), "l"(bd + b_dp), "l"(ad - 64), "l"(bd + 2 * b_dp),
+            "l"(ad - 96), "l"(bd + 3 * b_dp)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\telect.sync _|pe, 0xffffffff;\n\t"
+        "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+}
+
 struct UmmaGeom {
     int na;      // a-chunks (128 bytes) per operand = m / 16
     int nt;      // D tile width in chunks (TMEM columns)
@@ -186,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(bs);
         for (int q = 0; q < nblocks; ++q) {
             const int slot = q % kSlots, s0 = q * kSB;
-            if (q >= kSlots) mbar_wait(smem_u32(&empty[slot]), uint32_t(q / kSlots - 1) & 1u);
+            if (q >= kSlots) mbar_sleep(smem_u32(&empty[slot]), uint32_t(q / kSlots - 1) & 1u);
             uint8_t* rs = ring + slot * (kTC * 128);
             const int t0 = 16 * s0 - 12;
 #pragma unroll 2
@@ -205,39 +253,21 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
         }
-    } else if (lane == 0) {
-        // issuer: one thread, MMAs of a slot once its 4 builder warps arrived
+    } else {
+        // issuer: warp 4 (converged, one elected lane issues), MMAs of a slot once its 4
+        // builder warps arrived
+        const uint64_t b_p0 = sdesc(smem_u32(bh) + kPadJ * 16, G.la, 128);
+        const uint64_t b_dp = uint64_t(2 * G.la / 16);
         for (int q = 0; q < nblocks; ++q) {
             const int slot = q % kSlots, s0 = q * kSB;
             mbar_wait(smem_u32(&full[slot]), uint32_t(q / kSlots) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint8_t* rs = ring + slot * (kTC * 128);
-            const int s1 = s0 + kSB < nb + 1 ? s0 + kSB : nb + 1;
-            for (int s = s0; s < s1; ++s) {
-                int lo = s - C0, hi = s - C0 + na;
-                if (lo < 0) lo = 0;
-                if (hi > G.nt) hi = G.nt;
-                if (hi <= lo) continue;
-                const int lo16 = lo & ~15, hi16 = (hi + 15) & ~15;
-                const uint32_t id = idesc_u8(uint32_t(hi16 - lo16));
-                const uint32_t dcol = tm + uint32_t(lo16);
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const uint64_t ad = sdesc(smem_u32(rs + (16 * (s - s0) + 12 - 4 * p) * 128), 256, 128);
-                    const uint64_t bd = sdesc(smem_u32(bh + (2 * p) * G.la + (C0 + lo16 - s + kPadJ) * 16), G.la, 128);
-                    asm volatile(
-                        "{\n\t.reg .pred pa;\n\tsetp.ne.b32 pa, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pa;\n\t}" ::"r"(dcol),
-                        "l"(ad), "l"(bd), "r"(id), "r"(1u)
-                        : "memory");
-                }
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             smem_u32(q == nblocks - 1 ? &done : &empty[slot]))
-                         : "memory");
+            issue_block(smem_u32(ring + slot * (kTC * 128)), s0, s0 + kSB < nb + 1 ? s0 + kSB : nb + 1, C0, na, G.nt,
+                        tm, b_p0, b_dp);
+            commit_elect(smem_u32(q == nblocks - 1 ? &done : &empty[slot]));
         }
     }
-    mbar_wait(smem_u32(&done), 0u);
+    mbar_sleep(smem_u32(&done), 0u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     // Epilogue (all operand shared memory is free now).
@@ -372,24 +402,26 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     if (batch == 0) return cudaSuccess;
     if (!(m >= 256 && m <= 4096 && m % 16 == 0)) return cudaErrorInvalidValue;
     const UmmaGeom G = umma_geom(int(m));
-    // occupancy: TMEM holds 512 columns per SM, so ask for enough shared memory that no
-    // more CTAs than that fit (a CTA waiting in tcgen05.alloc would hold its SM slot)
-    const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
-    const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
-    const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
-    cudaError_t e = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    const size_t ctas = batch * size_t(G.tiles);
-    if (ctas > size_t(0x7fffffff)) return cudaErrorInvalidConfiguration;
+    cudaError_t e = cudaSuccess;
+    const size_t items = batch * size_t(G.tiles);
+    if (items > size_t(0x7fffffff)) return cudaErrorInvalidConfiguration;
     uint64_t* cw = nullptr;
     if (G.tiles > 1) {
         retain_stream_pool();
         e = cudaMallocAsync(&cw, batch * size_t(G.tiles) * 8, st);
         if (e != cudaSuccess) return e;
     }
-    k_mul_umma<<<unsigned(ctas), kThreads, smem, st>>>(out, cw, a, b, int(m));
-    count_launch();
-    e = cudaGetLastError();
+    // occupancy: TMEM holds 512 columns per SM, so ask for enough shared memory that no
+    // more CTAs than that fit (a CTA waiting in tcgen05.alloc would hold its SM slot)
+    const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
+    const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
+    const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
+    e = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e == cudaSuccess) {
+        k_mul_umma<<<unsigned(items), kThreads, smem, st>>>(out, cw, a, b, int(m));
+        count_launch();
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess && G.tiles > 1) {
         k_umma_tile_carries<<<unsigned((batch + 127) / 128), 128, 0, st>>>(out, cw, m, batch, G.tiles, 16 * G.nt);
         count_launch();
