@@ -14,7 +14,7 @@ C1 (4096-bit add/sub), C3/C4 (1024/4096-bit mul, products/s vs the measured IMAD
 roofline), C5 (one 2^30-limb add/sub), plus the interleaved layout.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--only C1,C3,C4,C5,IL] [--no-secondary]
+                  [--only C1,C3,C4,C5,IL,R52,WIDE] [--no-secondary]
 
 N > 1: launched by torch.distributed.run, one rank per GPU. Strong scaling: rank r runs
 the contiguous slice [B*r/N, B*(r+1)/N) of every named batch (no collective on the data
@@ -484,6 +484,12 @@ def hbm_roofline(alg_bytes, launch_s, peak, kernel, peak_kind="measured (MEASURE
          "launch_us_avg": launch_s * 1e6, "peak_kind": peak_kind}
     r.update(extra)
     return r
+
+
+# tcgen05.mma kind::i8 dense rate (tools/umma_i8_probe.cu, profiles/r02_umma_i8_probe.jsonl: N = 128 / 256)
+UMMA_U8_MACS_PER_CLK_SM = 8192
+# dotg_mul_batch on the mma.sync Karatsuba route before the tcgen05 kernel (profiles/r02_umma_wide_variants.txt)
+WIDE_PRIOR_US = {(1024, 1024): 223.8, (2048, 256): 210.0, (4096, 64): 206.6}
 
 
 def per_launch_us(torch, dg, lib, stream, make_calls, reps=4):
@@ -1145,6 +1151,37 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                          "frac_hbm": byts / (us * 1e-6) / 1e9 / hbm_peak, "batch": Bq}
             del a, b, o
         out["base_case_256bit"] = r52
+        torch.cuda.empty_cache()
+
+    # ---------------- wide products on tcgen05 (mul_umma.cu; Karatsuba leaves above 4096 limbs) ----------------
+    if want("WIDE") and world == 1 and not args.no_layouts:
+        wide = {}
+        tensor_peak = sms * UMMA_U8_MACS_PER_CLK_SM * sm_max * 1e6  # byte-MACs / s at max clock
+        for m, B in ((1024, 1024), (2048, 256), (4096, 64)):
+            sets = []
+            for r in range(2):
+                a = W.fill(B * m, 0x3C + m + 7 * r, 0).view(B, m)
+                b = W.fill(B * m, 0x3C + m + 7 * r, 1 << 40).view(B, m)
+                sets.append((a, b, torch.empty((B, 2 * m), dtype=torch.int64, device="cuda")))
+
+            def mk(Lc, sets=sets, m=m, B=B):
+                return [(lambda args_=(P(o), P(a), P(b), m, B, 0, Lc.stream): lib.dotg_mul_batch(*args_))
+                        for a, b, o in sets]
+            us = per_launch_us(torch, dg, lib, stream, mk)
+            macs = B * (8 * m) ** 2
+            wide[f"m{m}_B{B}"] = {"pairs_s": B / (us * 1e-6), "us": us, "byte_macs_per_s": macs / (us * 1e-6),
+                                  "frac_tensor_u8": macs / (us * 1e-6) / tensor_peak,
+                                  "prior_route_us": WIDE_PRIOR_US.get((m, B))}
+            del sets
+        out["wide_products"] = {
+            "kernel": "k_mul_umma: tcgen05.mma.cta_group::1.kind::i8 M=128, Hankel core-matrix ring (A) and "
+                      "byte-reversed a-chunk arrays (B) in shared memory, column sums in TMEM, in-CTA carry resolve",
+            "per_shape": wide, "tensor_peak_byte_macs_per_s": tensor_peak,
+            "peak_note": "148 SMs x 8192 u8 MACs/clk/SM (tools/umma_i8_probe.cu, N=128/256) x max SM clock; "
+                         "schoolbook byte-MACs (8m)^2 per pair counted",
+            "prior_route_note": "prior_route_us: the same call on the mma.sync Karatsuba route (DOTG_MUL_UMMA=0), "
+                                "profiles/r02_umma_wide_variants.txt",
+            "timing": "back-to-back calls over 2 rotating input sets (CUDA graph, events on the stream)"}
         torch.cuda.empty_cache()
 
     # ---------------- C5: one 2^30-limb add / sub ----------------

@@ -378,6 +378,18 @@ __global__ void k_umma_tile_carries(uint64_t* __restrict__ out, const uint64_t* 
     }
 }
 
+uint32_t umma_max_smem() {
+    uint32_t mx = 0;
+    for (int m = 256; m <= 4096; m += 16) {
+        const UmmaGeom G = umma_geom(m);
+        const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
+        const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
+        const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
+        if (smem > mx) mx = smem;
+    }
+    return mx;
+}
+
 }  // namespace
 
 bool mul_umma_supported(size_t m) {
@@ -416,7 +428,11 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
     const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
     const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
-    e = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    // the largest dynamic shared memory any size needs, set once per process (not a stream
+    // operation, so launches stay capturable into CUDA graphs)
+    static const cudaError_t attr = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         int(umma_max_smem()));
+    e = attr;
     if (e == cudaSuccess) {
         k_mul_umma<<<unsigned(items), kThreads, smem, st>>>(out, cw, a, b, int(m));
         count_launch();

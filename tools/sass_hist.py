@@ -14,6 +14,7 @@ KERNELS = {
     "addsub_batch.o": ["k_addsub_grouped", "k_addsub_timed", "k_addsub_ilf", "k_il_local", "k_il_finish"],
     "mul_batch.o": ["k_mul_kara16", "k_mul_regblk", "k_mul52_regs"],
     "mul_imma.o": ["k_mul_imma"],
+    "mul_umma.o": ["k_mul_umma", "k_umma_tile_carries"],
     "addsub_long.o": ["k_long_local", "k_long_finish"],
 }
 KEY = re.compile(r"^(UTC\w*|LDTM|STTM|UBLKCP|SYNCS|IMMA|HMMA|IMAD|IADD3|LDS|STS|LDG|STG|SHFL|VOTE|BAR|LOP3|SEL|DFMA|DADD)")
