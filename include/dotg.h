@@ -114,8 +114,12 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
 /* Which pipe dotg_mul_batch (and everything built on it) takes the partial products on.
  * AUTO (row-major, 32-byte aligned pointers): m <= 16 on the IMAD column kernels; m in
  * {32, 64, 128} on the integer tensor pipe (radix-2^8 IMMA column sums); other
- * 16 < m < 128 zero-padded to the next of those; m > 128 as padded Karatsuba down to
- * m = 128 tensor-pipe leaves. Interleaved or misaligned operands: IMAD kernels.
+ * 16 < m < 128 zero-padded to the next of those; 128 < m < 256 as padded Karatsuba down
+ * to m = 128 tensor-pipe leaves; 256 <= m <= 4096 on the 5th-generation tensor core
+ * (tcgen05.mma kind::i8, column sums in tensor memory; rows padded to a multiple of 16
+ * limbs); m > 4096 as padded Karatsuba down to 2048-limb tcgen05 leaves (environment:
+ * DOTG_MUL_UMMA=0 keeps the mma.sync leaves, DOTG_UMMA_LEAF picks the leaf size).
+ * Interleaved or misaligned operands: IMAD kernels.
  * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
  * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it
  * does not cover). Both are bit-exact; the knob exists for A/B measurement and for
