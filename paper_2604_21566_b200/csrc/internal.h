@@ -88,12 +88,13 @@ cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t*
 cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st);
 // Wide operands on the 5th-generation tensor core (mul_umma.cu): row-major, 16-byte
-// aligned rows, 256 <= m <= 4096, m % 16 == 0 (DOTG_MUL_UMMA=0 disables the route).
+// aligned rows, 256 <= m <= 16384, m % 16 == 0 (DOTG_MUL_UMMA=0 disables the route).
 bool mul_umma_supported(size_t m);
 cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st);
-// Karatsuba leaf size above the tcgen05 range (DOTG_UMMA_LEAF, default 2048).
-size_t mul_umma_leaf();
+// Karatsuba leaf size above the tcgen05 range for an m-limb product (DOTG_UMMA_LEAF
+// overrides: 16384 up to 2^18 limbs, 4096 above).
+size_t mul_umma_leaf(size_t m);
 // Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
 extern std::atomic<int> g_mul_route;
 

@@ -54,6 +54,7 @@ constexpr int kTC = 16 * kSB + 16;   // core matrices per ring slot
 constexpr int kSlots = 3;            // ring slots
 constexpr int kWorkers = 128;        // builder / epilogue warps 0-3 (TMEM lane quarters)
 constexpr int kThreads = 160;        // + warp 4: the MMA issuer
+constexpr int kUmmaMaxM = 16384;     // direct route up to here, Karatsuba leaves above
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -123,77 +124,96 @@ __device__ __forceinline__ void commit_elect(uint32_t bar) {
         : "memory");
 }
 
-struct UmmaGeom {
-    int na;      // a-chunks (128 bytes) per operand = m / 16
-    int nt;      // D tile width in chunks (TMEM columns)
-    int tiles;   // tiles per pair
-    int cols;    // TMEM columns allocated (power of two >= 32)
-    uint32_t la; // bytes of one B array
+// Work decomposition of one product size. An item is (pair, D tile of NT output chunks,
+// split of the b-window steps s); m <= 4096 runs every s in one item (the CTA finishes the
+// tile's limbs), larger m splits s into ranges of <= 128 steps (column sums of <= 16 KB of
+// b per accumulator: < 2^31) whose folded partial limbs a second kernel adds.
+struct UmmaPlan {
+    int m, na, nt, tiles, splits, ss, cols;
+    int jrows;        // a-chunk rows staged per B array (without pads)
+    uint32_t la;      // bytes of one B array
+    int bmax;         // b bytes staged at most
     uint32_t off_ring, off_b, smem;
 };
 
-__host__ __device__ inline UmmaGeom umma_geom(int m) {
-    UmmaGeom g{};
+inline UmmaPlan umma_plan(int m) {
+    UmmaPlan g{};
+    g.m = m;
     g.na = m / 16;
     g.nt = 2 * g.na < 256 ? (2 * g.na + 15) & ~15 : 256;
     g.tiles = (2 * g.na + g.nt - 1) / g.nt;
     g.cols = g.nt <= 32 ? 32 : (g.nt <= 64 ? 64 : (g.nt <= 128 ? 128 : 256));
-    g.la = uint32_t(g.na + 2 * kPadJ) * 16;
+    const int steps = g.na + 1;
+    g.splits = g.na <= 256 ? 1 : (steps + 127) / 128;
+    g.ss = (steps + g.splits - 1) / g.splits;
+    g.jrows = g.splits == 1 ? g.na : (g.na < g.nt + g.ss ? g.na : g.nt + g.ss);
+    g.la = uint32_t(g.jrows + 2 * kPadJ) * 16;
+    g.bmax = g.splits == 1 ? 8 * m : 128 * (g.ss + 1);
     g.off_ring = 8 * g.la;
     g.off_b = g.off_ring + kSlots * kTC * 128;
-    g.smem = g.off_b + uint32_t(8 * m + 2 * kPadB);
+    g.smem = g.off_b + uint32_t(g.bmax + 2 * kPadB);
     const uint32_t epi = uint32_t(12 * 16 * g.nt + 4 * 16 * 32 * 4);  // LO, HI, per-warp transpose
     if (g.smem < epi) g.smem = epi;
     return g;
 }
 
 __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ out, uint64_t* __restrict__ carry_words,
+                                                     uint64_t* __restrict__ part_lo, uint32_t* __restrict__ part_hi,
                                                      const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                                                     int m) {
+                                                     const UmmaPlan G) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots], done;
     __shared__ uint32_t tbase_sh;
-    const UmmaGeom G = umma_geom(m);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const size_t pair = blockIdx.x / unsigned(G.tiles);
-    const int C0 = int(blockIdx.x % unsigned(G.tiles)) * G.nt;
-    const int na = G.na, nb = G.na, n = 8 * m;
-    uint8_t* bh = sm;                       // 8 arrays [p][kk], (na + 2 kPadJ) rows of 16 B
-    uint8_t* ring = sm + G.off_ring;        // 2 slots x kTC core matrices
-    uint8_t* bs = sm + G.off_b;             // kPadB zeros | b | kPadB zeros
+    const int m = G.m, na = G.na, nb = G.na, n = 8 * m;
+    const int split = int(blockIdx.x % unsigned(G.splits));
+    const int C0 = int((blockIdx.x / unsigned(G.splits)) % unsigned(G.tiles)) * G.nt;
+    const size_t pair = blockIdx.x / unsigned(G.splits * G.tiles);
+    // this item's b-window steps, the a-chunks they pair with, the b bytes they read
+    const int s_lo = split * G.ss, s_hi = s_lo + G.ss < nb + 1 ? s_lo + G.ss : nb + 1;
+    const int j_lo = C0 - s_hi + 1 > 0 ? C0 - s_hi + 1 : 0;
+    const int j_hi = C0 + G.nt - s_lo < na ? C0 + G.nt - s_lo : na;
+    const int b_lo = 128 * s_lo - 128 > 0 ? 128 * s_lo - 128 : 0;
+    const int b_hi = 128 * s_hi < n ? 128 * s_hi : n;
+    const int nbs = b_hi - b_lo;  // staged b bytes (a multiple of 128)
+    uint8_t* bh = sm;                       // 8 arrays [p][kk], rows J - j_lo + kPadJ of 16 B
+    uint8_t* ring = sm + G.off_ring;        // kSlots slots x kTC core matrices
+    uint8_t* bs = sm + G.off_b;             // kPadB zeros | b[b_lo, b_hi) | kPadB zeros
     const uint4* ga = reinterpret_cast<const uint4*>(a + pair * size_t(m));
-    const uint4* gb = reinterpret_cast<const uint4*>(b + pair * size_t(m));
+    const uint4* gb = reinterpret_cast<const uint4*>(b + pair * size_t(m) + size_t(b_lo / 8));
 
     // a -> B arrays: 16-byte segment g of the operand is half (g & 1) of block 4J + p,
     // J = g / 8, p = (g / 2) % 4; stored byte-reversed as row J of array (p, kk = 1 - half).
-    for (int g0 = tid; g0 < n / 16; g0 += 4 * kThreads) {  // n / 16 is a multiple of 128: 4 loads in flight
+    const int g_lo = 8 * j_lo, g_hi = j_hi > j_lo ? 8 * j_hi : g_lo;
+    for (int g0 = g_lo + tid; g0 < g_hi; g0 += 4 * kThreads) {  // 4 loads in flight
         uint4 w[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < n / 16 ? __ldg(ga + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < g_hi ? __ldg(ga + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int g = g0 + u * kThreads;
-            if (g >= n / 16) break;
+            if (g >= g_hi) break;
             const int J = g >> 3, p = (g >> 1) & 3, kk = 1 - (g & 1);
-            *reinterpret_cast<uint4*>(bh + (2 * p + kk) * G.la + (J + kPadJ) * 16) =
+            *reinterpret_cast<uint4*>(bh + (2 * p + kk) * G.la + (J - j_lo + kPadJ) * 16) =
                 make_uint4(bswap32(w[u].w), bswap32(w[u].z), bswap32(w[u].y), bswap32(w[u].x));
         }
     }
+    const int rows = j_hi > j_lo ? j_hi - j_lo : 0;
     for (int e = tid; e < 8 * 2 * kPadJ; e += kThreads) {  // zero chunks on both sides
         const int arr = e / (2 * kPadJ), q = e % (2 * kPadJ);
-        const int row = q < kPadJ ? q : na + q;
+        const int row = q < kPadJ ? q : rows + q;
         *reinterpret_cast<uint4*>(bh + arr * G.la + row * 16) = make_uint4(0, 0, 0, 0);
     }
-    for (int g0 = tid; g0 < n / 16; g0 += 4 * kThreads) {
+    for (int g0 = tid; g0 < nbs / 16; g0 += 4 * kThreads) {
         uint4 w[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < n / 16 ? __ldg(gb + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < nbs / 16 ? __ldg(gb + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (g0 + u * kThreads < n / 16) reinterpret_cast<uint4*>(bs + kPadB)[g0 + u * kThreads] = w[u];
+            if (g0 + u * kThreads < nbs / 16) reinterpret_cast<uint4*>(bs + kPadB)[g0 + u * kThreads] = w[u];
     }
     for (int e = tid; e < 2 * kPadB / 16; e += kThreads) {
-        const int off = e < kPadB / 16 ? e * 16 : kPadB + n + (e - kPadB / 16) * 16;
+        const int off = e < kPadB / 16 ? e * 16 : kPadB + nbs + (e - kPadB / 16) * 16;
         *reinterpret_cast<uint4*>(bs + off) = make_uint4(0, 0, 0, 0);
     }
     // barriers: full[q] (4 builder warps arrive), empty[q] (MMA commit), done (last commit)
@@ -228,20 +248,20 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
 
-    const int nblocks = (nb + 1 + kSB - 1) / kSB;  // s = 0 .. nb in blocks of kSB steps
+    const int nblocks = (s_hi - s_lo + kSB - 1) / kSB;  // s = s_lo .. s_hi-1 in blocks of kSB steps
     if (warp < 4) {
         // builders: ring slot q % kSlots <- core matrices t = 16 s0 - 12 + (row / 8), row rr = row % 8
         const uint32_t* bw = reinterpret_cast<const uint32_t*>(bs);
         for (int q = 0; q < nblocks; ++q) {
-            const int slot = q % kSlots, s0 = q * kSB;
+            const int slot = q % kSlots, s0 = s_lo + q * kSB;
             if (q >= kSlots) mbar_sleep(smem_u32(&empty[slot]), uint32_t(q / kSlots - 1) & 1u);
             uint8_t* rs = ring + slot * (kTC * 128);
             const int t0 = 16 * s0 - 12;
 #pragma unroll 2
             for (int row = tid; row < kTC * 8; row += kWorkers) {
-                const int o = 8 * (t0 + (row >> 3)) + (row & 7) - 31 + kPadB;  // byte offset in bs
+                const int o = 8 * (t0 + (row >> 3)) + (row & 7) - 31 - b_lo + kPadB;  // byte offset in bs
                 uint4 v = make_uint4(0, 0, 0, 0);
-                if (o + 16 > kPadB && o < kPadB + n) {
+                if (o + 16 > kPadB && o < kPadB + nbs) {
                     const int w0 = o >> 2, sh = (o & 3) * 8;
                     const uint32_t x0 = bw[w0], x1 = bw[w0 + 1], x2 = bw[w0 + 2], x3 = bw[w0 + 3], x4 = bw[w0 + 4];
                     v = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh),
@@ -256,14 +276,15 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
     } else {
         // issuer: warp 4 (converged, one elected lane issues), MMAs of a slot once its 4
         // builder warps arrived
-        const uint64_t b_p0 = sdesc(smem_u32(bh) + kPadJ * 16, G.la, 128);
+        // B row of chunk J is J - j_lo + kPadJ (issue_block adds J)
+        const uint64_t b_p0 = sdesc(smem_u32(bh) + kPadJ * 16, G.la, 128) - uint64_t(j_lo);
         const uint64_t b_dp = uint64_t(2 * G.la / 16);
         for (int q = 0; q < nblocks; ++q) {
-            const int slot = q % kSlots, s0 = q * kSB;
+            const int slot = q % kSlots, s0 = s_lo + q * kSB;
             mbar_wait(smem_u32(&full[slot]), uint32_t(q / kSlots) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            issue_block(smem_u32(ring + slot * (kTC * 128)), s0, s0 + kSB < nb + 1 ? s0 + kSB : nb + 1, C0, na, G.nt,
-                        tm, b_p0, b_dp);
+            issue_block(smem_u32(ring + slot * (kTC * 128)), s0, s0 + kSB < s_hi ? s0 + kSB : s_hi, C0, na, G.nt, tm,
+                        b_p0, b_dp);
             commit_elect(smem_u32(q == nblocks - 1 ? &done : &empty[slot]));
         }
     }
@@ -309,52 +330,61 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
-    // add kernel's generate / propagate algebra. Warp w owns limbs [w nl/4, (w+1) nl/4) in
-    // rounds of 32 consecutive limbs (lane = limb, conflict-free): pass 1 folds the rounds
-    // into the warp's (carry-out, all-propagate), pass 2 applies the carries.
-    {
-        const int per_warp = nl / 4, rounds = per_warp / 32;  // nl = 16 * xe16 -> rounds >= 2
-        const int base = warp * per_warp;
-        __shared__ uint32_t wagg[4][2];
-        if (warp < 4) {
-            uint32_t Gw = 0, Pw = 1;
-            for (int r = 0; r < rounds; ++r) {
-                const int L = base + 32 * r + lane;
-                const uint64_t lo = LO[L];
-                const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
-                const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
-                const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
-                Gw = go | ((pp == 0xffffffffu) & Gw);
-                Pw &= pp == 0xffffffffu;
+    if (G.splits > 1) {
+        // partial limbs of this s-range: a second kernel adds the splits and the carries
+        const size_t base = (pair * size_t(G.splits) + size_t(split)) * size_t(2 * m) + size_t(16 * C0);
+        for (int e = tid; e < 16 * xend; e += kThreads) {
+            part_lo[base + e] = LO[e];
+            part_hi[base + e] = HI[e];
+        }
+    } else {
+        // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
+        // add kernel's generate / propagate algebra. Warp w owns limbs [w nl/4, (w+1) nl/4) in
+        // rounds of 32 consecutive limbs (lane = limb, conflict-free): pass 1 folds the rounds
+        // into the warp's (carry-out, all-propagate), pass 2 applies the carries.
+        {
+            const int per_warp = nl / 4, rounds = per_warp / 32;  // nl = 16 * xe16 -> rounds >= 2
+            const int base = warp * per_warp;
+            __shared__ uint32_t wagg[4][2];
+            if (warp < 4) {
+                uint32_t Gw = 0, Pw = 1;
+                for (int r = 0; r < rounds; ++r) {
+                    const int L = base + 32 * r + lane;
+                    const uint64_t lo = LO[L];
+                    const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                    const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                    const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
+                    Gw = go | ((pp == 0xffffffffu) & Gw);
+                    Pw &= pp == 0xffffffffu;
+                }
+                if (lane == 0) {
+                    wagg[warp][0] = Gw;
+                    wagg[warp][1] = Pw;
+                }
             }
-            if (lane == 0) {
-                wagg[warp][0] = Gw;
-                wagg[warp][1] = Pw;
+            __syncthreads();
+            if (warp < 4) {
+                uint32_t c = 0;
+                for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
+                for (int r = 0; r < rounds; ++r) {
+                    const int L = base + 32 * r + lane;
+                    const uint64_t lo = LO[L];
+                    const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                    const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                    const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
+                    LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
+                    c = uint32_t(y >> 32);
+                }
+                if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
+                    carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
             }
         }
         __syncthreads();
-        if (warp < 4) {
-            uint32_t c = 0;
-            for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
-            for (int r = 0; r < rounds; ++r) {
-                const int L = base + 32 * r + lane;
-                const uint64_t lo = LO[L];
-                const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
-                const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
-                const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
-                LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
-                c = uint32_t(y >> 32);
-            }
-            if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
-                carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
+        {
+            uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
+            for (int e = tid; e < 8 * xend; e += kThreads)
+                reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
         }
-    }
-    __syncthreads();
-    {
-        uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
-        for (int e = tid; e < 8 * xend; e += kThreads)
-            reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -378,10 +408,30 @@ __global__ void k_umma_tile_carries(uint64_t* __restrict__ out, const uint64_t* 
     }
 }
 
+// Split items: out[L] = sum of the splits' low words, next[L + 1] = their high words plus
+// the low-word carries (then one batched add resolves out + next).
+__global__ void k_umma_reduce(uint64_t* __restrict__ out, uint64_t* __restrict__ next,
+                              const uint64_t* __restrict__ part_lo, const uint32_t* __restrict__ part_hi, size_t m,
+                              size_t batch, int splits) {
+    const size_t idx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= batch * 2 * m) return;
+    const size_t pair = idx / (2 * m), L = idx % (2 * m);
+    uint64_t lo = 0, hi = 0;
+    for (int sp = 0; sp < splits; ++sp) {
+        const size_t k = (pair * size_t(splits) + size_t(sp)) * 2 * m + L;
+        const uint64_t v = part_lo[k];
+        lo += v;
+        hi += (lo < v ? 1u : 0u) + uint64_t(part_hi[k]);
+    }
+    out[idx] = lo;
+    if (L + 1 < 2 * m) next[idx + 1] = hi;
+    if (L == 0) next[idx] = 0;
+}
+
 uint32_t umma_max_smem() {
     uint32_t mx = 0;
-    for (int m = 256; m <= 4096; m += 16) {
-        const UmmaGeom G = umma_geom(m);
+    for (int m = 256; m <= kUmmaMaxM; m += 16) {
+        const UmmaPlan G = umma_plan(m);
         const int per_sm = 512 / G.cols < 8 ? 512 / G.cols : 8;
         const uint32_t floor_smem = uint32_t(228 * 1024 / (per_sm + 1)) + 16;
         const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
@@ -397,31 +447,39 @@ bool mul_umma_supported(size_t m) {
         const char* e = std::getenv("DOTG_MUL_UMMA");
         return e ? std::atoi(e) : 1;
     }();
-    return enabled != 0 && m >= 256 && m <= 4096 && m % 16 == 0;
+    return enabled != 0 && m >= 256 && m <= size_t(kUmmaMaxM) && m % 16 == 0;
 }
 
-size_t mul_umma_leaf() {
-    static const size_t leaf = [] {
+size_t mul_umma_leaf(size_t m) {
+    // Karatsuba level passes are latency-bound for a handful of huge numbers, so few levels
+    // over big leaves win up to 2^18 limbs; above, the 25% of products saved per level win
+    // (tools/umma_timing.py, profiles/r02_umma_wide_variants.txt: 2^16 limbs 524 / 698 /
+    // 850 us with 16384 / 8192 / 4096-limb leaves, 2^20 limbs 9.7 / 9.0 / 7.4 ms).
+    static const long env = [] {
         const char* e = std::getenv("DOTG_UMMA_LEAF");
-        const long v = e ? std::atol(e) : 2048;
-        return size_t(v >= 256 && v <= 4096 && (v & (v - 1)) == 0 ? v : 2048);
+        return e ? std::atol(e) : 0L;
     }();
-    return leaf;
+    if (env >= 256 && env <= kUmmaMaxM && (env & (env - 1)) == 0) return size_t(env);
+    return m <= (size_t(1) << 18) ? size_t(kUmmaMaxM) : size_t(4096);
 }
 
 cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
-    if (!(m >= 256 && m <= 4096 && m % 16 == 0)) return cudaErrorInvalidValue;
-    const UmmaGeom G = umma_geom(int(m));
+    if (!(m >= 256 && m <= size_t(kUmmaMaxM) && m % 16 == 0)) return cudaErrorInvalidValue;
+    const UmmaPlan G = umma_plan(int(m));
     cudaError_t e = cudaSuccess;
-    const size_t items = batch * size_t(G.tiles);
+    const size_t items = batch * size_t(G.tiles) * size_t(G.splits);
     if (items > size_t(0x7fffffff)) return cudaErrorInvalidConfiguration;
-    uint64_t* cw = nullptr;
-    if (G.tiles > 1) {
-        retain_stream_pool();
+    retain_stream_pool();
+    uint64_t *cw = nullptr, *plo = nullptr, *nxt = nullptr;
+    uint32_t* phi = nullptr;
+    if (G.splits > 1) {
+        e = cudaMallocAsync(&plo, batch * size_t(G.splits) * 2 * m * 8, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&phi, batch * size_t(G.splits) * 2 * m * 4, st);
+        if (e == cudaSuccess) e = cudaMallocAsync(&nxt, batch * 2 * m * 8, st);
+    } else if (G.tiles > 1) {
         e = cudaMallocAsync(&cw, batch * size_t(G.tiles) * 8, st);
-        if (e != cudaSuccess) return e;
     }
     // occupancy: TMEM holds 512 columns per SM, so ask for enough shared memory that no
     // more CTAs than that fit (a CTA waiting in tcgen05.alloc would hold its SM slot)
@@ -432,17 +490,25 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     // operation, so launches stay capturable into CUDA graphs)
     static const cudaError_t attr = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          int(umma_max_smem()));
-    e = attr;
+    if (e == cudaSuccess) e = attr;
     if (e == cudaSuccess) {
-        k_mul_umma<<<unsigned(items), kThreads, smem, st>>>(out, cw, a, b, int(m));
+        k_mul_umma<<<unsigned(items), kThreads, smem, st>>>(out, cw, plo, phi, a, b, G);
         count_launch();
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess && G.tiles > 1) {
+    if (e == cudaSuccess && G.splits > 1) {
+        k_umma_reduce<<<unsigned((batch * 2 * m + 255) / 256), 256, 0, st>>>(out, nxt, plo, phi, m, batch, G.splits);
+        count_launch();
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = launch_addsub_batch(false, out, out, nxt, nullptr, 2 * m, batch, 0, st);
+    }
+    if (e == cudaSuccess && G.splits == 1 && G.tiles > 1) {
         k_umma_tile_carries<<<unsigned((batch + 127) / 128), 128, 0, st>>>(out, cw, m, batch, G.tiles, 16 * G.nt);
         count_launch();
         e = cudaGetLastError();
     }
+    for (void* q : {static_cast<void*>(plo), static_cast<void*>(phi), static_cast<void*>(nxt)})
+        if (q != nullptr) cudaFreeAsync(q, st);
     if (cw != nullptr) cudaFreeAsync(cw, st);
     return e;
 }

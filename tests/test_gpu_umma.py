@@ -1,7 +1,8 @@
 """Wide products on the 5th-generation tensor core (mul_umma.cu: tcgen05.mma kind::i8,
 column sums in tensor memory) vs the oracle - the reference's own product contract
 (mul.cpp:96-103, exactly 2m limbs), restated at the sizes that route there: 256 <= m <= 4096
-directly (m % 16 == 0, rows padded otherwise) and the Karatsuba leaves above 4096 limbs.
+directly (m % 16 == 0, rows padded otherwise; s-range splits above 4096) and the
+Karatsuba leaves above 16384 limbs.
 All-ones rows give the largest column sums (n * 255^2 < 2^31 at m = 4096) and carries."""
 import numpy as np
 import pytest
@@ -51,7 +52,20 @@ def test_umma_many_pairs_both_tiles(cuda, oracle):
         assert np.array_equal(g[idx], oracle.mul_batch(a[idx], b[idx])), m
 
 
-@pytest.mark.parametrize("m", [6000, 8192])
+@pytest.mark.parametrize("m", [4112, 6000, 8192, 16384])
+def test_umma_split_route(cuda, oracle, m):
+    """4096 < m <= 16384: the b-window steps split into ranges of <= 128 (s32 column sums
+    stay exact), partial limbs added by k_umma_reduce, carries by one batched add."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(1450 + m)
+    a, b = _rows(rng, 5, m)
+    got = dg.mul_batch(torch.from_numpy(a.view(np.int64)).cuda(), torch.from_numpy(b.view(np.int64)).cuda())
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), oracle.mul_batch(a, b)), m
+
+
+@pytest.mark.parametrize("m", [20000])
 def test_umma_karatsuba_leaves(cuda, oracle, m):
     import paper_2604_21566_b200 as dg
 
