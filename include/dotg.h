@@ -115,10 +115,11 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
  * AUTO (row-major, 32-byte aligned pointers): m <= 16 on the IMAD column kernels; m in
  * {32, 64, 128} on the integer tensor pipe (radix-2^8 IMMA column sums); other
  * 16 < m < 128 zero-padded to the next of those; 128 < m < 256 as padded Karatsuba down
- * to m = 128 tensor-pipe leaves; 256 <= m <= 4096 on the 5th-generation tensor core
+ * to m = 128 tensor-pipe leaves; 256 <= m <= 65536 on the 5th-generation tensor core
  * (tcgen05.mma kind::i8, column sums in tensor memory; rows padded to a multiple of 16
- * limbs); m > 4096 as padded Karatsuba down to 2048-limb tcgen05 leaves (environment:
- * DOTG_MUL_UMMA=0 keeps the mma.sync leaves, DOTG_UMMA_LEAF picks the leaf size).
+ * limbs); m > 65536 as padded Karatsuba down to tcgen05 leaves (environment:
+ * DOTG_MUL_UMMA=0 keeps the mma.sync leaves, DOTG_UMMA_LEAF / DOTG_UMMA_DIRECT pick the
+ * leaf size and the direct limit).
  * Interleaved or misaligned operands: IMAD kernels.
  * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
  * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it

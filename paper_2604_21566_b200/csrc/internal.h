@@ -92,9 +92,11 @@ cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t*
 bool mul_umma_supported(size_t m);
 cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st);
-// Karatsuba leaf size above the tcgen05 range for an m-limb product (DOTG_UMMA_LEAF
-// overrides: 16384 up to 2^18 limbs, 4096 above).
-size_t mul_umma_leaf(size_t m);
+// Karatsuba leaf size above the direct tcgen05 range for a batch of m-limb products
+// (DOTG_UMMA_LEAF overrides; by batch x m: 65536 up to 2^17 limbs, 16384 up to 2^18, 4096).
+size_t mul_umma_leaf(size_t m, size_t batch);
+// Largest m taken directly (DOTG_UMMA_DIRECT, default 65536); Karatsuba above.
+size_t mul_umma_direct_max();
 // Route for launch_mul_batch: 0 auto, 1 IMAD only, 2 IMMA where supported.
 extern std::atomic<int> g_mul_route;
 

@@ -1064,12 +1064,13 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
         return launch_mul_imma_rt(out, a, b, m, batch, stream);
     // m >= 256: the tcgen05 column kernel (mul_umma.cu) up to 16384 limbs (rows padded to a
     // multiple of 16 limbs when needed), Karatsuba down to its leaves above that.
-    if (layout == 0 && route != 1 && m >= 256 && mul_umma_supported((m + 15) & ~size_t(15))) {
+    if (layout == 0 && route != 1 && m >= 256 && ((m + 15) & ~size_t(15)) <= mul_umma_direct_max() &&
+        mul_umma_supported((m + 15) & ~size_t(15))) {
         if (m % 16 == 0 && aligned16(a) && aligned16(b)) return launch_mul_umma(out, a, b, m, batch, stream);
         return mul_padded_rows(out, a, b, m, batch, (m + 15) & ~size_t(15), stream);
     }
-    if (layout == 0 && route != 1 && m > 16384 && mul_umma_supported(mul_umma_leaf(m)))
-        return launch_karatsuba_padded(out, a, b, m, batch, mul_umma_leaf(m), stream);
+    if (layout == 0 && route != 1 && m > mul_umma_direct_max() && mul_umma_supported(mul_umma_leaf(m, batch)))
+        return launch_karatsuba_padded(out, a, b, m, batch, mul_umma_leaf(m, batch), stream);
     if (layout == 0 && route != 1 && m > 16 && !mul_imma_supported(m))
         return launch_karatsuba_padded(out, a, b, m, batch, m <= 32 ? 32 : (m <= 64 ? 64 : 128), stream);
     // 4 < m < 16 off the power-of-two kernels, or misaligned rows of 5..16: the register

@@ -54,7 +54,7 @@ constexpr int kTC = 16 * kSB + 16;   // core matrices per ring slot
 constexpr int kSlots = 3;            // ring slots
 constexpr int kWorkers = 128;        // builder / epilogue warps 0-3 (TMEM lane quarters)
 constexpr int kThreads = 160;        // + warp 4: the MMA issuer
-constexpr int kUmmaMaxM = 16384;     // direct route up to here, Karatsuba leaves above
+constexpr int kUmmaMaxM = 65536;     // largest m the kernel takes (s-range splits above 4096)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -450,17 +450,27 @@ bool mul_umma_supported(size_t m) {
     return enabled != 0 && m >= 256 && m <= size_t(kUmmaMaxM) && m % 16 == 0;
 }
 
-size_t mul_umma_leaf(size_t m) {
+size_t mul_umma_direct_max() {
+    static const size_t v = [] {
+        const char* e = std::getenv("DOTG_UMMA_DIRECT");
+        const long x = e ? std::atol(e) : kUmmaMaxM;
+        return size_t(x >= 256 && x <= kUmmaMaxM ? x : kUmmaMaxM);
+    }();
+    return v;
+}
+
+size_t mul_umma_leaf(size_t m, size_t batch) {
     // Karatsuba level passes are latency-bound for a handful of huge numbers, so few levels
-    // over big leaves win up to 2^18 limbs; above, the 25% of products saved per level win
-    // (tools/umma_timing.py, profiles/r02_umma_wide_variants.txt: 2^16 limbs 524 / 698 /
-    // 850 us with 16384 / 8192 / 4096-limb leaves, 2^20 limbs 9.7 / 9.0 / 7.4 ms).
+    // over big leaves win when the batch holds little work; with more limbs in flight the
+    // 25% of products saved per level win (tools/umma_timing.py,
+    // profiles/r02_umma_wide_variants.txt).
     static const long env = [] {
         const char* e = std::getenv("DOTG_UMMA_LEAF");
         return e ? std::atol(e) : 0L;
     }();
     if (env >= 256 && env <= kUmmaMaxM && (env & (env - 1)) == 0) return size_t(env);
-    return m <= (size_t(1) << 18) ? size_t(kUmmaMaxM) : size_t(4096);
+    const double limbs = double(m) * double(batch);
+    return limbs <= double(1 << 17) ? size_t(65536) : (limbs <= double(1 << 18) ? size_t(16384) : size_t(4096));
 }
 
 cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
@@ -468,6 +478,18 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     if (batch == 0) return cudaSuccess;
     if (!(m >= 256 && m <= size_t(kUmmaMaxM) && m % 16 == 0)) return cudaErrorInvalidValue;
     const UmmaPlan G = umma_plan(int(m));
+    if (G.splits > 1) {  // partial limbs: 12 B per limb per split; keep them under 1 GiB per launch
+        const size_t per_pair = size_t(G.splits) * 2 * m * 12 + 2 * m * 8;
+        const size_t chunk = (size_t(1) << 30) / per_pair > 0 ? (size_t(1) << 30) / per_pair : 1;
+        if (batch > chunk) {
+            for (size_t p0 = 0; p0 < batch; p0 += chunk) {
+                const size_t nb = batch - p0 < chunk ? batch - p0 : chunk;
+                const cudaError_t e = launch_mul_umma(out + p0 * 2 * m, a + p0 * m, b + p0 * m, m, nb, st);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        }
+    }
     cudaError_t e = cudaSuccess;
     const size_t items = batch * size_t(G.tiles) * size_t(G.splits);
     if (items > size_t(0x7fffffff)) return cudaErrorInvalidConfiguration;
