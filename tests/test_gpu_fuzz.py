@@ -10,7 +10,7 @@ from helpers import CATEGORIES, category
 pytestmark = pytest.mark.gpu
 
 M_CHOICES = [1, 2, 3, 4, 5, 8, 9, 15, 16, 17, 24, 31, 32, 33, 48, 63, 64, 65, 96, 100, 127, 128, 129, 160, 200,
-             255, 256, 257, 300]
+             255, 256, 257, 300, 512, 777, 1040]
 
 
 def _dev(torch, x, offset):
