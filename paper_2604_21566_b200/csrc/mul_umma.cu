@@ -160,62 +160,13 @@ inline UmmaPlan umma_plan(int m) {
 __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ out, uint64_t* __restrict__ carry_words,
                                                      uint64_t* __restrict__ part_lo, uint32_t* __restrict__ part_hi,
                                                      const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                                                     const UmmaPlan G) {
+                                                     const UmmaPlan G, unsigned items,
+                                                     unsigned* __restrict__ next_item) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t full[kSlots], empty[kSlots], done;
     __shared__ uint32_t tbase_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int m = G.m, na = G.na, nb = G.na, n = 8 * m;
-    const int split = int(blockIdx.x % unsigned(G.splits));
-    const int C0 = int((blockIdx.x / unsigned(G.splits)) % unsigned(G.tiles)) * G.nt;
-    const size_t pair = blockIdx.x / unsigned(G.splits * G.tiles);
-    // this item's b-window steps, the a-chunks they pair with, the b bytes they read
-    const int s_lo = split * G.ss, s_hi = s_lo + G.ss < nb + 1 ? s_lo + G.ss : nb + 1;
-    const int j_lo = C0 - s_hi + 1 > 0 ? C0 - s_hi + 1 : 0;
-    const int j_hi = C0 + G.nt - s_lo < na ? C0 + G.nt - s_lo : na;
-    const int b_lo = 128 * s_lo - 128 > 0 ? 128 * s_lo - 128 : 0;
-    const int b_hi = 128 * s_hi < n ? 128 * s_hi : n;
-    const int nbs = b_hi - b_lo;  // staged b bytes (a multiple of 128)
-    uint8_t* bh = sm;                       // 8 arrays [p][kk], rows J - j_lo + kPadJ of 16 B
-    uint8_t* ring = sm + G.off_ring;        // kSlots slots x kTC core matrices
-    uint8_t* bs = sm + G.off_b;             // kPadB zeros | b[b_lo, b_hi) | kPadB zeros
-    const uint4* ga = reinterpret_cast<const uint4*>(a + pair * size_t(m));
-    const uint4* gb = reinterpret_cast<const uint4*>(b + pair * size_t(m) + size_t(b_lo / 8));
-
-    // a -> B arrays: 16-byte segment g of the operand is half (g & 1) of block 4J + p,
-    // J = g / 8, p = (g / 2) % 4; stored byte-reversed as row J of array (p, kk = 1 - half).
-    const int g_lo = 8 * j_lo, g_hi = j_hi > j_lo ? 8 * j_hi : g_lo;
-    for (int g0 = g_lo + tid; g0 < g_hi; g0 += 4 * kThreads) {  // 4 loads in flight
-        uint4 w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < g_hi ? __ldg(ga + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int g = g0 + u * kThreads;
-            if (g >= g_hi) break;
-            const int J = g >> 3, p = (g >> 1) & 3, kk = 1 - (g & 1);
-            *reinterpret_cast<uint4*>(bh + (2 * p + kk) * G.la + (J - j_lo + kPadJ) * 16) =
-                make_uint4(bswap32(w[u].w), bswap32(w[u].z), bswap32(w[u].y), bswap32(w[u].x));
-        }
-    }
-    const int rows = j_hi > j_lo ? j_hi - j_lo : 0;
-    for (int e = tid; e < 8 * 2 * kPadJ; e += kThreads) {  // zero chunks on both sides
-        const int arr = e / (2 * kPadJ), q = e % (2 * kPadJ);
-        const int row = q < kPadJ ? q : rows + q;
-        *reinterpret_cast<uint4*>(bh + arr * G.la + row * 16) = make_uint4(0, 0, 0, 0);
-    }
-    for (int g0 = tid; g0 < nbs / 16; g0 += 4 * kThreads) {
-        uint4 w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < nbs / 16 ? __ldg(gb + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (g0 + u * kThreads < nbs / 16) reinterpret_cast<uint4*>(bs + kPadB)[g0 + u * kThreads] = w[u];
-    }
-    for (int e = tid; e < 2 * kPadB / 16; e += kThreads) {
-        const int off = e < kPadB / 16 ? e * 16 : kPadB + nbs + (e - kPadB / 16) * 16;
-        *reinterpret_cast<uint4*>(bs + off) = make_uint4(0, 0, 0, 0);
-    }
     // barriers: full[q] (4 builder warps arrive), empty[q] (MMA commit), done (last commit)
     if (tid == 0) {
         for (int q = 0; q < kSlots; ++q) {
@@ -235,156 +186,220 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm = tbase_sh;
-    if (warp < 4) {  // zero the accumulator tile (every MMA accumulates)
-        const uint32_t z = 0;
-        for (int c = 0; c < G.nt; c += 16)
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                    tm + (uint32_t(warp * 32) << 16) + uint32_t(c)),
-                "r"(z)
-                : "memory");
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    unsigned it = 0;   // items done by this CTA (phase of `done`)
+    unsigned qg = 0;   // ring blocks issued so far (phases of full / empty)
+    // items: blockIdx.x first, then taken from a global counter (dynamic balance across SMs)
+    __shared__ unsigned item_sh;
+    for (unsigned item = blockIdx.x; item < items; ++it) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int split = int(item % unsigned(G.splits));
+        const int C0 = int((item / unsigned(G.splits)) % unsigned(G.tiles)) * G.nt;
+        const size_t pair = item / unsigned(G.splits * G.tiles);
+        // this item's b-window steps, the a-chunks they pair with, the b bytes they read
+        const int s_lo = split * G.ss, s_hi = s_lo + G.ss < nb + 1 ? s_lo + G.ss : nb + 1;
+        const int j_lo = C0 - s_hi + 1 > 0 ? C0 - s_hi + 1 : 0;
+        const int j_hi = C0 + G.nt - s_lo < na ? C0 + G.nt - s_lo : na;
+        const int b_lo = 128 * s_lo - 128 > 0 ? 128 * s_lo - 128 : 0;
+        const int b_hi = 128 * s_hi < n ? 128 * s_hi : n;
+        const int nbs = b_hi - b_lo;  // staged b bytes (a multiple of 128)
+        uint8_t* bh = sm;                       // 8 arrays [p][kk], rows J - j_lo + kPadJ of 16 B
+        uint8_t* ring = sm + G.off_ring;        // kSlots slots x kTC core matrices
+        uint8_t* bs = sm + G.off_b;             // kPadB zeros | b[b_lo, b_hi) | kPadB zeros
+        const uint4* ga = reinterpret_cast<const uint4*>(a + pair * size_t(m));
+        const uint4* gb = reinterpret_cast<const uint4*>(b + pair * size_t(m) + size_t(b_lo / 8));
 
-    const int nblocks = (s_hi - s_lo + kSB - 1) / kSB;  // s = s_lo .. s_hi-1 in blocks of kSB steps
-    if (warp < 4) {
-        // builders: ring slot q % kSlots <- core matrices t = 16 s0 - 12 + (row / 8), row rr = row % 8
-        const uint32_t* bw = reinterpret_cast<const uint32_t*>(bs);
-        for (int q = 0; q < nblocks; ++q) {
-            const int slot = q % kSlots, s0 = s_lo + q * kSB;
-            if (q >= kSlots) mbar_sleep(smem_u32(&empty[slot]), uint32_t(q / kSlots - 1) & 1u);
-            uint8_t* rs = ring + slot * (kTC * 128);
-            const int t0 = 16 * s0 - 12;
+        // a -> B arrays: 16-byte segment g of the operand is half (g & 1) of block 4J + p,
+        // J = g / 8, p = (g / 2) % 4; stored byte-reversed as row J of array (p, kk = 1 - half).
+        const int g_lo = 8 * j_lo, g_hi = j_hi > j_lo ? 8 * j_hi : g_lo;
+        for (int g0 = g_lo + tid; g0 < g_hi; g0 += 4 * kThreads) {  // 4 loads in flight
+            uint4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < g_hi ? __ldg(ga + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int g = g0 + u * kThreads;
+                if (g >= g_hi) break;
+                const int J = g >> 3, p = (g >> 1) & 3, kk = 1 - (g & 1);
+                *reinterpret_cast<uint4*>(bh + (2 * p + kk) * G.la + (J - j_lo + kPadJ) * 16) =
+                    make_uint4(bswap32(w[u].w), bswap32(w[u].z), bswap32(w[u].y), bswap32(w[u].x));
+            }
+        }
+        const int rows = j_hi > j_lo ? j_hi - j_lo : 0;
+        for (int e = tid; e < 8 * 2 * kPadJ; e += kThreads) {  // zero chunks on both sides
+            const int arr = e / (2 * kPadJ), q = e % (2 * kPadJ);
+            const int row = q < kPadJ ? q : rows + q;
+            *reinterpret_cast<uint4*>(bh + arr * G.la + row * 16) = make_uint4(0, 0, 0, 0);
+        }
+        for (int g0 = tid; g0 < nbs / 16; g0 += 4 * kThreads) {
+            uint4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = g0 + u * kThreads < nbs / 16 ? __ldg(gb + g0 + u * kThreads) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (g0 + u * kThreads < nbs / 16) reinterpret_cast<uint4*>(bs + kPadB)[g0 + u * kThreads] = w[u];
+        }
+        for (int e = tid; e < 2 * kPadB / 16; e += kThreads) {
+            const int off = e < kPadB / 16 ? e * 16 : kPadB + nbs + (e - kPadB / 16) * 16;
+            *reinterpret_cast<uint4*>(bs + off) = make_uint4(0, 0, 0, 0);
+        }
+        if (warp < 4) {  // zero the accumulator tile (every MMA accumulates)
+            const uint32_t z = 0;
+            for (int c = 0; c < G.nt; c += 16)
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                        tm + (uint32_t(warp * 32) << 16) + uint32_t(c)),
+                    "r"(z)
+                    : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+
+        const int nblocks = (s_hi - s_lo + kSB - 1) / kSB;  // s = s_lo .. s_hi-1 in blocks of kSB steps
+        if (warp < 4) {
+            // builders: ring slot q % kSlots <- core matrices t = 16 s0 - 12 + (row / 8), row rr = row % 8
+            const uint32_t* bw = reinterpret_cast<const uint32_t*>(bs);
+            for (int q = 0; q < nblocks; ++q) {
+                const unsigned qq = qg + unsigned(q);
+                const int slot = int(qq % kSlots), s0 = s_lo + q * kSB;
+                if (qq >= unsigned(kSlots)) mbar_sleep(smem_u32(&empty[slot]), (qq / kSlots - 1) & 1u);
+                uint8_t* rs = ring + slot * (kTC * 128);
+                const int t0 = 16 * s0 - 12;
 #pragma unroll 2
-            for (int row = tid; row < kTC * 8; row += kWorkers) {
-                const int o = 8 * (t0 + (row >> 3)) + (row & 7) - 31 - b_lo + kPadB;  // byte offset in bs
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (o + 16 > kPadB && o < kPadB + nbs) {
-                    const int w0 = o >> 2, sh = (o & 3) * 8;
-                    const uint32_t x0 = bw[w0], x1 = bw[w0 + 1], x2 = bw[w0 + 2], x3 = bw[w0 + 3], x4 = bw[w0 + 4];
-                    v = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh),
-                                   __funnelshift_r(x2, x3, sh), __funnelshift_r(x3, x4, sh));
+                for (int row = tid; row < kTC * 8; row += kWorkers) {
+                    const int o = 8 * (t0 + (row >> 3)) + (row & 7) - 31 - b_lo + kPadB;  // byte offset in bs
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (o + 16 > kPadB && o < kPadB + nbs) {
+                        const int w0 = o >> 2, sh = (o & 3) * 8;
+                        const uint32_t x0 = bw[w0], x1 = bw[w0 + 1], x2 = bw[w0 + 2], x3 = bw[w0 + 3], x4 = bw[w0 + 4];
+                        v = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh),
+                                       __funnelshift_r(x2, x3, sh), __funnelshift_r(x3, x4, sh));
+                    }
+                    *reinterpret_cast<uint4*>(rs + row * 16) = v;
                 }
-                *reinterpret_cast<uint4*>(rs + row * 16) = v;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[slot])) : "memory");
+        } else {
+            // issuer: warp 4 (converged, one elected lane issues), MMAs of a slot once its 4
+            // builder warps arrived
+            // B row of chunk J is J - j_lo + kPadJ (issue_block adds J)
+            const uint64_t b_p0 = sdesc(smem_u32(bh) + kPadJ * 16, G.la, 128) - uint64_t(j_lo);
+            const uint64_t b_dp = uint64_t(2 * G.la / 16);
+            for (int q = 0; q < nblocks; ++q) {
+                const unsigned qq = qg + unsigned(q);
+                const int slot = int(qq % kSlots), s0 = s_lo + q * kSB;
+                mbar_wait(smem_u32(&full[slot]), (qq / kSlots) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                issue_block(smem_u32(ring + slot * (kTC * 128)), s0, s0 + kSB < s_hi ? s0 + kSB : s_hi, C0, na, G.nt, tm,
+                            b_p0, b_dp);
+                commit_elect(smem_u32(&empty[slot]));
+                if (q == nblocks - 1) commit_elect(smem_u32(&done));
+            }
         }
-    } else {
-        // issuer: warp 4 (converged, one elected lane issues), MMAs of a slot once its 4
-        // builder warps arrived
-        // B row of chunk J is J - j_lo + kPadJ (issue_block adds J)
-        const uint64_t b_p0 = sdesc(smem_u32(bh) + kPadJ * 16, G.la, 128) - uint64_t(j_lo);
-        const uint64_t b_dp = uint64_t(2 * G.la / 16);
-        for (int q = 0; q < nblocks; ++q) {
-            const int slot = q % kSlots, s0 = s_lo + q * kSB;
-            mbar_wait(smem_u32(&full[slot]), uint32_t(q / kSlots) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            issue_block(smem_u32(ring + slot * (kTC * 128)), s0, s0 + kSB < s_hi ? s0 + kSB : s_hi, C0, na, G.nt, tm,
-                        b_p0, b_dp);
-            commit_elect(smem_u32(q == nblocks - 1 ? &done : &empty[slot]));
-        }
-    }
-    mbar_sleep(smem_u32(&done), 0u);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        qg += unsigned(nblocks);
+        mbar_sleep(smem_u32(&done), it & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    // Epilogue (all operand shared memory is free now).
-    // E1: per 16 columns, warp w's lanes hold byte 32w + lane of each output chunk; a
-    // per-warp transpose through shared memory gives each thread all 8 byte columns of
-    // one limb: V = sum_u S[u] 2^(8u) = lo + hi 2^64 (hi < 2^25), kept as LO / HI.
-    const int xend = 2 * na - C0 < G.nt ? 2 * na - C0 : G.nt;  // columns inside the product
-    const int xe16 = (xend + 15) & ~15;                         // + zero columns up to 16
-    const int nl = 16 * xe16;                                   // limbs resolved (multiple of 256)
-    uint64_t* LO = reinterpret_cast<uint64_t*>(sm);
-    uint32_t* HI = reinterpret_cast<uint32_t*>(sm + 8 * 16 * G.nt);
-    uint32_t* Tw = reinterpret_cast<uint32_t*>(sm + 12 * 16 * G.nt) + warp * (16 * 32);
-    for (int c0 = 0; c0 < (warp < 4 ? xe16 : 0); c0 += 16) {
-        uint32_t v[16];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(tm + (uint32_t(warp * 32) << 16) + uint32_t(c0)));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // Epilogue (all operand shared memory is free now).
+        // E1: per 16 columns, warp w's lanes hold byte 32w + lane of each output chunk; a
+        // per-warp transpose through shared memory gives each thread all 8 byte columns of
+        // one limb: V = sum_u S[u] 2^(8u) = lo + hi 2^64 (hi < 2^25), kept as LO / HI.
+        const int xend = 2 * na - C0 < G.nt ? 2 * na - C0 : G.nt;  // columns inside the product
+        const int xe16 = (xend + 15) & ~15;                         // + zero columns up to 16
+        const int nl = 16 * xe16;                                   // limbs resolved (multiple of 256)
+        uint64_t* LO = reinterpret_cast<uint64_t*>(sm);
+        uint32_t* HI = reinterpret_cast<uint32_t*>(sm + 8 * 16 * G.nt);
+        uint32_t* Tw = reinterpret_cast<uint32_t*>(sm + 12 * 16 * G.nt) + warp * (16 * 32);
+        for (int c0 = 0; c0 < (warp < 4 ? xe16 : 0); c0 += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(tm + (uint32_t(warp * 32) << 16) + uint32_t(c0)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 16; ++j) Tw[j * 32 + lane] = v[j];
-        __syncwarp();
+            for (int j = 0; j < 16; ++j) Tw[j * 32 + lane] = v[j];
+            __syncwarp();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int task = lane + 32 * h, c = task >> 2, u = task & 3;
-            {
-                const uint4 q0 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u);
-                const uint4 q1 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u + 4);
-                const uint64_t x = uint64_t(q0.x) + (uint64_t(q0.y) << 8) + (uint64_t(q0.z) << 16) + (uint64_t(q0.w) << 24);
-                const uint64_t y = uint64_t(q1.x) + (uint64_t(q1.y) << 8) + (uint64_t(q1.z) << 16) + (uint64_t(q1.w) << 24);
-                const uint64_t lo = x + (y << 32);
-                const int L = 16 * (c0 + c) + 4 * warp + u;
-                LO[L] = lo;
-                HI[L] = uint32_t(y >> 32) + (lo < x ? 1u : 0u);
-            }
-        }
-        __syncwarp();
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (G.splits > 1) {
-        // partial limbs of this s-range: a second kernel adds the splits and the carries
-        const size_t base = (pair * size_t(G.splits) + size_t(split)) * size_t(2 * m) + size_t(16 * C0);
-        for (int e = tid; e < 16 * xend; e += kThreads) {
-            part_lo[base + e] = LO[e];
-            part_hi[base + e] = HI[e];
-        }
-    } else {
-        // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
-        // add kernel's generate / propagate algebra. Warp w owns limbs [w nl/4, (w+1) nl/4) in
-        // rounds of 32 consecutive limbs (lane = limb, conflict-free): pass 1 folds the rounds
-        // into the warp's (carry-out, all-propagate), pass 2 applies the carries.
-        {
-            const int per_warp = nl / 4, rounds = per_warp / 32;  // nl = 16 * xe16 -> rounds >= 2
-            const int base = warp * per_warp;
-            __shared__ uint32_t wagg[4][2];
-            if (warp < 4) {
-                uint32_t Gw = 0, Pw = 1;
-                for (int r = 0; r < rounds; ++r) {
-                    const int L = base + 32 * r + lane;
-                    const uint64_t lo = LO[L];
-                    const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
-                    const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
-                    const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
-                    Gw = go | ((pp == 0xffffffffu) & Gw);
-                    Pw &= pp == 0xffffffffu;
+            for (int h = 0; h < 2; ++h) {
+                const int task = lane + 32 * h, c = task >> 2, u = task & 3;
+                {
+                    const uint4 q0 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u);
+                    const uint4 q1 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u + 4);
+                    const uint64_t x = uint64_t(q0.x) + (uint64_t(q0.y) << 8) + (uint64_t(q0.z) << 16) + (uint64_t(q0.w) << 24);
+                    const uint64_t y = uint64_t(q1.x) + (uint64_t(q1.y) << 8) + (uint64_t(q1.z) << 16) + (uint64_t(q1.w) << 24);
+                    const uint64_t lo = x + (y << 32);
+                    const int L = 16 * (c0 + c) + 4 * warp + u;
+                    LO[L] = lo;
+                    HI[L] = uint32_t(y >> 32) + (lo < x ? 1u : 0u);
                 }
-                if (lane == 0) {
-                    wagg[warp][0] = Gw;
-                    wagg[warp][1] = Pw;
+            }
+            __syncwarp();
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (G.splits > 1) {
+            // partial limbs of this s-range: a second kernel adds the splits and the carries
+            const size_t base = (pair * size_t(G.splits) + size_t(split)) * size_t(2 * m) + size_t(16 * C0);
+            for (int e = tid; e < 16 * xend; e += kThreads) {
+                part_lo[base + e] = LO[e];
+                part_hi[base + e] = HI[e];
+            }
+        } else {
+            // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
+            // add kernel's generate / propagate algebra. Warp w owns limbs [w nl/4, (w+1) nl/4) in
+            // rounds of 32 consecutive limbs (lane = limb, conflict-free): pass 1 folds the rounds
+            // into the warp's (carry-out, all-propagate), pass 2 applies the carries.
+            {
+                const int per_warp = nl / 4, rounds = per_warp / 32;  // nl = 16 * xe16 -> rounds >= 2
+                const int base = warp * per_warp;
+                __shared__ uint32_t wagg[4][2];
+                if (warp < 4) {
+                    uint32_t Gw = 0, Pw = 1;
+                    for (int r = 0; r < rounds; ++r) {
+                        const int L = base + 32 * r + lane;
+                        const uint64_t lo = LO[L];
+                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                        const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                        const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
+                        Gw = go | ((pp == 0xffffffffu) & Gw);
+                        Pw &= pp == 0xffffffffu;
+                    }
+                    if (lane == 0) {
+                        wagg[warp][0] = Gw;
+                        wagg[warp][1] = Pw;
+                    }
+                }
+                __syncthreads();
+                if (warp < 4) {
+                    uint32_t c = 0;
+                    for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
+                    for (int r = 0; r < rounds; ++r) {
+                        const int L = base + 32 * r + lane;
+                        const uint64_t lo = LO[L];
+                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                        const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
+                        const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
+                        LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
+                        c = uint32_t(y >> 32);
+                    }
+                    if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
+                        carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
                 }
             }
             __syncthreads();
-            if (warp < 4) {
-                uint32_t c = 0;
-                for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
-                for (int r = 0; r < rounds; ++r) {
-                    const int L = base + 32 * r + lane;
-                    const uint64_t lo = LO[L];
-                    const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
-                    const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
-                    const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
-                    LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
-                    c = uint32_t(y >> 32);
-                }
-                if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
-                    carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
+            {
+                uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
+                for (int e = tid; e < 8 * xend; e += kThreads)
+                    reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
             }
         }
-        __syncthreads();
-        {
-            uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
-            for (int e = tid; e < 8 * xend; e += kThreads)
-                reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
-        }
+        if (tid == 0) item_sh = next_item != nullptr ? gridDim.x + atomicAdd(next_item, 1u) : items;
+        __syncthreads();  // epilogue done with shared memory and TMEM before the next item stages
+        item = item_sh;
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -510,14 +525,44 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     const uint32_t smem = G.smem > floor_smem ? G.smem : floor_smem;
     // the largest dynamic shared memory any size needs, set once per process (not a stream
     // operation, so launches stay capturable into CUDA graphs)
-    static const cudaError_t attr = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         int(umma_max_smem()));
+    static const cudaError_t attr = [] {
+        cudaError_t r = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(umma_max_smem()));
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(k_mul_umma, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     int(cudaSharedmemCarveoutMaxShared));
+        return r;
+    }();
     if (e == cudaSuccess) e = attr;
+    // persistent: as many CTAs as fit (TMEM and shared memory), each looping over items
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+    }
+    // CTAs per SM: TMEM columns and shared memory (228 KB per SM, 1 KB reserved per CTA plus
+    // the static barriers); cudaOccupancyMaxActiveBlocksPerMultiprocessor reports 1 here (it
+    // assumes the carveout of the largest dynamic size set on the function).
+    int occ = int((228 * 1024) / (smem + 2048));
+    if (occ > per_sm) occ = per_sm;
+    if (occ < 1) occ = 1;
+    // DOTG_UMMA_PERSIST=P > 0: P CTAs per SM slot, items taken from a global counter (same
+    // speed as one CTA per item, measured: profiles/r02_umma_wide_variants.txt); default 0
+    static const int persist = std::getenv("DOTG_UMMA_PERSIST") ? std::atoi(std::getenv("DOTG_UMMA_PERSIST")) : 0;
+    const size_t cap = persist > 0 ? size_t(sms) * size_t(occ) * size_t(persist) : items;
+    const size_t grid = items < cap ? items : cap;
+    unsigned* ctr = nullptr;
+    if (e == cudaSuccess && grid < items) {
+        e = cudaMallocAsync(&ctr, sizeof(unsigned), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(ctr, 0, sizeof(unsigned), st);
+    }
     if (e == cudaSuccess) {
-        k_mul_umma<<<unsigned(items), kThreads, smem, st>>>(out, cw, plo, phi, a, b, G);
+        k_mul_umma<<<unsigned(grid), kThreads, smem, st>>>(out, cw, plo, phi, a, b, G, unsigned(items), ctr);
         count_launch();
         e = cudaGetLastError();
     }
+    if (ctr != nullptr) cudaFreeAsync(ctr, st);
     if (e == cudaSuccess && G.splits > 1) {
         k_umma_reduce<<<unsigned((batch * 2 * m + 255) / 256), 256, 0, st>>>(out, nxt, plo, phi, m, batch, G.splits);
         count_launch();
