@@ -1007,13 +1007,31 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
         nrot = rotations(2 * nb * m * 8) if world > 1 else 1
         rot = [(fa[lo:hi].clone(), fb[lo:hi].clone()) for _ in range(nrot)] if world > 1 else [(fa, fb)]
         outs = [torch.empty((nb, 2 * m), dtype=torch.int64, device="cuda") for _ in rot]
-        calls = [make_rotating([L.mul(o, a_, b_, m, nb) for o, (a_, b_) in zip(outs, rot)])]
+        # one CUDA-graph replay of the captured dotg_mul_batch launch per step (as the headline)
+        replays, mgraphs = [], []
+        for o, (a_, b_) in zip(outs, rot):
+            fn, _, g = capture_graph(torch, dg, lib, stream, lambda Lc, o=o, a_=a_, b_=b_: Lc.mul(o, a_, b_, m, nb))
+            if fn is None:
+                replays = None
+                break
+            replays.append(fn)
+            mgraphs.append(g)
+        calls = [make_rotating(replays if replays else [L.mul(o, a_, b_, m, nb) for o, (a_, b_) in zip(outs, rot)])]
         ms, per = timed_steps(torch, dd, world, stream, calls, steps, warm)
-        pairs_s = nb / (per[0] * 1e-3)
+        # the kernel's launch duration with launches back to back (8 per graph over rotating
+        # sets, events on the stream); the per-call event pair above also times the idle gap
+        # before each replay
+        b2b = per_launch_us(torch, dg, lib, stream,
+                            lambda Lc: [Lc.mul(o, a_, b_, m, nb) for o, (a_, b_) in zip(outs, rot)] * 2)
+        launch_ms = b2b * 1e-3 if b2b else per[0]
+        pairs_s = nb / (launch_ms * 1e-3)
         prods = 4 * m * m
         o, (a, b) = outs[0], rot[0]
         res = {"metric": f"{64 * m}-bit mul products/s (pairs/s)", "value": Bn / (ms * 1e-3),
-               "unit": "pairs/s", "kernel_pairs_s": pairs_s, "kernel_us": per[0] * 1e3,
+               "unit": "pairs/s", "kernel_pairs_s": pairs_s, "kernel_us": launch_ms * 1e3,
+               "kernel_us_event_per_call": per[0] * 1e3,
+               "timing": "value: one CUDA-graph replay of the launch per step; kernel_us: launches back to back "
+                         "in one graph over rotating inputs, events on the stream",
                "u32_products_per_s": pairs_s * prods,
                "imad_roofline_u32_products_per_s": imad_peak_pps,
                "frac_imad": pairs_s * prods / imad_peak_pps,
@@ -1021,7 +1039,7 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                "note": "roofline = SMs x 32 IMAD.WIDE.U32/clk/SM (measured, tools/imad_peak.cu) x max SM clock"}
         roof = {"bound": "imad", "achieved": pairs_s * prods / 1e12, "peak": imad_peak_pps / 1e12,
                 "unit": "T u32-products/s", "frac": pairs_s * prods / imad_peak_pps, "traffic": None,
-                "algorithmic_units_per_launch": f"{nb} pairs x {prods} u32 products", "launch_us_avg": per[0] * 1e3}
+                "algorithmic_units_per_launch": f"{nb} pairs x {prods} u32 products", "launch_us_avg": launch_ms * 1e3}
         if m in IMMA_ROUTE_M:
             # tensor-pipe kernel (k_mul_imma): radix-2^8 products, (8m)^2 byte-MACs per pair
             imma_peak = sms * IMMA_U8_MACS_PER_CLK_SM * sm_max * 1e6

@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <cstdlib>
 
 #include "device.cuh"
@@ -454,10 +455,8 @@ __device__ __forceinline__ uint32_t absdiff16(const uint32_t (&X)[kK], const uin
 // IL = true: the interleaved [m][batch] layout (limb i of pair p at i * batch + p), every
 // load / store coalesced across the warp's 32 consecutive pairs.
 template <bool IL>
-__global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint64_t* out, const uint64_t* a,
-                                                                           const uint64_t* b, size_t batch) {
-    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (pidx >= batch) return;
+__device__ __forceinline__ void kara16_pair(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t batch,
+                                            size_t pidx) {
     // output limbs [l0, l0 + 4) of this pair
     auto put4 = [&](size_t l0, const uint64_t (&o)[4]) {
         if constexpr (IL) {
@@ -540,6 +539,14 @@ __global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint
         for (int k = 0; k < 4; ++k) o[k] = uint64_t(r[2 * k]) | (uint64_t(r[2 * k + 1]) << 32);
         put4(size_t(8 + 4 * q), o);
     }
+}
+
+template <bool IL>
+__global__ void __launch_bounds__(DOTG_K16_TPB, DOTG_K16_MINB) k_mul_kara16(uint64_t* out, const uint64_t* a,
+                                                                           const uint64_t* b, size_t batch) {
+    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (pidx >= batch) return;
+    kara16_pair<IL>(out, a, b, batch, pidx);
 }
 
 // ---------------------------------------------------------------------------
