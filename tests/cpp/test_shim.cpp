@@ -347,7 +347,7 @@ int main() {
     });
     run("generic product matches the oracle across sizes", [] {  // test_mul.cpp:345-359
         std::mt19937_64 rng(23);
-        const std::size_t sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 33, 48, 64};
+        const std::size_t sizes[] = {1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 33, 48, 64, 256, 1000, 4096};
         for (const std::size_t m : sizes) {
             for (int iter = 0; iter < 12; ++iter) {
                 const Limbs a = uniform_limbs(rng, m), b = uniform_limbs(rng, m);

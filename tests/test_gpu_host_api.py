@@ -75,7 +75,7 @@ def test_round_trip_and_mul(cuda, oracle):
         wide = np.append(s.limbs, np.uint64(s.flag))
         back = dg.dot_sub_words(wide, np.append(b, np.uint64(0)))
         assert back.flag == 0 and np.array_equal(back.limbs[:m], a) and back.limbs[m] == 0
-    for m in (1, 2, 7, 16, 64):
+    for m in (1, 2, 7, 16, 64, 300, 1024, 5000):  # up to the tcgen05 routes (direct and split)
         a, b = uniform(rng, m), uniform(rng, m)
         p = dg.dot_mul_words(a, b)
         want = oracle.mul(a, b)
@@ -107,6 +107,11 @@ def test_batch_host_pipeline(cuda, oracle):
     assert np.array_equal(out, want) and np.array_equal(fl, wf)
     a, b = uniform(rng, (30000, 16)), uniform(rng, (30000, 16))
     assert np.array_equal(dg.mul_batch_host(a, b), oracle.mul_batch(a, b))
+    for m, n in ((1024, 40), (8192, 3)):  # tcgen05 direct / split routes through the host pipeline
+        a, b = spiky(rng, (n, m)), spiky(rng, (n, m))
+        a[0] = MAX
+        b[0] = MAX
+        assert np.array_equal(dg.mul_batch_host(a, b), oracle.mul_batch(a, b)), m
 
 
 def test_grouped_host_pipeline(cuda, oracle):
