@@ -68,13 +68,13 @@ for m in (1, 3, 4, 16, 64, 100, 256, 512, 9000):
     check_addsub(m, 5 if m < 9000 else 2)
 for m in (4, 64, 200, 300, 700):
     check_addsub(m, 40, "interleaved")
-for m in (1, 4, 5, 8, 12, 16, 24, 33, 64, 96, 128, 200):
-    check_mul(m, 9)
+for m in (1, 4, 5, 8, 12, 16, 24, 33, 64, 96, 128, 200, 256, 1000, 4096, 5000):  # ... tcgen05 direct / split
+    check_mul(m, 9 if m <= 1000 else 2)
 for m in (8, 16):
     check_mul(m, 9, route="imma")
 for m in (32, 64):
     check_mul(m, 9, route="imad")
-for m in (16, 40):
+for m in (16, 40, 300):
     check_mul(m, 33, "interleaved")
 x, y = rand(70000), rand(70000)
 o, c = dg.add_words(dev(x), dev(y))
