@@ -38,7 +38,7 @@ def main():
                 "instructions": sum(base.values()),
                 "by_opcode": dict(base.most_common(20)),
                 "imad_wide": sum(v for k, v in full.items() if k.startswith("IMAD.WIDE")),
-                "tensor": {k: v for k, v in full.items() if k.startswith(("IMMA", "HMMA", "UTC"))},
+                "tensor": {k: v for k, v in full.items() if k.startswith(("IMMA", "HMMA", "UTC", "LDTM", "STTM"))},
                 "tcgen05_present": any(k.startswith(("UTC", "LDTM", "STTM")) for k in full),
                 "bulk_copy_mbarrier": {k: v for k, v in full.items() if k.startswith(("UBLKCP", "SYNCS"))},
                 "vector_256b_global": sum(v for k, v in full.items() if k.startswith(("LDG.E.ENL2.256", "STG.E.ENL2.256"))
