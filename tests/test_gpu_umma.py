@@ -93,3 +93,27 @@ def test_umma_misaligned_rows(cuda, oracle):
     db[1:] = torch.from_numpy(b.reshape(-1).view(np.int64)).cuda()
     got = dg.mul_batch(da[1:].view(n, m), db[1:].view(n, m))
     assert np.array_equal(got.cpu().numpy().view(np.uint64), oracle.mul_batch(a, b))
+
+
+def test_umma_route_taken(cuda):
+    """The tcgen05 route is the one that runs: one launch for a direct product, two with
+    the tile-carry pass (m = 4096), a few for split items (reduce + the batched add's
+    passes) - the Karatsuba route it replaced issues tens of launches per call."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    for m, want in ((256, 1), (1024, 1), (4096, 2), (8192, 6)):
+        a = torch.ones((2, m), dtype=torch.int64, device="cuda")
+        out = torch.empty((2, 2 * m), dtype=torch.int64, device="cuda")
+        dg.mul_batch(a, a, out=out)  # warm (pool, attributes)
+        torch.cuda.synchronize()
+        n0 = dg.kernel_launches()
+        dg.mul_batch(a, a, out=out)
+        torch.cuda.synchronize()
+        n = dg.kernel_launches() - n0
+        assert (n == want) if m <= 4096 else (2 <= n <= want), (m, n)
+        # (1 + 2^64 + ... ) squared pattern: the all-ones-limb value 1 per limb
+        got = out.cpu().numpy().view(np.uint64)
+        exp = np.array([min(i + 1, 2 * m - 1 - i) for i in range(2 * m)], np.uint64)
+        exp[-1] = 0
+        assert np.array_equal(got[0], exp), m
