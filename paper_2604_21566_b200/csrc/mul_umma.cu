@@ -136,7 +136,9 @@ struct UmmaPlan {
     uint32_t off_ring, off_b, smem;
 };
 
-inline UmmaPlan umma_plan(int m) {
+// min_splits > 1 splits the s-range further (more items for a batch too small to fill the
+// SMs); every split keeps >= 32 steps.
+inline UmmaPlan umma_plan(int m, int min_splits = 1) {
     UmmaPlan g{};
     g.m = m;
     g.na = m / 16;
@@ -145,6 +147,7 @@ inline UmmaPlan umma_plan(int m) {
     g.cols = g.nt <= 32 ? 32 : (g.nt <= 64 ? 64 : (g.nt <= 128 ? 128 : 256));
     const int steps = g.na + 1;
     g.splits = g.na <= 256 ? 1 : (steps + 127) / 128;
+    if (min_splits > g.splits) g.splits = min_splits < steps / 32 ? min_splits : (steps / 32 > g.splits ? steps / 32 : g.splits);
     g.ss = (steps + g.splits - 1) / g.splits;
     g.jrows = g.splits == 1 ? g.na : (g.na < g.nt + g.ss ? g.na : g.nt + g.ss);
     g.la = uint32_t(g.jrows + 2 * kPadJ) * 16;
@@ -492,7 +495,24 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
                             cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
     if (!(m >= 256 && m <= size_t(kUmmaMaxM) && m % 16 == 0)) return cudaErrorInvalidValue;
-    const UmmaPlan G = umma_plan(int(m));
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+    }
+    // DOTG_UMMA_FILL=1: a batch with fewer (pair, tile) items than CTA slots gets its s-range
+    // split so every SM holds MMA streams. Measured slower in most shapes (the split items'
+    // partial limbs, reduce and batched add cost more than the idle SMs:
+    // profiles/r02_umma_wide_variants.txt), so off by default.
+    static const int fill = std::getenv("DOTG_UMMA_FILL") ? std::atoi(std::getenv("DOTG_UMMA_FILL")) : 0;
+    UmmaPlan G = umma_plan(int(m));
+    {
+        const int per_sm0 = 512 / G.cols < 8 ? 512 / G.cols : 8;
+        const size_t slots = size_t(sms) * size_t(per_sm0);
+        const size_t base = batch * size_t(G.tiles);
+        if (fill && G.splits == 1 && base < slots) G = umma_plan(int(m), int((slots + base - 1) / base));
+    }
     if (G.splits > 1) {  // partial limbs: 12 B per limb per split; keep them under 1 GiB per launch
         const size_t per_pair = size_t(G.splits) * 2 * m * 12 + 2 * m * 8;
         const size_t chunk = (size_t(1) << 30) / per_pair > 0 ? (size_t(1) << 30) / per_pair : 1;
@@ -535,12 +555,6 @@ cudaError_t launch_mul_umma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     }();
     if (e == cudaSuccess) e = attr;
     // persistent: as many CTAs as fit (TMEM and shared memory), each looping over items
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            sms = 148;
-    }
     // CTAs per SM: TMEM columns and shared memory (228 KB per SM, 1 KB reserved per CTA plus
     // the static barriers); cudaOccupancyMaxActiveBlocksPerMultiprocessor reports 1 here (it
     // assumes the carveout of the largest dynamic size set on the function).
