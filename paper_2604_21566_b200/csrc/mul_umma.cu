@@ -3,12 +3,13 @@
 //
 // Same contract as every product kernel here (dot_mul_words, include/dot/mul.hpp:75-76,
 // src/mul.cpp:96-103: all column sums, one deferred carry pass, exactly 2m limbs), for
-// 256 <= m <= 4096 limbs (m % 16 == 0), and the leaves of the Karatsuba route above.
+// 256 <= m <= 65536 limbs (m % 16 == 0; other sizes are row-padded by the caller), and the
+// leaves of the Karatsuba route above (mul_batch.cu, karatsuba.cu).
 //
 // Why tcgen05 here and mma.sync below 256 limbs: a UMMA with M = 128 reads its A tile
 // (4 KB) from shared memory for every instruction, so it only pays when N (the columns
 // sharing that tile) is large. One pair's column product offers N = number of a-chunks
-// of 128 bytes sharing a b-window - 16 for m = 128, 64 for m = 1024, 256 for m = 4096
+// of 128 bytes sharing a b-window - 16 for m = 256, 64 for m = 1024, 256 from m = 4096
 // (tools/umma_i8_probe.cu measured the small-N ceiling).
 //
 // Formulation (bytes; a, b of n = 8m bytes; x = i + j; S[x] = sum a[j] b[i]):
@@ -27,15 +28,22 @@
 //   * A: core matrix (g, kk) of MMA (s, p) is C_t with t = 16 s - 4 p + g + 2 kk, where
 //     C_t[rr][jj] = b[8 t + rr + jj - 31]. So the Hankel tiles of all (s, p) are windows
 //     of ONE array of core matrices (SBO 128 B, LBO 256 B): 16x the b bytes, built per
-//     block of s-steps into a 2-slot ring by funnel shifts from b staged in shared memory.
+//     block of kSB s-steps into a kSlots-slot ring by funnel shifts from b staged in
+//     shared memory.
 //   * B: per (p, kk) an array of 16-byte rows indexed by J (reversed half-blocks), so
 //     shifting the a-chunk range by one (next s) is a 16-byte step of the start address
 //     (SBO 128 B, LBO = the array length).
-// Accumulation: s32 column sums < n * 255^2 < 2^31 for n <= 32 KB (m <= 4096).
+// Roles: warps 0-3 stage the operands and build ring slots (mbarrier `full`), warp 4
+// issues each slot's MMAs from one elected lane and commits them to the slot's `empty`
+// mbarrier. Work items are (pair, D tile, s-range split); m > 4096 splits s into ranges of
+// <= 128 steps.
+// Accumulation: s32 column sums < (b bytes per item) * 255^2 < 2^31 (<= 32 KB of b per item).
 // Epilogue: tcgen05.ld (warp w holds lanes 32w..32w+31 = bytes of 4 limbs per chunk), a
-// 3-step shuffle fold of 8 byte columns per limb into lo64 + hi (< 2^25), lo to `out`,
-// hi to the next limb of a scratch row; one batched add (the add/sub kernel) then
-// resolves every inter-limb carry: product = LO + HI * 2^64.
+// per-warp transpose through shared memory folds 8 byte columns per limb into lo64 + hi
+// (< 2^25); unsplit items resolve every carry of the tile in the CTA (generate / propagate
+// ballots, as the add kernel) and store the limbs; a second tile gets the first tile's
+// carry word from k_umma_tile_carries; split items store partial limbs that
+// k_umma_reduce adds before one batched add resolves LO + HI * 2^64.
 #include <cuda_runtime.h>
 
 #include <cstdint>
