@@ -63,6 +63,8 @@ constexpr int kSlots = 3;            // ring slots
 constexpr int kWorkers = 128;        // builder / epilogue warps 0-3 (TMEM lane quarters)
 constexpr int kThreads = 160;        // + warp 4: the MMA issuer
 constexpr int kUmmaMaxM = 65536;     // largest m the kernel takes (s-range splits above 4096)
+constexpr int kEpiLoBytes = 8 * 18;  // epilogue bytes per D column: 16 limbs (+2 pad) of LO
+constexpr int kEpiHiBytes = 4 * 20;  // and 16 (+4 pad) of HI
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -163,7 +165,7 @@ inline UmmaPlan umma_plan(int m, int min_splits = 1) {
     g.off_ring = 8 * g.la;
     g.off_b = g.off_ring + kSlots * kTC * 128;
     g.smem = g.off_b + uint32_t(g.bmax + 2 * kPadB);
-    const uint32_t epi = uint32_t(12 * 16 * g.nt + 4 * 16 * 32 * 4);  // LO, HI, per-warp transpose
+    const uint32_t epi = uint32_t((kEpiLoBytes + kEpiHiBytes) * g.nt + 4 * 16 * 36 * 4);  // LO, HI, transposes
     if (g.smem < epi) g.smem = epi;
     return g;
 }
@@ -320,9 +322,13 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
         const int xend = 2 * na - C0 < G.nt ? 2 * na - C0 : G.nt;  // columns inside the product
         const int xe16 = (xend + 15) & ~15;                         // + zero columns up to 16
         const int nl = 16 * xe16;                                   // limbs resolved (multiple of 256)
+        // padded layouts keep the transpose and the limb stores free of bank conflicts:
+        // Tw rows of 36 words; limb L of LO at L + 2 (L >> 4), of HI at L + 4 (L >> 4)
         uint64_t* LO = reinterpret_cast<uint64_t*>(sm);
-        uint32_t* HI = reinterpret_cast<uint32_t*>(sm + 8 * 16 * G.nt);
-        uint32_t* Tw = reinterpret_cast<uint32_t*>(sm + 12 * 16 * G.nt) + warp * (16 * 32);
+        uint32_t* HI = reinterpret_cast<uint32_t*>(sm + kEpiLoBytes * G.nt);
+        uint32_t* Tw = reinterpret_cast<uint32_t*>(sm + (kEpiLoBytes + kEpiHiBytes) * G.nt) + warp * (16 * 36);
+        auto lx = [](int L) { return L + 2 * (L >> 4); };
+        auto hx = [](int L) { return L + 4 * (L >> 4); };
         for (int c0 = 0; c0 < (warp < 4 ? xe16 : 0); c0 += 16) {
             uint32_t v[16];
             asm volatile(
@@ -332,20 +338,20 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
                 : "r"(tm + (uint32_t(warp * 32) << 16) + uint32_t(c0)));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 16; ++j) Tw[j * 32 + lane] = v[j];
+            for (int j = 0; j < 16; ++j) Tw[j * 36 + lane] = v[j];
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int task = lane + 32 * h, c = task >> 2, u = task & 3;
+                const int c = (lane & 7) + 8 * h, u = lane >> 3;  // round h: columns 8h..8h+7 x 4 limbs
                 {
-                    const uint4 q0 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u);
-                    const uint4 q1 = *reinterpret_cast<const uint4*>(Tw + c * 32 + 8 * u + 4);
+                    const uint4 q0 = *reinterpret_cast<const uint4*>(Tw + c * 36 + 8 * u);
+                    const uint4 q1 = *reinterpret_cast<const uint4*>(Tw + c * 36 + 8 * u + 4);
                     const uint64_t x = uint64_t(q0.x) + (uint64_t(q0.y) << 8) + (uint64_t(q0.z) << 16) + (uint64_t(q0.w) << 24);
                     const uint64_t y = uint64_t(q1.x) + (uint64_t(q1.y) << 8) + (uint64_t(q1.z) << 16) + (uint64_t(q1.w) << 24);
                     const uint64_t lo = x + (y << 32);
                     const int L = 16 * (c0 + c) + 4 * warp + u;
-                    LO[L] = lo;
-                    HI[L] = uint32_t(y >> 32) + (lo < x ? 1u : 0u);
+                    LO[lx(L)] = lo;
+                    HI[hx(L)] = uint32_t(y >> 32) + (lo < x ? 1u : 0u);
                 }
             }
             __syncwarp();
@@ -356,8 +362,8 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
             // partial limbs of this s-range: a second kernel adds the splits and the carries
             const size_t base = (pair * size_t(G.splits) + size_t(split)) * size_t(2 * m) + size_t(16 * C0);
             for (int e = tid; e < 16 * xend; e += kThreads) {
-                part_lo[base + e] = LO[e];
-                part_hi[base + e] = HI[e];
+                part_lo[base + e] = LO[lx(e)];
+                part_hi[base + e] = HI[hx(e)];
             }
         } else {
             // E2: the tile's limbs = LO + HI shifted one limb, carries resolved in the CTA with the
@@ -372,8 +378,8 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
                     uint32_t Gw = 0, Pw = 1;
                     for (int r = 0; r < rounds; ++r) {
                         const int L = base + 32 * r + lane;
-                        const uint64_t lo = LO[L];
-                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                        const uint64_t lo = LO[lx(L)];
+                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[hx(L - 1)]) : 0ull);
                         const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
                         const uint32_t go = uint32_t(((uint64_t(g) << 1) + pp) >> 32);  // round carry-out, carry-in 0
                         Gw = go | ((pp == 0xffffffffu) & Gw);
@@ -390,22 +396,22 @@ __global__ void __launch_bounds__(kThreads) k_mul_umma(uint64_t* __restrict__ ou
                     for (int w = 0; w < warp; ++w) c = wagg[w][0] | (wagg[w][1] & c);
                     for (int r = 0; r < rounds; ++r) {
                         const int L = base + 32 * r + lane;
-                        const uint64_t lo = LO[L];
-                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[L - 1]) : 0ull);
+                        const uint64_t lo = LO[lx(L)];
+                        const uint64_t sv = lo + (L > 0 ? uint64_t(HI[hx(L - 1)]) : 0ull);
                         const uint32_t g = __ballot_sync(0xffffffffu, sv < lo), pp = __ballot_sync(0xffffffffu, sv == ~0ull);
                         const uint64_t y = ((uint64_t(g) << 1) | c) + pp;
-                        LO[L] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
+                        LO[lx(L)] = sv + (uint32_t((y ^ pp) >> lane) & 1u);
                         c = uint32_t(y >> 32);
                     }
                     if (warp == 3 && lane == 31 && G.tiles > 1)  // carry word into the next tile
-                        carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[nl - 1]) + c;
+                        carry_words[pair * size_t(G.tiles) + size_t(C0 / G.nt)] = uint64_t(HI[hx(nl - 1)]) + c;
                 }
             }
             __syncthreads();
             {
                 uint64_t* orow = out + pair * size_t(2 * m) + size_t(16 * C0);
                 for (int e = tid; e < 8 * xend; e += kThreads)
-                    reinterpret_cast<uint4*>(orow)[e] = reinterpret_cast<const uint4*>(LO)[e];
+                    reinterpret_cast<uint4*>(orow)[e] = *reinterpret_cast<const uint4*>(LO + lx(2 * e));
             }
         }
         if (tid == 0) item_sh = next_item != nullptr ? gridDim.x + atomicAdd(next_item, 1u) : items;
