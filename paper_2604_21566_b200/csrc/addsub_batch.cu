@@ -27,6 +27,8 @@
 //
 // Interleaved layout [m][batch] and non-power-of-two m use a thread-per-pair strided
 // kernel with the same carry semantics.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -759,6 +761,211 @@ cudaError_t run_interleaved_ilf(uint64_t* out, const uint64_t* a, const uint64_t
     return cudaGetLastError();
 }
 
+// Interleaved layout, thread per pair fed by a TMA ring (k_addsub_ilt): a one-warp CTA
+// owns a strip of P pairs (P * 8 contiguous bytes of every limb row) and walks all m rows
+// of its strip serially, one carry per thread, like the limb-serial oracle
+// (oracle.cpp:16-48) - no segments, no fix-up. Its operands arrive through an S-stage ring
+// of [R rows][P pairs] boxes, one 2-D tensor copy (cp.async.bulk.tensor, the TMA engine)
+// per operand and stage, so S * R rows per CTA are in flight without holding them in
+// registers (the register-held loads of the thread-per-pair kernel cap it at 16 rows per
+// lane: 0.52 of HBM at m = 128). Out-of-range pairs and rows of a box are zero-filled by
+// the TMA unit. Every CTA has the same work and the grid fits the GPU at once, so the
+// strips progress at the rate HBM serves them and end together (k_addsub_ilf's
+// strip-per-CTA grid loses ~25% of the SM time to strips spread 1-2 per SM). Rows are
+// stored straight from registers (coalesced P * 8 bytes per warp). Measured first with one
+// 1-D bulk copy per row: a CTA then completed ~16 row copies per microsecond whatever the
+// ring depth, so the time grew with m (m = 128: 0.88 of HBM, m = 256: 0.54, m = 1024:
+// 0.15); a box per stage removes that per-copy cost.
+// Needs batch even and 16-byte aligned operands (the tensor map's row stride and base).
+template <bool SUB, int P, int R, int S>
+__global__ void __launch_bounds__(P) k_addsub_ilt(const __grid_constant__ CUtensorMap ta,
+                                                  const __grid_constant__ CUtensorMap tb,
+                                                  uint64_t* __restrict__ out, uint32_t* __restrict__ flags, size_t m,
+                                                  size_t batch) {
+    static_assert(P <= 32 && P % 2 == 0, "one warp per strip, 16-byte rows");
+    constexpr unsigned kMask = P == 32 ? 0xffffffffu : (1u << P) - 1u;  // the CTA's lanes
+    constexpr uint32_t kBox = R * P * 8;                                 // bytes per operand box
+    extern __shared__ __align__(128) uint64_t ring[];  // [S][2][R][P]
+    __shared__ uint64_t bar[S];
+    const int t = int(threadIdx.x);
+    const size_t p0 = size_t(blockIdx.x) * P;
+    const size_t nst = (m + R - 1) / R;
+    auto issue = [&](size_t k) {  // lane 0: stage k into slot k % S
+        const int s = int(k % S);
+        uint64_t* dst = ring + size_t(s) * 2 * R * P;
+        bulk::expect_tx(&bar[s], 2u * kBox);
+        const int x = int(p0), y = int(k * R);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(bulk::saddr(dst)),
+            "l"(&ta), "r"(x), "r"(y), "r"(bulk::saddr(&bar[s]))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+            "[%4];" ::"r"(bulk::saddr(dst + R * P)),
+            "l"(&tb), "r"(x), "r"(y), "r"(bulk::saddr(&bar[s]))
+            : "memory");
+    };
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) bulk::init(&bar[s]);
+        bulk::init_fence();
+        for (size_t k = 0; k < size_t(S) && k < nst; ++k) issue(k);
+    }
+    __syncwarp(kMask);
+    const bool act = p0 + size_t(t) < batch;
+    uint32_t c = 0;
+    for (size_t k = 0; k < nst; ++k) {
+        const int s = int(k % S);
+        bulk::wait(&bar[s], uint32_t(k / S) & 1u);
+        const uint64_t* sa = ring + size_t(s) * 2 * R * P + t;
+        const uint64_t* sb = sa + R * P;
+        const size_t r0 = k * R;
+        uint64_t x[R], y[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = sa[r * P], y[r] = sb[r * P];
+        if (act) {
+            uint64_t* po = out + r0 * batch + p0 + t;
+            if (r0 + R <= m) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    uint32_t g, p;
+                    const uint64_t v = apply_carry<SUB>(lane_op<SUB>(x[r], y[r], g, p), c);
+                    c = g | (p & c);
+                    __stcs(po + size_t(r) * batch, v);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (r0 + r < m) {
+                        uint32_t g, p;
+                        const uint64_t v = apply_carry<SUB>(lane_op<SUB>(x[r], y[r], g, p), c);
+                        c = g | (p & c);
+                        __stcs(po + size_t(r) * batch, v);
+                    }
+            }
+        }
+        // slot s is consumed (its values were used above): refill it with stage k + S
+        __syncwarp(kMask);
+        if (t == 0 && k + S < nst) issue(k + S);
+    }
+    if (act && flags != nullptr) flags[p0 + t] = c;
+}
+
+// Tensor map of one [m][batch] u64 operand with [R][P] boxes (cuTensorMapEncodeTiled
+// through the runtime's driver entry point: no link against libcuda).
+bool encode_rows_map(CUtensorMap* map, const uint64_t* base, size_t m, size_t batch, uint32_t P, uint32_t R) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    if (fn == nullptr) return false;
+    const cuuint64_t dims[2] = {cuuint64_t(batch), cuuint64_t(m)};
+    const cuuint64_t strides[1] = {cuuint64_t(batch) * 8u};
+    const cuuint32_t box[2] = {P, R};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Shape for k_addsub_ilt: 32-pair strips (256-byte box rows) when that gives at least two
+// strips per SM, else 16-pair strips; 8-row stages, as many of them in flight per strip
+// (4, 8 or 16) as keep every strip of the grid resident at once. Returns
+// cudaErrorNotSupported for shapes it does not take (odd batch, unaligned operands, no
+// tensor-map entry point, dimensions past the tensor map's 2^32 limit).
+template <bool SUB>
+cudaError_t run_interleaved_ilt(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                                size_t batch, cudaStream_t st) {
+    if (batch % 2 != 0 || (reinterpret_cast<uintptr_t>(a) & 15u) != 0 || (reinterpret_cast<uintptr_t>(b) & 15u) != 0 ||
+        batch >= (size_t(1) << 32) || m >= (size_t(1) << 31))
+        return cudaErrorNotSupported;
+    static thread_local struct { int dev = -1, sms = 148, smem_sm = 233472, smem_cta = 232448; } di;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (di.dev != dev) {
+        cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&di.smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&di.smem_cta, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        di.dev = dev;
+    }
+    static const int s_knob = [] {
+        const char* e = std::getenv("DOTG_ILT_STAGES");  // A/B knob: 4, 8 or 16 stages (0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int p_knob = [] {
+        const char* e = std::getenv("DOTG_ILT_P");  // A/B knob: 16 or 32 pairs per strip (0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    static const int r_knob = [] {
+        const char* e = std::getenv("DOTG_ILT_R");  // A/B knob: rows per stage (8 or 32; 0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    const bool wide = p_knob ? p_knob == 32 : (batch + 31) / 32 >= 2 * size_t(di.sms);
+    const int PP = wide ? 32 : 16;
+    const size_t strips = (batch + PP - 1) / PP;
+    if (strips > size_t(0x7fffffff)) return cudaErrorNotSupported;
+    CUtensorMap ta, tb;
+    // (rows per stage R, stages S): the most rows in flight per strip with every strip of
+    // the grid resident at once (each CTA also takes ~1 KB of reserved and static shared
+    // memory), ties to the bigger box - a CTA's TMA boxes complete at a rate set by their
+    // count more than their bytes (m = 512: R = 32 x 4 stages 0.86 of HBM, R = 8 x 16 0.67).
+    // When no shape fits one wave, the smallest.
+    const size_t per_sm = (strips + di.sms - 1) / di.sms;
+    static constexpr int kRS[6][2] = {{32, 16}, {32, 8}, {32, 4}, {8, 16}, {8, 8}, {8, 4}};
+    int pick = 5;
+    for (int i = 0; i < 6; ++i) {
+        const size_t bytes = size_t(kRS[i][0]) * kRS[i][1] * 2 * PP * 8 + 2048;
+        const bool fits = per_sm * bytes <= size_t(di.smem_sm) && bytes - 2048 <= size_t(di.smem_cta);
+        const int rows = kRS[i][0] * kRS[i][1], best = kRS[pick][0] * kRS[pick][1];
+        const bool pick_fits = per_sm * (size_t(kRS[pick][0]) * kRS[pick][1] * 2 * PP * 8 + 2048) <= size_t(di.smem_sm);
+        if (fits && (!pick_fits || rows > best)) pick = i;
+    }
+    for (int i = 0; i < 6; ++i)  // A/B knobs
+        if ((r_knob == 0 || r_knob == kRS[i][0]) && (s_knob == 0 || s_knob == kRS[i][1]) && (r_knob || s_knob) &&
+            size_t(kRS[i][0]) * kRS[i][1] * 2 * PP * 8 <= size_t(di.smem_cta)) {
+            pick = i;
+            break;
+        }
+    const int R = kRS[pick][0];
+    if (!encode_rows_map(&ta, a, m, batch, uint32_t(PP), uint32_t(R)) ||
+        !encode_rows_map(&tb, b, m, batch, uint32_t(PP), uint32_t(R)))
+        return cudaErrorNotSupported;
+#define DOTG_ILT_LAUNCH(P_, R_, S_)                                                                      \
+    do {                                                                                                 \
+        const size_t smem = size_t(S_) * 2 * (R_) * (P_) * sizeof(uint64_t);                              \
+        static thread_local int attr_dev = -1;                                                           \
+        if (attr_dev != dev) {                                                                           \
+            cudaError_t e = cudaFuncSetAttribute(k_addsub_ilt<SUB, P_, R_, S_>,                           \
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+            if (e != cudaSuccess) return e;                                                              \
+            attr_dev = dev;                                                                              \
+        }                                                                                                \
+        k_addsub_ilt<SUB, P_, R_, S_><<<unsigned(strips), P_, smem, st>>>(ta, tb, out, flags, m, batch); \
+    } while (0)
+#define DOTG_ILT_SHAPES(P_)                              \
+    switch (pick) {                                      \
+        case 0: DOTG_ILT_LAUNCH(P_, 32, 16); break;      \
+        case 1: DOTG_ILT_LAUNCH(P_, 32, 8); break;       \
+        case 2: DOTG_ILT_LAUNCH(P_, 32, 4); break;       \
+        case 3: DOTG_ILT_LAUNCH(P_, 8, 16); break;       \
+        case 4: DOTG_ILT_LAUNCH(P_, 8, 8); break;        \
+        default: DOTG_ILT_LAUNCH(P_, 8, 4); break;       \
+    }
+    if (PP == 32) {
+        DOTG_ILT_SHAPES(32)
+    } else {
+        DOTG_ILT_SHAPES(16)
+    }
+#undef DOTG_ILT_SHAPES
+#undef DOTG_ILT_LAUNCH
+    count_launch();
+    return cudaGetLastError();
+}
+
 // Interleaved layout, two streaming passes (no barrier, no register holding): the
 // long-number scheme of addsub_long.cu applied to segments of kSL limbs x 32 pairs.
 //   pass 1 (k_il_local): warp = (strip of 32 pairs, segment of kSL limb rows); every
@@ -1015,9 +1222,11 @@ int il_route(size_t m, size_t batch) {
     if (mode == 3) return m >= 16 ? 3 : 0;
     if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
     if (mode == 5) return m >= 2 && (batch + 7) / 8 <= size_t(0x7fffffff) ? 5 : 0;
+    if (mode == 6) return 6;  // k_addsub_ilt where it applies (else thread per pair)
     if ((batch + 7) / 8 > size_t(0x7fffffff)) return 0;        // ilf's grid has a CTA per strip
     if (m <= 4) return 5;                                      // ilf, one warp per strip
     if (m < 48) return 0;                                      // thread per pair
+    if (batch >= 8192 && batch % 2 == 0) return 6;             // thread per pair on a TMA ring
     if (m <= 2048 || batch >= 4096) return 5;                  // streaming pass + in-CTA fix-up
     return nseg_fits(m, batch) ? 4 : 5;  // a few very long numbers: (strip, segment) warps fill the GPU
 }
@@ -1130,6 +1339,16 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
                 else if (ir == 5)
                     e = P.sub ? run_interleaved_ilf<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_ilf<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                else if (ir == 6) {
+                    e = P.sub ? run_interleaved_ilt<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                              : run_interleaved_ilt<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                    if (e == cudaErrorNotSupported && P.m >= 2)  // odd batch or unaligned rows
+                        e = P.sub ? run_interleaved_ilf<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                                  : run_interleaved_ilf<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                    else if (e == cudaErrorNotSupported)
+                        e = P.sub ? run_strided<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, 1, P.batch, stream)
+                                  : run_strided<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, 1, P.batch, stream);
+                }
                 else
                     e = P.sub ? run_interleaved_2pass<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_2pass<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);

@@ -4,7 +4,8 @@ The route for an interleaved [m][batch] problem is picked inside the library
 (csrc/addsub_batch.cu il_route); DOTG_IL_MODE forces one, read once per process, so each
 route runs in its own child: 2 thread per pair, 3 re-read segmented CTAs (k_addsub_il2),
 4 two streaming passes, 5 streaming pass with in-CTA fix-up (k_addsub_ilf, in each of its
-chunk / pairs-per-lane / double-buffering variants). Shapes cover ragged m, partial strips,
+chunk / pairs-per-lane / double-buffering variants), 6 thread per pair fed by a bulk-copy
+ring (k_addsub_ilt; odd batches fall back to thread per pair). Shapes cover ragged m, partial strips,
 segments with no rows, in-place calls (out = a), and the carry-stress categories whose propagate runs cross
 segment boundaries (the fix-up's rare multi-row branch)."""
 import json
@@ -73,6 +74,12 @@ SETTINGS = {
     "ilf_g16": {"DOTG_IL_MODE": "5", "DOTG_ILF_G": "16"},
     "ilf_g8_ppl1": {"DOTG_IL_MODE": "5", "DOTG_ILF_G": "8", "DOTG_ILF_PPL": "1"},
     "ilf_ppl4_single": {"DOTG_IL_MODE": "5", "DOTG_ILF_PPL": "4", "DOTG_ILF_DB": "0"},
+    "ilt": {"DOTG_IL_MODE": "6"},
+    "ilt_p16_r8_s4": {"DOTG_IL_MODE": "6", "DOTG_ILT_P": "16", "DOTG_ILT_R": "8", "DOTG_ILT_STAGES": "4"},
+    "ilt_p32_r8_s16": {"DOTG_IL_MODE": "6", "DOTG_ILT_P": "32", "DOTG_ILT_R": "8", "DOTG_ILT_STAGES": "16"},
+    "ilt_p16_r32_s4": {"DOTG_IL_MODE": "6", "DOTG_ILT_P": "16", "DOTG_ILT_R": "32", "DOTG_ILT_STAGES": "4"},
+    "ilt_p16_r32_s16": {"DOTG_IL_MODE": "6", "DOTG_ILT_P": "16", "DOTG_ILT_R": "32", "DOTG_ILT_STAGES": "16"},
+    "ilt_p32_r32": {"DOTG_IL_MODE": "6", "DOTG_ILT_P": "32", "DOTG_ILT_R": "32"},
 }
 
 
@@ -85,3 +92,19 @@ def test_forced_route(cuda, name):
     assert r.returncode == 0, r.stderr[-2000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["cases"] > 0 and not res["bad"], (name, res)
+
+
+# The automatic route at the sizes where it switches to k_addsub_ilt (48 <= m, batch >= 8192
+# and even) and just past them: an odd batch (ilf), the smallest ilt batch, ragged m, boxes
+# whose last stage is partial.
+AUTO_SHAPES = [(48, 8192), (64, 8193), (100, 8194), (130, 8192), (513, 8192), (47, 8192)]
+
+
+def test_auto_route_at_ilt_sizes(cuda):
+    code = CHILD.replace("SHAPES", repr(AUTO_SHAPES))
+    env = {k: v for k, v in os.environ.items() if not k.startswith(("DOTG_IL", "DOTG_ILT", "DOTG_ILF"))}
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["cases"] > 0 and not res["bad"], res
