@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device.cuh"
 #include "internal.h"
@@ -288,47 +289,98 @@ cudaError_t launch_addsub_timed(bool sub, uint64_t* out, const uint64_t* a, cons
 // Thread per pair, any m and any strides: pair p, limb i at p*sp + i*si. Interleaved
 // layout (sp = 1, si = batch) is coalesced; row-major (sp = m, si = 1) is the fallback
 // for m that is not a power of two or misaligned pointers. Same carry semantics as the
-// limb-serial oracle (src/oracle.cpp:16-48).
-template <bool SUB>
-__global__ void __launch_bounds__(256) k_addsub_strided(uint64_t* out, const uint64_t* a,
+// limb-serial oracle (src/oracle.cpp:16-48). Rows go UN at a time with all their loads
+// in flight - the last, partial group too (predicated), so m < UN and ragged tails keep
+// their loads batched (r02: a one-row-at-a-time tail held m = 1 ... 7 at 0.69-0.77 of HBM).
+// VP = 2 (interleaved, even batch, 16-byte aligned rows): a thread owns two adjacent
+// pairs and moves 16 bytes per row and operand.
+#ifndef DOTG_TPP_UN
+#define DOTG_TPP_UN 8
+#endif
+template <bool SUB, int VP>
+__global__ void __launch_bounds__(256, VP == 1 ? 6 : 3) k_addsub_strided(uint64_t* out, const uint64_t* a,
                                                         const uint64_t* b, uint32_t* flags,
                                                         size_t m, size_t batch, size_t sp,
                                                         size_t si) {
-    const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    constexpr int UN = DOTG_TPP_UN;
+    const size_t pidx = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * VP;
     if (pidx >= batch) return;
     const uint64_t* pa = a + pidx * sp;
     const uint64_t* pb = b + pidx * sp;
     uint64_t* po = out + pidx * sp;
-    uint32_t c = 0;
+    uint32_t c[VP];
+#pragma unroll
+    for (int v = 0; v < VP; ++v) c[v] = 0;
+    // rows i .. i + n - 1 (n <= N), every load of the group first
+    auto chunk = [&](auto NN, size_t i, int n) {
+        constexpr int N = decltype(NN)::value;
+        uint64_t x[N][VP], y[N][VP];
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (k < n) {
+                if constexpr (VP == 2) {
+                    const ulonglong2 u = *reinterpret_cast<const ulonglong2*>(pa + (i + k) * si);
+                    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(pb + (i + k) * si);
+                    x[k][0] = u.x, x[k][1] = u.y, y[k][0] = w.x, y[k][1] = w.y;
+                } else {
+                    x[k][0] = pa[(i + k) * si];
+                    y[k][0] = pb[(i + k) * si];
+                }
+            }
+#pragma unroll
+        for (int k = 0; k < N; ++k)
+            if (k < n) {
+#pragma unroll
+                for (int v = 0; v < VP; ++v) {
+                    uint32_t g, p;
+                    const uint64_t sv = lane_op<SUB>(x[k][v], y[k][v], g, p);
+                    x[k][v] = apply_carry<SUB>(sv, c[v]);
+                    c[v] = g | (p & c[v]);
+                }
+                if constexpr (VP == 2)
+                    *reinterpret_cast<ulonglong2*>(po + (i + k) * si) = make_ulonglong2(x[k][0], x[k][1]);
+                else
+                    po[(i + k) * si] = x[k][0];
+            }
+    };
     size_t i = 0;
-#ifndef DOTG_TPP_UN
-#define DOTG_TPP_UN 8
-#endif
-    constexpr int UN = DOTG_TPP_UN;
-    for (; i + UN <= m; i += UN) {
-        uint64_t x[UN], y[UN];
+    for (; i + UN <= m; i += UN) chunk(std::integral_constant<int, UN>{}, i, UN);
+    for (; i < m; i += 4) chunk(std::integral_constant<int, 4>{}, i, m - i < 4 ? int(m - i) : 4);  // tail, 4 rows at a time
+    if (flags != nullptr) {
 #pragma unroll
-        for (int k = 0; k < UN; ++k) {
-            x[k] = pa[(i + k) * si];
-            y[k] = pb[(i + k) * si];
-        }
-#pragma unroll
-        for (int k = 0; k < UN; ++k) {
-            uint32_t g, p;
-            const uint64_t sv = lane_op<SUB>(x[k], y[k], g, p);
-            x[k] = apply_carry<SUB>(sv, c);
-            c = g | (p & c);
-        }
-#pragma unroll
-        for (int k = 0; k < UN; ++k) po[(i + k) * si] = x[k];
+        for (int v = 0; v < VP; ++v) flags[pidx + v] = c[v];
     }
-    for (; i < m; ++i) {
-        uint32_t g, p;
-        const uint64_t sv = lane_op<SUB>(pa[i * si], pb[i * si], g, p);
-        po[i * si] = apply_carry<SUB>(sv, c);
-        c = g | (p & c);
+}
+
+// Interleaved numbers of M <= 3 limbs: a thread owns 4 adjacent pairs, every row one
+// 32-byte load per operand and one 32-byte store (all M rows in flight), the 4 flags one
+// 16-byte store - a carry-chained streaming add. (The per-pair kernel above keeps only
+// 2-6 loads of 8 bytes per thread in flight at these sizes: 0.38-0.77 of HBM.)
+template <bool SUB, int M>
+__global__ void __launch_bounds__(256) k_addsub_il_tiny(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                        const uint64_t* __restrict__ b, uint32_t* __restrict__ flags,
+                                                        size_t batch) {
+    const size_t p = (size_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (p >= batch) return;
+    uint64_t x[M][4], y[M][4];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        ld_stream<4>(a + size_t(r) * batch + p, x[r]);
+        ld_stream<4>(b + size_t(r) * batch + p, y[r]);
     }
-    if (flags != nullptr) flags[pidx] = c;
+    uint32_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            uint32_t g, pr;
+            const uint64_t sv = lane_op<SUB>(x[r][v], y[r][v], g, pr);
+            x[r][v] = apply_carry<SUB>(sv, c[v]);
+            c[v] = g | (pr & c[v]);
+        }
+        st_stream<4>(out + size_t(r) * batch + p, x[r]);
+    }
+    if (flags != nullptr) *reinterpret_cast<uint4*>(flags + p) = make_uint4(c[0], c[1], c[2], c[3]);
 }
 
 // Row-pitched thread per pair: operand rows at their own pitches (views of wider arrays).
@@ -876,12 +928,12 @@ bool encode_rows_map(CUtensorMap* map, const uint64_t* base, size_t m, size_t ba
 // strips per SM, else 16-pair strips; 8-row stages, as many of them in flight per strip
 // (4, 8 or 16) as keep every strip of the grid resident at once. Returns
 // cudaErrorNotSupported for shapes it does not take (odd batch, unaligned operands, no
-// tensor-map entry point, dimensions past the tensor map's 2^32 limit).
+// tensor-map entry point, 2^31 or more pairs or rows).
 template <bool SUB>
 cudaError_t run_interleaved_ilt(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                                 size_t batch, cudaStream_t st) {
     if (batch % 2 != 0 || (reinterpret_cast<uintptr_t>(a) & 15u) != 0 || (reinterpret_cast<uintptr_t>(b) & 15u) != 0 ||
-        batch >= (size_t(1) << 32) || m >= (size_t(1) << 31))
+        batch >= (size_t(1) << 31) || m >= (size_t(1) << 31))  // TMA box coordinates are signed 32-bit
         return cudaErrorNotSupported;
     static thread_local struct { int dev = -1, sms = 148, smem_sm = 233472, smem_cta = 232448; } di;
     int dev = 0;
@@ -1200,16 +1252,19 @@ cudaError_t run_interleaved_2pass(uint64_t* out, const uint64_t* a, const uint64
 // Interleaved routes, per-launch fraction of HBM when launches run back to back (CUDA
 // graph over 3 rotating input copies, tools/il_graph.py; B200, B x m = 2^22 limbs) at
 // m = 4 / 16 / 32 / 64 / 128 / 256 / 512 / 1024 (profiles/r02_il_graph*.jsonl):
-//   thread per pair           0.77 / 0.86 / 0.90 / 0.75 / 0.52 / 0.30 / 0.17 / 0.09
-//   re-read CTAs (il2)        0.77 / 0.73 / 0.74 / 0.74 / 0.71 / 0.69 / 0.67 / 0.64
-//   two passes                0.82 / 0.56 / 0.64 / 0.71 / 0.69 / 0.60 / 0.48 / 0.35
-//   streaming + fix-up (ilf)     - / 0.84 / 0.83 / 0.82 / 0.80 / 0.80 / 0.77 / 0.72
-// Auto: k_addsub_ilf up to 4 limbs (one warp per strip: add and sub 0.82 at m = 4, where
-// the two-pass route's first pass alone gave add 0.82 / sub 0.77), thread per pair below
-// 48 limbs (0.90 at m = 8), then k_addsub_ilf, except a few very long numbers (m > 2048
-// and fewer than 4096 pairs), which take the two-pass route (its warps are (strip,
-// segment) pairs, so they still fill the GPU). DOTG_IL_MODE (A/B knob) forces 2 (thread per pair), 3
-// (il2), 4 (two passes) or 5 (ilf) where they apply.
+//   thread per pair (r01 tail)   0.77 / 0.86 / 0.90 / 0.75 / 0.52 / 0.30 / 0.17 / 0.09
+//   re-read CTAs (il2)           0.77 / 0.73 / 0.74 / 0.74 / 0.71 / 0.69 / 0.67 / 0.64
+//   two passes                   0.82 / 0.56 / 0.64 / 0.71 / 0.69 / 0.60 / 0.48 / 0.35
+//   streaming + fix-up (ilf)        - / 0.84 / 0.83 / 0.82 / 0.80 / 0.80 / 0.77 / 0.72
+//   TMA box ring (ilt)           0.57 / 0.88 / 0.87 / 0.85 / 0.88 / 0.86 / 0.86 / 0.59
+// Auto (profiles/r02_il_graph_auto_final.jsonl: 0.80-0.91 for m = 1 ... 512, 0.76 at
+// m = 1024 with 4096 pairs): k_addsub_il_tiny for m <= 3 (4 pairs per thread, 32-byte
+// rows; 0.89-0.91, where ilf ran 0.09-0.23), thread per pair below 48 limbs (two pairs per
+// thread under 8 limbs; 0.85-0.91), k_addsub_ilt from 48 limbs for even batches of >= 8192
+// pairs, k_addsub_ilf otherwise, except a few very long numbers (m > 2048 and fewer than
+// 4096 pairs), which take the two-pass route (its warps are (strip, segment) pairs, so they
+// still fill the GPU). DOTG_IL_MODE (A/B knob) forces 2 (thread per pair), 3 (il2), 4 (two
+// passes), 5 (ilf), 6 (ilt) or 7 (il_tiny) where they apply.
 int il_mode() {
     static const int v = [] {
         const char* e = std::getenv("DOTG_IL_MODE");
@@ -1224,8 +1279,9 @@ int il_route(size_t m, size_t batch) {
     if (mode == 4) return nseg_fits(m, batch) ? 4 : 0;
     if (mode == 5) return m >= 2 && (batch + 7) / 8 <= size_t(0x7fffffff) ? 5 : 0;
     if (mode == 6) return 6;  // k_addsub_ilt where it applies (else thread per pair)
+    if (mode == 7) return m <= 3 ? 7 : 0;  // k_addsub_il_tiny where it applies
+    if (m <= 3) return 7;                                      // 4 pairs per thread, 32-byte rows
     if ((batch + 7) / 8 > size_t(0x7fffffff)) return 0;        // ilf's grid has a CTA per strip
-    if (m <= 4) return 5;                                      // ilf, one warp per strip
     if (m < 48) return 0;                                      // thread per pair
     if (batch >= 8192 && batch % 2 == 0) return 6;             // thread per pair on a TMA ring
     if (m <= 2048 || batch >= 4096) return 5;                  // streaming pass + in-CTA fix-up
@@ -1240,13 +1296,42 @@ cudaError_t run_strided(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
         const int v = e ? std::atoi(e) : 256;
         return unsigned(v >= 32 && v <= 256 ? v : 256);
     }();
-    const size_t blocks = (batch + bs - 1) / bs;
-    k_addsub_strided<SUB><<<unsigned(blocks), bs, 0, st>>>(out, a, b, flags, m, batch, sp, si);
+    static const int vp_knob = [] {
+        const char* e = std::getenv("DOTG_TPP_VP");  // A/B knob: pairs per thread (1 or 2; 0 = auto)
+        return e ? std::atoi(e) : 0;
+    }();
+    // two pairs per thread: interleaved rows, even batch, 16-byte aligned rows, and a
+    // grid that still has >= 8 threads per SM lane slot (small m, big batch)
+    const bool can2 = sp == 1 && batch % 2 == 0 && si % 2 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
+                        reinterpret_cast<uintptr_t>(b)) & 15u) == 0;
+    const bool two = can2 && (vp_knob ? vp_knob == 2 : (m < 8 && batch >= (size_t(1) << 20)));
+    const size_t threads = two ? batch / 2 : batch;
+    const size_t blocks = (threads + bs - 1) / bs;
+    if (two) k_addsub_strided<SUB, 2><<<unsigned(blocks), bs, 0, st>>>(out, a, b, flags, m, batch, sp, si);
+    else k_addsub_strided<SUB, 1><<<unsigned(blocks), bs, 0, st>>>(out, a, b, flags, m, batch, sp, si);
     count_launch();
     return cudaGetLastError();
 }
 
 bool aligned(const void* p, size_t bytes) { return (reinterpret_cast<uintptr_t>(p) % bytes) == 0; }
+
+// k_addsub_il_tiny for 1 <= m <= 3: batch % 4 == 0, rows 32-byte aligned (operands and
+// output), flags 16-byte aligned; cudaErrorNotSupported otherwise.
+template <bool SUB>
+cudaError_t run_il_tiny(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m, size_t batch,
+                        cudaStream_t st) {
+    if (m < 1 || m > 3 || batch % 4 != 0 || !aligned(out, 32) || !aligned(a, 32) || !aligned(b, 32) ||
+        (flags != nullptr && !aligned(flags, 16)))
+        return cudaErrorNotSupported;
+    const size_t blocks = (batch / 4 + 255) / 256;
+    if (blocks > size_t(0x7fffffff)) return cudaErrorNotSupported;
+    if (m == 1) k_addsub_il_tiny<SUB, 1><<<unsigned(blocks), 256, 0, st>>>(out, a, b, flags, batch);
+    else if (m == 2) k_addsub_il_tiny<SUB, 2><<<unsigned(blocks), 256, 0, st>>>(out, a, b, flags, batch);
+    else k_addsub_il_tiny<SUB, 3><<<unsigned(blocks), 256, 0, st>>>(out, a, b, flags, batch);
+    count_launch();
+    return cudaGetLastError();
+}
 
 template <bool SUB>
 cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
@@ -1340,7 +1425,13 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
                 else if (ir == 5)
                     e = P.sub ? run_interleaved_ilf<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_ilf<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
-                else if (ir == 6) {
+                else if (ir == 7) {
+                    e = P.sub ? run_il_tiny<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                              : run_il_tiny<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+                    if (e == cudaErrorNotSupported)  // batch % 4 or alignment
+                        e = P.sub ? run_strided<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, 1, P.batch, stream)
+                                  : run_strided<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, 1, P.batch, stream);
+                } else if (ir == 6) {
                     e = P.sub ? run_interleaved_ilt<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
                               : run_interleaved_ilt<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
                     if (e == cudaErrorNotSupported && P.m >= 2)  // odd batch or unaligned rows

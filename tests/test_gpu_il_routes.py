@@ -57,11 +57,13 @@ for m, batch in SHAPES:
 print(json.dumps({"cases": n, "bad": bad[:10]}))
 '''.replace("ROOT", repr(ROOT))
 
-SHAPES = [(2, 70), (5, 33), (16, 64), (33, 40), (64, 96), (100, 65), (128, 128), (200, 130), (256, 190),
+SHAPES = [(1, 64), (2, 70), (3, 68), (5, 33), (16, 64), (33, 40), (64, 96), (100, 65), (128, 128), (200, 130), (256, 190),
           (257, 40), (512, 66), (777, 33), (1024, 64), (1500, 40), (2048, 6), (3000, 2)]
 
 SETTINGS = {
     "tpp": {"DOTG_IL_MODE": "2"},
+    "tpp_vp2": {"DOTG_IL_MODE": "2", "DOTG_TPP_VP": "2"},
+    "tiny": {"DOTG_IL_MODE": "7"},
     "il2": {"DOTG_IL_MODE": "3"},
     "two_pass": {"DOTG_IL_MODE": "4"},
     "ilf": {"DOTG_IL_MODE": "5"},
@@ -96,8 +98,10 @@ def test_forced_route(cuda, name):
 
 # The automatic route at the sizes where it switches to k_addsub_ilt (48 <= m, batch >= 8192
 # and even) and just past them: an odd batch (ilf), the smallest ilt batch, ragged m, boxes
-# whose last stage is partial.
-AUTO_SHAPES = [(48, 8192), (64, 8193), (100, 8194), (130, 8192), (513, 8192), (47, 8192)]
+# whose last stage is partial; and m <= 3 (k_addsub_il_tiny, batch % 4 == 0, else thread
+# per pair) and m = 4 ... 7 (thread per pair).
+AUTO_SHAPES = [(48, 8192), (64, 8193), (100, 8194), (130, 8192), (513, 8192), (47, 8192),
+               (1, 4096), (2, 4100), (3, 4098), (3, 4097), (4, 4096), (7, 4098)]
 
 
 def test_auto_route_at_ilt_sizes(cuda):
