@@ -1134,7 +1134,7 @@ __global__ void __launch_bounds__(256) k_il_finish(uint64_t* __restrict__ out, c
 // carry, so in the lane fold it clears both G and P (nothing crosses a pair boundary),
 // and the flag of a pair is the carry out of its last limb. Pair positions advance by
 // the precomputed 128 / m and 128 % m per chunk - no division in the loop.
-template <bool SUB>
+template <bool SUB, int U>
 __global__ void __launch_bounds__(256) k_addsub_rows_any(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
                                                          const uint64_t* __restrict__ b, uint32_t* flags, size_t m,
                                                          size_t batch, size_t ppt, size_t ntasks, bool vec) {
@@ -1151,66 +1151,80 @@ __global__ void __launch_bounds__(256) k_addsub_rows_any(uint64_t* __restrict__ 
         size_t pidx = p0 + q_l;  // pair of this lane's first limb in the current chunk
         uint32_t pos = r_l;      // its position inside that pair
         uint32_t cin = 0;        // carry into the chunk
-        for (size_t cb = p0 * m; cb < end; cb += 128) {
-            const size_t f = cb + l4;
-            uint64_t x[4] = {0, 0, 0, 0}, y[4] = {0, 0, 0, 0};
-            if (vec && f + 3 < end) {
-                ld_stream<4>(a + f, x);
-                ld_stream<4>(b + f, y);
-            } else {
+        // U chunks of 128 limbs per step: every load of the step in flight before the
+        // first chunk's carries resolve (r02: one chunk at a time held odd m at 0.70-0.79
+        // of HBM and m = 4096 rows at 0.45)
+        for (size_t cb0 = p0 * m; cb0 < end; cb0 += 128 * U) {
+            uint64_t x[U][4], y[U][4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (f + k < end) {
-                        x[k] = a[f + k];
-                        y[k] = b[f + k];
-                    }
+            for (int u = 0; u < U; ++u) {
+                const size_t f = cb0 + 128 * u + l4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[u][k] = y[u][k] = 0;
+                if (vec && f + 3 < end) {
+                    ld_stream<4>(a + f, x[u]);
+                    ld_stream<4>(b + f, y[u]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (f + k < end) {
+                            x[u][k] = a[f + k];
+                            y[u][k] = b[f + k];
+                        }
+                }
             }
-            uint64_t sv[4];
-            uint32_t g[4], pr[4], start = 0, last = 0;
-            uint32_t G = 0, P = 1;
-            {
-                uint32_t ps = pos;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const size_t cb = cb0 + 128 * u;
+                if (cb >= end) break;
+                const size_t f = cb + l4;
+                uint64_t sv[4];
+                uint32_t g[4], pr[4], start = 0, last = 0;
+                uint32_t G = 0, P = 1;
+                {
+                    uint32_t ps = pos;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const bool ok = f + k < end;
+                        sv[k] = lane_op<SUB>(x[u][k], y[u][k], g[k], pr[k]);
+                        if (!ok) g[k] = pr[k] = 0;
+                        if (ok && ps == 0) start |= 1u << k;
+                        if (ok && ps + 1 == mm) last |= 1u << k;
+                        if ((start >> k) & 1u) G = P = 0;  // a pair starts: nothing enters from below
+                        G = g[k] | (pr[k] & G);
+                        P &= pr[k];
+                        ps = ps + 1 == mm ? 0 : ps + 1;
+                    }
+                }
+                const uint32_t Gm = __ballot_sync(0xffffffffu, G), Pm = __ballot_sync(0xffffffffu, P);
+                const uint64_t yv = ((uint64_t(Gm) << 1) | cin) + uint64_t(Pm);
+                uint32_t c = ((uint32_t(yv) ^ Pm) >> lane) & 1u;
+                cin = uint32_t(yv >> 32);
+                size_t pq = pidx;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const bool ok = f + k < end;
-                    sv[k] = lane_op<SUB>(x[k], y[k], g[k], pr[k]);
-                    if (!ok) g[k] = pr[k] = 0;
-                    if (ok && ps == 0) start |= 1u << k;
-                    if (ok && ps + 1 == mm) last |= 1u << k;
-                    if ((start >> k) & 1u) G = P = 0;  // a pair starts: nothing enters from below
-                    G = g[k] | (pr[k] & G);
-                    P &= pr[k];
-                    ps = ps + 1 == mm ? 0 : ps + 1;
+                    if ((start >> k) & 1u) c = 0;
+                    const uint64_t o = apply_carry<SUB>(sv[k], c);
+                    c = g[k] | (pr[k] & c);
+                    sv[k] = o;
+                    if ((last >> k) & 1u) {
+                        if (flags != nullptr) flags[pq] = c;
+                        ++pq;
+                    }
                 }
-            }
-            const uint32_t Gm = __ballot_sync(0xffffffffu, G), Pm = __ballot_sync(0xffffffffu, P);
-            const uint64_t yv = ((uint64_t(Gm) << 1) | cin) + uint64_t(Pm);
-            uint32_t c = ((uint32_t(yv) ^ Pm) >> lane) & 1u;
-            cin = uint32_t(yv >> 32);
-            size_t pq = pidx;
+                if (vec && f + 3 < end) {
+                    st_stream<4>(out + f, sv);
+                } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if ((start >> k) & 1u) c = 0;
-                const uint64_t o = apply_carry<SUB>(sv[k], c);
-                c = g[k] | (pr[k] & c);
-                sv[k] = o;
-                if ((last >> k) & 1u) {
-                    if (flags != nullptr) flags[pq] = c;
-                    ++pq;
+                    for (int k = 0; k < 4; ++k)
+                        if (f + k < end) out[f + k] = sv[k];
                 }
-            }
-            if (vec && f + 3 < end) {
-                st_stream<4>(out + f, sv);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (f + k < end) out[f + k] = sv[k];
-            }
-            pidx += q128;
-            pos += r128;
-            if (pos >= mm) {
-                pos -= mm;
-                ++pidx;
+                pidx += q128;
+                pos += r128;
+                if (pos >= mm) {
+                    pos -= mm;
+                    ++pidx;
+                }
             }
         }
     }
@@ -1333,11 +1347,17 @@ cudaError_t run_il_tiny(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
     return cudaGetLastError();
 }
 
+constexpr int kRowsU = 4;  // chunks of 128 limbs in flight per warp
 template <bool SUB>
 cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
                          size_t batch, cudaStream_t st) {
     // tasks of whole pairs, ~512 limbs each, with a limb count that keeps every task start
     // 4-limb (32-byte) aligned so the 256-bit path applies throughout
+    static const int rows_u = [] {
+        const char* e = std::getenv("DOTG_ROWS_U");  // A/B knob: chunks in flight per warp (1, 2, 4)
+        const int v = e ? std::atoi(e) : kRowsU;
+        return v == 1 || v == 2 ? v : kRowsU;
+    }();
     size_t ppt = m >= 512 ? 1 : 512 / m;
     const size_t g4 = (m % 4 == 0) ? 1 : (m % 2 == 0 ? 2 : 4);  // pairs per 4-limb alignment
     ppt = (ppt + g4 - 1) / g4 * g4;
@@ -1349,13 +1369,15 @@ cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, ui
     if (di.dev != dev) {
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_addsub_rows_any<SUB>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_addsub_rows_any<SUB, kRowsU>, 256, 0);
         di.cap = sms * (per > 0 ? per : 1);
         di.dev = dev;
     }
     const size_t need = (ntasks + 7) / 8;
     const unsigned grid = unsigned(need < size_t(di.cap) ? need : size_t(di.cap));
-    k_addsub_rows_any<SUB><<<grid, 256, 0, st>>>(out, a, b, flags, m, batch, ppt, ntasks, vec);
+    if (rows_u == 1) k_addsub_rows_any<SUB, 1><<<grid, 256, 0, st>>>(out, a, b, flags, m, batch, ppt, ntasks, vec);
+    else if (rows_u == 2) k_addsub_rows_any<SUB, 2><<<grid, 256, 0, st>>>(out, a, b, flags, m, batch, ppt, ntasks, vec);
+    else k_addsub_rows_any<SUB, kRowsU><<<grid, 256, 0, st>>>(out, a, b, flags, m, batch, ppt, ntasks, vec);
     count_launch();
     return cudaGetLastError();
 }

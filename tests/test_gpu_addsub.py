@@ -263,3 +263,42 @@ def test_row_pitched_views(cuda, oracle):
     T = torch.zeros((10, 16), dtype=torch.int64, device="cuda")
     with pytest.raises(dg.InvalidArgument):
         dg.addsub_batch(False, T[:, 0:8], T[:, 8:16], out=T[:, 4:12])
+
+
+ROWS_CHILD = r'''
+import sys
+sys.path.insert(0, ROOT + "/tests"); sys.path.insert(0, ROOT)
+import numpy as np, torch
+import paper_2604_21566_b200 as dg
+from helpers import CATEGORIES, Oracle, category
+orc = Oracle()
+bad = []
+for m, batch in [(3, 301), (5, 97), (33, 130), (100, 41), (257, 12), (1000, 9), (2048, 5), (4096, 3)]:
+    rng = np.random.default_rng(77 + m)
+    for cat in CATEGORIES:
+        for op in ("add", "sub"):
+            a, b = category(rng, cat, op, (batch, m))
+            want, wf = orc.addsub_batch(op == "sub", a, b)
+            ta = torch.from_numpy(a.view(np.int64)).cuda()
+            tb = torch.from_numpy(b.view(np.int64)).cuda()
+            out, fl = dg.addsub_batch(op == "sub", ta, tb)
+            if not (np.array_equal(out.cpu().numpy().view(np.uint64), want)
+                    and np.array_equal(fl.cpu().numpy().view(np.uint32), wf)):
+                bad.append([m, batch, cat, op])
+print("BAD", bad)
+'''
+
+
+@pytest.mark.parametrize("u", ["1", "2", "4"])
+def test_rows_any_chunks_in_flight(cuda, u):
+    """The any-m row kernel with 1, 2 and 4 chunks of loads in flight per warp (DOTG_ROWS_U,
+    read once per process: one child each), ragged m and pow2 m above 512."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", ROWS_CHILD.replace("ROOT", repr(root))],
+                       env={**os.environ, "DOTG_ROWS_U": u}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
