@@ -1080,6 +1080,30 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
         return launch_karatsuba_padded(out, a, b, m, batch, mul_umma_leaf(m, batch), stream);
     if (layout == 0 && route != 1 && m > 16 && !mul_imma_supported(m))
         return launch_karatsuba_padded(out, a, b, m, batch, m <= 32 ? 32 : (m <= 64 ? 64 : 128), stream);
+    // m = 3, 6, 10, 12, 14: a register kernel of exactly m limbs, both layouts (no
+    // zero-extended columns). Measured (tools/mul_sweep.py, B x m = 2^22, row-major /
+    // interleaved, us): m = 3 39 / 22 vs 109 / 114 before, m = 6 24 / 115 vs 45 / 138,
+    // m = 10-14 30-38 / 94-100 vs 63-66 / 128-134. Odd m >= 5 stay on the zero-extended
+    // 8 / 16-limb kernels (row-major) and the generic loop (interleaved): with one column
+    // chain per thread and odd rows stored limb by limb, the exact kernel is no faster there
+    // (profiles/r02_mul_exact_ab.jsonl). DOTG_MUL_EXACT=0 (A/B) takes the old routes, =2
+    // forces the exact kernel for every m in 3 ... 15 off the powers of two.
+    static const int exact = [] {
+        const char* e = std::getenv("DOTG_MUL_EXACT");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (exact && route != 1 && m >= 3 && m <= 15 && (m & (m - 1)) != 0 &&
+        (exact == 2 || m == 3 || m % 2 == 0)) {
+        const int L = layout == 0 ? 0 : 1;
+        switch (m) {
+#define DOTG_EXACT(MM) \
+    case MM: return L ? run_regs<MM, 1>(out, a, b, batch, stream) : run_regs<MM, 0>(out, a, b, batch, stream);
+            DOTG_EXACT(3) DOTG_EXACT(5) DOTG_EXACT(6) DOTG_EXACT(7) DOTG_EXACT(9) DOTG_EXACT(10)
+            DOTG_EXACT(11) DOTG_EXACT(12) DOTG_EXACT(13) DOTG_EXACT(14) DOTG_EXACT(15)
+#undef DOTG_EXACT
+            default: break;
+        }
+    }
     // 4 < m < 16 off the power-of-two kernels, or misaligned rows of 5..16: the register
     // kernels of the next size with zero-extended operands, any alignment
     // (tools/odd_m_mul_timing.py: m = 12 92 us vs 492 us thread-per-pair generic).

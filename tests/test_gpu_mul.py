@@ -37,7 +37,7 @@ def route(request, cuda):
     dg.set_mul_route(prev)
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 12, 16, 24, 32, 33, 48, 64, 100, 128])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 24, 32, 33, 48, 64, 100, 128])
 def test_mul_matches_oracle(cuda, oracle, route, m):
     rng = np.random.default_rng(2000 + m)
     n = 67
@@ -196,3 +196,39 @@ def test_interleaved_tensor_pipe_in_place(cuda, oracle, m, n):
     b[1::4] = MAX
     want = oracle.mul_batch(a, b)
     assert np.array_equal(mul(cuda, a, b, "interleaved"), want), (m, n)
+
+
+EXACT_CHILD = r'''
+import sys
+sys.path.insert(0, ROOT + "/tests"); sys.path.insert(0, ROOT)
+import numpy as np, torch
+import paper_2604_21566_b200 as dg
+from helpers import Oracle, category
+orc = Oracle()
+bad = []
+for m in (3, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15):
+    rng = np.random.default_rng(4400 + m)
+    for cat in ("random", "maxed_limbs", "spiky"):
+        a, b = category(rng, cat, "mul", (131, m))
+        want = orc.mul_batch(a, b)
+        ta = torch.from_numpy(a.view(np.int64)).cuda(); tb = torch.from_numpy(b.view(np.int64)).cuda()
+        got = dg.mul_batch(ta, tb).cpu().numpy().view(np.uint64)
+        il = dg.mul_batch(ta.t().contiguous(), tb.t().contiguous(), layout="interleaved")
+        if not (np.array_equal(got, want) and np.array_equal(il.cpu().numpy().view(np.uint64).T, want)):
+            bad.append([m, cat])
+print("BAD", bad)
+'''
+
+
+def test_exact_small_kernels_every_odd_size(cuda):
+    """DOTG_MUL_EXACT=2 forces the exact-m register kernels for every m in 3 ... 15 off the
+    powers of two (the default takes them only where they measured faster), both layouts."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", EXACT_CHILD.replace("ROOT", repr(root))],
+                       env={**os.environ, "DOTG_MUL_EXACT": "2"}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
