@@ -1078,8 +1078,16 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     }
     if (layout == 0 && route != 1 && m > mul_umma_direct_max() && mul_umma_supported(mul_umma_leaf(m, batch)))
         return launch_karatsuba_padded(out, a, b, m, batch, mul_umma_leaf(m, batch), stream);
-    if (layout == 0 && route != 1 && m > 16 && !mul_imma_supported(m))
-        return launch_karatsuba_padded(out, a, b, m, batch, m <= 32 ? 32 : (m <= 64 ? 64 : 128), stream);
+    if (layout == 0 && route != 1 && m > 16 && !mul_imma_supported(m)) {
+        // rows copy-padded to the next tensor-pipe size: a multiple of 16 limbs up to 128
+        // (DOTG_IMMA_FINE=0: the next power of two), padded Karatsuba above
+        static const int fine = [] {
+            const char* e = std::getenv("DOTG_IMMA_FINE");
+            return e ? std::atoi(e) : 1;
+        }();
+        const size_t base = m > 128 ? 128 : (fine ? (m + 15) & ~size_t(15) : (m <= 32 ? 32 : (m <= 64 ? 64 : 128)));
+        return launch_karatsuba_padded(out, a, b, m, batch, base < 32 ? 32 : base, stream);
+    }
     // m = 3, 6, 10, 12, 14: a register kernel of exactly m limbs, both layouts (no
     // zero-extended columns). Measured (tools/mul_sweep.py, B x m = 2^22, row-major /
     // interleaved, us): m = 3 39 / 22 vs 109 / 114 before, m = 6 24 / 115 vs 45 / 138,

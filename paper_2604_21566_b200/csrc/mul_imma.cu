@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "internal.h"
@@ -81,7 +82,7 @@ struct ImmaCfg {
     static constexpr int VW = NW >= 32 ? NW / 32 : 1;  // operand words per lane
     static constexpr int LD_LANES = NW / VW;
     static_assert(OUT_LIMBS % LPL == 0 && LANES <= 32, "limb split");
-    static_assert(VW == 1 || VW == 2 || VW == 4 || VW == 8, "operand split");
+    static_assert(NW % VW == 0 && NW / VW <= 32, "operand split");  // VW of 3, 5, 6, 7: scalar moves
 };
 
 constexpr int kImmaWarps = 4;
@@ -130,8 +131,11 @@ __device__ __forceinline__ void lds_vec(const uint32_t* p, uint32_t (&w)[N]) {
     } else if constexpr (VW == 2) {
         const uint2 v = *reinterpret_cast<const uint2*>(p);
         w[0] = v.x, w[1] = v.y;
-    } else {
+    } else if constexpr (VW == 1) {
         w[0] = *p;
+    } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) w[e] = p[e];
     }
 }
 template <int VW>
@@ -143,8 +147,11 @@ __device__ __forceinline__ void sts_vec(uint32_t* p, const uint32_t (&w)[VW]) {
         *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
     } else if constexpr (VW == 2) {
         *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
-    } else {
+    } else if constexpr (VW == 1) {
         *p = w[0];
+    } else {
+#pragma unroll
+        for (int e = 0; e < VW; ++e) p[e] = w[e];
     }
 }
 
@@ -247,7 +254,12 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL
             sts_vec<C::VW>(cp + 1 * C::CLP + j0 + 8, c1);
             sts_vec<C::VW>(cp + 2 * C::CLP + j0 + 8, c2);
             sts_vec<C::VW>(cp + 3 * C::CLP + j0 + 8, c3);
-            sts_vec<C::VW>(sa + aidx(j0), sv);
+            if constexpr ((C::VW & (C::VW - 1)) == 0) {
+                sts_vec<C::VW>(sa + aidx(j0), sv);  // VW-aligned: inside one 8-word block
+            } else {
+#pragma unroll
+                for (int e = 0; e < C::VW; ++e) sa[aidx(j0 + e)] = sv[e];
+            }
             if (lane == 0) {
                 cp[0 * C::CLP + 7] = bv[0] << 24;
                 cp[1 * C::CLP + 7] = bv[0] << 16;
@@ -486,7 +498,9 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
 
 }  // namespace
 
-bool mul_imma_supported(size_t m) { return m == 8 || m == 16 || m == 32 || m == 64 || m == 128; }
+bool mul_imma_supported(size_t m) {
+    return m == 8 || m == 16 || m == 32 || m == 48 || m == 64 || m == 80 || m == 96 || m == 112 || m == 128;
+}
 
 cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                             cudaStream_t st) {
@@ -496,7 +510,11 @@ cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b,
         case 8: return run_imma<2>(out, a, b, batch, mr, st);
         case 16: return run_imma<4>(out, a, b, batch, mr, st);
         case 32: return run_imma<8>(out, a, b, batch, mr, st);
+        case 48: return run_imma<12>(out, a, b, batch, mr, st);
         case 64: return run_imma<16>(out, a, b, batch, mr, st);
+        case 80: return run_imma<20>(out, a, b, batch, mr, st);
+        case 96: return run_imma<24>(out, a, b, batch, mr, st);
+        case 112: return run_imma<28>(out, a, b, batch, mr, st);
         case 128: return run_imma<32>(out, a, b, batch, mr, st);
         default: return cudaErrorNotSupported;
     }
@@ -521,8 +539,17 @@ cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t*
     if (batch == 0) return cudaSuccess;
     if (m % 2 != 0 || m <= 16 || m >= 128) return cudaErrorNotSupported;
     const int mr = int(m);
+    // next multiple of 16 limbs (DOTG_IMMA_FINE=0: the next power of two, as in r01)
+    static const int fine = [] {
+        const char* e = std::getenv("DOTG_IMMA_FINE");
+        return e ? std::atoi(e) : 1;
+    }();
     if (m <= 32) return run_imma<8>(out, a, b, batch, mr, st);
+    if (fine && m <= 48) return run_imma<12>(out, a, b, batch, mr, st);
     if (m <= 64) return run_imma<16>(out, a, b, batch, mr, st);
+    if (fine && m <= 80) return run_imma<20>(out, a, b, batch, mr, st);
+    if (fine && m <= 96) return run_imma<24>(out, a, b, batch, mr, st);
+    if (fine && m <= 112) return run_imma<28>(out, a, b, batch, mr, st);
     return run_imma<32>(out, a, b, batch, mr, st);
 }
 

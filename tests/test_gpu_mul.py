@@ -232,3 +232,18 @@ def test_exact_small_kernels_every_odd_size(cuda):
                        env={**os.environ, "DOTG_MUL_EXACT": "2"}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("m", [17, 33, 40, 47, 48, 49, 65, 72, 80, 90, 96, 97, 110, 112, 127])
+def test_tensor_pipe_multiple_of_16_sizes(cuda, oracle, m):
+    """Sizes between the powers of two on the tensor pipe: 48 / 80 / 96 / 112 limbs
+    exactly (k_mul_imma<12 / 20 / 24 / 28>, operand words not a power of two per lane),
+    even m zero-extended in the ring to the next multiple of 16, odd m copy-padded; random,
+    all-ones (the largest column sums) and partial last warps."""
+    rng = np.random.default_rng(5100 + m)
+    for n in (1, 7, 301):
+        a, b = category(rng, "random", "mul", (n, m))
+        a[::2] = MAX
+        b[::3] = MAX
+        want = oracle.mul_batch(a, b)
+        assert np.array_equal(mul(cuda, a, b, "row"), want), (m, n)
