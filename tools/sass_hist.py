@@ -11,13 +11,13 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OBJ = os.path.join(ROOT, "paper_2604_21566_b200", "csrc", "build")
 KERNELS = {
-    "addsub_batch.o": ["k_addsub_grouped", "k_addsub_timed", "k_addsub_ilf", "k_il_local", "k_il_finish"],
+    "addsub_batch.o": ["k_addsub_grouped", "k_addsub_timed", "k_addsub_ilf", "k_addsub_ilt", "k_addsub_il_tiny", "k_il_local", "k_il_finish"],
     "mul_batch.o": ["k_mul_kara16", "k_mul_regblk", "k_mul52_regs"],
     "mul_imma.o": ["k_mul_imma"],
     "mul_umma.o": ["k_mul_umma", "k_umma_tile_carries"],
     "addsub_long.o": ["k_long_local", "k_long_finish"],
 }
-KEY = re.compile(r"^(UTC\w*|LDTM|STTM|UBLKCP|SYNCS|IMMA|HMMA|IMAD|IADD3|LDS|STS|LDG|STG|SHFL|VOTE|BAR|LOP3|SEL|DFMA|DADD)")
+KEY = re.compile(r"^(UTC\w*|LDTM|STTM|UBLKCP|UTMALDG|SYNCS|IMMA|HMMA|IMAD|IADD3|LDS|STS|LDG|STG|SHFL|VOTE|BAR|LOP3|SEL|DFMA|DADD)")
 
 
 def main():
