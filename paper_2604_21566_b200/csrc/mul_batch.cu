@@ -70,14 +70,41 @@ __device__ __forceinline__ uint32_t hi32(uint64_t x) { return uint32_t(x >> 32);
 // ---------------------------------------------------------------------------
 // M <= 16: everything in registers.
 // ---------------------------------------------------------------------------
+// LAYOUT 0: row-major, 1: interleaved, 2: row-major staged through shared memory (odd M:
+// the CTA's 128 rows of a and b are loaded, and its products stored, as contiguous
+// coalesced runs instead of per-thread strided limbs; r02: m = 5 / 7 / 9 / 11 / 13 / 15
+// row-major ran 39-69 us per 2^22 limbs unstaged against 24-42 us interleaved).
 template <int M, int LAYOUT>
 __global__ void __launch_bounds__(128) k_mul_regs(uint64_t* out, const uint64_t* a, const uint64_t* b,
                                                   size_t batch) {
     constexpr int N = 2 * M;  // words per operand
+    constexpr bool STG = LAYOUT == 2;
+    __shared__ uint64_t stage[STG ? 2 * 128 * M : 1];  // a rows | b rows, later the 2M-limb products
     const size_t pidx = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (pidx >= batch) return;
+    const size_t p0 = size_t(blockIdx.x) * blockDim.x;
+    const int np = STG ? int(batch - p0 < 128 ? batch - p0 : 128) : 0;
+    if constexpr (STG) {
+        for (int e = threadIdx.x; e < np * M; e += 128) {
+            stage[e] = __ldcs(a + p0 * M + e);
+            stage[128 * M + e] = __ldcs(b + p0 * M + e);
+        }
+        __syncthreads();
+    } else if (pidx >= batch) {
+        return;
+    }
+    const bool act = pidx < batch;
     uint32_t A[N], B[N];
-    if constexpr (LAYOUT == 0 && M % 4 == 0) {
+    if constexpr (STG) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const uint64_t x = act ? stage[threadIdx.x * M + i] : 0, y = act ? stage[128 * M + threadIdx.x * M + i] : 0;
+            A[2 * i] = lo32(x);
+            A[2 * i + 1] = hi32(x);
+            B[2 * i] = lo32(y);
+            B[2 * i + 1] = hi32(y);
+        }
+        __syncthreads();  // the operand rows are in registers: the buffer takes the products
+    } else if constexpr (LAYOUT == 0 && M % 4 == 0) {
 #pragma unroll
         for (int v = 0; v < M / 4; ++v) {
             uint64_t x[4], y[4];
@@ -119,7 +146,9 @@ __global__ void __launch_bounds__(128) k_mul_regs(uint64_t* out, const uint64_t*
         if (c & 1) {
             const int limb = c >> 1;
             const uint64_t v = uint64_t(prev) | (uint64_t(w) << 32);
-            if constexpr (LAYOUT == 0 && (2 * M) % 4 == 0) {
+            if constexpr (STG) {
+                stage[threadIdx.x * (2 * M) + limb] = v;
+            } else if constexpr (LAYOUT == 0 && (2 * M) % 4 == 0) {
                 o[limb & 3] = v;
                 if ((limb & 3) == 3) st_stream<4>(out + pidx * (2 * M) + (limb - 3), o);
             } else {
@@ -129,6 +158,10 @@ __global__ void __launch_bounds__(128) k_mul_regs(uint64_t* out, const uint64_t*
         } else {
             prev = w;
         }
+    }
+    if constexpr (STG) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < np * 2 * M; e += 128) __stcs(out + p0 * (2 * M) + e, stage[e]);
     }
 }
 
@@ -1051,6 +1084,31 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     // interleaved layout in place (tools/mul_layout_timing.py)
     if (layout == 1 && m > 16 && m <= 128 && m % 2 == 0 && g_mul_route.load(std::memory_order_relaxed) != 1)
         return launch_mul_imma_il(out, a, b, m, batch, stream);
+    // Small sizes off the powers of two (m = 3 ... 15) on a register kernel of exactly m
+    // limbs (no zero-extended columns; tools/mul_sweep.py, profiles/r02_mul_exact_ab.jsonl):
+    // interleaved rows are coalesced as they are (the transposes around the row-major route
+    // below cost 3-5x: m = 3 ... 15 at 24-42 us per 2^22 limbs, were 114-145); even row-major
+    // m too (m = 6 24 vs 45 us, m = 10-14 30-38 vs 63-66 zero-extended); odd row-major rows
+    // are staged through shared memory so loads and stores stay coalesced (unstaged they ran
+    // 39-69 us, no faster than zero-extension). DOTG_MUL_EXACT=0 (A/B) takes the old routes,
+    // =3 the exact kernel without staging.
+    static const int exact = [] {
+        const char* e = std::getenv("DOTG_MUL_EXACT");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (exact && g_mul_route.load(std::memory_order_relaxed) != 1 && m >= 3 && m <= 15 && (m & (m - 1)) != 0) {
+        const int L = layout == 1 ? 1 : (m % 2 == 1 && exact != 3 ? 2 : 0);  // odd rows: staged
+        switch (m) {
+#define DOTG_EXACT(MM)                                                                                           \
+    case MM:                                                                                                     \
+        return L == 1 ? run_regs<MM, 1>(out, a, b, batch, stream)                                               \
+                      : (L == 2 ? run_regs<MM, 2>(out, a, b, batch, stream) : run_regs<MM, 0>(out, a, b, batch, stream));
+            DOTG_EXACT(3) DOTG_EXACT(5) DOTG_EXACT(6) DOTG_EXACT(7) DOTG_EXACT(9) DOTG_EXACT(10)
+            DOTG_EXACT(11) DOTG_EXACT(12) DOTG_EXACT(13) DOTG_EXACT(14) DOTG_EXACT(15)
+#undef DOTG_EXACT
+            default: break;
+        }
+    }
     // other interleaved m > 16, and 4 < m < 16 off the powers of two (no interleaved register
     // kernel for those): transpose around the row-major route
     if (layout == 1 && (m > 16 || (m > 4 && (m & (m - 1)) != 0)) && g_mul_route.load(std::memory_order_relaxed) != 1 &&
@@ -1087,30 +1145,6 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
         }();
         const size_t base = m > 128 ? 128 : (fine ? (m + 15) & ~size_t(15) : (m <= 32 ? 32 : (m <= 64 ? 64 : 128)));
         return launch_karatsuba_padded(out, a, b, m, batch, base < 32 ? 32 : base, stream);
-    }
-    // m = 3, 6, 10, 12, 14: a register kernel of exactly m limbs, both layouts (no
-    // zero-extended columns). Measured (tools/mul_sweep.py, B x m = 2^22, row-major /
-    // interleaved, us): m = 3 39 / 22 vs 109 / 114 before, m = 6 24 / 115 vs 45 / 138,
-    // m = 10-14 30-38 / 94-100 vs 63-66 / 128-134. Odd m >= 5 stay on the zero-extended
-    // 8 / 16-limb kernels (row-major) and the generic loop (interleaved): with one column
-    // chain per thread and odd rows stored limb by limb, the exact kernel is no faster there
-    // (profiles/r02_mul_exact_ab.jsonl). DOTG_MUL_EXACT=0 (A/B) takes the old routes, =2
-    // forces the exact kernel for every m in 3 ... 15 off the powers of two.
-    static const int exact = [] {
-        const char* e = std::getenv("DOTG_MUL_EXACT");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (exact && route != 1 && m >= 3 && m <= 15 && (m & (m - 1)) != 0 &&
-        (exact == 2 || m == 3 || m % 2 == 0)) {
-        const int L = layout == 0 ? 0 : 1;
-        switch (m) {
-#define DOTG_EXACT(MM) \
-    case MM: return L ? run_regs<MM, 1>(out, a, b, batch, stream) : run_regs<MM, 0>(out, a, b, batch, stream);
-            DOTG_EXACT(3) DOTG_EXACT(5) DOTG_EXACT(6) DOTG_EXACT(7) DOTG_EXACT(9) DOTG_EXACT(10)
-            DOTG_EXACT(11) DOTG_EXACT(12) DOTG_EXACT(13) DOTG_EXACT(14) DOTG_EXACT(15)
-#undef DOTG_EXACT
-            default: break;
-        }
     }
     // 4 < m < 16 off the power-of-two kernels, or misaligned rows of 5..16: the register
     // kernels of the next size with zero-extended operands, any alignment

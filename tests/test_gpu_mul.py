@@ -220,16 +220,18 @@ print("BAD", bad)
 '''
 
 
-def test_exact_small_kernels_every_odd_size(cuda):
-    """DOTG_MUL_EXACT=2 forces the exact-m register kernels for every m in 3 ... 15 off the
-    powers of two (the default takes them only where they measured faster), both layouts."""
+@pytest.mark.parametrize("exact", ["1", "3"])
+def test_exact_small_kernels_every_odd_size(cuda, exact):
+    """The exact-m register kernels for m in 3 ... 15 off the powers of two, both layouts,
+    odd row-major rows staged through shared memory (DOTG_MUL_EXACT=1, the default) and
+    unstaged (=3); partial last CTAs (131 pairs)."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", EXACT_CHILD.replace("ROOT", repr(root))],
-                       env={**os.environ, "DOTG_MUL_EXACT": "2"}, capture_output=True, text=True, timeout=600)
+                       env={**os.environ, "DOTG_MUL_EXACT": exact}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
 
