@@ -1124,8 +1124,8 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     // size; m > 128 runs padded Karatsuba down to m = 128 tensor-pipe leaves (the generic
     // thread-per-pair kernel would be 100x slower there: tools/kara_timing.py). Both copy
     // the rows, so any alignment works.
-    if (layout == 0 && route != 1 && m > 16 && m < 128 && m % 2 == 0 && aligned16(out) && aligned16(a) &&
-        aligned16(b))
+    if (layout == 0 && route != 1 && m > 16 && m < 128 &&
+        (m % 2 == 1 || (aligned16(out) && aligned16(a) && aligned16(b))))  // odd rows: direct loads
         return launch_mul_imma_rt(out, a, b, m, batch, stream);
     // m >= 256: the tcgen05 column kernel (mul_umma.cu) up to 16384 limbs (rows padded to a
     // multiple of 16 limbs when needed), Karatsuba down to its leaves above that.

@@ -77,11 +77,11 @@ struct ImmaCfg {
     static constexpr int NC0 = (2 * NB + 7) / 8;  // accumulator tiles per R0
     static constexpr int NQ = NB + 7;             // Q[m], m in [-(NB-1), 7]
     static constexpr int OUT_LIMBS = 2 * M;
-    static constexpr int LPL = OUT_LIMBS >= 32 ? OUT_LIMBS / 32 : 1;  // output limbs per lane
-    static constexpr int LANES = OUT_LIMBS >= 32 ? 32 : OUT_LIMBS;     // lane l: limbs l + 32k
-    static constexpr int VW = NW >= 32 ? NW / 32 : 1;  // operand words per lane
+    static constexpr int LPL = OUT_LIMBS >= 32 ? (OUT_LIMBS + 31) / 32 : 1;  // output limbs per lane
+    static constexpr int LANES = OUT_LIMBS >= 32 ? 32 : OUT_LIMBS;  // lane l: limbs l + 32k (< OUT_LIMBS)
+    static constexpr int VW = (NW + 31) / 32;                        // operand words per lane
     static constexpr int LD_LANES = NW / VW;
-    static_assert(OUT_LIMBS % LPL == 0 && LANES <= 32, "limb split");
+    static_assert(LANES <= 32, "limb split");
     static_assert(NW % VW == 0 && NW / VW <= 32, "operand split");  // VW of 3, 5, 6, 7: scalar moves
 };
 
@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL
         bulk_load(dst, a + p * size_t(mr), kOpBytes, &bar[stage]);
         bulk_load(dst + C::NW, b + p * size_t(mr), kOpBytes, &bar[stage]);
     };
-    if (!IL && lane == 0) {
+    // odd mr: rows are not 16-byte aligned, so no bulk copies - each warp loads its pair's
+    // words straight from global memory (coalesced 32-bit loads, zero past 2 mr words)
+    const bool direct = !IL && (mr & 1) != 0;
+    if (!IL && !direct && lane == 0) {
         for (int st = 0; st < C::ST; ++st) mbar_init(&bar[st]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int st = 0; st < C::ST; ++st)
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL
         for (int k = 0; k < C::LPL; ++k) {
             const int L = lane + 32 * k;
             u128 v = 0;
-            if (active) {
+            if (active && L < C::OUT_LIMBS) {
                 const int base = 8 * L + 4 * (L >> 2);
                 const int4 s0 = *reinterpret_cast<const int4*>(S + base);
                 const int4 s1 = *reinterpret_cast<const int4*>(S + base + 4);
@@ -350,7 +353,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL
             const uint64_t hwrap = k > 0 ? __shfl_sync(0xffffffffu, hi[k > 0 ? k - 1 : 0], 31) : 0ull;
             if (lane == 0) h = hwrap;
             uint64_t sv = lo[k] + h;
-            const uint32_t gk = active && sv < h, pk = active && sv == ~0ull;
+            const bool ak = active && lane + 32 * k < C::OUT_LIMBS;  // last segment may be partial
+            const uint32_t gk = ak && sv < h, pk = ak && sv == ~0ull;
             const uint32_t Gm = __ballot_sync(0xffffffffu, gk), Pm = __ballot_sync(0xffffffffu, pk);
             const uint64_t y = ((uint64_t(Gm) << 1) | cseg) + uint64_t(Pm);
             const uint32_t Cm = uint32_t(y) ^ Pm;
@@ -430,6 +434,30 @@ __global__ void __launch_bounds__(kImmaWarps * 32, NB == 16 ? (IL ? DOTG_IMMA_IL
                 }
             }
         }
+    } else if (direct) {
+        const uint32_t nw = 2u * uint32_t(mr);  // u32 words per operand row
+        for (size_t pair = first; pair < batch; pair += nwarps) {
+            const uint32_t* a32 = reinterpret_cast<const uint32_t*>(a + pair * size_t(mr));
+            const uint32_t* b32 = reinterpret_cast<const uint32_t*>(b + pair * size_t(mr));
+            uint32_t bv[C::VW + 1], av[C::VW];
+            if (lane < C::LD_LANES) {
+#pragma unroll
+                for (int e = 0; e < C::VW; ++e) {
+                    const uint32_t w = uint32_t(lane * C::VW + e);
+                    av[e] = w < nw ? __ldg(a32 + w) : 0u;
+                    bv[e] = w < nw ? __ldg(b32 + w) : 0u;
+                }
+            }
+            stage_pair(av, bv);
+            uint64_t lo[C::LPL];
+            multiply_staged(lo);
+            if (active) {
+                uint64_t* po = out + pair * (2 * size_t(mr)) + lane;
+#pragma unroll
+                for (int k = 0; k < C::LPL; ++k)
+                    if (lane + 32 * k < 2 * mr) po[32 * k] = lo[k];
+            }
+        }
     } else {
         int stage = 0;
         uint32_t parity = 0;
@@ -499,7 +527,8 @@ cudaError_t run_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t
 }  // namespace
 
 bool mul_imma_supported(size_t m) {
-    return m == 8 || m == 16 || m == 32 || m == 48 || m == 64 || m == 80 || m == 96 || m == 112 || m == 128;
+    return m == 8 || m == 16 || m == 20 || m == 24 || m == 28 || m == 32 || m == 48 || m == 64 || m == 80 ||
+           m == 96 || m == 112 || m == 128;
 }
 
 cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
@@ -509,6 +538,9 @@ cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b,
     switch (m) {
         case 8: return run_imma<2>(out, a, b, batch, mr, st);
         case 16: return run_imma<4>(out, a, b, batch, mr, st);
+        case 20: return run_imma<5>(out, a, b, batch, mr, st);
+        case 24: return run_imma<6>(out, a, b, batch, mr, st);
+        case 28: return run_imma<7>(out, a, b, batch, mr, st);
         case 32: return run_imma<8>(out, a, b, batch, mr, st);
         case 48: return run_imma<12>(out, a, b, batch, mr, st);
         case 64: return run_imma<16>(out, a, b, batch, mr, st);
@@ -537,13 +569,17 @@ cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t*
 cudaError_t launch_mul_imma_rt(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
-    if (m % 2 != 0 || m <= 16 || m >= 128) return cudaErrorNotSupported;
+    if (m <= 16 || m >= 128) return cudaErrorNotSupported;  // odd m: the kernel's direct loads
     const int mr = int(m);
-    // next multiple of 16 limbs (DOTG_IMMA_FINE=0: the next power of two, as in r01)
+    // next multiple of 4 limbs up to 32, of 16 above (DOTG_IMMA_FINE=0: the next power of
+    // two, as in r01)
     static const int fine = [] {
         const char* e = std::getenv("DOTG_IMMA_FINE");
         return e ? std::atoi(e) : 1;
     }();
+    if (fine && m <= 20) return run_imma<5>(out, a, b, batch, mr, st);
+    if (fine && m <= 24) return run_imma<6>(out, a, b, batch, mr, st);
+    if (fine && m <= 28) return run_imma<7>(out, a, b, batch, mr, st);
     if (m <= 32) return run_imma<8>(out, a, b, batch, mr, st);
     if (fine && m <= 48) return run_imma<12>(out, a, b, batch, mr, st);
     if (m <= 64) return run_imma<16>(out, a, b, batch, mr, st);
