@@ -236,7 +236,7 @@ def test_exact_small_kernels_every_odd_size(cuda, exact):
     assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
 
 
-@pytest.mark.parametrize("m", [17, 18, 19, 20, 21, 23, 24, 25, 27, 28, 29, 30, 31, 33, 40, 47, 48, 49, 65, 72, 80, 90, 96, 97, 110, 112, 127])
+@pytest.mark.parametrize("m", [17, 18, 19, 20, 21, 23, 24, 25, 27, 28, 29, 30, 31, 33, 40, 47, 48, 49, 65, 72, 80, 90, 96, 97, 110, 112, 127, 129, 160, 161, 200, 224, 255])
 def test_tensor_pipe_multiple_of_16_sizes(cuda, oracle, m):
     """Sizes between the powers of two on the tensor pipe: 48 / 80 / 96 / 112 limbs
     exactly (k_mul_imma<12 / 20 / 24 / 28>, operand words not a power of two per lane),
