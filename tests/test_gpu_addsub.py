@@ -273,7 +273,8 @@ import paper_2604_21566_b200 as dg
 from helpers import CATEGORIES, Oracle, category
 orc = Oracle()
 bad = []
-for m, batch in [(3, 301), (5, 97), (33, 130), (100, 41), (257, 12), (1000, 9), (2048, 5), (4096, 3)]:
+for m, batch in [(1, 4096), (1, 4097), (3, 301), (5, 97), (33, 130), (100, 41), (257, 12), (1000, 9), (2048, 5),
+                 (4096, 3)]:
     rng = np.random.default_rng(77 + m)
     for cat in CATEGORIES:
         for op in ("add", "sub"):
