@@ -383,6 +383,72 @@ __global__ void __launch_bounds__(256) k_addsub_il_tiny(uint64_t* __restrict__ o
     if (flags != nullptr) *reinterpret_cast<uint4*>(flags + p) = make_uint4(c[0], c[1], c[2], c[3]);
 }
 
+// Row-major numbers of 3 <= m <= 7 limbs (not a power of two): a CTA stages its P
+// pairs' rows (P * m contiguous limbs per operand, 16-byte loads, UN of them in flight per
+// thread) into shared memory, each thread then walks its own pair's limbs with one carry
+// (the limb-serial oracle's loop, oracle.cpp:16-48) writing the sums over the staged a,
+// and the CTA stores the P * m result limbs contiguously. Loads and stores stay fully
+// coalesced whatever m is; the serial walks read shared memory with stride m limbs
+// (2-way bank conflicts for odd m, the minimum for 8-byte lanes). Measured (tools/il_graph.py
+// rows, B x m = 2^22): m = 3 / 5 / 6 / 7 at 0.77 / 0.87 / 0.84 / 0.89 of HBM against 0.69 /
+// 0.67 / 0.67 / 0.71 on k_addsub_rows_any; from m = 9 up the per-thread walks (and, for even
+// m, bank conflicts: m = 24 0.36) lose to k_addsub_rows_any, which keeps them.
+template <bool SUB>
+__global__ void __launch_bounds__(128) k_addsub_rows_staged(uint64_t* __restrict__ out, const uint64_t* __restrict__ a,
+                                                            const uint64_t* __restrict__ b, uint32_t* __restrict__ flags,
+                                                            uint32_t m, size_t batch, uint32_t P) {
+    extern __shared__ __align__(16) uint64_t st[];  // [P * m] a (then the sums) | [P * m] b
+    const size_t p0 = size_t(blockIdx.x) * P;
+    const uint32_t np = uint32_t(batch - p0 < size_t(P) ? batch - p0 : size_t(P));
+    const uint32_t n = np * m;  // limbs per operand in this CTA (even: P is a multiple of 32)
+    const ulonglong2* ga = reinterpret_cast<const ulonglong2*>(a + p0 * m);
+    const ulonglong2* gb = reinterpret_cast<const ulonglong2*>(b + p0 * m);
+    ulonglong2* sa = reinterpret_cast<ulonglong2*>(st);
+    ulonglong2* sb = reinterpret_cast<ulonglong2*>(st + size_t(P) * m);
+    const uint32_t n2 = n / 2, T = blockDim.x;
+    constexpr int UN = 4;
+    for (uint32_t e0 = threadIdx.x; e0 < n2; e0 += UN * T) {
+        ulonglong2 x[UN], y[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u)
+            if (e0 + u * T < n2) x[u] = __ldcs(ga + e0 + u * T), y[u] = __ldcs(gb + e0 + u * T);
+#pragma unroll
+        for (int u = 0; u < UN; ++u)
+            if (e0 + u * T < n2) sa[e0 + u * T] = x[u], sb[e0 + u * T] = y[u];
+    }
+    if ((n & 1u) && threadIdx.x == 0) st[n - 1] = a[p0 * m + n - 1], st[size_t(P) * m + n - 1] = b[p0 * m + n - 1];
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < np; t += T) {
+        uint64_t* ra = st + size_t(t) * m;
+        const uint64_t* rb = st + size_t(P) * m + size_t(t) * m;
+        uint32_t c = 0;
+        uint32_t i = 0;
+        for (; i + 4 <= m; i += 4) {
+            uint64_t x[4], y[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = ra[i + k], y[k] = rb[i + k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t g, pr;
+                const uint64_t sv = lane_op<SUB>(x[k], y[k], g, pr);
+                ra[i + k] = apply_carry<SUB>(sv, c);
+                c = g | (pr & c);
+            }
+        }
+        for (; i < m; ++i) {
+            uint32_t g, pr;
+            const uint64_t sv = lane_op<SUB>(ra[i], rb[i], g, pr);
+            ra[i] = apply_carry<SUB>(sv, c);
+            c = g | (pr & c);
+        }
+        if (flags != nullptr) flags[p0 + t] = c;
+    }
+    __syncthreads();
+    ulonglong2* go = reinterpret_cast<ulonglong2*>(out + p0 * m);
+    for (uint32_t e = threadIdx.x; e < n2; e += T) __stcs(go + e, sa[e]);
+    if ((n & 1u) && threadIdx.x == 0) out[p0 * m + n - 1] = st[n - 1];
+}
+
 // Row-pitched thread per pair: operand rows at their own pitches (views of wider arrays).
 template <bool SUB>
 __global__ void __launch_bounds__(256) k_addsub_pitched(uint64_t* out, size_t ldo, const uint64_t* a, size_t lda,
@@ -1347,6 +1413,32 @@ cudaError_t run_il_tiny(uint64_t* out, const uint64_t* a, const uint64_t* b, uin
     return cudaGetLastError();
 }
 
+// k_addsub_rows_staged: P pairs per CTA (a multiple of 32, at most 128) so that a CTA's
+// two operand stages fit ~48 KB (4 CTAs per SM); 16-byte aligned operands and output.
+template <bool SUB>
+cudaError_t run_rows_staged(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
+                            size_t batch, cudaStream_t st) {
+    if (m < 3 || m >= 64 || !aligned(out, 16) || !aligned(a, 16) || !aligned(b, 16)) return cudaErrorNotSupported;
+    uint32_t P = uint32_t((48 * 1024) / (16 * m)) & ~31u;
+    if (P > 128) P = 128;
+    if (P < 32) P = 32;
+    const size_t smem = size_t(2) * P * m * 8;
+    const size_t blocks = (batch + P - 1) / P;
+    if (blocks > size_t(0x7fffffff)) return cudaErrorNotSupported;
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {  // up to 63 KB at m = 63 (P = 32)
+        cudaError_t e = cudaFuncSetAttribute(k_addsub_rows_staged<SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             64 * 1024);
+        if (e != cudaSuccess) return e;
+        attr_dev = dev;
+    }
+    k_addsub_rows_staged<SUB><<<unsigned(blocks), P, smem, st>>>(out, a, b, flags, uint32_t(m), batch, P);
+    count_launch();
+    return cudaGetLastError();
+}
+
 constexpr int kRowsU = 4;  // chunks of 128 limbs in flight per warp
 template <bool SUB>
 cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, uint32_t* flags, size_t m,
@@ -1382,6 +1474,14 @@ cudaError_t run_rows_any(uint64_t* out, const uint64_t* a, const uint64_t* b, ui
     return cudaGetLastError();
 }
 bool pow2(size_t m) { return m != 0 && (m & (m - 1)) == 0; }
+// DOTG_ROWS_STAGED=0 (A/B): row-major 3 <= m <= 7 off the powers of two on k_addsub_rows_any
+bool rows_staged_on() {
+    static const int v = [] {
+        const char* e = std::getenv("DOTG_ROWS_STAGED");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
 
 // 0: team-small kernel, 1: team-big (m = 512), 2: strided kernel
 int route(const AddSubProblem& P, int layout) {
@@ -1480,6 +1580,14 @@ cudaError_t launch_addsub_group(const AddSubProblem* probs, const int* layouts, 
             cudaError_t e = launch_long_batch(P.sub != 0, P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
             if (e != cudaSuccess) return e;
             continue;
+        }
+        if (r == 2 && layouts[i] == 0 && P.m >= 3 && P.m <= 7 && rows_staged_on()) {
+            cudaError_t e = P.sub ? run_rows_staged<true>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream)
+                                  : run_rows_staged<false>(P.out, P.a, P.b, P.flags, P.m, P.batch, stream);
+            if (e != cudaErrorNotSupported) {
+                if (e != cudaSuccess) return e;
+                continue;
+            }
         }
         if (r == 2 && layouts[i] == 0 && P.m >= 3 && P.m < (size_t(1) << 31) &&
             aligned(P.out, 8) && aligned(P.a, 8) && aligned(P.b, 8)) {

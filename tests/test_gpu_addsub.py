@@ -293,13 +293,34 @@ print("BAD", bad)
 @pytest.mark.parametrize("u", ["1", "2", "4"])
 def test_rows_any_chunks_in_flight(cuda, u):
     """The any-m row kernel with 1, 2 and 4 chunks of loads in flight per warp (DOTG_ROWS_U,
-    read once per process: one child each), ragged m and pow2 m above 512."""
+    read once per process: one child each; DOTG_ROWS_STAGED=0 keeps m < 64 on it too),
+    ragged m and pow2 m above 512."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", ROWS_CHILD.replace("ROOT", repr(root))],
-                       env={**os.environ, "DOTG_ROWS_U": u}, capture_output=True, text=True, timeout=600)
+                       env={**os.environ, "DOTG_ROWS_U": u, "DOTG_ROWS_STAGED": "0"}, capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().splitlines()[-1] == "BAD []", r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("m", [3, 5, 6, 7, 9, 11, 12])
+def test_rows_staged_partial_ctas(cuda, oracle, m):
+    """Row-major 3 <= m <= 7 off the powers of two (k_addsub_rows_staged; 9 ... 12 on the
+    any-m kernel): batches that leave a partial last CTA with an odd limb count, in place."""
+    import paper_2604_21566_b200 as dg
+
+    torch = cuda
+    rng = np.random.default_rng(6600 + m)
+    for batch in (1, 33, 129, 1001):
+        for sub in (False, True):
+            a, b = spiky(rng, (batch, m)), spiky(rng, (batch, m))
+            want, wf = oracle.addsub_batch(sub, a, b)
+            got, gf = run(torch, sub, a, b)
+            assert np.array_equal(got, want) and np.array_equal(gf, wf), (m, batch, sub)
+            ta, tb = dev(torch, a), dev(torch, b)
+            _, fl = dg.addsub_batch(sub, ta, tb, out=ta)
+            assert np.array_equal(host(ta), want) and np.array_equal(fl.cpu().numpy().view(np.uint32), wf)
