@@ -1082,7 +1082,7 @@ cudaError_t launch_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b
     const bool al = aligned32(out) && aligned32(a) && aligned32(b);
     // interleaved even 16 < m <= 128: the tensor-pipe kernel reads and writes the
     // interleaved layout in place (tools/mul_layout_timing.py)
-    if (layout == 1 && m > 16 && m <= 128 && m % 2 == 0 && g_mul_route.load(std::memory_order_relaxed) != 1)
+    if (layout == 1 && m > 16 && m <= 128 && g_mul_route.load(std::memory_order_relaxed) != 1)
         return launch_mul_imma_il(out, a, b, m, batch, stream);
     // Small sizes off the powers of two (m = 3 ... 15) on a register kernel of exactly m
     // limbs (no zero-extended columns; tools/mul_sweep.py, profiles/r02_mul_exact_ab.jsonl):

@@ -557,10 +557,15 @@ cudaError_t launch_mul_imma(uint64_t* out, const uint64_t* a, const uint64_t* b,
 cudaError_t launch_mul_imma_il(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m, size_t batch,
                                cudaStream_t st) {
     if (batch == 0) return cudaSuccess;
-    if (m % 2 != 0 || m <= 16 || m > 128) return cudaErrorNotSupported;
+    if (m <= 16 || m > 128) return cudaErrorNotSupported;  // any m: tile rows past m load as zero
     const int mr = int(m);
+    static const int fine = [] {
+        const char* e = std::getenv("DOTG_IMMA_FINE");
+        return e ? std::atoi(e) : 1;
+    }();
     if (m <= 32) return run_imma<8, true>(out, a, b, batch, mr, st);
     if (m <= 64) return run_imma<16, true>(out, a, b, batch, mr, st);
+    if (fine && m <= 96) return run_imma<24, true>(out, a, b, batch, mr, st);  // 6 words per lane (even)
     return run_imma<32, true>(out, a, b, batch, mr, st);
 }
 

@@ -184,7 +184,7 @@ def test_row_pitched_views(cuda, oracle):
         assert np.array_equal(dg.mul_batch(ta, tb).cpu().numpy().view(np.uint64), want)
 
 
-@pytest.mark.parametrize("m", [18, 32, 64, 126, 128])
+@pytest.mark.parametrize("m", [17, 18, 32, 33, 47, 64, 65, 80, 95, 96, 97, 126, 127, 128])
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 9, 1031])
 def test_interleaved_tensor_pipe_in_place(cuda, oracle, m, n):
     """The interleaved tensor-pipe route reads and writes [m][batch] in place through
