@@ -1182,7 +1182,7 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
         tensor_peak = sms * UMMA_U8_MACS_PER_CLK_SM * sm_max * 1e6  # byte-MACs / s at max clock
         for m, B in ((1024, 1024), (2048, 256), (4096, 64)):
             sets = []
-            for r in range(2):
+            for r in range(rotations(2 * B * m * 8)):  # more than the L2 read between reuses
                 a = W.fill(B * m, 0x3C + m + 7 * r, 0).view(B, m)
                 b = W.fill(B * m, 0x3C + m + 7 * r, 1 << 40).view(B, m)
                 sets.append((a, b, torch.empty((B, 2 * m), dtype=torch.int64, device="cuda")))
@@ -1204,7 +1204,7 @@ def run_secondary(args, torch, dg, W, L, stream, rank, world, dist, hbm_peak, sm
                          "schoolbook byte-MACs (8m)^2 per pair counted",
             "prior_route_note": "prior_route_us: the same call on the mma.sync Karatsuba route (DOTG_MUL_UMMA=0), "
                                 "profiles/r02_umma_wide_variants.txt",
-            "timing": "back-to-back calls over 2 rotating input sets (CUDA graph, events on the stream)"}
+            "timing": "back-to-back calls over rotating input sets (more than the L2 read between reuses; CUDA graph, events on the stream)"}
         torch.cuda.empty_cache()
 
     # ---------------- C5: one 2^30-limb add / sub ----------------
