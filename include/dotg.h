@@ -112,15 +112,17 @@ int dotg_mul_batch(uint64_t* out, const uint64_t* a, const uint64_t* b, size_t m
                    int layout, dotg_stream_t stream);
 
 /* Which pipe dotg_mul_batch (and everything built on it) takes the partial products on.
- * AUTO (row-major, 32-byte aligned pointers): m <= 16 on the IMAD column kernels; m in
- * {32, 64, 128} on the integer tensor pipe (radix-2^8 IMMA column sums); other
- * 16 < m < 128 zero-padded to the next of those; 128 < m < 256 as padded Karatsuba down
- * to m = 128 tensor-pipe leaves; 256 <= m <= 65536 on the 5th-generation tensor core
- * (tcgen05.mma kind::i8, column sums in tensor memory; rows padded to a multiple of 16
- * limbs); m > 65536 as padded Karatsuba down to tcgen05 leaves (environment:
- * DOTG_MUL_UMMA=0 keeps the mma.sync leaves, DOTG_UMMA_LEAF / DOTG_UMMA_DIRECT pick the
- * leaf size and the direct limit).
- * Interleaved or misaligned operands: IMAD kernels.
+ * AUTO (row-major): m <= 16 on the IMAD column kernels (exact-size register kernels for
+ * m = 3 ... 15 off the powers of two); m in {20, 24, 28, 32, 48, 64, 80, 96, 112, 128} on
+ * the integer tensor pipe (radix-2^8 IMMA column sums), other 16 < m < 128 zero-extended
+ * to the next of those (odd rows loaded directly, even rows through the bulk-copy ring);
+ * 128 < m < 256 as one Karatsuba level over 80 / 96 / 112 / 128-limb tensor-pipe leaves;
+ * 256 <= m <= 65536 on the 5th-generation tensor core (tcgen05.mma kind::i8, column sums
+ * in tensor memory; rows padded to a multiple of 16 limbs); m > 65536 as padded Karatsuba
+ * down to tcgen05 leaves (environment: DOTG_MUL_UMMA=0 keeps the mma.sync leaves,
+ * DOTG_UMMA_LEAF / DOTG_UMMA_DIRECT pick the leaf size and the direct limit).
+ * Interleaved: m <= 16 on register kernels in place, 16 < m <= 128 on the tensor pipe in
+ * place, larger m transposed around the row-major route.
  * IMMA also covers m in {8, 16} (slower there than IMAD; taken only when forced).
  * IMAD / IMMA force one side where it applies (IMMA falls back to IMAD for shapes it
  * does not cover). Both are bit-exact; the knob exists for A/B measurement and for
