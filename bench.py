@@ -858,6 +858,12 @@ def run_ours(args, rank, world, dist):
                                  "k_addsub_grouped (persistent batched add/sub, warp-ballot lookahead)",
                                  peak_kind=f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)", traffic=traffic,
                                  per_size=per_size, mix_peak=mix_peak,
+                                 traffic_steady=(traffic_table().get("C2_steady_per_launch_bytes")
+                                                 if world == 1 and not args.ungrouped else None),
+                                 traffic_steady_note=("ncu --cache-control none over consecutive launches of this "
+                                                      "kernel in the bench command: DRAM read + write per launch in "
+                                                      "steady state (profiles/r02_ncu_headline_steady.csv); "
+                                                      "traffic is one --set full capture with caches flushed"),
                                  note="achieved = this rank's algorithmic bytes per step launch / the launch's "
                                       "CUDA-event time on the launching stream (one launch per step)"),
         "cpu_baseline": cpu_baseline,
